@@ -1,0 +1,145 @@
+/*
+ * libhiermoe -- C-ABI of the B200 (sm_100a) HierMoE dedup dispatch/combine +
+ * expert-swap hot path.  Plain pointers and sizes only; every device pointer
+ * is caller-owned (torch allocations) unless it comes from an hm_world.
+ * Every call is stream-ordered on `stream` (a cudaStream_t) and returns
+ *   0  ok,  < 0  invalid argument (message: hm_last_error()),  > 0  CUDA error.
+ * Reentrant; the only state lives in hm_world objects created explicitly.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/hiera2a/<file>:<line>).
+ */
+#ifndef HIERMOE_H
+#define HIERMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* hm_last_error(void);
+int hm_version(void);
+
+/* ---------------- decision path (planner) ---------------------------------
+ * Mask layout: packed rows, W = ceil(E/32) uint32 words per row; bit e of row
+ * t = (bits[t*W + e/32] >> (e%32)) & 1.                                      */
+
+/* bool T x E mask -> packed bits, optional column gather (slot view).
+ * Replaces RoutingMask (routing.py:31-56: row popcounts for the K check),
+ * mask_bits (routing.py:84-90) and slot_view/apply_placement
+ * (routing.py:98-106, 177-186). */
+int hm_mask_pack(const uint8_t* mask, int64_t T, int32_t E, const int32_t* slot_to_expert,
+                 uint32_t* bits, int32_t* row_popcount, void* stream);
+int hm_mask_unpack(const uint32_t* bits, int64_t T, int32_t E, uint8_t* mask, void* stream);
+/* K-per-row id lists -> packed slot-space bits (RoutingMask.bits from top-K ids) */
+int hm_ids_to_bits(const int32_t* ids, int64_t T, int32_t K, int32_t E,
+                   const int32_t* expert_to_slot, uint32_t* bits, int32_t* bad_flag,
+                   void* stream);
+
+/* Dedup and raw per-group counts for n_cuts group cuts in one pass, plus the
+ * optional T x g dedup mask of cut `hit_cut`.  Replaces group_reduce
+ * (traffic.py:58-64), dedup_counts (traffic.py:67-71), raw_counts
+ * (traffic.py:74-82); duplication_rate (traffic.py:85-90) derives from them. */
+int hm_level_counts(const uint32_t* bits, int64_t T, int32_t E, const int32_t* groups,
+                    int32_t n_cuts, int64_t* dedup, int64_t* raw, uint8_t* hit,
+                    int32_t hit_cut, void* stream);
+
+/* Device-wide exclusive scan of int64 (workspace: hm_scan_workspace(n) bytes). */
+size_t hm_scan_workspace(int64_t n);
+int hm_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* grand, void* workspace,
+                void* stream);
+
+/* Hierarchical propagation: copies per row, then emit one copy per
+ * (row, level group hit) in row-major order with restricted selections,
+ * origin token and parent group.  Replaces propagate_level
+ * (routing.py:189-215) and PropagatedMask (routing.py:59-78). */
+int hm_propagate_count(const uint32_t* bits, int64_t T, int32_t E, int32_t groups,
+                       int64_t* copies, void* stream);
+int hm_propagate_emit(const uint32_t* bits, int64_t T, int32_t E, int32_t groups,
+                      const int64_t* first_copy, const int64_t* origin_in, uint32_t* out_bits,
+                      int64_t* out_origin, int64_t* out_parent, void* stream);
+
+/* Swap partials of one group cut (base[g], sel[E], hitsel[E*g], lone[E],
+ * lonesel[E*E]) and the E x E x g swap tensor.  Replaces
+ * _swap_tensor_incremental / swap_tensors_incremental (swap.py:81-138). */
+int hm_swap_partials(const uint32_t* bits, int64_t T, int32_t E, int32_t groups, int64_t* base,
+                     int64_t* sel, int64_t* hitsel, int64_t* lone, int64_t* lonesel,
+                     int32_t* too_dense, void* stream);
+int hm_swap_tensor(const int64_t* base, const int64_t* sel, const int64_t* hitsel,
+                   const int64_t* lone, const int64_t* lonesel, int32_t E, int32_t groups,
+                   int64_t* z, void* stream);
+
+/* Smooth-max cost matrix (gamma and exact max) for dimension *dim_dev (or
+ * dim_host when dim_dev is NULL), numpy rounding order.  Replaces
+ * smooth_max/_smooth_max_lastaxis (swap.py:35-57) and cost_matrix
+ * (swap.py:180-206). */
+int hm_swap_cost(const int64_t* const* inter_z, const int32_t* inter_groups,
+                 const int32_t* inter_part, const double* a_inter, const double* b_inter,
+                 const int64_t* const* intra_z, const int32_t* intra_groups,
+                 const int32_t* intra_part, const double* a_intra, const double* b_intra,
+                 int32_t depth, int32_t E, int64_t token_bytes, double gamma,
+                 const int32_t* dim_dev, int32_t dim_host, double* q, double* q_exact,
+                 void* stream);
+/* First-occurrence argmin + exact-max gate.  out_i64 = {flat, r, c, chosen},
+ * out_f64 = {no_swap_time, saving}.  Replaces select_swap's decision
+ * (swap.py:240-252). */
+int hm_swap_select(const double* q, const double* q_exact, int32_t E, int64_t* out_i64,
+                   double* out_f64, void* stream);
+
+/* Phase time model and d* from dedup counts of cuts [U[1..D-1], G].
+ * Replaces _time_for_dim/all_times/pick_dimension/optimal_dimension
+ * (traffic.py:144-221); per-level counts are invariant under propagation
+ * (swap.py:172-175), so no copy mask is materialised. */
+int hm_time_model(const int64_t* dedup_concat, const int32_t* fanout_groups, int32_t depth,
+                  int32_t gpus, int64_t token_bytes, const double* a_inter, const double* b_inter,
+                  const double* a_intra, const double* b_intra, int32_t* cut_offsets_dev,
+                  double* times, int32_t* d_star, int64_t* maxima, void* stream);
+/* smooth_max over `rows` vectors of length n (swap.py:35-48). */
+int hm_smooth_max_rows(const double* x, int64_t rows, int32_t n, double gamma, double* out,
+                       void* stream);
+
+/* ---------------- layer path (dispatch / combine) -------------------------
+ * A world = G virtual EP ranks on P GPUs (L = G/P per GPU); slot s lives on
+ * rank s / (E/G) (topology.py:99-100), tokens are rank-major.
+ * The reference only models this exchange (traffic.py:93-170: AlltoAll with
+ * and without dedup); these calls execute it. */
+typedef struct hm_world hm_world;
+int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
+                    int32_t top_k, int32_t hidden, int32_t elem_bytes, int64_t tokens_per_rank,
+                    int64_t n_cap_rows, hm_world** out);
+int hm_world_destroy(hm_world* w);
+int64_t hm_world_ipc_handle_size(void);
+int hm_world_ipc_handle(hm_world* w, void* out_handle);
+int hm_world_open_peers(hm_world* w, const void* handles);
+int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void** ptr, int64_t* bytes);
+int hm_world_info(hm_world* w, int64_t* out8);
+int hm_world_barrier(hm_world* w, void* stream);
+/* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
+ * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */
+int hm_world_set_timing(hm_world* w, int32_t enable);
+int hm_world_timings(hm_world* w, float* ms, int32_t n);
+/* stream-ordered copy between any two addresses (buffer inspection) */
+int hm_memcpy(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* Softmax top-K gating -> slot ids (RoutingMask rows, K per
+ * row, routing.py:31-56) and gate weights. */
+int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
+                  const int32_t* expert_to_slot, int32_t renormalize, int32_t* slot_ids,
+                  float* weights, int32_t* expert_ids, void* stream);
+/* Dedup (one row per token x destination rank) or raw (one per selection)
+ * dispatch; the per-destination histogram equals dedup_counts / raw_counts
+ * at G (traffic.py:67-82). */
+int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts, int32_t dedup,
+                void* stream);
+/* Destination-side re-expansion of dedup rows into expert-major rows. */
+int hm_expand(hm_world* w, void* stream);
+/* Gate-weighted combine (pre-reduce per destination + source sum for dedup). */
+int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIERMOE_H */

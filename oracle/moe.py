@@ -165,3 +165,45 @@ def dedup_combine(plan: DispatchPlan, weights, y_expert_major, payload_round=Non
             acc += part
         out[tok] = acc
     return out
+
+
+def cpu_dispatch_combine(x, ids, weights, ranks: int, experts: int, y_major=None, threads: int = 1):
+    """Vectorised CPU port of one dedup dispatch + combine step (the timed
+    CPU baseline; TEST/BENCH INFRASTRUCTURE ONLY).
+
+    Performs the same data movement as the GPU step on host memory: per
+    destination gather of the dedup rows, re-expansion into expert-major rows,
+    gate-weighted pre-reduce per (token, destination) and the source-side sum
+    over destinations.  ``y_major[d]`` are the destination's expert outputs
+    (defaults to the expert-major inputs, i.e. identity experts).  Returns
+    (out [T, M], y_major, plan).
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    plan = DispatchPlan(ids, ranks, experts)
+    e_loc = experts // ranks
+    t, k = plan.ids.shape
+    w = np.asarray(weights, dtype=x.dtype)
+
+    def dest_step(d):
+        rows = plan.recv_rows(d)                       # arrival order (global token order)
+        recv = x[rows]                                 # pack + exchange
+        local = (plan.ids[rows] // e_loc) == d         # [R, K] picks on d
+        rr, kk = np.nonzero(local)
+        n = int(plan.n_e[d * e_loc:(d + 1) * e_loc].sum())
+        xm = np.empty((n, x.shape[1]), dtype=x.dtype)
+        xm[plan.epos[rows[rr], kk]] = recv[rr]         # expand
+        ym = xm if y_major is None else y_major[d]
+        part = np.zeros_like(recv)                     # pre-reduce, k order
+        for kq in range(k):
+            sel = local[:, kq]
+            part[sel] += w[rows[sel], kq][:, None] * ym[plan.epos[rows[sel], kq]]
+        return rows, part, ym
+
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
+        res = list(pool.map(dest_step, range(ranks)))
+    out = np.zeros_like(x)
+    for d in range(ranks):                             # ascending destination order
+        rows, part, _ = res[d]
+        out[rows] += part
+    return out, [r[2] for r in res], plan

@@ -1,0 +1,1067 @@
+// MoE-layer hot path: top-K gating, dedup dispatch, expert-side re-expansion,
+// dedup combine -- over a world of G virtual EP ranks hosted on P physical
+// GPUs (L = G/P per GPU), connected by CUDA-IPC peer mappings over NVLink.
+//
+// Step (all stream-ordered on the caller's stream, no host synchronisation):
+//   k_plan     per 256-token chunk of every local source rank: destination
+//              mask, stable within-chunk ranks per destination and per slot,
+//              chunk histograms (G dest + E slot counters)
+//   k_notify   one CTA: chunk prefix sums, this GPU's per-source totals
+//              (= h[s,:] dedup rows per destination, c[s,:] selections per
+//              slot) stored into every peer's count matrix, barrier, derived
+//              offsets (receive offsets, expert-major bases, group sizes)
+//   k_pack     warp per token: 16-B vector copy of the row into every hit
+//              destination's receive buffer (dedup: one copy per destination;
+//              raw: one copy per selection straight into expert-major rows),
+//              peer stores over NVLink for remote destinations
+//   barrier
+//   k_expand   (dedup) destination re-expands each received row into its
+//              local experts' expert-major rows
+//   ... expert FFN on expert-major rows (grouped GEMM) ...
+//   k_reduce   (dedup) destination pre-reduces sum_k w_k y_k over its local
+//              experts into one row per (token, destination)
+//   barrier
+//   k_gather   source sums its (token, destination) rows in ascending
+//              destination order (dedup) or sum_k w_k y_k (raw), peer loads
+//
+// Receive order at destination d is the global (rank-major) token order of
+// the tokens hitting d: the row-major copy order of propagate_level
+// (routing.py:204-215) restricted to d, with h = group_reduce column sums
+// (traffic.py:58-71).
+
+#include "hm_common.cuh"
+
+#include <cuda_bf16.h>
+#include <string.h>
+#include <stdlib.h>
+#include <vector>
+
+namespace {
+
+using namespace hm;
+
+constexpr int kMaxRanks = 64;
+constexpr int kMaxK = 16;
+constexpr int kChunk = 256;      // tokens per plan chunk (8 warps x 32)
+constexpr int kPlanWarps = kChunk / 32;
+
+struct RowMeta {
+  int32_t epos;  // expert-major row at this destination, -1 if not local
+  float w;
+};
+
+// device-resident view of the world (pointers valid on this GPU)
+struct WorldDev {
+  int G, L, P, p, E, K, M, E_loc, elem;
+  int64_t T_r, R_cap, N_cap, row_bytes;
+  uint8_t* recv_x[kMaxRanks];
+  RowMeta* recv_meta[kMaxRanks];
+  uint8_t* xmaj[kMaxRanks];
+  uint8_t* ymaj[kMaxRanks];
+  uint8_t* comb[kMaxRanks];
+  int32_t* counts[kMaxRanks];                 // count matrix [G][G+E] on d's GPU
+  unsigned long long* flags[kMaxRanks];       // per GPU q: flags[q][0..P)
+};
+
+// per-step offsets computed by k_notify (local, not symmetric)
+struct Offsets {
+  int32_t off[kMaxRanks][kMaxRanks];  // [local src][dest]  receive offset
+  int32_t R[kMaxRanks];               // rows received per local dest
+  int32_t Nd[kMaxRanks];              // expert-major rows per local dest
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Called by one full CTA after its peer stores.  Thread 0 publishes `epoch`
+// to every GPU and waits (bounded, 20 s) until every GPU published it.
+__device__ void cta_barrier(const WorldDev& w, unsigned long long epoch, int* status) {
+  __syncthreads();
+  if (threadIdx.x == 0 && w.P > 1) {
+    __threadfence_system();
+    for (int q = 0; q < w.P; ++q) st_release_sys(w.flags[q * w.L] + w.p, epoch);
+    unsigned long long* mine = w.flags[w.p * w.L];
+    uint64_t t0 = globaltimer();
+    for (int q = 0; q < w.P; ++q) {
+      while (ld_acquire_sys(mine + q) < epoch) {
+        if (globaltimer() - t0 > 20000000000ull) {
+          atomicExch(status, 3);  // barrier timeout
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void k_barrier(const WorldDev* __restrict__ wp, unsigned long long epoch, int* status) {
+  cta_barrier(*wp, epoch, status);
+}
+
+// ---------------------------------------------------------------------------
+// K1 router: fp32 logits -> top-K (value desc, index asc) -> softmax weights
+// (renormalised over the picks when renorm) -> slot ids via expert_to_slot.
+// One warp per token; lanes hold E/32 logits each.
+template <int kPerLane>
+__global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int K,
+                        const int32_t* __restrict__ e2s, int renorm,
+                        int32_t* __restrict__ slot_ids, float* __restrict__ weights,
+                        int32_t* __restrict__ expert_ids) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = warp; t < T; t += nw) {
+    const float* row = logits + t * E;
+    float v[kPerLane];
+#pragma unroll
+    for (int j = 0; j < kPerLane; ++j) {
+      int e = j * 32 + lane;
+      v[j] = e < E ? row[e] : -INFINITY;
+    }
+    unsigned taken = 0;
+    float vmax = 0.f, sum_all = 0.f;
+    float pick_v[kMaxK];
+    int pick_e[kMaxK];
+    for (int k = 0; k < K; ++k) {
+      float bv = -INFINITY;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        int e = j * 32 + lane;
+        if (e < E && !(taken & (1u << j)) && (v[j] > bv || (v[j] == bv && e < be))) {
+          bv = v[j];
+          be = e;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (ov > bv || (ov == bv && oe < be)) {
+          bv = ov;
+          be = oe;
+        }
+      }
+      if ((be & 31) == lane) taken |= 1u << (be >> 5);
+      pick_v[k] = bv;
+      pick_e[k] = be;
+    }
+    vmax = pick_v[0];
+    if (!renorm) {
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j)
+        if (j * 32 + lane < E) s += expf(v[j] - vmax);
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      sum_all = s;
+    } else {
+      float s = 0.f;
+      for (int k = 0; k < K; ++k) s += expf(pick_v[k] - vmax);
+      sum_all = s;
+    }
+    if (lane < K) {
+      int k = lane;
+      float pv = 0.f;
+      int pe = 0;
+      for (int q = 0; q < K; ++q)
+        if (q == k) {
+          pv = pick_v[q];
+          pe = pick_e[q];
+        }
+      weights[t * K + k] = expf(pv - vmax) / sum_all;
+      slot_ids[t * K + k] = e2s ? e2s[pe] : pe;
+      if (expert_ids) expert_ids[t * K + k] = pe;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan: grid (chunks, L).  Stable ranks: destination ranks by warp ballot,
+// slot ranks by comparing with earlier lanes' picks via shuffles, then a
+// prefix over the chunk's warps.
+__global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp,
+                                                 const int32_t* __restrict__ ids, int nchunks,
+                                                 int32_t* __restrict__ chunk_cnt,
+                                                 int32_t* __restrict__ rank_d,
+                                                 int32_t* __restrict__ rank_e,
+                                                 unsigned long long* __restrict__ hitmask,
+                                                 int* __restrict__ status) {
+  const WorldDev& w = *wp;
+  extern __shared__ int32_t s_cnt[];  // [kPlanWarps][G+E]
+  const int C = w.G + w.E;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s_loc = blockIdx.y;
+  const int chunk = blockIdx.x;
+  for (int i = threadIdx.x; i < kPlanWarps * C; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int64_t t_in = (int64_t)chunk * kChunk + warp * 32 + lane;  // token within source
+  const bool valid = t_in < w.T_r;
+  const int64_t t = (int64_t)s_loc * w.T_r + t_in;                   // local token index
+  int S[kMaxK];
+  unsigned long long hit = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxK; ++k) {
+    S[k] = -1;
+    if (k < w.K && valid) {
+      int e = ids[t * w.K + k];
+      if (e < 0 || e >= w.E) {
+        atomicExch(status, 4);
+        e = -1;
+      }
+      S[k] = e;
+      if (e >= 0) hit |= 1ull << (e / w.E_loc);
+    }
+  }
+  // destination ranks within the warp
+  int rd[kMaxRanks > 32 ? 32 : kMaxRanks];
+  (void)rd;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int d = 0; d < w.G; ++d) {
+    unsigned b = __ballot_sync(0xffffffffu, (hit >> d) & 1ull);
+    if ((hit >> d) & 1ull) rank_d[t * w.G + d] = __popc(b & lt);
+    else if (valid) rank_d[t * w.G + d] = -1;
+    if (lane == 0) s_cnt[warp * C + d] = __popc(b);
+  }
+  // slot ranks within the warp: earlier lanes' picks equal to mine
+  int re[kMaxK];
+#pragma unroll
+  for (int k = 0; k < kMaxK; ++k) re[k] = 0;
+  for (int j = 0; j < 31; ++j) {
+    for (int k2 = 0; k2 < w.K; ++k2) {
+      int sj = __shfl_sync(0xffffffffu, S[k2 < kMaxK ? k2 : 0], j);
+      if (j < lane && sj >= 0) {
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k)
+          if (k < w.K && S[k] == sj) re[k]++;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxK; ++k)
+    if (k < w.K && S[k] >= 0) atomicAdd(&s_cnt[warp * C + w.G + S[k]], 1);
+  __syncthreads();
+  // exclusive prefix over warps per counter; chunk totals out
+  int32_t* out = chunk_cnt + ((int64_t)s_loc * nchunks + chunk) * C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    int run = 0;
+    for (int wi = 0; wi < kPlanWarps; ++wi) {
+      int v = s_cnt[wi * C + c];
+      s_cnt[wi * C + c] = run;
+      run += v;
+    }
+    out[c] = run;
+  }
+  __syncthreads();
+  if (valid) {
+    for (int d = 0; d < w.G; ++d)
+      if ((hit >> d) & 1ull) rank_d[t * w.G + d] += s_cnt[warp * C + d];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k)
+      if (k < w.K) rank_e[t * w.K + k] = S[k] >= 0 ? re[k] + s_cnt[warp * C + w.G + S[k]] : -1;
+    hitmask[t] = hit;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// notify: one CTA.  chunk_cnt -> exclusive chunk offsets (in place) + totals;
+// totals stored into every GPU's count matrix; barrier; derived offsets.
+//   eoff[s_loc][e] = ebase[e] + sum_{s' < s} c[s', e]  (expert-major base of
+//   source s's rows for slot e at dest(e)), where ebase[e] = sum of N_e' over
+//   earlier local slots of the same destination.
+__global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp, int nchunks,
+                                                 int32_t* __restrict__ chunk_cnt,
+                                                 Offsets* __restrict__ offs,
+                                                 int32_t* __restrict__ eoff,
+                                                 int32_t* __restrict__ n_e,
+                                                 unsigned long long epoch, int* __restrict__ status) {
+  const WorldDev& w = *wp;
+  const int C = w.G + w.E;
+  for (int i = threadIdx.x; i < w.L * C; i += blockDim.x) {
+    int s_loc = i / C, c = i % C;
+    int32_t* col = chunk_cnt + (int64_t)s_loc * nchunks * C + c;
+    int run = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      int v = col[(int64_t)ch * C];
+      col[(int64_t)ch * C] = run;
+      run += v;
+    }
+    int sg = w.p * w.L + s_loc;
+    for (int q = 0; q < w.P; ++q) w.counts[q * w.L][(int64_t)sg * C + c] = run;
+  }
+  cta_barrier(w, epoch, status);
+  const int32_t* cnt = w.counts[w.p * w.L];  // complete [G][G+E] matrix
+  __shared__ int32_t s_n[1024];
+  for (int e = threadIdx.x; e < w.E; e += blockDim.x) {
+    int s = 0;
+    for (int src = 0; src < w.G; ++src) s += cnt[(int64_t)src * C + w.G + e];
+    s_n[e] = s;
+    n_e[e] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < w.L * w.E; i += blockDim.x) {
+    int s_loc = i / w.E, e = i % w.E;
+    int sg = w.p * w.L + s_loc;
+    int base = 0;
+    for (int e2 = (e / w.E_loc) * w.E_loc; e2 < e; ++e2) base += s_n[e2];
+    for (int src = 0; src < sg; ++src) base += cnt[(int64_t)src * C + w.G + e];
+    eoff[i] = base;
+  }
+  for (int i = threadIdx.x; i < w.L * w.G; i += blockDim.x) {
+    int s_loc = i / w.G, d = i % w.G;
+    int sg = w.p * w.L + s_loc;
+    int o = 0;
+    for (int src = 0; src < sg; ++src) o += cnt[(int64_t)src * C + d];
+    offs->off[s_loc][d] = o;
+  }
+  for (int d_loc = threadIdx.x; d_loc < w.L; d_loc += blockDim.x) {
+    int dg = w.p * w.L + d_loc;
+    int r = 0;
+    for (int src = 0; src < w.G; ++src) r += cnt[(int64_t)src * C + dg];
+    offs->R[d_loc] = r;
+    int n = 0;
+    for (int e = dg * w.E_loc; e < (dg + 1) * w.E_loc; ++e) n += s_n[e];
+    offs->Nd[d_loc] = n;
+    if (r > w.R_cap || n > w.N_cap) atomicExch(status, 2);  // capacity overflow
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 16-byte vector helpers
+__device__ __forceinline__ int4 ld_nc_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_na_v4(int4* p, int4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w));
+}
+
+constexpr int kUnroll = 8;  // 16-B vectors per lane in flight (4 KB per warp)
+
+// pack: warp per token.  dedup: one copy per hit destination + per-row meta;
+// raw: one copy per selection into expert-major rows.
+__global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
+                                              const uint8_t* __restrict__ x,
+                                              const int32_t* __restrict__ ids,
+                                              const float* __restrict__ wts,
+                                              const int32_t* __restrict__ chunk_off,
+                                              const int32_t* __restrict__ rank_d,
+                                              const int32_t* __restrict__ rank_e,
+                                              const unsigned long long* __restrict__ hitmask,
+                                              const Offsets* __restrict__ offs,
+                                              const int32_t* __restrict__ eoff, int nchunks,
+                                              int dedup, int32_t* __restrict__ gpos,
+                                              int32_t* __restrict__ epos_out,
+                                              int* __restrict__ status) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int C = w.G + w.E;
+  const int64_t nvec = w.row_bytes / 16;
+  const int64_t T = (int64_t)w.L * w.T_r;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = warp; t < T; t += nw) {
+    const int s_loc = (int)(t / w.T_r);
+    const int64_t t_in = t - (int64_t)s_loc * w.T_r;
+    const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
+    // expert-major positions of my picks (lane k < K computes pick k)
+    int my_e = -1, my_ep = -1;
+    float my_w = 0.f;
+    if (lane < w.K) {
+      my_e = ids[t * w.K + lane];
+      my_w = wts ? wts[t * w.K + lane] : 0.f;
+      if (my_e >= 0) {
+        my_ep = eoff[s_loc * w.E + my_e] + coff[w.G + my_e] + rank_e[t * w.K + lane];
+        if (my_ep >= w.N_cap) {
+          atomicExch(status, 2);
+          my_ep = -1;
+        }
+      }
+      epos_out[t * w.K + lane] = my_ep;
+    }
+    const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
+    unsigned long long hit = hitmask[t];
+    // destinations (dedup) or picks (raw) this row goes to
+    int ndst = 0;
+    int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+    uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+    if (dedup) {
+      for (int d = 0; d < w.G; ++d) {
+        if (!((hit >> d) & 1ull)) continue;
+        int64_t g = (int64_t)offs->off[s_loc][d] + coff[d] + rank_d[t * w.G + d];
+        if (lane == 0) gpos[t * w.G + d] = (int32_t)g;
+        if (g >= w.R_cap) {
+          if (lane == 0) atomicExch(status, 2);
+          continue;
+        }
+        // meta: lane k writes pick k's local expert-major row (or -1) + weight
+        int pe = __shfl_sync(0xffffffffu, my_e, lane < w.K ? lane : 0);
+        (void)pe;
+        if (lane < w.K) {
+          RowMeta m;
+          m.epos = (my_e >= 0 && my_e / w.E_loc == d) ? my_ep : -1;
+          m.w = my_w;
+          w.recv_meta[d][g * w.K + lane] = m;
+        }
+        dst_base[ndst] = w.recv_x[d];
+        dst_row[ndst] = g;
+        ++ndst;
+      }
+      if (lane == 0)
+        for (int d = 0; d < w.G; ++d)
+          if (!((hit >> d) & 1ull)) gpos[t * w.G + d] = -1;
+    } else {
+      for (int k = 0; k < w.K; ++k) {
+        int e = __shfl_sync(0xffffffffu, my_e, k);
+        int ep = __shfl_sync(0xffffffffu, my_ep, k);
+        if (e < 0 || ep < 0) continue;
+        dst_base[ndst] = w.xmaj[e / w.E_loc];
+        dst_row[ndst] = ep;
+        ++ndst;
+      }
+    }
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+      int4 buf[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = ld_nc_v4(src + v);
+      }
+      for (int j = 0; j < ndst; ++j) {
+        int4* dst = reinterpret_cast<int4*>(dst_base[j] + dst_row[j] * w.row_bytes);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          int64_t v = v0 + u * 32 + lane;
+          if (v < nvec) st_na_v4(dst + v, buf[u]);
+        }
+      }
+    }
+  }
+}
+
+// expand (dedup, destination side): warp per received row -> its local
+// experts' expert-major rows.
+__global__ void __launch_bounds__(256) k_expand(const WorldDev* __restrict__ wp,
+                                                const Offsets* __restrict__ offs) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t total = 0;
+  for (int d = 0; d < w.L; ++d) total += offs->R[d];
+  for (int64_t i = warp; i < total; i += nw) {
+    int d_loc = 0;
+    int64_t r = i;
+    while (r >= offs->R[d_loc]) {
+      r -= offs->R[d_loc];
+      ++d_loc;
+    }
+    const int dg = w.p * w.L + d_loc;
+    int ep = -1;
+    if (lane < w.K) ep = w.recv_meta[dg][r * w.K + lane].epos;
+    const int4* src = reinterpret_cast<const int4*>(w.recv_x[dg] + r * w.row_bytes);
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+      int4 buf[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = ld_nc_v4(src + v);
+      }
+      for (int k = 0; k < w.K; ++k) {
+        int e = __shfl_sync(0xffffffffu, ep, k);
+        if (e < 0) continue;
+        int4* dst = reinterpret_cast<int4*>(w.xmaj[dg] + (int64_t)e * w.row_bytes);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          int64_t v = v0 + u * 32 + lane;
+          if (v < nvec) st_na_v4(dst + v, buf[u]);
+        }
+      }
+    }
+  }
+}
+
+// element conversion helpers for 16-B vectors: 8 bf16 or 4 fp32
+template <typename T>
+struct Vec;
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void to_f32(const int4& v, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 x = __bfloat1622float2(h[i]);
+      f[2 * i] = x.x;
+      f[2 * i + 1] = x.y;
+    }
+  }
+  __device__ static int4 from_f32(const float* f) {
+    int4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ static void to_f32(const int4& v, float* f) {
+    f[0] = __int_as_float(v.x);
+    f[1] = __int_as_float(v.y);
+    f[2] = __int_as_float(v.z);
+    f[3] = __int_as_float(v.w);
+  }
+  __device__ static int4 from_f32(const float* f) {
+    return make_int4(__float_as_int(f[0]), __float_as_int(f[1]), __float_as_int(f[2]),
+                     __float_as_int(f[3]));
+  }
+};
+
+constexpr int kRedUnroll = 4;
+
+// reduce (dedup, destination side): partial[i] = sum_k w_k * y[epos_k] over the
+// row's local picks in k order, fp32 accumulation, stored in payload dtype.
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
+                                                const Offsets* __restrict__ offs) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t total = 0;
+  for (int d = 0; d < w.L; ++d) total += offs->R[d];
+  for (int64_t i = warp; i < total; i += nw) {
+    int d_loc = 0;
+    int64_t r = i;
+    while (r >= offs->R[d_loc]) {
+      r -= offs->R[d_loc];
+      ++d_loc;
+    }
+    const int dg = w.p * w.L + d_loc;
+    int ep = -1;
+    float wt = 0.f;
+    if (lane < w.K) {
+      RowMeta m = w.recv_meta[dg][r * w.K + lane];
+      ep = m.epos;
+      wt = m.w;
+    }
+    int4* dst = reinterpret_cast<int4*>(w.comb[dg] + r * w.row_bytes);
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kRedUnroll) {
+      float acc[kRedUnroll][Vec<T>::N];
+#pragma unroll
+      for (int u = 0; u < kRedUnroll; ++u)
+#pragma unroll
+        for (int j = 0; j < Vec<T>::N; ++j) acc[u][j] = 0.f;
+      for (int k = 0; k < w.K; ++k) {
+        int e = __shfl_sync(0xffffffffu, ep, k);
+        float wk = __shfl_sync(0xffffffffu, wt, k);
+        if (e < 0) continue;
+        const int4* src = reinterpret_cast<const int4*>(w.ymaj[dg] + (int64_t)e * w.row_bytes);
+        int4 buf[kRedUnroll];
+#pragma unroll
+        for (int u = 0; u < kRedUnroll; ++u) {
+          int64_t v = v0 + u * 32 + lane;
+          if (v < nvec) buf[u] = ld_nc_v4(src + v);
+        }
+#pragma unroll
+        for (int u = 0; u < kRedUnroll; ++u) {
+          float f[Vec<T>::N];
+          Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+          for (int j = 0; j < Vec<T>::N; ++j) acc[u][j] = fmaf(wk, f[j], acc[u][j]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRedUnroll; ++u) {
+        int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) st_na_v4(dst + v, Vec<T>::from_f32(acc[u]));
+      }
+    }
+  }
+}
+
+// gather (source side).  dedup: out[t] = sum over hit destinations d
+// (ascending) of comb[d][gpos[t,d]]; raw: out[t] = sum_k w_k * ymaj[dest][epos].
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
+                                                const int32_t* __restrict__ ids,
+                                                const float* __restrict__ wts,
+                                                const unsigned long long* __restrict__ hitmask,
+                                                const int32_t* __restrict__ gpos,
+                                                const int32_t* __restrict__ epos, int dedup,
+                                                uint8_t* __restrict__ out) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  const int64_t ntok = (int64_t)w.L * w.T_r;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = warp; t < ntok; t += nw) {
+    int n = 0;
+    const uint8_t* srcs[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+    float ws[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+    if (dedup) {
+      unsigned long long hit = hitmask[t];
+      for (int d = 0; d < w.G; ++d) {
+        if (!((hit >> d) & 1ull)) continue;
+        int g = gpos[t * w.G + d];
+        if (g < 0 || g >= w.R_cap) continue;
+        srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
+        ws[n] = 1.f;
+        ++n;
+      }
+    } else {
+      for (int k = 0; k < w.K; ++k) {
+        int e = ids[t * w.K + k];
+        int ep = epos[t * w.K + k];
+        if (e < 0 || ep < 0) continue;
+        srcs[n] = w.ymaj[e / w.E_loc] + (int64_t)ep * w.row_bytes;
+        ws[n] = wts[t * w.K + k];
+        ++n;
+      }
+    }
+    int4* dst = reinterpret_cast<int4*>(out + t * w.row_bytes);
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kRedUnroll) {
+      float acc[kRedUnroll][Vec<T>::N];
+#pragma unroll
+      for (int u = 0; u < kRedUnroll; ++u)
+#pragma unroll
+        for (int j = 0; j < Vec<T>::N; ++j) acc[u][j] = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const int4* src = reinterpret_cast<const int4*>(srcs[j]);
+        int4 buf[kRedUnroll];
+#pragma unroll
+        for (int u = 0; u < kRedUnroll; ++u) {
+          int64_t v = v0 + u * 32 + lane;
+          if (v < nvec) buf[u] = ld_v4(src + v);
+        }
+        const float wj = ws[j];
+#pragma unroll
+        for (int u = 0; u < kRedUnroll; ++u) {
+          float f[Vec<T>::N];
+          Vec<T>::to_f32(buf[u], f);
+          if (dedup) {
+#pragma unroll
+            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] += f[q];
+          } else {
+#pragma unroll
+            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRedUnroll; ++u) {
+        int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) st_na_v4(dst + v, Vec<T>::from_f32(acc[u]));
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// world object (host side)
+// ===========================================================================
+
+struct hm_world {
+  WorldDev h;            // host copy of the device table
+  WorldDev* d = nullptr;
+  int device = 0;
+  uint8_t* sym = nullptr;  // symmetric allocation (this GPU)
+  size_t sym_bytes = 0;
+  size_t off_recv_x = 0, off_meta = 0, off_xmaj = 0, off_ymaj = 0, off_comb = 0, off_counts = 0,
+         off_flags = 0;
+  std::vector<void*> opened;  // peer bases opened via IPC
+  // local scratch
+  int nchunks = 0;
+  int32_t* chunk_cnt = nullptr;
+  int32_t* rank_d = nullptr;
+  int32_t* rank_e = nullptr;
+  unsigned long long* hitmask = nullptr;
+  int32_t* gpos = nullptr;
+  int32_t* epos = nullptr;
+  Offsets* offs = nullptr;
+  int32_t* eoff = nullptr;
+  int32_t* n_e = nullptr;
+  int* status = nullptr;
+  unsigned long long epoch = 0;
+  bool peers_ready = false;
+  // optional per-kernel CUDA-event timing (segments recorded on the launch stream)
+  bool timing = false;
+  cudaEvent_t ev[2 * 16];
+  float seg_ms[16] = {0};
+  int seg_used[16] = {0};
+};
+
+// segment ids for hm_world_timings
+enum Seg { kSegPlan, kSegNotify, kSegPack, kSegBarrier1, kSegExpand, kSegReduce, kSegBarrier2,
+           kSegGather, kSegCount };
+
+struct SegScope {
+  hm_world* w;
+  int id;
+  cudaStream_t s;
+  SegScope(hm_world* w_, int id_, cudaStream_t s_) : w(w_), id(id_), s(s_) {
+    if (w->timing) cudaEventRecord(w->ev[2 * id], s);
+  }
+  ~SegScope() {
+    if (w->timing) {
+      cudaEventRecord(w->ev[2 * id + 1], s);
+      w->seg_used[id] = 1;
+    }
+  }
+};
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static void fill_tables(hm_world* w, int q, uint8_t* base) {
+  // virtual ranks q*L .. q*L+L-1 live on GPU q at `base`
+  WorldDev& h = w->h;
+  for (int l = 0; l < h.L; ++l) {
+    int d = q * h.L + l;
+    h.recv_x[d] = base + w->off_recv_x + (size_t)l * h.R_cap * h.row_bytes;
+    h.recv_meta[d] = reinterpret_cast<RowMeta*>(base + w->off_meta) + (size_t)l * h.R_cap * h.K;
+    h.xmaj[d] = base + w->off_xmaj + (size_t)l * h.N_cap * h.row_bytes;
+    h.ymaj[d] = base + w->off_ymaj + (size_t)l * h.N_cap * h.row_bytes;
+    h.comb[d] = base + w->off_comb + (size_t)l * h.R_cap * h.row_bytes;
+    h.counts[d] = reinterpret_cast<int32_t*>(base + w->off_counts);
+    h.flags[d] = reinterpret_cast<unsigned long long*>(base + w->off_flags);
+  }
+}
+
+HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
+                           int32_t top_k, int32_t hidden, int32_t elem_bytes,
+                           int64_t tokens_per_rank, int64_t n_cap_rows, hm_world** out) {
+  HM_CHECK_ARG(out, "hm_world_create: null out");
+  *out = nullptr;
+  HM_CHECK_ARG(ranks >= 1 && ranks <= kMaxRanks, "ranks must be 1..%d", kMaxRanks);
+  HM_CHECK_ARG(gpus >= 1 && ranks % gpus == 0, "ranks (%d) must be a multiple of gpus (%d)", ranks, gpus);
+  HM_CHECK_ARG(gpu_index >= 0 && gpu_index < gpus, "gpu_index out of range");
+  HM_CHECK_ARG(experts >= ranks && experts % ranks == 0,
+               "experts (%d) must be a positive multiple of the rank count (%d)", experts, ranks);
+  HM_CHECK_ARG(top_k >= 1 && top_k <= kMaxK && top_k <= experts, "top_k must be 1..%d", kMaxK);
+  HM_CHECK_ARG(elem_bytes == 2 || elem_bytes == 4, "elem_bytes must be 2 (bf16) or 4 (fp32)");
+  HM_CHECK_ARG(((int64_t)hidden * elem_bytes) % 16 == 0 && hidden > 0,
+               "hidden * elem_bytes must be a positive multiple of 16");
+  HM_CHECK_ARG(tokens_per_rank >= 1, "tokens_per_rank must be >= 1");
+  HM_CHECK_ARG(experts + ranks <= 8192, "experts too large");
+  hm_world* w = new hm_world();
+  WorldDev& h = w->h;
+  memset(&h, 0, sizeof(h));
+  h.G = ranks;
+  h.P = gpus;
+  h.p = gpu_index;
+  h.L = ranks / gpus;
+  h.E = experts;
+  h.K = top_k;
+  h.M = hidden;
+  h.E_loc = experts / ranks;
+  h.elem = elem_bytes;
+  h.T_r = tokens_per_rank;
+  h.row_bytes = (int64_t)hidden * elem_bytes;
+  h.R_cap = (int64_t)ranks * tokens_per_rank;
+  int64_t worst = (int64_t)ranks * tokens_per_rank * (top_k < h.E_loc ? top_k : h.E_loc);
+  h.N_cap = n_cap_rows > 0 && n_cap_rows < worst ? n_cap_rows : worst;
+  HM_CHECK_ARG(h.R_cap < (1ll << 31) && h.N_cap < (1ll << 31), "row capacity exceeds int32");
+  cudaGetDevice(&w->device);
+
+  size_t o = 0;
+  w->off_recv_x = o; o = align_up(o + (size_t)h.L * h.R_cap * h.row_bytes, 256);
+  w->off_meta = o;   o = align_up(o + (size_t)h.L * h.R_cap * h.K * sizeof(RowMeta), 256);
+  w->off_xmaj = o;   o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
+  w->off_ymaj = o;   o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
+  w->off_comb = o;   o = align_up(o + (size_t)h.L * h.R_cap * h.row_bytes, 256);
+  w->off_counts = o; o = align_up(o + (size_t)h.G * (h.G + h.E) * 4, 256);
+  w->off_flags = o;  o = align_up(o + (size_t)h.P * 8, 256);
+  w->sym_bytes = o;
+  int st;
+#define HM_TRY(call) do { st = hm::cuda_status(call); if (st) { delete w; return st; } } while (0)
+  HM_TRY(cudaMalloc(&w->sym, w->sym_bytes));
+  HM_TRY(cudaMemset(w->sym + w->off_counts, 0, w->sym_bytes - w->off_counts));
+  w->nchunks = (int)((tokens_per_rank + kChunk - 1) / kChunk);
+  const int64_t T = (int64_t)h.L * h.T_r;
+  HM_TRY(cudaMalloc(&w->chunk_cnt, (size_t)h.L * w->nchunks * (h.G + h.E) * 4));
+  HM_TRY(cudaMalloc(&w->rank_d, (size_t)T * h.G * 4));
+  HM_TRY(cudaMalloc(&w->rank_e, (size_t)T * h.K * 4));
+  HM_TRY(cudaMalloc(&w->hitmask, (size_t)T * 8));
+  HM_TRY(cudaMalloc(&w->gpos, (size_t)T * h.G * 4));
+  HM_TRY(cudaMalloc(&w->epos, (size_t)T * h.K * 4));
+  HM_TRY(cudaMalloc(&w->offs, sizeof(Offsets)));
+  HM_TRY(cudaMalloc(&w->eoff, (size_t)h.L * h.E * 4));
+  HM_TRY(cudaMalloc(&w->n_e, (size_t)h.E * 4));
+  HM_TRY(cudaMalloc(&w->status, 16));
+  HM_TRY(cudaMemset(w->status, 0, 16));
+  HM_TRY(cudaMalloc(&w->d, sizeof(WorldDev)));
+  fill_tables(w, h.p, w->sym);
+  if (h.P == 1) {
+    HM_TRY(cudaMemcpy(w->d, &h, sizeof(WorldDev), cudaMemcpyHostToDevice));
+    w->peers_ready = true;
+  }
+#undef HM_TRY
+  *out = w;
+  return 0;
+}
+
+HM_API int hm_world_destroy(hm_world* w) {
+  if (!w) return 0;
+  if (w->timing)
+    for (int i = 0; i < 2 * 16; ++i) cudaEventDestroy(w->ev[i]);
+  for (void* p : w->opened) cudaIpcCloseMemHandle(p);
+  cudaFree(w->sym);
+  cudaFree(w->chunk_cnt);
+  cudaFree(w->rank_d);
+  cudaFree(w->rank_e);
+  cudaFree(w->hitmask);
+  cudaFree(w->gpos);
+  cudaFree(w->epos);
+  cudaFree(w->offs);
+  cudaFree(w->eoff);
+  cudaFree(w->n_e);
+  cudaFree(w->status);
+  cudaFree(w->d);
+  delete w;
+  return 0;
+}
+
+HM_API int64_t hm_world_ipc_handle_size(void) { return (int64_t)sizeof(cudaIpcMemHandle_t); }
+
+HM_API int hm_world_ipc_handle(hm_world* w, void* out_handle) {
+  HM_CHECK_ARG(w && out_handle, "hm_world_ipc_handle: null argument");
+  cudaIpcMemHandle_t hnd;
+  HM_CUDA(cudaIpcGetMemHandle(&hnd, w->sym));
+  memcpy(out_handle, &hnd, sizeof(hnd));
+  return 0;
+}
+
+// handles: P consecutive cudaIpcMemHandle_t, index = GPU index (own entry ignored)
+HM_API int hm_world_open_peers(hm_world* w, const void* handles) {
+  HM_CHECK_ARG(w && handles, "hm_world_open_peers: null argument");
+  const cudaIpcMemHandle_t* hs = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int q = 0; q < w->h.P; ++q) {
+    if (q == w->h.p) continue;
+    void* base = nullptr;
+    HM_CUDA(cudaIpcOpenMemHandle(&base, hs[q], cudaIpcMemLazyEnablePeerAccess));
+    w->opened.push_back(base);
+    fill_tables(w, q, reinterpret_cast<uint8_t*>(base));
+  }
+  HM_CUDA(cudaMemcpy(w->d, &w->h, sizeof(WorldDev), cudaMemcpyHostToDevice));
+  w->peers_ready = true;
+  return 0;
+}
+
+HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
+                         const int32_t* expert_to_slot, int32_t renormalize, int32_t* slot_ids,
+                         float* weights, int32_t* expert_ids, void* stream) {
+  HM_CHECK_ARG(E >= 1 && E <= 512, "hm_route_topk: E must be 1..512");
+  HM_CHECK_ARG(K >= 1 && K <= kMaxK && K <= E, "hm_route_topk: K must be 1..%d and <= E", kMaxK);
+  if (T == 0) return 0;
+  int blocks = grid_for(T, 8, kSMs * 16);
+  cudaStream_t s = (cudaStream_t)stream;
+  int per = (E + 31) / 32;
+  if (per <= 1)
+    k_route<1><<<blocks, 256, 0, s>>>(logits, T, E, K, expert_to_slot, renormalize, slot_ids, weights, expert_ids);
+  else if (per <= 2)
+    k_route<2><<<blocks, 256, 0, s>>>(logits, T, E, K, expert_to_slot, renormalize, slot_ids, weights, expert_ids);
+  else if (per <= 4)
+    k_route<4><<<blocks, 256, 0, s>>>(logits, T, E, K, expert_to_slot, renormalize, slot_ids, weights, expert_ids);
+  else if (per <= 8)
+    k_route<8><<<blocks, 256, 0, s>>>(logits, T, E, K, expert_to_slot, renormalize, slot_ids, weights, expert_ids);
+  else
+    k_route<16><<<blocks, 256, 0, s>>>(logits, T, E, K, expert_to_slot, renormalize, slot_ids, weights, expert_ids);
+  HM_LAUNCHED();
+  return 0;
+}
+
+// dispatch: plan + notify (+barrier) + pack + barrier.  x: [L*T_r, M] payload
+// rows of this GPU's local source ranks; ids/wts: [L*T_r, K] slot ids + gates.
+HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
+                       int32_t dedup, void* stream) {
+  HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
+  if (!w->peers_ready) {
+    hm::set_error("hm_dispatch: peers not opened");
+    return hm::kNotReady;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const WorldDev& h = w->h;
+  dim3 grid(w->nchunks, h.L);
+  size_t smem = (size_t)kPlanWarps * (h.G + h.E) * 4;
+  if (smem > 48 * 1024)
+    HM_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  {SegScope sc(w, kSegPlan, s);
+  k_plan<<<grid, kChunk, smem, s>>>(w->d, ids, w->nchunks, w->chunk_cnt, w->rank_d, w->rank_e,
+                                    w->hitmask, w->status);
+  }
+  HM_LAUNCHED();
+  {SegScope sc(w, kSegNotify, s);
+  k_notify<<<1, 1024, 0, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e,
+                              ++w->epoch, w->status);
+  }
+  HM_LAUNCHED();
+  const int64_t T = (int64_t)h.L * h.T_r;
+  int blocks = grid_for(T, 8, kSMs * 8);
+  {SegScope sc(w, kSegPack, s);
+  k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
+                                w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, dedup,
+                                w->gpos, w->epos, w->status);
+  }
+  HM_LAUNCHED();
+  if (h.P > 1) {
+    SegScope sc(w, kSegBarrier1, s);
+    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    HM_LAUNCHED();
+  }
+  return 0;
+}
+
+HM_API int hm_expand(hm_world* w, void* stream) {
+  HM_CHECK_ARG(w, "hm_expand: null world");
+  int blocks = kSMs * 8;
+  SegScope sc(w, kSegExpand, (cudaStream_t)stream);
+  k_expand<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
+  HM_LAUNCHED();
+  return 0;
+}
+
+// combine: dedup -> reduce + barrier + gather; raw -> barrier + gather.
+// `out`: [L*T_r, M] payload rows.
+HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
+                      void* stream) {
+  HM_CHECK_ARG(w && out, "hm_combine: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const WorldDev& h = w->h;
+  if (dedup) {
+    SegScope sc(w, kSegReduce, s);
+    if (h.elem == 2)
+      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+    else
+      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+    HM_LAUNCHED();
+  } else {
+    HM_CHECK_ARG(wts && ids, "hm_combine: raw combine needs ids and weights");
+  }
+  if (h.P > 1) {
+    SegScope sc(w, kSegBarrier2, s);
+    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    HM_LAUNCHED();
+  }
+  const int64_t T = (int64_t)h.L * h.T_r;
+  int blocks = grid_for(T, 8, kSMs * 8);
+  SegScope sc(w, kSegGather, s);
+  if (h.elem == 2)
+    k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos,
+                                                   dedup, (uint8_t*)out);
+  else
+    k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos, dedup,
+                                           (uint8_t*)out);
+  HM_LAUNCHED();
+  return 0;
+}
+
+// explicit barrier (e.g. after an expert FFN when the raw combine follows)
+HM_API int hm_world_barrier(hm_world* w, void* stream) {
+  HM_CHECK_ARG(w, "hm_world_barrier: null world");
+  if (w->h.P > 1) {
+    k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(w->d, ++w->epoch, w->status);
+    HM_LAUNCHED();
+  }
+  return 0;
+}
+
+// buffer access for tests / the expert FFN.  kinds:
+//  0 recv_x  1 recv_meta  2 xmaj  3 ymaj  4 comb  (local rank l in 0..L-1)
+//  5 counts [G][G+E]  6 gpos [L*T_r][G]  7 epos [L*T_r][K]  8 hitmask [L*T_r]
+//  9 offsets (R[L] then Nd[L], int32)  10 n_e [E]  11 status [4] int32
+HM_API int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void** ptr,
+                           int64_t* bytes) {
+  HM_CHECK_ARG(w && ptr && bytes, "hm_world_buffer: null argument");
+  const WorldDev& h = w->h;
+  HM_CHECK_ARG(local_rank >= 0 && local_rank < h.L, "local_rank out of range");
+  int d = h.p * h.L + local_rank;
+  const int64_t T = (int64_t)h.L * h.T_r;
+  switch (kind) {
+    case 0: *ptr = h.recv_x[d]; *bytes = h.R_cap * h.row_bytes; break;
+    case 1: *ptr = h.recv_meta[d]; *bytes = h.R_cap * h.K * (int64_t)sizeof(RowMeta); break;
+    case 2: *ptr = h.xmaj[d]; *bytes = h.N_cap * h.row_bytes; break;
+    case 3: *ptr = h.ymaj[d]; *bytes = h.N_cap * h.row_bytes; break;
+    case 4: *ptr = h.comb[d]; *bytes = h.R_cap * h.row_bytes; break;
+    case 5: *ptr = h.counts[d]; *bytes = (int64_t)h.G * (h.G + h.E) * 4; break;
+    case 6: *ptr = w->gpos; *bytes = T * h.G * 4; break;
+    case 7: *ptr = w->epos; *bytes = T * h.K * 4; break;
+    case 8: *ptr = w->hitmask; *bytes = T * 8; break;
+    case 9: *ptr = reinterpret_cast<uint8_t*>(w->offs) + offsetof(Offsets, R);
+            *bytes = sizeof(int32_t) * 2 * kMaxRanks; break;
+    case 10: *ptr = w->n_e; *bytes = h.E * 4; break;
+    case 11: *ptr = w->status; *bytes = 16; break;
+    default: hm::set_error("hm_world_buffer: unknown kind %d", kind); return hm::kInvalid;
+  }
+  return 0;
+}
+
+HM_API int hm_world_info(hm_world* w, int64_t* out8) {
+  HM_CHECK_ARG(w && out8, "hm_world_info: null argument");
+  const WorldDev& h = w->h;
+  out8[0] = h.G; out8[1] = h.P; out8[2] = h.p; out8[3] = h.L;
+  out8[4] = h.R_cap; out8[5] = h.N_cap; out8[6] = h.row_bytes; out8[7] = (int64_t)w->sym_bytes;
+  return 0;
+}
+
+// stream-ordered device/host copy (cudaMemcpyDefault), for buffer inspection
+HM_API int hm_memcpy(void* dst, const void* src, int64_t bytes, void* stream) {
+  HM_CHECK_ARG(bytes >= 0, "hm_memcpy: negative size");
+  if (bytes == 0) return 0;
+  HM_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return 0;
+}
+
+// Per-kernel CUDA-event timing of the world's launches (enable=1 creates the
+// events; each launch records a start/stop pair on its stream).
+HM_API int hm_world_set_timing(hm_world* w, int32_t enable) {
+  HM_CHECK_ARG(w, "hm_world_set_timing: null world");
+  if (enable && !w->timing) {
+    for (int i = 0; i < 2 * 16; ++i) HM_CUDA(cudaEventCreate(&w->ev[i]));
+  }
+  w->timing = enable != 0 || w->timing;
+  if (!enable) w->timing = false;
+  for (int i = 0; i < 16; ++i) w->seg_used[i] = 0;
+  return 0;
+}
+
+// Milliseconds of the most recent launch of each segment (after a stream sync):
+// plan, notify, pack, barrier1, expand, reduce, barrier2, gather; -1 if unused.
+HM_API int hm_world_timings(hm_world* w, float* ms, int32_t n) {
+  HM_CHECK_ARG(w && ms, "hm_world_timings: null argument");
+  for (int i = 0; i < n && i < kSegCount; ++i) {
+    ms[i] = -1.f;
+    if (w->timing && w->seg_used[i]) {
+      float v = 0.f;
+      if (cudaEventElapsedTime(&v, w->ev[2 * i], w->ev[2 * i + 1]) == cudaSuccess) ms[i] = v;
+    }
+  }
+  return 0;
+}

@@ -1,0 +1,196 @@
+"""HierMoE layer hot path: gating, dedup dispatch, combine over an EP world.
+
+The reference (hiera2a) only *models* this exchange -- per-destination dedup
+counts (traffic.py:58-82) priced by an alpha-beta AlltoAll model
+(traffic.py:93-170).  ``EPWorld`` executes it on B200s:
+
+* G virtual expert-parallel ranks (``Topology.num_gpus``) are hosted on P
+  physical GPUs, one process per GPU (P = 1: all G ranks on one GPU, the
+  exchange runs through HBM; P > 1: CUDA-IPC peer mappings over NVLink 5);
+* slot s lives on rank s // (E/G) (topology.py:99-100); tokens are rank-major
+  (SPEC.md:310);
+* ``dispatch(dedup=True)`` ships one row per (token, destination rank) -- the
+  dedup mask is group_reduce(bits, G) (traffic.py:58-64) -- and re-expands it
+  into expert-major rows at the destination; ``dedup=False`` is the
+  non-deduplicated baseline (one row per selection, the reference's "std"
+  strategy, engine.py:6-8);
+* ``combine`` gate-weights and sums expert outputs back to the source:
+  dedup pre-reduces per destination and the source sums in ascending rank
+  order (deterministic, no float atomics).
+
+All kernels are stream-ordered; a dispatch/combine step performs no host
+synchronisation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ptr, stream_ptr
+
+_KIND = {"recv_x": 0, "recv_meta": 1, "xmaj": 2, "ymaj": 3, "comb": 4, "counts": 5, "gpos": 6,
+         "epos": 7, "hitmask": 8, "offsets": 9, "n_e": 10, "status": 11}
+
+_STATUS = {2: "row capacity overflow", 3: "peer barrier timeout", 4: "slot id out of range"}
+
+
+def route_topk(logits: torch.Tensor, top_k: int, expert_to_slot: torch.Tensor | None = None,
+               renormalize: bool = True):
+    """Softmax top-K gating on the GPU.
+
+    Selection is value-descending, expert-index-ascending on ties (bit-exact
+    indices); weights are softmax probabilities of the picks, renormalised
+    over the K picks when ``renormalize``.  Returns (slot_ids int32 [T,K],
+    weights fp32 [T,K], expert_ids int32 [T,K]).
+    """
+    if logits.dtype != torch.float32 or not logits.is_cuda or logits.ndim != 2:
+        raise ValueError("logits must be a 2-D float32 CUDA tensor")
+    logits = logits.contiguous()
+    t, e = logits.shape
+    slot = torch.empty((t, top_k), dtype=torch.int32, device=logits.device)
+    w = torch.empty((t, top_k), dtype=torch.float32, device=logits.device)
+    ex = torch.empty((t, top_k), dtype=torch.int32, device=logits.device)
+    e2s = None if expert_to_slot is None else expert_to_slot.to(device=logits.device,
+                                                               dtype=torch.int32).contiguous()
+    _lib.call("hm_route_topk", ptr(logits), t, e, top_k, ptr(e2s), int(bool(renormalize)),
+              ptr(slot), ptr(w), ptr(ex), stream_ptr())
+    return slot, w, ex
+
+
+class EPWorld:
+    """G virtual EP ranks on P GPUs with symmetric dispatch/combine buffers.
+
+    ``tokens_per_rank`` is the per-rank token capacity T_r; every call moves
+    all L = G/P local ranks' tokens: x is [L*T_r, M], ids/weights [L*T_r, K].
+    """
+
+    def __init__(self, ranks: int, experts: int, top_k: int, hidden: int,
+                 tokens_per_rank: int, dtype: torch.dtype = torch.bfloat16,
+                 gpus: int = 1, gpu_index: int = 0, group=None, n_cap_rows: int = 0):
+        lib = _lib.load()
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("payload dtype must be bfloat16 or float32")
+        self.ranks, self.experts, self.top_k, self.hidden = ranks, experts, top_k, hidden
+        self.tokens_per_rank, self.dtype = tokens_per_rank, dtype
+        self.gpus, self.gpu_index = gpus, gpu_index
+        self.local = ranks // gpus
+        self.elem = 2 if dtype == torch.bfloat16 else 4
+        h = ctypes.c_void_p()
+        _lib.check(lib.hm_world_create(ranks, gpus, gpu_index, experts, top_k, hidden, self.elem,
+                                       tokens_per_rank, n_cap_rows, ctypes.byref(h)),
+                   "hm_world_create")
+        self._h = h
+        info = (ctypes.c_int64 * 8)()
+        _lib.check(lib.hm_world_info(h, info), "hm_world_info")
+        self.r_cap, self.n_cap, self.row_bytes, self.sym_bytes = info[4], info[5], info[6], info[7]
+        if gpus > 1:
+            self._open_peers(group)
+
+    def _open_peers(self, group) -> None:
+        import torch.distributed as dist
+        lib = _lib.load()
+        n = int(lib.hm_world_ipc_handle_size())
+        mine = (ctypes.c_uint8 * n)()
+        _lib.check(lib.hm_world_ipc_handle(self._h, mine), "hm_world_ipc_handle")
+        local = torch.tensor(bytearray(mine), dtype=torch.uint8, device="cuda")
+        gathered = [torch.empty_like(local) for _ in range(self.gpus)]
+        dist.all_gather(gathered, local, group=group)
+        allh = torch.cat(gathered).cpu().numpy().tobytes()
+        buf = (ctypes.c_uint8 * len(allh)).from_buffer_copy(allh)
+        _lib.check(lib.hm_world_open_peers(self._h, buf), "hm_world_open_peers")
+        dist.barrier(group=group)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and _lib._lib is not None:
+            _lib._lib.hm_world_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ step
+    def dispatch(self, x: torch.Tensor, slot_ids: torch.Tensor, weights: torch.Tensor | None,
+                 dedup: bool = True) -> None:
+        """Plan + exchange; afterwards each local rank's expert-major rows
+        (``xmaj``) hold its experts' inputs."""
+        self._check_rows(x, slot_ids)
+        s = stream_ptr()
+        _lib.call("hm_dispatch", self._h, ptr(x), ptr(slot_ids), ptr(weights), int(dedup), s)
+        if dedup:
+            _lib.call("hm_expand", self._h, s)
+
+    def combine(self, slot_ids: torch.Tensor, weights: torch.Tensor, dedup: bool = True,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+        """Gate-weighted sum of the expert outputs (``ymaj``) back at the source."""
+        t = self.local * self.tokens_per_rank
+        if out is None:
+            out = torch.empty((t, self.hidden), dtype=self.dtype, device="cuda")
+        _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), int(dedup), ptr(out),
+                  stream_ptr())
+        return out
+
+    def barrier(self) -> None:
+        _lib.call("hm_world_barrier", self._h, stream_ptr())
+
+    def _check_rows(self, x, ids):
+        t = self.local * self.tokens_per_rank
+        if x.shape != (t, self.hidden) or x.dtype != self.dtype or not x.is_contiguous():
+            raise ValueError(f"x must be a contiguous [{t}, {self.hidden}] {self.dtype} tensor")
+        if ids.shape != (t, self.top_k) or ids.dtype != torch.int32 or not ids.is_contiguous():
+            raise ValueError(f"slot ids must be a contiguous [{t}, {self.top_k}] int32 tensor")
+
+    # --------------------------------------------------------------- buffers
+    def buffer(self, kind: str, local_rank: int = 0) -> tuple[int, int]:
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _lib.call("hm_world_buffer", self._h, _KIND[kind], local_rank, ctypes.byref(p),
+                  ctypes.byref(n))
+        return int(p.value or 0), int(n.value)
+
+    def read(self, kind: str, local_rank: int = 0, dtype=torch.uint8, count: int | None = None):
+        """Copy (a prefix of) a world buffer into a new device tensor."""
+        p, n = self.buffer(kind, local_rank)
+        esz = torch.empty((), dtype=dtype).element_size()
+        count = n // esz if count is None else count
+        out = torch.empty(count, dtype=dtype, device="cuda")
+        _lib.call("hm_memcpy", ptr(out), p, count * esz, stream_ptr())
+        return out
+
+    def write(self, kind: str, src: torch.Tensor, local_rank: int = 0, offset_bytes: int = 0):
+        p, n = self.buffer(kind, local_rank)
+        nbytes = src.numel() * src.element_size()
+        if offset_bytes + nbytes > n:
+            raise ValueError("write exceeds buffer")
+        _lib.call("hm_memcpy", p + offset_bytes, ptr(src.contiguous()), nbytes, stream_ptr())
+
+    def counts(self) -> np.ndarray:
+        """[G, G+E] count matrix: h[s, d] dedup rows, then c[s, e] selections."""
+        c = self.read("counts", 0, torch.int32).cpu().numpy()
+        return c.reshape(self.ranks, self.ranks + self.experts)
+
+    def rows_received(self) -> np.ndarray:
+        """Per local rank: (dedup rows received R, expert-major rows N)."""
+        o = self.read("offsets", 0, torch.int32).cpu().numpy()
+        return np.stack([o[:self.local], o[64:64 + self.local]], axis=1)
+
+    def check_status(self) -> None:
+        st = self.read("status", 0, torch.int32).cpu().numpy()
+        if st[0]:
+            raise RuntimeError(f"EPWorld: {_STATUS.get(int(st[0]), 'device error')} "
+                               f"(status {int(st[0])})")
+
+    def expert_rows(self, local_rank: int, dtype=None) -> torch.Tensor:
+        """Copy of the expert-major inputs of a local rank ([N, M])."""
+        n = int(self.rows_received()[local_rank, 1])
+        dt = self.dtype if dtype is None else dtype
+        return self.read("xmaj", local_rank, dt, n * self.hidden).view(n, self.hidden)
+
+    def set_expert_outputs(self, local_rank: int, y: torch.Tensor) -> None:
+        self.write("ymaj", y.to(self.dtype), local_rank)
