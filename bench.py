@@ -1,0 +1,370 @@
+"""Benchmark: MoE-layer dispatch+combine (µs & tokens/s) with dedup, on B200.
+
+Default workload (BASELINE.json configs[1]): Qwen3-30B-A3B-shaped MoE layer,
+E = 128 experts, top-8, hidden 2048, bf16, expert parallelism over G = 8 EP
+ranks, 4096 tokens per rank, GPU-level dedup.  The 8 EP ranks are hosted on
+the N GPUs of the run (8/N ranks per GPU; N = 1 exchanges through HBM, N > 1
+over NVLink via CUDA-IPC peer stores), so the total work is fixed: strong
+scaling.
+
+One step = dispatch (top-K gating kernel, dedup plan, count exchange + barrier,
+pack/exchange of one row per (token, destination rank), destination
+re-expansion into expert-major rows) + combine (destination gate-weighted
+pre-reduce, barrier, source sum over destinations).  The expert FFN between
+them is excluded by the metric's definition (it is timed separately by
+--ffn when the grouped GEMM is built).  Expert outputs are resident in HBM.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+For N > 1 launch with torch.distributed.run (one process per GPU).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE layer dispatch+combine µs & tokens/s at 1/2/4/8 B200; comm bytes cut by dedup"
+CONFIGS = {
+    # name: (G ranks, E, K, M, tokens per rank, description)
+    "qwen3": (8, 128, 8, 2048, 4096,
+              "Qwen3-30B-A3B-shaped MoE layer: 128 experts, top-8, hidden 2048, bf16, EP=8, "
+              "GPU-level dedup"),
+    "dsv3": (8, 256, 8, 7168, 4096,
+             "DeepSeek-V3-shaped MoE layer: 256 routed experts, top-8, hidden 7168, bf16, EP=8"),
+    "configA": (8, 16, 2, 256, 512,
+                "reference CPU config: 16 experts, top-2, hidden 256, 4096 tokens, 8-rank EP world"),
+}
+SEGMENTS = ["plan", "notify", "pack", "barrier1", "expand", "reduce", "barrier2", "gather"]
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+class ClockSampler:
+    """SM clock + throttle reasons sampled via NVML every 10 ms during the
+    timed region (the B200_PROFILING.md clocks line, at finer resolution)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(sm), int(rs)))
+                    except Exception:
+                        pass
+                    time.sleep(0.01)
+
+            self.t = threading.Thread(target=run, daemon=True)
+            self.t.start()
+        except Exception:
+            self.t = None
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm = [s for s, _ in self.samples]
+        loaded = [s for s in sm if self.max_mhz and s > 0.5 * self.max_mhz] or sm
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(cfg_name: str, steps: int, warmup: int, tokens_per_rank: int | None):
+    """The oracle port of the dispatch+combine step on the host cores."""
+    from oracle import moe as OM
+    G, E, K, M, T_r, _ = CONFIGS[cfg_name]
+    T_r = min(T_r, tokens_per_rank or 512)
+    rng = np.random.default_rng(0)
+    logits = rng.standard_normal((G * T_r, E)).astype(np.float32)
+    x = rng.standard_normal((G * T_r, M)).astype(np.float32)
+    threads = os.cpu_count() or 1
+    ids, w, _ = OM.route_topk(logits, K)
+    _, ym, _ = OM.cpu_dispatch_combine(x, ids, w, G, E, threads=threads)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        ids, w, _ = OM.route_topk(logits, K)
+        OM.cpu_dispatch_combine(x, ids, w, G, E, y_major=ym, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    sec = float(np.mean(times))
+    return {"value": G * T_r / sec, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{G * T_r} tokens ({G} ranks x {T_r}) of the {cfg_name} layer shape, "
+                      f"numpy fp32 dispatch+combine (oracle/moe.py cpu_dispatch_combine)",
+            "ms_per_step": sec * 1e3}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="qwen3", choices=list(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per EP rank")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    G, E, K, M, T_r, desc = CONFIGS[args.config]
+    if args.tokens:
+        T_r = args.tokens
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(args.config, max(1, min(args.steps, 5)), min(args.warmup, 1), 512)
+        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic", "impl": "reference",
+                "config": {"workload": desc, "ranks": G, "experts": E, "top_k": K, "hidden": M,
+                           "tokens_per_rank_sampled": 512},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200.layer import EPWorld, route_topk
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if G % world:
+        raise SystemExit(f"{G} EP ranks do not split over {world} GPUs")
+    L = G // world
+    dtype = torch.bfloat16
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    T = L * T_r
+    logits = torch.randn(T, E, device="cuda", generator=gen)
+    x = torch.randn(T, M, device="cuda", generator=gen).to(dtype)
+    ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
+    raw_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # 256 MB > L2
+
+    def prime(w_, dedup):
+        slot, wts, _ = route_topk(logits, K)
+        w_.dispatch(x, slot, wts, dedup=dedup)
+        for l in range(L):   # expert outputs: the expert-major inputs (resident)
+            p_x, _ = w_.buffer("xmaj", l)
+            p_y, nbytes = w_.buffer("ymaj", l)
+            _lib.call("hm_memcpy", p_y, p_x, nbytes, _lib.stream_ptr())
+        w_.combine(slot, wts, dedup=dedup)
+        torch.cuda.synchronize()
+        return slot, wts
+
+    def step(w_, dedup, out):
+        slot, wts, _ = route_topk(logits, K)
+        w_.dispatch(x, slot, wts, dedup=dedup)
+        w_.combine(slot, wts, dedup=dedup, out=out)
+
+    out = torch.empty(T, M, dtype=dtype, device="cuda")
+
+    def timed(w_, dedup, steps, warmup):
+        prime(w_, dedup)
+        for _ in range(warmup):
+            step(w_, dedup, out)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        total = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            step(w_, dedup, out)
+            s1.record()
+            s1.synchronize()
+            total += s0.elapsed_time(s1)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = torch.tensor([total / steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        w_.check_status()
+        return float(t.item())
+
+    with ClockSampler(local) as clocks:
+        ms = timed(ep, True, args.steps, args.warmup)
+    ms_raw = timed(raw_ep, False, max(3, args.steps // 2), args.warmup)
+
+    # per-kernel timing (CUDA events recorded by the library on the launch stream)
+    def seg_times(w_, dedup):
+        _lib.call("hm_world_set_timing", w_._h, 1)
+        acc = np.zeros(len(SEGMENTS))
+        n = 5
+        for _ in range(n):
+            flush.zero_()
+            step(w_, dedup, out)
+            torch.cuda.synchronize()
+            buf = (__import__("ctypes").c_float * len(SEGMENTS))()
+            _lib.call("hm_world_timings", w_._h, buf, len(SEGMENTS))
+            acc += np.maximum(np.array(buf[:]), 0)
+        _lib.call("hm_world_set_timing", w_._h, 0)
+        return acc / n
+
+    seg = seg_times(ep, True)
+    seg_raw = seg_times(raw_ep, False)
+
+    # bytes moved (this GPU)
+    cnt = ep.counts()
+    rows_dedup_out = int(cnt[rank * L:(rank + 1) * L, :G].sum())
+    rows_raw_out = int(cnt[rank * L:(rank + 1) * L, G:].sum())
+    recv = ep.rows_received()
+    R_in, N_in = int(recv[:, 0].sum()), int(recv[:, 1].sum())
+    rb = M * 2
+    # remote-only rows (destinations on other GPUs)
+    dest_gpu = np.arange(G) // L
+    remote = dest_gpu != rank
+    src_rows = cnt[rank * L:(rank + 1) * L]
+    rem_dedup = int(src_rows[:, :G][:, remote].sum())
+    slot_gpu = (np.arange(E) // (E // G)) // L
+    rem_raw = int(src_rows[:, G:][:, slot_gpu != rank].sum())
+    alg = {
+        "pack": T * rb + rows_dedup_out * rb + rows_dedup_out * K * 8,
+        "expand": R_in * rb + N_in * rb,
+        "reduce": N_in * rb + R_in * rb,
+        "gather": rows_dedup_out * rb + T * rb,
+    }
+    seg_ms = dict(zip(SEGMENTS, seg.tolist()))
+    dom = max(alg, key=lambda k: seg_ms[k])
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg[dom] / (seg_ms[dom] * 1e-3) / 1e9
+    tokens_total = G * T_r
+    value = tokens_total / (ms * 1e-3)
+
+    # end-to-end through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(T, M, dtype=dtype).pin_memory()
+        hx.copy_(x.cpu())
+        hl = torch.empty(T, E, dtype=torch.float32).pin_memory()
+        hl.copy_(logits.cpu())
+        ho = torch.empty(T, M, dtype=dtype).pin_memory()
+        dx = torch.empty_like(x)
+        dl = torch.empty_like(logits)
+        for _ in range(2):
+            dx.copy_(hx, non_blocking=True)
+            dl.copy_(hl, non_blocking=True)
+            slot, wts, _ = route_topk(dl, K)
+            ep.dispatch(dx, slot, wts, dedup=True)
+            ep.combine(slot, wts, dedup=True, out=out)
+            ho.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        n_e2e = max(3, args.steps // 2)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(n_e2e):
+            dx.copy_(hx, non_blocking=True)
+            dl.copy_(hl, non_blocking=True)
+            slot, wts, _ = route_topk(dl, K)
+            ep.dispatch(dx, slot, wts, dedup=True)
+            ep.combine(slot, wts, dedup=True, out=out)
+            ho.copy_(out, non_blocking=True)
+        s1.record()
+        s1.synchronize()
+        t = torch.tensor([s0.elapsed_time(s1) / n_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        e2e = {"value": tokens_total / (e2e_ms * 1e-3), "unit": "tokens/s",
+               "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(hx.numel() * 2 + hl.numel() * 4),
+               "d2h_bytes_per_step": int(ho.numel() * 2)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(args.config, 3, 1, 512)
+
+    launches_per_step = 1 + 3 + 1 + 1 + 1 + (2 if world > 1 else 0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "us_per_layer": ms * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": desc, "ranks": G, "gpus": world, "ranks_per_gpu": L,
+                       "experts": E, "top_k": K, "hidden": M, "tokens_per_rank": T_r,
+                       "global_tokens": tokens_total, "dedup_level": "GPU (EP rank)",
+                       "l2": "256 MB buffer written between timed steps (> 126 MB L2)",
+                       "timed": "route+plan+notify+pack+expand | reduce+gather (+barriers)"},
+            "dispatch_us": 1e3 * (seg_ms["plan"] + seg_ms["notify"] + seg_ms["pack"]
+                                  + seg_ms["barrier1"] + seg_ms["expand"]),
+            "combine_us": 1e3 * (seg_ms["reduce"] + seg_ms["barrier2"] + seg_ms["gather"]),
+            "kernel_ms": {k: round(v, 4) for k, v in seg_ms.items()},
+            "nodedup": {"ms_per_step": ms_raw, "value": tokens_total / (ms_raw * 1e-3),
+                        "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_raw.tolist())},
+                        "speedup_dedup_vs_nodedup": ms_raw / ms},
+            "comm_bytes": {"dedup_rows_out": rows_dedup_out, "raw_rows_out": rows_raw_out,
+                           "dedup_remote_bytes": rem_dedup * rb, "raw_remote_bytes": rem_raw * rb,
+                           "row_ratio_raw_over_dedup": rows_raw_out / max(1, rows_dedup_out)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "algorithmic_bytes": alg[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "cpu_baseline": None if cpu is None else
+            {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+    ep.close()
+    raw_ep.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

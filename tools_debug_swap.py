@@ -18,6 +18,6 @@ steps = [
 ]
 for name, fn in steps:
     try:
-        r = fn(); torch.cuda.synchronize(); print(name, "OK", r if not hasattr(r, "shape") or r.size < 40 else r.shape)
+        r = fn(); torch.cuda.synchronize(); print(name, "OK", r if not hasattr(r, "shape") else tuple(r.shape))
     except Exception as e:
         print(name, "FAIL", repr(e)[:300]); break
