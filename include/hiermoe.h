@@ -96,6 +96,9 @@ int hm_time_model(const int64_t* dedup_concat, const int32_t* fanout_groups, int
                   int32_t gpus, int64_t token_bytes, const double* a_inter, const double* b_inter,
                   const double* a_intra, const double* b_intra, int32_t* cut_offsets_dev,
                   double* times, int32_t* d_star, int64_t* maxima, void* stream);
+/* elementwise float64 x^y with numpy's rounding (np.power, used by
+ * swap.py:56-57; numpy_pow.cuh restates numpy's SVML pow). */
+int hm_np_pow(const double* x, const double* y, int64_t n, double* out, void* stream);
 /* smooth_max over `rows` vectors of length n (swap.py:35-48). */
 int hm_smooth_max_rows(const double* x, int64_t rows, int32_t n, double gamma, double* out,
                        void* stream);

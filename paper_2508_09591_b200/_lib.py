@@ -44,6 +44,7 @@ _SIGS = {
     "hm_time_model": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int64, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p]),
+    "hm_np_pow": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "hm_smooth_max_rows": (c_int32, [c_void_p, c_int64, c_int32, c_double, c_void_p, c_void_p]),
     "hm_world_create": (c_int32, [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
                                   c_int64, c_int64, POINTER(c_void_p)]),

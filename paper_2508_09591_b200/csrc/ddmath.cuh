@@ -81,7 +81,7 @@ HM_HD ddv mul_d(ddv a, double b) {
 // Taylor polynomial for expm1, ten squarings, scale by 2^m.
 HM_HD ddv exp(ddv a) {
   const ddv kLn2 = {6.9314718055994529e-01, 2.3190468138462996e-17};
-  if (a.hi > 709.7) return {INFINITY, 0.0};
+  if (a.hi > 709.782712893384) return {INFINITY, 0.0};
   if (a.hi < -745.2) return {0.0, 0.0};
   if (a.hi == 0.0 && a.lo == 0.0) return {1.0, 0.0};
   double m = floor(a.hi / kLn2.hi + 0.5);
@@ -115,15 +115,28 @@ HM_HD ddv exp(ddv a) {
   return {ldexp(e.hi, mi), ldexp(e.lo, mi)};
 }
 
-// natural log of a positive finite double, as double-double: one Newton step
-// y1 = y0 + x*exp(-y0) - 1 from the libm estimate y0.
+// natural log of a positive finite double, as double-double: x = m 2^e with
+// m in [0.5, 1); one Newton step y1 = y0 + m*exp(-y0) - 1 from the libm
+// estimate y0 = log(m), plus e*ln2 in double-double (no overflow for
+// subnormal x).
 HM_HD ddv log(double x) {
-  double y0 = ::log(x);
-  if (y0 == 0.0 && x == 1.0) return {0.0, 0.0};
-  ddv e = exp(ddv{-y0, 0.0});
-  ddv t = mul_d(e, x);
-  t = add_d(t, -1.0);
-  return add_d(t, y0);
+  if (x == 1.0) return {0.0, 0.0};
+  const ddv kLn2 = {6.9314718055994529e-01, 2.3190468138462996e-17};
+  int e;
+  double m = frexp(x, &e);
+  double y0 = ::log(m);
+  ddv ym = {y0, 0.0};
+  if (m != 0.5) {
+    ddv t = mul_d(exp(ddv{-y0, 0.0}), m);
+    t = add_d(t, -1.0);
+    ym = add_d(t, y0);
+  } else {
+    ym = {-kLn2.hi, -kLn2.lo};
+  }
+  ddv el = two_prod((double)e, kLn2.hi);
+  el.lo += (double)e * kLn2.lo;
+  el = quick_two_sum(el.hi, el.lo);
+  return add(el, ym);
 }
 
 }  // namespace dd

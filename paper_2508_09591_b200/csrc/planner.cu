@@ -584,6 +584,13 @@ __global__ void k_smooth_max_rows(const double* __restrict__ x, int64_t rows, in
   }
 }
 
+__global__ void k_np_pow(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                         double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = np_pow(x[i], y[i]);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -822,6 +829,16 @@ HM_API int hm_smooth_max_rows(const double* x, int64_t rows, int32_t n, double g
   HM_CHECK_ARG(gamma >= 1.0, "gamma must be >= 1, got %g", gamma);
   int blocks = grid_for(rows, 128, kSMs * 4);
   k_smooth_max_rows<<<blocks, 128, 0, (cudaStream_t)stream>>>(x, rows, n, gamma, 1.0 / gamma, out);
+  HM_LAUNCHED();
+  return 0;
+}
+
+// elementwise numpy float64 power (np.power rounding, see numpy_pow.cuh)
+HM_API int hm_np_pow(const double* x, const double* y, int64_t n, double* out, void* stream) {
+  HM_CHECK_ARG(n >= 0, "hm_np_pow: n < 0");
+  if (n == 0) return 0;
+  int blocks = grid_for(n, 256, kSMs * 16);
+  k_np_pow<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n, out);
   HM_LAUNCHED();
   return 0;
 }

@@ -101,9 +101,7 @@ def test_cost_matrix(hm, case):
             if ref is None:
                 continue
             q = hm.cost_matrix(st, topo, params, dim, gm)
-            np.testing.assert_allclose(q, ref, rtol=2e-15, atol=0)
-            if gname == "inf":
-                assert np.array_equal(q, ref)          # exact max: bitwise
+            assert np.array_equal(q, ref)              # bitwise, incl. numpy's SVML pow
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
@@ -165,3 +163,32 @@ def test_generator_matches_reference_stream(hm):
     # smoke-sim protocol: layer_seed(0, it, layer), uniform, 512 x 128, K = 8
     m = hm.generate_uniform(512, 128, 8, hm.layer_seed(0, 0, 0))
     assert m.bits.sum(axis=1).tolist() == [8] * 512
+
+
+def _svml_numpy() -> bool:
+    try:
+        from numpy._core._multiarray_umath import __cpu_features__ as f
+        return bool(f.get("AVX512_SKX"))
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(not _svml_numpy(), reason="host numpy does not use SVML pow")
+def test_device_np_pow_bitwise(hm):
+    """The device restatement of numpy's pow equals the host's np.power bit
+    for bit (numpy's AVX512_SKX SVML path, numpy_pow.cuh)."""
+    import torch
+    from paper_2508_09591_b200 import _lib
+    rng = np.random.default_rng(21)
+    z = rng.integers(0, 1 << 20, 500000)
+    m = z + rng.integers(0, 1 << 20, 500000) + 1
+    xs = [z / m, rng.uniform(1, 64, 500000), np.exp(rng.uniform(-60, 60, 500000))]
+    ys = [np.full(500000, 10.0), np.full(500000, 0.1), rng.uniform(0.02, 30, 500000)]
+    for x, y in zip(xs, ys):
+        dx, dy = torch.as_tensor(x, device="cuda"), torch.as_tensor(y, device="cuda")
+        out = torch.empty_like(dx)
+        _lib.call("hm_np_pow", dx.data_ptr(), dy.data_ptr(), x.size, out.data_ptr(),
+                  _lib.stream_ptr())
+        with np.errstate(over="ignore", under="ignore"):
+            ref = np.power(x, y)
+        assert np.array_equal(out.cpu().numpy(), ref)
