@@ -61,6 +61,30 @@ def route_topk(logits: torch.Tensor, top_k: int, expert_to_slot: torch.Tensor | 
     return slot, w, ex
 
 
+def exchange_handles(mine: bytes, index: int, gpus: int, group=None) -> bytes:
+    """All-gather one fixed-size IPC handle per GPU, ordered by GPU index.
+
+    Works over NCCL (CUDA tensors) and gloo (CPU tensors); the GPU index of a
+    process must equal its rank in ``group``.
+    """
+    import torch.distributed as dist
+    if dist.get_world_size(group) != gpus or dist.get_rank(group) != index:
+        raise ValueError("gpu_index/gpus must match the process group rank/size")
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    local = torch.tensor(bytearray(mine), dtype=torch.uint8, device=dev)
+    parts = [torch.empty_like(local) for _ in range(gpus)]
+    dist.all_gather(parts, local, group=group)
+    return torch.cat(parts).cpu().numpy().tobytes()
+
+
+def rank_placement(ranks: int, gpus: int, gpu_index: int) -> range:
+    """Virtual EP ranks hosted on one GPU: contiguous blocks of L = G/P."""
+    if gpus < 1 or ranks % gpus:
+        raise ValueError(f"ranks ({ranks}) must be a multiple of gpus ({gpus})")
+    per = ranks // gpus
+    return range(gpu_index * per, (gpu_index + 1) * per)
+
+
 class EPWorld:
     """G virtual EP ranks on P GPUs with symmetric dispatch/combine buffers.
 
@@ -96,10 +120,7 @@ class EPWorld:
         n = int(lib.hm_world_ipc_handle_size())
         mine = (ctypes.c_uint8 * n)()
         _lib.check(lib.hm_world_ipc_handle(self._h, mine), "hm_world_ipc_handle")
-        local = torch.tensor(bytearray(mine), dtype=torch.uint8, device="cuda")
-        gathered = [torch.empty_like(local) for _ in range(self.gpus)]
-        dist.all_gather(gathered, local, group=group)
-        allh = torch.cat(gathered).cpu().numpy().tobytes()
+        allh = exchange_handles(bytes(mine), self.gpu_index, self.gpus, group)
         buf = (ctypes.c_uint8 * len(allh)).from_buffer_copy(allh)
         _lib.check(lib.hm_world_open_peers(self._h, buf), "hm_world_open_peers")
         dist.barrier(group=group)
