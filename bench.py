@@ -174,6 +174,7 @@ def main():
     from paper_2508_09591_b200.layer import EPWorld, route_topk
 
     torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if G % world:
@@ -186,6 +187,8 @@ def main():
     x = torch.randn(T, M, device="cuda", generator=gen).to(dtype)
     ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
     raw_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
+    all_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
+    MODE = "remote"   # dedup rows across GPUs; same-GPU ranks go expert-major directly
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # 256 MB > L2
 
     def prime(w_, dedup):
@@ -233,8 +236,9 @@ def main():
         return float(t.item())
 
     with ClockSampler(local) as clocks:
-        ms = timed(ep, True, args.steps, args.warmup)
-    ms_raw = timed(raw_ep, False, max(3, args.steps // 2), args.warmup)
+        ms = timed(ep, MODE, args.steps, args.warmup)
+    ms_raw = timed(raw_ep, "none", max(3, args.steps // 2), args.warmup)
+    ms_all = timed(all_ep, "all", max(3, args.steps // 2), args.warmup)
 
     # per-kernel timing (CUDA events recorded by the library on the launch stream)
     def seg_times(w_, dedup):
@@ -251,34 +255,46 @@ def main():
         _lib.call("hm_world_set_timing", w_._h, 0)
         return acc / n
 
-    seg = seg_times(ep, True)
-    seg_raw = seg_times(raw_ep, False)
+    seg = seg_times(ep, MODE)
+    seg_raw = seg_times(raw_ep, "none")
+    seg_all = seg_times(all_ep, "all")
 
-    # bytes moved (this GPU)
+    # bytes moved by this GPU's kernels (algorithmic, per launch)
     cnt = ep.counts()
-    rows_dedup_out = int(cnt[rank * L:(rank + 1) * L, :G].sum())
-    rows_raw_out = int(cnt[rank * L:(rank + 1) * L, G:].sum())
-    recv = ep.rows_received()
-    R_in, N_in = int(recv[:, 0].sum()), int(recv[:, 1].sum())
     rb = M * 2
-    # remote-only rows (destinations on other GPUs)
+    mine = list(range(rank * L, (rank + 1) * L))
+    e_loc = E // G
     dest_gpu = np.arange(G) // L
-    remote = dest_gpu != rank
-    src_rows = cnt[rank * L:(rank + 1) * L]
-    rem_dedup = int(src_rows[:, :G][:, remote].sum())
-    slot_gpu = (np.arange(E) // (E // G)) // L
+    slot_gpu = (np.arange(E) // e_loc) // L
+    src_rows = cnt[mine]
+    rows_dedup_out = int(src_rows[:, :G].sum())             # "all" dedup rows
+    rows_raw_out = int(src_rows[:, G:].sum())               # one per selection
+    rem_dedup = int(src_rows[:, :G][:, dest_gpu != rank].sum())
     rem_raw = int(src_rows[:, G:][:, slot_gpu != rank].sum())
+    loc_direct = int(src_rows[:, G:][:, slot_gpu == rank].sum())
+    recv = ep.rows_received()
+    R_in = int(recv[:, 0].sum())                            # remote dedup rows received
+    src_gpu = np.arange(G) // L
+    N_rem_in = int(cnt[src_gpu != rank][:, G:][:, slot_gpu == rank].sum())
     alg = {
-        "pack": T * rb + rows_dedup_out * rb + rows_dedup_out * K * 8,
-        "expand": R_in * rb + N_in * rb,
-        "reduce": N_in * rb + R_in * rb,
-        "gather": rows_dedup_out * rb + T * rb,
+        "pack": T * rb + (rem_dedup + loc_direct) * rb + rem_dedup * K * 8,
+        "expand": R_in * rb + N_rem_in * rb + R_in * K * 8,
+        "reduce": N_rem_in * rb + R_in * rb + R_in * K * 8,
+        "gather": (rem_dedup + loc_direct) * rb + T * rb,
     }
+    link = {"pack": rem_dedup * rb, "gather": rem_dedup * rb}
     seg_ms = dict(zip(SEGMENTS, seg.tolist()))
+    raw_ms = dict(zip(SEGMENTS, seg_raw.tolist()))
+    link_dedup = seg_ms["pack"] + seg_ms["gather"] if world > 1 else 0.0
+    link_raw = raw_ms["pack"] + raw_ms["gather"] if world > 1 else 0.0
     dom = max(alg, key=lambda k: seg_ms[k])
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
     achieved = alg[dom] / (seg_ms[dom] * 1e-3) / 1e9
+    per_kernel = {k: {"ms": round(seg_ms[k], 4), "bytes": alg[k],
+                      "GBps": round(alg[k] / max(seg_ms[k], 1e-9) / 1e6, 1)} for k in alg}
+    for k in link:
+        per_kernel[k]["link_GBps"] = round(link[k] / max(seg_ms[k], 1e-9) / 1e6, 1)
     tokens_total = G * T_r
     value = tokens_total / (ms * 1e-3)
 
@@ -296,8 +312,8 @@ def main():
             dx.copy_(hx, non_blocking=True)
             dl.copy_(hl, non_blocking=True)
             slot, wts, _ = route_topk(dl, K)
-            ep.dispatch(dx, slot, wts, dedup=True)
-            ep.combine(slot, wts, dedup=True, out=out)
+            ep.dispatch(dx, slot, wts, dedup=MODE)
+            ep.combine(slot, wts, dedup=MODE, out=out)
             ho.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
         if world > 1:
@@ -310,8 +326,8 @@ def main():
             dx.copy_(hx, non_blocking=True)
             dl.copy_(hl, non_blocking=True)
             slot, wts, _ = route_topk(dl, K)
-            ep.dispatch(dx, slot, wts, dedup=True)
-            ep.combine(slot, wts, dedup=True, out=out)
+            ep.dispatch(dx, slot, wts, dedup=MODE)
+            ep.combine(slot, wts, dedup=MODE, out=out)
             ho.copy_(out, non_blocking=True)
         s1.record()
         s1.synchronize()
@@ -344,15 +360,28 @@ def main():
                                   + seg_ms["barrier1"] + seg_ms["expand"]),
             "combine_us": 1e3 * (seg_ms["reduce"] + seg_ms["barrier2"] + seg_ms["gather"]),
             "kernel_ms": {k: round(v, 4) for k, v in seg_ms.items()},
+            "kernels": per_kernel,
+            "transport": MODE,
             "nodedup": {"ms_per_step": ms_raw, "value": tokens_total / (ms_raw * 1e-3),
                         "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_raw.tolist())},
-                        "speedup_dedup_vs_nodedup": ms_raw / ms},
+                        "speedup_dedup_vs_nodedup": ms_raw / ms,
+                        "link_time_ratio": link_raw / max(link_dedup, 1e-9) if link_dedup else None},
+            "dedup_all_ranks": {"ms_per_step": ms_all,
+                                "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_all.tolist())}},
             "comm_bytes": {"dedup_rows_out": rows_dedup_out, "raw_rows_out": rows_raw_out,
                            "dedup_remote_bytes": rem_dedup * rb, "raw_remote_bytes": rem_raw * rb,
-                           "row_ratio_raw_over_dedup": rows_raw_out / max(1, rows_dedup_out)},
+                           "row_ratio_raw_over_dedup": rows_raw_out / max(1, rows_dedup_out),
+                           "remote_byte_ratio_raw_over_dedup":
+                               (rem_raw / rem_dedup) if rem_dedup else None},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                          "algorithmic_bytes": alg[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "link_roofline": None if world == 1 else {
+                "bound": "nvlink", "kernel": "pack+gather",
+                "achieved": 2 * rem_dedup * rb / (link_dedup * 1e-3) / 1e9,
+                "peak": 770.0, "unit": "GB/s",
+                "frac": 2 * rem_dedup * rb / (link_dedup * 1e-3) / 1e9 / 770.0,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"},
             "cpu_baseline": None if cpu is None else
             {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": e2e,
@@ -362,6 +391,7 @@ def main():
         print(json.dumps(line))
     ep.close()
     raw_ep.close()
+    all_ep.close()
     if world > 1:
         dist.destroy_process_group()
 

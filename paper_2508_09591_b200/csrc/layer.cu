@@ -198,12 +198,12 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
                                                  unsigned long long* __restrict__ hitmask,
                                                  int* __restrict__ status) {
   const WorldDev& w = *wp;
-  extern __shared__ int32_t s_cnt[];  // [kPlanWarps][G+E]
+  extern __shared__ int32_t s_cnt[];  // [kPlanWarps][G+E] counters, then [kPlanWarps][E] lane masks
   const int C = w.G + w.E;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s_loc = blockIdx.y;
   const int chunk = blockIdx.x;
-  for (int i = threadIdx.x; i < kPlanWarps * C; i += blockDim.x) s_cnt[i] = 0;
+  for (int i = threadIdx.x; i < kPlanWarps * (C + w.E); i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
   const int64_t t_in = (int64_t)chunk * kChunk + warp * 32 + lane;  // token within source
   const bool valid = t_in < w.T_r;
@@ -233,23 +233,18 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
     else if (valid) rank_d[t * w.G + d] = -1;
     if (lane == 0) s_cnt[warp * C + d] = __popc(b);
   }
-  // slot ranks within the warp: earlier lanes' picks equal to mine
-  int re[kMaxK];
-#pragma unroll
-  for (int k = 0; k < kMaxK; ++k) re[k] = 0;
-  for (int j = 0; j < 31; ++j) {
-    for (int k2 = 0; k2 < w.K; ++k2) {
-      int sj = __shfl_sync(0xffffffffu, S[k2 < kMaxK ? k2 : 0], j);
-      if (j < lane && sj >= 0) {
-#pragma unroll
-        for (int k = 0; k < kMaxK; ++k)
-          if (k < w.K && S[k] == sj) re[k]++;
-      }
-    }
-  }
+  // slot ranks within the warp: a lane mask per slot in shared memory; the
+  // rank of my pick = earlier lanes in that slot's mask (stable, O(K))
+  unsigned* s_lanes = reinterpret_cast<unsigned*>(s_cnt + kPlanWarps * C) + warp * w.E;
 #pragma unroll
   for (int k = 0; k < kMaxK; ++k)
-    if (k < w.K && S[k] >= 0) atomicAdd(&s_cnt[warp * C + w.G + S[k]], 1);
+    if (k < w.K && S[k] >= 0) atomicOr(s_lanes + S[k], 1u << lane);
+  __syncwarp();
+  int re[kMaxK];
+#pragma unroll
+  for (int k = 0; k < kMaxK; ++k)
+    re[k] = (k < w.K && S[k] >= 0) ? __popc(s_lanes[S[k]] & lt) : 0;
+  for (int e = lane; e < w.E; e += 32) s_cnt[warp * C + w.G + e] = __popc(s_lanes[e]);
   __syncthreads();
   // exclusive prefix over warps per counter; chunk totals out
   int32_t* out = chunk_cnt + ((int64_t)s_loc * nchunks + chunk) * C;
@@ -283,10 +278,13 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  int32_t* __restrict__ chunk_cnt,
                                                  Offsets* __restrict__ offs,
                                                  int32_t* __restrict__ eoff,
-                                                 int32_t* __restrict__ n_e,
+                                                 int32_t* __restrict__ n_e, int mode,
                                                  unsigned long long epoch, int* __restrict__ status) {
   const WorldDev& w = *wp;
   const int C = w.G + w.E;
+  // mode 2 (dedup across GPUs only): sources on the destination's own GPU
+  // write expert-major rows directly and occupy no receive rows
+  auto ships = [&](int src, int dst) { return mode != 2 || src / w.L != dst / w.L; };
   for (int i = threadIdx.x; i < w.L * C; i += blockDim.x) {
     int s_loc = i / C, c = i % C;
     int32_t* col = chunk_cnt + (int64_t)s_loc * nchunks * C + c;
@@ -319,15 +317,18 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
   }
   for (int i = threadIdx.x; i < w.L * w.G; i += blockDim.x) {
     int s_loc = i / w.G, d = i % w.G;
+    (void)0;
     int sg = w.p * w.L + s_loc;
     int o = 0;
-    for (int src = 0; src < sg; ++src) o += cnt[(int64_t)src * C + d];
+    for (int src = 0; src < sg; ++src)
+      if (ships(src, d)) o += cnt[(int64_t)src * C + d];
     offs->off[s_loc][d] = o;
   }
   for (int d_loc = threadIdx.x; d_loc < w.L; d_loc += blockDim.x) {
     int dg = w.p * w.L + d_loc;
     int r = 0;
-    for (int src = 0; src < w.G; ++src) r += cnt[(int64_t)src * C + dg];
+    for (int src = 0; src < w.G; ++src)
+      if (ships(src, dg)) r += cnt[(int64_t)src * C + dg];
     offs->R[d_loc] = r;
     int n = 0;
     for (int e = dg * w.E_loc; e < (dg + 1) * w.E_loc; ++e) n += s_n[e];
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               const unsigned long long* __restrict__ hitmask,
                                               const Offsets* __restrict__ offs,
                                               const int32_t* __restrict__ eoff, int nchunks,
-                                              int dedup, int32_t* __restrict__ gpos,
+                                              int mode, int32_t* __restrict__ gpos,
                                               int32_t* __restrict__ epos_out,
                                               int* __restrict__ status) {
   const WorldDev& w = *wp;
@@ -406,9 +407,22 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
     int ndst = 0;
     int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
     uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    if (dedup) {
+    if (mode) {
       for (int d = 0; d < w.G; ++d) {
         if (!((hit >> d) & 1ull)) continue;
+        if (mode == 2 && d / w.L == w.p) {
+          // same GPU: no link to save bytes on -- write expert-major rows directly
+          if (lane == 0) gpos[t * w.G + d] = -1;
+          for (int k = 0; k < w.K; ++k) {
+            int e = __shfl_sync(0xffffffffu, my_e, k);
+            int ep = __shfl_sync(0xffffffffu, my_ep, k);
+            if (e < 0 || ep < 0 || e / w.E_loc != d) continue;
+            dst_base[ndst] = w.xmaj[d];
+            dst_row[ndst] = ep;
+            ++ndst;
+          }
+          continue;
+        }
         int64_t g = (int64_t)offs->off[s_loc][d] + coff[d] + rank_d[t * w.G + d];
         if (lane == 0) gpos[t * w.G + d] = (int32_t)g;
         if (g >= w.R_cap) {
@@ -416,8 +430,6 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
           continue;
         }
         // meta: lane k writes pick k's local expert-major row (or -1) + weight
-        int pe = __shfl_sync(0xffffffffu, my_e, lane < w.K ? lane : 0);
-        (void)pe;
         if (lane < w.K) {
           RowMeta m;
           m.epos = (my_e >= 0 && my_e / w.E_loc == d) ? my_ep : -1;
@@ -613,7 +625,7 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
                                                 const float* __restrict__ wts,
                                                 const unsigned long long* __restrict__ hitmask,
                                                 const int32_t* __restrict__ gpos,
-                                                const int32_t* __restrict__ epos, int dedup,
+                                                const int32_t* __restrict__ epos, int mode,
                                                 uint8_t* __restrict__ out) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
@@ -625,10 +637,21 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
     int n = 0;
     const uint8_t* srcs[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
     float ws[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    if (dedup) {
+    if (mode) {
       unsigned long long hit = hitmask[t];
       for (int d = 0; d < w.G; ++d) {
         if (!((hit >> d) & 1ull)) continue;
+        if (mode == 2 && d / w.L == w.p) {  // same GPU: weighted expert rows directly
+          for (int k = 0; k < w.K; ++k) {
+            int e = ids[t * w.K + k];
+            int ep = epos[t * w.K + k];
+            if (e < 0 || ep < 0 || e / w.E_loc != d) continue;
+            srcs[n] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
+            ws[n] = wts[t * w.K + k];
+            ++n;
+          }
+          continue;
+        }
         int g = gpos[t * w.G + d];
         if (g < 0 || g >= w.R_cap) continue;
         srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
@@ -665,13 +688,8 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
         for (int u = 0; u < kRedUnroll; ++u) {
           float f[Vec<T>::N];
           Vec<T>::to_f32(buf[u], f);
-          if (dedup) {
 #pragma unroll
-            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] += f[q];
-          } else {
-#pragma unroll
-            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
-          }
+          for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
         }
       }
 #pragma unroll
@@ -901,8 +919,10 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
 // dispatch: plan + notify (+barrier) + pack + barrier.  x: [L*T_r, M] payload
 // rows of this GPU's local source ranks; ids/wts: [L*T_r, K] slot ids + gates.
 HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
-                       int32_t dedup, void* stream) {
+                       int32_t mode, void* stream) {
   HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
+  HM_CHECK_ARG(mode >= 0 && mode <= 2, "hm_dispatch: mode must be 0 (raw), 1 (dedup), 2 (dedup across GPUs)");
+  if (mode) HM_CHECK_ARG(wts, "hm_dispatch: dedup modes need gate weights");
   if (!w->peers_ready) {
     hm::set_error("hm_dispatch: peers not opened");
     return hm::kNotReady;
@@ -910,7 +930,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
   dim3 grid(w->nchunks, h.L);
-  size_t smem = (size_t)kPlanWarps * (h.G + h.E) * 4;
+  size_t smem = (size_t)kPlanWarps * (h.G + 2 * h.E) * 4;
   if (smem > 48 * 1024)
     HM_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {SegScope sc(w, kSegPlan, s);
@@ -919,7 +939,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   }
   HM_LAUNCHED();
   {SegScope sc(w, kSegNotify, s);
-  k_notify<<<1, 1024, 0, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e,
+  k_notify<<<1, 1024, 0, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e, mode,
                               ++w->epoch, w->status);
   }
   HM_LAUNCHED();
@@ -927,7 +947,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   int blocks = grid_for(T, 8, kSMs * 8);
   {SegScope sc(w, kSegPack, s);
   k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
-                                w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, dedup,
+                                w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
                                 w->gpos, w->epos, w->status);
   }
   HM_LAUNCHED();
@@ -950,9 +970,11 @@ HM_API int hm_expand(hm_world* w, void* stream) {
 
 // combine: dedup -> reduce + barrier + gather; raw -> barrier + gather.
 // `out`: [L*T_r, M] payload rows.
-HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
+HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t mode, void* out,
                       void* stream) {
   HM_CHECK_ARG(w && out, "hm_combine: null argument");
+  HM_CHECK_ARG(mode >= 0 && mode <= 2, "hm_combine: mode must be 0, 1 or 2");
+  const int dedup = mode;
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
   if (dedup) {
@@ -962,9 +984,8 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
     else
       k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
     HM_LAUNCHED();
-  } else {
-    HM_CHECK_ARG(wts && ids, "hm_combine: raw combine needs ids and weights");
   }
+  if (mode != 1) HM_CHECK_ARG(wts && ids, "hm_combine: raw/hybrid combine needs ids and weights");
   if (h.P > 1) {
     SegScope sc(w, kSegBarrier2, s);
     k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
@@ -975,9 +996,9 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   SegScope sc(w, kSegGather, s);
   if (h.elem == 2)
     k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos,
-                                                   dedup, (uint8_t*)out);
+                                                   mode, (uint8_t*)out);
   else
-    k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos, dedup,
+    k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode,
                                            (uint8_t*)out);
   HM_LAUNCHED();
   return 0;

@@ -37,6 +37,23 @@ _KIND = {"recv_x": 0, "recv_meta": 1, "xmaj": 2, "ymaj": 3, "comb": 4, "counts":
 
 _STATUS = {2: "row capacity overflow", 3: "peer barrier timeout", 4: "slot id out of range"}
 
+# transport modes: "none" one row per selection (no dedup, the reference's "std");
+# "all" one row per (token, destination rank) for every destination, including
+# ranks on the same GPU (the full dedup copy list); "remote" dedup rows only
+# across GPUs -- ranks sharing a GPU exchange through HBM without a link to
+# save bytes on, so their rows go straight to expert-major positions.
+MODES = {"none": 0, "all": 1, "remote": 2}
+
+
+def transport_mode(dedup) -> int:
+    if dedup is True:
+        return MODES["remote"]
+    if dedup is False or dedup is None:
+        return MODES["none"]
+    if dedup not in MODES:
+        raise ValueError(f"dedup must be a bool or one of {sorted(MODES)}")
+    return MODES[dedup]
+
 
 def route_topk(logits: torch.Tensor, top_k: int, expert_to_slot: torch.Tensor | None = None,
                renormalize: bool = True):
@@ -138,23 +155,25 @@ class EPWorld:
 
     # ------------------------------------------------------------------ step
     def dispatch(self, x: torch.Tensor, slot_ids: torch.Tensor, weights: torch.Tensor | None,
-                 dedup: bool = True) -> None:
+                 dedup=True) -> None:
         """Plan + exchange; afterwards each local rank's expert-major rows
-        (``xmaj``) hold its experts' inputs."""
+        (``xmaj``) hold its experts' inputs.  ``dedup``: True (= "remote"),
+        "all", or False (= "none"), see MODES."""
         self._check_rows(x, slot_ids)
+        mode = transport_mode(dedup)
         s = stream_ptr()
-        _lib.call("hm_dispatch", self._h, ptr(x), ptr(slot_ids), ptr(weights), int(dedup), s)
-        if dedup:
+        _lib.call("hm_dispatch", self._h, ptr(x), ptr(slot_ids), ptr(weights), mode, s)
+        if mode:
             _lib.call("hm_expand", self._h, s)
 
-    def combine(self, slot_ids: torch.Tensor, weights: torch.Tensor, dedup: bool = True,
+    def combine(self, slot_ids: torch.Tensor, weights: torch.Tensor, dedup=True,
                 out: torch.Tensor | None = None) -> torch.Tensor:
         """Gate-weighted sum of the expert outputs (``ymaj``) back at the source."""
         t = self.local * self.tokens_per_rank
         if out is None:
             out = torch.empty((t, self.hidden), dtype=self.dtype, device="cuda")
-        _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), int(dedup), ptr(out),
-                  stream_ptr())
+        _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), transport_mode(dedup),
+                  ptr(out), stream_ptr())
         return out
 
     def barrier(self) -> None:

@@ -46,11 +46,14 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
         xm = ep.read("xmaj", l, dtype, n * M).view(n, M).cpu()
         tt, kk = np.nonzero(ids_all // e_loc == d)
         assert torch.equal(xm.view(xb.dtype)[plan.epos[tt, kk]], xb[tt]), f"xmaj rank {d}"
-        if dedup:
+        if dedup in ("all", "remote"):
+            want = plan.recv_rows(d)
+            if dedup == "remote":   # only rows from sources on other GPUs cross a link
+                want = want[(want // T_r) // L != rank]
             r = int(rows[l, 0])
-            assert r == int(plan.h[:, d].sum())
+            assert r == want.size, (r, want.size)
             rx = ep.read("recv_x", l, dtype, r * M).view(r, M).cpu()
-            assert torch.equal(rx.view(xb.dtype), xb[plan.recv_rows(d)]), f"recv rank {d}"
+            assert torch.equal(rx.view(xb.dtype), xb[want]), f"recv rank {d}"
         # stand-in expert: y = x * (1 + slot / E)
         row_slot = np.repeat(np.arange(d * e_loc, (d + 1) * e_loc), plan.n_e[d * e_loc:(d + 1) * e_loc])
         s = torch.as_tensor(1.0 + row_slot / E, dtype=torch.float32).cuda()[:, None]
@@ -81,7 +84,7 @@ def main():
     cases = [(8, 16, 2, 256, 256, torch.float32), (8, 128, 8, 2048, 128, torch.bfloat16),
              (8, 256, 8, 512, 96, torch.bfloat16)]
     for i, (G, E, K, M, T_r, dt) in enumerate(cases):
-        for dedup in (True, False):
+        for dedup in ("all", "remote", "none"):
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
             dist.barrier()
     if rank == 0:
