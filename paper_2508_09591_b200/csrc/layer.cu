@@ -186,6 +186,88 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
   }
 }
 
+// K1 router, lane-per-token variant for compile-time K: a warp stages 32
+// tokens x 32 logits at a time in shared memory (coalesced loads, padded
+// rows -> conflict-free lane reads), every lane keeps its token's sorted top-K
+// in registers (insertion with an early-out against the K-th value; strict >
+// keeps the lower index on ties because columns arrive in ascending order).
+template <int K>
+__global__ void __launch_bounds__(256) k_route_lane(const float* __restrict__ logits, int64_t T,
+                                                    int E, const int32_t* __restrict__ e2s,
+                                                    int renorm, int32_t* __restrict__ slot_ids,
+                                                    float* __restrict__ weights,
+                                                    int32_t* __restrict__ expert_ids) {
+  __shared__ float tile[8][32][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float (*tl)[33] = tile[wid];
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t base = ((int64_t)blockIdx.x * 8 + wid) * 32; base < T; base += nwarps * 32) {
+    const int64_t t = base + lane;
+    float vals[K];
+    int idx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      vals[k] = -INFINITY;
+      idx[k] = 0x7fffffff;
+    }
+    for (int c0 = 0; c0 < E; c0 += 32) {
+      const int col = c0 + lane;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) {
+        int64_t tr = base + r;
+        tl[r][lane] = (tr < T && col < E) ? __ldg(logits + tr * E + col) : -INFINITY;
+      }
+      __syncwarp();
+      const int ncol = E - c0 < 32 ? E - c0 : 32;
+      for (int j = 0; j < ncol; ++j) {
+        float v = tl[lane][j];
+        if (v > vals[K - 1]) {
+          const int e = c0 + j;
+#pragma unroll
+          for (int k = K - 1; k > 0; --k) {
+            if (v > vals[k]) {
+              bool up = v > vals[k - 1];
+              vals[k] = up ? vals[k - 1] : v;
+              idx[k] = up ? idx[k - 1] : e;
+            }
+          }
+          if (v > vals[0]) {
+            vals[0] = v;
+            idx[0] = e;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    const float vmax = vals[0];
+    float denom = 0.f;
+    if (renorm) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) denom += expf(vals[k] - vmax);
+    } else {
+      for (int c0 = 0; c0 < E; c0 += 32) {   // second pass: full softmax denominator
+        const int col = c0 + lane;
+        for (int r = 0; r < 32; ++r) {
+          int64_t tr = base + r;
+          tl[r][lane] = (tr < T && col < E) ? __ldg(logits + tr * E + col) : -INFINITY;
+        }
+        __syncwarp();
+        const int ncol = E - c0 < 32 ? E - c0 : 32;
+        for (int j = 0; j < ncol; ++j) denom += expf(tl[lane][j] - vmax);
+        __syncwarp();
+      }
+    }
+    if (t < T) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        weights[t * K + k] = expf(vals[k] - vmax) / denom;
+        slot_ids[t * K + k] = e2s ? e2s[idx[k]] : idx[k];
+        if (expert_ids) expert_ids[t * K + k] = idx[k];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // plan: grid (chunks, L).  Stable ranks: destination ranks by warp ballot,
 // slot ranks by comparing with earlier lanes' picks via shuffles, then a
@@ -284,7 +366,9 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
   const int C = w.G + w.E;
   // mode 2 (dedup across GPUs only): sources on the destination's own GPU
   // write expert-major rows directly and occupy no receive rows
-  auto ships = [&](int src, int dst) { return mode != 2 || src / w.L != dst / w.L; };
+  auto ships = [&](int src, int dst) {
+    return mode == 1 || (mode == 2 && src / w.L != dst / w.L);
+  };
   for (int i = threadIdx.x; i < w.L * C; i += blockDim.x) {
     int s_loc = i / C, c = i % C;
     int32_t* col = chunk_cnt + (int64_t)s_loc * nchunks * C + c;
@@ -407,20 +491,25 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
     int ndst = 0;
     int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
     uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    if (mode) {
+    // direct expert-major rows: every pick (mode 0) or picks on this GPU (mode 2)
+    if (mode != 1) {
+      for (int k = 0; k < w.K; ++k) {
+        int e = __shfl_sync(0xffffffffu, my_e, k);
+        int ep = __shfl_sync(0xffffffffu, my_ep, k);
+        if (e < 0 || ep < 0) continue;
+        const int d = e / w.E_loc;
+        if (mode == 2 && d / w.L != w.p) continue;
+        dst_base[ndst] = w.xmaj[d];
+        dst_row[ndst] = ep;
+        ++ndst;
+      }
+    }
+    // dedup rows: every hit destination (mode 1) or destinations on other GPUs (mode 2)
+    if (mode != 0) {
       for (int d = 0; d < w.G; ++d) {
         if (!((hit >> d) & 1ull)) continue;
         if (mode == 2 && d / w.L == w.p) {
-          // same GPU: no link to save bytes on -- write expert-major rows directly
           if (lane == 0) gpos[t * w.G + d] = -1;
-          for (int k = 0; k < w.K; ++k) {
-            int e = __shfl_sync(0xffffffffu, my_e, k);
-            int ep = __shfl_sync(0xffffffffu, my_ep, k);
-            if (e < 0 || ep < 0 || e / w.E_loc != d) continue;
-            dst_base[ndst] = w.xmaj[d];
-            dst_row[ndst] = ep;
-            ++ndst;
-          }
           continue;
         }
         int64_t g = (int64_t)offs->off[s_loc][d] + coff[d] + rank_d[t * w.G + d];
@@ -443,15 +532,6 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
       if (lane == 0)
         for (int d = 0; d < w.G; ++d)
           if (!((hit >> d) & 1ull)) gpos[t * w.G + d] = -1;
-    } else {
-      for (int k = 0; k < w.K; ++k) {
-        int e = __shfl_sync(0xffffffffu, my_e, k);
-        int ep = __shfl_sync(0xffffffffu, my_ep, k);
-        if (e < 0 || ep < 0) continue;
-        dst_base[ndst] = w.xmaj[e / w.E_loc];
-        dst_row[ndst] = ep;
-        ++ndst;
-      }
     }
     for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
       int4 buf[kUnroll];
@@ -637,34 +717,29 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
     int n = 0;
     const uint8_t* srcs[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
     float ws[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    if (mode) {
-      unsigned long long hit = hitmask[t];
-      for (int d = 0; d < w.G; ++d) {
-        if (!((hit >> d) & 1ull)) continue;
-        if (mode == 2 && d / w.L == w.p) {  // same GPU: weighted expert rows directly
-          for (int k = 0; k < w.K; ++k) {
-            int e = ids[t * w.K + k];
-            int ep = epos[t * w.K + k];
-            if (e < 0 || ep < 0 || e / w.E_loc != d) continue;
-            srcs[n] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
-            ws[n] = wts[t * w.K + k];
-            ++n;
-          }
-          continue;
-        }
-        int g = gpos[t * w.G + d];
-        if (g < 0 || g >= w.R_cap) continue;
-        srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
-        ws[n] = 1.f;
-        ++n;
-      }
-    } else {
+    // weighted expert rows: every pick (mode 0) or picks on this GPU (mode 2), k order
+    if (mode != 1) {
       for (int k = 0; k < w.K; ++k) {
         int e = ids[t * w.K + k];
         int ep = epos[t * w.K + k];
         if (e < 0 || ep < 0) continue;
-        srcs[n] = w.ymaj[e / w.E_loc] + (int64_t)ep * w.row_bytes;
+        const int d = e / w.E_loc;
+        if (mode == 2 && d / w.L != w.p) continue;
+        srcs[n] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
         ws[n] = wts[t * w.K + k];
+        ++n;
+      }
+    }
+    // pre-reduced partial rows of dedup destinations, ascending rank
+    if (mode != 0) {
+      unsigned long long hit = hitmask[t];
+      for (int d = 0; d < w.G; ++d) {
+        if (!((hit >> d) & 1ull)) continue;
+        if (mode == 2 && d / w.L == w.p) continue;
+        int g = gpos[t * w.G + d];
+        if (g < 0 || g >= w.R_cap) continue;
+        srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
+        ws[n] = 1.f;
         ++n;
       }
     }
@@ -730,6 +805,7 @@ struct hm_world {
   int* status = nullptr;
   unsigned long long epoch = 0;
   bool peers_ready = false;
+  int last_mode = 0;
   // optional per-kernel CUDA-event timing (segments recorded on the launch stream)
   bool timing = false;
   cudaEvent_t ev[2 * 16];
@@ -899,8 +975,23 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
   HM_CHECK_ARG(E >= 1 && E <= 512, "hm_route_topk: E must be 1..512");
   HM_CHECK_ARG(K >= 1 && K <= kMaxK && K <= E, "hm_route_topk: K must be 1..%d and <= E", kMaxK);
   if (T == 0) return 0;
-  int blocks = grid_for(T, 8, kSMs * 16);
   cudaStream_t s = (cudaStream_t)stream;
+  if (K <= 8) {
+    int blocks = grid_for(T, 256, kSMs * 8);
+#define HM_ROUTE_K(KK)                                                                      \
+  case KK:                                                                                  \
+    k_route_lane<KK><<<blocks, 256, 0, s>>>(logits, T, E, expert_to_slot, renormalize,      \
+                                            slot_ids, weights, expert_ids);                 \
+    break;
+    switch (K) {
+      HM_ROUTE_K(1) HM_ROUTE_K(2) HM_ROUTE_K(3) HM_ROUTE_K(4)
+      HM_ROUTE_K(5) HM_ROUTE_K(6) HM_ROUTE_K(7) HM_ROUTE_K(8)
+    }
+#undef HM_ROUTE_K
+    HM_LAUNCHED();
+    return 0;
+  }
+  int blocks = grid_for(T, 8, kSMs * 16);
   int per = (E + 31) / 32;
   if (per <= 1)
     k_route<1><<<blocks, 256, 0, s>>>(logits, T, E, K, expert_to_slot, renormalize, slot_ids, weights, expert_ids);
@@ -923,6 +1014,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
   HM_CHECK_ARG(mode >= 0 && mode <= 2, "hm_dispatch: mode must be 0 (raw), 1 (dedup), 2 (dedup across GPUs)");
   if (mode) HM_CHECK_ARG(wts, "hm_dispatch: dedup modes need gate weights");
+  w->last_mode = mode;
   if (!w->peers_ready) {
     hm::set_error("hm_dispatch: peers not opened");
     return hm::kNotReady;
@@ -961,6 +1053,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
 
 HM_API int hm_expand(hm_world* w, void* stream) {
   HM_CHECK_ARG(w, "hm_expand: null world");
+  if (w->h.P == 1 && w->last_mode == 2) return 0;  // every rank shares this GPU: nothing received
   int blocks = kSMs * 8;
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
   k_expand<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
@@ -977,7 +1070,7 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   const int dedup = mode;
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
-  if (dedup) {
+  if (dedup && !(h.P == 1 && mode == 2)) {
     SegScope sc(w, kSegReduce, s);
     if (h.elem == 2)
       k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
