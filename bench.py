@@ -136,7 +136,17 @@ def cpu_reference(cfg_name: str, steps: int, warmup: int, tokens_per_rank: int |
             "ms_per_step": sec * 1e3}
 
 
+def _json_out():
+    """Keep stdout for the one JSON line: library banners (NCCL's version line,
+    torchrun notices) are redirected to stderr for the whole run."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
+
+
 def main():
+    out_stream = _json_out()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -165,7 +175,7 @@ def main():
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        print(json.dumps(line), file=out_stream, flush=True)
         return
 
     import torch
@@ -388,7 +398,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
         }
-        print(json.dumps(line))
+        print(json.dumps(line), file=out_stream, flush=True)
     ep.close()
     raw_ep.close()
     all_ep.close()

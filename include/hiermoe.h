@@ -142,6 +142,17 @@ int hm_expand(hm_world* w, void* stream);
 int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
                void* stream);
 
+/* ---------------- expert FFN (tcgen05 + TMA + TMEM, sm_100a) -------------
+ * The only dense contraction of the layer (E expert FFNs); no
+ * reference implementation.  Groups are consecutive row blocks of A with
+ * device-side sizes n_rows[g] (the dispatch's expert-major layout). */
+int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t groups,
+                    const int32_t* n_rows, int32_t N, int32_t K, int32_t swiglu, void* out,
+                    int64_t ld_out, void* stream);
+int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                  const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
+                  void* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

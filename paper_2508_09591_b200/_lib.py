@@ -63,11 +63,10 @@ _SIGS = {
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
-}
-
-# entry points added by later kernels are bound lazily if present
-_OPTIONAL = {
-    "hm_grouped_gemm": None,
+    "hm_grouped_gemm": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32,
+                                  c_int32, c_int32, c_void_p, c_int64, c_void_p]),
+    "hm_expert_ffn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
 }
 
 

@@ -1,0 +1,439 @@
+// Grouped expert FFN GEMMs on sm_100a tensor cores (tcgen05 + TMA + TMEM).
+//
+// Expert-major rows (the dispatch output, one contiguous block of n_g rows
+// per local expert g) are multiplied by per-expert weights:
+//   GEMM1: H[r, :] = silu(X W1_g^T) * (X W3_g^T)   (SwiGLU fused in the epilogue)
+//   GEMM2: Y[r, :] = H W2_g^T
+// with X [rows, K] bf16 K-major, W [groups * N, K] bf16 K-major, fp32
+// accumulation in TMEM, bf16 output.  For GEMM1 the weight rows are packed in
+// blocks of 128: rows [256 b, 256 b + 128) = W1 rows [128 b, 128 b + 128) and
+// rows [256 b + 128, 256 b + 256) = W3 rows of the same block, so one
+// 128 x 256 accumulator tile holds a gate tile and its matching up tile.
+//
+// Kernel shape (one CTA per SM, persistent over (group, m-tile, n-tile)):
+//   warp 0      TMA producer (one elected lane): A 128x64 + B 256x64 bf16 per
+//               stage, 128-byte swizzle, 4-stage smem ring (mbarrier full/empty)
+//   warp 1      MMA issuer (one lane): 4 x tcgen05.mma.kind::f16 M128 N256 K16
+//               per stage into one of two TMEM accumulators (256 columns each),
+//               tcgen05.commit -> empty[stage] / tmem_full[acc]
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> fp32 regs -> (SwiGLU) -> bf16
+//               stores, rows >= n_g masked; arrive tmem_empty[acc]
+// Group sizes are read on the device (no host sync).
+
+#include "hm_common.cuh"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <string.h>
+
+namespace {
+
+using namespace hm;
+
+constexpr int BM = 128, BN = 256, BK = 64, UK = 16;
+constexpr int kStages = 4;
+constexpr int kThreads = 256;
+constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB
+constexpr uint32_t kBBytes = BN * BK * 2;   // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr int kMaxGroups = 64;
+constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
+
+struct GemmArgs {
+  const int32_t* n_rows;  // [groups] rows per group (device)
+  int groups;
+  int N;                  // output features per group (weight rows per group)
+  int K;                  // reduction length
+  int swiglu;             // 1: out = silu(gate) * up, out_cols = N / 2
+  __nv_bfloat16* out;     // [rows, out_cols]
+  int64_t ld_out;         // elements
+  int* status;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t mbar_try(uint32_t addr, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(phase)
+      : "memory");
+  return ok;
+}
+// bounded wait: a pipeline bug must not hang the GPU (trap after ~10 s)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try(addr, phase)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try(addr, phase)) {
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 10000000000ull) __trap();
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: 8-row x 128 B
+// atoms stacked at SBO = 1024 B; version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                  // version
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// 32 lanes x 32 columns fp32 from TMEM (warp w accesses lanes 32*(w%4)..)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TileMap {
+  int ntile_n;
+  int total;
+  int start[kMaxGroups + 1];    // first tile index of each group
+  int row0[kMaxGroups];         // first row of each group in A
+  int rows[kMaxGroups];
+};
+
+__device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t, int& g, int& mt,
+                                            int& nt) {
+  g = 0;
+  while (g + 1 < groups && tm.start[g + 1] <= t) ++g;
+  int local = t - tm.start[g];
+  mt = local / tm.ntile_n;
+  nt = local % tm.ntile_n;
+}
+
+template <int kSwiGLU>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ TileMap tm;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    int acc = 0, row = 0;
+    tm.ntile_n = args.N / BN;
+    for (int g = 0; g < args.groups; ++g) {
+      int n = args.n_rows[g];
+      tm.start[g] = acc;
+      tm.row0[g] = row;
+      tm.rows[g] = n;
+      acc += ((n + BM - 1) / BM) * tm.ntile_n;
+      row += n;
+    }
+    tm.start[args.groups] = acc;
+    tm.total = acc;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);   // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kblocks = args.K / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        const int arow = tm.row0[g] + mt * BM;
+        const int brow = g * args.N + nt * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_expect_tx(full + stage, kStageBytes);
+          tma_load_2d(sa + stage * kABytes, &map_a, full + stage, kb * BK, arow);
+          tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, kb * BK, brow);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * kABytes);
+          const uint32_t b0 = smem_u32(sb + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_bf16(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
+                      (kb | k) ? 1u : 0u);
+          umma_commit(empty + stage);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull + acc);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;  // TMEM lane quarter
+    int it = 0;
+    for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int r_in = mt * BM + q * 32 + lane;          // row within group
+      const bool valid = r_in < tm.rows[g];
+      __nv_bfloat16* orow = args.out + (int64_t)(tm.row0[g] + r_in) * args.ld_out;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (kSwiGLU) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          float gv[32], uv[32];
+          tmem_ld32(tbase + c, gv);
+          tmem_ld32(tbase + BN / 2 + c, uv);
+          if (valid) {
+            __align__(16) __nv_bfloat162 hv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float g0 = gv[2 * i], g1 = gv[2 * i + 1];
+              float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
+              float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
+              hv[i] = __floats2bfloat162_rn(h0, h1);
+            }
+            int4* dst = reinterpret_cast<int4*>(orow + nt * (BN / 2) + c);
+            const int4* src = reinterpret_cast<const int4*>(hv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = src[i];
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          if (valid) {
+            __align__(16) __nv_bfloat162 hv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hv[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
+            const int4* src = reinterpret_cast<const int4*>(hv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = src[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: tensor maps through the driver entry point (no -lcuda link needed)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return kInvalid;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return kInvalid;
+  }
+  return 0;
+}
+
+int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
+                int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
+                cudaStream_t s) {
+  HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
+  HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
+  HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
+  CUtensorMap ma, mb;
+  int st = make_map(&ma, a, (uint64_t)a_rows, (uint64_t)K, BM);
+  if (st) return st;
+  st = make_map(&mb, b, (uint64_t)groups * N, (uint64_t)K, BN);
+  if (st) return st;
+  GemmArgs args;
+  args.n_rows = n_rows;
+  args.groups = groups;
+  args.N = N;
+  args.K = K;
+  args.swiglu = swiglu;
+  args.out = reinterpret_cast<__nv_bfloat16*>(out);
+  args.ld_out = ld_out;
+  args.status = status;
+  const size_t smem = kStages * kStageBytes + 1024 + 256;
+  int dev = 0;
+  HM_CUDA(cudaGetDevice(&dev));
+  int sms = kSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (swiglu) {
+    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_grouped_gemm<1><<<sms, kThreads, smem, s>>>(ma, mb, args);
+  } else {
+    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_grouped_gemm<0><<<sms, kThreads, smem, s>>>(ma, mb, args);
+  }
+  HM_LAUNCHED();
+  return 0;
+}
+
+}  // namespace
+
+// Grouped GEMM: out[rows of group g] = A[rows of g] . B_g^T (bf16 in, fp32
+// accumulate, bf16 out); groups are consecutive row blocks of A with sizes
+// n_rows[g] (device).  swiglu=1 applies silu(gate)*up to 128-column gate/up
+// block pairs (out has N/2 columns).
+HM_API int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t groups,
+                           const int32_t* n_rows, int32_t N, int32_t K, int32_t swiglu, void* out,
+                           int64_t ld_out, void* stream) {
+  return launch_gemm(a, a_rows, b, groups, n_rows, N, K, swiglu, out, ld_out, nullptr,
+                     (cudaStream_t)stream);
+}
+
+// Expert SwiGLU FFN on expert-major rows: H = silu(X W1^T) * (X W3^T),
+// Y = H W2^T.  w13: [groups][2I][M] (128-row gate/up blocks interleaved),
+// w2: [groups][M][I], h: [a_rows][I], y: [a_rows][M].
+HM_API int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                         const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
+                         void* y, void* stream) {
+  int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
+                       (cudaStream_t)stream);
+  if (st) return st;
+  return launch_gemm(h, a_rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
+                     (cudaStream_t)stream);
+}

@@ -1,0 +1,47 @@
+"""Expert SwiGLU FFN on the dispatch's expert-major rows (tcgen05 grouped GEMM).
+
+H = silu(X W1^T) * (X W3^T), Y = H W2^T per local expert, bf16 in/out with
+fp32 accumulation in TMEM (csrc/gemm_sm100.cu).  Group sizes stay on the
+device (the dispatch's per-slot counts), so the FFN needs no host sync.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import ptr, stream_ptr
+
+BLOCK = 128
+
+
+def pack_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
+    """[G, I, M] gate + up weights -> [G, 2I, M] with 128-row gate/up blocks
+    interleaved (one 256-row GEMM tile = a gate block and its up block)."""
+    g, inter, m = w1.shape
+    if w3.shape != w1.shape or inter % BLOCK:
+        raise ValueError("w1/w3 must be [G, I, M] with I a multiple of 128")
+    nb = inter // BLOCK
+    return torch.stack([w1.view(g, nb, BLOCK, m), w3.view(g, nb, BLOCK, m)], dim=2) \
+        .reshape(g, 2 * inter, m).contiguous()
+
+
+def grouped_gemm(a: torch.Tensor, b: torch.Tensor, n_rows: torch.Tensor, swiglu: bool = False,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[rows of g] = a[rows of g] @ b[g]^T (b: [G, N, K]); swiglu -> N/2 cols."""
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
+        raise ValueError("bf16 operands required")
+    groups, n, k = b.shape
+    cols = n // 2 if swiglu else n
+    if out is None:
+        out = torch.empty((a.shape[0], cols), dtype=torch.bfloat16, device=a.device)
+    _lib.call("hm_grouped_gemm", ptr(a.contiguous()), a.shape[0], ptr(b.contiguous()), groups,
+              ptr(n_rows), n, k, int(swiglu), ptr(out), out.stride(0), stream_ptr())
+    return out
+
+
+def expert_ffn_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int, w13: torch.Tensor,
+                    w2: torch.Tensor, hidden: int, inter: int, h: torch.Tensor, y_ptr: int) -> None:
+    """FFN on raw device rows (e.g. an EPWorld's xmaj -> ymaj buffers)."""
+    _lib.call("hm_expert_ffn", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w2), hidden,
+              inter, ptr(h), y_ptr, stream_ptr())

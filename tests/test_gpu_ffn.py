@@ -1,0 +1,61 @@
+"""tcgen05 grouped GEMM / expert SwiGLU FFN vs a plain PyTorch fp32 reference
+(bf16 operands, fp32 accumulation; tolerance: bf16 output rounding)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_gemm(a, b, n_rows):
+    out, r = [], 0
+    for g, n in enumerate(n_rows):
+        out.append(a[r:r + n].float() @ b[g].float().T)
+        r += n
+    return torch.cat(out) if out else a.new_zeros((0, b.shape[1]), dtype=torch.float32)
+
+
+@pytest.mark.parametrize("n_rows,N,K", [
+    ([128], 256, 64),
+    ([300, 0, 77, 513], 512, 256),
+    ([1, 129, 255, 256, 257], 256, 2048),
+    ([2048] * 4, 2048, 768),
+])
+def test_grouped_gemm_matches_fp32(hm, n_rows, N, K):
+    from paper_2508_09591_b200.ffn import grouped_gemm
+    torch.manual_seed(0)
+    G = len(n_rows)
+    rows = sum(n_rows)
+    a = torch.randn(max(rows, 1), K, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(G, N, K, device="cuda") * K ** -0.5).to(torch.bfloat16)
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    out = grouped_gemm(a, b, nr)
+    torch.cuda.synchronize()
+    ref = _ref_gemm(a, b, n_rows)
+    torch.testing.assert_close(out[:rows].float(), ref, rtol=2e-2, atol=2e-2)
+
+
+def test_swiglu_ffn_matches_fp32(hm):
+    from paper_2508_09591_b200.ffn import expert_ffn_ptrs, pack_w13
+    torch.manual_seed(1)
+    G, M, I = 4, 2048, 768
+    n_rows = [700, 0, 1500, 333]
+    rows = sum(n_rows)
+    x = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    w1 = (torch.randn(G, I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w3 = (torch.randn(G, I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    w13 = pack_w13(w1, w3)
+    h = torch.empty(rows, I, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(rows, M, dtype=torch.bfloat16, device="cuda")
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    expert_ffn_ptrs(x.data_ptr(), rows, nr.data_ptr(), G, w13, w2, M, I, h, y.data_ptr())
+    torch.cuda.synchronize()
+    refs, r = [], 0
+    for g, n in enumerate(n_rows):
+        xs = x[r:r + n].float()
+        hh = torch.nn.functional.silu(xs @ w1[g].float().T) * (xs @ w3[g].float().T)
+        refs.append(hh.to(torch.bfloat16).float() @ w2[g].float().T)
+        r += n
+    ref = torch.cat(refs)
+    torch.testing.assert_close(y.float(), ref, rtol=3e-2, atol=3e-2)
