@@ -44,6 +44,7 @@ CONFIGS = {
     "configA": (8, 16, 2, 256, 512,
                 "reference CPU config: 16 experts, top-2, hidden 256, 4096 tokens, 8-rank EP world"),
 }
+INTER = {"qwen3": 768, "dsv3": 2048, "configA": 512}
 SEGMENTS = ["plan", "notify", "pack", "barrier1", "expand", "reduce", "barrier2", "gather"]
 
 
@@ -156,6 +157,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=None, help="tokens per EP rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-layer", action="store_true", help="skip the full layer forward")
     args = ap.parse_args()
     world, rank, local = dist_env()
     G, E, K, M, T_r, desc = CONFIGS[args.config]
@@ -350,6 +352,53 @@ def main():
                "h2d_bytes_per_step": int(hx.numel() * 2 + hl.numel() * 4),
                "d2h_bytes_per_step": int(ho.numel() * 2)}
 
+    # full layer forward: gating + dispatch + tcgen05 SwiGLU experts + combine
+    layer_fwd = None
+    if not args.no_layer:
+        from paper_2508_09591_b200.moe import HierMoELayer
+        inter = INTER[args.config]
+        all_ep.close()
+        raw_ep.close()
+        layer = HierMoELayer(G, E, K, M, inter, T_r, gpus=world, gpu_index=rank, dedup=MODE)
+        lout = torch.empty(T, M, dtype=dtype, device="cuda")
+        for _ in range(3):
+            layer(x, out=lout)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        n_l = max(5, args.steps // 10)
+        tot = ffn = 0.0
+        for _ in range(n_l):
+            flush.zero_()
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            e0.record()
+            slot_l, w_l, _ = layer.route(x)
+            layer.world.dispatch(x, slot_l, w_l, dedup=MODE)
+            e1.record()
+            layer.experts_forward()
+            e2.record()
+            layer.world.combine(slot_l, w_l, dedup=MODE, out=lout)
+            e3.record()
+            e3.synchronize()
+            tot += e0.elapsed_time(e3)
+            ffn += e1.elapsed_time(e2)
+        t = torch.tensor([tot / n_l, ffn / n_l], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        fl = layer.flops_per_forward()
+        fl_t = torch.tensor([float(fl)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(fl_t, op=dist.ReduceOp.MAX)
+        ffn_tflops = fl_t.item() / (t[1].item() * 1e-3) / 1e12
+        peak_tf = peaks.get("bf16_tflops", 1590.0)
+        layer_fwd = {"ms_per_step": t[0].item(), "tokens_per_s": tokens_total / (t[0].item() * 1e-3),
+                     "ffn_ms": t[1].item(), "ffn_flops_per_gpu": int(fl_t.item()),
+                     "ffn_roofline": {"bound": "tensor", "achieved": ffn_tflops, "peak": peak_tf,
+                                      "unit": "TFLOP/s", "frac": ffn_tflops / peak_tf,
+                                      "kernel": "k_grouped_gemm (tcgen05, 2 GEMMs)"},
+                     "inter": inter, "note": "router logits GEMM in torch (cuBLAS), rest ours"}
+        layer.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(args.config, 3, 1, 512)
@@ -395,13 +444,14 @@ def main():
             "cpu_baseline": None if cpu is None else
             {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": e2e,
+            "layer_fwd": layer_fwd,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), file=out_stream, flush=True)
     ep.close()
     raw_ep.close()
-    all_ep.close()
+    all_ep.close()  # (closing twice is a no-op)
     if world > 1:
         dist.destroy_process_group()
 

@@ -1,0 +1,85 @@
+"""HierMoELayer: the MoE layer the reference models, executed on B200s.
+
+Forward: router logits -> softmax top-K (``hm_route_topk``,
+slot ids through the current Placement) -> dedup dispatch over the EP world
+(``hm_dispatch``/``hm_expand``) -> per-local-expert SwiGLU FFN on the
+expert-major rows (tcgen05 grouped GEMM, ``hm_expert_ffn``) -> gate-weighted
+dedup combine (``hm_combine``).  One process per GPU; the layer owns the
+weights of the slots its local EP ranks host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .ffn import expert_ffn_ptrs, pack_w13
+from .layer import EPWorld, route_topk
+from .routing import Placement
+
+
+class HierMoELayer:
+    def __init__(self, ranks: int, experts: int, top_k: int, hidden: int, inter: int,
+                 tokens_per_rank: int, gpus: int = 1, gpu_index: int = 0, group=None,
+                 dedup=True, seed: int = 0, renormalize: bool = True):
+        if inter % 128 or hidden % 256:
+            raise ValueError("hidden must be a multiple of 256 and inter of 128")
+        self.ranks, self.experts, self.top_k = ranks, experts, top_k
+        self.hidden, self.inter = hidden, inter
+        self.tokens_per_rank = tokens_per_rank
+        self.gpus, self.gpu_index = gpus, gpu_index
+        self.local = ranks // gpus
+        self.e_loc = experts // ranks
+        self.dedup = dedup
+        self.renormalize = renormalize
+        self.world = EPWorld(ranks, experts, top_k, hidden, tokens_per_rank,
+                             dtype=torch.bfloat16, gpus=gpus, gpu_index=gpu_index, group=group)
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        # router replicated on every GPU; experts: only the slots of local ranks
+        self.w_router = torch.randn(experts, hidden, device="cuda", generator=g) * hidden ** -0.5
+        n_loc = self.local * self.e_loc
+        w1 = torch.randn(n_loc, inter, hidden, device="cuda", generator=g) * hidden ** -0.5
+        w3 = torch.randn(n_loc, inter, hidden, device="cuda", generator=g) * hidden ** -0.5
+        self.w13 = pack_w13(w1.to(torch.bfloat16), w3.to(torch.bfloat16)) \
+            .view(self.local, self.e_loc, 2 * inter, hidden)
+        self.w2 = (torch.randn(n_loc, hidden, inter, device="cuda", generator=g) * inter ** -0.5) \
+            .to(torch.bfloat16).view(self.local, self.e_loc, hidden, inter)
+        self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
+        self.set_placement(Placement.identity(experts))
+
+    def set_placement(self, placement: Placement) -> None:
+        self.placement = placement
+        self.expert_to_slot = torch.as_tensor(placement.expert_to_slot, dtype=torch.int32,
+                                              device="cuda")
+
+    def route(self, x: torch.Tensor):
+        logits = x.float() @ self.w_router.T
+        return route_topk(logits, self.top_k, self.expert_to_slot, self.renormalize)
+
+    def experts_forward(self) -> None:
+        """SwiGLU FFN of every local rank's experts on its expert-major rows."""
+        p_ne, _ = self.world.buffer("n_e", 0)
+        for l in range(self.local):
+            rank = self.gpu_index * self.local + l
+            x_ptr, _ = self.world.buffer("xmaj", l)
+            y_ptr, _ = self.world.buffer("ymaj", l)
+            expert_ffn_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
+                            self.w13[l], self.w2[l], self.hidden, self.inter, self.h, y_ptr)
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        slot, w, _ = self.route(x)
+        self.world.dispatch(x, slot, w, dedup=self.dedup)
+        self.experts_forward()   # expert-major rows are local after the dispatch barrier
+        # hm_combine barriers before the source reads peers' rows (any mode)
+        return self.world.combine(slot, w, dedup=self.dedup, out=out)
+
+    __call__ = forward
+
+    def flops_per_forward(self) -> int:
+        """Expert FFN flops of this GPU's last forward (6 * rows * hidden * inter)."""
+        rows = int(self.world.rows_received()[:, 1].sum())
+        return 6 * rows * self.hidden * self.inter
+
+    def close(self) -> None:
+        self.world.close()
