@@ -109,9 +109,15 @@ int hm_smooth_max_rows(const double* x, int64_t rows, int32_t n, double gamma, d
  * The reference only models this exchange (traffic.py:93-170: AlltoAll with
  * and without dedup); these calls execute it. */
 typedef struct hm_world hm_world;
+/* relay_groups = U[1] > 0 makes a phase-1 (inter-level-1) world of a two-level
+ * dispatch: one row per (token, level-1 group) to the rank with the source's
+ * local index in that group, carrying the restricted slot ids:
+ * the copy list of propagate_level (routing.py:189-215). */
 int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
                     int32_t top_k, int32_t hidden, int32_t elem_bytes, int64_t tokens_per_rank,
-                    int64_t n_cap_rows, hm_world** out);
+                    int64_t n_cap_rows, int32_t relay_groups, hm_world** out);
+/* phase-2 ids/gates from a relay world's received copies (HD2 relay, K5) */
+int hm_relay_ids(hm_world* w, int32_t* ids2, float* w2, void* stream);
 int hm_world_destroy(hm_world* w);
 int64_t hm_world_ipc_handle_size(void);
 int hm_world_ipc_handle(hm_world* w, void* out_handle);

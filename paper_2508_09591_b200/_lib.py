@@ -47,7 +47,8 @@ _SIGS = {
     "hm_np_pow": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "hm_smooth_max_rows": (c_int32, [c_void_p, c_int64, c_int32, c_double, c_void_p, c_void_p]),
     "hm_world_create": (c_int32, [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
-                                  c_int64, c_int64, POINTER(c_void_p)]),
+                                  c_int64, c_int64, c_int32, POINTER(c_void_p)]),
+    "hm_relay_ids": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_world_destroy": (c_int32, [c_void_p]),
     "hm_world_ipc_handle_size": (c_int64, []),
     "hm_world_ipc_handle": (c_int32, [c_void_p, c_void_p]),

@@ -46,13 +46,18 @@ constexpr int kChunk = 256;      // tokens per plan chunk (8 warps x 32)
 constexpr int kPlanWarps = kChunk / 32;
 
 struct RowMeta {
-  int32_t epos;  // expert-major row at this destination, -1 if not local
+  int32_t epos;  // expert-major row at this destination (relay: slot id), -1 if not here
   float w;
 };
+
 
 // device-resident view of the world (pointers valid on this GPU)
 struct WorldDev {
   int G, L, P, p, E, K, M, E_loc, elem;
+  // relay (phase-1 of a two-level dispatch): U1 > 0 groups of F = G/U1 ranks;
+  // pick e of source s goes to rank (e / (E/U1)) * F + s % F (the rank with
+  // the source's local index inside the pick's group), carrying slot ids
+  int U1, F;
   int64_t T_r, R_cap, N_cap, row_bytes;
   uint8_t* recv_x[kMaxRanks];
   RowMeta* recv_meta[kMaxRanks];
@@ -62,6 +67,10 @@ struct WorldDev {
   int32_t* counts[kMaxRanks];                 // count matrix [G][G+E] on d's GPU
   unsigned long long* flags[kMaxRanks];       // per GPU q: flags[q][0..P)
 };
+
+__device__ __forceinline__ int dest_of(const WorldDev& w, int s, int e) {
+  return w.U1 ? (e / (w.E / w.U1)) * w.F + s % w.F : e / w.E_loc;
+}
 
 // per-step offsets computed by k_notify (local, not symmetric)
 struct Offsets {
@@ -297,12 +306,12 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
     S[k] = -1;
     if (k < w.K && valid) {
       int e = ids[t * w.K + k];
-      if (e < 0 || e >= w.E) {
+      if (e < -1 || e >= w.E) {   // -1 = padding (no pick)
         atomicExch(status, 4);
         e = -1;
       }
       S[k] = e;
-      if (e >= 0) hit |= 1ull << (e / w.E_loc);
+      if (e >= 0) hit |= 1ull << dest_of(w, w.p * w.L + s_loc, e);
     }
   }
   // destination ranks within the warp
@@ -518,10 +527,13 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
           if (lane == 0) atomicExch(status, 2);
           continue;
         }
-        // meta: lane k writes pick k's local expert-major row (or -1) + weight
+        // meta: lane k writes pick k's local expert-major row (relay: its slot
+        // id, restricted to the destination's group) or -1, plus the gate
         if (lane < w.K) {
           RowMeta m;
-          m.epos = (my_e >= 0 && my_e / w.E_loc == d) ? my_ep : -1;
+          const int sg = w.p * w.L + s_loc;
+          const bool here = my_e >= 0 && dest_of(w, sg, my_e) == d;
+          m.epos = here ? (w.U1 ? my_e : my_ep) : -1;
           m.w = my_w;
           w.recv_meta[d][g * w.K + lane] = m;
         }
@@ -776,6 +788,31 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
   }
 }
 
+// relay -> phase-2 inputs: per local relay rank, received row i carries the
+// token's picks inside this rank's group (slot ids, -1 elsewhere) + gates;
+// rows past the received count are padding (-1).
+__global__ void k_relay_ids(const WorldDev* __restrict__ wp, const Offsets* __restrict__ offs,
+                            int32_t* __restrict__ ids2, float* __restrict__ w2) {
+  const WorldDev& w = *wp;
+  const int64_t n = (int64_t)w.L * w.R_cap * w.K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / w.K;
+    const int k = (int)(i % w.K);
+    const int l = (int)(row / w.R_cap);
+    const int64_t r = row % w.R_cap;
+    int32_t id = -1;
+    float wt = 0.f;
+    if (r < offs->R[l]) {
+      RowMeta m = w.recv_meta[w.p * w.L + l][r * w.K + k];
+      id = m.epos;
+      wt = m.w;
+    }
+    ids2[i] = id;
+    w2[i] = wt;
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -851,7 +888,8 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
 
 HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
                            int32_t top_k, int32_t hidden, int32_t elem_bytes,
-                           int64_t tokens_per_rank, int64_t n_cap_rows, hm_world** out) {
+                           int64_t tokens_per_rank, int64_t n_cap_rows, int32_t relay_groups,
+                           hm_world** out) {
   HM_CHECK_ARG(out, "hm_world_create: null out");
   *out = nullptr;
   HM_CHECK_ARG(ranks >= 1 && ranks <= kMaxRanks, "ranks must be 1..%d", kMaxRanks);
@@ -879,9 +917,13 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   h.elem = elem_bytes;
   h.T_r = tokens_per_rank;
   h.row_bytes = (int64_t)hidden * elem_bytes;
-  h.R_cap = (int64_t)ranks * tokens_per_rank;
+  h.U1 = relay_groups;
+  h.F = relay_groups ? ranks / relay_groups : 0;
+  // a relay receives from the U1 ranks sharing its local index; it never
+  // builds expert-major rows
+  h.R_cap = (int64_t)(relay_groups ? relay_groups : ranks) * tokens_per_rank;
   int64_t worst = (int64_t)ranks * tokens_per_rank * (top_k < h.E_loc ? top_k : h.E_loc);
-  h.N_cap = n_cap_rows > 0 && n_cap_rows < worst ? n_cap_rows : worst;
+  h.N_cap = relay_groups ? 1 : (n_cap_rows > 0 && n_cap_rows < worst ? n_cap_rows : worst);
   HM_CHECK_ARG(h.R_cap < (1ll << 31) && h.N_cap < (1ll << 31), "row capacity exceeds int32");
   cudaGetDevice(&w->device);
 
@@ -1014,6 +1056,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
   HM_CHECK_ARG(mode >= 0 && mode <= 2, "hm_dispatch: mode must be 0 (raw), 1 (dedup), 2 (dedup across GPUs)");
   if (mode) HM_CHECK_ARG(wts, "hm_dispatch: dedup modes need gate weights");
+  HM_CHECK_ARG(!w->h.U1 || mode == 1, "hm_dispatch: a relay world ships dedup rows (mode 1)");
   w->last_mode = mode;
   if (!w->peers_ready) {
     hm::set_error("hm_dispatch: peers not opened");
@@ -1054,6 +1097,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
 HM_API int hm_expand(hm_world* w, void* stream) {
   HM_CHECK_ARG(w, "hm_expand: null world");
   if (w->h.P == 1 && w->last_mode == 2) return 0;  // every rank shares this GPU: nothing received
+  if (w->h.U1) return 0;                             // relay rows are re-dispatched, not expanded
   int blocks = kSMs * 8;
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
   k_expand<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
@@ -1070,7 +1114,7 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   const int dedup = mode;
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
-  if (dedup && !(h.P == 1 && mode == 2)) {
+  if (dedup && !(h.P == 1 && mode == 2) && !h.U1) {   // relay: rows arrive pre-reduced
     SegScope sc(w, kSegReduce, s);
     if (h.elem == 2)
       k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
@@ -1177,5 +1221,17 @@ HM_API int hm_world_timings(hm_world* w, float* ms, int32_t n) {
       if (cudaEventElapsedTime(&v, w->ev[2 * i], w->ev[2 * i + 1]) == cudaSuccess) ms[i] = v;
     }
   }
+  return 0;
+}
+
+// phase-2 inputs of a two-level dispatch from a relay world's received rows:
+// ids2/w2 are [L * R_cap, K] (R_cap = U1 * T_r), the same row layout as the
+// relay's receive buffer (which is the phase-2 payload).
+HM_API int hm_relay_ids(hm_world* w, int32_t* ids2, float* w2, void* stream) {
+  HM_CHECK_ARG(w && ids2 && w2, "hm_relay_ids: null argument");
+  HM_CHECK_ARG(w->h.U1 > 0, "hm_relay_ids: not a relay world");
+  int64_t n = (int64_t)w->h.L * w->h.R_cap * w->h.K;
+  k_relay_ids<<<grid_for(n, 256, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(w->d, w->offs, ids2, w2);
+  HM_LAUNCHED();
   return 0;
 }

@@ -111,7 +111,8 @@ class EPWorld:
 
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int,
                  tokens_per_rank: int, dtype: torch.dtype = torch.bfloat16,
-                 gpus: int = 1, gpu_index: int = 0, group=None, n_cap_rows: int = 0):
+                 gpus: int = 1, gpu_index: int = 0, group=None, n_cap_rows: int = 0,
+                 relay_groups: int = 0):
         lib = _lib.load()
         if dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("payload dtype must be bfloat16 or float32")
@@ -122,8 +123,9 @@ class EPWorld:
         self.elem = 2 if dtype == torch.bfloat16 else 4
         h = ctypes.c_void_p()
         _lib.check(lib.hm_world_create(ranks, gpus, gpu_index, experts, top_k, hidden, self.elem,
-                                       tokens_per_rank, n_cap_rows, ctypes.byref(h)),
+                                       tokens_per_rank, n_cap_rows, relay_groups, ctypes.byref(h)),
                    "hm_world_create")
+        self.relay_groups = relay_groups
         self._h = h
         info = (ctypes.c_int64 * 8)()
         _lib.check(lib.hm_world_info(h, info), "hm_world_info")
@@ -165,6 +167,21 @@ class EPWorld:
         _lib.call("hm_dispatch", self._h, ptr(x), ptr(slot_ids), ptr(weights), mode, s)
         if mode:
             _lib.call("hm_expand", self._h, s)
+
+    def dispatch_ptr(self, x_ptr: int, slot_ids: torch.Tensor, weights: torch.Tensor,
+                     dedup=True) -> None:
+        """dispatch() with the payload given as a device pointer to
+        [L*T_r, M] rows (e.g. a relay world's receive buffer)."""
+        mode = transport_mode(dedup)
+        s = stream_ptr()
+        _lib.call("hm_dispatch", self._h, x_ptr, ptr(slot_ids), ptr(weights), mode, s)
+        if mode:
+            _lib.call("hm_expand", self._h, s)
+
+    def combine_into(self, out_ptr: int, slot_ids: torch.Tensor, weights: torch.Tensor,
+                     dedup=True) -> None:
+        _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), transport_mode(dedup),
+                  out_ptr, stream_ptr())
 
     def combine(self, slot_ids: torch.Tensor, weights: torch.Tensor, dedup=True,
                 out: torch.Tensor | None = None) -> torch.Tensor:
@@ -234,3 +251,49 @@ class EPWorld:
 
     def set_expert_outputs(self, local_rank: int, y: torch.Tensor) -> None:
         self.write("ymaj", y.to(self.dtype), local_rank)
+
+
+class TwoLevelWorld:
+    """HD2 dispatch/combine over a two-level hierarchy [U1, F] (the
+    reference's d = 2 variant, traffic.py:144-152 / PAPER.md:238).
+
+    Phase 1 (inter-level-1): one row per (token, level-1 group), sent to the
+    rank with the source's local index in that group, carrying the token's
+    picks restricted to the group -- exactly propagate_level's copies
+    (routing.py:189-215).  Phase 2 (intra-level-1): each relay re-dedups its
+    received copies to the ranks of its group.  Combine runs the mirror:
+    phase-2 combine into the relay's per-copy rows, phase-1 gather at the
+    source.  On one NVSwitch box the hierarchy is virtual (2x4, 4x2 groups).
+    """
+
+    def __init__(self, fanouts, experts: int, top_k: int, hidden: int, tokens_per_rank: int,
+                 dtype=torch.bfloat16, gpus: int = 1, gpu_index: int = 0, group=None,
+                 n_cap_rows: int = 0):
+        u1, f = int(fanouts[0]), int(np.prod(fanouts[1:]))
+        if len(fanouts) != 2:
+            raise ValueError("TwoLevelWorld takes fan-outs [U1, F]")
+        ranks = u1 * f
+        self.u1, self.f, self.ranks = u1, f, ranks
+        self.top_k, self.hidden = top_k, hidden
+        self.phase1 = EPWorld(ranks, experts, top_k, hidden, tokens_per_rank, dtype, gpus,
+                              gpu_index, group, relay_groups=u1)
+        self.phase2 = EPWorld(ranks, experts, top_k, hidden, u1 * tokens_per_rank, dtype, gpus,
+                              gpu_index, group, n_cap_rows=n_cap_rows)
+        n2 = self.phase2.local * u1 * tokens_per_rank
+        self.ids2 = torch.empty((n2, top_k), dtype=torch.int32, device="cuda")
+        self.w2 = torch.empty((n2, top_k), dtype=torch.float32, device="cuda")
+
+    def dispatch(self, x, slot_ids, weights, dedup2=True) -> None:
+        self.phase1.dispatch(x, slot_ids, weights, dedup="all")
+        _lib.call("hm_relay_ids", self.phase1._h, ptr(self.ids2), ptr(self.w2), stream_ptr())
+        rx, _ = self.phase1.buffer("recv_x", 0)
+        self.phase2.dispatch_ptr(rx, self.ids2, self.w2, dedup=dedup2)
+
+    def combine(self, slot_ids, weights, dedup2=True, out=None):
+        comb, _ = self.phase1.buffer("comb", 0)
+        self.phase2.combine_into(comb, self.ids2, self.w2, dedup=dedup2)
+        return self.phase1.combine(slot_ids, weights, dedup="all", out=out)
+
+    def close(self) -> None:
+        self.phase1.close()
+        self.phase2.close()
