@@ -159,6 +159,20 @@ int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t 
                   const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                   void* y, void* stream);
 
+/* ---------------- expert migration (K11) ------------------------------------
+ * Apply a planned swap (apply_swap, swap.py:255-259) to the physical expert
+ * state: per-GPU symmetric store of n_arrays slot-major tensors (weights,
+ * master copy, optimizer moments), peer-to-peer over CUDA IPC / NVLink. */
+typedef struct hm_store hm_store;
+int hm_store_create(int32_t gpus, int32_t gpu_index, int32_t slots_per_gpu,
+                    const int64_t* slice_bytes, int32_t n_arrays, hm_store** out);
+int hm_store_destroy(hm_store* s);
+int hm_store_ipc_handle(hm_store* s, void* out_handle);
+int hm_store_open_peers(hm_store* s, const void* handles);
+int hm_store_array(hm_store* s, int32_t a, void** ptr);
+int hm_store_status(hm_store* s, int32_t* out4);
+int hm_migrate(hm_store* s, int32_t slot_r, int32_t slot_c, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

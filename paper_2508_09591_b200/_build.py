@@ -17,7 +17,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hi
           "-I", str(ROOT / "include")]
 # per-file extra flags: the planner must not contract fp64 a*b+c (numpy parity)
 EXTRA = {"planner.cu": ["-fmad=false"]}
-SOURCES = ["planner.cu", "layer.cu", "gemm_sm100.cu"]
+SOURCES = ["planner.cu", "layer.cu", "gemm_sm100.cu", "migrate.cu"]
 
 
 def nvcc() -> str:

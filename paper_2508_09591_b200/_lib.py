@@ -66,6 +66,13 @@ _SIGS = {
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "hm_grouped_gemm": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32,
                                   c_int32, c_int32, c_void_p, c_int64, c_void_p]),
+    "hm_store_create": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int32, POINTER(c_void_p)]),
+    "hm_store_destroy": (c_int32, [c_void_p]),
+    "hm_store_ipc_handle": (c_int32, [c_void_p, c_void_p]),
+    "hm_store_open_peers": (c_int32, [c_void_p, c_void_p]),
+    "hm_store_array": (c_int32, [c_void_p, c_int32, POINTER(c_void_p)]),
+    "hm_store_status": (c_int32, [c_void_p, c_void_p]),
+    "hm_migrate": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "hm_expert_ffn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
 }

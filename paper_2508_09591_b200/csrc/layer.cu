@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
     int n = 0;
     for (int e = dg * w.E_loc; e < (dg + 1) * w.E_loc; ++e) n += s_n[e];
     offs->Nd[d_loc] = n;
-    if (r > w.R_cap || n > w.N_cap) atomicExch(status, 2);  // capacity overflow
+    if (r > w.R_cap || (!w.U1 && n > w.N_cap)) atomicExch(status, 2);  // capacity overflow
   }
 }
 
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
     if (lane < w.K) {
       my_e = ids[t * w.K + lane];
       my_w = wts ? wts[t * w.K + lane] : 0.f;
-      if (my_e >= 0) {
+      if (my_e >= 0 && !w.U1) {   // relay worlds build no expert-major rows
         my_ep = eoff[s_loc * w.E + my_e] + coff[w.G + my_e] + rank_e[t * w.K + lane];
         if (my_ep >= w.N_cap) {
           atomicExch(status, 2);

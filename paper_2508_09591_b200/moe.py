@@ -16,6 +16,7 @@ import torch
 from . import _lib
 from .ffn import expert_ffn_ptrs, pack_w13
 from .layer import EPWorld, route_topk
+from .migrate import ExpertStore
 from .routing import Placement
 
 
@@ -35,16 +36,34 @@ class HierMoELayer:
         self.renormalize = renormalize
         self.world = EPWorld(ranks, experts, top_k, hidden, tokens_per_rank,
                              dtype=torch.bfloat16, gpus=gpus, gpu_index=gpu_index, group=group)
+        # router replicated on every GPU (seeded identically); experts: the
+        # slots of local ranks, seeded by global slot so any GPU count builds
+        # the same model
         g = torch.Generator(device="cuda").manual_seed(seed)
-        # router replicated on every GPU; experts: only the slots of local ranks
         self.w_router = torch.randn(experts, hidden, device="cuda", generator=g) * hidden ** -0.5
         n_loc = self.local * self.e_loc
-        w1 = torch.randn(n_loc, inter, hidden, device="cuda", generator=g) * hidden ** -0.5
-        w3 = torch.randn(n_loc, inter, hidden, device="cuda", generator=g) * hidden ** -0.5
-        self.w13 = pack_w13(w1.to(torch.bfloat16), w3.to(torch.bfloat16)) \
-            .view(self.local, self.e_loc, 2 * inter, hidden)
-        self.w2 = (torch.randn(n_loc, hidden, inter, device="cuda", generator=g) * inter ** -0.5) \
-            .to(torch.bfloat16).view(self.local, self.e_loc, hidden, inter)
+        n_par = 3 * hidden * inter
+        # expert state in a symmetric store: bf16 weights (used by the FFN), fp32
+        # master weights and Adam moments (moved with the expert on a swap)
+        self.store = ExpertStore(n_loc, {
+            "w13": ((2 * inter, hidden), torch.bfloat16),
+            "w2": ((hidden, inter), torch.bfloat16),
+            "master": ((n_par,), torch.float32),
+            "adam_m": ((n_par,), torch.float32),
+            "adam_v": ((n_par,), torch.float32)}, gpus=gpus, gpu_index=gpu_index, group=group)
+        first = gpu_index * n_loc
+        for i in range(n_loc):
+            gs = torch.Generator(device="cuda").manual_seed(seed * 100003 + first + i)
+            w1 = torch.randn(1, inter, hidden, device="cuda", generator=gs) * hidden ** -0.5
+            w3 = torch.randn(1, inter, hidden, device="cuda", generator=gs) * hidden ** -0.5
+            w2 = torch.randn(hidden, inter, device="cuda", generator=gs) * inter ** -0.5
+            self.store["w13"][i].copy_(pack_w13(w1.to(torch.bfloat16), w3.to(torch.bfloat16))[0])
+            self.store["w2"][i].copy_(w2.to(torch.bfloat16))
+            self.store["master"][i].copy_(torch.cat([w1.flatten(), w3.flatten(), w2.flatten()]))
+        self.store["adam_m"].zero_()
+        self.store["adam_v"].zero_()
+        self.w13 = self.store["w13"].view(self.local, self.e_loc, 2 * inter, hidden)
+        self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
         self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
         self.set_placement(Placement.identity(experts))
 
@@ -52,6 +71,16 @@ class HierMoELayer:
         self.placement = placement
         self.expert_to_slot = torch.as_tensor(placement.expert_to_slot, dtype=torch.int32,
                                               device="cuda")
+
+    def apply_swap(self, pair) -> None:
+        """Apply a planned slot swap (swap.SwapPlan.pair): the placement and the
+        physical expert state (weights + optimizer moments) move together, the
+        bytes peer-to-peer when the slots live on different GPUs."""
+        if pair is None:
+            return
+        r, c = int(pair[0]), int(pair[1])
+        self.set_placement(self.placement.swapped(r, c))
+        self.store.migrate(r, c)
 
     def route(self, x: torch.Tensor):
         logits = x.float() @ self.w_router.T
@@ -83,3 +112,4 @@ class HierMoELayer:
 
     def close(self) -> None:
         self.world.close()
+        self.store.close()

@@ -76,6 +76,33 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
     ep.close()
 
 
+def run_migrate(rank, world):
+    """Cross-GPU and same-GPU slot swaps through the expert store."""
+    from paper_2508_09591_b200.migrate import ExpertStore
+    S = 8
+    arrays = {"w": ((128, 64), torch.bfloat16), "m": ((4096,), torch.float32)}
+    st = ExpertStore(S, arrays, gpus=world, gpu_index=rank)
+    for i, k in enumerate(arrays):
+        v = st[k]
+        glob = rank * S + torch.arange(S, device="cuda")
+        v.copy_((glob.view(-1, *([1] * (v.dim() - 1))) * 10 + i).to(v.dtype).expand_as(v))
+    torch.cuda.synchronize()
+    dist.barrier()
+    r, c = 1, world * S - 2          # GPU 0 <-> last GPU
+    st.migrate(r, c)
+    st.migrate(2, 5)                 # both on GPU 0
+    torch.cuda.synchronize()
+    st.check_status()
+    for i, k in enumerate(arrays):
+        v = st[k]
+        glob = [rank * S + j for j in range(S)]
+        for j, gslot in enumerate(glob):
+            src = {r: c, c: r, 2: 5, 5: 2}.get(gslot, gslot)
+            want = float(src * 10 + i)
+            assert float(v[j].flatten()[0]) == want and float(v[j].flatten()[-1]) == want, (k, gslot)
+    st.close()
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -87,6 +114,8 @@ def main():
         for dedup in ("all", "remote", "none"):
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
             dist.barrier()
+    run_migrate(rank, world)
+    dist.barrier()
     if rank == 0:
         print("MULTI-GPU PARITY OK", world)
     dist.destroy_process_group()
