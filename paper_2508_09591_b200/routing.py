@@ -263,6 +263,19 @@ def device_mask(mask: MaskLike, placement: "Placement | None" = None) -> DeviceM
     return DeviceMask(words, e, level, origin, parent)
 
 
+def mask_from_ids(slot_ids: torch.Tensor, experts: int) -> DeviceMask:
+    """Packed slot-space mask of K-per-row slot ids (the router's output), on
+    the GPU (hm_ids_to_bits); -1 entries are ignored."""
+    ids = slot_ids.to(device="cuda", dtype=torch.int32).contiguous()
+    t, k = ids.shape
+    words = _words(t, experts)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if t:
+        _lib.call("hm_ids_to_bits", ptr(ids), t, k, experts, None, ptr(words), ptr(bad),
+                  stream_ptr())
+    return DeviceMask(words, experts)
+
+
 def slot_view(mask: MaskLike, placement: "Placement | None") -> np.ndarray:
     """Host bool matrix re-indexed into slot space (routing.py:98-106)."""
     if placement is None:

@@ -53,9 +53,10 @@ class SwapTensors:
 
 
 class _Partials:
-    """Device swap statistics of one group cut."""
+    """Device swap statistics of one group cut (``reduce`` sums them over a
+    token-sharded mask before the tensor is built)."""
 
-    def __init__(self, dev: DeviceMask, groups: int):
+    def __init__(self, dev: DeviceMask, groups: int, reduce=None):
         e = dev.experts
         if groups < 1 or e % groups:
             raise ValueError(f"group count {groups} does not divide {e} experts")
@@ -70,6 +71,9 @@ class _Partials:
         _lib.call("hm_swap_partials", ptr(dev.words), dev.num_tokens, e, groups, ptr(self.base),
                   ptr(self.sel), ptr(self.hitsel), ptr(self.lone), ptr(self.lonesel),
                   ptr(self.flag), stream_ptr())
+        if reduce is not None:
+            for t in (self.base, self.sel, self.hitsel, self.lone, self.lonesel):
+                reduce(t)
         self.z = torch.empty((e, e, groups), **kw)
         _lib.call("hm_swap_tensor", ptr(self.base), ptr(self.sel), ptr(self.hitsel),
                   ptr(self.lone), ptr(self.lonesel), e, groups, ptr(self.z), stream_ptr())
@@ -86,10 +90,10 @@ class _Partials:
         return raises.sum() * size + (drops * other).sum()
 
 
-def _build(dev: DeviceMask, topology: Topology, upto: int):
+def _build(dev: DeviceMask, topology: Topology, upto: int, reduce=None):
     u = topology.level_group_counts
-    inter = [_Partials(dev, u[level]) for level in range(1, upto)]
-    intra = _Partials(dev, topology.num_gpus)
+    inter = [_Partials(dev, u[level], reduce) for level in range(1, upto)]
+    intra = _Partials(dev, topology.num_gpus, reduce)
     return inter, intra
 
 
@@ -214,15 +218,25 @@ class SwapPlan:
 
 
 def select_swap(mask: MaskLike, topology: Topology, params: LevelParams, gamma: float = 10.0,
-                placement: Placement | None = None) -> SwapPlan:
+                placement: Placement | None = None, group=None) -> SwapPlan:
     """Slot pair minimising the predicted dispatch time (swap.py:226-252).
 
     Device pipeline: counts -> d* (hm_time_model) -> swap tensors of every
     level -> cost at d* (read on the device) -> argmin + exact-max gate.
+
+    ``group`` (extension): ``mask`` holds only this process's tokens; the
+    counts and swap statistics, additive over tokens, are all-reduced over the
+    process group (NCCL) and every rank then computes the identical decision
+    -- the same result as the reference on the concatenated global mask.
     """
-    model = _Model(mask, topology, params, placement, True)
+    reduce = None
+    if group is not None:
+        import torch.distributed as dist
+        if dist.get_world_size(group) > 1:
+            reduce = lambda t: dist.all_reduce(t, group=group)  # noqa: E731
+    model = _Model(mask, topology, params, placement, True, reduce)
     dev = model.dev
-    inter, intra = _build(dev, topology, topology.num_levels)
+    inter, intra = _build(dev, topology, topology.num_levels, reduce)
     q, qx = _launch_cost([p.z for p in inter], intra.z, topology, params, topology.num_levels,
                          model.dstar_dev, gamma, True, True)
     out_i = torch.empty(4, dtype=torch.int64, device="cuda")

@@ -154,7 +154,7 @@ class _Model:
     """Device evaluation of counts + time model for one mask/placement."""
 
     def __init__(self, mask: MaskLike, topology: Topology, params: LevelParams,
-                 placement: Placement | None, dedup: bool = True):
+                 placement: Placement | None, dedup: bool = True, reduce=None):
         dev = device_mask(mask, placement)
         if dev.experts != topology.experts:
             # the reference indexes experts through the topology; keep its failure mode
@@ -162,6 +162,9 @@ class _Model:
         self.dev = dev
         self.cuts = model_cuts(topology)
         dd, raw, _ = _device_counts(dev, self.cuts)
+        if reduce is not None:      # token-sharded mask: counts are additive over tokens
+            reduce(dd)
+            reduce(raw)
         self.dedup_dev, self.raw_dev = dd, raw
         depth = topology.num_levels
         a_i, b_i, a_a, b_a = _param_arrays(topology, params)

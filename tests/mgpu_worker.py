@@ -76,6 +76,28 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
     ep.close()
 
 
+def run_planner(rank, world):
+    """Token-sharded swap planning: all-reduced statistics give every rank the
+    reference's decision on the concatenated global mask."""
+    import paper_2508_09591_b200 as hm
+    from oracle import hiera as O
+    G, E, K, T_r = 8, 128, 8, 512
+    L = G // world
+    g = torch.Generator().manual_seed(77)
+    logits = torch.randn(G * T_r, E, generator=g)
+    logits += 3.0 * torch.log1p(torch.arange(E, dtype=torch.float32)).neg()[torch.randperm(E, generator=g)]
+    ids_all, _, _ = OM.route_topk(logits.numpy(), K)
+    lo, hi = rank * L * T_r, (rank + 1) * L * T_r
+    local = hm.mask_from_ids(torch.as_tensor(ids_all[lo:hi]), E)
+    topo = hm.build_topology([8], E, 2048, 2)
+    params = hm.LevelParams((), (), (2.0e-5,), (1.3e-12,))
+    plan = hm.select_swap(local, topo, params, 10.0, None, group=dist.group.WORLD)
+    bits = OM.ids_to_bits(ids_all, E)
+    pair, saving, d, no_swap, q = O.select_swap(bits, (8,), ((), (), (2.0e-5,), (1.3e-12,)), 4096, 10.0)
+    assert plan.pair == pair and plan.predicted_saving == saving and plan.no_swap_time == no_swap
+    assert np.array_equal(plan.cost_matrix, q)
+
+
 def run_migrate(rank, world):
     """Cross-GPU and same-GPU slot swaps through the expert store."""
     from paper_2508_09591_b200.migrate import ExpertStore
@@ -115,6 +137,8 @@ def main():
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
             dist.barrier()
     run_migrate(rank, world)
+    dist.barrier()
+    run_planner(rank, world)
     dist.barrier()
     if rank == 0:
         print("MULTI-GPU PARITY OK", world)
