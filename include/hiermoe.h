@@ -115,7 +115,7 @@ typedef struct hm_world hm_world;
  * the copy list of propagate_level (routing.py:189-215). */
 int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
                     int32_t top_k, int32_t hidden, int32_t elem_bytes, int64_t tokens_per_rank,
-                    int64_t n_cap_rows, int32_t relay_groups, hm_world** out);
+                    int64_t n_cap_rows, int32_t relay_groups, int32_t flags, hm_world** out);
 /* phase-2 ids/gates from a relay world's received copies (HD2 relay, K5) */
 int hm_relay_ids(hm_world* w, int32_t* ids2, float* w2, void* stream);
 int hm_world_destroy(hm_world* w);
@@ -147,6 +147,15 @@ int hm_expand(hm_world* w, void* stream);
 /* Gate-weighted combine (pre-reduce per destination + source sum for dedup). */
 int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
                void* stream);
+/* Backward (world created with flags & 1).  hm_dispatch_grad = combine
+ * backward: output grads -> expert-output grads (dedup broadcast, replaying the
+ * forward plan) + direct picks' gate grads; hm_combine_grad = dispatch
+ * backward: expert-input grads -> token grads (dedup reduction) + remaining
+ * gate grads. */
+int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, const float* wts,
+                     int32_t mode, float* dw, void* stream);
+int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float* dw, void* dx,
+                    void* stream);
 
 /* ---------------- expert FFN (tcgen05 + TMA + TMEM, sm_100a) -------------
  * The only dense contraction of the layer (E expert FFNs); no

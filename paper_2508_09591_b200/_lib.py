@@ -47,7 +47,7 @@ _SIGS = {
     "hm_np_pow": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "hm_smooth_max_rows": (c_int32, [c_void_p, c_int64, c_int32, c_double, c_void_p, c_void_p]),
     "hm_world_create": (c_int32, [c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
-                                  c_int64, c_int64, c_int32, POINTER(c_void_p)]),
+                                  c_int64, c_int64, c_int32, c_int32, POINTER(c_void_p)]),
     "hm_relay_ids": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_world_destroy": (c_int32, [c_void_p]),
     "hm_world_ipc_handle_size": (c_int64, []),
@@ -63,6 +63,9 @@ _SIGS = {
                                 c_void_p, c_void_p, c_void_p]),
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
+    "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
+                                   c_void_p]),
+    "hm_combine_grad": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "hm_grouped_gemm": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32,
                                   c_int32, c_int32, c_void_p, c_int64, c_void_p]),

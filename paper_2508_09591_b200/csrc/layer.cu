@@ -64,6 +64,9 @@ struct WorldDev {
   uint8_t* xmaj[kMaxRanks];
   uint8_t* ymaj[kMaxRanks];
   uint8_t* comb[kMaxRanks];
+  uint8_t* gy[kMaxRanks];     // backward: grad of expert outputs (expert-major), or null
+  uint8_t* gx[kMaxRanks];     // backward: grad of expert inputs (expert-major), or null
+  float* gw[kMaxRanks];       // backward: gate grads of dedup picks [R_cap][K], or null
   int32_t* counts[kMaxRanks];                 // count matrix [G][G+E] on d's GPU
   unsigned long long* flags[kMaxRanks];       // per GPU q: flags[q][0..P)
 };
@@ -651,7 +654,7 @@ constexpr int kRedUnroll = 4;
 // row's local picks in k order, fp32 accumulation, stored in payload dtype.
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
-                                                const Offsets* __restrict__ offs) {
+                                                const Offsets* __restrict__ offs, int grad) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
@@ -672,8 +675,9 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
     if (lane < w.K) {
       RowMeta m = w.recv_meta[dg][r * w.K + lane];
       ep = m.epos;
-      wt = m.w;
+      wt = grad ? 1.f : m.w;   // dispatch backward: unweighted sum of input grads
     }
+    const uint8_t* ysrc = grad ? w.gx[dg] : w.ymaj[dg];
     int4* dst = reinterpret_cast<int4*>(w.comb[dg] + r * w.row_bytes);
     for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kRedUnroll) {
       float acc[kRedUnroll][Vec<T>::N];
@@ -685,7 +689,7 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
         int e = __shfl_sync(0xffffffffu, ep, k);
         float wk = __shfl_sync(0xffffffffu, wt, k);
         if (e < 0) continue;
-        const int4* src = reinterpret_cast<const int4*>(w.ymaj[dg] + (int64_t)e * w.row_bytes);
+        const int4* src = reinterpret_cast<const int4*>(ysrc + (int64_t)e * w.row_bytes);
         int4 buf[kRedUnroll];
 #pragma unroll
         for (int u = 0; u < kRedUnroll; ++u) {
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
                                                 const unsigned long long* __restrict__ hitmask,
                                                 const int32_t* __restrict__ gpos,
                                                 const int32_t* __restrict__ epos, int mode,
-                                                uint8_t* __restrict__ out) {
+                                                int grad, uint8_t* __restrict__ out) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
@@ -737,8 +741,8 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
         if (e < 0 || ep < 0) continue;
         const int d = e / w.E_loc;
         if (mode == 2 && d / w.L != w.p) continue;
-        srcs[n] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
-        ws[n] = wts[t * w.K + k];
+        srcs[n] = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
+        ws[n] = grad ? 1.f : wts[t * w.K + k];
         ++n;
       }
     }
@@ -813,6 +817,171 @@ __global__ void k_relay_ids(const WorldDev* __restrict__ wp, const Offsets* __re
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// backward (K8).  Combine backward = dedup broadcast of the output gradient g
+// replaying the forward plan (same gpos/epos): direct picks get
+// gy[epos] = w_k g and their gate grad <g, y_k>; dedup destinations get g once
+// and scale per local pick there (k_expand_grad).  Dispatch backward = the
+// combine machinery with unit weights over gx (k_reduce/k_gather grad=1).
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ wp,
+                                                   const uint8_t* __restrict__ g,
+                                                   const int32_t* __restrict__ ids,
+                                                   const float* __restrict__ wts,
+                                                   const unsigned long long* __restrict__ hitmask,
+                                                   const int32_t* __restrict__ gpos,
+                                                   const int32_t* __restrict__ epos, int mode,
+                                                   float* __restrict__ dw) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  const int64_t ntok = (int64_t)w.L * w.T_r;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = warp; t < ntok; t += nw) {
+    // direct picks (scaled rows + dot products) and dedup destinations (raw rows)
+    int nd = 0, nr = 0;
+    uint8_t* drow[kMaxK];
+    const uint8_t* yrow[kMaxK];
+    float dwk[kMaxK];
+    int dk[kMaxK];
+    uint8_t* rrow[kMaxRanks];
+    if (mode != 1) {
+      for (int k = 0; k < w.K; ++k) {
+        int e = ids[t * w.K + k], ep = epos[t * w.K + k];
+        if (e < 0 || ep < 0) continue;
+        const int d = e / w.E_loc;
+        if (mode == 2 && d / w.L != w.p) continue;
+        drow[nd] = w.gy[d] + (int64_t)ep * w.row_bytes;
+        yrow[nd] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
+        dwk[nd] = wts[t * w.K + k];
+        dk[nd] = k;
+        ++nd;
+      }
+    }
+    if (mode != 0) {
+      unsigned long long hit = hitmask[t];
+      for (int d = 0; d < w.G; ++d) {
+        if (!((hit >> d) & 1ull)) continue;
+        if (mode == 2 && d / w.L == w.p) continue;
+        int gp = gpos[t * w.G + d];
+        if (gp < 0) continue;
+        rrow[nr++] = w.recv_x[d] + (int64_t)gp * w.row_bytes;
+      }
+    }
+    float dot[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) dot[j] = 0.f;
+    const int4* src = reinterpret_cast<const int4*>(g + t * w.row_bytes);
+    for (int64_t v = lane; v < nvec; v += 32) {
+      int4 gv = src[v];
+      float gf[Vec<T>::N];
+      Vec<T>::to_f32(gv, gf);
+      for (int j = 0; j < nr; ++j) st_na_v4(reinterpret_cast<int4*>(rrow[j]) + v, gv);
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) {
+        if (j >= nd) break;
+        float yf[Vec<T>::N], sf[Vec<T>::N];
+        Vec<T>::to_f32(ld_v4(reinterpret_cast<const int4*>(yrow[j]) + v), yf);
+#pragma unroll
+        for (int q = 0; q < Vec<T>::N; ++q) {
+          dot[j] = fmaf(gf[q], yf[q], dot[j]);
+          sf[q] = dwk[j] * gf[q];
+        }
+        st_na_v4(reinterpret_cast<int4*>(drow[j]) + v, Vec<T>::from_f32(sf));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j >= nd) break;
+      float x = dot[j];
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) dw[t * w.K + dk[j]] = x;
+    }
+  }
+}
+
+// destination: received gradient row -> scaled rows for each local pick, and
+// the pick's gate gradient <g, y_k> into gw[row][k]
+template <typename T>
+__global__ void __launch_bounds__(256) k_expand_grad(const WorldDev* __restrict__ wp,
+                                                     const Offsets* __restrict__ offs) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t total = 0;
+  for (int d = 0; d < w.L; ++d) total += offs->R[d];
+  for (int64_t i = warp; i < total; i += nw) {
+    int d_loc = 0;
+    int64_t r = i;
+    while (r >= offs->R[d_loc]) {
+      r -= offs->R[d_loc];
+      ++d_loc;
+    }
+    const int dg = w.p * w.L + d_loc;
+    int nd = 0;
+    int eps[kMaxK], ks[kMaxK];
+    float wk[kMaxK];
+    for (int k = 0; k < w.K; ++k) {
+      RowMeta m = w.recv_meta[dg][r * w.K + k];
+      if (m.epos < 0) continue;
+      eps[nd] = m.epos;
+      wk[nd] = m.w;
+      ks[nd] = k;
+      ++nd;
+    }
+    float dot[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) dot[j] = 0.f;
+    const int4* src = reinterpret_cast<const int4*>(w.recv_x[dg] + r * w.row_bytes);
+    for (int64_t v = lane; v < nvec; v += 32) {
+      float gf[Vec<T>::N];
+      Vec<T>::to_f32(ld_nc_v4(src + v), gf);
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) {
+        if (j >= nd) break;
+        float yf[Vec<T>::N], sf[Vec<T>::N];
+        Vec<T>::to_f32(ld_nc_v4(reinterpret_cast<const int4*>(w.ymaj[dg] + (int64_t)eps[j] * w.row_bytes) + v), yf);
+#pragma unroll
+        for (int q = 0; q < Vec<T>::N; ++q) {
+          dot[j] = fmaf(gf[q], yf[q], dot[j]);
+          sf[q] = wk[j] * gf[q];
+        }
+        st_na_v4(reinterpret_cast<int4*>(w.gy[dg] + (int64_t)eps[j] * w.row_bytes) + v,
+                 Vec<T>::from_f32(sf));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j >= nd) break;
+      float x = dot[j];
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) w.gw[dg][r * w.K + ks[j]] = x;
+    }
+  }
+}
+
+// source: gate grads of dedup picks from the destination's gw rows (peer loads)
+__global__ void k_gate_grad(const WorldDev* __restrict__ wp, const int32_t* __restrict__ ids,
+                            const int32_t* __restrict__ gpos, int mode, float* __restrict__ dw) {
+  const WorldDev& w = *wp;
+  const int64_t n = (int64_t)w.L * w.T_r * w.K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / w.K;
+    const int k = (int)(i % w.K);
+    const int e = ids[i];
+    if (e < 0 || mode == 0) continue;
+    const int d = e / w.E_loc;
+    if (mode == 2 && d / w.L == w.p) continue;   // direct pick: k_pack_grad wrote it
+    const int gp = gpos[t * w.G + d];
+    if (gp >= 0) dw[i] = w.gw[d][(int64_t)gp * w.K + k];
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -826,7 +995,8 @@ struct hm_world {
   uint8_t* sym = nullptr;  // symmetric allocation (this GPU)
   size_t sym_bytes = 0;
   size_t off_recv_x = 0, off_meta = 0, off_xmaj = 0, off_ymaj = 0, off_comb = 0, off_counts = 0,
-         off_flags = 0;
+         off_flags = 0, off_gy = 0, off_gx = 0, off_gw = 0;
+  bool grad = false;
   std::vector<void*> opened;  // peer bases opened via IPC
   // local scratch
   int nchunks = 0;
@@ -881,6 +1051,10 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
     h.xmaj[d] = base + w->off_xmaj + (size_t)l * h.N_cap * h.row_bytes;
     h.ymaj[d] = base + w->off_ymaj + (size_t)l * h.N_cap * h.row_bytes;
     h.comb[d] = base + w->off_comb + (size_t)l * h.R_cap * h.row_bytes;
+    h.gy[d] = w->grad ? base + w->off_gy + (size_t)l * h.N_cap * h.row_bytes : nullptr;
+    h.gx[d] = w->grad ? base + w->off_gx + (size_t)l * h.N_cap * h.row_bytes : nullptr;
+    h.gw[d] = w->grad ? reinterpret_cast<float*>(base + w->off_gw) + (size_t)l * h.R_cap * h.K
+                      : nullptr;
     h.counts[d] = reinterpret_cast<int32_t*>(base + w->off_counts);
     h.flags[d] = reinterpret_cast<unsigned long long*>(base + w->off_flags);
   }
@@ -889,7 +1063,7 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
 HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
                            int32_t top_k, int32_t hidden, int32_t elem_bytes,
                            int64_t tokens_per_rank, int64_t n_cap_rows, int32_t relay_groups,
-                           hm_world** out) {
+                           int32_t flags, hm_world** out) {
   HM_CHECK_ARG(out, "hm_world_create: null out");
   *out = nullptr;
   HM_CHECK_ARG(ranks >= 1 && ranks <= kMaxRanks, "ranks must be 1..%d", kMaxRanks);
@@ -933,6 +1107,12 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   w->off_xmaj = o;   o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
   w->off_ymaj = o;   o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
   w->off_comb = o;   o = align_up(o + (size_t)h.L * h.R_cap * h.row_bytes, 256);
+  w->grad = (flags & 1) != 0;   // backward buffers gy, gx, gw
+  if (w->grad) {
+    w->off_gy = o; o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
+    w->off_gx = o; o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
+    w->off_gw = o; o = align_up(o + (size_t)h.L * h.R_cap * h.K * 4, 256);
+  }
   w->off_counts = o; o = align_up(o + (size_t)h.G * (h.G + h.E) * 4, 256);
   w->off_flags = o;  o = align_up(o + (size_t)h.P * 8, 256);
   w->sym_bytes = o;
@@ -1117,9 +1297,9 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   if (dedup && !(h.P == 1 && mode == 2) && !h.U1) {   // relay: rows arrive pre-reduced
     SegScope sc(w, kSegReduce, s);
     if (h.elem == 2)
-      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
     else
-      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
     HM_LAUNCHED();
   }
   if (mode != 1) HM_CHECK_ARG(wts && ids, "hm_combine: raw/hybrid combine needs ids and weights");
@@ -1133,10 +1313,10 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   SegScope sc(w, kSegGather, s);
   if (h.elem == 2)
     k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos,
-                                                   mode, (uint8_t*)out);
+                                                   mode, 0, (uint8_t*)out);
   else
     k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode,
-                                           (uint8_t*)out);
+                                           0, (uint8_t*)out);
   HM_LAUNCHED();
   return 0;
 }
@@ -1176,6 +1356,8 @@ HM_API int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void**
             *bytes = sizeof(int32_t) * 2 * kMaxRanks; break;
     case 10: *ptr = w->n_e; *bytes = h.E * 4; break;
     case 11: *ptr = w->status; *bytes = 16; break;
+    case 12: *ptr = h.gy[d]; *bytes = w->grad ? h.N_cap * h.row_bytes : 0; break;
+    case 13: *ptr = h.gx[d]; *bytes = w->grad ? h.N_cap * h.row_bytes : 0; break;
     default: hm::set_error("hm_world_buffer: unknown kind %d", kind); return hm::kInvalid;
   }
   return 0;
@@ -1232,6 +1414,74 @@ HM_API int hm_relay_ids(hm_world* w, int32_t* ids2, float* w2, void* stream) {
   HM_CHECK_ARG(w->h.U1 > 0, "hm_relay_ids: not a relay world");
   int64_t n = (int64_t)w->h.L * w->h.R_cap * w->h.K;
   k_relay_ids<<<grid_for(n, 256, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(w->d, w->offs, ids2, w2);
+  HM_LAUNCHED();
+  return 0;
+}
+
+// Combine backward: grad of the combined output g [L*T_r, M] -> expert-output
+// grads gy (expert-major, every local rank) + gate grads of direct picks into
+// dw [L*T_r, K]; replays the last forward plan (no re-planning).
+HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, const float* wts,
+                            int32_t mode, float* dw, void* stream) {
+  HM_CHECK_ARG(w && g && ids && wts && dw, "hm_dispatch_grad: null argument");
+  HM_CHECK_ARG(w->grad, "hm_dispatch_grad: world created without backward buffers");
+  HM_CHECK_ARG(mode == w->last_mode, "hm_dispatch_grad: mode differs from the forward's");
+  HM_CHECK_ARG(!w->h.U1, "hm_dispatch_grad: relay worlds have no backward");
+  cudaStream_t s = (cudaStream_t)stream;
+  const WorldDev& h = w->h;
+  const int64_t T = (int64_t)h.L * h.T_r;
+  int blocks = grid_for(T, 8, kSMs * 8);
+  if (h.elem == 2)
+    k_pack_grad<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->hitmask,
+                                                      w->gpos, w->epos, mode, dw);
+  else
+    k_pack_grad<float><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->hitmask,
+                                              w->gpos, w->epos, mode, dw);
+  HM_LAUNCHED();
+  if (h.P > 1) {
+    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    HM_LAUNCHED();
+  }
+  if (mode != 0 && !(h.P == 1 && mode == 2)) {
+    if (h.elem == 2)
+      k_expand_grad<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+    else
+      k_expand_grad<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+    HM_LAUNCHED();
+  }
+  return 0;
+}
+
+// Dispatch backward: expert-input grads gx (expert-major) -> token grads
+// dx [L*T_r, M] (unweighted dedup reduction), and the dedup picks' gate grads
+// into dw.
+HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float* dw, void* dx,
+                           void* stream) {
+  HM_CHECK_ARG(w && ids && dw && dx, "hm_combine_grad: null argument");
+  HM_CHECK_ARG(w->grad, "hm_combine_grad: world created without backward buffers");
+  cudaStream_t s = (cudaStream_t)stream;
+  const WorldDev& h = w->h;
+  if (mode != 0 && !(h.P == 1 && mode == 2)) {
+    if (h.elem == 2)
+      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1);
+    else
+      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1);
+    HM_LAUNCHED();
+  }
+  if (h.P > 1) {
+    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    HM_LAUNCHED();
+  }
+  const int64_t T = (int64_t)h.L * h.T_r;
+  int blocks = grid_for(T, 8, kSMs * 8);
+  if (h.elem == 2)
+    k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, nullptr, w->hitmask, w->gpos, w->epos,
+                                                   mode, 1, (uint8_t*)dx);
+  else
+    k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, nullptr, w->hitmask, w->gpos, w->epos, mode, 1,
+                                           (uint8_t*)dx);
+  HM_LAUNCHED();
+  k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode, dw);
   HM_LAUNCHED();
   return 0;
 }

@@ -33,7 +33,7 @@ from . import _lib
 from ._lib import ptr, stream_ptr
 
 _KIND = {"recv_x": 0, "recv_meta": 1, "xmaj": 2, "ymaj": 3, "comb": 4, "counts": 5, "gpos": 6,
-         "epos": 7, "hitmask": 8, "offsets": 9, "n_e": 10, "status": 11}
+         "epos": 7, "hitmask": 8, "offsets": 9, "n_e": 10, "status": 11, "gy": 12, "gx": 13}
 
 _STATUS = {2: "row capacity overflow", 3: "peer barrier timeout", 4: "slot id out of range"}
 
@@ -112,7 +112,7 @@ class EPWorld:
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int,
                  tokens_per_rank: int, dtype: torch.dtype = torch.bfloat16,
                  gpus: int = 1, gpu_index: int = 0, group=None, n_cap_rows: int = 0,
-                 relay_groups: int = 0):
+                 relay_groups: int = 0, grad: bool = False):
         lib = _lib.load()
         if dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("payload dtype must be bfloat16 or float32")
@@ -123,7 +123,8 @@ class EPWorld:
         self.elem = 2 if dtype == torch.bfloat16 else 4
         h = ctypes.c_void_p()
         _lib.check(lib.hm_world_create(ranks, gpus, gpu_index, experts, top_k, hidden, self.elem,
-                                       tokens_per_rank, n_cap_rows, relay_groups, ctypes.byref(h)),
+                                       tokens_per_rank, n_cap_rows, relay_groups, int(grad),
+                                       ctypes.byref(h)),
                    "hm_world_create")
         self.relay_groups = relay_groups
         self._h = h
@@ -190,6 +191,27 @@ class EPWorld:
         if out is None:
             out = torch.empty((t, self.hidden), dtype=self.dtype, device="cuda")
         _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), transport_mode(dedup),
+                  ptr(out), stream_ptr())
+        return out
+
+    def dispatch_grad(self, grad_out: torch.Tensor, slot_ids: torch.Tensor,
+                      weights: torch.Tensor, dedup=True) -> torch.Tensor:
+        """Combine backward: d(out) -> expert-output grads (buffer "gy") and the
+        gate grads of direct picks; returns the [T, K] gate-grad tensor (the
+        dedup picks' entries are filled by combine_grad)."""
+        self._check_rows(grad_out, slot_ids)
+        dw = torch.zeros(slot_ids.shape, dtype=torch.float32, device="cuda")
+        _lib.call("hm_dispatch_grad", self._h, ptr(grad_out), ptr(slot_ids), ptr(weights),
+                  transport_mode(dedup), ptr(dw), stream_ptr())
+        return dw
+
+    def combine_grad(self, slot_ids: torch.Tensor, dw: torch.Tensor, dedup=True,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        """Dispatch backward: expert-input grads (buffer "gx") -> token grads."""
+        t = self.local * self.tokens_per_rank
+        if out is None:
+            out = torch.empty((t, self.hidden), dtype=self.dtype, device="cuda")
+        _lib.call("hm_combine_grad", self._h, ptr(slot_ids), transport_mode(dedup), ptr(dw),
                   ptr(out), stream_ptr())
         return out
 
