@@ -167,6 +167,14 @@ int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t groups
 int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                   const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                   void* y, void* stream);
+/* Expert FFN backward: recomputed pre-activations, dgrad GEMMs with
+ * transposed weights (w13t [g][M][2I], w2t [g][I][M]), SwiGLU backward, and
+ * weight-gradient GEMMs over each expert's own token range. */
+int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                           const void* w13, const void* w13t, const void* w2t, const void* gy,
+                           int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
+                           void* h, void* ta, void* tb, int64_t kmax, int32_t* layout, void* gx,
+                           void* dw13, void* dw2, void* stream);
 
 /* ---------------- expert migration (K11) ------------------------------------
  * Apply a planned swap (apply_swap, swap.py:255-259) to the physical expert

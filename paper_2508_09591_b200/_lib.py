@@ -76,6 +76,10 @@ _SIGS = {
     "hm_store_array": (c_int32, [c_void_p, c_int32, POINTER(c_void_p)]),
     "hm_store_status": (c_int32, [c_void_p, c_void_p]),
     "hm_migrate": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
+    "hm_expert_ffn_backward": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_expert_ffn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
 }

@@ -41,8 +41,9 @@ constexpr int kMaxGroups = 64;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
 
 struct GemmArgs {
-  const int32_t* n_rows;  // [groups] rows per group (device)
+  const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
   int groups;
+  int m_out;              // wgrad: output rows per group (A rows)
   int N;                  // output features per group (weight rows per group)
   int K;                  // reduction length
   int swiglu;             // 1: out = silu(gate) * up, out_cols = N / 2
@@ -153,8 +154,8 @@ struct TileMap {
   int ntile_n;
   int total;
   int start[kMaxGroups + 1];    // first tile index of each group
-  int row0[kMaxGroups];         // first row of each group in A
-  int rows[kMaxGroups];
+  int row0[kMaxGroups];         // first row of each group in A (wgrad: first K column)
+  int rows[kMaxGroups];         // rows of each group (wgrad: padded K extent)
 };
 
 __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t, int& g, int& mt,
@@ -166,7 +167,11 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
   nt = local % tm.ntile_n;
 }
 
-template <int kSwiGLU>
+// kMode 0: out = A_g B_g^T over row groups; 1: same + SwiGLU epilogue;
+// 2: weight-gradient mode -- every group g is a full [m_out x N] output
+// (rows g*m_out..), reducing over its own K range [row0_g, row0_g + rows_g)
+// of A [m_out x K_total] and B [N x K_total] (K_total = padded token rows).
+template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
@@ -188,10 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tm.ntile_n = args.N / BN;
     for (int g = 0; g < args.groups; ++g) {
       int n = args.n_rows[g];
+      if (kMode == 2) n = (n + BK - 1) / BK * BK;   // K padded to the k-block
       tm.start[g] = acc;
       tm.row0[g] = row;
       tm.rows[g] = n;
-      acc += ((n + BM - 1) / BM) * tm.ntile_n;
+      acc += (kMode == 2 ? args.m_out / BM : (n + BM - 1) / BM) * tm.ntile_n;
       row += n;
     }
     tm.start[args.groups] = acc;
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int kblocks = args.K / BK;
+  const int kblocks_fixed = args.K / BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -227,13 +233,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
         int g, mt, nt;
         tile_coords(tm, args.groups, t, g, mt, nt);
-        const int arow = tm.row0[g] + mt * BM;
-        const int brow = g * args.N + nt * BN;
+        const int arow = kMode == 2 ? mt * BM : tm.row0[g] + mt * BM;
+        const int brow = kMode == 2 ? nt * BN : g * args.N + nt * BN;
+        const int k0 = kMode == 2 ? tm.row0[g] : 0;
+        const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           mbar_expect_tx(full + stage, kStageBytes);
-          tma_load_2d(sa + stage * kABytes, &map_a, full + stage, kb * BK, arow);
-          tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, kb * BK, brow);
+          tma_load_2d(sa + stage * kABytes, &map_a, full + stage, k0 + kb * BK, arow);
+          tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, k0 + kb * BK, brow);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -252,6 +260,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
+        int kblocks = kblocks_fixed;
+        if (kMode == 2) {
+          int g, mt, nt;
+          tile_coords(tm, args.groups, t, g, mt, nt);
+          kblocks = tm.rows[g] / BK;
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
@@ -281,10 +295,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int r_in = mt * BM + q * 32 + lane;          // row within group
-      const bool valid = r_in < tm.rows[g];
-      __nv_bfloat16* orow = args.out + (int64_t)(tm.row0[g] + r_in) * args.ld_out;
+      const bool valid = kMode == 2 ? true : r_in < tm.rows[g];
+      const bool zero = kMode == 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
+      __nv_bfloat16* orow =
+          args.out + (kMode == 2 ? (int64_t)g * args.m_out + r_in : (int64_t)(tm.row0[g] + r_in)) *
+                         args.ld_out;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (kSwiGLU) {
+      if (kMode == 1) {
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
           float gv[32], uv[32];
@@ -310,6 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tbase + c, v);
+          if (zero) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
           if (valid) {
             __align__(16) __nv_bfloat162 hv[16];
 #pragma unroll
@@ -331,6 +352,91 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(kTmemCols));
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// expert FFN backward helpers
+// group layout for the weight-gradient GEMMs: token rows of group g are
+// [row0_g, row0_g + n_g); as K columns they start at col0_g, padded to 64
+__global__ void k_group_layout(const int32_t* __restrict__ n_rows, int groups,
+                               int32_t* __restrict__ row0, int32_t* __restrict__ col0) {
+  if (threadIdx.x || blockIdx.x) return;
+  int r = 0, c = 0;
+  for (int g = 0; g < groups; ++g) {
+    row0[g] = r;
+    col0[g] = c;
+    r += n_rows[g];
+    c += (n_rows[g] + BK - 1) / BK * BK;
+  }
+  row0[groups] = r;
+  col0[groups] = c;
+}
+
+// dst[c][col0_g + i] = src[row0_g + i][c] (bf16), zero padding columns
+__global__ void k_transpose_groups(const __nv_bfloat16* __restrict__ src, int C,
+                                   const int32_t* __restrict__ n_rows, int groups,
+                                   const int32_t* __restrict__ row0, const int32_t* __restrict__ col0,
+                                   __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
+  __shared__ __nv_bfloat16 tile[64][65];
+  const int total = row0[groups];
+  const int r_base = blockIdx.y * 64, c_base = blockIdx.x * 64;
+  if (r_base < total) {
+    for (int i = threadIdx.y; i < 64; i += blockDim.y) {
+      const int r = r_base + i;
+      for (int j = threadIdx.x; j < 64; j += blockDim.x) {
+        const int c = c_base + j;
+        tile[i][j] = (r < total && c < C) ? src[(int64_t)r * C + c] : __float2bfloat16(0.f);
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 64; j += blockDim.y) {
+      const int c = c_base + j;
+      if (c >= C) continue;
+      for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+        const int r = r_base + i;
+        if (r >= total) continue;
+        int g = 0;
+        while (g + 1 < groups && row0[g + 1] <= r) ++g;
+        dst[(int64_t)c * ld_dst + col0[g] + (r - row0[g])] = tile[i][j];
+      }
+    }
+  }
+  // padding columns of every group (first row-tile blocks only)
+  if (blockIdx.y == 0) {
+    for (int g = 0; g < groups; ++g) {
+      const int pad0 = col0[g] + n_rows[g], pad1 = col0[g + 1];
+      for (int j = threadIdx.y; j < 64; j += blockDim.y) {
+        const int c = c_base + j;
+        if (c >= C) continue;
+        for (int k = pad0 + threadIdx.x; k < pad1; k += blockDim.x)
+          dst[(int64_t)c * ld_dst + k] = __float2bfloat16(0.f);
+      }
+    }
+  }
+}
+
+// SwiGLU backward on 128-column gate/up interleaved pre-activations:
+// h = silu(a) u;  da = dh u silu'(a);  du = dh silu(a)
+__global__ void k_swiglu_bwd(const __nv_bfloat16* __restrict__ g13, const __nv_bfloat16* __restrict__ dh,
+                             const int32_t* __restrict__ row0, int groups, int inter,
+                             __nv_bfloat16* __restrict__ dg13, __nv_bfloat16* __restrict__ h) {
+  const int64_t rows = row0[groups];
+  const int64_t n = rows * inter;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / inter;
+    const int j = (int)(i % inter);
+    const int b = j / 128, c = j % 128;
+    const int64_t ga = r * 2 * inter + 256 * b + c, gu = ga + 128;
+    const float a = __bfloat162float(g13[ga]), u = __bfloat162float(g13[gu]);
+    const float d = __bfloat162float(dh[i]);
+    const float sg = 1.f / (1.f + __expf(-a));
+    const float si = a * sg;
+    h[i] = __float2bfloat16(si * u);
+    dg13[gu] = __float2bfloat16(d * si);
+    dg13[ga] = __float2bfloat16(d * u * sg * (1.f + a * (1.f - sg)));
   }
 }
 
@@ -376,16 +482,17 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
 
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
-                cudaStream_t s) {
+                cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
   CUtensorMap ma, mb;
   int st = make_map(&ma, a, (uint64_t)a_rows, (uint64_t)K, BM);
   if (st) return st;
-  st = make_map(&mb, b, (uint64_t)groups * N, (uint64_t)K, BN);
+  st = make_map(&mb, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, BN);
   if (st) return st;
   GemmArgs args;
+  args.m_out = wgrad_m_out;
   args.n_rows = n_rows;
   args.groups = groups;
   args.N = N;
@@ -399,7 +506,11 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (swiglu) {
+  if (wgrad_m_out) {
+    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_grouped_gemm<2><<<sms, kThreads, smem, s>>>(ma, mb, args);
+  } else if (swiglu) {
     HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     k_grouped_gemm<1><<<sms, kThreads, smem, s>>>(ma, mb, args);
@@ -436,4 +547,53 @@ HM_API int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, i
   if (st) return st;
   return launch_gemm(h, a_rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
                      (cudaStream_t)stream);
+}
+
+// Expert SwiGLU FFN backward (tcgen05 GEMMs + elementwise/transposes):
+//   G13 = X W13^T (recomputed pre-activations), dH = gY W2 (via W2^T),
+//   dG13 = swiglu'(G13, dH), H = swiglu(G13), gX = dG13 W13 (via W13^T),
+//   dW2 = gY^T H, dW13 = dG13^T X  (weight-gradient GEMMs over each expert's
+//   own token range, K padded to 64).
+// Buffers (rows = a_rows capacity): g13, dg13 [rows, 2I]; dh, h [rows, I];
+// ta [max(M, 2I), kmax], tb [max(M, I), kmax] with kmax >= rows + 64*groups;
+// layout: 2*(groups+1) int32 scratch.  Outputs: gx [rows, M],
+// dw13 [groups][2I][M], dw2 [groups][M][I].
+HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                  int32_t groups, const void* w13, const void* w13t,
+                                  const void* w2t, const void* gy, int32_t hidden, int32_t inter,
+                                  void* g13, void* dh, void* dg13, void* h, void* ta, void* tb,
+                                  int64_t kmax, int32_t* layout, void* gx, void* dw13, void* dw2,
+                                  void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  HM_CHECK_ARG(kmax % BK == 0 && kmax >= a_rows + (int64_t)BK * groups,
+               "hm_expert_ffn_backward: kmax must cover the padded rows");
+  const int M = hidden, I = inter;
+  int st;
+  // recompute gate/up pre-activations, then dH
+  if ((st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I, nullptr, s))) return st;
+  if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s))) return st;
+  int32_t* row0 = layout;
+  int32_t* col0 = layout + groups + 1;
+  k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, row0, col0);
+  HM_LAUNCHED();
+  k_swiglu_bwd<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh, row0,
+                                         groups, I, (__nv_bfloat16*)dg13, (__nv_bfloat16*)h);
+  HM_LAUNCHED();
+  // data gradient
+  if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s))) return st;
+  // weight gradients: transposed activations, reduction over each expert's rows
+  auto transpose = [&](const void* src, int C, void* dst) -> int {
+    dim3 grid((C + 63) / 64, (unsigned)((a_rows + 63) / 64));
+    k_transpose_groups<<<grid, dim3(32, 8), 0, s>>>((const __nv_bfloat16*)src, C, n_rows, groups,
+                                                    row0, col0, (__nv_bfloat16*)dst, kmax);
+    return launch_status();
+  };
+  if ((st = transpose(gy, M, ta))) return st;
+  if ((st = transpose(h, I, tb))) return st;
+  if ((st = launch_gemm(ta, M, tb, groups, n_rows, I, (int)kmax, 0, dw2, I, nullptr, s, M, I))) return st;
+  if ((st = transpose(dg13, 2 * I, ta))) return st;
+  if ((st = transpose(x, M, tb))) return st;
+  if ((st = launch_gemm(ta, 2 * I, tb, groups, n_rows, M, (int)kmax, 0, dw13, M, nullptr, s, 2 * I, M)))
+    return st;
+  return 0;
 }

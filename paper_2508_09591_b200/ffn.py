@@ -45,3 +45,30 @@ def expert_ffn_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int, w13: 
     """FFN on raw device rows (e.g. an EPWorld's xmaj -> ymaj buffers)."""
     _lib.call("hm_expert_ffn", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w2), hidden,
               inter, ptr(h), y_ptr, stream_ptr())
+
+
+class FFNBackwardScratch:
+    """Work buffers of one expert-FFN backward (capacity rows x widths)."""
+
+    def __init__(self, rows: int, groups: int, hidden: int, inter: int):
+        kw = dict(dtype=torch.bfloat16, device="cuda")
+        self.rows, self.groups = rows, groups
+        self.kmax = (rows + BLOCK // 2 * groups + 63) // 64 * 64 + 64 * groups
+        self.g13 = torch.empty(rows, 2 * inter, **kw)
+        self.dg13 = torch.empty(rows, 2 * inter, **kw)
+        self.dh = torch.empty(rows, inter, **kw)
+        self.h = torch.empty(rows, inter, **kw)
+        self.ta = torch.empty(max(hidden, 2 * inter), self.kmax, **kw)
+        self.tb = torch.empty(max(hidden, inter), self.kmax, **kw)
+        self.layout = torch.empty(2 * (groups + 1), dtype=torch.int32, device="cuda")
+
+
+def expert_ffn_backward_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
+                             w13: torch.Tensor, w13t: torch.Tensor, w2t: torch.Tensor,
+                             gy_ptr: int, hidden: int, inter: int, sc: FFNBackwardScratch,
+                             gx_ptr: int, dw13: torch.Tensor, dw2: torch.Tensor) -> None:
+    """Grads of the SwiGLU experts: gx (rows), dW13 [g][2I][M], dW2 [g][M][I]."""
+    _lib.call("hm_expert_ffn_backward", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w13t),
+              ptr(w2t), gy_ptr, hidden, inter, ptr(sc.g13), ptr(sc.dh), ptr(sc.dg13), ptr(sc.h),
+              ptr(sc.ta), ptr(sc.tb), sc.kmax, ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
+              stream_ptr())

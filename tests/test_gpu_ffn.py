@@ -59,3 +59,45 @@ def test_swiglu_ffn_matches_fp32(hm):
         r += n
     ref = torch.cat(refs)
     torch.testing.assert_close(y.float(), ref, rtol=3e-2, atol=3e-2)
+
+
+def test_swiglu_ffn_backward_matches_autograd(hm):
+    """tcgen05 FFN backward (dgrad + weight grads) vs torch autograd in fp32."""
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
+                                           pack_w13)
+    torch.manual_seed(4)
+    G, M, I = 3, 256, 256
+    n_rows = [100, 0, 257]
+    rows = sum(n_rows)
+    cap = rows + 40
+    x = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+    x[:rows] = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    gy = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+    gy[:rows] = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    w1 = (torch.randn(G, I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w3 = (torch.randn(G, I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    w13 = pack_w13(w1, w3)
+    w13t = w13.transpose(1, 2).contiguous()
+    w2t = w2.transpose(1, 2).contiguous()
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    sc = FFNBackwardScratch(cap, G, M, I)
+    gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+    dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
+    dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
+    expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t, gy.data_ptr(),
+                             M, I, sc, gx.data_ptr(), dw13, dw2)
+    torch.cuda.synchronize()
+    r = 0
+    for g, n in enumerate(n_rows):
+        xs = x[r:r + n].float().requires_grad_(True)
+        a1 = w1[g].float().requires_grad_(True)
+        a3 = w3[g].float().requires_grad_(True)
+        b2 = w2[g].float().requires_grad_(True)
+        y = (torch.nn.functional.silu(xs @ a1.T) * (xs @ a3.T)) @ b2.T
+        y.backward(gy[r:r + n].float())
+        torch.testing.assert_close(gx[r:r + n].float(), xs.grad, rtol=3e-2, atol=3e-2)
+        d13 = pack_w13(a1.grad[None], a3.grad[None])[0]
+        torch.testing.assert_close(dw13[g].float(), d13, rtol=3e-2, atol=3e-2 * max(1.0, d13.abs().max().item()))
+        torch.testing.assert_close(dw2[g].float(), b2.grad, rtol=3e-2, atol=3e-2 * max(1.0, b2.grad.abs().max().item()))
+        r += n
