@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .ffn import expert_ffn_ptrs, pack_w13
+from .ffn import FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs, pack_w13
 from .layer import EPWorld, route_topk
 from .migrate import ExpertStore
 from .routing import Placement
@@ -23,7 +23,8 @@ from .routing import Placement
 class HierMoELayer:
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int, inter: int,
                  tokens_per_rank: int, gpus: int = 1, gpu_index: int = 0, group=None,
-                 dedup=True, seed: int = 0, renormalize: bool = True):
+                 dedup=True, seed: int = 0, renormalize: bool = True, grad: bool = False,
+                 n_cap_rows: int = 0):
         if inter % 128 or hidden % 256:
             raise ValueError("hidden must be a multiple of 256 and inter of 128")
         self.ranks, self.experts, self.top_k = ranks, experts, top_k
@@ -35,7 +36,9 @@ class HierMoELayer:
         self.dedup = dedup
         self.renormalize = renormalize
         self.world = EPWorld(ranks, experts, top_k, hidden, tokens_per_rank,
-                             dtype=torch.bfloat16, gpus=gpus, gpu_index=gpu_index, group=group)
+                             dtype=torch.bfloat16, gpus=gpus, gpu_index=gpu_index, group=group,
+                             grad=grad, n_cap_rows=n_cap_rows)
+        self.grad = grad
         # router replicated on every GPU (seeded identically); experts: the
         # slots of local ranks, seeded by global slot so any GPU count builds
         # the same model
@@ -66,6 +69,19 @@ class HierMoELayer:
         self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
         self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
         self.set_placement(Placement.identity(experts))
+        self._saved = None
+        if grad:
+            self.refresh_transposed_weights()
+            self.bwd = FFNBackwardScratch(self.world.n_cap, self.e_loc, hidden, inter)
+            self.dw13 = torch.zeros_like(self.w13)
+            self.dw2 = torch.zeros_like(self.w2)
+            self.dw_router = torch.zeros_like(self.w_router)
+
+    def refresh_transposed_weights(self) -> None:
+        """Transposed bf16 weights for the data-gradient GEMMs (after any
+        weight update or migration)."""
+        self.w13t = self.w13.transpose(2, 3).contiguous()
+        self.w2t = self.w2.transpose(2, 3).contiguous()
 
     def set_placement(self, placement: Placement) -> None:
         self.placement = placement
@@ -81,6 +97,8 @@ class HierMoELayer:
         r, c = int(pair[0]), int(pair[1])
         self.set_placement(self.placement.swapped(r, c))
         self.store.migrate(r, c)
+        if self.grad:
+            self.refresh_transposed_weights()
 
     def route(self, x: torch.Tensor):
         logits = x.float() @ self.w_router.T
@@ -97,13 +115,51 @@ class HierMoELayer:
                             self.w13[l], self.w2[l], self.hidden, self.inter, self.h, y_ptr)
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        slot, w, _ = self.route(x)
+        slot, w, ex = self.route(x)
+        if self.grad:
+            self._saved = (x, slot, w, ex)
         self.world.dispatch(x, slot, w, dedup=self.dedup)
         self.experts_forward()   # expert-major rows are local after the dispatch barrier
         # hm_combine barriers before the source reads peers' rows (any mode)
         return self.world.combine(slot, w, dedup=self.dedup, out=out)
 
     __call__ = forward
+
+    def backward(self, grad_out: torch.Tensor) -> torch.Tensor:
+        """Gradients of the last forward: returns dL/dx; accumulates expert
+        weight grads (dw13, dw2, slot layout) and the router grad.
+
+        combine bwd (dedup broadcast of dL/dout, replaying the forward plan)
+        -> expert FFN bwd (tcgen05) -> dispatch bwd (dedup reduction) ->
+        softmax top-K bwd -> router GEMM bwd (cuBLAS).
+        """
+        if not self.grad or self._saved is None:
+            raise RuntimeError("HierMoELayer.backward needs grad=True and a forward first")
+        x, slot, w, ex = self._saved
+        dw = self.world.dispatch_grad(grad_out.contiguous(), slot, w, dedup=self.dedup)
+        p_ne, _ = self.world.buffer("n_e", 0)
+        for l in range(self.local):
+            rank = self.gpu_index * self.local + l
+            x_ptr, _ = self.world.buffer("xmaj", l)
+            gy_ptr, _ = self.world.buffer("gy", l)
+            gx_ptr, _ = self.world.buffer("gx", l)
+            expert_ffn_backward_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
+                                     self.e_loc, self.w13[l], self.w13t[l], self.w2t[l], gy_ptr,
+                                     self.hidden, self.inter, self.bwd, gx_ptr, self.dw13[l],
+                                     self.dw2[l])
+        dx = self.world.combine_grad(slot, dw, dedup=self.dedup)
+        # softmax over the K picks (renormalised) or over all experts
+        if self.renormalize:
+            dsel = w * (dw - (w * dw).sum(dim=1, keepdim=True))
+            dlogits = torch.zeros(x.shape[0], self.experts, device="cuda")
+            dlogits.scatter_(1, ex.long(), dsel)
+        else:
+            logits = x.float() @ self.w_router.T
+            p = torch.softmax(logits, dim=1)
+            dp = torch.zeros_like(p).scatter_(1, ex.long(), dw)
+            dlogits = p * (dp - (p * dp).sum(dim=1, keepdim=True))
+        self.dw_router += dlogits.T @ x.float()
+        return (dx.float() + dlogits @ self.w_router).to(x.dtype)
 
     def flops_per_forward(self) -> int:
         """Expert FFN flops of this GPU's last forward (6 * rows * hidden * inter)."""

@@ -1,0 +1,52 @@
+"""Full HierMoELayer backward (combine bwd -> tcgen05 FFN bwd -> dispatch bwd ->
+softmax top-K bwd -> router) vs torch autograd in fp32 on the same bf16
+inputs/weights and the same routing picks (bf16 tolerance)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dedup", ["all", "remote", "none"])
+def test_layer_backward_matches_autograd(hm, dedup):
+    from paper_2508_09591_b200.moe import HierMoELayer
+    G, E, K, M, I, T_r = 8, 16, 2, 256, 256, 32
+    layer = HierMoELayer(G, E, K, M, I, T_r, dedup=dedup, seed=9, grad=True)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(G * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    gout = torch.randn(G * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    out = layer(x)
+    dx = layer.backward(gout)
+    torch.cuda.synchronize()
+    layer.world.check_status()
+    _, slot, w, ex = layer._saved
+    # reference: same picks, fp32 autograd
+    xr = x.float().requires_grad_(True)
+    wr = layer.w_router.clone().requires_grad_(True)
+    nb = I // 128
+    w13 = layer.w13.reshape(E, nb, 2, 128, M).float()
+    w1 = w13[:, :, 0].reshape(E, I, M).clone().requires_grad_(True)
+    w3 = w13[:, :, 1].reshape(E, I, M).clone().requires_grad_(True)
+    w2 = layer.w2.reshape(E, M, I).float().clone().requires_grad_(True)
+    logits = xr @ wr.T
+    picked = torch.gather(logits, 1, ex.long())
+    gates = torch.softmax(picked, dim=1)
+    slots = slot.long()
+    y = torch.zeros_like(xr)
+    for k in range(K):
+        e = slots[:, k]
+        a = torch.einsum("tm,tim->ti", xr, w1[e])
+        b = torch.einsum("tm,tim->ti", xr, w3[e])
+        hcur = torch.nn.functional.silu(a) * b
+        y = y + gates[:, k:k + 1] * torch.einsum("ti,tmi->tm", hcur, w2[e])
+    y.backward(gout.float())
+    torch.testing.assert_close(out.float(), y.detach(), rtol=3e-2, atol=3e-2)
+    torch.testing.assert_close(dx.float(), xr.grad, rtol=3e-2, atol=3e-2)
+    torch.testing.assert_close(layer.dw_router, wr.grad, rtol=3e-2, atol=3e-2 * wr.grad.abs().max().item())
+    d13 = torch.stack([w1.grad.view(E, nb, 128, M), w3.grad.view(E, nb, 128, M)], dim=2).reshape(E, 2 * I, M)
+    got13 = layer.dw13.reshape(E, 2 * I, M).float()
+    torch.testing.assert_close(got13, d13, rtol=3e-2, atol=3e-2 * d13.abs().max().item())
+    got2 = layer.dw2.reshape(E, M, I).float()
+    torch.testing.assert_close(got2, w2.grad, rtol=3e-2, atol=3e-2 * w2.grad.abs().max().item())
+    layer.close()
