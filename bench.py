@@ -352,51 +352,64 @@ def main():
                "h2d_bytes_per_step": int(hx.numel() * 2 + hl.numel() * 4),
                "d2h_bytes_per_step": int(ho.numel() * 2)}
 
-    # full layer forward: gating + dispatch + tcgen05 SwiGLU experts + combine
+    # full layer forward + backward: gating, dedup dispatch, tcgen05 SwiGLU
+    # experts, combine; backward: combine-bwd, tcgen05 FFN bwd, dispatch-bwd
     layer_fwd = None
     if not args.no_layer:
         from paper_2508_09591_b200.moe import HierMoELayer
         inter = INTER[args.config]
+        ep.close()
         all_ep.close()
         raw_ep.close()
-        layer = HierMoELayer(G, E, K, M, inter, T_r, gpus=world, gpu_index=rank, dedup=MODE)
+        layer = HierMoELayer(G, E, K, M, inter, T_r, gpus=world, gpu_index=rank, dedup=MODE,
+                             grad=True, n_cap_rows=3 * T_r * K)
         lout = torch.empty(T, M, dtype=dtype, device="cuda")
+        gout = torch.randn(T, M, device="cuda", generator=gen).to(dtype)
         for _ in range(3):
             layer(x, out=lout)
+            layer.backward(gout)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         n_l = max(5, args.steps // 10)
-        tot = ffn = 0.0
+        acc = np.zeros(4)
         for _ in range(n_l):
             flush.zero_()
-            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-            e0.record()
-            slot_l, w_l, _ = layer.route(x)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            ev[0].record()
+            slot_l, w_l, ex_l = layer.route(x)
+            layer._saved = (x, slot_l, w_l, ex_l)
             layer.world.dispatch(x, slot_l, w_l, dedup=MODE)
-            e1.record()
+            ev[1].record()
             layer.experts_forward()
-            e2.record()
+            ev[2].record()
             layer.world.combine(slot_l, w_l, dedup=MODE, out=lout)
-            e3.record()
-            e3.synchronize()
-            tot += e0.elapsed_time(e3)
-            ffn += e1.elapsed_time(e2)
-        t = torch.tensor([tot / n_l, ffn / n_l], dtype=torch.float64, device="cuda")
+            ev[3].record()
+            layer.backward(gout)
+            ev[4].record()
+            ev[4].synchronize()
+            acc += [ev[0].elapsed_time(ev[3]), ev[1].elapsed_time(ev[2]),
+                    ev[3].elapsed_time(ev[4]), ev[0].elapsed_time(ev[4])]
+        t = torch.tensor(acc / n_l, dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         fl = layer.flops_per_forward()
         fl_t = torch.tensor([float(fl)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(fl_t, op=dist.ReduceOp.MAX)
-        ffn_tflops = fl_t.item() / (t[1].item() * 1e-3) / 1e12
+        fwd_ms, ffn_ms, bwd_ms, tot_ms = (float(v) for v in t.tolist())
+        ffn_tflops = fl_t.item() / (ffn_ms * 1e-3) / 1e12
         peak_tf = peaks.get("bf16_tflops", 1590.0)
-        layer_fwd = {"ms_per_step": t[0].item(), "tokens_per_s": tokens_total / (t[0].item() * 1e-3),
-                     "ffn_ms": t[1].item(), "ffn_flops_per_gpu": int(fl_t.item()),
+        layer_fwd = {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "fwd_bwd_ms": tot_ms,
+                     "fwd_tokens_per_s": tokens_total / (fwd_ms * 1e-3),
+                     "fwd_bwd_tokens_per_s": tokens_total / (tot_ms * 1e-3),
+                     "ffn_fwd_ms": ffn_ms, "ffn_flops_per_gpu": int(fl_t.item()),
                      "ffn_roofline": {"bound": "tensor", "achieved": ffn_tflops, "peak": peak_tf,
                                       "unit": "TFLOP/s", "frac": ffn_tflops / peak_tf,
-                                      "kernel": "k_grouped_gemm (tcgen05, 2 GEMMs)"},
-                     "inter": inter, "note": "router logits GEMM in torch (cuBLAS), rest ours"}
+                                      "kernel": "k_grouped_gemm (tcgen05, 2 GEMMs, fwd)"},
+                     "inter": inter,
+                     "note": "router logits GEMM and top-K softmax bwd in torch (cuBLAS); "
+                             "dispatch/combine/experts fwd+bwd are our kernels"}
         layer.close()
 
     cpu = None
