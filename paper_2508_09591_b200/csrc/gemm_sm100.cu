@@ -374,32 +374,46 @@ __global__ void k_group_layout(const int32_t* __restrict__ n_rows, int groups,
   col0[groups] = c;
 }
 
-// dst[c][col0_g + i] = src[row0_g + i][c] (bf16), zero padding columns
+// dst[c][col0_g + i] = src[row0_g + i][c] (bf16), zero padding columns.
+// 64x64 tiles through shared memory; each source row's destination column
+// is resolved once per tile.
 __global__ void k_transpose_groups(const __nv_bfloat16* __restrict__ src, int C,
                                    const int32_t* __restrict__ n_rows, int groups,
                                    const int32_t* __restrict__ row0, const int32_t* __restrict__ col0,
                                    __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
-  __shared__ __nv_bfloat16 tile[64][65];
+  __shared__ __nv_bfloat16 tile[64][66];
+  __shared__ int dcol[64];
   const int total = row0[groups];
   const int r_base = blockIdx.y * 64, c_base = blockIdx.x * 64;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   if (r_base < total) {
+    if (tid < 64) {
+      const int r = r_base + tid;
+      int g = 0;
+      if (r < total)
+        while (g + 1 < groups && row0[g + 1] <= r) ++g;
+      dcol[tid] = r < total ? col0[g] + (r - row0[g]) : -1;
+    }
+    // coalesced loads: each thread moves bf16 pairs
     for (int i = threadIdx.y; i < 64; i += blockDim.y) {
       const int r = r_base + i;
-      for (int j = threadIdx.x; j < 64; j += blockDim.x) {
-        const int c = c_base + j;
-        tile[i][j] = (r < total && c < C) ? src[(int64_t)r * C + c] : __float2bfloat16(0.f);
-      }
+      const int j = 2 * threadIdx.x;
+      const int c = c_base + j;
+      __nv_bfloat162 v = __floats2bfloat162_rn(0.f, 0.f);
+      if (r < total && c + 1 < C)
+        v = *reinterpret_cast<const __nv_bfloat162*>(src + (int64_t)r * C + c);
+      else if (r < total && c < C)
+        v.x = src[(int64_t)r * C + c];
+      tile[i][j] = v.x;
+      tile[i][j + 1] = v.y;
     }
     __syncthreads();
     for (int j = threadIdx.y; j < 64; j += blockDim.y) {
       const int c = c_base + j;
       if (c >= C) continue;
       for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-        const int r = r_base + i;
-        if (r >= total) continue;
-        int g = 0;
-        while (g + 1 < groups && row0[g + 1] <= r) ++g;
-        dst[(int64_t)c * ld_dst + col0[g] + (r - row0[g])] = tile[i][j];
+        const int dc = dcol[i];
+        if (dc >= 0) dst[(int64_t)c * ld_dst + dc] = tile[i][j];
       }
     }
   }
@@ -407,6 +421,7 @@ __global__ void k_transpose_groups(const __nv_bfloat16* __restrict__ src, int C,
   if (blockIdx.y == 0) {
     for (int g = 0; g < groups; ++g) {
       const int pad0 = col0[g] + n_rows[g], pad1 = col0[g + 1];
+      if (pad0 >= pad1) continue;
       for (int j = threadIdx.y; j < 64; j += blockDim.y) {
         const int c = c_base + j;
         if (c >= C) continue;
@@ -418,25 +433,29 @@ __global__ void k_transpose_groups(const __nv_bfloat16* __restrict__ src, int C,
 }
 
 // SwiGLU backward on 128-column gate/up interleaved pre-activations:
-// h = silu(a) u;  da = dh u silu'(a);  du = dh silu(a)
+// h = silu(a) u;  da = dh u silu'(a);  du = dh silu(a).  Two columns per thread.
 __global__ void k_swiglu_bwd(const __nv_bfloat16* __restrict__ g13, const __nv_bfloat16* __restrict__ dh,
                              const int32_t* __restrict__ row0, int groups, int inter,
                              __nv_bfloat16* __restrict__ dg13, __nv_bfloat16* __restrict__ h) {
-  const int64_t rows = row0[groups];
-  const int64_t n = rows * inter;
+  const int rows = row0[groups];
+  const int half = inter / 2;
+  const int64_t n = (int64_t)rows * half;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / inter;
-    const int j = (int)(i % inter);
-    const int b = j / 128, c = j % 128;
-    const int64_t ga = r * 2 * inter + 256 * b + c, gu = ga + 128;
-    const float a = __bfloat162float(g13[ga]), u = __bfloat162float(g13[gu]);
-    const float d = __bfloat162float(dh[i]);
-    const float sg = 1.f / (1.f + __expf(-a));
-    const float si = a * sg;
-    h[i] = __float2bfloat16(si * u);
-    dg13[gu] = __float2bfloat16(d * si);
-    dg13[ga] = __float2bfloat16(d * u * sg * (1.f + a * (1.f - sg)));
+    const int r = (int)(i / half);
+    const int j = 2 * (int)(i - (int64_t)r * half);
+    const int b = j >> 7, c = j & 127;
+    const int64_t ga = (int64_t)r * 2 * inter + 256 * b + c, gu = ga + 128;
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g13 + ga));
+    const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g13 + gu));
+    const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dh + (int64_t)r * inter + j));
+    const float s0 = 1.f / (1.f + __expf(-a.x)), s1 = 1.f / (1.f + __expf(-a.y));
+    const float si0 = a.x * s0, si1 = a.y * s1;
+    *reinterpret_cast<__nv_bfloat162*>(h + (int64_t)r * inter + j) = __floats2bfloat162_rn(si0 * u.x, si1 * u.y);
+    *reinterpret_cast<__nv_bfloat162*>(dg13 + gu) = __floats2bfloat162_rn(d.x * si0, d.y * si1);
+    *reinterpret_cast<__nv_bfloat162*>(dg13 + ga) =
+        __floats2bfloat162_rn(d.x * u.x * s0 * (1.f + a.x * (1.f - s0)),
+                              d.y * u.y * s1 * (1.f + a.y * (1.f - s1)));
   }
 }
 

@@ -20,6 +20,17 @@ from .migrate import ExpertStore
 from .routing import Placement
 
 
+class _tf32:
+    """Router GEMMs on TF32 tensor cores (cuBLAS); restores the global flag."""
+
+    def __enter__(self):
+        self.old = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+
+    def __exit__(self, *exc):
+        torch.backends.cuda.matmul.allow_tf32 = self.old
+
+
 class HierMoELayer:
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int, inter: int,
                  tokens_per_rank: int, gpus: int = 1, gpu_index: int = 0, group=None,
@@ -101,7 +112,8 @@ class HierMoELayer:
             self.refresh_transposed_weights()
 
     def route(self, x: torch.Tensor):
-        logits = x.float() @ self.w_router.T
+        with _tf32():
+            logits = x.float() @ self.w_router.T
         return route_topk(logits, self.top_k, self.expert_to_slot, self.renormalize)
 
     def experts_forward(self) -> None:
@@ -158,8 +170,9 @@ class HierMoELayer:
             p = torch.softmax(logits, dim=1)
             dp = torch.zeros_like(p).scatter_(1, ex.long(), dw)
             dlogits = p * (dp - (p * dp).sum(dim=1, keepdim=True))
-        self.dw_router += dlogits.T @ x.float()
-        return (dx.float() + dlogits @ self.w_router).to(x.dtype)
+        with _tf32():
+            self.dw_router += dlogits.T @ x.float()
+            return (dx.float() + dlogits @ self.w_router).to(x.dtype)
 
     def flops_per_forward(self) -> int:
         """Expert FFN flops of this GPU's last forward (6 * rows * hidden * inter)."""
