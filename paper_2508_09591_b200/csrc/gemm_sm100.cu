@@ -408,12 +408,22 @@ __global__ void k_transpose_groups(const __nv_bfloat16* __restrict__ src, int C,
       tile[i][j + 1] = v.y;
     }
     __syncthreads();
+    // each lane writes two consecutive source rows: one 4-B store when they
+    // land in adjacent destination columns (same group), else two 2-B stores
     for (int j = threadIdx.y; j < 64; j += blockDim.y) {
       const int c = c_base + j;
       if (c >= C) continue;
-      for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-        const int dc = dcol[i];
-        if (dc >= 0) dst[(int64_t)c * ld_dst + dc] = tile[i][j];
+      const int i = 2 * threadIdx.x;
+      const int d0 = dcol[i], d1 = dcol[i + 1];
+      __nv_bfloat16* row = dst + (int64_t)c * ld_dst;
+      if (d0 >= 0 && d1 == d0 + 1 && (d0 & 1) == 0) {
+        __nv_bfloat162 v;
+        v.x = tile[i][j];
+        v.y = tile[i + 1][j];
+        *reinterpret_cast<__nv_bfloat162*>(row + d0) = v;
+      } else {
+        if (d0 >= 0) row[d0] = tile[i][j];
+        if (d1 >= 0) row[d1] = tile[i + 1][j];
       }
     }
   }

@@ -648,7 +648,55 @@ struct Vec<float> {
   }
 };
 
-constexpr int kRedUnroll = 4;
+
+// dst row = sum_j ws[j] * row_j (fp32 accumulation in j order), rows in the
+// payload dtype.  Loads of up to kBatch source rows are issued before any
+// accumulation so each warp keeps kBatch * kU 16-B loads per lane in flight
+// (one memory round trip per 1 KB slice instead of one per source).
+constexpr int kBatch = 8, kU = 2;
+template <typename T>
+__device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
+                                                 int n, int64_t nvec, int lane, int4* dst) {
+  for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kU) {
+    float acc[kU][Vec<T>::N];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
+    for (int j0 = 0; j0 < n; j0 += kBatch) {
+      int4 buf[kBatch][kU];
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        if (j0 + b < n) {
+          const int4* src = reinterpret_cast<const int4*>(srcs[j0 + b]);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int64_t v = v0 + u * 32 + lane;
+            if (v < nvec) buf[b][u] = ld_v4(src + v);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b) {
+        if (j0 + b < n) {
+          const float wj = ws[j0 + b];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            float f[Vec<T>::N];
+            Vec<T>::to_f32(buf[b][u], f);
+#pragma unroll
+            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t v = v0 + u * 32 + lane;
+      if (v < nvec) st_na_v4(dst + v, Vec<T>::from_f32(acc[u]));
+    }
+  }
+}
 
 // reduce (dedup, destination side): partial[i] = sum_k w_k * y[epos_k] over the
 // row's local picks in k order, fp32 accumulation, stored in payload dtype.
@@ -670,46 +718,18 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
       ++d_loc;
     }
     const int dg = w.p * w.L + d_loc;
-    int ep = -1;
-    float wt = 0.f;
-    if (lane < w.K) {
-      RowMeta m = w.recv_meta[dg][r * w.K + lane];
-      ep = m.epos;
-      wt = grad ? 1.f : m.w;   // dispatch backward: unweighted sum of input grads
-    }
     const uint8_t* ysrc = grad ? w.gx[dg] : w.ymaj[dg];
-    int4* dst = reinterpret_cast<int4*>(w.comb[dg] + r * w.row_bytes);
-    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kRedUnroll) {
-      float acc[kRedUnroll][Vec<T>::N];
-#pragma unroll
-      for (int u = 0; u < kRedUnroll; ++u)
-#pragma unroll
-        for (int j = 0; j < Vec<T>::N; ++j) acc[u][j] = 0.f;
-      for (int k = 0; k < w.K; ++k) {
-        int e = __shfl_sync(0xffffffffu, ep, k);
-        float wk = __shfl_sync(0xffffffffu, wt, k);
-        if (e < 0) continue;
-        const int4* src = reinterpret_cast<const int4*>(ysrc + (int64_t)e * w.row_bytes);
-        int4 buf[kRedUnroll];
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) {
-          int64_t v = v0 + u * 32 + lane;
-          if (v < nvec) buf[u] = ld_nc_v4(src + v);
-        }
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) {
-          float f[Vec<T>::N];
-          Vec<T>::to_f32(buf[u], f);
-#pragma unroll
-          for (int j = 0; j < Vec<T>::N; ++j) acc[u][j] = fmaf(wk, f[j], acc[u][j]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kRedUnroll; ++u) {
-        int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) st_na_v4(dst + v, Vec<T>::from_f32(acc[u]));
-      }
+    const uint8_t* srcs[kMaxK];
+    float ws[kMaxK];
+    int n = 0;
+    for (int k = 0; k < w.K; ++k) {
+      RowMeta m = w.recv_meta[dg][r * w.K + k];
+      if (m.epos < 0) continue;
+      srcs[n] = ysrc + (int64_t)m.epos * w.row_bytes;
+      ws[n] = grad ? 1.f : m.w;   // dispatch backward: unweighted sum of input grads
+      ++n;
     }
+    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(w.comb[dg] + r * w.row_bytes));
   }
 }
 
@@ -759,36 +779,7 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
         ++n;
       }
     }
-    int4* dst = reinterpret_cast<int4*>(out + t * w.row_bytes);
-    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kRedUnroll) {
-      float acc[kRedUnroll][Vec<T>::N];
-#pragma unroll
-      for (int u = 0; u < kRedUnroll; ++u)
-#pragma unroll
-        for (int j = 0; j < Vec<T>::N; ++j) acc[u][j] = 0.f;
-      for (int j = 0; j < n; ++j) {
-        const int4* src = reinterpret_cast<const int4*>(srcs[j]);
-        int4 buf[kRedUnroll];
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) {
-          int64_t v = v0 + u * 32 + lane;
-          if (v < nvec) buf[u] = ld_v4(src + v);
-        }
-        const float wj = ws[j];
-#pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) {
-          float f[Vec<T>::N];
-          Vec<T>::to_f32(buf[u], f);
-#pragma unroll
-          for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kRedUnroll; ++u) {
-        int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) st_na_v4(dst + v, Vec<T>::from_f32(acc[u]));
-      }
-    }
+    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
   }
 }
 
