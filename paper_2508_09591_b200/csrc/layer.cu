@@ -650,10 +650,10 @@ struct Vec<float> {
 
 
 // dst row = sum_j ws[j] * row_j (fp32 accumulation in j order), rows in the
-// payload dtype.  Loads of up to kBatch source rows are issued before any
-// accumulation so each warp keeps kBatch * kU 16-B loads per lane in flight
-// (one memory round trip per 1 KB slice instead of one per source).
-constexpr int kBatch = 8, kU = 2;
+// payload dtype; 4 x 16-B loads per lane per source in flight (measured: a
+// batched variant holding 8 sources' loads in registers lost more to
+// occupancy than it gained in memory-level parallelism).
+constexpr int kU = 4;
 template <typename T>
 __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
                                                  int n, int64_t nvec, int lane, int4* dst) {
@@ -663,31 +663,21 @@ __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, con
     for (int u = 0; u < kU; ++u)
 #pragma unroll
       for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
-    for (int j0 = 0; j0 < n; j0 += kBatch) {
-      int4 buf[kBatch][kU];
+    for (int j = 0; j < n; ++j) {
+      const int4* src = reinterpret_cast<const int4*>(srcs[j]);
+      int4 buf[kU];
 #pragma unroll
-      for (int b = 0; b < kBatch; ++b) {
-        if (j0 + b < n) {
-          const int4* src = reinterpret_cast<const int4*>(srcs[j0 + b]);
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int64_t v = v0 + u * 32 + lane;
-            if (v < nvec) buf[b][u] = ld_v4(src + v);
-          }
-        }
+      for (int u = 0; u < kU; ++u) {
+        const int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = ld_v4(src + v);
       }
+      const float wj = ws[j];
 #pragma unroll
-      for (int b = 0; b < kBatch; ++b) {
-        if (j0 + b < n) {
-          const float wj = ws[j0 + b];
+      for (int u = 0; u < kU; ++u) {
+        float f[Vec<T>::N];
+        Vec<T>::to_f32(buf[u], f);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            float f[Vec<T>::N];
-            Vec<T>::to_f32(buf[b][u], f);
-#pragma unroll
-            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
-          }
-        }
+        for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
       }
     }
 #pragma unroll
