@@ -204,7 +204,7 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
 // in registers (insertion with an early-out against the K-th value; strict >
 // keeps the lower index on ties because columns arrive in ascending order).
 template <int K>
-__global__ void __launch_bounds__(256) k_route_lane(const float* __restrict__ logits, int64_t T,
+__global__ void __launch_bounds__(256, 3) k_route_lane(const float* __restrict__ logits, int64_t T,
                                                     int E, const int32_t* __restrict__ e2s,
                                                     int renorm, int32_t* __restrict__ slot_ids,
                                                     float* __restrict__ weights,
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) k_route_lane(const float* __restrict__ lo
     }
     for (int c0 = 0; c0 < E; c0 += 32) {
       const int col = c0 + lane;
-#pragma unroll 8
+#pragma unroll 4
       for (int r = 0; r < 32; ++r) {
         int64_t tr = base + r;
         tl[r][lane] = (tr < T && col < E) ? __ldg(logits + tr * E + col) : -INFINITY;
@@ -654,9 +654,53 @@ struct Vec<float> {
 // batched variant holding 8 sources' loads in registers lost more to
 // occupancy than it gained in memory-level parallelism).
 constexpr int kU = 4;
+
+// compile-time row width: VPL 16-B vectors per lane (row = 32 * VPL vectors)
+template <typename T, int VPL>
+__device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* srcs, const float* ws,
+                                                       int n, int lane, int4* dst) {
+  constexpr int CH = VPL < kU ? VPL : kU;
+  static_assert(VPL % CH == 0, "row width must be a multiple of the chunk");
+#pragma unroll 1
+  for (int c = 0; c < VPL; c += CH) {
+    float acc[CH][Vec<T>::N];
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+#pragma unroll
+      for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
+    const int off = c * 32 + lane;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      const int4* src = reinterpret_cast<const int4*>(srcs[j]) + off;
+      int4 buf[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) buf[u] = ld_v4(src + u * 32);
+      const float wj = ws[j];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        float f[Vec<T>::N];
+        Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+        for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) st_na_v4(dst + off + u * 32, Vec<T>::from_f32(acc[u]));
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
                                                  int n, int64_t nvec, int lane, int4* dst) {
+  switch (nvec) {   // common row widths take the unrolled path
+    case 32: return weighted_row_sum_fixed<T, 1>(srcs, ws, n, lane, dst);
+    case 64: return weighted_row_sum_fixed<T, 2>(srcs, ws, n, lane, dst);
+    case 128: return weighted_row_sum_fixed<T, 4>(srcs, ws, n, lane, dst);
+    case 256: return weighted_row_sum_fixed<T, 8>(srcs, ws, n, lane, dst);
+    case 512: return weighted_row_sum_fixed<T, 16>(srcs, ws, n, lane, dst);
+    case 896: return weighted_row_sum_fixed<T, 28>(srcs, ws, n, lane, dst);
+    default: break;
+  }
   for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kU) {
     float acc[kU][Vec<T>::N];
 #pragma unroll
