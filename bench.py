@@ -200,7 +200,7 @@ def main():
     ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
     raw_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
     all_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
-    MODE = "remote"   # dedup rows across GPUs; same-GPU ranks go expert-major directly
+    MODE = "gpu"   # one row per (token, remote GPU); same-GPU ranks go expert-major directly
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # 256 MB > L2
 
     def prime(w_, dedup):
@@ -281,11 +281,12 @@ def main():
     src_rows = cnt[mine]
     rows_dedup_out = int(src_rows[:, :G].sum())             # "all" dedup rows
     rows_raw_out = int(src_rows[:, G:].sum())               # one per selection
-    rem_dedup = int(src_rows[:, :G][:, dest_gpu != rank].sum())
+    gcnt = ep.gpu_counts()[mine]                            # [L, P] rows per (src, gpu)
+    rem_dedup = int(np.delete(gcnt, rank, axis=1).sum())    # per-GPU dedup rows that cross NVLink
+    rem_rank_dedup = int(src_rows[:, :G][:, dest_gpu != rank].sum())
     rem_raw = int(src_rows[:, G:][:, slot_gpu != rank].sum())
     loc_direct = int(src_rows[:, G:][:, slot_gpu == rank].sum())
-    recv = ep.rows_received()
-    R_in = int(recv[:, 0].sum())                            # remote dedup rows received
+    R_in = ep.rows_received_gpu()                           # per-GPU dedup rows received
     src_gpu = np.arange(G) // L
     N_rem_in = int(cnt[src_gpu != rank][:, G:][:, slot_gpu == rank].sum())
     alg = {
@@ -442,6 +443,7 @@ def main():
                                 "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_all.tolist())}},
             "comm_bytes": {"dedup_rows_out": rows_dedup_out, "raw_rows_out": rows_raw_out,
                            "dedup_remote_bytes": rem_dedup * rb, "raw_remote_bytes": rem_raw * rb,
+                           "rank_dedup_remote_bytes": rem_rank_dedup * rb,
                            "row_ratio_raw_over_dedup": rows_raw_out / max(1, rows_dedup_out),
                            "remote_byte_ratio_raw_over_dedup":
                                (rem_raw / rem_dedup) if rem_dedup else None},

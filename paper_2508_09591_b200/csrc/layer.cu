@@ -64,6 +64,14 @@ struct WorldDev {
   uint8_t* xmaj[kMaxRanks];
   uint8_t* ymaj[kMaxRanks];
   uint8_t* comb[kMaxRanks];
+  uint8_t* ret[kMaxRanks];    // per source rank: [G][T_r][M] pre-reduced rows pushed back
+  // mode 3 (dedup per destination GPU): per GPU q a receive buffer + meta
+  // (epos = local rank * N_cap + expert-major row), per source rank a return
+  // buffer [P][T_r][M]
+  uint8_t* recv_g[kMaxRanks];
+  RowMeta* meta_g[kMaxRanks];
+  uint8_t* ret_g[kMaxRanks];
+  int64_t Rg_cap;
   uint8_t* gy[kMaxRanks];     // backward: grad of expert outputs (expert-major), or null
   uint8_t* gx[kMaxRanks];     // backward: grad of expert inputs (expert-major), or null
   float* gw[kMaxRanks];       // backward: gate grads of dedup picks [R_cap][K], or null
@@ -78,6 +86,10 @@ __device__ __forceinline__ int dest_of(const WorldDev& w, int s, int e) {
 // per-step offsets computed by k_notify (local, not symmetric)
 struct Offsets {
   int32_t off[kMaxRanks][kMaxRanks];  // [local src][dest]  receive offset
+  int32_t offd[kMaxRanks][kMaxRanks + 1];  // [local dest][src] receive offset (+ total)
+  int32_t off_g[kMaxRanks][kMaxRanks];  // [local src][dest gpu] mode-3 receive offset
+  int32_t offd_g[kMaxRanks + 1];        // [src] mode-3 offset of src's rows on this GPU
+  int32_t R_g;                          // mode-3 rows received by this GPU
   int32_t R[kMaxRanks];               // rows received per local dest
   int32_t Nd[kMaxRanks];              // expert-major rows per local dest
 };
@@ -290,10 +302,12 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
                                                  int32_t* __restrict__ rank_d,
                                                  int32_t* __restrict__ rank_e,
                                                  unsigned long long* __restrict__ hitmask,
+                                                 int32_t* __restrict__ rank_g,
                                                  int* __restrict__ status) {
   const WorldDev& w = *wp;
-  extern __shared__ int32_t s_cnt[];  // [kPlanWarps][G+E] counters, then [kPlanWarps][E] lane masks
-  const int C = w.G + w.E;
+  // [kPlanWarps][G+E+P] counters (ranks, slots, GPUs), then [kPlanWarps][E] lane masks
+  extern __shared__ int32_t s_cnt[];
+  const int C = w.G + w.E + w.P;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s_loc = blockIdx.y;
   const int chunk = blockIdx.x;
@@ -318,14 +332,20 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
     }
   }
   // destination ranks within the warp
-  int rd[kMaxRanks > 32 ? 32 : kMaxRanks];
-  (void)rd;
   const unsigned lt = (1u << lane) - 1u;
   for (int d = 0; d < w.G; ++d) {
     unsigned b = __ballot_sync(0xffffffffu, (hit >> d) & 1ull);
     if ((hit >> d) & 1ull) rank_d[t * w.G + d] = __popc(b & lt);
     else if (valid) rank_d[t * w.G + d] = -1;
     if (lane == 0) s_cnt[warp * C + d] = __popc(b);
+  }
+  // destination GPUs (mode 3): hit if any of the GPU's L ranks is hit
+  const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
+  for (int q = 0; q < w.P; ++q) {
+    const bool hq = (hit >> (q * w.L)) & gmask;
+    unsigned b = __ballot_sync(0xffffffffu, hq);
+    if (valid) rank_g[t * w.P + q] = hq ? __popc(b & lt) : -1;
+    if (lane == 0) s_cnt[warp * C + w.G + w.E + q] = __popc(b);
   }
   // slot ranks within the warp: a lane mask per slot in shared memory; the
   // rank of my pick = earlier lanes in that slot's mask (stable, O(K))
@@ -355,6 +375,8 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
   if (valid) {
     for (int d = 0; d < w.G; ++d)
       if ((hit >> d) & 1ull) rank_d[t * w.G + d] += s_cnt[warp * C + d];
+    for (int q = 0; q < w.P; ++q)
+      if ((hit >> (q * w.L)) & gmask) rank_g[t * w.P + q] += s_cnt[warp * C + w.G + w.E + q];
 #pragma unroll
     for (int k = 0; k < kMaxK; ++k)
       if (k < w.K) rank_e[t * w.K + k] = S[k] >= 0 ? re[k] + s_cnt[warp * C + w.G + S[k]] : -1;
@@ -375,7 +397,7 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  int32_t* __restrict__ n_e, int mode,
                                                  unsigned long long epoch, int* __restrict__ status) {
   const WorldDev& w = *wp;
-  const int C = w.G + w.E;
+  const int C = w.G + w.E + w.P;
   // mode 2 (dedup across GPUs only): sources on the destination's own GPU
   // write expert-major rows directly and occupy no receive rows
   auto ships = [&](int src, int dst) {
@@ -419,6 +441,34 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
     for (int src = 0; src < sg; ++src)
       if (ships(src, d)) o += cnt[(int64_t)src * C + d];
     offs->off[s_loc][d] = o;
+  }
+  for (int i = threadIdx.x; i < w.L * (w.G + 1); i += blockDim.x) {
+    const int d_loc = i / (w.G + 1), src = i % (w.G + 1);
+    const int dg = w.p * w.L + d_loc;
+    int o = 0;
+    for (int s2 = 0; s2 < src; ++s2)
+      if (ships(s2, dg)) o += cnt[(int64_t)s2 * C + dg];
+    offs->offd[d_loc][src] = o;
+  }
+  // mode 3: GPU-level offsets (only sources on other GPUs ship)
+  const int CG = w.G + w.E;
+  for (int i = threadIdx.x; i < w.L * w.P; i += blockDim.x) {
+    const int s_loc = i / w.P, q = i % w.P;
+    const int sg = w.p * w.L + s_loc;
+    int o = 0;
+    for (int src = 0; src < sg; ++src)
+      if (src / w.L != q) o += cnt[(int64_t)src * C + CG + q];
+    offs->off_g[s_loc][q] = o;
+  }
+  for (int src = threadIdx.x; src <= w.G; src += blockDim.x) {
+    int o = 0;
+    for (int s2 = 0; s2 < src; ++s2)
+      if (s2 / w.L != w.p) o += cnt[(int64_t)s2 * C + CG + w.p];
+    offs->offd_g[src] = o;
+    if (src == w.G) {
+      offs->R_g = o;
+      if (mode == 3 && o > w.Rg_cap) atomicExch(status, 2);
+    }
   }
   for (int d_loc = threadIdx.x; d_loc < w.L; d_loc += blockDim.x) {
     int dg = w.p * w.L + d_loc;
@@ -470,10 +520,13 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               const int32_t* __restrict__ eoff, int nchunks,
                                               int mode, int32_t* __restrict__ gpos,
                                               int32_t* __restrict__ epos_out,
+                                              const int32_t* __restrict__ rank_g,
+                                              int32_t* __restrict__ gpos_g,
                                               int* __restrict__ status) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
-  const int C = w.G + w.E;
+  const int C = w.G + w.E + w.P;
+  const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
   const int64_t nvec = w.row_bytes / 16;
   const int64_t T = (int64_t)w.L * w.T_r;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -503,21 +556,49 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
     int ndst = 0;
     int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
     uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    // direct expert-major rows: every pick (mode 0) or picks on this GPU (mode 2)
+    // direct expert-major rows: every pick (mode 0) or picks on this GPU (modes 2, 3)
     if (mode != 1) {
       for (int k = 0; k < w.K; ++k) {
         int e = __shfl_sync(0xffffffffu, my_e, k);
         int ep = __shfl_sync(0xffffffffu, my_ep, k);
         if (e < 0 || ep < 0) continue;
         const int d = e / w.E_loc;
-        if (mode == 2 && d / w.L != w.p) continue;
+        if (mode >= 2 && d / w.L != w.p) continue;
         dst_base[ndst] = w.xmaj[d];
         dst_row[ndst] = ep;
         ++ndst;
       }
     }
+    // mode 3: one row per (token, other GPU hit); meta carries, per pick on
+    // that GPU, its local rank's expert-major row (l * N_cap + epos)
+    if (mode == 3) {
+      for (int q = 0; q < w.P; ++q) {
+        if (q == w.p) continue;
+        if (!((hit >> (q * w.L)) & gmask)) {
+          if (lane == 0) gpos_g[t * w.P + q] = -1;
+          continue;
+        }
+        const int64_t g = (int64_t)offs->off_g[s_loc][q] + coff[w.G + w.E + q] + rank_g[t * w.P + q];
+        if (lane == 0) gpos_g[t * w.P + q] = (int32_t)g;
+        if (g >= w.Rg_cap) {
+          if (lane == 0) atomicExch(status, 2);
+          continue;
+        }
+        if (lane < w.K) {
+          RowMeta m;
+          const int dr = my_e >= 0 ? my_e / w.E_loc : -1;
+          m.epos = (dr >= 0 && dr / w.L == q && my_ep >= 0)
+                       ? (int32_t)((dr - q * w.L) * w.N_cap + my_ep) : -1;
+          m.w = my_w;
+          w.meta_g[q][g * w.K + lane] = m;
+        }
+        dst_base[ndst] = w.recv_g[q];
+        dst_row[ndst] = g;
+        ++ndst;
+      }
+    }
     // dedup rows: every hit destination (mode 1) or destinations on other GPUs (mode 2)
-    if (mode != 0) {
+    if (mode == 1 || mode == 2) {
       for (int d = 0; d < w.G; ++d) {
         if (!((hit >> d) & 1ull)) continue;
         if (mode == 2 && d / w.L == w.p) {
@@ -736,7 +817,8 @@ __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, con
 // row's local picks in k order, fp32 accumulation, stored in payload dtype.
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
-                                                const Offsets* __restrict__ offs, int grad) {
+                                                const Offsets* __restrict__ offs, int grad,
+                                                int push) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
@@ -763,7 +845,14 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
       ws[n] = grad ? 1.f : m.w;   // dispatch backward: unweighted sum of input grads
       ++n;
     }
-    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(w.comb[dg] + r * w.row_bytes));
+    uint8_t* out_row = w.comb[dg] + r * w.row_bytes;
+    if (push) {   // store straight into the source rank's return buffer (NVLink if remote)
+      int src = 0;
+      while (src + 1 < w.G && offs->offd[d_loc][src + 1] <= r) ++src;
+      const int64_t pos = r - offs->offd[d_loc][src];
+      out_row = w.ret[src] + ((int64_t)dg * w.T_r + pos) * w.row_bytes;
+    }
+    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
   }
 }
 
@@ -776,7 +865,10 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
                                                 const unsigned long long* __restrict__ hitmask,
                                                 const int32_t* __restrict__ gpos,
                                                 const int32_t* __restrict__ epos, int mode,
-                                                int grad, uint8_t* __restrict__ out) {
+                                                int grad, int push,
+                                                const Offsets* __restrict__ offs,
+                                                const int32_t* __restrict__ gpos_g,
+                                                uint8_t* __restrict__ out) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
@@ -794,26 +886,117 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
         int ep = epos[t * w.K + k];
         if (e < 0 || ep < 0) continue;
         const int d = e / w.E_loc;
-        if (mode == 2 && d / w.L != w.p) continue;
+        if (mode >= 2 && d / w.L != w.p) continue;
         srcs[n] = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
         ws[n] = grad ? 1.f : wts[t * w.K + k];
         ++n;
       }
     }
+    // mode 3: pre-reduced rows of the other GPUs hit, pushed into our return buffer
+    if (mode == 3) {
+      const unsigned long long hit = hitmask[t];
+      const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
+      const int s_loc = (int)(t / w.T_r);
+      for (int q = 0; q < w.P; ++q) {
+        if (q == w.p || !((hit >> (q * w.L)) & gmask)) continue;
+        const int g = gpos_g[t * w.P + q];
+        if (g < 0) continue;
+        const int64_t pos = g - offs->off_g[s_loc][q];
+        srcs[n] = w.ret_g[w.p * w.L + s_loc] + ((int64_t)q * w.T_r + pos) * w.row_bytes;
+        ws[n] = 1.f;
+        ++n;
+      }
+    }
     // pre-reduced partial rows of dedup destinations, ascending rank
-    if (mode != 0) {
+    if (mode == 1 || mode == 2) {
       unsigned long long hit = hitmask[t];
       for (int d = 0; d < w.G; ++d) {
         if (!((hit >> d) & 1ull)) continue;
         if (mode == 2 && d / w.L == w.p) continue;
         int g = gpos[t * w.G + d];
         if (g < 0 || g >= w.R_cap) continue;
-        srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
+        if (push) {
+          const int s_loc = (int)(t / w.T_r);
+          const int64_t pos = g - offs->off[s_loc][d];
+          srcs[n] = w.ret[w.p * w.L + s_loc] + ((int64_t)d * w.T_r + pos) * w.row_bytes;
+        } else {
+          srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
+        }
         ws[n] = 1.f;
         ++n;
       }
     }
     weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
+  }
+}
+
+// mode 3 destination side: rows received by this GPU (one per token x GPU)
+// re-expanded into the local ranks' expert-major rows (xmaj is [L][N_cap]
+// contiguous, meta epos = l * N_cap + row) ...
+__global__ void __launch_bounds__(256) k_expand_g(const WorldDev* __restrict__ wp,
+                                                  const Offsets* __restrict__ offs) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = offs->R_g;
+  uint8_t* xbase = w.xmaj[w.p * w.L];
+  const RowMeta* meta = w.meta_g[w.p];
+  for (int64_t r = warp; r < total; r += nw) {
+    int ep = -1;
+    if (lane < w.K) ep = meta[r * w.K + lane].epos;
+    const int4* src = reinterpret_cast<const int4*>(w.recv_g[w.p] + r * w.row_bytes);
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+      int4 buf[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = ld_nc_v4(src + v);
+      }
+      for (int k = 0; k < w.K; ++k) {
+        int e = __shfl_sync(0xffffffffu, ep, k);
+        if (e < 0) continue;
+        int4* dst = reinterpret_cast<int4*>(xbase + (int64_t)e * w.row_bytes);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          int64_t v = v0 + u * 32 + lane;
+          if (v < nvec) st_na_v4(dst + v, buf[u]);
+        }
+      }
+    }
+  }
+}
+
+// ... and pre-reduced (sum_k w_k y_k over this GPU's picks), pushed straight
+// into the source rank's return buffer slot [this GPU][position]
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_g(const WorldDev* __restrict__ wp,
+                                                  const Offsets* __restrict__ offs, int grad) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = offs->R_g;
+  const uint8_t* ybase = grad ? w.gx[w.p * w.L] : w.ymaj[w.p * w.L];
+  const RowMeta* meta = w.meta_g[w.p];
+  for (int64_t r = warp; r < total; r += nw) {
+    const uint8_t* srcs[kMaxK];
+    float ws[kMaxK];
+    int n = 0;
+    for (int k = 0; k < w.K; ++k) {
+      RowMeta m = meta[r * w.K + k];
+      if (m.epos < 0) continue;
+      srcs[n] = ybase + (int64_t)m.epos * w.row_bytes;
+      ws[n] = grad ? 1.f : m.w;
+      ++n;
+    }
+    int src = 0;
+    while (src + 1 < w.G && offs->offd_g[src + 1] <= r) ++src;
+    const int64_t pos = r - offs->offd_g[src];
+    uint8_t* out_row = w.ret_g[src] + ((int64_t)w.p * w.T_r + pos) * w.row_bytes;
+    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
   }
 }
 
@@ -1020,7 +1203,8 @@ struct hm_world {
   uint8_t* sym = nullptr;  // symmetric allocation (this GPU)
   size_t sym_bytes = 0;
   size_t off_recv_x = 0, off_meta = 0, off_xmaj = 0, off_ymaj = 0, off_comb = 0, off_counts = 0,
-         off_flags = 0, off_gy = 0, off_gx = 0, off_gw = 0;
+         off_flags = 0, off_gy = 0, off_gx = 0, off_gw = 0, off_ret = 0, off_recv_g = 0,
+         off_meta_g = 0, off_ret_g = 0;
   bool grad = false;
   std::vector<void*> opened;  // peer bases opened via IPC
   // local scratch
@@ -1031,6 +1215,8 @@ struct hm_world {
   unsigned long long* hitmask = nullptr;
   int32_t* gpos = nullptr;
   int32_t* epos = nullptr;
+  int32_t* rank_g = nullptr;   // mode 3: within-chunk rank per destination GPU
+  int32_t* gpos_g = nullptr;   // mode 3: receive row per (token, destination GPU)
   Offsets* offs = nullptr;
   int32_t* eoff = nullptr;
   int32_t* n_e = nullptr;
@@ -1076,6 +1262,8 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
     h.xmaj[d] = base + w->off_xmaj + (size_t)l * h.N_cap * h.row_bytes;
     h.ymaj[d] = base + w->off_ymaj + (size_t)l * h.N_cap * h.row_bytes;
     h.comb[d] = base + w->off_comb + (size_t)l * h.R_cap * h.row_bytes;
+    h.ret[d] = base + w->off_ret + (size_t)l * h.G * h.T_r * h.row_bytes;
+    h.ret_g[d] = base + w->off_ret_g + (size_t)l * h.P * h.T_r * h.row_bytes;
     h.gy[d] = w->grad ? base + w->off_gy + (size_t)l * h.N_cap * h.row_bytes : nullptr;
     h.gx[d] = w->grad ? base + w->off_gx + (size_t)l * h.N_cap * h.row_bytes : nullptr;
     h.gw[d] = w->grad ? reinterpret_cast<float*>(base + w->off_gw) + (size_t)l * h.R_cap * h.K
@@ -1083,6 +1271,8 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
     h.counts[d] = reinterpret_cast<int32_t*>(base + w->off_counts);
     h.flags[d] = reinterpret_cast<unsigned long long*>(base + w->off_flags);
   }
+  h.recv_g[q] = base + w->off_recv_g;
+  h.meta_g[q] = reinterpret_cast<RowMeta*>(base + w->off_meta_g);
 }
 
 HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32_t experts,
@@ -1123,7 +1313,12 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   h.R_cap = (int64_t)(relay_groups ? relay_groups : ranks) * tokens_per_rank;
   int64_t worst = (int64_t)ranks * tokens_per_rank * (top_k < h.E_loc ? top_k : h.E_loc);
   h.N_cap = relay_groups ? 1 : (n_cap_rows > 0 && n_cap_rows < worst ? n_cap_rows : worst);
-  HM_CHECK_ARG(h.R_cap < (1ll << 31) && h.N_cap < (1ll << 31), "row capacity exceeds int32");
+  // mode 3 receive capacity: every token of every rank on another GPU
+  h.Rg_cap = (int64_t)(ranks - h.L) * tokens_per_rank;
+  if (h.Rg_cap < 1 || relay_groups) h.Rg_cap = 1;
+  HM_CHECK_ARG(h.R_cap < (1ll << 31) && h.N_cap < (1ll << 31) && h.Rg_cap < (1ll << 31) &&
+                   (int64_t)h.L * h.N_cap < (1ll << 31),
+               "row capacity exceeds int32");
   cudaGetDevice(&w->device);
 
   size_t o = 0;
@@ -1132,13 +1327,17 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   w->off_xmaj = o;   o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
   w->off_ymaj = o;   o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
   w->off_comb = o;   o = align_up(o + (size_t)h.L * h.R_cap * h.row_bytes, 256);
+  w->off_ret = o;    o = align_up(o + (size_t)(h.U1 ? 0 : h.L * h.G * h.T_r) * h.row_bytes, 256);
+  w->off_recv_g = o; o = align_up(o + (size_t)h.Rg_cap * h.row_bytes, 256);
+  w->off_meta_g = o; o = align_up(o + (size_t)h.Rg_cap * h.K * sizeof(RowMeta), 256);
+  w->off_ret_g = o;  o = align_up(o + (size_t)(h.U1 ? 0 : h.L * h.P * h.T_r) * h.row_bytes, 256);
   w->grad = (flags & 1) != 0;   // backward buffers gy, gx, gw
   if (w->grad) {
     w->off_gy = o; o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
     w->off_gx = o; o = align_up(o + (size_t)h.L * h.N_cap * h.row_bytes, 256);
     w->off_gw = o; o = align_up(o + (size_t)h.L * h.R_cap * h.K * 4, 256);
   }
-  w->off_counts = o; o = align_up(o + (size_t)h.G * (h.G + h.E) * 4, 256);
+  w->off_counts = o; o = align_up(o + (size_t)h.G * (h.G + h.E + h.P) * 4, 256);
   w->off_flags = o;  o = align_up(o + (size_t)h.P * 8, 256);
   w->sym_bytes = o;
   int st;
@@ -1147,7 +1346,9 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   HM_TRY(cudaMemset(w->sym + w->off_counts, 0, w->sym_bytes - w->off_counts));
   w->nchunks = (int)((tokens_per_rank + kChunk - 1) / kChunk);
   const int64_t T = (int64_t)h.L * h.T_r;
-  HM_TRY(cudaMalloc(&w->chunk_cnt, (size_t)h.L * w->nchunks * (h.G + h.E) * 4));
+  HM_TRY(cudaMalloc(&w->chunk_cnt, (size_t)h.L * w->nchunks * (h.G + h.E + h.P) * 4));
+  HM_TRY(cudaMalloc(&w->rank_g, (size_t)T * h.P * 4));
+  HM_TRY(cudaMalloc(&w->gpos_g, (size_t)T * h.P * 4));
   HM_TRY(cudaMalloc(&w->rank_d, (size_t)T * h.G * 4));
   HM_TRY(cudaMalloc(&w->rank_e, (size_t)T * h.K * 4));
   HM_TRY(cudaMalloc(&w->hitmask, (size_t)T * 8));
@@ -1181,6 +1382,8 @@ HM_API int hm_world_destroy(hm_world* w) {
   cudaFree(w->hitmask);
   cudaFree(w->gpos);
   cudaFree(w->epos);
+  cudaFree(w->rank_g);
+  cudaFree(w->gpos_g);
   cudaFree(w->offs);
   cudaFree(w->eoff);
   cudaFree(w->n_e);
@@ -1259,7 +1462,9 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
 HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
                        int32_t mode, void* stream) {
   HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
-  HM_CHECK_ARG(mode >= 0 && mode <= 2, "hm_dispatch: mode must be 0 (raw), 1 (dedup), 2 (dedup across GPUs)");
+  HM_CHECK_ARG(mode >= 0 && mode <= 3,
+               "hm_dispatch: mode must be 0 (raw), 1 (dedup per rank), 2 (dedup per remote rank), "
+               "3 (dedup per remote GPU)");
   if (mode) HM_CHECK_ARG(wts, "hm_dispatch: dedup modes need gate weights");
   HM_CHECK_ARG(!w->h.U1 || mode == 1, "hm_dispatch: a relay world ships dedup rows (mode 1)");
   w->last_mode = mode;
@@ -1270,12 +1475,12 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
   dim3 grid(w->nchunks, h.L);
-  size_t smem = (size_t)kPlanWarps * (h.G + 2 * h.E) * 4;
+  size_t smem = (size_t)kPlanWarps * (h.G + 2 * h.E + h.P) * 4;
   if (smem > 48 * 1024)
     HM_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {SegScope sc(w, kSegPlan, s);
   k_plan<<<grid, kChunk, smem, s>>>(w->d, ids, w->nchunks, w->chunk_cnt, w->rank_d, w->rank_e,
-                                    w->hitmask, w->status);
+                                    w->hitmask, w->rank_g, w->status);
   }
   HM_LAUNCHED();
   {SegScope sc(w, kSegNotify, s);
@@ -1288,7 +1493,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   {SegScope sc(w, kSegPack, s);
   k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
                                 w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
-                                w->gpos, w->epos, w->status);
+                                w->gpos, w->epos, w->rank_g, w->gpos_g, w->status);
   }
   HM_LAUNCHED();
   if (h.P > 1) {
@@ -1303,9 +1508,13 @@ HM_API int hm_expand(hm_world* w, void* stream) {
   HM_CHECK_ARG(w, "hm_expand: null world");
   if (w->h.P == 1 && w->last_mode == 2) return 0;  // every rank shares this GPU: nothing received
   if (w->h.U1) return 0;                             // relay rows are re-dispatched, not expanded
+  if (w->last_mode == 3 && w->h.P == 1) return 0;    // one GPU: every row went direct
   int blocks = kSMs * 8;
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
-  k_expand<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
+  if (w->last_mode == 3)
+    k_expand_g<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
+  else
+    k_expand<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
   HM_LAUNCHED();
   return 0;
 }
@@ -1315,16 +1524,27 @@ HM_API int hm_expand(hm_world* w, void* stream) {
 HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t mode, void* out,
                       void* stream) {
   HM_CHECK_ARG(w && out, "hm_combine: null argument");
-  HM_CHECK_ARG(mode >= 0 && mode <= 2, "hm_combine: mode must be 0, 1 or 2");
+  HM_CHECK_ARG(mode >= 0 && mode <= 3, "hm_combine: mode must be 0..3");
   const int dedup = mode;
+  // non-relay worlds push pre-reduced rows to the source (stores over NVLink);
+  // a relay's rows are produced by phase 2 and pulled by the source
+  const int push = w->h.U1 ? 0 : 1;
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
-  if (dedup && !(h.P == 1 && mode == 2) && !h.U1) {   // relay: rows arrive pre-reduced
+  if (mode == 3 && h.P > 1) {
     SegScope sc(w, kSegReduce, s);
     if (h.elem == 2)
-      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
+      k_reduce_g<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
     else
-      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
+      k_reduce_g<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
+    HM_LAUNCHED();
+  }
+  if (dedup && mode != 3 && !(h.P == 1 && mode == 2) && !h.U1) {   // relay: rows arrive pre-reduced
+    SegScope sc(w, kSegReduce, s);
+    if (h.elem == 2)
+      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0, 1);
+    else
+      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0, 1);
     HM_LAUNCHED();
   }
   if (mode != 1) HM_CHECK_ARG(wts && ids, "hm_combine: raw/hybrid combine needs ids and weights");
@@ -1338,10 +1558,10 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   SegScope sc(w, kSegGather, s);
   if (h.elem == 2)
     k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos,
-                                                   mode, 0, (uint8_t*)out);
+                                                   mode, 0, push, w->offs, w->gpos_g, (uint8_t*)out);
   else
     k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode,
-                                           0, (uint8_t*)out);
+                                           0, push, w->offs, w->gpos_g, (uint8_t*)out);
   HM_LAUNCHED();
   return 0;
 }
@@ -1373,7 +1593,7 @@ HM_API int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void**
     case 2: *ptr = h.xmaj[d]; *bytes = h.N_cap * h.row_bytes; break;
     case 3: *ptr = h.ymaj[d]; *bytes = h.N_cap * h.row_bytes; break;
     case 4: *ptr = h.comb[d]; *bytes = h.R_cap * h.row_bytes; break;
-    case 5: *ptr = h.counts[d]; *bytes = (int64_t)h.G * (h.G + h.E) * 4; break;
+    case 5: *ptr = h.counts[d]; *bytes = (int64_t)h.G * (h.G + h.E + h.P) * 4; break;
     case 6: *ptr = w->gpos; *bytes = T * h.G * 4; break;
     case 7: *ptr = w->epos; *bytes = T * h.K * 4; break;
     case 8: *ptr = w->hitmask; *bytes = T * 8; break;
@@ -1383,6 +1603,9 @@ HM_API int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void**
     case 11: *ptr = w->status; *bytes = 16; break;
     case 12: *ptr = h.gy[d]; *bytes = w->grad ? h.N_cap * h.row_bytes : 0; break;
     case 13: *ptr = h.gx[d]; *bytes = w->grad ? h.N_cap * h.row_bytes : 0; break;
+    case 14: *ptr = h.recv_g[h.p]; *bytes = h.Rg_cap * h.row_bytes; break;
+    case 15: *ptr = w->gpos_g; *bytes = T * h.P * 4; break;
+    case 16: *ptr = reinterpret_cast<uint8_t*>(w->offs) + offsetof(Offsets, R_g); *bytes = 4; break;
     default: hm::set_error("hm_world_buffer: unknown kind %d", kind); return hm::kInvalid;
   }
   return 0;
@@ -1451,6 +1674,7 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
   HM_CHECK_ARG(w && g && ids && wts && dw, "hm_dispatch_grad: null argument");
   HM_CHECK_ARG(w->grad, "hm_dispatch_grad: world created without backward buffers");
   HM_CHECK_ARG(mode == w->last_mode, "hm_dispatch_grad: mode differs from the forward's");
+  HM_CHECK_ARG(mode <= 2, "hm_dispatch_grad: backward supports modes 0..2");
   HM_CHECK_ARG(!w->h.U1, "hm_dispatch_grad: relay worlds have no backward");
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
@@ -1488,9 +1712,9 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   const WorldDev& h = w->h;
   if (mode != 0 && !(h.P == 1 && mode == 2)) {
     if (h.elem == 2)
-      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1);
+      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1, 1);
     else
-      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1);
+      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1, 1);
     HM_LAUNCHED();
   }
   if (h.P > 1) {
@@ -1501,10 +1725,10 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   int blocks = grid_for(T, 8, kSMs * 8);
   if (h.elem == 2)
     k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, nullptr, w->hitmask, w->gpos, w->epos,
-                                                   mode, 1, (uint8_t*)dx);
+                                                   mode, 1, 1, w->offs, w->gpos_g, (uint8_t*)dx);
   else
     k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, nullptr, w->hitmask, w->gpos, w->epos, mode, 1,
-                                           (uint8_t*)dx);
+                                           1, w->offs, w->gpos_g, (uint8_t*)dx);
   HM_LAUNCHED();
   k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode, dw);
   HM_LAUNCHED();

@@ -33,7 +33,8 @@ from . import _lib
 from ._lib import ptr, stream_ptr
 
 _KIND = {"recv_x": 0, "recv_meta": 1, "xmaj": 2, "ymaj": 3, "comb": 4, "counts": 5, "gpos": 6,
-         "epos": 7, "hitmask": 8, "offsets": 9, "n_e": 10, "status": 11, "gy": 12, "gx": 13}
+         "epos": 7, "hitmask": 8, "offsets": 9, "n_e": 10, "status": 11, "gy": 12, "gx": 13,
+         "recv_g": 14, "gpos_g": 15, "rows_g": 16}
 
 _STATUS = {2: "row capacity overflow", 3: "peer barrier timeout", 4: "slot id out of range"}
 
@@ -42,12 +43,17 @@ _STATUS = {2: "row capacity overflow", 3: "peer barrier timeout", 4: "slot id ou
 # ranks on the same GPU (the full dedup copy list); "remote" dedup rows only
 # across GPUs -- ranks sharing a GPU exchange through HBM without a link to
 # save bytes on, so their rows go straight to expert-major positions.
-MODES = {"none": 0, "all": 1, "remote": 2}
+# "gpu" dedups per (token, destination GPU): one row crosses NVLink per
+# remote GPU a token hits, and the receiving GPU re-expands it into its local
+# ranks' expert rows -- the HierMoE principle (dedup at the level that owns a
+# link) for ranks hosted several per GPU; with one rank per GPU it equals
+# "remote".
+MODES = {"none": 0, "all": 1, "remote": 2, "gpu": 3}
 
 
 def transport_mode(dedup) -> int:
     if dedup is True:
-        return MODES["remote"]
+        return MODES["gpu"]
     if dedup is False or dedup is None:
         return MODES["none"]
     if dedup not in MODES:
@@ -251,8 +257,18 @@ class EPWorld:
 
     def counts(self) -> np.ndarray:
         """[G, G+E] count matrix: h[s, d] dedup rows, then c[s, e] selections."""
+        return self._count_matrix()[:, :self.ranks + self.experts]
+
+    def gpu_counts(self) -> np.ndarray:
+        """[G, P]: rows source rank s sends to GPU q under per-GPU dedup."""
+        return self._count_matrix()[:, self.ranks + self.experts:]
+
+    def rows_received_gpu(self) -> int:
+        return int(self.read("rows_g", 0, torch.int32).cpu().numpy()[0])
+
+    def _count_matrix(self) -> np.ndarray:
         c = self.read("counts", 0, torch.int32).cpu().numpy()
-        return c.reshape(self.ranks, self.ranks + self.experts)
+        return c.reshape(self.ranks, self.ranks + self.experts + self.gpus)
 
     def rows_received(self) -> np.ndarray:
         """Per local rank: (dedup rows received R, expert-major rows N)."""

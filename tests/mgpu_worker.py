@@ -35,6 +35,20 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
     ep.check_status()
     cnt = ep.counts()
     assert np.array_equal(cnt[:, :G], plan.h), "dedup counts"
+    # per-GPU dedup: rows per (source rank, GPU) == dedup counts of the [P, L]
+    # hierarchy's level-1 cut restricted to each source (group_reduce at U[1]=P)
+    gh = plan.hit.reshape(-1, world, L).any(axis=2)
+    src_of = np.arange(G * T_r) // T_r
+    want_g = np.stack([gh[src_of == s_].sum(axis=0) for s_ in range(G)])
+    assert np.array_equal(ep.gpu_counts(), want_g), "gpu counts"
+    if dedup == "gpu":
+        rows = np.nonzero(gh[:, rank] & ((src_of // L) != rank))[0]   # copy order
+        rg = ep.rows_received_gpu()
+        assert rg == rows.size
+        if rg:
+            rx = ep.read("recv_g", 0, dtype, rg * M).view(rg, M).cpu()
+            xb0 = x.view(torch.int16) if dtype == torch.bfloat16 else x.view(torch.int32)
+            assert torch.equal(rx.view(xb0.dtype), xb0[rows]), "recv_g rows"
     assert np.array_equal(cnt[:, G:], plan.c), "slot counts"
     rows = ep.rows_received()
     e_loc = E // G
@@ -133,7 +147,7 @@ def main():
     cases = [(8, 16, 2, 256, 256, torch.float32), (8, 128, 8, 2048, 128, torch.bfloat16),
              (8, 256, 8, 512, 96, torch.bfloat16)]
     for i, (G, E, K, M, T_r, dt) in enumerate(cases):
-        for dedup in ("all", "remote", "none"):
+        for dedup in ("all", "remote", "gpu", "none"):
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
             dist.barrier()
     run_migrate(rank, world)

@@ -75,7 +75,7 @@ def _apply_experts(world, plan, E, dtype):
 
 
 @pytest.mark.parametrize("name", list(CONFIGS))
-@pytest.mark.parametrize("dedup", ["all", "remote", "none"])
+@pytest.mark.parametrize("dedup", ["all", "remote", "gpu", "none"])
 def test_dispatch_combine_parity(hm, name, dedup):
     from paper_2508_09591_b200.layer import route_topk
     G, E, K, M, T_r, dtype = CONFIGS[name]
