@@ -380,11 +380,11 @@ def main():
             ev[0].record()
             slot_l, w_l, ex_l = layer.route(x)
             layer._saved = (x, slot_l, w_l, ex_l)
-            layer.world.dispatch(x, slot_l, w_l, dedup=MODE)
+            layer.world.dispatch(x, slot_l, w_l, dedup=layer.dedup)
             ev[1].record()
             layer.experts_forward()
             ev[2].record()
-            layer.world.combine(slot_l, w_l, dedup=MODE, out=lout)
+            layer.world.combine(slot_l, w_l, dedup=layer.dedup, out=lout)
             ev[3].record()
             layer.backward(gout)
             ev[4].record()
@@ -408,7 +408,7 @@ def main():
                      "ffn_roofline": {"bound": "tensor", "achieved": ffn_tflops, "peak": peak_tf,
                                       "unit": "TFLOP/s", "frac": ffn_tflops / peak_tf,
                                       "kernel": "k_grouped_gemm (tcgen05, 2 GEMMs, fwd)"},
-                     "inter": inter,
+                     "inter": inter, "transport": layer.dedup,
                      "note": "router logits GEMM and top-K softmax bwd in torch (cuBLAS); "
                              "dispatch/combine/experts fwd+bwd are our kernels"}
         layer.close()

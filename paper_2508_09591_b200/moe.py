@@ -46,7 +46,7 @@ class HierMoELayer:
         self.e_loc = experts // ranks
         # backward supports the per-rank transports; True means per-GPU dedup
         # for inference and per-remote-rank dedup when gradients are needed
-        self.dedup = "remote" if (grad and dedup is True) else dedup
+        self.dedup = "remote" if (grad and (dedup is True or dedup == "gpu")) else dedup
         self.renormalize = renormalize
         self.world = EPWorld(ranks, experts, top_k, hidden, tokens_per_rank,
                              dtype=torch.bfloat16, gpus=gpus, gpu_index=gpu_index, group=group,
