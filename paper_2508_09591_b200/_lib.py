@@ -56,6 +56,7 @@ _SIGS = {
     "hm_world_buffer": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_void_p), POINTER(c_int64)]),
     "hm_world_info": (c_int32, [c_void_p, c_void_p]),
     "hm_world_barrier": (c_int32, [c_void_p, c_void_p]),
+    "hm_world_set_option": (c_int32, [c_void_p, c_int32, c_int32]),
     "hm_memcpy": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     "hm_world_set_timing": (c_int32, [c_void_p, c_int32]),
     "hm_world_timings": (c_int32, [c_void_p, c_void_p, c_int32]),

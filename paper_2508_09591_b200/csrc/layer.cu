@@ -858,6 +858,64 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
 
 // gather (source side).  dedup: out[t] = sum over hit destinations d
 // (ascending) of comb[d][gpos[t,d]]; raw: out[t] = sum_k w_k * ymaj[dest][epos].
+// Source rows of token t in summation order (shared by both gather kernels).
+__device__ __forceinline__ int gather_sources(const WorldDev& w, int64_t t, const int32_t* ids,
+                                              const float* wts, const unsigned long long* hitmask,
+                                              const int32_t* gpos, const int32_t* epos, int mode,
+                                              int grad, int push, const Offsets* offs,
+                                              const int32_t* gpos_g, const uint8_t** srcs,
+                                              float* ws) {
+  int n = 0;
+  // weighted expert rows: every pick (mode 0) or picks on this GPU (modes 2, 3), k order
+  if (mode != 1) {
+    for (int k = 0; k < w.K; ++k) {
+      int e = ids[t * w.K + k];
+      int ep = epos[t * w.K + k];
+      if (e < 0 || ep < 0) continue;
+      const int d = e / w.E_loc;
+      if (mode >= 2 && d / w.L != w.p) continue;
+      srcs[n] = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
+      ws[n] = grad ? 1.f : wts[t * w.K + k];
+      ++n;
+    }
+  }
+  // mode 3: pre-reduced rows of the other GPUs hit, pushed into our return buffer
+  if (mode == 3) {
+    const unsigned long long hit = hitmask[t];
+    const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
+    const int s_loc = (int)(t / w.T_r);
+    for (int q = 0; q < w.P; ++q) {
+      if (q == w.p || !((hit >> (q * w.L)) & gmask)) continue;
+      const int g = gpos_g[t * w.P + q];
+      if (g < 0) continue;
+      const int64_t pos = g - offs->off_g[s_loc][q];
+      srcs[n] = w.ret_g[w.p * w.L + s_loc] + ((int64_t)q * w.T_r + pos) * w.row_bytes;
+      ws[n] = 1.f;
+      ++n;
+    }
+  }
+  // pre-reduced partial rows of dedup destinations, ascending rank
+  if (mode == 1 || mode == 2) {
+    unsigned long long hit = hitmask[t];
+    for (int d = 0; d < w.G; ++d) {
+      if (!((hit >> d) & 1ull)) continue;
+      if (mode == 2 && d / w.L == w.p) continue;
+      int g = gpos[t * w.G + d];
+      if (g < 0 || g >= w.R_cap) continue;
+      if (push) {
+        const int s_loc = (int)(t / w.T_r);
+        const int64_t pos = g - offs->off[s_loc][d];
+        srcs[n] = w.ret[w.p * w.L + s_loc] + ((int64_t)d * w.T_r + pos) * w.row_bytes;
+      } else {
+        srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
+      }
+      ws[n] = 1.f;
+      ++n;
+    }
+  }
+  return n;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
                                                 const int32_t* __restrict__ ids,
@@ -876,57 +934,146 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t t = warp; t < ntok; t += nw) {
-    int n = 0;
     const uint8_t* srcs[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
     float ws[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    // weighted expert rows: every pick (mode 0) or picks on this GPU (mode 2), k order
-    if (mode != 1) {
-      for (int k = 0; k < w.K; ++k) {
-        int e = ids[t * w.K + k];
-        int ep = epos[t * w.K + k];
-        if (e < 0 || ep < 0) continue;
-        const int d = e / w.E_loc;
-        if (mode >= 2 && d / w.L != w.p) continue;
-        srcs[n] = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
-        ws[n] = grad ? 1.f : wts[t * w.K + k];
-        ++n;
-      }
-    }
-    // mode 3: pre-reduced rows of the other GPUs hit, pushed into our return buffer
-    if (mode == 3) {
-      const unsigned long long hit = hitmask[t];
-      const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
-      const int s_loc = (int)(t / w.T_r);
-      for (int q = 0; q < w.P; ++q) {
-        if (q == w.p || !((hit >> (q * w.L)) & gmask)) continue;
-        const int g = gpos_g[t * w.P + q];
-        if (g < 0) continue;
-        const int64_t pos = g - offs->off_g[s_loc][q];
-        srcs[n] = w.ret_g[w.p * w.L + s_loc] + ((int64_t)q * w.T_r + pos) * w.row_bytes;
-        ws[n] = 1.f;
-        ++n;
-      }
-    }
-    // pre-reduced partial rows of dedup destinations, ascending rank
-    if (mode == 1 || mode == 2) {
-      unsigned long long hit = hitmask[t];
-      for (int d = 0; d < w.G; ++d) {
-        if (!((hit >> d) & 1ull)) continue;
-        if (mode == 2 && d / w.L == w.p) continue;
-        int g = gpos[t * w.G + d];
-        if (g < 0 || g >= w.R_cap) continue;
-        if (push) {
-          const int s_loc = (int)(t / w.T_r);
-          const int64_t pos = g - offs->off[s_loc][d];
-          srcs[n] = w.ret[w.p * w.L + s_loc] + ((int64_t)d * w.T_r + pos) * w.row_bytes;
-        } else {
-          srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
-        }
-        ws[n] = 1.f;
-        ++n;
-      }
-    }
+    const int n = gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push, offs,
+                                 gpos_g, srcs, ws);
     weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
+  }
+}
+
+// TMA variant: one lane per warp issues cp.async.bulk loads of every source's
+// 1 KB chunk into a shared-memory stage (mbarrier transaction count), the
+// warp accumulates from shared memory while the next chunk's loads are in
+// flight (2 stages).  Bytes in flight no longer cost registers.  Used when
+// the sources are local (modes 2/3, or any mode on one GPU) and rows are a
+// multiple of 1 KB; tokens with more than kTmaSrc sources take the register
+// path.
+constexpr int kTmaWarps = 6, kTmaStages = 2, kTmaSrc = 16, kTmaChunk = 1024;
+constexpr size_t kTmaSmem = (size_t)kTmaWarps * kTmaStages * kTmaSrc * kTmaChunk;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+    k_gather_tma(const WorldDev* __restrict__ wp, const int32_t* __restrict__ ids,
+                 const float* __restrict__ wts, const unsigned long long* __restrict__ hitmask,
+                 const int32_t* __restrict__ gpos, const int32_t* __restrict__ epos, int mode,
+                 int grad, int push, const Offsets* __restrict__ offs,
+                 const int32_t* __restrict__ gpos_g, uint8_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t tma_smem[];
+  __shared__ uint64_t bars[kTmaWarps][kTmaStages];
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint8_t* stage_base = tma_smem + (size_t)wid * kTmaStages * kTmaSrc * kTmaChunk;
+  if (lane == 0)
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&bars[wid][st], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int chunks = (int)(w.row_bytes / kTmaChunk);
+  const int64_t ntok = (int64_t)w.L * w.T_r;
+  const int64_t gw = (int64_t)blockIdx.x * kTmaWarps + wid;
+  const int64_t nw = (int64_t)gridDim.x * kTmaWarps;
+  const uint8_t* srcs[2][kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+  float ws[2][kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+  int nsrc[2] = {0, 0};
+  uint32_t phase[kTmaStages] = {0, 0};
+  // item i = (token slot i / chunks, chunk i % chunks) of this warp's tokens
+  auto token_of = [&](int64_t i) { return gw + (i / chunks) * nw; };
+  auto issue = [&](int64_t i, int st) {
+    const int64_t t = token_of(i);
+    const int slot = (int)((i / chunks) & 1);
+    const int c = (int)(i % chunks);
+    const int n = nsrc[slot];
+    if (lane == 0 && n <= kTmaSrc) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[wid][st], (uint32_t)(n * kTmaChunk));
+      for (int j = 0; j < n; ++j)
+        bulk_load(stage_base + ((size_t)st * kTmaSrc + j) * kTmaChunk,
+                  srcs[slot][j] + (size_t)c * kTmaChunk, kTmaChunk, &bars[wid][st]);
+    }
+    (void)t;
+  };
+  auto build = [&](int64_t t, int slot) {
+    nsrc[slot] = t < ntok ? gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push,
+                                           offs, gpos_g, srcs[slot], ws[slot])
+                          : 0;
+  };
+  const int64_t my_tokens = gw < ntok ? (ntok - gw + nw - 1) / nw : 0;
+  const int64_t items = my_tokens * chunks;
+  if (items == 0) return;
+  build(token_of(0), 0);
+  issue(0, 0);
+  for (int64_t i = 0; i < items; ++i) {
+    const int st = (int)(i & 1);
+    const int64_t t = token_of(i);
+    const int slot = (int)((i / chunks) & 1);
+    const int c = (int)(i % chunks);
+    // prefetch the next item (building the next token's source list first)
+    if (i + 1 < items) {
+      if ((i + 1) % chunks == 0) build(token_of(i + 1), (int)(((i + 1) / chunks) & 1));
+      issue(i + 1, st ^ 1);
+    }
+    const int n = nsrc[slot];
+    int4* dst = reinterpret_cast<int4*>(out + t * w.row_bytes + (size_t)c * kTmaChunk);
+    constexpr int VPC = kTmaChunk / 16 / 32;   // 16-B vectors per lane per chunk (2)
+    if (n <= kTmaSrc) {
+      mbar_wait(&bars[wid][st], phase[st]);
+      phase[st] ^= 1;
+      float acc[VPC][Vec<T>::N];
+#pragma unroll
+      for (int u = 0; u < VPC; ++u)
+#pragma unroll
+        for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const int4* sm = reinterpret_cast<const int4*>(stage_base + ((size_t)st * kTmaSrc + j) * kTmaChunk);
+        const float wj = ws[slot][j];
+#pragma unroll
+        for (int u = 0; u < VPC; ++u) {
+          float f[Vec<T>::N];
+          Vec<T>::to_f32(sm[u * 32 + lane], f);
+#pragma unroll
+          for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < VPC; ++u) st_na_v4(dst + u * 32 + lane, Vec<T>::from_f32(acc[u]));
+    } else if (c == 0) {
+      // too many sources for a stage: whole row on the register path
+      weighted_row_sum<T>(srcs[slot], ws[slot], n, w.row_bytes / 16, lane,
+                          reinterpret_cast<int4*>(out + t * w.row_bytes));
+    }
+    __syncwarp();
   }
 }
 
@@ -1224,6 +1371,7 @@ struct hm_world {
   unsigned long long epoch = 0;
   bool peers_ready = false;
   int last_mode = 0;
+  bool tma_gather = true;   // hm_world_set_option(w, 0, 0) selects the register gather
   // optional per-kernel CUDA-event timing (segments recorded on the launch stream)
   bool timing = false;
   cudaEvent_t ev[2 * 16];
@@ -1556,6 +1704,25 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, kSMs * 8);
   SegScope sc(w, kSegGather, s);
+  // local sources: modes 2/3 (pushed returns + same-GPU rows) or one GPU
+  const bool local_src = (mode >= 2 || h.P == 1) && !(mode == 1 && !push);
+  if (local_src && w->tma_gather && h.row_bytes % kTmaChunk == 0) {
+    if (h.elem == 2) {
+      HM_CUDA(cudaFuncSetAttribute(k_gather_tma<__nv_bfloat16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      k_gather_tma<__nv_bfloat16><<<kSMs, kTmaWarps * 32, kTmaSmem, s>>>(
+          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
+          (uint8_t*)out);
+    } else {
+      HM_CUDA(cudaFuncSetAttribute(k_gather_tma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kTmaSmem));
+      k_gather_tma<float><<<kSMs, kTmaWarps * 32, kTmaSmem, s>>>(
+          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
+          (uint8_t*)out);
+    }
+    HM_LAUNCHED();
+    return 0;
+  }
   if (h.elem == 2)
     k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos,
                                                    mode, 0, push, w->offs, w->gpos_g, (uint8_t*)out);
@@ -1732,5 +1899,13 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   HM_LAUNCHED();
   k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode, dw);
   HM_LAUNCHED();
+  return 0;
+}
+
+// runtime options: 0 = use the TMA gather (1, default) or the register gather (0)
+HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
+  HM_CHECK_ARG(w, "hm_world_set_option: null world");
+  HM_CHECK_ARG(option == 0, "hm_world_set_option: unknown option %d", option);
+  w->tma_gather = value != 0;
   return 0;
 }

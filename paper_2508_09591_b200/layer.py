@@ -224,6 +224,10 @@ class EPWorld:
     def barrier(self) -> None:
         _lib.call("hm_world_barrier", self._h, stream_ptr())
 
+    def set_tma_gather(self, enabled: bool) -> None:
+        """Source-side sum via TMA bulk copies (default) or register loads."""
+        _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
+
     def _check_rows(self, x, ids):
         t = self.local * self.tokens_per_rank
         if x.shape != (t, self.hidden) or x.dtype != self.dtype or not x.is_contiguous():

@@ -115,9 +115,14 @@ def test_dispatch_combine_parity(hm, name, dedup):
             r = int(rn[d, 0])
             rx = world.read("recv_x", d, dtype, r * M).view(r, M).cpu()
             assert torch.equal(rx.view(xb.dtype), xb[plan.recv_rows(d)])
-    # combine with a stand-in expert y = x * scale[slot]
+    # combine with a stand-in expert y = x * scale[slot]; both gather variants
     _apply_experts(world, plan, E, dtype)
+    world.set_tma_gather(False)
+    out_reg = world.combine(slot, w, dedup=dedup).clone()
+    world.set_tma_gather(True)
     out = world.combine(slot, w, dedup=dedup)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out_reg)      # same summation order -> identical bits
     torch.cuda.synchronize()
     world.check_status()
     sc = _scale(E).numpy()
