@@ -267,9 +267,9 @@ def main():
         _lib.call("hm_world_set_timing", w_._h, 0)
         return acc / n
 
-    ep.set_tma_gather(False)
-    seg_reg = seg_times(ep, MODE)
     ep.set_tma_gather(True)
+    seg_tma = seg_times(ep, MODE)
+    ep.set_tma_gather(False)
     seg = seg_times(ep, MODE)
     seg_raw = seg_times(raw_ep, "none")
     seg_all = seg_times(all_ep, "all")
@@ -437,7 +437,7 @@ def main():
             "combine_us": 1e3 * (seg_ms["reduce"] + seg_ms["barrier2"] + seg_ms["gather"]),
             "kernel_ms": {k: round(v, 4) for k, v in seg_ms.items()},
             "kernels": per_kernel,
-            "gather_register_variant_ms": round(float(seg_reg[SEGMENTS.index("gather")]), 4),
+            "gather_tma_variant_ms": round(float(seg_tma[SEGMENTS.index("gather")]), 4),
             "transport": MODE,
             "nodedup": {"ms_per_step": ms_raw, "value": tokens_total / (ms_raw * 1e-3),
                         "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_raw.tolist())},

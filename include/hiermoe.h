@@ -74,7 +74,9 @@ int hm_swap_tensor(const int64_t* base, const int64_t* sel, const int64_t* hitse
 /* Smooth-max cost matrix (gamma and exact max) for dimension *dim_dev (or
  * dim_host when dim_dev is NULL), numpy rounding order.  Replaces
  * smooth_max/_smooth_max_lastaxis (swap.py:35-57) and cost_matrix
- * (swap.py:180-206). */
+ * (swap.py:180-206).  The inter_* arrays hold depth - 1 entries and the
+ * intra_* arrays depth entries; cuts past the dimension evaluated are not
+ * read by the kernel and may be passed as a null tensor with 0 groups. */
 int hm_swap_cost(const int64_t* const* inter_z, const int32_t* inter_groups,
                  const int32_t* inter_part, const double* a_inter, const double* b_inter,
                  const int64_t* const* intra_z, const int32_t* intra_groups,

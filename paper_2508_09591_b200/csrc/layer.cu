@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 #include <string.h>
 #include <stdlib.h>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -731,16 +732,20 @@ struct Vec<float> {
 
 
 // dst row = sum_j ws[j] * row_j (fp32 accumulation in j order), rows in the
-// payload dtype; 4 x 16-B loads per lane per source in flight (measured: a
-// batched variant holding 8 sources' loads in registers lost more to
-// occupancy than it gained in memory-level parallelism).
+// payload dtype.  The source table (srcs/ws) lives in shared memory (one slice
+// per warp; broadcast reads) so it costs neither registers nor a local-memory
+// stack frame.  Fixed-width rows: each lane owns kCh 16-B vectors per chunk
+// and the loads of kSu sources are issued before the first is accumulated
+// (kCh * kSu * 16 B in flight per lane; registers stay under the 3-CTA/SM
+// budget of __launch_bounds__(256, 3)).
 constexpr int kU = 4;
+constexpr int kCh = 2, kSu = 4;
 
 // compile-time row width: VPL 16-B vectors per lane (row = 32 * VPL vectors)
 template <typename T, int VPL>
 __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* srcs, const float* ws,
                                                        int n, int lane, int4* dst) {
-  constexpr int CH = VPL < kU ? VPL : kU;
+  constexpr int CH = VPL < kCh ? VPL : kCh;
   static_assert(VPL % CH == 0, "row width must be a multiple of the chunk");
 #pragma unroll 1
   for (int c = 0; c < VPL; c += CH) {
@@ -751,18 +756,28 @@ __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* src
       for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
     const int off = c * 32 + lane;
 #pragma unroll 1
-    for (int j = 0; j < n; ++j) {
-      const int4* src = reinterpret_cast<const int4*>(srcs[j]) + off;
-      int4 buf[CH];
+    for (int j0 = 0; j0 < n; j0 += kSu) {
+      int4 buf[kSu][CH];
 #pragma unroll
-      for (int u = 0; u < CH; ++u) buf[u] = ld_v4(src + u * 32);
-      const float wj = ws[j];
+      for (int s = 0; s < kSu; ++s) {
+        if (j0 + s < n) {
+          const int4* src = reinterpret_cast<const int4*>(srcs[j0 + s]) + off;
 #pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        float f[Vec<T>::N];
-        Vec<T>::to_f32(buf[u], f);
+          for (int u = 0; u < CH; ++u) buf[s][u] = ld_v4(src + u * 32);
+        }
+      }
 #pragma unroll
-        for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
+      for (int s = 0; s < kSu; ++s) {
+        if (j0 + s < n) {
+          const float wj = ws[j0 + s];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            float f[Vec<T>::N];
+            Vec<T>::to_f32(buf[s][u], f);
+#pragma unroll
+            for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
+          }
+        }
       }
     }
 #pragma unroll
@@ -770,18 +785,11 @@ __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* src
   }
 }
 
+// VPL > 0: compile-time row width (one kernel instantiation per width, so the
+// register allocation is not shared with the generic loop); VPL == 0: any width
 template <typename T>
-__device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
-                                                 int n, int64_t nvec, int lane, int4* dst) {
-  switch (nvec) {   // common row widths take the unrolled path
-    case 32: return weighted_row_sum_fixed<T, 1>(srcs, ws, n, lane, dst);
-    case 64: return weighted_row_sum_fixed<T, 2>(srcs, ws, n, lane, dst);
-    case 128: return weighted_row_sum_fixed<T, 4>(srcs, ws, n, lane, dst);
-    case 256: return weighted_row_sum_fixed<T, 8>(srcs, ws, n, lane, dst);
-    case 512: return weighted_row_sum_fixed<T, 16>(srcs, ws, n, lane, dst);
-    case 896: return weighted_row_sum_fixed<T, 28>(srcs, ws, n, lane, dst);
-    default: break;
-  }
+__device__ __forceinline__ void weighted_row_sum_any(const uint8_t* const* srcs, const float* ws,
+                                                     int n, int64_t nvec, int lane, int4* dst) {
   for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kU) {
     float acc[kU][Vec<T>::N];
 #pragma unroll
@@ -813,13 +821,24 @@ __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, con
   }
 }
 
+template <typename T, int VPL>
+__device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
+                                                 int n, int64_t nvec, int lane, int4* dst) {
+  if constexpr (VPL > 0)
+    weighted_row_sum_fixed<T, VPL>(srcs, ws, n, lane, dst);
+  else
+    weighted_row_sum_any<T>(srcs, ws, n, nvec, lane, dst);
+}
+
 // reduce (dedup, destination side): partial[i] = sum_k w_k * y[epos_k] over the
 // row's local picks in k order, fp32 accumulation, stored in payload dtype.
-template <typename T>
-__global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
-                                                const Offsets* __restrict__ offs, int grad,
-                                                int push) {
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256, 3) k_reduce(const WorldDev* __restrict__ wp,
+                                                   const Offsets* __restrict__ offs, int grad,
+                                                   int push) {
   const WorldDev& w = *wp;
+  __shared__ const uint8_t* s_src[8][kMaxK];
+  __shared__ float s_w[8][kMaxK];
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -835,8 +854,9 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
     }
     const int dg = w.p * w.L + d_loc;
     const uint8_t* ysrc = grad ? w.gx[dg] : w.ymaj[dg];
-    const uint8_t* srcs[kMaxK];
-    float ws[kMaxK];
+    __syncwarp();
+    const uint8_t** srcs = s_src[threadIdx.x >> 5];
+    float* ws = s_w[threadIdx.x >> 5];
     int n = 0;
     for (int k = 0; k < w.K; ++k) {
       RowMeta m = w.recv_meta[dg][r * w.K + k];
@@ -852,7 +872,8 @@ __global__ void __launch_bounds__(256) k_reduce(const WorldDev* __restrict__ wp,
       const int64_t pos = r - offs->offd[d_loc][src];
       out_row = w.ret[src] + ((int64_t)dg * w.T_r + pos) * w.row_bytes;
     }
-    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
+    __syncwarp();
+    weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
   }
 }
 
@@ -916,8 +937,10 @@ __device__ __forceinline__ int gather_sources(const WorldDev& w, int64_t t, cons
   return n;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
+constexpr int kMaxSrc = kMaxRanks > kMaxK ? kMaxRanks : kMaxK;
+
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ wp,
                                                 const int32_t* __restrict__ ids,
                                                 const float* __restrict__ wts,
                                                 const unsigned long long* __restrict__ hitmask,
@@ -933,12 +956,16 @@ __global__ void __launch_bounds__(256) k_gather(const WorldDev* __restrict__ wp,
   const int64_t ntok = (int64_t)w.L * w.T_r;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  __shared__ const uint8_t* s_src[8][kMaxSrc];
+  __shared__ float s_w[8][kMaxSrc];
+  const uint8_t** srcs = s_src[threadIdx.x >> 5];
+  float* ws = s_w[threadIdx.x >> 5];
   for (int64_t t = warp; t < ntok; t += nw) {
-    const uint8_t* srcs[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    float ws[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+    __syncwarp();
     const int n = gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push, offs,
                                  gpos_g, srcs, ws);
-    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
+    __syncwarp();
+    weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
   }
 }
 
@@ -1070,7 +1097,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1)
       for (int u = 0; u < VPC; ++u) st_na_v4(dst + u * 32 + lane, Vec<T>::from_f32(acc[u]));
     } else if (c == 0) {
       // too many sources for a stage: whole row on the register path
-      weighted_row_sum<T>(srcs[slot], ws[slot], n, w.row_bytes / 16, lane,
+      weighted_row_sum<T, 0>(srcs[slot], ws[slot], n, w.row_bytes / 16, lane,
                           reinterpret_cast<int4*>(out + t * w.row_bytes));
     }
     __syncwarp();
@@ -1117,10 +1144,14 @@ __global__ void __launch_bounds__(256) k_expand_g(const WorldDev* __restrict__ w
 
 // ... and pre-reduced (sum_k w_k y_k over this GPU's picks), pushed straight
 // into the source rank's return buffer slot [this GPU][position]
-template <typename T>
-__global__ void __launch_bounds__(256) k_reduce_g(const WorldDev* __restrict__ wp,
-                                                  const Offsets* __restrict__ offs, int grad) {
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256, 3) k_reduce_g(const WorldDev* __restrict__ wp,
+                                                     const Offsets* __restrict__ offs, int grad) {
   const WorldDev& w = *wp;
+  __shared__ const uint8_t* s_src[8][kMaxK];
+  __shared__ float s_w[8][kMaxK];
+  const uint8_t** srcs = s_src[threadIdx.x >> 5];
+  float* ws = s_w[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1129,8 +1160,7 @@ __global__ void __launch_bounds__(256) k_reduce_g(const WorldDev* __restrict__ w
   const uint8_t* ybase = grad ? w.gx[w.p * w.L] : w.ymaj[w.p * w.L];
   const RowMeta* meta = w.meta_g[w.p];
   for (int64_t r = warp; r < total; r += nw) {
-    const uint8_t* srcs[kMaxK];
-    float ws[kMaxK];
+    __syncwarp();
     int n = 0;
     for (int k = 0; k < w.K; ++k) {
       RowMeta m = meta[r * w.K + k];
@@ -1143,7 +1173,8 @@ __global__ void __launch_bounds__(256) k_reduce_g(const WorldDev* __restrict__ w
     while (src + 1 < w.G && offs->offd_g[src + 1] <= r) ++src;
     const int64_t pos = r - offs->offd_g[src];
     uint8_t* out_row = w.ret_g[src] + ((int64_t)w.p * w.T_r + pos) * w.row_bytes;
-    weighted_row_sum<T>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
+    __syncwarp();
+    weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
   }
 }
 
@@ -1371,7 +1402,8 @@ struct hm_world {
   unsigned long long epoch = 0;
   bool peers_ready = false;
   int last_mode = 0;
-  bool tma_gather = true;   // hm_world_set_option(w, 0, 0) selects the register gather
+  bool tma_gather = false;  // hm_world_set_option(w, 0, 1) selects the TMA bulk-copy gather
+                           // (measured slower than the register gather: 0.386 vs 0.311 ms, N=1)
   // optional per-kernel CUDA-event timing (segments recorded on the launch stream)
   bool timing = false;
   cudaEvent_t ev[2 * 16];
@@ -1668,6 +1700,31 @@ HM_API int hm_expand(hm_world* w, void* stream) {
 }
 
 // combine: dedup -> reduce + barrier + gather; raw -> barrier + gather.
+// host dispatch of the row-sum kernels on (payload dtype, row width): common
+// widths get their own compile-time instantiation, others the generic loop
+template <class T>
+struct TypeTag {
+  using type = T;
+};
+template <class F>
+static void with_row_type(const WorldDev& h, F&& f) {
+  auto width = [&](auto t) {
+    switch (h.row_bytes / 16) {
+      case 32: return f(t, std::integral_constant<int, 1>{});
+      case 64: return f(t, std::integral_constant<int, 2>{});
+      case 128: return f(t, std::integral_constant<int, 4>{});
+      case 256: return f(t, std::integral_constant<int, 8>{});
+      case 512: return f(t, std::integral_constant<int, 16>{});
+      case 896: return f(t, std::integral_constant<int, 28>{});
+      default: return f(t, std::integral_constant<int, 0>{});
+    }
+  };
+  if (h.elem == 2)
+    width(TypeTag<__nv_bfloat16>{});
+  else
+    width(TypeTag<float>{});
+}
+
 // `out`: [L*T_r, M] payload rows.
 HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t mode, void* out,
                       void* stream) {
@@ -1681,18 +1738,18 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   const WorldDev& h = w->h;
   if (mode == 3 && h.P > 1) {
     SegScope sc(w, kSegReduce, s);
-    if (h.elem == 2)
-      k_reduce_g<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
-    else
-      k_reduce_g<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
+    with_row_type(h, [&](auto t, auto v) {
+      k_reduce_g<typename decltype(t)::type, decltype(v)::value>
+          <<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
+    });
     HM_LAUNCHED();
   }
   if (dedup && mode != 3 && !(h.P == 1 && mode == 2) && !h.U1) {   // relay: rows arrive pre-reduced
     SegScope sc(w, kSegReduce, s);
-    if (h.elem == 2)
-      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0, 1);
-    else
-      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0, 1);
+    with_row_type(h, [&](auto t, auto v) {
+      k_reduce<typename decltype(t)::type, decltype(v)::value>
+          <<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0, 1);
+    });
     HM_LAUNCHED();
   }
   if (mode != 1) HM_CHECK_ARG(wts && ids, "hm_combine: raw/hybrid combine needs ids and weights");
@@ -1723,12 +1780,11 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
     HM_LAUNCHED();
     return 0;
   }
-  if (h.elem == 2)
-    k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos,
-                                                   mode, 0, push, w->offs, w->gpos_g, (uint8_t*)out);
-  else
-    k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode,
-                                           0, push, w->offs, w->gpos_g, (uint8_t*)out);
+  with_row_type(h, [&](auto t, auto v) {
+    k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
+        w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
+        (uint8_t*)out);
+  });
   HM_LAUNCHED();
   return 0;
 }
@@ -1878,10 +1934,10 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
   if (mode != 0 && !(h.P == 1 && mode == 2)) {
-    if (h.elem == 2)
-      k_reduce<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1, 1);
-    else
-      k_reduce<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1, 1);
+    with_row_type(h, [&](auto t, auto v) {
+      k_reduce<typename decltype(t)::type, decltype(v)::value>
+          <<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1, 1);
+    });
     HM_LAUNCHED();
   }
   if (h.P > 1) {
@@ -1890,12 +1946,11 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   }
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, kSMs * 8);
-  if (h.elem == 2)
-    k_gather<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, ids, nullptr, w->hitmask, w->gpos, w->epos,
-                                                   mode, 1, 1, w->offs, w->gpos_g, (uint8_t*)dx);
-  else
-    k_gather<float><<<blocks, 256, 0, s>>>(w->d, ids, nullptr, w->hitmask, w->gpos, w->epos, mode, 1,
-                                           1, w->offs, w->gpos_g, (uint8_t*)dx);
+  with_row_type(h, [&](auto t, auto v) {
+    k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
+        w->d, ids, nullptr, w->hitmask, w->gpos, w->epos, mode, 1, 1, w->offs, w->gpos_g,
+        (uint8_t*)dx);
+  });
   HM_LAUNCHED();
   k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode, dw);
   HM_LAUNCHED();

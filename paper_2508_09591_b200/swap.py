@@ -169,11 +169,15 @@ def _launch_cost(inter_z, intra_z, topology: Topology, params: LevelParams, dim_
     g = topology.num_gpus
     e = int(intra_z.shape[0])
     n_inter = len(inter_z)
-    inter_ptrs = np.array([ptr(z) for z in inter_z] + [0], dtype=np.uint64)
-    inter_groups = np.array([int(z.shape[2]) for z in inter_z] + [0], dtype=np.int32)
-    inter_part = np.array([u[i] // u[i - 1] for i in range(1, n_inter + 1)] + [0], dtype=np.int32)
-    a_inter = np.array([params.inter(i)[0] for i in range(1, n_inter + 1)] + [0.0])
-    b_inter = np.array([params.inter(i)[1] for i in range(1, n_inter + 1)] + [0.0])
+    # the library reads depth - 1 inter entries: cuts past the requested
+    # dimension are passed as empty (null tensor, 0 groups)
+    pad = max(depth - n_inter, 1)
+    inter_ptrs = np.array([ptr(z) for z in inter_z] + [0] * pad, dtype=np.uint64)
+    inter_groups = np.array([int(z.shape[2]) for z in inter_z] + [0] * pad, dtype=np.int32)
+    inter_part = np.array([u[i] // u[i - 1] for i in range(1, n_inter + 1)] + [0] * pad,
+                          dtype=np.int32)
+    a_inter = np.array([params.inter(i)[0] for i in range(1, n_inter + 1)] + [0.0] * pad)
+    b_inter = np.array([params.inter(i)[1] for i in range(1, n_inter + 1)] + [0.0] * pad)
     intra_ptrs = np.array([ptr(intra_z)] * depth, dtype=np.uint64)
     intra_groups = np.array([g] * depth, dtype=np.int32)
     intra_part = np.array([g // u[d - 1] for d in range(1, depth + 1)], dtype=np.int32)
