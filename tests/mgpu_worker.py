@@ -145,7 +145,9 @@ def main():
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
     cases = [(8, 16, 2, 256, 256, torch.float32), (8, 128, 8, 2048, 128, torch.bfloat16),
-             (8, 256, 8, 512, 96, torch.bfloat16)]
+             (8, 256, 8, 512, 96, torch.bfloat16),
+             # one EP rank per GPU (the N = 8 bench layout at this world size)
+             (world, 32 * world, 4, 1024, 128, torch.bfloat16)]
     for i, (G, E, K, M, T_r, dt) in enumerate(cases):
         for dedup in ("all", "remote", "gpu", "none"):
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
