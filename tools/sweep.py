@@ -4,7 +4,8 @@ tokens/rank x top-k x hierarchy at the launched GPU count.
 For each (T_r, K, topology): synthetic uniform routing of the Qwen3 layer
 (E=128, hidden 2048, bf16, G = 8 EP ranks on N GPUs); measured (CUDA events,
 max over ranks) dispatch+combine ms for
-  flat [8]      dedup across GPUs ("remote") and no dedup ("none")
+  flat [8]      dedup per destination GPU ("gpu", rows re-expanded at the
+                destination), per destination rank ("remote") and none
   [2,4], [4,2]  the two-level HD2 path (TwoLevelWorld) and the flat dedup
 plus the rows moved and the time model's d* for the mask (reference
 params).  One JSON line per case.
@@ -74,7 +75,7 @@ def main():
             cap = 3 * t_r * k
             res = {"n_gpus": world, "tokens_per_rank": t_r, "top_k": k, "experts": E, "hidden": M}
             out = torch.empty_like(x)
-            for mode in ("remote", "none"):
+            for mode in ("gpu", "remote", "none"):
                 ep = EPWorld(G, E, k, M, t_r, gpus=world, gpu_index=rank, n_cap_rows=cap)
 
                 def step():
@@ -82,6 +83,8 @@ def main():
                     ep.combine(slot, w, dedup=mode, out=out)
 
                 res[f"flat_{mode}_ms"] = timed(step, world=world)
+                if mode == "gpu":
+                    res["gpu_rows"] = int(ep.gpu_counts().sum())
                 if mode == "remote":
                     cnt = ep.counts()
                     res["dedup_rows"] = int(cnt[:, :G].sum())
