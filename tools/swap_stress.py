@@ -35,7 +35,7 @@ from paper_2508_09591_b200.moe import HierMoELayer  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--swap-every", type=int, default=50)
+    ap.add_argument("--swap-every", type=int, default=10)
     ap.add_argument("--zipf", type=float, default=1.2)
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--gamma", type=float, default=10.0)
@@ -49,10 +49,13 @@ def main():
     G, E, K, M, I, T_r = 8, 128, 8, 2048, 768, args.tokens
     L = G // world
     layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, dedup=True)
-    topo = hm.build_topology([G], E, M, 2)
-    # alpha/beta of the flat dispatch, fitted on this box's exchange (bench
-    # runs): the planner only needs their ratio for a one-level topology
-    params = hm.LevelParams((), (), (2.0e-5,), (1.3e-12,))
+    # the runtime's hierarchy: GPUs (per-GPU dedup over NVLink), then the EP
+    # ranks inside a GPU; one GPU plans for the virtual [2, 4] split.  alpha/
+    # beta are the B200 fits of tools/calibrate.py (profiles/r01_calib_n4.json:
+    # inter.1 = the GPU-level phase, std / intra.1 = the flat / in-group ones)
+    fan = [world, L] if world > 1 else [2, 4]
+    topo = hm.build_topology(fan, E, M, 2)
+    params = hm.LevelParams((3.14e-5,), (1.80e-13,), (3.36e-5, 3.15e-5), (2.84e-13, 3.59e-13))
     g = torch.Generator(device="cuda").manual_seed(2024)
     ranking = torch.randperm(E, device="cuda", generator=g)
     zipf_bias = torch.empty(E, device="cuda")
@@ -66,7 +69,7 @@ def main():
         return zipf_bias[None, :] - torch.log(-torch.log(u))   # + Gumbel(0, 1)
 
     out = torch.empty_like(x)
-    step_ms, plan_ms, mig_ms, swaps, loads = [], [], [], [], []
+    step_ms, plan_ms, mig_ms, swaps, loads, gpu_rows = [], [], [], [], [], []
     for step in range(args.steps):
         lg = logits_for(step)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -80,6 +83,7 @@ def main():
         step_ms.append(e0.elapsed_time(e1))
         rows = layer.world.rows_received()[:, 1].astype(np.int64)
         loads.append(int(rows.max()))
+        gpu_rows.append(int(layer.world.gpu_counts().sum()))
         if args.swap_every and step % args.swap_every == 0:
             p0, p1, p2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             p0.record()
@@ -92,12 +96,14 @@ def main():
             plan_ms.append(p0.elapsed_time(p1))
             mig_ms.append(p1.elapsed_time(p2))
             swaps.append({"step": step, "pair": list(plan.pair) if plan.pair else None,
+                          "d_star": plan.d_star,
                           "predicted_saving_s": plan.predicted_saving,
                           "no_swap_time_s": plan.no_swap_time})
     layer.world.check_status()
     layer.store.check_status()
     t = torch.tensor([np.mean(step_ms[5:]), np.mean(step_ms[5:55]), np.mean(step_ms[-50:]),
-                      max(plan_ms) if plan_ms else 0.0, max(mig_ms) if mig_ms else 0.0],
+                      max(plan_ms) if plan_ms else 0.0, max(mig_ms) if mig_ms else 0.0,
+                      np.mean(gpu_rows[:10]), np.mean(gpu_rows[-10:])],
                      dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -110,6 +116,9 @@ def main():
             "planner_ms_max": t[3].item(), "migration_ms_max": t[4].item(),
             "migration_bytes_per_expert": layer.store.bytes_per_slot(),
             "expert_rows_max_per_rank_first": loads[0], "expert_rows_max_per_rank_last": loads[-1],
+            "topology": fan,
+            "gpu_dedup_rows_first10": t[5].item(), "gpu_dedup_rows_last10": t[6].item(),
+            "swaps_taken": sum(1 for s_ in swaps if s_["pair"]),
             "swaps": swaps}))
     layer.close()
     if world > 1:
