@@ -138,6 +138,68 @@ def cpu_reference(cfg_name: str, steps: int, warmup: int, tokens_per_rank: int |
             "ms_per_step": sec * 1e3}
 
 
+# swap planner per step (optimal_dimension + select_swap beside
+# the reference's CPU path) on the uniform Qwen3 (B) and DSv3 (C) masks of a
+# full 8-rank step, B200 alpha/beta (tools/calibrate.py, profiles/r01_calib_n4.json)
+PLANNER_CASES = [
+    ("B", (8,), 128, 2048, ((), (), (3.36e-5,), (2.84e-13,))),
+    ("C", (2, 4), 256, 7168, ((3.14e-5,), (1.80e-13,), (3.36e-5, 3.15e-5), (2.84e-13, 3.59e-13))),
+]
+
+
+def _planner_mask(E, T, K, seed):
+    import paper_2508_09591_b200 as hm
+    return hm.generate_uniform(T, E, K, seed)
+
+
+def planner_gpu(T: int, K: int = 8, reps: int = 5) -> dict:
+    """Device planner: d* (optimal_dimension) and the swap choice (select_swap)
+    on a resident mask; CUDA events, best of `reps` after a warm-up."""
+    import paper_2508_09591_b200 as hm
+    res = {}
+    for name, fan, E, M, p in PLANNER_CASES:
+        mask = hm.device_mask(_planner_mask(E, T, K, 7))
+        topo = hm.build_topology(list(fan), E, M, 2)
+        params = hm.LevelParams(*p)
+        times = {"optimal_dimension": [], "select_swap": []}
+        for it in range(reps + 1):
+            for key, fn in (("optimal_dimension", lambda: hm.optimal_dimension(mask, topo, params)),
+                            ("select_swap", lambda: hm.select_swap(mask, topo, params, 10.0))):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r = fn()
+                e1.record()
+                e1.synchronize()
+                if it:
+                    times[key].append(e0.elapsed_time(e1))
+        res[name] = {"topology": list(fan), "experts": E, "tokens": T,
+                     "gpu_ms": {k: round(min(v), 3) for k, v in times.items()},
+                     "d_star": r.d_star, "pair": list(r.pair) if r.pair else None}
+    return res
+
+
+def planner_cpu(T: int, K: int = 8) -> dict:
+    """The oracle restatement of the same two calls (numpy, host BLAS threads)."""
+    from oracle import hiera as O
+    res = {}
+    for name, fan, E, M, p in PLANNER_CASES:
+        bits = _planner_mask(E, T, K, 7).bits
+        reps = 3 if E <= 128 else 1
+        t_dim, t_sel = [], []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            O.optimal_dimension(bits, fan, p, M * 2)
+            t1 = time.perf_counter()
+            O.select_swap(bits, fan, p, M * 2, 10.0)
+            t2 = time.perf_counter()
+            t_dim.append(t1 - t0)
+            t_sel.append(t2 - t1)
+        res[name] = {"optimal_dimension": round(min(t_dim) * 1e3, 2),
+                     "select_swap": round(min(t_sel) * 1e3, 2)}
+    return res
+
+
 def _json_out():
     """Keep stdout for the one JSON line: library banners (NCCL's version line,
     torchrun notices) are redirected to stderr for the whole run."""
@@ -159,6 +221,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the full layer forward")
+    ap.add_argument("--no-planner", action="store_true", help="skip the swap-planner timing")
     args = ap.parse_args()
     world, rank, local = dist_env()
     G, E, K, M, T_r, desc = CONFIGS[args.config]
@@ -222,6 +285,8 @@ def main():
 
     out = torch.empty(T, M, dtype=dtype, device="cuda")
 
+    launches = {}   # library kernel launches inside the timed steps, per transport
+
     def timed(w_, dedup, steps, warmup):
         prime(w_, dedup)
         for _ in range(warmup):
@@ -230,6 +295,7 @@ def main():
         if world > 1:
             dist.barrier()
         total = 0.0
+        n0 = _lib.load().hm_launch_count()
         for _ in range(steps):
             flush.zero_()
             s0 = torch.cuda.Event(enable_timing=True)
@@ -239,6 +305,7 @@ def main():
             s1.record()
             s1.synchronize()
             total += s0.elapsed_time(s1)
+        launches[dedup] = int(_lib.load().hm_launch_count() - n0)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -430,11 +497,18 @@ def main():
                              "dispatch/combine/experts fwd+bwd are our kernels"}
         layer.close()
 
+    planner = None
+    if world == 1 and not args.no_planner:
+        planner = planner_gpu(G * T_r, K)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(args.config, 3, 1, 512)
+        if planner is not None:
+            cpu_pl = planner_cpu(G * T_r, K)
+            for name in planner:
+                planner[name]["cpu_ms"] = cpu_pl[name]
+            planner["cpu_cores"] = os.cpu_count()
 
-    launches_per_step = 1 + 3 + 1 + 1 + 1 + (2 if world > 1 else 0)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -476,7 +550,8 @@ def main():
             {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": e2e,
             "layer_fwd": layer_fwd,
-            "gpu_launches": launches_per_step * args.steps,
+            "planner": planner,
+            "gpu_launches": launches[MODE],
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), file=out_stream, flush=True)

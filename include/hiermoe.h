@@ -21,6 +21,9 @@ extern "C" {
 
 const char* hm_last_error(void);
 int hm_version(void);
+/* Number of kernels this library has launched since it was loaded (for the
+ * bench's gpu_launches count; no reference counterpart). */
+unsigned long long hm_launch_count(void);
 
 /* ---------------- decision path (planner) ---------------------------------
  * Mask layout: packed rows, W = ceil(E/32) uint32 words per row; bit e of row

@@ -21,6 +21,7 @@ _lib = None
 _SIGS = {
     "hm_last_error": (ctypes.c_char_p, []),
     "hm_version": (c_int32, []),
+    "hm_launch_count": (ctypes.c_uint64, []),
     "hm_mask_pack": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_mask_unpack": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     "hm_ids_to_bits": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p,

@@ -8,6 +8,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #define HM_API extern "C" __attribute__((visibility("default")))
 
 namespace hm {
@@ -24,7 +26,17 @@ inline int cuda_status(cudaError_t e) {
   return (int)e;
 }
 
-inline int launch_status() { return cuda_status(cudaGetLastError()); }
+// kernels launched by this library since load (every launch is followed by
+// exactly one HM_LAUNCHED / launch_status check); read with hm_launch_count()
+inline std::atomic<unsigned long long>& launch_counter() {
+  static std::atomic<unsigned long long> n{0};
+  return n;
+}
+
+inline int launch_status() {
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
 
 inline int grid_for(int64_t work, int per_block, int max_blocks) {
   int64_t b = (work + per_block - 1) / per_block;

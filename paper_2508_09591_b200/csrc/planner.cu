@@ -32,6 +32,7 @@ void set_error(const char* fmt, ...) {
 
 HM_API const char* hm_last_error(void) { return hm::g_err; }
 HM_API int hm_version(void) { return 10000; }
+HM_API unsigned long long hm_launch_count(void) { return hm::launch_counter().load(); }
 
 namespace {
 

@@ -9,9 +9,9 @@ timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/${TAG}_g
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.log 2>&1; echo "exit=$?" >> $OUT/${TAG}_smoke.log
 timeout 600 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "exit=$?" >> $OUT/${TAG}_bench.err
 if [ "${2:-}" = "ncu" ]; then
-  CMD="python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e"
+  CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-layer --no-planner"
   timeout 300 $CMD > $OUT/${TAG}_plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_launches.csv $CMD > $OUT/${TAG}_ncu1.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_reduce|k_expand|k_pack|k_gather|k_plan" -s 10 -c 6 -o $OUT/${TAG}_prof $CMD > $OUT/${TAG}_ncu2.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pack|k_gather|k_plan|k_notify|k_route" -s 20 -c 10 -o $OUT/${TAG}_prof $CMD > $OUT/${TAG}_ncu2.log 2>&1
   echo "ncu exit=$?" >> $OUT/${TAG}_ncu2.log
 fi
