@@ -212,11 +212,13 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
 }
 
 // K1 router, lane-per-token variant for compile-time K: a warp stages 32
-// tokens x 32 logits at a time in shared memory (coalesced loads, padded
-// rows -> conflict-free lane reads), every lane keeps its token's sorted top-K
-// in registers (insertion with an early-out against the K-th value; strict >
-// keeps the lower index on ties because columns arrive in ascending order).
-template <int K>
+// tokens x 32 logits at a time in shared memory (padded rows -> conflict-free
+// lane reads), every lane keeps its token's sorted top-K in registers
+// (insertion with an early-out against the K-th value; strict > keeps the
+// lower index on ties because columns arrive in ascending order).  With
+// E % 4 == 0 the tile is fetched as 16-B vectors (8 per lane, all in flight)
+// and the next tile's loads are issued before the current one is scanned.
+template <int K, bool VEC>
 __global__ void __launch_bounds__(256, 3) k_route_lane(const float* __restrict__ logits, int64_t T,
                                                     int E, const int32_t* __restrict__ e2s,
                                                     int renorm, int32_t* __restrict__ slot_ids,
@@ -226,6 +228,37 @@ __global__ void __launch_bounds__(256, 3) k_route_lane(const float* __restrict__
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   float (*tl)[33] = tile[wid];
   const int64_t nwarps = (int64_t)gridDim.x * 8;
+  // vector staging: lane owns rows (lane >> 3) + 4 i, columns 4 (lane & 7) .. +3
+  const int vr = lane >> 3, vc = (lane & 7) * 4;
+  auto load_tile = [&](int64_t base, int c0, float4* buf) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t tr = base + vr + 4 * i;
+      const int col = c0 + vc;
+      buf[i] = (tr < T && col < E)
+                   ? __ldg(reinterpret_cast<const float4*>(logits + tr * E + col))
+                   : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+  };
+  auto stage = [&](int64_t base, int c0, const float4* buf) {
+    if constexpr (VEC) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float* d = &tl[vr + 4 * i][vc];
+        d[0] = buf[i].x;
+        d[1] = buf[i].y;
+        d[2] = buf[i].z;
+        d[3] = buf[i].w;
+      }
+    } else {
+      const int col = c0 + lane;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) {
+        int64_t tr = base + r;
+        tl[r][lane] = (tr < T && col < E) ? __ldg(logits + tr * E + col) : -INFINITY;
+      }
+    }
+  };
   for (int64_t base = ((int64_t)blockIdx.x * 8 + wid) * 32; base < T; base += nwarps * 32) {
     const int64_t t = base + lane;
     float vals[K];
@@ -235,14 +268,14 @@ __global__ void __launch_bounds__(256, 3) k_route_lane(const float* __restrict__
       vals[k] = -INFINITY;
       idx[k] = 0x7fffffff;
     }
+    float4 buf[VEC ? 8 : 1];
+    if constexpr (VEC) load_tile(base, 0, buf);
     for (int c0 = 0; c0 < E; c0 += 32) {
-      const int col = c0 + lane;
-#pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        int64_t tr = base + r;
-        tl[r][lane] = (tr < T && col < E) ? __ldg(logits + tr * E + col) : -INFINITY;
-      }
+      stage(base, c0, buf);
       __syncwarp();
+      if constexpr (VEC) {
+        if (c0 + 32 < E) load_tile(base, c0 + 32, buf);   // in flight during the scan
+      }
       const int ncol = E - c0 < 32 ? E - c0 : 32;
       for (int j = 0; j < ncol; ++j) {
         float v = tl[lane][j];
@@ -332,20 +365,17 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
       if (e >= 0) hit |= 1ull << dest_of(w, w.p * w.L + s_loc, e);
     }
   }
-  // destination ranks within the warp
+  // per-warp counts per destination rank and per destination GPU (mode 3:
+  // a GPU is hit if any of its L ranks is); the within-warp ranks are
+  // recomputed from the same ballots after the prefix (no global RMW)
   const unsigned lt = (1u << lane) - 1u;
   for (int d = 0; d < w.G; ++d) {
     unsigned b = __ballot_sync(0xffffffffu, (hit >> d) & 1ull);
-    if ((hit >> d) & 1ull) rank_d[t * w.G + d] = __popc(b & lt);
-    else if (valid) rank_d[t * w.G + d] = -1;
     if (lane == 0) s_cnt[warp * C + d] = __popc(b);
   }
-  // destination GPUs (mode 3): hit if any of the GPU's L ranks is hit
   const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
   for (int q = 0; q < w.P; ++q) {
-    const bool hq = (hit >> (q * w.L)) & gmask;
-    unsigned b = __ballot_sync(0xffffffffu, hq);
-    if (valid) rank_g[t * w.P + q] = hq ? __popc(b & lt) : -1;
+    unsigned b = __ballot_sync(0xffffffffu, (hit >> (q * w.L)) & gmask);
     if (lane == 0) s_cnt[warp * C + w.G + w.E + q] = __popc(b);
   }
   // slot ranks within the warp: a lane mask per slot in shared memory; the
@@ -373,11 +403,17 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
     out[c] = run;
   }
   __syncthreads();
+  for (int d = 0; d < w.G; ++d) {
+    const bool h = (hit >> d) & 1ull;
+    const unsigned b = __ballot_sync(0xffffffffu, h);
+    if (valid) rank_d[t * w.G + d] = h ? __popc(b & lt) + s_cnt[warp * C + d] : -1;
+  }
+  for (int q = 0; q < w.P; ++q) {
+    const bool h = (hit >> (q * w.L)) & gmask;
+    const unsigned b = __ballot_sync(0xffffffffu, h);
+    if (valid) rank_g[t * w.P + q] = h ? __popc(b & lt) + s_cnt[warp * C + w.G + w.E + q] : -1;
+  }
   if (valid) {
-    for (int d = 0; d < w.G; ++d)
-      if ((hit >> d) & 1ull) rank_d[t * w.G + d] += s_cnt[warp * C + d];
-    for (int q = 0; q < w.P; ++q)
-      if ((hit >> (q * w.L)) & gmask) rank_g[t * w.P + q] += s_cnt[warp * C + w.G + w.E + q];
 #pragma unroll
     for (int k = 0; k < kMaxK; ++k)
       if (k < w.K) rank_e[t * w.K + k] = S[k] >= 0 ? re[k] + s_cnt[warp * C + w.G + S[k]] : -1;
@@ -408,10 +444,15 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
     int s_loc = i / C, c = i % C;
     int32_t* col = chunk_cnt + (int64_t)s_loc * nchunks * C + c;
     int run = 0;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      int v = col[(int64_t)ch * C];
-      col[(int64_t)ch * C] = run;
-      run += v;
+    for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {   // 8 loads in flight, then the stores
+      int v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = ch0 + j < nchunks ? col[(int64_t)(ch0 + j) * C] : 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (ch0 + j < nchunks) col[(int64_t)(ch0 + j) * C] = run;
+        run += v[j];
+      }
     }
     int sg = w.p * w.L + s_loc;
     for (int q = 0; q < w.P; ++q) w.counts[q * w.L][(int64_t)sg * C + c] = run;
@@ -1610,8 +1651,13 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
     int blocks = grid_for(T, 256, kSMs * 8);
 #define HM_ROUTE_K(KK)                                                                      \
   case KK:                                                                                  \
-    k_route_lane<KK><<<blocks, 256, 0, s>>>(logits, T, E, expert_to_slot, renormalize,      \
-                                            slot_ids, weights, expert_ids);                 \
+    if (E % 4 == 0 && ((uintptr_t)logits & 15) == 0)                                        \
+      k_route_lane<KK, true><<<blocks, 256, 0, s>>>(logits, T, E, expert_to_slot, renormalize, \
+                                                    slot_ids, weights, expert_ids);         \
+    else                                                                                    \
+      k_route_lane<KK, false><<<blocks, 256, 0, s>>>(logits, T, E, expert_to_slot,          \
+                                                     renormalize, slot_ids, weights,        \
+                                                     expert_ids);                           \
     break;
     switch (K) {
       HM_ROUTE_K(1) HM_ROUTE_K(2) HM_ROUTE_K(3) HM_ROUTE_K(4)
