@@ -389,6 +389,14 @@ def main():
                 "unit": "GB/s", "traffic": None, "algorithmic_bytes": alg[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # DRAM bytes per launch of the same kernel from the committed ncu --set
+    # full capture of this command (profiles/ncu_traffic.json, qwen3 at N=1)
+    tr_path = ROOT / "profiles" / "ncu_traffic.json"
+    if (roof["bound"] == "hbm" and world == 1 and args.config == "qwen3" and args.tokens is None
+            and tr_path.exists()):
+        tr = json.loads(tr_path.read_text())["dram_bytes_per_launch"]
+        roof["traffic"] = tr.get("k_" + dom)
+        roof["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full, dram read+write)"
     per_kernel = {k: {"ms": round(seg_ms[k], 4), "bytes": alg[k],
                       "GBps": round(alg[k] / max(seg_ms[k], 1e-9) / 1e6, 1)} for k in alg}
     for k in link:

@@ -63,7 +63,31 @@ def full(path: str) -> str:
     return "\n".join(out)
 
 
+def traffic(path: str) -> dict:
+    """Mean DRAM bytes (read + write) per launch per kernel of a --set full
+    report: the `roofline.traffic` figure bench.py reports."""
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    acc = collections.defaultdict(list)
+    for r in rows[2:]:
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(m)
+            b += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+        acc[kname(r[ki]).split("<")[0]].append(b)
+    return {k: sum(v) / len(v) for k, v in acc.items()}
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--traffic":
+        import json
+        print(json.dumps({"report": sys.argv[2], "note": sys.argv[3] if len(sys.argv) > 3 else "",
+                          "dram_bytes_per_launch": traffic(sys.argv[2])}, indent=1))
+        sys.exit(0)
     print(launches(sys.argv[1]))
     if len(sys.argv) > 2:
         print()
