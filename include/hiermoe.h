@@ -130,7 +130,12 @@ int hm_world_open_peers(hm_world* w, const void* handles);
 int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void** ptr, int64_t* bytes);
 int hm_world_info(hm_world* w, int64_t* out8);
 int hm_world_barrier(hm_world* w, void* stream);
-/* runtime options: 0 -> 1 = TMA bulk-copy gather (default), 0 = register gather */
+/* Runtime options (no reference counterpart):
+ *   0: 1 = TMA bulk-copy gather, 0 = register gather (default, faster on B200)
+ *   1: 1 = pipelined per-GPU dedup exchange at N > 1 (default): dispatch and
+ *      combine each one kernel with per-stage flags instead of barriers;
+ *      0 = barrier-separated pack / expand / reduce / gather kernels
+ *   2: percent (1..99) of the pipelined kernels' CTAs that push (default 50) */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);
 /* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
  * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */

@@ -42,6 +42,8 @@ namespace {
 using namespace hm;
 
 constexpr int kMaxRanks = 64;
+constexpr int kMaxJ = 8;      // pipeline stages per source rank (mode 3, N > 1)
+constexpr int kStages = 8;    // target pipeline stages per GPU (L * J)
 constexpr int kMaxK = 16;
 constexpr int kChunk = 256;      // tokens per plan chunk (8 warps x 32)
 constexpr int kPlanWarps = kChunk / 32;
@@ -78,6 +80,14 @@ struct WorldDev {
   float* gw[kMaxRanks];       // backward: gate grads of dedup picks [R_cap][K], or null
   int32_t* counts[kMaxRanks];                 // count matrix [G][G+E] on d's GPU
   unsigned long long* flags[kMaxRanks];       // per GPU q: flags[q][0..P)
+  // pipelined mode-3 exchange (indexed by the first rank of a GPU, q * L):
+  // cpre[G src][kMaxJ + 1] = rows of src for this GPU before each stage
+  // boundary (written by src's GPU), dflag[G src][kMaxJ] = dispatch stage j
+  // of src delivered, rflag[P * L][kMaxJ] = returns of stage j for local
+  // source (dest GPU * L + s_loc) delivered
+  int32_t* cpre[kMaxRanks];
+  unsigned long long* dflag[kMaxRanks];
+  unsigned long long* rflag[kMaxRanks];
 };
 
 __device__ __forceinline__ int dest_of(const WorldDev& w, int s, int e) {
@@ -432,9 +442,11 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  Offsets* __restrict__ offs,
                                                  int32_t* __restrict__ eoff,
                                                  int32_t* __restrict__ n_e, int mode,
-                                                 unsigned long long epoch, int* __restrict__ status) {
+                                                 unsigned long long epoch, int* __restrict__ status,
+                                                 int J, int32_t* __restrict__ pipe, int pipe_len) {
   const WorldDev& w = *wp;
   const int C = w.G + w.E + w.P;
+  for (int i = threadIdx.x; i < pipe_len; i += blockDim.x) pipe[i] = 0;
   // mode 2 (dedup across GPUs only): sources on the destination's own GPU
   // write expert-major rows directly and occupy no receive rows
   auto ships = [&](int src, int dst) {
@@ -456,6 +468,15 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
     }
     int sg = w.p * w.L + s_loc;
     for (int q = 0; q < w.P; ++q) w.counts[q * w.L][(int64_t)sg * C + c] = run;
+    // pipelined mode 3: this source's row prefix for GPU q at every stage
+    // boundary, stored on q (receive rows of stage j = [cpre[j], cpre[j+1]))
+    if (J > 0 && c >= w.G + w.E && c - (w.G + w.E) != w.p) {
+      const int q = c - (w.G + w.E);
+      for (int j = 0; j <= J; ++j) {
+        const int b = j * nchunks / J;
+        w.cpre[q * w.L][sg * (kMaxJ + 1) + j] = b < nchunks ? col[(int64_t)b * C] : run;
+      }
+    }
   }
   cta_barrier(w, epoch, status);
   const int32_t* cnt = w.counts[w.p * w.L];  // complete [G][G+E] matrix
@@ -541,6 +562,14 @@ __device__ __forceinline__ int4 ld_v4(const int4* p) {
                : "l"(p));
   return r;
 }
+// L2-coherent load (no L1 allocation) for rows a peer wrote during this kernel
+__device__ __forceinline__ int4 ld_cg_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void st_na_v4(int4* p, int4 v) {
   asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w));
@@ -550,6 +579,141 @@ constexpr int kUnroll = 8;  // 16-B vectors per lane in flight (4 KB per warp)
 
 // pack: warp per token.  dedup: one copy per hit destination + per-row meta;
 // raw: one copy per selection into expert-major rows.
+// one token's dispatch (warp): expert-major positions of its picks, then the
+// row to every place it goes (direct expert-major rows for picks on this GPU
+// in modes 0/2/3, one row per hit remote GPU in mode 3, one row per hit
+// destination rank in modes 1/2) with its per-row metadata
+__device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lane,
+                                           const uint8_t* __restrict__ x,
+                                           const int32_t* __restrict__ ids,
+                                           const float* __restrict__ wts,
+                                           const int32_t* __restrict__ chunk_off,
+                                           const int32_t* __restrict__ rank_d,
+                                           const int32_t* __restrict__ rank_e,
+                                           const unsigned long long* __restrict__ hitmask,
+                                           const Offsets* __restrict__ offs,
+                                           const int32_t* __restrict__ eoff, int nchunks, int mode,
+                                           int32_t* __restrict__ gpos, int32_t* __restrict__ epos_out,
+                                           const int32_t* __restrict__ rank_g,
+                                           int32_t* __restrict__ gpos_g, int* __restrict__ status) {
+  const int C = w.G + w.E + w.P;
+  const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
+  const int64_t nvec = w.row_bytes / 16;
+  const int s_loc = (int)(t / w.T_r);
+  const int64_t t_in = t - (int64_t)s_loc * w.T_r;
+  const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
+  // expert-major positions of my picks (lane k < K computes pick k)
+  int my_e = -1, my_ep = -1;
+  float my_w = 0.f;
+  if (lane < w.K) {
+    my_e = ids[t * w.K + lane];
+    my_w = wts ? wts[t * w.K + lane] : 0.f;
+    if (my_e >= 0 && !w.U1) {   // relay worlds build no expert-major rows
+      my_ep = eoff[s_loc * w.E + my_e] + coff[w.G + my_e] + rank_e[t * w.K + lane];
+      if (my_ep >= w.N_cap) {
+        atomicExch(status, 2);
+        my_ep = -1;
+      }
+    }
+    epos_out[t * w.K + lane] = my_ep;
+  }
+  const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
+  unsigned long long hit = hitmask[t];
+  // destinations (dedup) or picks (raw) this row goes to
+  int ndst = 0;
+  int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+  uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+  // direct expert-major rows: every pick (mode 0) or picks on this GPU (modes 2, 3)
+  if (mode != 1) {
+    for (int k = 0; k < w.K; ++k) {
+      int e = __shfl_sync(0xffffffffu, my_e, k);
+      int ep = __shfl_sync(0xffffffffu, my_ep, k);
+      if (e < 0 || ep < 0) continue;
+      const int d = e / w.E_loc;
+      if (mode >= 2 && d / w.L != w.p) continue;
+      dst_base[ndst] = w.xmaj[d];
+      dst_row[ndst] = ep;
+      ++ndst;
+    }
+  }
+  // mode 3: one row per (token, other GPU hit); meta carries, per pick on
+  // that GPU, its local rank's expert-major row (l * N_cap + epos)
+  if (mode == 3) {
+    for (int q = 0; q < w.P; ++q) {
+      if (q == w.p) continue;
+      if (!((hit >> (q * w.L)) & gmask)) {
+        if (lane == 0) gpos_g[t * w.P + q] = -1;
+        continue;
+      }
+      const int64_t g = (int64_t)offs->off_g[s_loc][q] + coff[w.G + w.E + q] + rank_g[t * w.P + q];
+      if (lane == 0) gpos_g[t * w.P + q] = (int32_t)g;
+      if (g >= w.Rg_cap) {
+        if (lane == 0) atomicExch(status, 2);
+        continue;
+      }
+      if (lane < w.K) {
+        RowMeta m;
+        const int dr = my_e >= 0 ? my_e / w.E_loc : -1;
+        m.epos = (dr >= 0 && dr / w.L == q && my_ep >= 0)
+                     ? (int32_t)((dr - q * w.L) * w.N_cap + my_ep) : -1;
+        m.w = my_w;
+        w.meta_g[q][g * w.K + lane] = m;
+      }
+      dst_base[ndst] = w.recv_g[q];
+      dst_row[ndst] = g;
+      ++ndst;
+    }
+  }
+  // dedup rows: every hit destination (mode 1) or destinations on other GPUs (mode 2)
+  if (mode == 1 || mode == 2) {
+    for (int d = 0; d < w.G; ++d) {
+      if (!((hit >> d) & 1ull)) continue;
+      if (mode == 2 && d / w.L == w.p) {
+        if (lane == 0) gpos[t * w.G + d] = -1;
+        continue;
+      }
+      int64_t g = (int64_t)offs->off[s_loc][d] + coff[d] + rank_d[t * w.G + d];
+      if (lane == 0) gpos[t * w.G + d] = (int32_t)g;
+      if (g >= w.R_cap) {
+        if (lane == 0) atomicExch(status, 2);
+        continue;
+      }
+      // meta: lane k writes pick k's local expert-major row (relay: its slot
+      // id, restricted to the destination's group) or -1, plus the gate
+      if (lane < w.K) {
+        RowMeta m;
+        const int sg = w.p * w.L + s_loc;
+        const bool here = my_e >= 0 && dest_of(w, sg, my_e) == d;
+        m.epos = here ? (w.U1 ? my_e : my_ep) : -1;
+        m.w = my_w;
+        w.recv_meta[d][g * w.K + lane] = m;
+      }
+      dst_base[ndst] = w.recv_x[d];
+      dst_row[ndst] = g;
+      ++ndst;
+    }
+    if (lane == 0)
+      for (int d = 0; d < w.G; ++d)
+        if (!((hit >> d) & 1ull)) gpos[t * w.G + d] = -1;
+  }
+  for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+    int4 buf[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      int64_t v = v0 + u * 32 + lane;
+      if (v < nvec) buf[u] = ld_nc_v4(src + v);
+    }
+    for (int j = 0; j < ndst; ++j) {
+      int4* dst = reinterpret_cast<int4*>(dst_base[j] + dst_row[j] * w.row_bytes);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) st_na_v4(dst + v, buf[u]);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               const uint8_t* __restrict__ x,
                                               const int32_t* __restrict__ ids,
@@ -567,127 +731,12 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               int* __restrict__ status) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
-  const int C = w.G + w.E + w.P;
-  const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
-  const int64_t nvec = w.row_bytes / 16;
   const int64_t T = (int64_t)w.L * w.T_r;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = warp; t < T; t += nw) {
-    const int s_loc = (int)(t / w.T_r);
-    const int64_t t_in = t - (int64_t)s_loc * w.T_r;
-    const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
-    // expert-major positions of my picks (lane k < K computes pick k)
-    int my_e = -1, my_ep = -1;
-    float my_w = 0.f;
-    if (lane < w.K) {
-      my_e = ids[t * w.K + lane];
-      my_w = wts ? wts[t * w.K + lane] : 0.f;
-      if (my_e >= 0 && !w.U1) {   // relay worlds build no expert-major rows
-        my_ep = eoff[s_loc * w.E + my_e] + coff[w.G + my_e] + rank_e[t * w.K + lane];
-        if (my_ep >= w.N_cap) {
-          atomicExch(status, 2);
-          my_ep = -1;
-        }
-      }
-      epos_out[t * w.K + lane] = my_ep;
-    }
-    const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
-    unsigned long long hit = hitmask[t];
-    // destinations (dedup) or picks (raw) this row goes to
-    int ndst = 0;
-    int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-    // direct expert-major rows: every pick (mode 0) or picks on this GPU (modes 2, 3)
-    if (mode != 1) {
-      for (int k = 0; k < w.K; ++k) {
-        int e = __shfl_sync(0xffffffffu, my_e, k);
-        int ep = __shfl_sync(0xffffffffu, my_ep, k);
-        if (e < 0 || ep < 0) continue;
-        const int d = e / w.E_loc;
-        if (mode >= 2 && d / w.L != w.p) continue;
-        dst_base[ndst] = w.xmaj[d];
-        dst_row[ndst] = ep;
-        ++ndst;
-      }
-    }
-    // mode 3: one row per (token, other GPU hit); meta carries, per pick on
-    // that GPU, its local rank's expert-major row (l * N_cap + epos)
-    if (mode == 3) {
-      for (int q = 0; q < w.P; ++q) {
-        if (q == w.p) continue;
-        if (!((hit >> (q * w.L)) & gmask)) {
-          if (lane == 0) gpos_g[t * w.P + q] = -1;
-          continue;
-        }
-        const int64_t g = (int64_t)offs->off_g[s_loc][q] + coff[w.G + w.E + q] + rank_g[t * w.P + q];
-        if (lane == 0) gpos_g[t * w.P + q] = (int32_t)g;
-        if (g >= w.Rg_cap) {
-          if (lane == 0) atomicExch(status, 2);
-          continue;
-        }
-        if (lane < w.K) {
-          RowMeta m;
-          const int dr = my_e >= 0 ? my_e / w.E_loc : -1;
-          m.epos = (dr >= 0 && dr / w.L == q && my_ep >= 0)
-                       ? (int32_t)((dr - q * w.L) * w.N_cap + my_ep) : -1;
-          m.w = my_w;
-          w.meta_g[q][g * w.K + lane] = m;
-        }
-        dst_base[ndst] = w.recv_g[q];
-        dst_row[ndst] = g;
-        ++ndst;
-      }
-    }
-    // dedup rows: every hit destination (mode 1) or destinations on other GPUs (mode 2)
-    if (mode == 1 || mode == 2) {
-      for (int d = 0; d < w.G; ++d) {
-        if (!((hit >> d) & 1ull)) continue;
-        if (mode == 2 && d / w.L == w.p) {
-          if (lane == 0) gpos[t * w.G + d] = -1;
-          continue;
-        }
-        int64_t g = (int64_t)offs->off[s_loc][d] + coff[d] + rank_d[t * w.G + d];
-        if (lane == 0) gpos[t * w.G + d] = (int32_t)g;
-        if (g >= w.R_cap) {
-          if (lane == 0) atomicExch(status, 2);
-          continue;
-        }
-        // meta: lane k writes pick k's local expert-major row (relay: its slot
-        // id, restricted to the destination's group) or -1, plus the gate
-        if (lane < w.K) {
-          RowMeta m;
-          const int sg = w.p * w.L + s_loc;
-          const bool here = my_e >= 0 && dest_of(w, sg, my_e) == d;
-          m.epos = here ? (w.U1 ? my_e : my_ep) : -1;
-          m.w = my_w;
-          w.recv_meta[d][g * w.K + lane] = m;
-        }
-        dst_base[ndst] = w.recv_x[d];
-        dst_row[ndst] = g;
-        ++ndst;
-      }
-      if (lane == 0)
-        for (int d = 0; d < w.G; ++d)
-          if (!((hit >> d) & 1ull)) gpos[t * w.G + d] = -1;
-    }
-    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
-      int4 buf[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) buf[u] = ld_nc_v4(src + v);
-      }
-      for (int j = 0; j < ndst; ++j) {
-        int4* dst = reinterpret_cast<int4*>(dst_base[j] + dst_row[j] * w.row_bytes);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          int64_t v = v0 + u * 32 + lane;
-          if (v < nvec) st_na_v4(dst + v, buf[u]);
-        }
-      }
-    }
-  }
+  for (int64_t t = warp; t < T; t += nw)
+    pack_token(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs, eoff, nchunks,
+               mode, gpos, epos_out, rank_g, gpos_g, status);
 }
 
 // expand (dedup, destination side): warp per received row -> its local
@@ -783,7 +832,7 @@ constexpr int kU = 4;
 constexpr int kCh = 2, kSu = 4;
 
 // compile-time row width: VPL 16-B vectors per lane (row = 32 * VPL vectors)
-template <typename T, int VPL>
+template <typename T, int VPL, bool CG = false>
 __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* srcs, const float* ws,
                                                        int n, int lane, int4* dst) {
   constexpr int CH = VPL < kCh ? VPL : kCh;
@@ -804,7 +853,7 @@ __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* src
         if (j0 + s < n) {
           const int4* src = reinterpret_cast<const int4*>(srcs[j0 + s]) + off;
 #pragma unroll
-          for (int u = 0; u < CH; ++u) buf[s][u] = ld_v4(src + u * 32);
+          for (int u = 0; u < CH; ++u) buf[s][u] = CG ? ld_cg_v4(src + u * 32) : ld_v4(src + u * 32);
         }
       }
 #pragma unroll
@@ -828,7 +877,7 @@ __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* src
 
 // VPL > 0: compile-time row width (one kernel instantiation per width, so the
 // register allocation is not shared with the generic loop); VPL == 0: any width
-template <typename T>
+template <typename T, bool CG = false>
 __device__ __forceinline__ void weighted_row_sum_any(const uint8_t* const* srcs, const float* ws,
                                                      int n, int64_t nvec, int lane, int4* dst) {
   for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kU) {
@@ -843,7 +892,7 @@ __device__ __forceinline__ void weighted_row_sum_any(const uint8_t* const* srcs,
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) buf[u] = ld_v4(src + v);
+        if (v < nvec) buf[u] = CG ? ld_cg_v4(src + v) : ld_v4(src + v);
       }
       const float wj = ws[j];
 #pragma unroll
@@ -862,13 +911,13 @@ __device__ __forceinline__ void weighted_row_sum_any(const uint8_t* const* srcs,
   }
 }
 
-template <typename T, int VPL>
+template <typename T, int VPL, bool CG = false>
 __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
                                                  int n, int64_t nvec, int lane, int4* dst) {
   if constexpr (VPL > 0)
-    weighted_row_sum_fixed<T, VPL>(srcs, ws, n, lane, dst);
+    weighted_row_sum_fixed<T, VPL, CG>(srcs, ws, n, lane, dst);
   else
-    weighted_row_sum_any<T>(srcs, ws, n, nvec, lane, dst);
+    weighted_row_sum_any<T, CG>(srcs, ws, n, nvec, lane, dst);
 }
 
 // reduce (dedup, destination side): partial[i] = sum_k w_k * y[epos_k] over the
@@ -1219,6 +1268,228 @@ __global__ void __launch_bounds__(256, 3) k_reduce_g(const WorldDev* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined per-GPU dedup exchange (mode 3, N > 1).  Each local source's
+// tokens are cut into J stages at chunk boundaries (L * J ~ kStages per GPU).
+// Dispatch: one kernel whose CTAs take a role by ticket: pushers pack the
+// stages in order (all pusher warps on stage k before k + 1) and the warp
+// that completes a stage publishes dflag[src][j] on every peer; expanders
+// walk the same stage order over the peers' sources, wait for the stage's
+// flag and re-expand its received rows into expert-major rows while the
+// later stages are still crossing NVLink.  Combine mirrors it: reducers push
+// the pre-reduced rows of each (source, stage) back and publish rflag at the
+// source; gatherers wait for a stage's returns from every peer and sum.  No
+// device-wide barrier: the flags carry the step sequence number; waits are
+// bounded (20 s -> status 3).  Every CTA is co-resident (grid = occupancy x
+// SMs), pushers/reducers never wait, so progress needs no particular CTA
+// schedule on either GPU.
+
+__device__ __forceinline__ void stage_tokens(const WorldDev& w, int nchunks, int J, int j,
+                                             int64_t& t0, int64_t& t1) {
+  const int b0 = j * nchunks / J, b1 = (j + 1) * nchunks / J;
+  t0 = (int64_t)b0 * kChunk;
+  t1 = (int64_t)b1 * kChunk < w.T_r ? (int64_t)b1 * kChunk : w.T_r;
+  if (t0 > t1) t0 = t1;
+}
+
+// all lanes spin on the flag (acquire at system scope), bounded
+__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long seq,
+                                          int* status) {
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(f) < seq) {
+    if (globaltimer() - t0 > 20000000000ull) {
+      atomicExch(status, 3);
+      break;
+    }
+    __nanosleep(32);
+  }
+}
+
+// after this warp's n > 0 items of a stage of `total`: true in the warp that
+// completed it (fence -> counter: the completing warp's later release covers
+// every contributing warp's stores)
+__device__ __forceinline__ bool stage_done(int* counter, int n, int total, int lane) {
+  __threadfence_system();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) last = (atomicAdd(counter, n) + n == total);
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+__global__ void __launch_bounds__(256) k_dispatch_g(const WorldDev* __restrict__ wp,
+                                                    const uint8_t* __restrict__ x,
+                                                    const int32_t* __restrict__ ids,
+                                                    const float* __restrict__ wts,
+                                                    const int32_t* __restrict__ chunk_off,
+                                                    const int32_t* __restrict__ rank_e,
+                                                    const unsigned long long* __restrict__ hitmask,
+                                                    const Offsets* __restrict__ offs,
+                                                    const int32_t* __restrict__ eoff, int nchunks,
+                                                    int J, int32_t* __restrict__ epos_out,
+                                                    const int32_t* __restrict__ rank_g,
+                                                    int32_t* __restrict__ gpos_g,
+                                                    int* __restrict__ status, int* __restrict__ pipe,
+                                                    int n_push, unsigned long long seq) {
+  const WorldDev& w = *wp;
+  __shared__ int s_role;
+  if (threadIdx.x == 0) s_role = atomicAdd(pipe + 0, 1);
+  __syncthreads();
+  const int role = s_role;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nstage = w.L * J;
+  if (role < n_push) {
+    int* done = pipe + 2;
+    const int64_t gw = (int64_t)role * 8 + wid, nw = (int64_t)n_push * 8;
+    for (int k = 0; k < nstage; ++k) {
+      const int s_loc = k / J, j = k % J;
+      int64_t t0, t1;
+      stage_tokens(w, nchunks, J, j, t0, t1);
+      int n = 0;
+      for (int64_t ti = t0 + gw; ti < t1; ti += nw, ++n)
+        pack_token(w, (int64_t)s_loc * w.T_r + ti, lane, x, ids, wts, chunk_off, nullptr, rank_e,
+                   hitmask, offs, eoff, nchunks, 3, nullptr, epos_out, rank_g, gpos_g, status);
+      const int total = (int)(t1 - t0);
+      const bool publish = n ? stage_done(done + k, n, total, lane) : (total == 0 && gw == 0);
+      if (publish && lane == 0) {
+        __threadfence_system();
+        const int sg = w.p * w.L + s_loc;
+        for (int q = 0; q < w.P; ++q)
+          if (q != w.p) st_release_sys(w.dflag[q * w.L] + sg * kMaxJ + j, seq);
+      }
+    }
+    return;
+  }
+  // expanders: received rows of (peer source, stage) -> local expert-major rows
+  const int64_t gw = (int64_t)(role - n_push) * 8 + wid;
+  const int64_t nw = (int64_t)(gridDim.x - n_push) * 8;
+  const int64_t nvec = w.row_bytes / 16;
+  uint8_t* xbase = w.xmaj[w.p * w.L];
+  const RowMeta* meta = w.meta_g[w.p];
+  const int32_t* cpre = w.cpre[w.p * w.L];
+  for (int k = 0; k < nstage; ++k) {
+    const int kl = k / J, j = k % J;
+    for (int q = 0; q < w.P; ++q) {
+      if (q == w.p) continue;
+      const int s = q * w.L + kl;
+      const int64_t base = offs->offd_g[s];
+      const int64_t r0 = base + cpre[s * (kMaxJ + 1) + j];
+      const int64_t r1 = base + cpre[s * (kMaxJ + 1) + j + 1];
+      if (r0 + gw >= r1) continue;
+      wait_flag(w.dflag[w.p * w.L] + s * kMaxJ + j, seq, status);
+      for (int64_t r = r0 + gw; r < r1; r += nw) {
+        int ep = -1;
+        if (lane < w.K) ep = __ldcg(&meta[r * w.K + lane].epos);
+        const int4* src = reinterpret_cast<const int4*>(w.recv_g[w.p] + r * w.row_bytes);
+        for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+          int4 buf[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            int64_t v = v0 + u * 32 + lane;
+            if (v < nvec) buf[u] = ld_cg_v4(src + v);
+          }
+          for (int kk = 0; kk < w.K; ++kk) {
+            int e = __shfl_sync(0xffffffffu, ep, kk);
+            if (e < 0) continue;
+            int4* dst = reinterpret_cast<int4*>(xbase + (int64_t)e * w.row_bytes);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+              int64_t v = v0 + u * 32 + lane;
+              if (v < nvec) st_na_v4(dst + v, buf[u]);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict__ wp,
+                                                      const int32_t* __restrict__ ids,
+                                                      const float* __restrict__ wts,
+                                                      const unsigned long long* __restrict__ hitmask,
+                                                      const int32_t* __restrict__ epos,
+                                                      const Offsets* __restrict__ offs,
+                                                      const int32_t* __restrict__ gpos_g,
+                                                      uint8_t* __restrict__ out, int nchunks, int J,
+                                                      int* __restrict__ status,
+                                                      int* __restrict__ pipe, int n_red,
+                                                      unsigned long long seq) {
+  const WorldDev& w = *wp;
+  __shared__ int s_role;
+  __shared__ const uint8_t* s_src[8][kMaxSrc];
+  __shared__ float s_w[8][kMaxSrc];
+  if (threadIdx.x == 0) s_role = atomicAdd(pipe + 1, 1);
+  __syncthreads();
+  const int role = s_role;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint8_t** srcs = s_src[wid];
+  float* ws = s_w[wid];
+  const int64_t nvec = w.row_bytes / 16;
+  const int nstage = w.L * J;
+  if (role < n_red) {
+    // reducers: pre-reduce this GPU's picks of every received row, push to the source
+    int* done = pipe + 2 + kMaxRanks * kMaxJ;
+    const int64_t gw = (int64_t)role * 8 + wid, nw = (int64_t)n_red * 8;
+    const uint8_t* ybase = w.ymaj[w.p * w.L];
+    const RowMeta* meta = w.meta_g[w.p];
+    const int32_t* cpre = w.cpre[w.p * w.L];
+    for (int k = 0; k < nstage; ++k) {
+      const int kl = k / J, j = k % J;
+      for (int q = 0; q < w.P; ++q) {
+        if (q == w.p) continue;
+        const int s = q * w.L + kl;
+        const int64_t base = offs->offd_g[s];
+        const int64_t r0 = base + cpre[s * (kMaxJ + 1) + j];
+        const int64_t r1 = base + cpre[s * (kMaxJ + 1) + j + 1];
+        int cnt = 0;
+        for (int64_t r = r0 + gw; r < r1; r += nw, ++cnt) {
+          __syncwarp();
+          int n = 0;
+          for (int kk = 0; kk < w.K; ++kk) {
+            RowMeta m = meta[r * w.K + kk];
+            if (m.epos < 0) continue;
+            srcs[n] = ybase + (int64_t)m.epos * w.row_bytes;
+            ws[n] = m.w;
+            ++n;
+          }
+          uint8_t* out_row = w.ret_g[s] + ((int64_t)w.p * w.T_r + (r - base)) * w.row_bytes;
+          __syncwarp();
+          weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
+        }
+        const int total = (int)(r1 - r0);
+        const bool publish = cnt ? stage_done(done + s * kMaxJ + j, cnt, total, lane)
+                                 : (total == 0 && gw == 0);
+        if (publish && lane == 0) {
+          __threadfence_system();
+          st_release_sys(w.rflag[q * w.L] + (w.p * w.L + kl) * kMaxJ + j, seq);
+        }
+      }
+    }
+    return;
+  }
+  // gatherers: a stage's tokens once every peer returned it
+  const int64_t gw = (int64_t)(role - n_red) * 8 + wid;
+  const int64_t nw = (int64_t)(gridDim.x - n_red) * 8;
+  for (int k = 0; k < nstage; ++k) {
+    const int s_loc = k / J, j = k % J;
+    int64_t t0, t1;
+    stage_tokens(w, nchunks, J, j, t0, t1);
+    if (t0 + gw >= t1) continue;
+    for (int q = 0; q < w.P; ++q)
+      if (q != w.p) wait_flag(w.rflag[w.p * w.L] + (q * w.L + s_loc) * kMaxJ + j, seq, status);
+    for (int64_t ti = t0 + gw; ti < t1; ti += nw) {
+      const int64_t t = (int64_t)s_loc * w.T_r + ti;
+      __syncwarp();
+      const int n = gather_sources(w, t, ids, wts, hitmask, nullptr, epos, 3, 0, 1, offs, gpos_g,
+                                   srcs, ws);
+      __syncwarp();
+      weighted_row_sum<T, VPL, true>(srcs, ws, n, nvec, lane,
+                                     reinterpret_cast<int4*>(out + t * w.row_bytes));
+    }
+  }
+}
+
 // relay -> phase-2 inputs: per local relay rank, received row i carries the
 // token's picks inside this rank's group (slot ids, -1 elsewhere) + gates;
 // rows past the received count are padding (-1).
@@ -1423,7 +1694,7 @@ struct hm_world {
   size_t sym_bytes = 0;
   size_t off_recv_x = 0, off_meta = 0, off_xmaj = 0, off_ymaj = 0, off_comb = 0, off_counts = 0,
          off_flags = 0, off_gy = 0, off_gx = 0, off_gw = 0, off_ret = 0, off_recv_g = 0,
-         off_meta_g = 0, off_ret_g = 0;
+         off_meta_g = 0, off_ret_g = 0, off_cpre = 0, off_dflag = 0, off_rflag = 0;
   bool grad = false;
   std::vector<void*> opened;  // peer bases opened via IPC
   // local scratch
@@ -1440,6 +1711,15 @@ struct hm_world {
   int32_t* eoff = nullptr;
   int32_t* n_e = nullptr;
   int* status = nullptr;
+  // pipelined mode 3 (N > 1): role tickets + stage completion counters,
+  // step sequence number carried by the stage flags, CTA split
+  int32_t* pipe = nullptr;
+  int pipe_len = 0;
+  unsigned long long seq = 0;  // flag value of the current pipelined step
+  bool pipelined = true;       // hm_world_set_option(w, 1, 0) -> barrier-separated kernels
+  int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
+  int fused_blocks = 0;        // co-resident grid of the pipelined kernels
+  int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
   bool peers_ready = false;
   int last_mode = 0;
@@ -1491,6 +1771,9 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
                       : nullptr;
     h.counts[d] = reinterpret_cast<int32_t*>(base + w->off_counts);
     h.flags[d] = reinterpret_cast<unsigned long long*>(base + w->off_flags);
+    h.cpre[d] = reinterpret_cast<int32_t*>(base + w->off_cpre);
+    h.dflag[d] = reinterpret_cast<unsigned long long*>(base + w->off_dflag);
+    h.rflag[d] = reinterpret_cast<unsigned long long*>(base + w->off_rflag);
   }
   h.recv_g[q] = base + w->off_recv_g;
   h.meta_g[q] = reinterpret_cast<RowMeta*>(base + w->off_meta_g);
@@ -1560,6 +1843,9 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   }
   w->off_counts = o; o = align_up(o + (size_t)h.G * (h.G + h.E + h.P) * 4, 256);
   w->off_flags = o;  o = align_up(o + (size_t)h.P * 8, 256);
+  w->off_cpre = o;   o = align_up(o + (size_t)h.G * (kMaxJ + 1) * 4, 256);
+  w->off_dflag = o;  o = align_up(o + (size_t)h.G * kMaxJ * 8, 256);
+  w->off_rflag = o;  o = align_up(o + (size_t)h.G * kMaxJ * 8, 256);
   w->sym_bytes = o;
   int st;
 #define HM_TRY(call) do { st = hm::cuda_status(call); if (st) { delete w; return st; } } while (0)
@@ -1578,6 +1864,9 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   HM_TRY(cudaMalloc(&w->offs, sizeof(Offsets)));
   HM_TRY(cudaMalloc(&w->eoff, (size_t)h.L * h.E * 4));
   HM_TRY(cudaMalloc(&w->n_e, (size_t)h.E * 4));
+  w->pipe_len = 2 + 2 * kMaxRanks * kMaxJ;
+  HM_TRY(cudaMalloc(&w->pipe, (size_t)w->pipe_len * 4));
+  HM_TRY(cudaMemset(w->pipe, 0, (size_t)w->pipe_len * 4));
   HM_TRY(cudaMalloc(&w->status, 16));
   HM_TRY(cudaMemset(w->status, 0, 16));
   HM_TRY(cudaMalloc(&w->d, sizeof(WorldDev)));
@@ -1609,6 +1898,7 @@ HM_API int hm_world_destroy(hm_world* w) {
   cudaFree(w->eoff);
   cudaFree(w->n_e);
   cudaFree(w->status);
+  cudaFree(w->pipe);
   cudaFree(w->d);
   delete w;
   return 0;
@@ -1709,11 +1999,37 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
                                     w->hitmask, w->rank_g, w->status);
   }
   HM_LAUNCHED();
+  // pipelined per-GPU dedup: J stages per source (L * J ~ kStages per GPU)
+  int J = 0;
+  if (mode == 3 && h.P > 1 && !h.U1 && w->pipelined) {
+    J = kStages / h.L;
+    if (J < 1) J = 1;
+    if (J > kMaxJ) J = kMaxJ;
+    if (J > w->nchunks) J = w->nchunks;
+  }
+  w->last_J = J;
   {SegScope sc(w, kSegNotify, s);
   k_notify<<<1, 1024, 0, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e, mode,
-                              ++w->epoch, w->status);
+                              ++w->epoch, w->status, J, w->pipe, w->pipe_len);
   }
   HM_LAUNCHED();
+  if (J) {
+    int occ = 0;
+    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dispatch_g, 256, 0));
+    const int blocks = kSMs * (occ > 0 ? occ : 1);
+    int n_push = blocks * w->push_pct / 100;
+    if (n_push < 1) n_push = 1;
+    if (n_push > blocks - 1) n_push = blocks - 1;
+    // the notify barrier's epoch: equal on every GPU for the same step (all
+    // GPUs issue the same sequence of barrier-carrying calls), monotonic
+    w->seq = w->epoch;
+    SegScope sc(w, kSegPack, s);
+    k_dispatch_g<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_e,
+                                        w->hitmask, w->offs, w->eoff, w->nchunks, J, w->epos,
+                                        w->rank_g, w->gpos_g, w->status, w->pipe, n_push, w->seq);
+    HM_LAUNCHED();
+    return 0;
+  }
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, kSMs * 8);
   {SegScope sc(w, kSegPack, s);
@@ -1735,6 +2051,7 @@ HM_API int hm_expand(hm_world* w, void* stream) {
   if (w->h.P == 1 && w->last_mode == 2) return 0;  // every rank shares this GPU: nothing received
   if (w->h.U1) return 0;                             // relay rows are re-dispatched, not expanded
   if (w->last_mode == 3 && w->h.P == 1) return 0;    // one GPU: every row went direct
+  if (w->last_J) return 0;                           // pipelined: expanded inside the dispatch
   int blocks = kSMs * 8;
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
   if (w->last_mode == 3)
@@ -1782,6 +2099,27 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   const int push = w->h.U1 ? 0 : 1;
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
+  if (mode == 3 && w->last_J) {   // pipelined reduce + gather, one kernel
+    HM_CHECK_ARG(w->last_mode == 3, "hm_combine: mode 3 combine after a mode %d dispatch",
+                 w->last_mode);
+    HM_CHECK_ARG(wts && ids, "hm_combine: mode 3 needs ids and weights");
+    int rc = 0;
+    with_row_type(h, [&](auto t, auto v) {
+      auto kern = k_combine_g<typename decltype(t)::type, decltype(v)::value>;
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+      const int blocks = kSMs * (occ > 0 ? occ : 1);
+      int n_red = blocks * w->push_pct / 100;
+      if (n_red < 1) n_red = 1;
+      if (n_red > blocks - 1) n_red = blocks - 1;
+      SegScope sc(w, kSegGather, s);
+      kern<<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->epos, w->offs, w->gpos_g,
+                                  (uint8_t*)out, w->nchunks, w->last_J, w->status, w->pipe, n_red,
+                                  w->seq);
+      rc = hm::launch_status();
+    });
+    return rc;
+  }
   if (mode == 3 && h.P > 1) {
     SegScope sc(w, kSegReduce, s);
     with_row_type(h, [&](auto t, auto v) {
@@ -2003,10 +2341,17 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   return 0;
 }
 
-// runtime options: 0 = use the TMA gather (1, default) or the register gather (0)
+// runtime options: 0 = TMA bulk-copy gather (1) or the register gather (0, default);
+// 1 = pipelined mode-3 exchange at N > 1 (1, default) or barrier-separated
+// kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option == 0, "hm_world_set_option: unknown option %d", option);
-  w->tma_gather = value != 0;
+  HM_CHECK_ARG(option >= 0 && option <= 2, "hm_world_set_option: unknown option %d", option);
+  if (option == 0) w->tma_gather = value != 0;
+  if (option == 1) w->pipelined = value != 0;
+  if (option == 2) {
+    HM_CHECK_ARG(value >= 1 && value <= 99, "hm_world_set_option: split must be 1..99 %%");
+    w->push_pct = value;
+  }
   return 0;
 }

@@ -228,6 +228,13 @@ class EPWorld:
         """Source-side sum via TMA bulk copies or register loads (default; faster on B200)."""
         _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
 
+    def set_pipelined(self, enabled: bool, push_percent: int | None = None) -> None:
+        """Per-GPU dedup at N > 1: one pipelined kernel per direction with
+        per-stage flags (default) or the barrier-separated kernels."""
+        _lib.call("hm_world_set_option", self._h, 1, int(bool(enabled)))
+        if push_percent is not None:
+            _lib.call("hm_world_set_option", self._h, 2, int(push_percent))
+
     def _check_rows(self, x, ids):
         t = self.local * self.tokens_per_rank
         if x.shape != (t, self.hidden) or x.dtype != self.dtype or not x.is_contiguous():
