@@ -318,6 +318,13 @@ def main():
 
     with ClockSampler(local) as clocks:
         ms = timed(ep, MODE, args.steps, args.warmup)
+    main_launches = launches[MODE]
+    ms_barrier = None
+    if world > 1:   # the same transport with barrier-separated kernels (no stage pipelining)
+        ep.set_pipelined(False)
+        ms_barrier = timed(ep, MODE, max(3, args.steps // 2), args.warmup)
+        ep.set_pipelined(True)
+        timed(ep, MODE, 3, 1)   # re-prime the pipelined path
     ms_raw = timed(raw_ep, "none", max(3, args.steps // 2), args.warmup)
     ms_all = timed(all_ep, "all", max(3, args.steps // 2), args.warmup)
 
@@ -370,10 +377,17 @@ def main():
     # rows crossing NVLink: the dispatch pushes them in pack, the combine
     # pushes the pre-reduced rows back in reduce (per-GPU dedup transport);
     # the raw transport pushes in pack and pulls expert outputs in gather
-    link = {"pack": rem_dedup * rb, "reduce": R_in * rb} if world > 1 else {}
     seg_ms = dict(zip(SEGMENTS, seg.tolist()))
     raw_ms = dict(zip(SEGMENTS, seg_raw.tolist()))
-    link_dedup = seg_ms["pack"] + seg_ms["reduce"] if world > 1 else 0.0
+    # pipelined exchange (N > 1): the dispatch is one kernel (pack segment:
+    # push + expand), the combine one kernel (gather segment: reduce + gather)
+    pipelined = world > 1 and seg_ms["reduce"] == 0.0
+    if pipelined:
+        alg["pack"] += alg.pop("expand")
+        alg["gather"] += alg.pop("reduce")
+    ret_key = "gather" if pipelined else "reduce"
+    link = {"pack": rem_dedup * rb, ret_key: R_in * rb} if world > 1 else {}
+    link_dedup = seg_ms["pack"] + seg_ms[ret_key] if world > 1 else 0.0
     link_raw = raw_ms["pack"] + raw_ms["gather"] if world > 1 else 0.0
     dom = max(alg, key=lambda k: seg_ms[k])
     peaks = measured_peaks()
@@ -571,6 +585,7 @@ def main():
                         "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_raw.tolist())},
                         "speedup_dedup_vs_nodedup": ms_raw / ms,
                         "link_time_ratio": link_raw / max(link_dedup, 1e-9) if link_dedup else None},
+            "barrier_kernels_ms_per_step": ms_barrier,
             "dedup_all_ranks": {"ms_per_step": ms_all,
                                 "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_all.tolist())}},
             "comm_bytes": {"dedup_rows_out": rows_dedup_out, "raw_rows_out": rows_raw_out,
@@ -581,17 +596,17 @@ def main():
                                (rem_raw / rem_dedup) if rem_dedup else None},
             "roofline": roof,
             "link_roofline": None if world == 1 else {
-                "bound": "nvlink", "kernel": "pack+reduce",
-                "achieved": (link["pack"] + link["reduce"]) / (link_dedup * 1e-3) / 1e9,
+                "bound": "nvlink", "kernel": "dispatch+combine pushes",
+                "achieved": (link["pack"] + link[ret_key]) / (link_dedup * 1e-3) / 1e9,
                 "peak": NVLINK_GBS, "unit": "GB/s",
-                "frac": (link["pack"] + link["reduce"]) / (link_dedup * 1e-3) / 1e9 / NVLINK_GBS,
+                "frac": (link["pack"] + link[ret_key]) / (link_dedup * 1e-3) / 1e9 / NVLINK_GBS,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"},
             "cpu_baseline": None if cpu is None else
             {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": e2e,
             "layer_fwd": layer_fwd,
             "planner": planner,
-            "gpu_launches": launches[MODE],
+            "gpu_launches": main_launches,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), file=out_stream, flush=True)
