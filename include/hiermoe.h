@@ -135,7 +135,8 @@ int hm_world_barrier(hm_world* w, void* stream);
  *   1: 1 = pipelined per-GPU dedup exchange at N > 1 (default): dispatch and
  *      combine each one kernel with per-stage flags instead of barriers;
  *      0 = barrier-separated pack / expand / reduce / gather kernels
- *   2: percent (1..99) of the pipelined kernels' CTAs that push (default 50) */
+ *   2: percent (1..99) of the pipelined kernels' CTAs that push (default 50)
+ *   3: target pipeline stages per GPU (default 8; stages per source = n / L) */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);
 /* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
  * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */

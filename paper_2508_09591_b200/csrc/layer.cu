@@ -1292,27 +1292,34 @@ __device__ __forceinline__ void stage_tokens(const WorldDev& w, int nchunks, int
   if (t0 > t1) t0 = t1;
 }
 
-// all lanes spin on the flag (acquire at system scope), bounded
+// lane 0 polls the flag (bounded, backoff), then every lane takes its own
+// acquire of the published value (one load each, no spinning)
 __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long seq,
-                                          int* status) {
-  const uint64_t t0 = globaltimer();
-  while (ld_acquire_sys(f) < seq) {
-    if (globaltimer() - t0 > 20000000000ull) {
-      atomicExch(status, 3);
-      break;
+                                          int* status, int lane) {
+  if (lane == 0) {
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_sys(f) < seq) {
+      if (globaltimer() - t0 > 20000000000ull) {
+        atomicExch(status, 3);
+        break;
+      }
+      __nanosleep(128);
     }
-    __nanosleep(32);
   }
+  __syncwarp();
+  (void)ld_acquire_sys(f);
 }
 
 // after this warp's n > 0 items of a stage of `total`: true in the warp that
 // completed it (fence -> counter: the completing warp's later release covers
 // every contributing warp's stores)
 __device__ __forceinline__ bool stage_done(int* counter, int n, int total, int lane) {
-  __threadfence_system();
   __syncwarp();
   int last = 0;
-  if (lane == 0) last = (atomicAdd(counter, n) + n == total);
+  if (lane == 0) {
+    __threadfence_system();
+    last = (atomicAdd(counter, n) + n == total);
+  }
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
@@ -1375,7 +1382,7 @@ __global__ void __launch_bounds__(256) k_dispatch_g(const WorldDev* __restrict__
       const int64_t r0 = base + cpre[s * (kMaxJ + 1) + j];
       const int64_t r1 = base + cpre[s * (kMaxJ + 1) + j + 1];
       if (r0 + gw >= r1) continue;
-      wait_flag(w.dflag[w.p * w.L] + s * kMaxJ + j, seq, status);
+      wait_flag(w.dflag[w.p * w.L] + s * kMaxJ + j, seq, status, lane);
       for (int64_t r = r0 + gw; r < r1; r += nw) {
         int ep = -1;
         if (lane < w.K) ep = __ldcg(&meta[r * w.K + lane].epos);
@@ -1477,7 +1484,7 @@ __global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict
     stage_tokens(w, nchunks, J, j, t0, t1);
     if (t0 + gw >= t1) continue;
     for (int q = 0; q < w.P; ++q)
-      if (q != w.p) wait_flag(w.rflag[w.p * w.L] + (q * w.L + s_loc) * kMaxJ + j, seq, status);
+      if (q != w.p) wait_flag(w.rflag[w.p * w.L] + (q * w.L + s_loc) * kMaxJ + j, seq, status, lane);
     for (int64_t ti = t0 + gw; ti < t1; ti += nw) {
       const int64_t t = (int64_t)s_loc * w.T_r + ti;
       __syncwarp();
@@ -1718,6 +1725,7 @@ struct hm_world {
   unsigned long long seq = 0;  // flag value of the current pipelined step
   bool pipelined = true;       // hm_world_set_option(w, 1, 0) -> barrier-separated kernels
   int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
+  int stages = kStages;        // hm_world_set_option(w, 3, n): target pipeline stages per GPU
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -2002,7 +2010,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   // pipelined per-GPU dedup: J stages per source (L * J ~ kStages per GPU)
   int J = 0;
   if (mode == 3 && h.P > 1 && !h.U1 && w->pipelined) {
-    J = kStages / h.L;
+    J = w->stages / h.L;
     if (J < 1) J = 1;
     if (J > kMaxJ) J = kMaxJ;
     if (J > w->nchunks) J = w->nchunks;
@@ -2346,12 +2354,16 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 2, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 3, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
     HM_CHECK_ARG(value >= 1 && value <= 99, "hm_world_set_option: split must be 1..99 %%");
     w->push_pct = value;
+  }
+  if (option == 3) {
+    HM_CHECK_ARG(value >= 1 && value <= kMaxRanks * kMaxJ, "hm_world_set_option: bad stage count");
+    w->stages = value;
   }
   return 0;
 }

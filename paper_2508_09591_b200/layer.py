@@ -228,12 +228,16 @@ class EPWorld:
         """Source-side sum via TMA bulk copies or register loads (default; faster on B200)."""
         _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
 
-    def set_pipelined(self, enabled: bool, push_percent: int | None = None) -> None:
+    def set_pipelined(self, enabled: bool, push_percent: int | None = None,
+                      stages: int | None = None) -> None:
         """Per-GPU dedup at N > 1: one pipelined kernel per direction with
-        per-stage flags (default) or the barrier-separated kernels."""
+        per-stage flags (default) or the barrier-separated kernels.  Must be
+        set identically on every GPU of the world."""
         _lib.call("hm_world_set_option", self._h, 1, int(bool(enabled)))
         if push_percent is not None:
             _lib.call("hm_world_set_option", self._h, 2, int(push_percent))
+        if stages is not None:
+            _lib.call("hm_world_set_option", self._h, 3, int(stages))
 
     def _check_rows(self, x, ids):
         t = self.local * self.tokens_per_rank
