@@ -132,9 +132,10 @@ int hm_world_info(hm_world* w, int64_t* out8);
 int hm_world_barrier(hm_world* w, void* stream);
 /* Runtime options (no reference counterpart):
  *   0: 1 = TMA bulk-copy gather, 0 = register gather (default, faster on B200)
- *   1: 1 = pipelined per-GPU dedup exchange at N > 1 (default): dispatch and
- *      combine each one kernel with per-stage flags instead of barriers;
- *      0 = barrier-separated pack / expand / reduce / gather kernels
+ *   1: 1 = pipelined per-GPU dedup exchange at N > 1: dispatch and combine
+ *      each one kernel with per-stage flags instead of barriers (bit-identical
+ *      results, measured slower); 0 = barrier-separated pack / expand /
+ *      reduce / gather kernels (default)
  *   2: percent (1..99) of the pipelined kernels' CTAs that push (default 50)
  *   3: target pipeline stages per GPU (default 8; stages per source = n / L) */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);

@@ -1723,7 +1723,13 @@ struct hm_world {
   int32_t* pipe = nullptr;
   int pipe_len = 0;
   unsigned long long seq = 0;  // flag value of the current pipelined step
-  bool pipelined = true;       // hm_world_set_option(w, 1, 0) -> barrier-separated kernels
+  // hm_world_set_option(w, 1, 1) -> staged dispatch/combine kernels.  Off by
+  // default: measured slower on B200 (N = 2: 0.52-1.5 ms vs 0.40 ms for the
+  // barrier-separated kernels, tools/pipe_tune.py) -- every stage boundary
+  // costs ~15 us because each pusher's release has to wait for its NVLink
+  // stores to be acknowledged, and splitting the SMs between pushers and
+  // expanders starves the local HBM copies the pushers also do.
+  bool pipelined = false;
   int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
   int stages = kStages;        // hm_world_set_option(w, 3, n): target pipeline stages per GPU
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels

@@ -231,8 +231,8 @@ class EPWorld:
     def set_pipelined(self, enabled: bool, push_percent: int | None = None,
                       stages: int | None = None) -> None:
         """Per-GPU dedup at N > 1: one pipelined kernel per direction with
-        per-stage flags (default) or the barrier-separated kernels.  Must be
-        set identically on every GPU of the world."""
+        per-stage flags, or the barrier-separated kernels (default; faster on
+        B200).  Must be set identically on every GPU of the world."""
         _lib.call("hm_world_set_option", self._h, 1, int(bool(enabled)))
         if push_percent is not None:
             _lib.call("hm_world_set_option", self._h, 2, int(push_percent))
