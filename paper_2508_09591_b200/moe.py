@@ -17,7 +17,7 @@ from . import _lib
 from .ffn import FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs, pack_w13
 from .layer import EPWorld, route_topk
 from .migrate import ExpertStore
-from .routing import Placement
+from .routing import Placement, RoutingMask, load_placements, save_placements, save_trace
 
 
 class _tf32:
@@ -35,7 +35,7 @@ class HierMoELayer:
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int, inter: int,
                  tokens_per_rank: int, gpus: int = 1, gpu_index: int = 0, group=None,
                  dedup=True, seed: int = 0, renormalize: bool = True, grad: bool = False,
-                 n_cap_rows: int = 0):
+                 n_cap_rows: int = 0, layer_index: int = 0):
         if inter % 128 or hidden % 256:
             raise ValueError("hidden must be a multiple of 256 and inter of 128")
         self.ranks, self.experts, self.top_k = ranks, experts, top_k
@@ -83,6 +83,10 @@ class HierMoELayer:
         self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
         self.set_placement(Placement.identity(experts))
         self._saved = None
+        self.group = group
+        self.layer_index = layer_index
+        self.iteration = 0            # forward calls so far (trace "iter" column)
+        self._trace = None            # [(iter, expert ids [T_local, K] on device)] when recording
         if grad:
             self.refresh_transposed_weights()
             self.bwd = FFNBackwardScratch(self.world.n_cap, self.e_loc, hidden, inter)
@@ -132,6 +136,9 @@ class HierMoELayer:
         slot, w, ex = self.route(x)
         if self.grad:
             self._saved = (x, slot, w, ex)
+        if self._trace is not None:
+            self._trace.append((self.iteration, ex.clone()))
+        self.iteration += 1
         self.world.dispatch(x, slot, w, dedup=self.dedup)
         self.experts_forward()   # expert-major rows are local after the dispatch barrier
         # hm_combine barriers before the source reads peers' rows (any mode)
@@ -175,6 +182,52 @@ class HierMoELayer:
         with _tf32():
             self.dw_router += dlogits.T @ x.float()
             return (dx.float() + dlogits @ self.w_router).to(x.dtype)
+
+    # --- routing traces and placements in the reference's file formats ---
+    def record_trace(self, enabled: bool = True) -> None:
+        """Keep every forward's expert ids (device copies) for save_trace."""
+        self._trace = [] if enabled else None
+
+    def routing_masks(self) -> list:
+        """(iteration, layer, RoutingMask) of the recorded forwards in expert
+        space; the mask is the global one (all GPUs' tokens, rank order,
+        SPEC.md:310) -- token shards are all-gathered over ``group``."""
+        import torch.distributed as dist
+        out = []
+        for it, ex in self._trace or []:
+            if self.gpus > 1:
+                parts = [torch.empty_like(ex) for _ in range(self.gpus)]
+                dist.all_gather(parts, ex, group=self.group)
+                ex = torch.cat(parts)
+            ids = ex.cpu().numpy()
+            bits = np.zeros((ids.shape[0], self.experts), dtype=bool)
+            np.put_along_axis(bits, ids.astype(np.int64), True, axis=1)
+            out.append((it, self.layer_index, RoutingMask(bits, self.top_k)))
+        return out
+
+    def save_trace(self, path) -> None:
+        """Recorded routing as the reference's trace CSV (routing.py:218-227),
+        readable by its analyze / plan / simulate commands."""
+        save_trace(self.routing_masks(), path)
+
+    def save_placement(self, path) -> None:
+        """This layer's placement as the reference's placement JSON (cli.py:193-198)."""
+        save_placements({self.layer_index: self.placement}, self.experts, path)
+
+    def load_placement(self, path) -> None:
+        """Adopt a planned placement (the reference's `plan --out-placement`):
+        every slot whose expert changes is migrated with its optimizer state."""
+        target = load_placements(path, self.experts).get(self.layer_index)
+        if target is None:
+            return
+        cur = np.asarray(self.placement.slot_to_expert).copy()
+        want = np.asarray(target.slot_to_expert)
+        for s in range(self.experts):        # selection sort by swaps
+            if cur[s] == want[s]:
+                continue
+            t = int(np.flatnonzero(cur == want[s])[0])
+            self.apply_swap((min(s, t), max(s, t)))
+            cur[[s, t]] = cur[[t, s]]
 
     def flops_per_forward(self) -> int:
         """Expert FFN flops of this GPU's last forward (6 * rows * hidden * inter)."""

@@ -362,6 +362,29 @@ def propagate_level(mask: MaskLike, topology: Topology):
     return _to_host_propagated(out)
 
 
+def save_placements(placements: dict[int, Placement], experts: int, path) -> None:
+    """Per-layer placements -> the reference's placement JSON
+    (cli.py:193-198: {"experts": E, "layers": {"<layer>": slot_to_expert}})."""
+    import json
+    doc = {"experts": int(experts),
+           "layers": {str(l): np.asarray(p.slot_to_expert).astype(int).tolist()
+                      for l, p in sorted(placements.items())}}
+    with open(path, "w") as fh:
+        fh.write(json.dumps(doc, indent=2) + "\n")
+
+
+def load_placements(path, experts: int) -> dict[int, Placement]:
+    """Placement JSON -> per-layer placements (cli.py:183-190, same error)."""
+    import json
+    with open(path) as fh:
+        raw = json.load(fh)
+    if raw.get("experts") != experts:
+        raise ValueError(f"placement file {path} is for {raw.get('experts')} "
+                         f"experts, topology has {experts}")
+    return {int(layer): Placement(np.array(perm, dtype=int))
+            for layer, perm in raw["layers"].items()}
+
+
 def save_trace(masks: list[tuple[int, int, RoutingMask]], path) -> None:
     """(iteration, layer, mask) triples -> trace CSV (routing.py:218-227)."""
     with open(path, "w", newline="") as fh:

@@ -51,3 +51,41 @@ def test_layer_forward_matches_oracle(hm, dedup, shape):
     got = out.double().cpu().numpy()
     np.testing.assert_allclose(got, ref, rtol=2e-2, atol=2e-2 * np.abs(ref).max())
     layer.close()
+
+
+def test_layer_trace_and_placement_files(hm, tmp_path):
+    """Routing trace CSV and placement JSON in the reference's formats: the
+    recorded trace is the router's expert choice per token; adopting a
+    planned placement file migrates the experts and leaves the layer's
+    function bit-for-bit unchanged."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    G, E, K, M, I, T_r = 8, 16, 2, 256, 256, 64
+    layer = HierMoELayer(G, E, K, M, I, T_r, dedup=True, seed=5, layer_index=3)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    xs = [torch.randn(G * T_r, M, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2)]
+    layer.record_trace()
+    outs = [layer(x).clone() for x in xs]
+    torch.cuda.synchronize()
+    path = tmp_path / "trace.csv"
+    layer.save_trace(path)
+    entries = hm.load_trace(path, E)
+    assert [(i, l) for i, l, _ in entries] == [(0, 3), (1, 3)]
+    for (_, _, m), x in zip(entries, xs):
+        _, _, ex = layer.route(x)
+        want = np.zeros((G * T_r, E), dtype=bool)
+        np.put_along_axis(want, ex.cpu().numpy().astype(np.int64), True, axis=1)
+        assert np.array_equal(m.bits, want)
+    # a planned placement (two swaps, one crossing local ranks) via the file
+    perm = np.arange(E)
+    perm[[1, 14]] = perm[[14, 1]]
+    perm[[4, 5]] = perm[[5, 4]]
+    hm.save_placements({3: hm.Placement(perm)}, E, tmp_path / "pl.json")
+    layer.load_placement(tmp_path / "pl.json")
+    assert np.array_equal(layer.placement.slot_to_expert, perm)
+    layer.store.check_status()
+    again = layer(xs[1])
+    torch.cuda.synchronize()
+    assert torch.equal(again, outs[1])
+    layer.save_placement(tmp_path / "pl2.json")
+    assert (tmp_path / "pl2.json").read_bytes() == (tmp_path / "pl.json").read_bytes()
+    layer.close()
