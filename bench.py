@@ -201,6 +201,48 @@ def planner_cpu(T: int, K: int = 8) -> dict:
     return res
 
 
+def dsv3_layer_forward(G, E, K, M, inter, T_r, world, rank, x, flush, tokens_total, n_l, peaks):
+    """Config C layer forward: DeepSeek-V3 group-limited gate (8 groups, top-4
+    groups, scale 2.5), dedup dispatch, tcgen05 experts, shared expert
+    (I = 2048) on a side stream overlapped with the dispatch, combine + shared
+    sum.  Inference only (no optimizer state: 256 x 44 M-parameter experts)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_09591_b200.moe import HierMoELayer
+    layer = HierMoELayer(G, E, K, M, inter, T_r, gpus=world, gpu_index=rank, dedup=True,
+                         n_cap_rows=3 * T_r * K, router="dsv3", n_group=8, topk_group=4,
+                         route_scale=2.5, shared_inter=2048, optimizer_state=False)
+    lout = torch.empty_like(x)
+    for _ in range(3):
+        layer(x, out=lout)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    acc = 0.0
+    for _ in range(n_l):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        layer(x, out=lout)
+        e1.record()
+        e1.synchronize()
+        acc += e0.elapsed_time(e1)
+    t = torch.tensor([acc / n_l], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    layer.world.check_status()
+    fl = layer.flops_per_forward() + 6 * x.shape[0] * M * 2048
+    ms = float(t.item())
+    out = {"fwd_ms": ms, "fwd_tokens_per_s": tokens_total / (ms * 1e-3),
+           "router": "dsv3 group-limited (n_group 8, topk_group 4, scale 2.5)",
+           "shared_expert_inter": 2048, "inter": inter, "transport": layer.dedup,
+           "ffn_flops_per_gpu_incl_shared": int(fl),
+           "layer_tflops": fl / (ms * 1e-3) / 1e12,
+           "note": "forward only; router logits GEMM in torch (cuBLAS TF32)"}
+    layer.close()
+    return out
+
+
 def _json_out():
     """Keep stdout for the one JSON line: library banners (NCCL's version line,
     torchrun notices) are redirected to stderr for the whole run."""
@@ -262,9 +304,10 @@ def main():
     T = L * T_r
     logits = torch.randn(T, E, device="cuda", generator=gen)
     x = torch.randn(T, M, device="cuda", generator=gen).to(dtype)
-    ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
-    raw_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
-    all_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
+    cap = 3 * T_r * K   # expert-major rows per rank (3x the uniform mean; overflow is flagged)
+    ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, n_cap_rows=cap)
+    raw_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, n_cap_rows=cap)
+    all_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, n_cap_rows=cap)
     MODE = "gpu"   # one row per (token, remote GPU); same-GPU ranks go expert-major directly
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # 256 MB > L2
 
@@ -500,6 +543,10 @@ def main():
         ep.close()
         all_ep.close()
         raw_ep.close()
+        if args.config == "dsv3":
+            layer_fwd = dsv3_layer_forward(G, E, K, M, inter, T_r, world, rank, x, flush,
+                                           tokens_total, max(5, args.steps // 10), peaks)
+    if not args.no_layer and args.config != "dsv3":
         layer = HierMoELayer(G, E, K, M, inter, T_r, gpus=world, gpu_index=rank, dedup=MODE,
                              grad=True, n_cap_rows=3 * T_r * K)
         lout = torch.empty(T, M, dtype=dtype, device="cuda")

@@ -151,6 +151,15 @@ int hm_memcpy(void* dst, const void* src, int64_t bytes, void* stream);
 int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
                   const int32_t* expert_to_slot, int32_t renormalize, int32_t* slot_ids,
                   float* weights, int32_t* expert_ids, void* stream);
+/* DeepSeek-V3 group-limited gate (the reference specifies only
+ * softmax top-K): sigmoid scores + bias choice, the topk_group
+ * best of n_group contiguous expert groups (group score = sum of its two
+ * largest choices), top-K inside them, weights = picked scores / sum *
+ * route_scale.  bias may be NULL.  Value-descending, index-ascending order. */
+int hm_route_group(const float* logits, int64_t T, int32_t E, int32_t K, int32_t n_group,
+                   int32_t topk_group, const float* bias, float route_scale,
+                   const int32_t* expert_to_slot, int32_t* slot_ids, float* weights,
+                   int32_t* expert_ids, void* stream);
 /* Dedup (one row per token x destination rank) or raw (one per selection)
  * dispatch; the per-destination histogram equals dedup_counts / raw_counts
  * at G (traffic.py:67-82). */
@@ -161,6 +170,12 @@ int hm_expand(hm_world* w, void* stream);
 /* Gate-weighted combine (pre-reduce per destination + source sum for dedup). */
 int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
                void* stream);
+/* hm_combine plus one addend row per token (payload dtype, [L*T_r][M]),
+ * accumulated in fp32 after the routed rows: out = sum_k w_k y_k + addend.
+ * Used for DeepSeek-V3's shared expert; no reference
+ * counterpart. */
+int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int32_t mode,
+                   const void* addend, void* out, void* stream);
 /* Backward (world created with flags & 1).  hm_dispatch_grad = combine
  * backward: output grads -> expert-output grads (dedup broadcast, replaying the
  * forward plan) + direct picks' gate grads; hm_combine_grad = dispatch

@@ -50,6 +50,39 @@ def route_topk(logits: np.ndarray, top_k: int, expert_to_slot=None,
     return e2s[experts].astype(np.int32), weights, experts
 
 
+def route_group_limited(logits: np.ndarray, top_k: int, n_group: int, topk_group: int,
+                        bias=None, route_scale: float = 1.0, expert_to_slot=None):
+    """DeepSeek-V3 gate (the reference only specifies softmax
+    top-K, so this follows DeepSeek-V3's published inference
+    gate): scores = sigmoid(logits) (evaluated in float64, rounded to
+    float32), choice = scores + bias (float32); group score = sum of the two
+    largest choice values of each of ``n_group`` contiguous expert groups;
+    keep the ``topk_group`` best groups; top-K of choice inside them; weights
+    = scores of the picks / their sum * route_scale.  Every selection is
+    value descending, index ascending.  Returns (slot ids int32 [T,K],
+    weights float64 [T,K], expert ids int32 [T,K]).
+    """
+    logits = np.asarray(logits, dtype=np.float32)
+    t, e = logits.shape
+    gs = e // n_group
+    sc = (1.0 / (1.0 + np.exp(-logits.astype(np.float64)))).astype(np.float32)
+    b = np.zeros(e, np.float32) if bias is None else np.asarray(bias, np.float32)
+    ch = (sc + b[None, :]).astype(np.float32)
+    grp = ch.reshape(t, n_group, gs)
+    top2 = -np.sort(-grp, axis=2)[:, :, :2]
+    gscore = (top2[:, :, 0] + top2[:, :, 1]).astype(np.float32) if gs > 1 else top2[:, :, 0]
+    gorder = np.lexsort((np.broadcast_to(np.arange(n_group), (t, n_group)), -gscore), axis=1)
+    keep = np.zeros((t, n_group), dtype=bool)
+    np.put_along_axis(keep, gorder[:, :topk_group], True, axis=1)
+    masked = np.where(np.repeat(keep, gs, axis=1), ch, -np.inf).astype(np.float32)
+    order = np.lexsort((np.broadcast_to(np.arange(e), (t, e)), -masked), axis=1)
+    experts = order[:, :top_k].astype(np.int32)
+    w = np.take_along_axis(sc, experts, axis=1).astype(np.float64)
+    w = w / w.sum(axis=1, keepdims=True) * route_scale
+    e2s = np.arange(e) if expert_to_slot is None else np.asarray(expert_to_slot)
+    return e2s[experts].astype(np.int32), w, experts
+
+
 def ids_to_bits(ids: np.ndarray, experts: int) -> np.ndarray:
     """K-per-row id lists -> T x E bool mask (RoutingMask.bits, routing.py:31-56)."""
     t = ids.shape[0]

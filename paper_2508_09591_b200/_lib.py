@@ -63,12 +63,16 @@ _SIGS = {
     "hm_world_timings": (c_int32, [c_void_p, c_void_p, c_int32]),
     "hm_route_topk": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_int32, c_void_p,
                                 c_void_p, c_void_p, c_void_p]),
+    "hm_route_group": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p,
+                                 ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
     "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                    c_void_p]),
     "hm_combine_grad": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
+    "hm_combine_add": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+                                 c_void_p]),
     "hm_grouped_gemm": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32,
                                   c_int32, c_int32, c_void_p, c_int64, c_void_p]),
     "hm_store_create": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int32, POINTER(c_void_p)]),

@@ -221,6 +221,123 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
   }
 }
 
+// DeepSeek-V3 gate (group-limited, sigmoid + bias correction):
+// scores = sigmoid(logit) (fp64, rounded to fp32), choice = scores + bias;
+// group score = sum of the two largest choices of each contiguous group of
+// E / n_group experts; the topk_group best groups stay; top-K choices inside
+// them; weights = picked scores / their sum * scale.  Selections are value
+// descending, index ascending.  Warp per token: lanes hold experts j*32+lane,
+// the choices are staged in shared memory for the per-group scans.
+template <int PER>
+__global__ void __launch_bounds__(256) k_route_group(const float* __restrict__ logits, int64_t T,
+                                                     int E, int K, int n_group, int topk_group,
+                                                     const float* __restrict__ bias, float scale,
+                                                     const int32_t* __restrict__ e2s,
+                                                     int32_t* __restrict__ slot_ids,
+                                                     float* __restrict__ weights,
+                                                     int32_t* __restrict__ expert_ids) {
+  __shared__ float s_ch[8][PER * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* chs = s_ch[wid];
+  const int gs = E / n_group;
+  int64_t warp = (int64_t)blockIdx.x * 8 + wid;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t t = warp; t < T; t += nw) {
+    float sc[PER], ch[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int e = j * 32 + lane;
+      if (e < E) {
+        const double xv = (double)logits[t * E + e];
+        sc[j] = (float)(1.0 / (1.0 + exp(-xv)));
+        ch[j] = sc[j] + (bias ? bias[e] : 0.f);
+      } else {
+        sc[j] = 0.f;
+        ch[j] = -INFINITY;
+      }
+      chs[j * 32 + lane] = ch[j];
+    }
+    __syncwarp();
+    // group scores (lane g scans group g), then the topk_group best groups
+    float gsc = -INFINITY;
+    if (lane < n_group) {
+      float a = -INFINITY, b = -INFINITY;
+      for (int i = 0; i < gs; ++i) {
+        const float v = chs[lane * gs + i];
+        if (v > a) {
+          b = a;
+          a = v;
+        } else if (v > b) {
+          b = v;
+        }
+      }
+      gsc = gs > 1 ? a + b : a;
+    }
+    unsigned gsel = 0;
+    bool avail = lane < n_group;
+    for (int r = 0; r < topk_group; ++r) {
+      float bv = avail ? gsc : -INFINITY;
+      int bi = avail ? lane : 0x7fffffff;
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      gsel |= 1u << bi;
+      if (lane == bi) avail = false;
+    }
+    // top-K choices inside the kept groups
+    unsigned taken = 0;
+    float pick_s[kMaxK];
+    int pick_e[kMaxK];
+    for (int k = 0; k < K; ++k) {
+      float bv = -INFINITY, bs = 0.f;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int e = j * 32 + lane;
+        if (e < E && !((taken >> j) & 1u) && ((gsel >> (e / gs)) & 1u) &&
+            (ch[j] > bv || (ch[j] == bv && e < be))) {
+          bv = ch[j];
+          be = e;
+          bs = sc[j];
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+        if (ov > bv || (ov == bv && oe < be)) {
+          bv = ov;
+          be = oe;
+          bs = os;
+        }
+      }
+      if ((be & 31) == lane) taken |= 1u << (be >> 5);
+      pick_s[k] = bs;
+      pick_e[k] = be;
+    }
+    float sum = 0.f;
+    for (int k = 0; k < K; ++k) sum += pick_s[k];
+    if (lane < K) {
+      float ps = 0.f;
+      int pe = 0;
+      for (int q = 0; q < K; ++q)
+        if (q == lane) {
+          ps = pick_s[q];
+          pe = pick_e[q];
+        }
+      weights[t * K + lane] = ps / sum * scale;
+      slot_ids[t * K + lane] = e2s ? e2s[pe] : pe;
+      if (expert_ids) expert_ids[t * K + lane] = pe;
+    }
+    __syncwarp();
+  }
+}
+
 // K1 router, lane-per-token variant for compile-time K: a warp stages 32
 // tokens x 32 logits at a time in shared memory (padded rows -> conflict-free
 // lane reads), every lane keeps its token's sorted top-K in registers
@@ -1039,7 +1156,8 @@ __global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ 
                                                 int grad, int push,
                                                 const Offsets* __restrict__ offs,
                                                 const int32_t* __restrict__ gpos_g,
-                                                uint8_t* __restrict__ out) {
+                                                uint8_t* __restrict__ out,
+                                                const uint8_t* __restrict__ addend) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t nvec = w.row_bytes / 16;
@@ -1052,8 +1170,13 @@ __global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ 
   float* ws = s_w[threadIdx.x >> 5];
   for (int64_t t = warp; t < ntok; t += nw) {
     __syncwarp();
-    const int n = gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push, offs,
-                                 gpos_g, srcs, ws);
+    int n = gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push, offs, gpos_g,
+                           srcs, ws);
+    if (addend) {   // e.g. the shared expert's output, added last in fp32
+      srcs[n] = addend + t * w.row_bytes;
+      ws[n] = 1.f;
+      ++n;
+    }
     __syncwarp();
     weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
   }
@@ -1421,7 +1544,8 @@ __global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict
                                                       uint8_t* __restrict__ out, int nchunks, int J,
                                                       int* __restrict__ status,
                                                       int* __restrict__ pipe, int n_red,
-                                                      unsigned long long seq) {
+                                                      unsigned long long seq,
+                                                      const uint8_t* __restrict__ addend) {
   const WorldDev& w = *wp;
   __shared__ int s_role;
   __shared__ const uint8_t* s_src[8][kMaxSrc];
@@ -1488,8 +1612,13 @@ __global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict
     for (int64_t ti = t0 + gw; ti < t1; ti += nw) {
       const int64_t t = (int64_t)s_loc * w.T_r + ti;
       __syncwarp();
-      const int n = gather_sources(w, t, ids, wts, hitmask, nullptr, epos, 3, 0, 1, offs, gpos_g,
-                                   srcs, ws);
+      int n = gather_sources(w, t, ids, wts, hitmask, nullptr, epos, 3, 0, 1, offs, gpos_g,
+                             srcs, ws);
+      if (addend) {
+        srcs[n] = addend + t * w.row_bytes;
+        ws[n] = 1.f;
+        ++n;
+      }
       __syncwarp();
       weighted_row_sum<T, VPL, true>(srcs, ws, n, nvec, lane,
                                      reinterpret_cast<int4*>(out + t * w.row_bytes));
@@ -1987,6 +2116,35 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
   return 0;
 }
 
+HM_API int hm_route_group(const float* logits, int64_t T, int32_t E, int32_t K, int32_t n_group,
+                          int32_t topk_group, const float* bias, float route_scale,
+                          const int32_t* expert_to_slot, int32_t* slot_ids, float* weights,
+                          int32_t* expert_ids, void* stream) {
+  HM_CHECK_ARG(E >= 1 && E <= 512, "hm_route_group: E must be 1..512");
+  HM_CHECK_ARG(n_group >= 1 && n_group <= 32 && E % n_group == 0,
+               "hm_route_group: n_group must be 1..32 and divide E");
+  HM_CHECK_ARG(topk_group >= 1 && topk_group <= n_group, "hm_route_group: bad topk_group");
+  HM_CHECK_ARG(K >= 1 && K <= kMaxK && K <= topk_group * (E / n_group),
+               "hm_route_group: K must be 1..%d and fit in the kept groups", kMaxK);
+  if (T == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = grid_for(T, 8, kSMs * 8);
+  const int per = (E + 31) / 32;
+#define HM_RG(P)                                                                              \
+  k_route_group<P><<<blocks, 256, 0, s>>>(logits, T, E, K, n_group, topk_group, bias,        \
+                                          route_scale, expert_to_slot, slot_ids, weights,   \
+                                          expert_ids)
+  if (per <= 4)
+    HM_RG(4);
+  else if (per <= 8)
+    HM_RG(8);
+  else
+    HM_RG(16);
+#undef HM_RG
+  HM_LAUNCHED();
+  return 0;
+}
+
 // dispatch: plan + notify (+barrier) + pack + barrier.  x: [L*T_r, M] payload
 // rows of this GPU's local source ranks; ids/wts: [L*T_r, K] slot ids + gates.
 HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
@@ -2103,8 +2261,9 @@ static void with_row_type(const WorldDev& h, F&& f) {
 }
 
 // `out`: [L*T_r, M] payload rows.
-HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t mode, void* out,
-                      void* stream) {
+static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32_t mode,
+                        const void* addend_v, void* out, void* stream) {
+  const uint8_t* addend = (const uint8_t*)addend_v;
   HM_CHECK_ARG(w && out, "hm_combine: null argument");
   HM_CHECK_ARG(mode >= 0 && mode <= 3, "hm_combine: mode must be 0..3");
   const int dedup = mode;
@@ -2129,7 +2288,7 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
       SegScope sc(w, kSegGather, s);
       kern<<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->epos, w->offs, w->gpos_g,
                                   (uint8_t*)out, w->nchunks, w->last_J, w->status, w->pipe, n_red,
-                                  w->seq);
+                                  w->seq, addend);
       rc = hm::launch_status();
     });
     return rc;
@@ -2161,7 +2320,7 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   SegScope sc(w, kSegGather, s);
   // local sources: modes 2/3 (pushed returns + same-GPU rows) or one GPU
   const bool local_src = (mode >= 2 || h.P == 1) && !(mode == 1 && !push);
-  if (local_src && w->tma_gather && h.row_bytes % kTmaChunk == 0) {
+  if (local_src && w->tma_gather && h.row_bytes % kTmaChunk == 0 && !addend) {
     if (h.elem == 2) {
       HM_CUDA(cudaFuncSetAttribute(k_gather_tma<__nv_bfloat16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
@@ -2181,10 +2340,23 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
   with_row_type(h, [&](auto t, auto v) {
     k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
         w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
-        (uint8_t*)out);
+        (uint8_t*)out, addend);
   });
   HM_LAUNCHED();
   return 0;
+}
+
+HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t mode, void* out,
+                      void* stream) {
+  return combine_impl(w, wts, ids, mode, nullptr, out, stream);
+}
+
+// combine + an addend row per token (e.g. the shared expert's output), summed
+// in fp32 after the routed rows: out = sum_k w_k y_k + addend
+HM_API int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int32_t mode,
+                          const void* addend, void* out, void* stream) {
+  HM_CHECK_ARG(addend, "hm_combine_add: null addend");
+  return combine_impl(w, wts, ids, mode, addend, out, stream);
 }
 
 // explicit barrier (e.g. after an expert FFN when the raw combine follows)
@@ -2347,7 +2519,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   with_row_type(h, [&](auto t, auto v) {
     k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
         w->d, ids, nullptr, w->hitmask, w->gpos, w->epos, mode, 1, 1, w->offs, w->gpos_g,
-        (uint8_t*)dx);
+        (uint8_t*)dx, nullptr);
   });
   HM_LAUNCHED();
   k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode, dw);

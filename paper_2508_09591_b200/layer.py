@@ -84,6 +84,28 @@ def route_topk(logits: torch.Tensor, top_k: int, expert_to_slot: torch.Tensor | 
     return slot, w, ex
 
 
+def route_group_limited(logits: torch.Tensor, top_k: int, n_group: int, topk_group: int,
+                        bias: torch.Tensor | None = None, route_scale: float = 1.0,
+                        expert_to_slot: torch.Tensor | None = None):
+    """DeepSeek-V3 group-limited gate on the GPU (sigmoid scores, bias-corrected
+    choice, the ``topk_group`` best of ``n_group`` expert groups, top-K inside;
+    weights = picked scores / their sum * ``route_scale``).  Returns (slot_ids
+    int32 [T,K], weights fp32 [T,K], expert_ids int32 [T,K])."""
+    if logits.dtype != torch.float32 or not logits.is_cuda or logits.ndim != 2:
+        raise ValueError("logits must be a 2-D float32 CUDA tensor")
+    logits = logits.contiguous()
+    t, e = logits.shape
+    slot = torch.empty((t, top_k), dtype=torch.int32, device=logits.device)
+    w = torch.empty((t, top_k), dtype=torch.float32, device=logits.device)
+    ex = torch.empty((t, top_k), dtype=torch.int32, device=logits.device)
+    b = None if bias is None else bias.to(device=logits.device, dtype=torch.float32).contiguous()
+    e2s = None if expert_to_slot is None else expert_to_slot.to(device=logits.device,
+                                                               dtype=torch.int32).contiguous()
+    _lib.call("hm_route_group", ptr(logits), t, e, top_k, n_group, topk_group, ptr(b),
+              float(route_scale), ptr(e2s), ptr(slot), ptr(w), ptr(ex), stream_ptr())
+    return slot, w, ex
+
+
 def exchange_handles(mine: bytes, index: int, gpus: int, group=None) -> bytes:
     """All-gather one fixed-size IPC handle per GPU, ordered by GPU index.
 
@@ -191,13 +213,24 @@ class EPWorld:
                   out_ptr, stream_ptr())
 
     def combine(self, slot_ids: torch.Tensor, weights: torch.Tensor, dedup=True,
-                out: torch.Tensor | None = None) -> torch.Tensor:
-        """Gate-weighted sum of the expert outputs (``ymaj``) back at the source."""
+                out: torch.Tensor | None = None,
+                addend: torch.Tensor | None = None) -> torch.Tensor:
+        """Gate-weighted sum of the expert outputs (``ymaj``) back at the source;
+        ``addend`` ([L*T_r, M], payload dtype, e.g. a shared expert's output) is
+        added in fp32 before the final rounding."""
         t = self.local * self.tokens_per_rank
         if out is None:
             out = torch.empty((t, self.hidden), dtype=self.dtype, device="cuda")
-        _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), transport_mode(dedup),
-                  ptr(out), stream_ptr())
+        if addend is None:
+            _lib.call("hm_combine", self._h, ptr(weights), ptr(slot_ids), transport_mode(dedup),
+                      ptr(out), stream_ptr())
+        else:
+            if addend.shape != (t, self.hidden) or addend.dtype != self.dtype \
+                    or not addend.is_contiguous():
+                raise ValueError(f"addend must be a contiguous [{t}, {self.hidden}] "
+                                 f"{self.dtype} tensor")
+            _lib.call("hm_combine_add", self._h, ptr(weights), ptr(slot_ids),
+                      transport_mode(dedup), ptr(addend), ptr(out), stream_ptr())
         return out
 
     def dispatch_grad(self, grad_out: torch.Tensor, slot_ids: torch.Tensor,

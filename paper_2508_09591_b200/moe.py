@@ -15,7 +15,7 @@ import torch
 
 from . import _lib
 from .ffn import FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs, pack_w13
-from .layer import EPWorld, route_topk
+from .layer import EPWorld, route_group_limited, route_topk
 from .migrate import ExpertStore
 from .routing import Placement, RoutingMask, load_placements, save_placements, save_trace
 
@@ -35,9 +35,23 @@ class HierMoELayer:
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int, inter: int,
                  tokens_per_rank: int, gpus: int = 1, gpu_index: int = 0, group=None,
                  dedup=True, seed: int = 0, renormalize: bool = True, grad: bool = False,
-                 n_cap_rows: int = 0, layer_index: int = 0):
-        if inter % 128 or hidden % 256:
-            raise ValueError("hidden must be a multiple of 256 and inter of 128")
+                 n_cap_rows: int = 0, layer_index: int = 0, router: str = "softmax",
+                 n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
+                 shared_inter: int = 0, optimizer_state: bool = True):
+        """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
+        (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
+        / ``route_scale`` and a per-expert score bias).
+        ``shared_inter`` > 0 adds a shared SwiGLU expert run on every local
+        token on a side stream, overlapped with the dispatch, and summed into
+        the combine.  ``optimizer_state`` keeps fp32 master weights and Adam
+        moments in the expert store (moved with an expert on a swap)."""
+        if inter % 128 or hidden % 256 or shared_inter % 128:
+            raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
+        if router not in ("softmax", "dsv3"):
+            raise ValueError(f"unknown router {router!r}")
+        if grad and (router != "softmax" or shared_inter):
+            raise ValueError("backward is implemented for the softmax router without a "
+                             "shared expert")
         self.ranks, self.experts, self.top_k = ranks, experts, top_k
         self.hidden, self.inter = hidden, inter
         self.tokens_per_rank = tokens_per_rank
@@ -61,12 +75,13 @@ class HierMoELayer:
         n_par = 3 * hidden * inter
         # expert state in a symmetric store: bf16 weights (used by the FFN), fp32
         # master weights and Adam moments (moved with the expert on a swap)
-        self.store = ExpertStore(n_loc, {
-            "w13": ((2 * inter, hidden), torch.bfloat16),
-            "w2": ((hidden, inter), torch.bfloat16),
-            "master": ((n_par,), torch.float32),
-            "adam_m": ((n_par,), torch.float32),
-            "adam_v": ((n_par,), torch.float32)}, gpus=gpus, gpu_index=gpu_index, group=group)
+        arrays = {"w13": ((2 * inter, hidden), torch.bfloat16),
+                  "w2": ((hidden, inter), torch.bfloat16)}
+        if optimizer_state:
+            arrays.update({"master": ((n_par,), torch.float32),
+                           "adam_m": ((n_par,), torch.float32),
+                           "adam_v": ((n_par,), torch.float32)})
+        self.store = ExpertStore(n_loc, arrays, gpus=gpus, gpu_index=gpu_index, group=group)
         first = gpu_index * n_loc
         for i in range(n_loc):
             gs = torch.Generator(device="cuda").manual_seed(seed * 100003 + first + i)
@@ -75,9 +90,32 @@ class HierMoELayer:
             w2 = torch.randn(hidden, inter, device="cuda", generator=gs) * inter ** -0.5
             self.store["w13"][i].copy_(pack_w13(w1.to(torch.bfloat16), w3.to(torch.bfloat16))[0])
             self.store["w2"][i].copy_(w2.to(torch.bfloat16))
-            self.store["master"][i].copy_(torch.cat([w1.flatten(), w3.flatten(), w2.flatten()]))
-        self.store["adam_m"].zero_()
-        self.store["adam_v"].zero_()
+            if optimizer_state:
+                self.store["master"][i].copy_(torch.cat([w1.flatten(), w3.flatten(),
+                                                         w2.flatten()]))
+        if optimizer_state:
+            self.store["adam_m"].zero_()
+            self.store["adam_v"].zero_()
+        self.router = router
+        self.n_group, self.topk_group, self.route_scale = n_group, topk_group, route_scale
+        self.score_bias = None
+        if router == "dsv3":
+            gb = torch.Generator(device="cuda").manual_seed(seed + 17)
+            self.score_bias = torch.randn(experts, device="cuda", generator=gb) * 0.01
+        self.shared_inter = shared_inter
+        if shared_inter:
+            gsh = torch.Generator(device="cuda").manual_seed(seed * 7919 + 1)
+            w1 = torch.randn(1, shared_inter, hidden, device="cuda", generator=gsh) * hidden ** -0.5
+            w3 = torch.randn(1, shared_inter, hidden, device="cuda", generator=gsh) * hidden ** -0.5
+            self.w13_shared = pack_w13(w1.to(torch.bfloat16), w3.to(torch.bfloat16))[0].contiguous()
+            self.w2_shared = (torch.randn(hidden, shared_inter, device="cuda", generator=gsh)
+                              * shared_inter ** -0.5).to(torch.bfloat16)
+            t_loc = self.local * tokens_per_rank
+            self._shared_rows = torch.tensor([t_loc], dtype=torch.int32, device="cuda")
+            self._shared_h = torch.empty(t_loc, shared_inter, dtype=torch.bfloat16, device="cuda")
+            self._shared_y = torch.empty(t_loc, hidden, dtype=torch.bfloat16, device="cuda")
+            self._side = torch.cuda.Stream()
+            self._shared_done = torch.cuda.Event()
         self.w13 = self.store["w13"].view(self.local, self.e_loc, 2 * inter, hidden)
         self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
         self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
@@ -120,7 +158,17 @@ class HierMoELayer:
     def route(self, x: torch.Tensor):
         with _tf32():
             logits = x.float() @ self.w_router.T
+        if self.router == "dsv3":
+            return route_group_limited(logits, self.top_k, self.n_group, self.topk_group,
+                                       self.score_bias, self.route_scale, self.expert_to_slot)
         return route_topk(logits, self.top_k, self.expert_to_slot, self.renormalize)
+
+    def shared_forward(self, x: torch.Tensor) -> torch.Tensor:
+        """The shared expert on every local token (one-group tcgen05 FFN)."""
+        expert_ffn_ptrs(x.data_ptr(), x.shape[0], self._shared_rows.data_ptr(), 1,
+                        self.w13_shared[None], self.w2_shared[None], self.hidden,
+                        self.shared_inter, self._shared_h, self._shared_y.data_ptr())
+        return self._shared_y
 
     def experts_forward(self) -> None:
         """SwiGLU FFN of every local rank's experts on its expert-major rows."""
@@ -133,16 +181,26 @@ class HierMoELayer:
                             self.w13[l], self.w2[l], self.hidden, self.inter, self.h, y_ptr)
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        x = x.contiguous()
         slot, w, ex = self.route(x)
         if self.grad:
             self._saved = (x, slot, w, ex)
         if self._trace is not None:
             self._trace.append((self.iteration, ex.clone()))
         self.iteration += 1
+        shared = None
+        if self.shared_inter:   # tensor-bound shared expert beside the link-bound dispatch
+            cur = torch.cuda.current_stream()
+            self._side.wait_stream(cur)
+            with torch.cuda.stream(self._side):
+                shared = self.shared_forward(x)
+                self._shared_done.record(self._side)
         self.world.dispatch(x, slot, w, dedup=self.dedup)
         self.experts_forward()   # expert-major rows are local after the dispatch barrier
+        if shared is not None:
+            torch.cuda.current_stream().wait_event(self._shared_done)
         # hm_combine barriers before the source reads peers' rows (any mode)
-        return self.world.combine(slot, w, dedup=self.dedup, out=out)
+        return self.world.combine(slot, w, dedup=self.dedup, out=out, addend=shared)
 
     __call__ = forward
 

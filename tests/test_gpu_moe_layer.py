@@ -89,3 +89,54 @@ def test_layer_trace_and_placement_files(hm, tmp_path):
     layer.save_placement(tmp_path / "pl2.json")
     assert (tmp_path / "pl2.json").read_bytes() == (tmp_path / "pl.json").read_bytes()
     layer.close()
+
+
+@pytest.mark.parametrize("dedup", [True, "none"])
+def test_layer_dsv3_router_shared_expert(hm, dedup):
+    """DeepSeek-V3-style layer: group-limited sigmoid gate (indices equal the
+    oracle's on the layer's own logits) and a shared expert overlapped with
+    the dispatch and summed into the combine."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    G, E, K, M, I, T_r, Is = 8, 64, 6, 512, 256, 40, 256
+    layer = HierMoELayer(G, E, K, M, I, T_r, dedup=dedup, seed=11, router="dsv3", n_group=4,
+                         topk_group=2, route_scale=2.5, shared_inter=Is, optimizer_state=False)
+    g = torch.Generator(device="cuda").manual_seed(13)
+    x = torch.randn(G * T_r, M, device="cuda", generator=g).to(torch.bfloat16)
+    out = layer(x)
+    torch.cuda.synchronize()
+    layer.world.check_status()
+    slot, w, ex = layer.route(x)
+    from paper_2508_09591_b200.moe import _tf32
+    with _tf32():
+        logits = (x.float() @ layer.w_router.T).cpu().numpy()
+    rs, rw, rex = OM.route_group_limited(logits, K, 4, 2, layer.score_bias.cpu().numpy(), 2.5,
+                                         layer.expert_to_slot.cpu().numpy())
+    assert np.array_equal(ex.cpu().numpy(), rex)
+    np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=1e-6, atol=1e-7)
+    nb = I // 128
+    w13 = layer.w13.reshape(E, 2 * I, M).float().cpu().numpy().reshape(E, nb, 2, 128, M)
+    gate, up = w13[:, :, 0].reshape(E, I, M), w13[:, :, 1].reshape(E, I, M)
+    w2 = layer.w2.reshape(E, M, I).float().cpu().numpy()
+    xs = x.float().cpu().numpy().astype(np.float64)
+
+    def ffn(rows, ga, u, d):
+        a = rows @ ga.T.astype(np.float64)
+        b = rows @ u.T.astype(np.float64)
+        h = torch.tensor(a / (1.0 + np.exp(-a)) * b).to(torch.bfloat16).double().numpy()
+        return h @ d.T.astype(np.float64)
+
+    def expert(rows, slots):
+        o = np.zeros((rows.shape[0], M))
+        for e in np.unique(slots):
+            sel = slots == e
+            o[sel] = ffn(rows[sel], gate[e], up[e], w2[e])
+        return o
+
+    routed = OM.moe_forward(xs, slot.cpu().numpy().astype(np.int64), w.cpu().numpy(), expert)
+    ws = layer.w13_shared.float().cpu().numpy().reshape(Is // 128, 2, 128, M)
+    shared = ffn(xs, ws[:, 0].reshape(Is, M), ws[:, 1].reshape(Is, M),
+                 layer.w2_shared.float().cpu().numpy())
+    ref = routed + shared
+    np.testing.assert_allclose(out.double().cpu().numpy(), ref, rtol=2e-2,
+                               atol=2e-2 * np.abs(ref).max())
+    layer.close()
