@@ -43,4 +43,4 @@ def test_route_group_rejects_bad_args(hm):
     with pytest.raises(ValueError):
         route_group_limited(x, 8, 5, 2)        # 5 does not divide 64
     with pytest.raises(ValueError):
-        route_group_limited(x, 8, 8, 1)        # 8 picks do not fit in one group of 8
+        route_group_limited(x, 8, 16, 1)       # 8 picks do not fit in one group of 4
