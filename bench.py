@@ -202,43 +202,52 @@ def planner_cpu(T: int, K: int = 8) -> dict:
 
 
 def dsv3_layer_forward(G, E, K, M, inter, T_r, world, rank, x, flush, tokens_total, n_l, peaks):
-    """Config C layer forward: DeepSeek-V3 group-limited gate (8 groups, top-4
-    groups, scale 2.5), dedup dispatch, tcgen05 experts, shared expert
-    (I = 2048) on a side stream overlapped with the dispatch, combine + shared
-    sum.  Inference only (no optimizer state: 256 x 44 M-parameter experts)."""
+    """Config C layer forward + backward: DeepSeek-V3 group-limited gate (8
+    groups, top-4 groups, scale 2.5), dedup dispatch, tcgen05 experts, the
+    shared expert (I = 2048) on a side stream overlapped with the dispatch,
+    combine + shared sum; backward through all of it.  No optimizer state
+    (256 experts x 44 M parameters; weights, transposes and grads are bf16)."""
     import torch
     import torch.distributed as dist
     from paper_2508_09591_b200.moe import HierMoELayer
     layer = HierMoELayer(G, E, K, M, inter, T_r, gpus=world, gpu_index=rank, dedup=True,
-                         n_cap_rows=3 * T_r * K, router="dsv3", n_group=8, topk_group=4,
-                         route_scale=2.5, shared_inter=2048, optimizer_state=False)
+                         n_cap_rows=2 * T_r * K, router="dsv3", n_group=8, topk_group=4,
+                         route_scale=2.5, shared_inter=2048, optimizer_state=False, grad=True)
     lout = torch.empty_like(x)
+    gen = torch.Generator(device="cuda").manual_seed(99 + rank)
+    gout = torch.randn(x.shape, device="cuda", generator=gen).to(x.dtype)
     for _ in range(3):
         layer(x, out=lout)
+        layer.backward(gout)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    acc = 0.0
+    acc = np.zeros(2)
     for _ in range(n_l):
         flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
         layer(x, out=lout)
-        e1.record()
-        e1.synchronize()
-        acc += e0.elapsed_time(e1)
-    t = torch.tensor([acc / n_l], dtype=torch.float64, device="cuda")
+        ev[1].record()
+        layer.backward(gout)
+        ev[2].record()
+        ev[2].synchronize()
+        acc += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])]
+    t = torch.tensor(acc / n_l, dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     layer.world.check_status()
     fl = layer.flops_per_forward() + 6 * x.shape[0] * M * 2048
-    ms = float(t.item())
-    out = {"fwd_ms": ms, "fwd_tokens_per_s": tokens_total / (ms * 1e-3),
+    fwd_ms, bwd_ms = (float(v) for v in t.tolist())
+    out = {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "fwd_bwd_ms": fwd_ms + bwd_ms,
+           "fwd_tokens_per_s": tokens_total / (fwd_ms * 1e-3),
+           "fwd_bwd_tokens_per_s": tokens_total / ((fwd_ms + bwd_ms) * 1e-3),
            "router": "dsv3 group-limited (n_group 8, topk_group 4, scale 2.5)",
            "shared_expert_inter": 2048, "inter": inter, "transport": layer.dedup,
            "ffn_flops_per_gpu_incl_shared": int(fl),
-           "layer_tflops": fl / (ms * 1e-3) / 1e12,
-           "note": "forward only; router logits GEMM in torch (cuBLAS TF32)"}
+           "fwd_tflops": fl / (fwd_ms * 1e-3) / 1e12,
+           "fwd_bwd_tflops": 3 * fl / ((fwd_ms + bwd_ms) * 1e-3) / 1e12,
+           "note": "router logits GEMM and gate bwd in torch (cuBLAS TF32)"}
     layer.close()
     return out
 

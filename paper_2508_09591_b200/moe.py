@@ -49,9 +49,6 @@ class HierMoELayer:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
         if router not in ("softmax", "dsv3"):
             raise ValueError(f"unknown router {router!r}")
-        if grad and (router != "softmax" or shared_inter):
-            raise ValueError("backward is implemented for the softmax router without a "
-                             "shared expert")
         self.ranks, self.experts, self.top_k = ranks, experts, top_k
         self.hidden, self.inter = hidden, inter
         self.tokens_per_rank = tokens_per_rank
@@ -116,6 +113,15 @@ class HierMoELayer:
             self._shared_y = torch.empty(t_loc, hidden, dtype=torch.bfloat16, device="cuda")
             self._side = torch.cuda.Stream()
             self._shared_done = torch.cuda.Event()
+            if grad:
+                self.w13t_shared = self.w13_shared.T.contiguous()[None]
+                self.w2t_shared = self.w2_shared.T.contiguous()[None]
+                self.bwd_shared = FFNBackwardScratch(t_loc, 1, hidden, shared_inter)
+                self.dw13_shared = torch.zeros(1, 2 * shared_inter, hidden, dtype=torch.bfloat16,
+                                               device="cuda")
+                self.dw2_shared = torch.zeros(1, hidden, shared_inter, dtype=torch.bfloat16,
+                                              device="cuda")
+                self._shared_dx = torch.empty(t_loc, hidden, dtype=torch.bfloat16, device="cuda")
         self.w13 = self.store["w13"].view(self.local, self.e_loc, 2 * inter, hidden)
         self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
         self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
@@ -210,12 +216,26 @@ class HierMoELayer:
 
         combine bwd (dedup broadcast of dL/dout, replaying the forward plan)
         -> expert FFN bwd (tcgen05) -> dispatch bwd (dedup reduction) ->
-        softmax top-K bwd -> router GEMM bwd (cuBLAS).
+        gate bwd (softmax top-K, or the DeepSeek-V3 normalised sigmoid) ->
+        router GEMM bwd (cuBLAS); the shared expert's FFN backward (tcgen05)
+        runs on a side stream beside the routed path.
         """
         if not self.grad or self._saved is None:
             raise RuntimeError("HierMoELayer.backward needs grad=True and a forward first")
         x, slot, w, ex = self._saved
-        dw = self.world.dispatch_grad(grad_out.contiguous(), slot, w, dedup=self.dedup)
+        g = grad_out.contiguous()
+        if self.shared_inter:   # shared expert backward beside the routed one
+            cur = torch.cuda.current_stream()
+            self._side.wait_stream(cur)
+            with torch.cuda.stream(self._side):
+                expert_ffn_backward_ptrs(x.data_ptr(), x.shape[0], self._shared_rows.data_ptr(),
+                                         1, self.w13_shared[None], self.w13t_shared,
+                                         self.w2t_shared, g.data_ptr(), self.hidden,
+                                         self.shared_inter, self.bwd_shared,
+                                         self._shared_dx.data_ptr(), self.dw13_shared,
+                                         self.dw2_shared)
+                self._shared_done.record(self._side)
+        dw = self.world.dispatch_grad(g, slot, w, dedup=self.dedup)
         p_ne, _ = self.world.buffer("n_e", 0)
         for l in range(self.local):
             rank = self.gpu_index * self.local + l
@@ -227,19 +247,31 @@ class HierMoELayer:
                                      self.hidden, self.inter, self.bwd, gx_ptr, self.dw13[l],
                                      self.dw2[l])
         dx = self.world.combine_grad(slot, dw, dedup=self.dedup)
-        # softmax over the K picks (renormalised) or over all experts
-        if self.renormalize:
+        if self.router == "dsv3":
+            # w_k = c s_k / S, s = sigmoid(logit); the bias only steers selection
+            with _tf32():
+                logits = x.float() @ self.w_router.T
+            sk = torch.sigmoid(torch.gather(logits, 1, ex.long()))
+            c = self.route_scale
+            ds = (c / sk.sum(dim=1, keepdim=True)) * (dw - (dw * w).sum(dim=1, keepdim=True) / c)
+            dlogits = torch.zeros(x.shape[0], self.experts, device="cuda")
+            dlogits.scatter_(1, ex.long(), ds * sk * (1.0 - sk))
+        elif self.renormalize:   # softmax over the K picks
             dsel = w * (dw - (w * dw).sum(dim=1, keepdim=True))
             dlogits = torch.zeros(x.shape[0], self.experts, device="cuda")
             dlogits.scatter_(1, ex.long(), dsel)
-        else:
+        else:                    # softmax over all experts
             logits = x.float() @ self.w_router.T
             p = torch.softmax(logits, dim=1)
             dp = torch.zeros_like(p).scatter_(1, ex.long(), dw)
             dlogits = p * (dp - (p * dp).sum(dim=1, keepdim=True))
         with _tf32():
             self.dw_router += dlogits.T @ x.float()
-            return (dx.float() + dlogits @ self.w_router).to(x.dtype)
+            dxf = torch.addmm(dx.float(), dlogits, self.w_router)
+        if self.shared_inter:
+            torch.cuda.current_stream().wait_event(self._shared_done)
+            dxf += self._shared_dx.float()
+        return dxf.to(x.dtype)
 
     # --- routing traces and placements in the reference's file formats ---
     def record_trace(self, enabled: bool = True) -> None:

@@ -50,3 +50,65 @@ def test_layer_backward_matches_autograd(hm, dedup):
     got2 = layer.dw2.reshape(E, M, I).float()
     torch.testing.assert_close(got2, w2.grad, rtol=3e-2, atol=3e-2 * w2.grad.abs().max().item())
     layer.close()
+
+
+def test_layer_backward_dsv3_shared_matches_autograd(hm):
+    """DeepSeek-V3-style layer backward: normalised-sigmoid gate (group-limited
+    picks), routed experts and the shared expert, vs fp32 autograd on the same
+    picks (bf16 tolerance)."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    G, E, K, M, I, T_r, Is, c = 8, 32, 4, 256, 128, 32, 256, 2.5
+    layer = HierMoELayer(G, E, K, M, I, T_r, dedup=True, seed=4, grad=True, router="dsv3",
+                         n_group=4, topk_group=2, route_scale=c, shared_inter=Is,
+                         optimizer_state=False)
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    x = torch.randn(G * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    gout = torch.randn(G * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    out = layer(x)
+    dx = layer.backward(gout)
+    torch.cuda.synchronize()
+    layer.world.check_status()
+    _, slot, w, ex = layer._saved
+    xr = x.float().requires_grad_(True)
+    wr = layer.w_router.clone().requires_grad_(True)
+
+    def split13(w13, n, i):
+        v = w13.reshape(n, i // 128, 2, 128, M).float()
+        return (v[:, :, 0].reshape(n, i, M).clone().requires_grad_(True),
+                v[:, :, 1].reshape(n, i, M).clone().requires_grad_(True))
+
+    w1, w3 = split13(layer.w13, E, I)
+    w2 = layer.w2.reshape(E, M, I).float().clone().requires_grad_(True)
+    s1, s3 = split13(layer.w13_shared, 1, Is)
+    s2 = layer.w2_shared.float().clone().requires_grad_(True)
+    logits = xr @ wr.T
+    sc = torch.sigmoid(torch.gather(logits, 1, ex.long()))
+    gates = sc / sc.sum(dim=1, keepdim=True) * c
+    slots = slot.long()
+    y = torch.zeros_like(xr)
+    for k in range(K):
+        e = slots[:, k]
+        a = torch.einsum("tm,tim->ti", xr, w1[e])
+        b = torch.einsum("tm,tim->ti", xr, w3[e])
+        y = y + gates[:, k:k + 1] * torch.einsum("ti,tmi->tm", torch.nn.functional.silu(a) * b,
+                                                   w2[e])
+    hs = torch.nn.functional.silu(xr @ s1[0].T) * (xr @ s3[0].T)
+    y = y + hs @ s2.T
+    y.backward(gout.float())
+    torch.testing.assert_close(out.float(), y.detach(), rtol=3e-2, atol=3e-2)
+    torch.testing.assert_close(dx.float(), xr.grad, rtol=3e-2, atol=3e-2 * xr.grad.abs().max().item())
+    torch.testing.assert_close(layer.dw_router, wr.grad, rtol=3e-2,
+                               atol=3e-2 * wr.grad.abs().max().item())
+    nb = I // 128
+    d13 = torch.stack([w1.grad.view(E, nb, 128, M), w3.grad.view(E, nb, 128, M)], dim=2).reshape(E, 2 * I, M)
+    torch.testing.assert_close(layer.dw13.reshape(E, 2 * I, M).float(), d13, rtol=3e-2,
+                               atol=3e-2 * d13.abs().max().item())
+    torch.testing.assert_close(layer.dw2.reshape(E, M, I).float(), w2.grad, rtol=3e-2,
+                               atol=3e-2 * w2.grad.abs().max().item())
+    nbs = Is // 128
+    ds13 = torch.stack([s1.grad.view(1, nbs, 128, M), s3.grad.view(1, nbs, 128, M)], dim=2).reshape(1, 2 * Is, M)
+    torch.testing.assert_close(layer.dw13_shared.float(), ds13, rtol=3e-2,
+                               atol=3e-2 * ds13.abs().max().item())
+    torch.testing.assert_close(layer.dw2_shared[0].float(), s2.grad, rtol=3e-2,
+                               atol=3e-2 * s2.grad.abs().max().item())
+    layer.close()
