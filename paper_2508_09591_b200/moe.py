@@ -47,6 +47,8 @@ class HierMoELayer:
         moments in the expert store (moved with an expert on a swap)."""
         if inter % 128 or hidden % 256 or shared_inter % 128:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
+        if grad and (inter % 256 or shared_inter % 256):
+            raise ValueError("backward needs inter / shared_inter multiples of 256 (GEMM tiles)")
         if router not in ("softmax", "dsv3"):
             raise ValueError(f"unknown router {router!r}")
         self.ranks, self.experts, self.top_k = ranks, experts, top_k

@@ -57,7 +57,7 @@ def test_layer_backward_dsv3_shared_matches_autograd(hm):
     picks), routed experts and the shared expert, vs fp32 autograd on the same
     picks (bf16 tolerance)."""
     from paper_2508_09591_b200.moe import HierMoELayer
-    G, E, K, M, I, T_r, Is, c = 8, 32, 4, 256, 128, 32, 256, 2.5
+    G, E, K, M, I, T_r, Is, c = 8, 32, 4, 256, 256, 32, 256, 2.5
     layer = HierMoELayer(G, E, K, M, I, T_r, dedup=True, seed=4, grad=True, router="dsv3",
                          n_group=4, topk_group=2, route_scale=c, shared_inter=Is,
                          optimizer_state=False)
