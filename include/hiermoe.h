@@ -204,6 +204,10 @@ int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
                            int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
                            void* h, void* ta, void* tb, int64_t kmax, int32_t* layout, void* gx,
                            void* dw13, void* dw2, void* stream);
+/* FFN options (no reference counterpart): 0 = weight-gradient path, 0 (default)
+ * = MN-major tcgen05 operands read the token-major activations directly,
+ * 1 = transposed copies + K-major GEMMs (kept as the comparison path). */
+int hm_ffn_set_option(int32_t option, int32_t value);
 
 /* ---------------- expert migration (K11) ------------------------------------
  * Apply a planned swap (apply_swap, swap.py:255-259) to the physical expert

@@ -110,16 +110,32 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
   return d;
 }
 
+// MN-major (transposed) operand, 128-byte swizzle: each K index is one 128 B
+// line of 64 MN-contiguous elements; 8-line atoms at SBO = 1024 B along K,
+// 64-element MN chunks (separate TMA boxes of 64 lines) at LBO = 8 KB.
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(8192 >> 4) << 16;        // LBO: next 64-element MN chunk
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: next 8 K-lines
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=256
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
+// ... with A and B MN-major (bits 15 / 16: transpose A / B)
+constexpr uint32_t kIdescMN = kIdesc | (1u << 15) | (1u << 16);
 
+template <uint32_t IDESC = kIdesc>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -171,6 +187,11 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
 // 2: weight-gradient mode -- every group g is a full [m_out x N] output
 // (rows g*m_out..), reducing over its own K range [row0_g, row0_g + rows_g)
 // of A [m_out x K_total] and B [N x K_total] (K_total = padded token rows).
+// 3: weight gradient straight from the token-major activations, no
+// transposes: out_g = A_g^T B_g with A [tokens, m_out], B [tokens, N] (the
+// group's tokens are its rows), both operands MN-major in shared memory (TMA
+// boxes of 64 tokens x 64 features, one 128 B line per token); the tail
+// k-block's lines past the group are zeroed before the MMA reads them.
 template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
@@ -197,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tm.start[g] = acc;
       tm.row0[g] = row;
       tm.rows[g] = n;
-      acc += (kMode == 2 ? args.m_out / BM : (n + BM - 1) / BM) * tm.ntile_n;
+      acc += (kMode >= 2 ? args.m_out / BM : (n + BM - 1) / BM) * tm.ntile_n;
       row += n;
     }
     tm.start[args.groups] = acc;
@@ -233,21 +254,83 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
         int g, mt, nt;
         tile_coords(tm, args.groups, t, g, mt, nt);
-        const int arow = kMode == 2 ? mt * BM : tm.row0[g] + mt * BM;
-        const int brow = kMode == 2 ? nt * BN : g * args.N + nt * BN;
-        const int k0 = kMode == 2 ? tm.row0[g] : 0;
-        const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
+        const int arow = kMode >= 2 ? mt * BM : tm.row0[g] + mt * BM;
+        const int brow = kMode >= 2 ? nt * BN : g * args.N + nt * BN;
+        const int k0 = kMode >= 2 ? tm.row0[g] : 0;
+        const int kblocks = kMode == 2   ? tm.rows[g] / BK
+                            : kMode == 3 ? (tm.rows[g] + BK - 1) / BK
+                                         : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           mbar_expect_tx(full + stage, kStageBytes);
-          tma_load_2d(sa + stage * kABytes, &map_a, full + stage, k0 + kb * BK, arow);
-          tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, k0 + kb * BK, brow);
+          if (kMode == 3) {   // 64-token x 64-feature boxes: 2 for A, 4 for B
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sa + stage * kABytes + j * 8192, &map_a, full + stage, arow + 64 * j,
+                          k0 + kb * BK);
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + stage * kBBytes + j * 8192, &map_b, full + stage, brow + 64 * j,
+                          k0 + kb * BK);
+          } else {
+            tma_load_2d(sa + stage * kABytes, &map_a, full + stage, k0 + kb * BK, arow);
+            tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, k0 + kb * BK, brow);
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+    }
+  } else if (warp == 1 && kMode == 3) {
+    // whole warp: lanes zero the tail k-block's lines past the group, lane 0
+    // issues the MMAs (MN-major operands: a 16-token k-step is 16 lines)
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(tempty + acc, acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      const int kblocks = (tm.rows[g] + BK - 1) / BK;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full + stage, phase);
+        const int valid = tm.rows[g] - kb * BK;
+        if (valid < BK) {   // 6 boxes x (64 - valid) lines of 128 B
+          const int nlines = BK - valid;
+          for (int i = lane; i < 6 * nlines * 8; i += 32) {
+            const int box = i / (nlines * 8), rem = i % (nlines * 8);
+            const int line = valid + rem / 8, chunk = rem % 8;
+            uint8_t* base = box < 2 ? sa + stage * kABytes + box * 8192
+                                    : sb + stage * kBBytes + (box - 2) * 8192;
+            *reinterpret_cast<int4*>(base + line * 128 + chunk * 16) = make_int4(0, 0, 0, 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+        }
+        if (lane == 0) {
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * kABytes);
+          const uint32_t b0 = smem_u32(sb + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_bf16<kIdescMN>(d, smem_desc_mn(a0 + k * UK * 128),
+                                smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+          umma_commit(empty + stage);
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) umma_commit(tfull + acc);
+      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -295,10 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int r_in = mt * BM + q * 32 + lane;          // row within group
-      const bool valid = kMode == 2 ? true : r_in < tm.rows[g];
-      const bool zero = kMode == 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
+      const bool valid = kMode >= 2 ? true : r_in < tm.rows[g];
+      const bool zero = kMode >= 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
       __nv_bfloat16* orow =
-          args.out + (kMode == 2 ? (int64_t)g * args.m_out + r_in : (int64_t)(tm.row0[g] + r_in)) *
+          args.out + (kMode >= 2 ? (int64_t)g * args.m_out + r_in : (int64_t)(tm.row0[g] + r_in)) *
                          args.ld_out;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (kMode == 1) {
@@ -509,6 +592,63 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
   return 0;
 }
 
+// token-major [rows][cols] bf16 activations as 64 x 64 boxes (64 features =
+// one 128 B swizzled line per token) for the MN-major weight-gradient mode
+int make_map_mn(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return kInvalid;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return kInvalid;
+  }
+  return 0;
+}
+
+// out[g] ([m_out][N], ld_out) = A_g^T B_g over group g's token rows of
+// A [a_rows][m_out] and B [a_rows][N] (kMode 3)
+int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
+                      const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
+                      cudaStream_t s) {
+  HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
+  HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
+  HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
+  CUtensorMap ma, mb;
+  int st = make_map_mn(&ma, a, (uint64_t)a_rows, (uint64_t)m_out);
+  if (st) return st;
+  st = make_map_mn(&mb, b, (uint64_t)a_rows, (uint64_t)N);
+  if (st) return st;
+  GemmArgs args;
+  args.m_out = m_out;
+  args.n_rows = n_rows;
+  args.groups = groups;
+  args.N = N;
+  args.K = BK;
+  args.swiglu = 0;
+  args.out = reinterpret_cast<__nv_bfloat16*>(out);
+  args.ld_out = ld_out;
+  args.status = nullptr;
+  const size_t smem = kStages * kStageBytes + 1024 + 256;
+  int dev = 0;
+  HM_CUDA(cudaGetDevice(&dev));
+  int sms = kSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  k_grouped_gemm<3><<<sms, kThreads, smem, s>>>(ma, mb, args);
+  HM_LAUNCHED();
+  return 0;
+}
+
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
                 cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0) {
@@ -552,7 +692,17 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   return 0;
 }
 
+int g_wgrad_transposed = 0;   // hm_ffn_set_option(0, 1): transposes + K-major wgrad
+
 }  // namespace
+
+// FFN options: 0 = weight-gradient path (0: MN-major tcgen05 operands read the
+// token-major activations directly, default; 1: transposed copies + K-major)
+HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
+  HM_CHECK_ARG(option == 0, "hm_ffn_set_option: unknown option %d", option);
+  g_wgrad_transposed = value != 0;
+  return 0;
+}
 
 // Grouped GEMM: out[rows of group g] = A[rows of g] . B_g^T (bf16 in, fp32
 // accumulate, bf16 out); groups are consecutive row blocks of A with sizes
@@ -610,19 +760,25 @@ HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* 
   HM_LAUNCHED();
   // data gradient
   if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s))) return st;
-  // weight gradients: transposed activations, reduction over each expert's rows
-  auto transpose = [&](const void* src, int C, void* dst) -> int {
-    dim3 grid((C + 63) / 64, (unsigned)((a_rows + 63) / 64));
-    k_transpose_groups<<<grid, dim3(32, 8), 0, s>>>((const __nv_bfloat16*)src, C, n_rows, groups,
-                                                    row0, col0, (__nv_bfloat16*)dst, kmax);
-    return launch_status();
-  };
-  if ((st = transpose(gy, M, ta))) return st;
-  if ((st = transpose(h, I, tb))) return st;
-  if ((st = launch_gemm(ta, M, tb, groups, n_rows, I, (int)kmax, 0, dw2, I, nullptr, s, M, I))) return st;
-  if ((st = transpose(dg13, 2 * I, ta))) return st;
-  if ((st = transpose(x, M, tb))) return st;
-  if ((st = launch_gemm(ta, 2 * I, tb, groups, n_rows, M, (int)kmax, 0, dw13, M, nullptr, s, 2 * I, M)))
-    return st;
-  return 0;
+  // weight gradients straight from the token-major activations (MN-major
+  // tcgen05 operands), reduction over each expert's own rows
+  if (g_wgrad_transposed) {   // reference path: transposed copies + K-major GEMMs
+    auto transpose = [&](const void* src, int C, void* dst) -> int {
+      dim3 grid((C + 63) / 64, (unsigned)((a_rows + 63) / 64));
+      k_transpose_groups<<<grid, dim3(32, 8), 0, s>>>((const __nv_bfloat16*)src, C, n_rows,
+                                                      groups, row0, col0, (__nv_bfloat16*)dst,
+                                                      kmax);
+      return launch_status();
+    };
+    if ((st = transpose(gy, M, ta))) return st;
+    if ((st = transpose(h, I, tb))) return st;
+    if ((st = launch_gemm(ta, M, tb, groups, n_rows, I, (int)kmax, 0, dw2, I, nullptr, s, M, I)))
+      return st;
+    if ((st = transpose(dg13, 2 * I, ta))) return st;
+    if ((st = transpose(x, M, tb))) return st;
+    return launch_gemm(ta, 2 * I, tb, groups, n_rows, M, (int)kmax, 0, dw13, M, nullptr, s,
+                       2 * I, M);
+  }
+  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s))) return st;
+  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s);
 }

@@ -47,6 +47,12 @@ def expert_ffn_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int, w13: 
               inter, ptr(h), y_ptr, stream_ptr())
 
 
+def set_wgrad_transposed(enabled: bool) -> None:
+    """Weight-gradient GEMMs via transposed copies (True) or straight from the
+    token-major activations with MN-major tcgen05 operands (False, default)."""
+    _lib.call("hm_ffn_set_option", 0, int(bool(enabled)))
+
+
 class FFNBackwardScratch:
     """Work buffers of one expert-FFN backward (capacity rows x widths)."""
 
