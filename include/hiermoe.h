@@ -196,6 +196,12 @@ int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t groups
 int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                   const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                   void* y, void* stream);
+/* Training forward: as hm_expert_ffn, and GEMM1's epilogue also stores the
+ * gate/up pre-activations g13 [a_rows][2I] (bf16, 128-column gate/up blocks)
+ * for hm_expert_ffn_backward_saved. */
+int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                       const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
+                       void* y, void* g13, void* stream);
 /* Expert FFN backward: recomputed pre-activations, dgrad GEMMs with
  * transposed weights (w13t [g][M][2I], w2t [g][I][M]), SwiGLU backward, and
  * weight-gradient GEMMs over each expert's own token range. */
@@ -204,6 +210,13 @@ int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
                            int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
                            void* h, void* ta, void* tb, int64_t kmax, int32_t* layout, void* gx,
                            void* dw13, void* dw2, void* stream);
+/* hm_expert_ffn_backward with g13 holding the forward's pre-activations
+ * (hm_expert_ffn_save): skips the GEMM1 recompute. */
+int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                 int32_t groups, const void* w13t, const void* w2t,
+                                 const void* gy, int32_t hidden, int32_t inter, const void* g13,
+                                 void* dh, void* dg13, void* h, void* ta, void* tb, int64_t kmax,
+                                 int32_t* layout, void* gx, void* dw13, void* dw2, void* stream);
 /* FFN options (no reference counterpart): 0 = weight-gradient path, 0 (default)
  * = MN-major tcgen05 operands read the token-major activations directly,
  * 1 = transposed copies + K-major GEMMs (kept as the comparison path). */

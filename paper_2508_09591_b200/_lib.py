@@ -89,6 +89,13 @@ _SIGS = {
                                          c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_expert_ffn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    "hm_expert_ffn_save": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                     c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "hm_expert_ffn_backward_saved": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p,
+                                               c_void_p, c_void_p, c_int32, c_int32, c_void_p,
+                                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                               c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                               c_void_p]),
 }
 
 

@@ -49,6 +49,7 @@ struct GemmArgs {
   int swiglu;             // 1: out = silu(gate) * up, out_cols = N / 2
   __nv_bfloat16* out;     // [rows, out_cols]
   int64_t ld_out;         // elements
+  __nv_bfloat16* out2;    // SwiGLU mode: optional pre-activations [rows, N] (gate/up blocks)
   int* status;
 };
 
@@ -403,6 +404,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int4* src = reinterpret_cast<const int4*>(hv);
 #pragma unroll
             for (int i = 0; i < 4; ++i) dst[i] = src[i];
+            if (args.out2) {   // keep the pre-activations for the backward
+              __nv_bfloat16* prow = args.out2 + (int64_t)(tm.row0[g] + r_in) * args.N + nt * BN;
+              __align__(16) __nv_bfloat162 gb[16], ub[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                gb[i] = __floats2bfloat162_rn(gv[2 * i], gv[2 * i + 1]);
+                ub[i] = __floats2bfloat162_rn(uv[2 * i], uv[2 * i + 1]);
+              }
+              int4* pg = reinterpret_cast<int4*>(prow + c);
+              int4* pu = reinterpret_cast<int4*>(prow + BN / 2 + c);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                pg[i] = reinterpret_cast<const int4*>(gb)[i];
+                pu[i] = reinterpret_cast<const int4*>(ub)[i];
+              }
+            }
           }
         }
       } else {
@@ -636,6 +653,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.swiglu = 0;
   args.out = reinterpret_cast<__nv_bfloat16*>(out);
   args.ld_out = ld_out;
+  args.out2 = nullptr;
   args.status = nullptr;
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
@@ -651,7 +669,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
 
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
-                cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0) {
+                cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0, void* out2 = nullptr) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -669,6 +687,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.swiglu = swiglu;
   args.out = reinterpret_cast<__nv_bfloat16*>(out);
   args.ld_out = ld_out;
+  args.out2 = reinterpret_cast<__nv_bfloat16*>(out2);
   args.status = status;
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
@@ -728,6 +747,19 @@ HM_API int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, i
                      (cudaStream_t)stream);
 }
 
+// ... training forward: GEMM1's epilogue also stores the gate/up
+// pre-activations g13 [a_rows][2I] so the backward needs no recompute
+HM_API int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_rows,
+                              int32_t groups, const void* w13, const void* w2, int32_t hidden,
+                              int32_t inter, void* h, void* y, void* g13, void* stream) {
+  HM_CHECK_ARG(g13, "hm_expert_ffn_save: null g13");
+  int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
+                       (cudaStream_t)stream, 0, 0, g13);
+  if (st) return st;
+  return launch_gemm(h, a_rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
+                     (cudaStream_t)stream);
+}
+
 // Expert SwiGLU FFN backward (tcgen05 GEMMs + elementwise/transposes):
 //   G13 = X W13^T (recomputed pre-activations), dH = gY W2 (via W2^T),
 //   dG13 = swiglu'(G13, dH), H = swiglu(G13), gX = dG13 W13 (via W13^T),
@@ -737,19 +769,49 @@ HM_API int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, i
 // ta [max(M, 2I), kmax], tb [max(M, I), kmax] with kmax >= rows + 64*groups;
 // layout: 2*(groups+1) int32 scratch.  Outputs: gx [rows, M],
 // dw13 [groups][2I][M], dw2 [groups][M][I].
+static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                        const void* w13, const void* w13t, const void* w2t, const void* gy,
+                        int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
+                        void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
+                        void* gx, void* dw13, void* dw2, void* stream);
+
 HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
                                   int32_t groups, const void* w13, const void* w13t,
                                   const void* w2t, const void* gy, int32_t hidden, int32_t inter,
                                   void* g13, void* dh, void* dg13, void* h, void* ta, void* tb,
                                   int64_t kmax, int32_t* layout, void* gx, void* dw13, void* dw2,
                                   void* stream) {
+  return ffn_backward(x, a_rows, n_rows, groups, w13, w13t, w2t, gy, hidden, inter, g13, 0, dh,
+                      dg13, h, ta, tb, kmax, layout, gx, dw13, dw2, stream);
+}
+
+// ... with g13 already holding the forward's pre-activations
+// (hm_expert_ffn_save): no GEMM1 recompute
+HM_API int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                        int32_t groups, const void* w13t, const void* w2t,
+                                        const void* gy, int32_t hidden, int32_t inter,
+                                        const void* g13, void* dh, void* dg13, void* h, void* ta,
+                                        void* tb, int64_t kmax, int32_t* layout, void* gx,
+                                        void* dw13, void* dw2, void* stream) {
+  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
+                      const_cast<void*>(g13), 1, dh, dg13, h, ta, tb, kmax, layout, gx, dw13, dw2,
+                      stream);
+}
+
+static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                        const void* w13, const void* w13t, const void* w2t, const void* gy,
+                        int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
+                        void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
+                        void* gx, void* dw13, void* dw2, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   HM_CHECK_ARG(kmax % BK == 0 && kmax >= a_rows + (int64_t)BK * groups,
                "hm_expert_ffn_backward: kmax must cover the padded rows");
   const int M = hidden, I = inter;
   int st;
-  // recompute gate/up pre-activations, then dH
-  if ((st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I, nullptr, s))) return st;
+  // gate/up pre-activations (recomputed unless the forward saved them), then dH
+  if (!g13_saved &&
+      (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I, nullptr, s)))
+    return st;
   if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s))) return st;
   int32_t* row0 = layout;
   int32_t* col0 = layout + groups + 1;

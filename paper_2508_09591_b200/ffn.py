@@ -47,33 +47,64 @@ def expert_ffn_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int, w13: 
               inter, ptr(h), y_ptr, stream_ptr())
 
 
+_WGRAD_TRANSPOSED = False
+
+
 def set_wgrad_transposed(enabled: bool) -> None:
     """Weight-gradient GEMMs via transposed copies (True) or straight from the
     token-major activations with MN-major tcgen05 operands (False, default)."""
+    global _WGRAD_TRANSPOSED
     _lib.call("hm_ffn_set_option", 0, int(bool(enabled)))
+    _WGRAD_TRANSPOSED = bool(enabled)
+
+
+def expert_ffn_save_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
+                         w13: torch.Tensor, w2: torch.Tensor, hidden: int, inter: int,
+                         h: torch.Tensor, y_ptr: int, g13_ptr: int) -> None:
+    """Training forward: the FFN plus GEMM1's pre-activations into g13_ptr."""
+    _lib.call("hm_expert_ffn_save", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w2), hidden,
+              inter, ptr(h), y_ptr, g13_ptr, stream_ptr())
 
 
 class FFNBackwardScratch:
-    """Work buffers of one expert-FFN backward (capacity rows x widths)."""
+    """Work buffers of one expert-FFN backward (capacity rows x widths).  The
+    transposed-activation buffers (ta, tb) are only allocated for the
+    transposed weight-gradient path."""
 
     def __init__(self, rows: int, groups: int, hidden: int, inter: int):
         kw = dict(dtype=torch.bfloat16, device="cuda")
-        self.rows, self.groups = rows, groups
+        self.rows, self.groups, self.hidden, self.inter = rows, groups, hidden, inter
         self.kmax = (rows + BLOCK // 2 * groups + 63) // 64 * 64 + 64 * groups
         self.g13 = torch.empty(rows, 2 * inter, **kw)
         self.dg13 = torch.empty(rows, 2 * inter, **kw)
         self.dh = torch.empty(rows, inter, **kw)
         self.h = torch.empty(rows, inter, **kw)
-        self.ta = torch.empty(max(hidden, 2 * inter), self.kmax, **kw)
-        self.tb = torch.empty(max(hidden, inter), self.kmax, **kw)
+        self.ta = self.tb = torch.empty(1, **kw)
         self.layout = torch.empty(2 * (groups + 1), dtype=torch.int32, device="cuda")
+
+    def ensure_transposed(self) -> None:
+        if self.ta.numel() == 1:
+            kw = dict(dtype=torch.bfloat16, device="cuda")
+            self.ta = torch.empty(max(self.hidden, 2 * self.inter), self.kmax, **kw)
+            self.tb = torch.empty(max(self.hidden, self.inter), self.kmax, **kw)
 
 
 def expert_ffn_backward_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
                              w13: torch.Tensor, w13t: torch.Tensor, w2t: torch.Tensor,
                              gy_ptr: int, hidden: int, inter: int, sc: FFNBackwardScratch,
-                             gx_ptr: int, dw13: torch.Tensor, dw2: torch.Tensor) -> None:
-    """Grads of the SwiGLU experts: gx (rows), dW13 [g][2I][M], dW2 [g][M][I]."""
+                             gx_ptr: int, dw13: torch.Tensor, dw2: torch.Tensor,
+                             g13_saved_ptr: int = 0) -> None:
+    """Grads of the SwiGLU experts: gx (rows), dW13 [g][2I][M], dW2 [g][M][I].
+    ``g13_saved_ptr``: the forward's pre-activations (expert_ffn_save_ptrs);
+    0 -> recomputed."""
+    if _WGRAD_TRANSPOSED:
+        sc.ensure_transposed()
+    if g13_saved_ptr:
+        _lib.call("hm_expert_ffn_backward_saved", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13t),
+                  ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh), ptr(sc.dg13),
+                  ptr(sc.h), ptr(sc.ta), ptr(sc.tb), sc.kmax, ptr(sc.layout), gx_ptr, ptr(dw13),
+                  ptr(dw2), stream_ptr())
+        return
     _lib.call("hm_expert_ffn_backward", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w13t),
               ptr(w2t), gy_ptr, hidden, inter, ptr(sc.g13), ptr(sc.dh), ptr(sc.dg13), ptr(sc.h),
               ptr(sc.ta), ptr(sc.tb), sc.kmax, ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),

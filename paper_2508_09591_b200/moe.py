@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .ffn import FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs, pack_w13
+from .ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs,
+                  expert_ffn_save_ptrs, pack_w13)
 from .layer import EPWorld, route_group_limited, route_topk
 from .migrate import ExpertStore
 from .routing import Placement, RoutingMask, load_placements, save_placements, save_trace
@@ -124,6 +125,8 @@ class HierMoELayer:
                 self.dw2_shared = torch.zeros(1, hidden, shared_inter, dtype=torch.bfloat16,
                                               device="cuda")
                 self._shared_dx = torch.empty(t_loc, hidden, dtype=torch.bfloat16, device="cuda")
+                self._shared_g13 = torch.empty(t_loc, 2 * shared_inter, dtype=torch.bfloat16,
+                                               device="cuda")
         self.w13 = self.store["w13"].view(self.local, self.e_loc, 2 * inter, hidden)
         self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
         self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
@@ -136,6 +139,9 @@ class HierMoELayer:
         if grad:
             self.refresh_transposed_weights()
             self.bwd = FFNBackwardScratch(self.world.n_cap, self.e_loc, hidden, inter)
+            # the forward keeps GEMM1's pre-activations per local rank (no recompute)
+            self.g13_saved = torch.empty(self.local, self.world.n_cap, 2 * inter,
+                                         dtype=torch.bfloat16, device="cuda")
             self.dw13 = torch.zeros_like(self.w13)
             self.dw2 = torch.zeros_like(self.w2)
             self.dw_router = torch.zeros_like(self.w_router)
@@ -173,9 +179,15 @@ class HierMoELayer:
 
     def shared_forward(self, x: torch.Tensor) -> torch.Tensor:
         """The shared expert on every local token (one-group tcgen05 FFN)."""
-        expert_ffn_ptrs(x.data_ptr(), x.shape[0], self._shared_rows.data_ptr(), 1,
-                        self.w13_shared[None], self.w2_shared[None], self.hidden,
-                        self.shared_inter, self._shared_h, self._shared_y.data_ptr())
+        if self.grad:
+            expert_ffn_save_ptrs(x.data_ptr(), x.shape[0], self._shared_rows.data_ptr(), 1,
+                                 self.w13_shared[None], self.w2_shared[None], self.hidden,
+                                 self.shared_inter, self._shared_h, self._shared_y.data_ptr(),
+                                 self._shared_g13.data_ptr())
+        else:
+            expert_ffn_ptrs(x.data_ptr(), x.shape[0], self._shared_rows.data_ptr(), 1,
+                            self.w13_shared[None], self.w2_shared[None], self.hidden,
+                            self.shared_inter, self._shared_h, self._shared_y.data_ptr())
         return self._shared_y
 
     def experts_forward(self) -> None:
@@ -185,8 +197,14 @@ class HierMoELayer:
             rank = self.gpu_index * self.local + l
             x_ptr, _ = self.world.buffer("xmaj", l)
             y_ptr, _ = self.world.buffer("ymaj", l)
-            expert_ffn_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
-                            self.w13[l], self.w2[l], self.hidden, self.inter, self.h, y_ptr)
+            if self.grad:
+                expert_ffn_save_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
+                                     self.e_loc, self.w13[l], self.w2[l], self.hidden, self.inter,
+                                     self.h, y_ptr, self.g13_saved[l].data_ptr())
+            else:
+                expert_ffn_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
+                                self.e_loc, self.w13[l], self.w2[l], self.hidden, self.inter,
+                                self.h, y_ptr)
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         x = x.contiguous()
@@ -235,7 +253,7 @@ class HierMoELayer:
                                          self.w2t_shared, g.data_ptr(), self.hidden,
                                          self.shared_inter, self.bwd_shared,
                                          self._shared_dx.data_ptr(), self.dw13_shared,
-                                         self.dw2_shared)
+                                         self.dw2_shared, self._shared_g13.data_ptr())
                 self._shared_done.record(self._side)
         dw = self.world.dispatch_grad(g, slot, w, dedup=self.dedup)
         p_ne, _ = self.world.buffer("n_e", 0)
@@ -247,7 +265,7 @@ class HierMoELayer:
             expert_ffn_backward_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
                                      self.e_loc, self.w13[l], self.w13t[l], self.w2t[l], gy_ptr,
                                      self.hidden, self.inter, self.bwd, gx_ptr, self.dw13[l],
-                                     self.dw2[l])
+                                     self.dw2[l], self.g13_saved[l].data_ptr())
         dx = self.world.combine_grad(slot, dw, dedup=self.dedup)
         if self.router == "dsv3":
             # w_k = c s_k / S, s = sigmoid(logit); the bias only steers selection
