@@ -140,3 +140,42 @@ def test_wgrad_paths_agree(hm):
     for a, b in zip(outs[0], outs[1]):
         torch.testing.assert_close(b, a, rtol=1e-2, atol=1e-2 * a.abs().max().item())
     assert torch.count_nonzero(outs[1][0][2]) == 0 and torch.count_nonzero(outs[1][1][2]) == 0
+
+
+def test_saved_preactivations_match_recompute(hm):
+    """Training forward's stored pre-activations + backward without recompute
+    == backward with the GEMM1 recompute (bit for bit)."""
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
+                                           expert_ffn_ptrs, expert_ffn_save_ptrs)
+    torch.manual_seed(6)
+    G, M, I = 3, 512, 256
+    n_rows = [130, 0, 300]
+    cap = sum(n_rows) + 20
+    x = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    w13t = w13.transpose(1, 2).contiguous()
+    w2t = w2.transpose(1, 2).contiguous()
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
+    y0 = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
+    y1 = torch.empty_like(y0)
+    g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
+    expert_ffn_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y0.data_ptr())
+    expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y1.data_ptr(),
+                         g13.data_ptr())
+    rows = sum(n_rows)
+    assert torch.equal(y0[:rows], y1[:rows])
+    res = []
+    for saved in (0, g13.data_ptr()):
+        sc = FFNBackwardScratch(cap, G, M, I)
+        gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+        dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
+        dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
+        expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t,
+                                 gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2, saved)
+        torch.cuda.synchronize()
+        res.append((gx[:rows].clone(), dw13.clone(), dw2.clone()))
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
