@@ -1037,6 +1037,27 @@ __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, con
     weighted_row_sum_any<T, CG>(srcs, ws, n, nvec, lane, dst);
 }
 
+// expert-side source rows of a received row: lane k resolves meta k
+__device__ __forceinline__ int meta_sources_warp(const RowMeta* meta, int K, const uint8_t* ybase,
+                                                 int64_t row_bytes, int grad, int lane,
+                                                 const uint8_t** srcs, float* ws) {
+  bool v = false;
+  RowMeta m;
+  m.epos = -1;
+  m.w = 0.f;
+  if (lane < K) {
+    m = meta[lane];
+    v = m.epos >= 0;
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, v);
+  if (v) {
+    const int pos = __popc(b & ((1u << lane) - 1u));
+    srcs[pos] = ybase + (int64_t)m.epos * row_bytes;
+    ws[pos] = grad ? 1.f : m.w;
+  }
+  return __popc(b);
+}
+
 // reduce (dedup, destination side): partial[i] = sum_k w_k * y[epos_k] over the
 // row's local picks in k order, fp32 accumulation, stored in payload dtype.
 template <typename T, int VPL>
@@ -1064,14 +1085,9 @@ __global__ void __launch_bounds__(256, 3) k_reduce(const WorldDev* __restrict__ 
     __syncwarp();
     const uint8_t** srcs = s_src[threadIdx.x >> 5];
     float* ws = s_w[threadIdx.x >> 5];
-    int n = 0;
-    for (int k = 0; k < w.K; ++k) {
-      RowMeta m = w.recv_meta[dg][r * w.K + k];
-      if (m.epos < 0) continue;
-      srcs[n] = ysrc + (int64_t)m.epos * w.row_bytes;
-      ws[n] = grad ? 1.f : m.w;   // dispatch backward: unweighted sum of input grads
-      ++n;
-    }
+    // dispatch backward (grad): unweighted sum of input grads
+    const int n = meta_sources_warp(w.recv_meta[dg] + r * w.K, w.K, ysrc, w.row_bytes, grad,
+                                    lane, srcs, ws);
     uint8_t* out_row = w.comb[dg] + r * w.row_bytes;
     if (push) {   // store straight into the source rank's return buffer (NVLink if remote)
       int src = 0;
@@ -1144,6 +1160,97 @@ __device__ __forceinline__ int gather_sources(const WorldDev& w, int64_t t, cons
   return n;
 }
 
+// Warp-cooperative gather_sources: lane k resolves pick k, lane q GPU q, lane
+// d rank d, in one round of loads; ballots compact them into the warp's
+// shared-memory source table in the same (summation) order.  Returns n
+// (warp-uniform); the caller __syncwarp()s before reading the table.
+__device__ __forceinline__ int gather_sources_warp(const WorldDev& w, int64_t t, int lane,
+                                                   const int32_t* ids, const float* wts,
+                                                   const unsigned long long* hitmask,
+                                                   const int32_t* gpos, const int32_t* epos,
+                                                   int mode, int grad, int push,
+                                                   const Offsets* offs, const int32_t* gpos_g,
+                                                   const uint8_t** srcs, float* ws) {
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  int n = 0;
+  if (mode != 1) {   // weighted expert rows on this GPU (every pick in mode 0), k order
+    bool v = false;
+    const uint8_t* ptr = nullptr;
+    float wk = 1.f;
+    if (lane < w.K) {
+      const int e = ids[t * w.K + lane];
+      const int ep = epos[t * w.K + lane];
+      if (e >= 0 && ep >= 0) {
+        const int d = e / w.E_loc;
+        if (!(mode >= 2 && d / w.L != w.p)) {
+          v = true;
+          ptr = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
+          if (!grad) wk = wts[t * w.K + lane];
+        }
+      }
+    }
+    const unsigned b = __ballot_sync(full, v);
+    if (v) {
+      const int pos = __popc(b & lt);
+      srcs[pos] = ptr;
+      ws[pos] = wk;
+    }
+    n = __popc(b);
+  }
+  if (mode == 3) {   // pre-reduced rows returned by the other GPUs hit, ascending GPU
+    bool v = false;
+    const uint8_t* ptr = nullptr;
+    if (lane < w.P && lane != w.p) {
+      const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
+      if ((hitmask[t] >> (lane * w.L)) & gmask) {
+        const int g = gpos_g[t * w.P + lane];
+        if (g >= 0) {
+          const int s_loc = (int)(t / w.T_r);
+          const int64_t pos = g - offs->off_g[s_loc][lane];
+          ptr = w.ret_g[w.p * w.L + s_loc] + ((int64_t)lane * w.T_r + pos) * w.row_bytes;
+          v = true;
+        }
+      }
+    }
+    const unsigned b = __ballot_sync(full, v);
+    if (v) {
+      const int pos = n + __popc(b & lt);
+      srcs[pos] = ptr;
+      ws[pos] = 1.f;
+    }
+    n += __popc(b);
+  }
+  if (mode == 1 || mode == 2) {   // partial rows of dedup destinations, ascending rank
+    const unsigned long long hit = hitmask[t];
+    for (int d0 = 0; d0 < w.G; d0 += 32) {
+      const int d = d0 + lane;
+      bool v = false;
+      const uint8_t* ptr = nullptr;
+      if (d < w.G && ((hit >> d) & 1ull) && !(mode == 2 && d / w.L == w.p)) {
+        const int g = gpos[t * w.G + d];
+        if (g >= 0 && g < w.R_cap) {
+          v = true;
+          if (push) {
+            const int s_loc = (int)(t / w.T_r);
+            const int64_t pos = g - offs->off[s_loc][d];
+            ptr = w.ret[w.p * w.L + s_loc] + ((int64_t)d * w.T_r + pos) * w.row_bytes;
+          } else {
+            ptr = w.comb[d] + (int64_t)g * w.row_bytes;
+          }
+        }
+      }
+      const unsigned b = __ballot_sync(full, v);
+      if (v) {
+        const int pos = n + __popc(b & lt);
+        srcs[pos] = ptr;
+        ws[pos] = 1.f;
+      }
+      n += __popc(b);
+    }
+  }
+  return n;
+}
+
 constexpr int kMaxSrc = kMaxRanks > kMaxK ? kMaxRanks : kMaxK;
 
 template <typename T, int VPL>
@@ -1170,8 +1277,8 @@ __global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ 
   float* ws = s_w[threadIdx.x >> 5];
   for (int64_t t = warp; t < ntok; t += nw) {
     __syncwarp();
-    int n = gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push, offs, gpos_g,
-                           srcs, ws);
+    int n = gather_sources_warp(w, t, lane, ids, wts, hitmask, gpos, epos, mode, grad, push,
+                                offs, gpos_g, srcs, ws);
     if (addend) {   // e.g. the shared expert's output, added last in fp32
       srcs[n] = addend + t * w.row_bytes;
       ws[n] = 1.f;
@@ -1374,14 +1481,8 @@ __global__ void __launch_bounds__(256, 3) k_reduce_g(const WorldDev* __restrict_
   const RowMeta* meta = w.meta_g[w.p];
   for (int64_t r = warp; r < total; r += nw) {
     __syncwarp();
-    int n = 0;
-    for (int k = 0; k < w.K; ++k) {
-      RowMeta m = meta[r * w.K + k];
-      if (m.epos < 0) continue;
-      srcs[n] = ybase + (int64_t)m.epos * w.row_bytes;
-      ws[n] = grad ? 1.f : m.w;
-      ++n;
-    }
+    const int n = meta_sources_warp(meta + r * w.K, w.K, ybase, w.row_bytes, grad, lane, srcs,
+                                    ws);
     int src = 0;
     while (src + 1 < w.G && offs->offd_g[src + 1] <= r) ++src;
     const int64_t pos = r - offs->offd_g[src];
@@ -1576,14 +1677,8 @@ __global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict
         int cnt = 0;
         for (int64_t r = r0 + gw; r < r1; r += nw, ++cnt) {
           __syncwarp();
-          int n = 0;
-          for (int kk = 0; kk < w.K; ++kk) {
-            RowMeta m = meta[r * w.K + kk];
-            if (m.epos < 0) continue;
-            srcs[n] = ybase + (int64_t)m.epos * w.row_bytes;
-            ws[n] = m.w;
-            ++n;
-          }
+          const int n = meta_sources_warp(meta + r * w.K, w.K, ybase, w.row_bytes, 0, lane,
+                                          srcs, ws);
           uint8_t* out_row = w.ret_g[s] + ((int64_t)w.p * w.T_r + (r - base)) * w.row_bytes;
           __syncwarp();
           weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
@@ -1612,8 +1707,8 @@ __global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict
     for (int64_t ti = t0 + gw; ti < t1; ti += nw) {
       const int64_t t = (int64_t)s_loc * w.T_r + ti;
       __syncwarp();
-      int n = gather_sources(w, t, ids, wts, hitmask, nullptr, epos, 3, 0, 1, offs, gpos_g,
-                             srcs, ws);
+      int n = gather_sources_warp(w, t, lane, ids, wts, hitmask, nullptr, epos, 3, 0, 1, offs,
+                                  gpos_g, srcs, ws);
       if (addend) {
         srcs[n] = addend + t * w.row_bytes;
         ws[n] = 1.f;
