@@ -217,6 +217,14 @@ int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n
                                  const void* gy, int32_t hidden, int32_t inter, const void* g13,
                                  void* dh, void* dg13, void* h, void* ta, void* tb, int64_t kmax,
                                  int32_t* layout, void* gx, void* dw13, void* dw2, void* stream);
+/* ... adding the weight grads to dw13 / dw2 (fp32 add of the stored bf16)
+ * instead of overwriting them: one call per micro-batch of a layer. */
+int hm_expert_ffn_backward_saved_acc(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                     int32_t groups, const void* w13t, const void* w2t,
+                                     const void* gy, int32_t hidden, int32_t inter,
+                                     const void* g13, void* dh, void* dg13, void* h,
+                                     int32_t* layout, void* gx, void* dw13, void* dw2,
+                                     void* stream);
 /* FFN options (no reference counterpart): 0 = weight-gradient path, 0 (default)
  * = MN-major tcgen05 operands read the token-major activations directly,
  * 1 = transposed copies + K-major GEMMs (kept as the comparison path). */

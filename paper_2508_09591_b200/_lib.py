@@ -67,6 +67,10 @@ _SIGS = {
                                  ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_ffn_set_option": (c_int32, [c_int32, c_int32]),
+    "hm_expert_ffn_backward_saved_acc": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p,
+                                                   c_void_p, c_void_p, c_int32, c_int32, c_void_p,
+                                                   c_void_p, c_void_p, c_void_p, c_void_p,
+                                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
     "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                    c_void_p]),

@@ -50,6 +50,7 @@ struct GemmArgs {
   __nv_bfloat16* out;     // [rows, out_cols]
   int64_t ld_out;         // elements
   __nv_bfloat16* out2;    // SwiGLU mode: optional pre-activations [rows, N] (gate/up blocks)
+  int accumulate;         // modes 2/3: out += result (fp32 add of the stored bf16)
   int* status;
 };
 
@@ -433,9 +434,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (valid) {
             __align__(16) __nv_bfloat162 hv[16];
+            int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
+            if (kMode >= 2 && args.accumulate) {   // weight grads summed over micro-batches
+              __align__(16) __nv_bfloat162 old[16];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(old)[i] = dst[i];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float2 o = __bfloat1622float2(old[i]);
+                v[2 * i] += o.x;
+                v[2 * i + 1] += o.y;
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 16; ++i) hv[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
             const int4* src = reinterpret_cast<const int4*>(hv);
 #pragma unroll
             for (int i = 0; i < 4; ++i) dst[i] = src[i];
@@ -635,7 +647,7 @@ int make_map_mn(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) 
 // A [a_rows][m_out] and B [a_rows][N] (kMode 3)
 int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
                       const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
-                      cudaStream_t s) {
+                      cudaStream_t s, int accumulate = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
   HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
@@ -654,6 +666,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.out = reinterpret_cast<__nv_bfloat16*>(out);
   args.ld_out = ld_out;
   args.out2 = nullptr;
+  args.accumulate = accumulate;
   args.status = nullptr;
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
@@ -688,6 +701,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.out = reinterpret_cast<__nv_bfloat16*>(out);
   args.ld_out = ld_out;
   args.out2 = reinterpret_cast<__nv_bfloat16*>(out2);
+  args.accumulate = 0;
   args.status = status;
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
@@ -773,7 +787,7 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                         const void* w13, const void* w13t, const void* w2t, const void* gy,
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
-                        void* gx, void* dw13, void* dw2, void* stream);
+                        void* gx, void* dw13, void* dw2, void* stream, int accumulate = 0);
 
 HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
                                   int32_t groups, const void* w13, const void* w13t,
@@ -798,12 +812,27 @@ HM_API int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int
                       stream);
 }
 
+// ... and the weight grads added to dw13 / dw2 instead of overwriting them
+// (micro-batched layers: one call per micro-batch)
+HM_API int hm_expert_ffn_backward_saved_acc(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                            int32_t groups, const void* w13t, const void* w2t,
+                                            const void* gy, int32_t hidden, int32_t inter,
+                                            const void* g13, void* dh, void* dg13, void* h,
+                                            int32_t* layout, void* gx, void* dw13, void* dw2,
+                                            void* stream) {
+  HM_CHECK_ARG(!g_wgrad_transposed, "accumulating weight grads need the MN-major path");
+  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
+                      const_cast<void*>(g13), 1, dh, dg13, h, nullptr, nullptr, 0, layout, gx,
+                      dw13, dw2, stream, 1);
+}
+
 static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                         const void* w13, const void* w13t, const void* w2t, const void* gy,
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
-                        void* gx, void* dw13, void* dw2, void* stream) {
+                        void* gx, void* dw13, void* dw2, void* stream, int accumulate) {
   cudaStream_t s = (cudaStream_t)stream;
+  if (g_wgrad_transposed)
   HM_CHECK_ARG(kmax % BK == 0 && kmax >= a_rows + (int64_t)BK * groups,
                "hm_expert_ffn_backward: kmax must cover the padded rows");
   const int M = hidden, I = inter;
@@ -841,6 +870,7 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
     return launch_gemm(ta, 2 * I, tb, groups, n_rows, M, (int)kmax, 0, dw13, M, nullptr, s,
                        2 * I, M);
   }
-  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s))) return st;
-  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s);
+  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate)))
+    return st;
+  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate);
 }

@@ -93,10 +93,19 @@ def expert_ffn_backward_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: i
                              w13: torch.Tensor, w13t: torch.Tensor, w2t: torch.Tensor,
                              gy_ptr: int, hidden: int, inter: int, sc: FFNBackwardScratch,
                              gx_ptr: int, dw13: torch.Tensor, dw2: torch.Tensor,
-                             g13_saved_ptr: int = 0) -> None:
+                             g13_saved_ptr: int = 0, accumulate: bool = False) -> None:
     """Grads of the SwiGLU experts: gx (rows), dW13 [g][2I][M], dW2 [g][M][I].
     ``g13_saved_ptr``: the forward's pre-activations (expert_ffn_save_ptrs);
-    0 -> recomputed."""
+    0 -> recomputed.  ``accumulate``: add the weight grads to dw13 / dw2
+    (needs the saved pre-activations and the MN-major path)."""
+    if accumulate:
+        if not g13_saved_ptr:
+            raise ValueError("accumulate needs the saved pre-activations")
+        _lib.call("hm_expert_ffn_backward_saved_acc", x_ptr, a_rows, n_rows_ptr, groups,
+                  ptr(w13t), ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh),
+                  ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
+                  stream_ptr())
+        return
     if _WGRAD_TRANSPOSED:
         sc.ensure_transposed()
     if g13_saved_ptr:

@@ -38,20 +38,26 @@ class HierMoELayer:
                  dedup=True, seed: int = 0, renormalize: bool = True, grad: bool = False,
                  n_cap_rows: int = 0, layer_index: int = 0, router: str = "softmax",
                  n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
-                 shared_inter: int = 0, optimizer_state: bool = True):
+                 shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1):
         """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
         (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
         / ``route_scale`` and a per-expert score bias).
         ``shared_inter`` > 0 adds a shared SwiGLU expert run on every local
         token on a side stream, overlapped with the dispatch, and summed into
         the combine.  ``optimizer_state`` keeps fp32 master weights and Adam
-        moments in the expert store (moved with an expert on a swap)."""
+        moments in the expert store (moved with an expert on a swap).
+        ``micro_batches`` > 1 splits every local rank's tokens into that many
+        micro-batches, each with its own EP world, issued on separate streams
+        so one micro-batch's exchange overlaps another's expert GEMMs (the
+        expert weight grads are accumulated over micro-batches)."""
         if inter % 128 or hidden % 256 or shared_inter % 128:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
         if grad and (inter % 256 or shared_inter % 256):
             raise ValueError("backward needs inter / shared_inter multiples of 256 (GEMM tiles)")
         if router not in ("softmax", "dsv3"):
             raise ValueError(f"unknown router {router!r}")
+        if micro_batches < 1 or tokens_per_rank % micro_batches:
+            raise ValueError("micro_batches must divide tokens_per_rank")
         self.ranks, self.experts, self.top_k = ranks, experts, top_k
         self.hidden, self.inter = hidden, inter
         self.tokens_per_rank = tokens_per_rank
@@ -62,9 +68,14 @@ class HierMoELayer:
         # for inference and per-remote-rank dedup when gradients are needed
         self.dedup = "remote" if (grad and (dedup is True or dedup == "gpu")) else dedup
         self.renormalize = renormalize
-        self.world = EPWorld(ranks, experts, top_k, hidden, tokens_per_rank,
-                             dtype=torch.bfloat16, gpus=gpus, gpu_index=gpu_index, group=group,
-                             grad=grad, n_cap_rows=n_cap_rows)
+        self.micro_batches = micro_batches
+        t_mb = tokens_per_rank // micro_batches
+        cap_mb = -(-n_cap_rows // micro_batches) if n_cap_rows else 0
+        self.worlds = [EPWorld(ranks, experts, top_k, hidden, t_mb, dtype=torch.bfloat16,
+                               gpus=gpus, gpu_index=gpu_index, group=group, grad=grad,
+                               n_cap_rows=cap_mb) for _ in range(micro_batches)]
+        self.world = self.worlds[0]
+        self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]
         self.grad = grad
         # router replicated on every GPU (seeded identically); experts: the
         # slots of local ranks, seeded by global slot so any GPU count builds
@@ -129,7 +140,9 @@ class HierMoELayer:
                                                device="cuda")
         self.w13 = self.store["w13"].view(self.local, self.e_loc, 2 * inter, hidden)
         self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
-        self.h = torch.empty(self.world.n_cap, inter, dtype=torch.bfloat16, device="cuda")
+        self.hs = [torch.empty(wd.n_cap, inter, dtype=torch.bfloat16, device="cuda")
+                   for wd in self.worlds]
+        self.h = self.hs[0]
         self.set_placement(Placement.identity(experts))
         self._saved = None
         self.group = group
@@ -140,8 +153,9 @@ class HierMoELayer:
             self.refresh_transposed_weights()
             self.bwd = FFNBackwardScratch(self.world.n_cap, self.e_loc, hidden, inter)
             # the forward keeps GEMM1's pre-activations per local rank (no recompute)
-            self.g13_saved = torch.empty(self.local, self.world.n_cap, 2 * inter,
-                                         dtype=torch.bfloat16, device="cuda")
+            self.g13s = [torch.empty(self.local, wd.n_cap, 2 * inter, dtype=torch.bfloat16,
+                                     device="cuda") for wd in self.worlds]
+            self.g13_saved = self.g13s[0]
             self.dw13 = torch.zeros_like(self.w13)
             self.dw2 = torch.zeros_like(self.w2)
             self.dw_router = torch.zeros_like(self.w_router)
@@ -190,21 +204,26 @@ class HierMoELayer:
                             self.shared_inter, self._shared_h, self._shared_y.data_ptr())
         return self._shared_y
 
-    def experts_forward(self) -> None:
-        """SwiGLU FFN of every local rank's experts on its expert-major rows."""
-        p_ne, _ = self.world.buffer("n_e", 0)
+    def experts_forward(self, mb: int = 0) -> None:
+        """SwiGLU FFN of every local rank's experts on its expert-major rows
+        (of micro-batch ``mb``'s world)."""
+        wd, h = self.worlds[mb], self.hs[mb]
+        p_ne, _ = wd.buffer("n_e", 0)
         for l in range(self.local):
             rank = self.gpu_index * self.local + l
-            x_ptr, _ = self.world.buffer("xmaj", l)
-            y_ptr, _ = self.world.buffer("ymaj", l)
+            x_ptr, _ = wd.buffer("xmaj", l)
+            y_ptr, _ = wd.buffer("ymaj", l)
             if self.grad:
-                expert_ffn_save_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
-                                     self.e_loc, self.w13[l], self.w2[l], self.hidden, self.inter,
-                                     self.h, y_ptr, self.g13_saved[l].data_ptr())
+                expert_ffn_save_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
+                                     self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr,
+                                     self.g13s[mb][l].data_ptr())
             else:
-                expert_ffn_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
-                                self.e_loc, self.w13[l], self.w2[l], self.hidden, self.inter,
-                                self.h, y_ptr)
+                expert_ffn_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
+                                self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr)
+
+    def _mb_rows(self, mb: int) -> slice:
+        n = self.local * self.tokens_per_rank // self.micro_batches
+        return slice(mb * n, (mb + 1) * n)
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         x = x.contiguous()
@@ -215,18 +234,32 @@ class HierMoELayer:
             self._trace.append((self.iteration, ex.clone()))
         self.iteration += 1
         shared = None
+        cur = torch.cuda.current_stream()
         if self.shared_inter:   # tensor-bound shared expert beside the link-bound dispatch
-            cur = torch.cuda.current_stream()
             self._side.wait_stream(cur)
             with torch.cuda.stream(self._side):
                 shared = self.shared_forward(x)
                 self._shared_done.record(self._side)
-        self.world.dispatch(x, slot, w, dedup=self.dedup)
-        self.experts_forward()   # expert-major rows are local after the dispatch barrier
-        if shared is not None:
-            torch.cuda.current_stream().wait_event(self._shared_done)
-        # hm_combine barriers before the source reads peers' rows (any mode)
-        return self.world.combine(slot, w, dedup=self.dedup, out=out, addend=shared)
+        if out is None:
+            out = torch.empty_like(x)
+        # micro-batch m on stream m: its dispatch / combine (NVLink, HBM) overlap
+        # the other micro-batches' expert GEMMs (tensor cores)
+        for m in range(self.micro_batches):
+            st = self._streams[m]
+            if st is not None:
+                st.wait_stream(cur)
+            with torch.cuda.stream(st if st is not None else cur):
+                rows = self._mb_rows(m)
+                wd = self.worlds[m]
+                wd.dispatch(x[rows], slot[rows], w[rows], dedup=self.dedup)
+                self.experts_forward(m)   # expert-major rows are local after the dispatch
+                if shared is not None:
+                    torch.cuda.current_stream().wait_event(self._shared_done)
+                wd.combine(slot[rows], w[rows], dedup=self.dedup, out=out[rows],
+                           addend=None if shared is None else shared[rows])
+        for st in self._streams[1:]:
+            cur.wait_stream(st)
+        return out
 
     __call__ = forward
 
@@ -255,18 +288,36 @@ class HierMoELayer:
                                          self._shared_dx.data_ptr(), self.dw13_shared,
                                          self.dw2_shared, self._shared_g13.data_ptr())
                 self._shared_done.record(self._side)
-        dw = self.world.dispatch_grad(g, slot, w, dedup=self.dedup)
-        p_ne, _ = self.world.buffer("n_e", 0)
-        for l in range(self.local):
-            rank = self.gpu_index * self.local + l
-            x_ptr, _ = self.world.buffer("xmaj", l)
-            gy_ptr, _ = self.world.buffer("gy", l)
-            gx_ptr, _ = self.world.buffer("gx", l)
-            expert_ffn_backward_ptrs(x_ptr, self.world.n_cap, p_ne + 4 * rank * self.e_loc,
-                                     self.e_loc, self.w13[l], self.w13t[l], self.w2t[l], gy_ptr,
-                                     self.hidden, self.inter, self.bwd, gx_ptr, self.dw13[l],
-                                     self.dw2[l], self.g13_saved[l].data_ptr())
-        dx = self.world.combine_grad(slot, dw, dedup=self.dedup)
+        cur = torch.cuda.current_stream()
+        dw = torch.empty(slot.shape, dtype=torch.float32, device="cuda")
+        dx = torch.empty_like(x)
+        ffn_done = None
+        for m in range(self.micro_batches):
+            st = self._streams[m]
+            if st is not None:
+                st.wait_stream(cur)
+            with torch.cuda.stream(st if st is not None else cur):
+                rows = self._mb_rows(m)
+                wd = self.worlds[m]
+                dw[rows] = wd.dispatch_grad(g[rows], slot[rows], w[rows], dedup=self.dedup)
+                if ffn_done is not None:   # weight grads accumulate in micro-batch order
+                    torch.cuda.current_stream().wait_event(ffn_done)
+                p_ne, _ = wd.buffer("n_e", 0)
+                for l in range(self.local):
+                    rank = self.gpu_index * self.local + l
+                    x_ptr, _ = wd.buffer("xmaj", l)
+                    gy_ptr, _ = wd.buffer("gy", l)
+                    gx_ptr, _ = wd.buffer("gx", l)
+                    expert_ffn_backward_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc,
+                                             self.e_loc, self.w13[l], self.w13t[l], self.w2t[l],
+                                             gy_ptr, self.hidden, self.inter, self.bwd, gx_ptr,
+                                             self.dw13[l], self.dw2[l],
+                                             self.g13s[m][l].data_ptr(), accumulate=m > 0)
+                ffn_done = torch.cuda.Event()
+                ffn_done.record()
+                wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])
+        for st in self._streams[1:]:
+            cur.wait_stream(st)
         if self.router == "dsv3":
             # w_k = c s_k / S, s = sigmoid(logit); the bias only steers selection
             with _tf32():
@@ -341,9 +392,10 @@ class HierMoELayer:
 
     def flops_per_forward(self) -> int:
         """Expert FFN flops of this GPU's last forward (6 * rows * hidden * inter)."""
-        rows = int(self.world.rows_received()[:, 1].sum())
+        rows = sum(int(wd.rows_received()[:, 1].sum()) for wd in self.worlds)
         return 6 * rows * self.hidden * self.inter
 
     def close(self) -> None:
-        self.world.close()
+        for wd in self.worlds:
+            wd.close()
         self.store.close()

@@ -112,3 +112,34 @@ def test_layer_backward_dsv3_shared_matches_autograd(hm):
     torch.testing.assert_close(layer.dw2_shared[0].float(), s2.grad, rtol=3e-2,
                                atol=3e-2 * s2.grad.abs().max().item())
     layer.close()
+
+
+@pytest.mark.parametrize("router", ["softmax", "dsv3"])
+def test_micro_batched_layer_matches_single(hm, router):
+    """Two micro-batches (separate EP worlds on two streams, exchange of one
+    overlapping the other's experts) give the same outputs and input grads
+    bit for bit, and the same weight grads up to the bf16 rounding of the
+    per-micro-batch accumulation."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    G, E, K, M, I, T_r = 8, 32, 4, 256, 256, 64
+    kw = dict(dedup=True, seed=21, grad=True, router=router, optimizer_state=False)
+    if router == "dsv3":
+        kw.update(n_group=4, topk_group=2, route_scale=2.5, shared_inter=256)
+    one = HierMoELayer(G, E, K, M, I, T_r, **kw)
+    two = HierMoELayer(G, E, K, M, I, T_r, micro_batches=2, **kw)
+    gen = torch.Generator(device="cuda").manual_seed(22)
+    x = torch.randn(G * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    gout = torch.randn(G * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    y1, y2 = one(x), two(x)
+    d1, d2 = one.backward(gout), two.backward(gout)
+    torch.cuda.synchronize()
+    for wd in two.worlds:
+        wd.check_status()
+    assert torch.equal(y1, y2)
+    assert torch.equal(d1, d2)
+    torch.testing.assert_close(two.dw_router, one.dw_router, rtol=1e-5, atol=1e-5)
+    for a, b in ((one.dw13, two.dw13), (one.dw2, two.dw2)):
+        torch.testing.assert_close(b.float(), a.float(), rtol=2e-2,
+                                   atol=2e-2 * a.float().abs().max().item())
+    one.close()
+    two.close()
