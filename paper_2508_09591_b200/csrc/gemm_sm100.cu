@@ -39,6 +39,7 @@ constexpr uint32_t kBBytes = BN * BK * 2;   // 32 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr int kMaxGroups = 64;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
+int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid (0 = all SMs)
 
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
@@ -673,6 +674,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
   HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   k_grouped_gemm<3><<<sms, kThreads, smem, s>>>(ma, mb, args);
@@ -708,6 +710,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
   if (wgrad_m_out) {
     HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
@@ -730,10 +733,13 @@ int g_wgrad_transposed = 0;   // hm_ffn_set_option(0, 1): transposes + K-major w
 }  // namespace
 
 // FFN options: 0 = weight-gradient path (0: MN-major tcgen05 operands read the
-// token-major activations directly, default; 1: transposed copies + K-major)
+// token-major activations directly, default; 1: transposed copies + K-major);
+// 1 = cap on the persistent GEMM grid (CTAs; 0 = one per SM, default) so
+// concurrent exchange kernels keep SMs of their own
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option == 0, "hm_ffn_set_option: unknown option %d", option);
-  g_wgrad_transposed = value != 0;
+  HM_CHECK_ARG(option == 0 || option == 1, "hm_ffn_set_option: unknown option %d", option);
+  if (option == 0) g_wgrad_transposed = value != 0;
+  if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
   return 0;
 }
 

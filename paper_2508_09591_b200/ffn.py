@@ -66,6 +66,11 @@ def expert_ffn_save_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
               inter, ptr(h), y_ptr, g13_ptr, stream_ptr())
 
 
+def set_gemm_ctas(n: int) -> None:
+    """Cap the persistent grouped-GEMM grid at n CTAs (0: one per SM)."""
+    _lib.call("hm_ffn_set_option", 1, int(n))
+
+
 class FFNBackwardScratch:
     """Work buffers of one expert-FFN backward (capacity rows x widths).  The
     transposed-activation buffers (ta, tb) are only allocated for the

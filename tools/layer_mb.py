@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="qwen3")
     ap.add_argument("--mbs", type=int, nargs="+", default=[1, 2, 4])
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--gemm-ctas", type=int, nargs="+", default=[0])
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -41,7 +42,9 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(5 + rank)
     x = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
     g = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
-    for mb in args.mbs:
+    from paper_2508_09591_b200.ffn import set_gemm_ctas
+    for mb, ctas in [(m, c) for m in args.mbs for c in args.gemm_ctas]:
+        set_gemm_ctas(ctas)
         layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, grad=True,
                              n_cap_rows=2 * T_r * K, micro_batches=mb, **kw)
         for _ in range(3):
@@ -68,6 +71,7 @@ def main():
             wd.check_status()
         if rank == 0:
             print(json.dumps({"config": args.config, "n_gpus": world, "micro_batches": mb,
+                              "gemm_ctas": ctas,
                               "fwd_ms": round(t[0].item(), 4), "bwd_ms": round(t[1].item(), 4),
                               "fwd_bwd_ms": round(t[0].item() + t[1].item(), 4)}), flush=True)
         layer.close()
