@@ -242,21 +242,32 @@ class HierMoELayer:
                 self._shared_done.record(self._side)
         if out is None:
             out = torch.empty_like(x)
-        # micro-batch m on stream m: its dispatch / combine (NVLink, HBM) overlap
-        # the other micro-batches' expert GEMMs (tensor cores)
+        # micro-batch m on stream m, pipelined: dispatch m follows dispatch m-1
+        # and combine m follows combine m-1, so the exchange of one micro-batch
+        # (NVLink, HBM) runs beside the expert GEMMs of its neighbour (tensor cores)
+        prev_d = prev_c = None
         for m in range(self.micro_batches):
             st = self._streams[m]
             if st is not None:
                 st.wait_stream(cur)
             with torch.cuda.stream(st if st is not None else cur):
+                s_m = torch.cuda.current_stream()
                 rows = self._mb_rows(m)
                 wd = self.worlds[m]
+                if prev_d is not None:
+                    s_m.wait_event(prev_d)
                 wd.dispatch(x[rows], slot[rows], w[rows], dedup=self.dedup)
+                prev_d = torch.cuda.Event()
+                prev_d.record(s_m)
                 self.experts_forward(m)   # expert-major rows are local after the dispatch
                 if shared is not None:
-                    torch.cuda.current_stream().wait_event(self._shared_done)
+                    s_m.wait_event(self._shared_done)
+                if prev_c is not None:
+                    s_m.wait_event(prev_c)
                 wd.combine(slot[rows], w[rows], dedup=self.dedup, out=out[rows],
                            addend=None if shared is None else shared[rows])
+                prev_c = torch.cuda.Event()
+                prev_c.record(s_m)
         for st in self._streams[1:]:
             cur.wait_stream(st)
         return out
