@@ -1956,6 +1956,7 @@ struct hm_world {
   bool pipelined = false;
   int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
   int stages = kStages;        // hm_world_set_option(w, 3, n): target pipeline stages per GPU
+  int max_blocks = 0;          // hm_world_set_option(w, 4, n): grid cap of the exchange kernels
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -1969,6 +1970,12 @@ struct hm_world {
   float seg_ms[16] = {0};
   int seg_used[16] = {0};
 };
+
+// grid of the grid-stride exchange kernels: 8 CTAs per SM, or the caller's
+// cap (leaves SMs to concurrent kernels, e.g. another micro-batch's GEMMs)
+static inline int exch_blocks(const hm_world* w) {
+  return w->max_blocks > 0 ? w->max_blocks : kSMs * 8;
+}
 
 // segment ids for hm_world_timings
 enum Seg { kSegPlan, kSegNotify, kSegPack, kSegBarrier1, kSegExpand, kSegReduce, kSegBarrier2,
@@ -2298,7 +2305,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     return 0;
   }
   const int64_t T = (int64_t)h.L * h.T_r;
-  int blocks = grid_for(T, 8, kSMs * 8);
+  int blocks = grid_for(T, 8, exch_blocks(w));
   {SegScope sc(w, kSegPack, s);
   k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
                                 w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
@@ -2319,7 +2326,7 @@ HM_API int hm_expand(hm_world* w, void* stream) {
   if (w->h.U1) return 0;                             // relay rows are re-dispatched, not expanded
   if (w->last_mode == 3 && w->h.P == 1) return 0;    // one GPU: every row went direct
   if (w->last_J) return 0;                           // pipelined: expanded inside the dispatch
-  int blocks = kSMs * 8;
+  int blocks = exch_blocks(w);
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
   if (w->last_mode == 3)
     k_expand_g<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
@@ -2392,7 +2399,7 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
     SegScope sc(w, kSegReduce, s);
     with_row_type(h, [&](auto t, auto v) {
       k_reduce_g<typename decltype(t)::type, decltype(v)::value>
-          <<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0);
+          <<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs, 0);
     });
     HM_LAUNCHED();
   }
@@ -2400,7 +2407,7 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
     SegScope sc(w, kSegReduce, s);
     with_row_type(h, [&](auto t, auto v) {
       k_reduce<typename decltype(t)::type, decltype(v)::value>
-          <<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 0, 1);
+          <<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs, 0, 1);
     });
     HM_LAUNCHED();
   }
@@ -2411,7 +2418,7 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
     HM_LAUNCHED();
   }
   const int64_t T = (int64_t)h.L * h.T_r;
-  int blocks = grid_for(T, 8, kSMs * 8);
+  int blocks = grid_for(T, 8, exch_blocks(w));
   SegScope sc(w, kSegGather, s);
   // local sources: modes 2/3 (pushed returns + same-GPU rows) or one GPU
   const bool local_src = (mode >= 2 || h.P == 1) && !(mode == 1 && !push);
@@ -2567,7 +2574,7 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
   const int64_t T = (int64_t)h.L * h.T_r;
-  int blocks = grid_for(T, 8, kSMs * 8);
+  int blocks = grid_for(T, 8, exch_blocks(w));
   if (h.elem == 2)
     k_pack_grad<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->hitmask,
                                                       w->gpos, w->epos, mode, dw);
@@ -2581,9 +2588,9 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
   }
   if (mode != 0 && !(h.P == 1 && mode == 2)) {
     if (h.elem == 2)
-      k_expand_grad<__nv_bfloat16><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+      k_expand_grad<__nv_bfloat16><<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs);
     else
-      k_expand_grad<float><<<kSMs * 8, 256, 0, s>>>(w->d, w->offs);
+      k_expand_grad<float><<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs);
     HM_LAUNCHED();
   }
   return 0;
@@ -2601,7 +2608,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   if (mode != 0 && !(h.P == 1 && mode == 2)) {
     with_row_type(h, [&](auto t, auto v) {
       k_reduce<typename decltype(t)::type, decltype(v)::value>
-          <<<kSMs * 8, 256, 0, s>>>(w->d, w->offs, 1, 1);
+          <<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs, 1, 1);
     });
     HM_LAUNCHED();
   }
@@ -2610,7 +2617,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
     HM_LAUNCHED();
   }
   const int64_t T = (int64_t)h.L * h.T_r;
-  int blocks = grid_for(T, 8, kSMs * 8);
+  int blocks = grid_for(T, 8, exch_blocks(w));
   with_row_type(h, [&](auto t, auto v) {
     k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
         w->d, ids, nullptr, w->hitmask, w->gpos, w->epos, mode, 1, 1, w->offs, w->gpos_g,
@@ -2627,7 +2634,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 3, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 4, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -2638,5 +2645,6 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
     HM_CHECK_ARG(value >= 1 && value <= kMaxRanks * kMaxJ, "hm_world_set_option: bad stage count");
     w->stages = value;
   }
+  if (option == 4) w->max_blocks = value > 0 ? value : 0;
   return 0;
 }

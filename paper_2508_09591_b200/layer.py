@@ -261,6 +261,10 @@ class EPWorld:
         """Source-side sum via TMA bulk copies or register loads (default; faster on B200)."""
         _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
 
+    def set_max_blocks(self, n: int) -> None:
+        """Cap the exchange kernels' grid at n CTAs (0: 8 per SM)."""
+        _lib.call("hm_world_set_option", self._h, 4, int(n))
+
     def set_pipelined(self, enabled: bool, push_percent: int | None = None,
                       stages: int | None = None) -> None:
         """Per-GPU dedup at N > 1: one pipelined kernel per direction with
