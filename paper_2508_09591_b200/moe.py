@@ -149,6 +149,7 @@ class HierMoELayer:
         self.layer_index = layer_index
         self.iteration = 0            # forward calls so far (trace "iter" column)
         self._trace = None            # [(iter, expert ids [T_local, K] on device)] when recording
+        self.timeline = None          # [(label, event)] of the forward phases when a list
         if grad:
             self.refresh_transposed_weights()
             self.bwd = FFNBackwardScratch(self.world.n_cap, self.e_loc, hidden, inter)
@@ -256,16 +257,21 @@ class HierMoELayer:
                 wd = self.worlds[m]
                 if prev_d is not None:
                     s_m.wait_event(prev_d)
+                self._mark(f"dispatch{m}")
                 wd.dispatch(x[rows], slot[rows], w[rows], dedup=self.dedup)
                 prev_d = torch.cuda.Event()
                 prev_d.record(s_m)
+                self._mark(f"experts{m}")
                 self.experts_forward(m)   # expert-major rows are local after the dispatch
+                self._mark(f"experts{m}_end")
                 if shared is not None:
                     s_m.wait_event(self._shared_done)
                 if prev_c is not None:
                     s_m.wait_event(prev_c)
+                self._mark(f"combine{m}")
                 wd.combine(slot[rows], w[rows], dedup=self.dedup, out=out[rows],
                            addend=None if shared is None else shared[rows])
+                self._mark(f"combine{m}_end")
                 prev_c = torch.cuda.Event()
                 prev_c.record(s_m)
         for st in self._streams[1:]:
@@ -273,6 +279,12 @@ class HierMoELayer:
         return out
 
     __call__ = forward
+
+    def _mark(self, label: str) -> None:
+        if self.timeline is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.timeline.append((label, ev))
 
     def backward(self, grad_out: torch.Tensor) -> torch.Tensor:
         """Gradients of the last forward: returns dL/dx; accumulates expert

@@ -73,6 +73,15 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         for wd in layer.worlds:
             wd.check_status()
+        # one forward with phase events (stream timeline, µs from the first mark)
+        layer.timeline = []
+        layer(x)
+        torch.cuda.synchronize()
+        t0 = layer.timeline[0][1]
+        tl = {lab: round(t0.elapsed_time(ev) * 1e3, 1) for lab, ev in layer.timeline}
+        layer.timeline = None
+        if rank == 0:
+            print(json.dumps({"timeline_us": tl}), flush=True)
         if rank == 0:
             print(json.dumps({"config": args.config, "n_gpus": world, "micro_batches": mb,
                               "gemm_ctas": ctas, "exch_blocks": xb,
