@@ -247,10 +247,12 @@ class HierMoELayer:
         # and combine m follows combine m-1, so the exchange of one micro-batch
         # (NVLink, HBM) runs beside the expert GEMMs of its neighbour (tensor cores)
         prev_d = prev_c = None
+        ready = torch.cuda.Event()   # routing done: the point every micro-batch starts from
+        ready.record(cur)
         for m in range(self.micro_batches):
             st = self._streams[m]
             if st is not None:
-                st.wait_stream(cur)
+                st.wait_event(ready)
             with torch.cuda.stream(st if st is not None else cur):
                 s_m = torch.cuda.current_stream()
                 rows = self._mb_rows(m)
@@ -315,10 +317,12 @@ class HierMoELayer:
         dw = torch.empty(slot.shape, dtype=torch.float32, device="cuda")
         dx = torch.empty_like(x)
         ffn_done = None
+        ready = torch.cuda.Event()
+        ready.record(cur)
         for m in range(self.micro_batches):
             st = self._streams[m]
             if st is not None:
-                st.wait_stream(cur)
+                st.wait_event(ready)
             with torch.cuda.stream(st if st is not None else cur):
                 rows = self._mb_rows(m)
                 wd = self.worlds[m]
