@@ -274,6 +274,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true", help="skip the full layer forward")
     ap.add_argument("--no-planner", action="store_true", help="skip the swap-planner timing")
+    ap.add_argument("--no-hd2", action="store_true", help="skip config C's two-level timing")
     args = ap.parse_args()
     world, rank, local = dist_env()
     G, E, K, M, T_r, desc = CONFIGS[args.config]
@@ -543,6 +544,57 @@ def main():
                "d2h_bytes_per_step": int(ho[0].numel() * 2),
                "pipeline": "double-buffered: H2D(i+1) and D2H(i-1) overlap step i"}
 
+    # config C's two-level dedup over virtual 2x4 GPU groups (HD2: relay to the
+    # level-1 group, re-dedup inside it) next to the flat per-GPU dedup, and
+    # the reference time model's choice between them under B200 alpha/beta
+    hd2 = None
+    if args.config == "dsv3" and not args.no_hd2:
+        from paper_2508_09591_b200.layer import TwoLevelWorld
+        import paper_2508_09591_b200 as hm
+        from paper_2508_09591_b200.traffic import _Model
+        raw_ep.close()
+        all_ep.close()
+        tw = TwoLevelWorld((2, 4), E, K, M, T_r, gpus=world, gpu_index=rank,
+                           n_cap_rows=2 * T_r * K)
+
+        def step_hd2():
+            slot, wts, _ = route_topk(logits, K)
+            tw.dispatch(x, slot, wts, dedup2="remote")
+            tw.combine(slot, wts, dedup2="remote", out=out)
+
+        for _ in range(max(3, args.warmup)):
+            step_hd2()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        n_h, tot = max(5, args.steps // 4), 0.0
+        for _ in range(n_h):
+            flush.zero_()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record()
+            step_hd2()
+            h1.record()
+            h1.synchronize()
+            tot += h0.elapsed_time(h1)
+        th = torch.tensor([tot / n_h], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(th, op=dist.ReduceOp.MAX)
+        tw.phase1.check_status()
+        tw.phase2.check_status()
+        tw.close()
+        slot_g, _, _ = route_topk(logits, K)
+        topo = hm.build_topology([2, 4], E, M, 2)
+        p = PLANNER_CASES[1][4]
+        red = (lambda t_: dist.all_reduce(t_)) if world > 1 else None
+        mdl = _Model(hm.mask_from_ids(slot_g, E), topo, hm.LevelParams(*p), None, True,
+                     red).fetch()
+        hd2 = {"topology": [2, 4], "ms_per_step": float(th.item()),
+               "vs_flat_per_gpu_dedup": float(th.item()) / ms,
+               "d_star_b200_params": int(mdl.d_star),
+               "model_times_s": [float(v) for v in mdl.times],
+               "note": "time model (B200 alpha/beta) picks d* = 1 (flat) when its t1 < t2; "
+                       "the layer runs the flat per-GPU dedup"}
+
     # full layer forward + backward: gating, dedup dispatch, tcgen05 SwiGLU
     # experts, combine; backward: combine-bwd, tcgen05 FFN bwd, dispatch-bwd
     layer_fwd = None
@@ -642,6 +694,7 @@ def main():
                         "speedup_dedup_vs_nodedup": ms_raw / ms,
                         "link_time_ratio": link_raw / max(link_dedup, 1e-9) if link_dedup else None},
             "pipelined_variant_ms_per_step": ms_pipelined,
+            "hd2_2x4": hd2,
             "dedup_all_ranks": {"ms_per_step": ms_all,
                                 "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_all.tolist())}},
             "comm_bytes": {"dedup_rows_out": rows_dedup_out, "raw_rows_out": rows_raw_out,
