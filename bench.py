@@ -592,8 +592,11 @@ def main():
                "vs_flat_per_gpu_dedup": float(th.item()) / ms,
                "d_star_b200_params": int(mdl.d_star),
                "model_times_s": [float(v) for v in mdl.times],
-               "note": "time model (B200 alpha/beta) picks d* = 1 (flat) when its t1 < t2; "
-                       "the layer runs the flat per-GPU dedup"}
+               "note": "d_star_b200_params: the reference time model's choice (traffic.py:"
+                       "188-221) with the B200 alpha/beta fits; ms_per_step: d = 2 run as two "
+                       "exchanges through relay ranks (TwoLevelWorld).  The layer's per-GPU "
+                       "dedup is the d = 2 copy list at GPU level in one exchange plus the "
+                       "destination's re-expansion (at N = 2 the level-1 groups are the GPUs)"}
 
     # full layer forward + backward: gating, dedup dispatch, tcgen05 SwiGLU
     # experts, combine; backward: combine-bwd, tcgen05 FFN bwd, dispatch-bwd
