@@ -1037,6 +1037,15 @@ __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, con
     weighted_row_sum_any<T, CG>(srcs, ws, n, nvec, lane, dst);
 }
 
+// Bijective spread of [0, n) (multiplication by a prime coprime with n): the
+// destination-side reducers walk their received rows in this order so that
+// at any moment the warps push to every source GPU instead of one source's
+// contiguous range at a time (spreads the NVLink traffic over the peers).
+__device__ __forceinline__ int64_t spread_index(int64_t i, int64_t n) {
+  const int64_t p = (n % 7919) ? 7919 : ((n % 104729) ? 104729 : 1);
+  return (i * p) % n;
+}
+
 // expert-side source rows of a received row: lane k resolves meta k
 __device__ __forceinline__ int meta_sources_warp(const RowMeta* meta, int K, const uint8_t* ybase,
                                                  int64_t row_bytes, int grad, int lane,
@@ -1075,7 +1084,7 @@ __global__ void __launch_bounds__(256, 3) k_reduce(const WorldDev* __restrict__ 
   for (int d = 0; d < w.L; ++d) total += offs->R[d];
   for (int64_t i = warp; i < total; i += nw) {
     int d_loc = 0;
-    int64_t r = i;
+    int64_t r = spread_index(i, total);
     while (r >= offs->R[d_loc]) {
       r -= offs->R[d_loc];
       ++d_loc;
@@ -1479,7 +1488,8 @@ __global__ void __launch_bounds__(256, 3) k_reduce_g(const WorldDev* __restrict_
   const int64_t total = offs->R_g;
   const uint8_t* ybase = grad ? w.gx[w.p * w.L] : w.ymaj[w.p * w.L];
   const RowMeta* meta = w.meta_g[w.p];
-  for (int64_t r = warp; r < total; r += nw) {
+  for (int64_t i = warp; i < total; i += nw) {
+    const int64_t r = spread_index(i, total);
     __syncwarp();
     const int n = meta_sources_warp(meta + r * w.K, w.K, ybase, w.row_bytes, grad, lane, srcs,
                                     ws);
