@@ -1340,6 +1340,76 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
       : "memory");
 }
 
+// Bulk-copy pack for one GPU (every destination local: modes 0, 2, 3 at
+// P = 1): per token one cp.async.bulk load of the row into a per-warp
+// shared-memory slot, then one cp.async.bulk store per pick straight from
+// that slot into the expert-major rows -- the row never passes through
+// registers.  Two slots per warp; a slot is reloaded once the stores issued
+// from it two tokens earlier have finished reading it.
+constexpr int kBulkWarps = 8;
+
+__global__ void __launch_bounds__(kBulkWarps * 32) k_pack_bulk(
+    const WorldDev* __restrict__ wp, const uint8_t* __restrict__ x, const int32_t* __restrict__ ids,
+    const int32_t* __restrict__ chunk_off, const int32_t* __restrict__ rank_e,
+    const int32_t* __restrict__ eoff, int nchunks, int32_t* __restrict__ epos_out,
+    int* __restrict__ status) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  __shared__ __align__(8) uint64_t bars[kBulkWarps][2];
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t rb = (uint32_t)w.row_bytes;
+  uint8_t* slot0 = bulk_smem + (size_t)wid * 2 * rb;
+  if (lane == 0) {
+    mbar_init(&bars[wid][0], 1);
+    mbar_init(&bars[wid][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int C = w.G + w.E + w.P;
+  const int64_t T = (int64_t)w.L * w.T_r;
+  const int64_t nw = (int64_t)gridDim.x * kBulkWarps;
+  uint32_t phase[2] = {0u, 0u};
+  int it = 0;
+  for (int64_t t = (int64_t)blockIdx.x * kBulkWarps + wid; t < T; t += nw, ++it) {
+    const int b = it & 1;
+    uint8_t* slot = slot0 + b * rb;
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      mbar_expect_tx(&bars[wid][b], rb);
+      bulk_load(slot, x + t * w.row_bytes, rb, &bars[wid][b]);
+    }
+    const int s_loc = (int)(t / w.T_r);
+    const int64_t t_in = t - (int64_t)s_loc * w.T_r;
+    const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
+    int my_e = -1, my_ep = -1;
+    if (lane < w.K) {
+      my_e = ids[t * w.K + lane];
+      if (my_e >= 0) {
+        my_ep = eoff[s_loc * w.E + my_e] + coff[w.G + my_e] + rank_e[t * w.K + lane];
+        if (my_ep >= w.N_cap) {
+          atomicExch(status, 2);
+          my_ep = -1;
+        }
+      }
+      epos_out[t * w.K + lane] = my_ep;
+    }
+    if (lane == 0) mbar_wait(&bars[wid][b], phase[b]);
+    // destinations: every lane resolves its own pick's address, lane 0 issues
+    uint8_t* dst = my_ep >= 0 ? w.xmaj[my_e / w.E_loc] + (int64_t)my_ep * w.row_bytes : nullptr;
+    for (int k = 0; k < w.K; ++k) {
+      uint8_t* dk = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)dst, k);
+      if (lane == 0 && dk)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dk),
+                     "r"(smem_addr(slot)), "r"(rb)
+                     : "memory");
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    phase[b] ^= 1u;
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
     k_gather_tma(const WorldDev* __restrict__ wp, const int32_t* __restrict__ ids,
@@ -1967,6 +2037,7 @@ struct hm_world {
   int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
   int stages = kStages;        // hm_world_set_option(w, 3, n): target pipeline stages per GPU
   int max_blocks = 0;          // hm_world_set_option(w, 4, n): grid cap of the exchange kernels
+  bool bulk_pack = true;       // hm_world_set_option(w, 5, 0): register pack on one GPU too
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -2316,10 +2387,24 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   }
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
-  {SegScope sc(w, kSegPack, s);
-  k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
-                                w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
-                                w->gpos, w->epos, w->rank_g, w->gpos_g, w->status);
+  const size_t bulk_smem = (size_t)kBulkWarps * 2 * h.row_bytes;
+  if (w->bulk_pack && h.P == 1 && mode != 1 && !h.U1 && h.row_bytes % 16 == 0 &&
+      bulk_smem <= 200 * 1024) {
+    HM_CUDA(cudaFuncSetAttribute(k_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bulk_smem));
+    int occ = 0;
+    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pack_bulk, kBulkWarps * 32,
+                                                          bulk_smem));
+    const int bb = grid_for(T, kBulkWarps, kSMs * (occ > 0 ? occ : 1));
+    SegScope sc(w, kSegPack, s);
+    k_pack_bulk<<<bb, kBulkWarps * 32, bulk_smem, s>>>(w->d, (const uint8_t*)x, ids,
+                                                       w->chunk_cnt, w->rank_e, w->eoff,
+                                                       w->nchunks, w->epos, w->status);
+  } else {
+    SegScope sc(w, kSegPack, s);
+    k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
+                                  w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
+                                  w->gpos, w->epos, w->rank_g, w->gpos_g, w->status);
   }
   HM_LAUNCHED();
   if (h.P > 1) {
@@ -2644,7 +2729,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 4, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 5, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -2656,5 +2741,6 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
     w->stages = value;
   }
   if (option == 4) w->max_blocks = value > 0 ? value : 0;
+  if (option == 5) w->bulk_pack = value != 0;
   return 0;
 }

@@ -261,6 +261,10 @@ class EPWorld:
         """Source-side sum via TMA bulk copies or register loads (default; faster on B200)."""
         _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
 
+    def set_bulk_pack(self, enabled: bool) -> None:
+        """One-GPU pack via cp.async.bulk copies (default) or register copies."""
+        _lib.call("hm_world_set_option", self._h, 5, int(bool(enabled)))
+
     def set_max_blocks(self, n: int) -> None:
         """Cap the exchange kernels' grid at n CTAs (0: 8 per SM)."""
         _lib.call("hm_world_set_option", self._h, 4, int(n))
