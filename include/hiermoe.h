@@ -139,8 +139,8 @@ int hm_world_barrier(hm_world* w, void* stream);
  *   2: percent (1..99) of the pipelined kernels' CTAs that push (default 50)
  *   3: target pipeline stages per GPU (default 8; stages per source = n / L)
  *   4: grid cap (CTAs) of the exchange kernels (0 = 8 per SM, default)
- *   5: 1 = bulk-copy (TMA) pack when every destination is local (one GPU,
- *      default), 0 = register pack */
+ *   5: 1 = bulk-copy (TMA) pack when every destination is local (one GPU),
+ *      0 = register pack (default; measured faster) */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);
 /* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
  * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */

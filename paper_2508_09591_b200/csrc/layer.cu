@@ -2037,7 +2037,10 @@ struct hm_world {
   int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
   int stages = kStages;        // hm_world_set_option(w, 3, n): target pipeline stages per GPU
   int max_blocks = 0;          // hm_world_set_option(w, 4, n): grid cap of the exchange kernels
-  bool bulk_pack = true;       // hm_world_set_option(w, 5, 0): register pack on one GPU too
+  // hm_world_set_option(w, 5, 1): bulk-copy pack on one GPU (measured 224 vs
+  // 217 us for the register pack, Qwen3 N = 1: the write-heavy pack is bound
+  // by HBM writes either way)
+  bool bulk_pack = false;
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;

@@ -262,7 +262,7 @@ class EPWorld:
         _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
 
     def set_bulk_pack(self, enabled: bool) -> None:
-        """One-GPU pack via cp.async.bulk copies (default) or register copies."""
+        """One-GPU pack via cp.async.bulk copies or register copies (default)."""
         _lib.call("hm_world_set_option", self._h, 5, int(bool(enabled)))
 
     def set_max_blocks(self, n: int) -> None:
