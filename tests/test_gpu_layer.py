@@ -115,6 +115,15 @@ def test_dispatch_combine_parity(hm, name, dedup):
             r = int(rn[d, 0])
             rx = world.read("recv_x", d, dtype, r * M).view(r, M).cpu()
             assert torch.equal(rx.view(xb.dtype), xb[plan.recv_rows(d)])
+    # the bulk-copy pack (one GPU, direct modes) writes the same expert-major rows
+    if dedup != "all":
+        before = [world.read("xmaj", d, dtype, int(rn[d, 1]) * M).clone() for d in range(G)]
+        world.set_bulk_pack(True)
+        world.dispatch(xd, slot, w, dedup=dedup)
+        world.set_bulk_pack(False)
+        torch.cuda.synchronize()
+        for d in range(G):
+            assert torch.equal(world.read("xmaj", d, dtype, int(rn[d, 1]) * M), before[d])
     # combine with a stand-in expert y = x * scale[slot]; both gather variants
     _apply_experts(world, plan, E, dtype)
     world.set_tma_gather(False)
