@@ -17,10 +17,17 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--no-backward", action="store_true")
+    ap.add_argument("--config", default="qwen3", choices=["qwen3", "dsv3"])
     args = ap.parse_args()
-    G, E, K, M, I, T_r = 8, 128, 8, 2048, 768, args.tokens
+    if args.config == "qwen3":
+        G, E, K, M, I, T_r = 8, 128, 8, 2048, 768, args.tokens
+        kw = {}
+    else:
+        G, E, K, M, I, T_r = 8, 256, 8, 7168, 2048, args.tokens
+        kw = dict(router="dsv3", n_group=8, topk_group=4, route_scale=2.5, shared_inter=2048,
+                  optimizer_state=False)
     layer = HierMoELayer(G, E, K, M, I, T_r, dedup=True, grad=not args.no_backward,
-                         n_cap_rows=3 * T_r * K)
+                         n_cap_rows=2 * T_r * K, **kw)
     x = torch.randn(G * T_r, M, device="cuda").to(torch.bfloat16)
     g = torch.randn(G * T_r, M, device="cuda").to(torch.bfloat16)
     for _ in range(args.steps):
