@@ -304,8 +304,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(full + stage, phase);
         const int valid = tm.rows[g] - kb * BK;
-        if (valid < BK) {   // 6 boxes x (64 - valid) lines of 128 B
-          const int nlines = BK - valid;
+        // tail block: MMAs only for the 16-token steps that hold group rows;
+        // the lines of the last partial step past the group are zeroed in all
+        // 6 boxes (at most 15 lines)
+        const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
+        const int zend = ksteps * UK;
+        if (valid < zend) {
+          const int nlines = zend - valid;
           for (int i = lane; i < 6 * nlines * 8; i += 32) {
             const int box = i / (nlines * 8), rem = i % (nlines * 8);
             const int line = valid + rem / 8, chunk = rem % 8;
@@ -320,8 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sa + stage * kABytes);
           const uint32_t b0 = smem_u32(sb + stage * kBBytes);
-#pragma unroll
-          for (int k = 0; k < BK / UK; ++k)
+          for (int k = 0; k < ksteps; ++k)
             umma_bf16<kIdescMN>(d, smem_desc_mn(a0 + k * UK * 128),
                                 smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
           umma_commit(empty + stage);
