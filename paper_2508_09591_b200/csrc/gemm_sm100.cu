@@ -40,6 +40,7 @@ constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr int kMaxGroups = 64;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
 int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid (0 = all SMs)
+int g_gemm_pair = 0;   // hm_ffn_set_option(2, 1): CTA-pair (cta_group::2) kernels for modes 0 / 1
 
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
@@ -198,6 +199,91 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
   int local = t - tm.start[g];
   mt = local / tm.ntile_n;
   nt = local % tm.ntile_n;
+}
+
+// Epilogue of one accumulator tile for the 32 rows of TMEM lane quarter q:
+// TMEM -> fp32 registers -> (SwiGLU / accumulate) -> bf16 row stores.  r_in =
+// this lane's row within group g (weight-gradient modes: output row).
+template <int kMode>
+__device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& tm, int g, int nt,
+                                           int r_in, uint32_t tbase) {
+  const bool valid = kMode >= 2 ? true : r_in < tm.rows[g];
+  const bool zero = kMode >= 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
+  __nv_bfloat16* orow =
+      args.out + (kMode >= 2 ? (int64_t)g * args.m_out + r_in : (int64_t)(tm.row0[g] + r_in)) *
+                     args.ld_out;
+  if (kMode == 1) {
+#pragma unroll 1
+    for (int c = 0; c < BN / 2; c += 32) {
+      float gv[32], uv[32];
+      tmem_ld32x2(tbase + c, tbase + BN / 2 + c, gv, uv);
+      if (valid) {
+        __align__(16) __nv_bfloat162 hv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float g0 = gv[2 * i], g1 = gv[2 * i + 1];
+          float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
+          float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
+          hv[i] = __floats2bfloat162_rn(h0, h1);
+        }
+        int4* dst = reinterpret_cast<int4*>(orow + nt * (BN / 2) + c);
+        const int4* src = reinterpret_cast<const int4*>(hv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = src[i];
+        if (args.out2) {   // keep the pre-activations for the backward
+          __nv_bfloat16* prow = args.out2 + (int64_t)(tm.row0[g] + r_in) * args.N + nt * BN;
+          __align__(16) __nv_bfloat162 gb[16], ub[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            gb[i] = __floats2bfloat162_rn(gv[2 * i], gv[2 * i + 1]);
+            ub[i] = __floats2bfloat162_rn(uv[2 * i], uv[2 * i + 1]);
+          }
+          int4* pg = reinterpret_cast<int4*>(prow + c);
+          int4* pu = reinterpret_cast<int4*>(prow + BN / 2 + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            pg[i] = reinterpret_cast<const int4*>(gb)[i];
+            pu[i] = reinterpret_cast<const int4*>(ub)[i];
+          }
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c2 = 0; c2 < BN; c2 += 64) {
+     float v2[2][32];
+     tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
+#pragma unroll
+     for (int half = 0; half < 2; ++half) {
+      const int c = c2 + 32 * half;
+      float* v = v2[half];
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (valid) {
+        __align__(16) __nv_bfloat162 hv[16];
+        int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
+        if (kMode >= 2 && args.accumulate) {   // weight grads summed over micro-batches
+          __align__(16) __nv_bfloat162 old[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(old)[i] = dst[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 o = __bfloat1622float2(old[i]);
+            v[2 * i] += o.x;
+            v[2 * i + 1] += o.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) hv[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        const int4* src = reinterpret_cast<const int4*>(hv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = src[i];
+      }
+     }
+    }
+  }
 }
 
 // kMode 0: out = A_g B_g^T over row groups; 1: same + SwiGLU epilogue;
@@ -399,84 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int r_in = mt * BM + q * 32 + lane;          // row within group
-      const bool valid = kMode >= 2 ? true : r_in < tm.rows[g];
-      const bool zero = kMode >= 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
-      __nv_bfloat16* orow =
-          args.out + (kMode >= 2 ? (int64_t)g * args.m_out + r_in : (int64_t)(tm.row0[g] + r_in)) *
-                         args.ld_out;
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (kMode == 1) {
-#pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-          float gv[32], uv[32];
-          tmem_ld32x2(tbase + c, tbase + BN / 2 + c, gv, uv);
-          if (valid) {
-            __align__(16) __nv_bfloat162 hv[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float g0 = gv[2 * i], g1 = gv[2 * i + 1];
-              float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
-              float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
-              hv[i] = __floats2bfloat162_rn(h0, h1);
-            }
-            int4* dst = reinterpret_cast<int4*>(orow + nt * (BN / 2) + c);
-            const int4* src = reinterpret_cast<const int4*>(hv);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = src[i];
-            if (args.out2) {   // keep the pre-activations for the backward
-              __nv_bfloat16* prow = args.out2 + (int64_t)(tm.row0[g] + r_in) * args.N + nt * BN;
-              __align__(16) __nv_bfloat162 gb[16], ub[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                gb[i] = __floats2bfloat162_rn(gv[2 * i], gv[2 * i + 1]);
-                ub[i] = __floats2bfloat162_rn(uv[2 * i], uv[2 * i + 1]);
-              }
-              int4* pg = reinterpret_cast<int4*>(prow + c);
-              int4* pu = reinterpret_cast<int4*>(prow + BN / 2 + c);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                pg[i] = reinterpret_cast<const int4*>(gb)[i];
-                pu[i] = reinterpret_cast<const int4*>(ub)[i];
-              }
-            }
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int c2 = 0; c2 < BN; c2 += 64) {
-         float v2[2][32];
-         tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
-#pragma unroll
-         for (int half = 0; half < 2; ++half) {
-          const int c = c2 + 32 * half;
-          float* v = v2[half];
-          if (zero) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          if (valid) {
-            __align__(16) __nv_bfloat162 hv[16];
-            int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
-            if (kMode >= 2 && args.accumulate) {   // weight grads summed over micro-batches
-              __align__(16) __nv_bfloat162 old[16];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(old)[i] = dst[i];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float2 o = __bfloat1622float2(old[i]);
-                v[2 * i] += o.x;
-                v[2 * i + 1] += o.y;
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) hv[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-            const int4* src = reinterpret_cast<const int4*>(hv);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = src[i];
-          }
-         }
-        }
-      }
+      store_tile<kMode>(args, tm, g, nt, r_in,
+                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
@@ -490,6 +500,196 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (modes 0 / 1): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile with tcgen05.mma.cta_group::2 -- each CTA stages 128 rows of
+// A and half (128 rows) of B per k-block (32 KB instead of 48 KB, so 6
+// stages fit), both CTAs' TMA loads complete on the leader's full barrier,
+// the leader's single MMA thread drives both SMs' tensor cores, commits are
+// multicast to both CTAs' barriers, and each CTA's epilogue drains the 128
+// accumulator rows in its own TMEM (arriving on the leader's tmem-empty
+// barrier through the cluster window).
+constexpr int BM2 = 256, kStages2 = 6;
+constexpr uint32_t kHalfBytes = 128 * BK * 2;                 // 16 KB
+constexpr uint32_t kStageBytes2 = 2 * kHalfBytes;             // A half + B half per CTA
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM2 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's smem, completing on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map,
+                                                 uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+template <int kMode>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages2 * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
+  uint64_t* empty = full + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ TileMap tm;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    int acc = 0, row = 0;
+    tm.ntile_n = args.N / BN;
+    for (int g = 0; g < args.groups; ++g) {
+      const int n = args.n_rows[g];
+      tm.start[g] = acc;
+      tm.row0[g] = row;
+      tm.rows[g] = n;
+      acc += (n + BM2 - 1) / BM2 * tm.ntile_n;
+      row += n;
+    }
+    tm.start[args.groups] = acc;
+    tm.total = acc;
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);   // 4 epilogue warps in each CTA of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kblocks = args.K / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < tm.total; t += ncl) {
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        const int arow = tm.row0[g] + mt * BM2 + (int)rank * 128;
+        const int brow = g * args.N + nt * BN + (int)rank * 128;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (leader) mbar_expect_tx(full + stage, 2 * kStageBytes2);
+          tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, kb * BK, arow);
+          tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, kb * BK, brow);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < tm.total; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
+          const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma_bf16_pair(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
+                           (kb | k) ? 1u : 0u);
+          umma_commit_pair(empty + stage);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(tfull + acc);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    int it = 0;
+    for (int t = cid; t < tm.total; t += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int r_in = mt * BM2 + (int)rank * 128 + q * 32 + lane;
+      store_tile<kMode>(args, tm, g, nt, r_in,
+                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
 
 // ---------------------------------------------------------------------------
 // expert FFN backward helpers
@@ -733,6 +933,24 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
+  if (!wgrad_m_out && g_gemm_pair) {   // 256 x 256 tiles on CTA pairs
+    CUtensorMap mb2;
+    st = make_map(&mb2, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, 128);
+    if (st) return st;
+    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
+    const int grid = sms & ~1;
+    if (swiglu) {
+      HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      k_grouped_gemm_pair<1><<<grid, kThreads, smem2, s>>>(ma, mb2, args);
+    } else {
+      HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<0>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      k_grouped_gemm_pair<0><<<grid, kThreads, smem2, s>>>(ma, mb2, args);
+    }
+    HM_LAUNCHED();
+    return 0;
+  }
   if (wgrad_m_out) {
     HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
@@ -757,11 +975,13 @@ int g_wgrad_transposed = 0;   // hm_ffn_set_option(0, 1): transposes + K-major w
 // FFN options: 0 = weight-gradient path (0: MN-major tcgen05 operands read the
 // token-major activations directly, default; 1: transposed copies + K-major);
 // 1 = cap on the persistent GEMM grid (CTAs; 0 = one per SM, default) so
-// concurrent exchange kernels keep SMs of their own
+// concurrent exchange kernels keep SMs of their own; 2 = CTA-pair
+// (cta_group::2, 256 x 256 tiles) kernels for the forward / data-gradient GEMMs
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option == 0 || option == 1, "hm_ffn_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 2, "hm_ffn_set_option: unknown option %d", option);
   if (option == 0) g_wgrad_transposed = value != 0;
   if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
+  if (option == 2) g_gemm_pair = value != 0;
   return 0;
 }
 

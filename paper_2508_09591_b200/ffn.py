@@ -66,6 +66,12 @@ def expert_ffn_save_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
               inter, ptr(h), y_ptr, g13_ptr, stream_ptr())
 
 
+def set_gemm_pair(enabled: bool) -> None:
+    """CTA-pair (cta_group::2, 256 x 256 tiles) kernels for the forward and
+    data-gradient GEMMs."""
+    _lib.call("hm_ffn_set_option", 2, int(bool(enabled)))
+
+
 def set_gemm_ctas(n: int) -> None:
     """Cap the persistent grouped-GEMM grid at n CTAs (0: one per SM)."""
     _lib.call("hm_ffn_set_option", 1, int(n))

@@ -1,0 +1,67 @@
+"""CTA-pair (tcgen05 cta_group::2, 256 x 256 tile) grouped GEMMs vs the
+single-CTA kernels: identical bits (same per-element k order), and vs an fp32
+reference; forward SwiGLU with the stored pre-activations included."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def pair():
+    from paper_2508_09591_b200.ffn import set_gemm_pair
+    yield set_gemm_pair
+    set_gemm_pair(False)
+
+
+@pytest.mark.parametrize("n_rows,N,K", [
+    ([128], 256, 64),
+    ([300, 0, 77, 513], 512, 256),
+    ([1, 129, 255, 256, 257], 256, 2048),
+    ([2048] * 4, 2048, 768),
+])
+def test_pair_gemm_equals_single(hm, pair, n_rows, N, K):
+    from paper_2508_09591_b200.ffn import grouped_gemm
+    torch.manual_seed(0)
+    G = len(n_rows)
+    rows = sum(n_rows)
+    a = torch.randn(max(rows, 1) + 300, K, device="cuda").to(torch.bfloat16)
+    b = (torch.randn(G, N, K, device="cuda") * K ** -0.5).to(torch.bfloat16)
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    pair(False)
+    one = grouped_gemm(a, b, nr)
+    pair(True)
+    two = grouped_gemm(a, b, nr)
+    torch.cuda.synchronize()
+    assert torch.equal(one[:rows], two[:rows])
+    r, refs = 0, []
+    for g, n in enumerate(n_rows):
+        refs.append(a[r:r + n].float() @ b[g].float().T)
+        r += n
+    torch.testing.assert_close(two[:rows].float(), torch.cat(refs), rtol=2e-2, atol=2e-2)
+
+
+def test_pair_swiglu_ffn_equals_single(hm, pair):
+    from paper_2508_09591_b200.ffn import expert_ffn_save_ptrs
+    torch.manual_seed(2)
+    G, M, I = 5, 512, 512
+    n_rows = [700, 0, 129, 1000, 64]
+    cap = sum(n_rows) + 256
+    x = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    res = []
+    for on in (False, True):
+        pair(on)
+        h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
+        y = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
+        g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
+        expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y.data_ptr(),
+                             g13.data_ptr())
+        torch.cuda.synchronize()
+        rows = sum(n_rows)
+        res.append((h[:rows].clone(), y[:rows].clone(), g13[:rows].clone()))
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
