@@ -60,5 +60,9 @@ def run(name, G, M, I, rows_per_group, steps=10):
 
 
 if __name__ == "__main__":
-    run("qwen3_rank", 16, 2048, 768, 2048)
-    run("dsv3_rank", 32, 7168, 2048, 1024)
+    from paper_2508_09591_b200.ffn import set_gemm_pair
+    for pair in (False, True):
+        set_gemm_pair(pair)
+        print(json.dumps({"gemm_pair": pair}))
+        run("qwen3_rank", 16, 2048, 768, 2048)
+        run("dsv3_rank", 32, 7168, 2048, 1024)
