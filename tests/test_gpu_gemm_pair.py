@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 def pair():
     from paper_2508_09591_b200.ffn import set_gemm_pair
     yield set_gemm_pair
-    set_gemm_pair(False)
+    set_gemm_pair(True)   # the library default
 
 
 @pytest.mark.parametrize("n_rows,N,K", [
