@@ -687,6 +687,22 @@ __device__ __forceinline__ int4 ld_cg_v4(const int4* p) {
                : "l"(p));
   return r;
 }
+__device__ __forceinline__ void st_cs_v4(int4* p, int4 v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w));
+}
+__device__ __forceinline__ void st_wb_v4(int4* p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w));
+}
+// pack store flavour (hm_world_set_option 6): 0 L1::no_allocate, 1 .cs, 2 default
+template <int SH>
+__device__ __forceinline__ void st_pack_v4(int4* p, int4 v);
+__device__ __forceinline__ void st_na_v4(int4* p, int4 v);
+template <>
+__device__ __forceinline__ void st_pack_v4<1>(int4* p, int4 v) { st_cs_v4(p, v); }
+template <>
+__device__ __forceinline__ void st_pack_v4<2>(int4* p, int4 v) { st_wb_v4(p, v); }
 __device__ __forceinline__ void st_na_v4(int4* p, int4 v) {
   asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w));
@@ -700,6 +716,7 @@ constexpr int kUnroll = 8;  // 16-B vectors per lane in flight (4 KB per warp)
 // row to every place it goes (direct expert-major rows for picks on this GPU
 // in modes 0/2/3, one row per hit remote GPU in mode 3, one row per hit
 // destination rank in modes 1/2) with its per-row metadata
+template <int SH = 0>
 __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lane,
                                            const uint8_t* __restrict__ x,
                                            const int32_t* __restrict__ ids,
@@ -825,12 +842,18 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) st_na_v4(dst + v, buf[u]);
+        if (v < nvec) {
+          if constexpr (SH == 0)
+            st_na_v4(dst + v, buf[u]);
+          else
+            st_pack_v4<SH>(dst + v, buf[u]);
+        }
       }
     }
   }
 }
 
+template <int SH>
 __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               const uint8_t* __restrict__ x,
                                               const int32_t* __restrict__ ids,
@@ -852,8 +875,8 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t t = warp; t < T; t += nw)
-    pack_token(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs, eoff, nchunks,
-               mode, gpos, epos_out, rank_g, gpos_g, status);
+    pack_token<SH>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs, eoff,
+                   nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
 }
 
 // expand (dedup, destination side): warp per received row -> its local
@@ -2041,6 +2064,7 @@ struct hm_world {
   // 217 us for the register pack, Qwen3 N = 1: the write-heavy pack is bound
   // by HBM writes either way)
   bool bulk_pack = false;
+  int pack_store = 0;          // hm_world_set_option(w, 6, v): pack store hint (0 na, 1 cs, 2 wb)
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -2405,9 +2429,17 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
                                                        w->nchunks, w->epos, w->status);
   } else {
     SegScope sc(w, kSegPack, s);
-    k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
-                                  w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
-                                  w->gpos, w->epos, w->rank_g, w->gpos_g, w->status);
+#define HM_PACK(SH)                                                                          \
+  k_pack<SH><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d, \
+                                    w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode, \
+                                    w->gpos, w->epos, w->rank_g, w->gpos_g, w->status)
+    if (w->pack_store == 1)
+      HM_PACK(1);
+    else if (w->pack_store == 2)
+      HM_PACK(2);
+    else
+      HM_PACK(0);
+#undef HM_PACK
   }
   HM_LAUNCHED();
   if (h.P > 1) {
@@ -2732,7 +2764,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 5, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 6, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -2745,5 +2777,6 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   }
   if (option == 4) w->max_blocks = value > 0 ? value : 0;
   if (option == 5) w->bulk_pack = value != 0;
+  if (option == 6) w->pack_store = value >= 0 && value <= 2 ? value : 0;
   return 0;
 }
