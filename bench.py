@@ -275,6 +275,8 @@ def main():
     ap.add_argument("--no-layer", action="store_true", help="skip the full layer forward")
     ap.add_argument("--no-planner", action="store_true", help="skip the swap-planner timing")
     ap.add_argument("--no-hd2", action="store_true", help="skip config C's two-level timing")
+    ap.add_argument("--pipelined-variant", action="store_true",
+                    help="also time the staged (flag-pipelined) exchange at N > 1")
     args = ap.parse_args()
     world, rank, local = dist_env()
     G, E, K, M, T_r, desc = CONFIGS[args.config]
@@ -373,7 +375,7 @@ def main():
         ms = timed(ep, MODE, args.steps, args.warmup)
     main_launches = launches[MODE]
     ms_pipelined = None
-    if world > 1:   # the same transport as staged kernels with NVLink flags (option, slower)
+    if world > 1 and args.pipelined_variant:   # staged kernels with NVLink flags (slower)
         ep.set_pipelined(True)
         ms_pipelined = timed(ep, MODE, max(3, args.steps // 2), args.warmup)
         ep.set_pipelined(False)
