@@ -716,7 +716,10 @@ constexpr int kUnroll = 8;  // 16-B vectors per lane in flight (4 KB per warp)
 // row to every place it goes (direct expert-major rows for picks on this GPU
 // in modes 0/2/3, one row per hit remote GPU in mode 3, one row per hit
 // destination rank in modes 1/2) with its per-row metadata
-template <int SH = 0>
+// PART: 0 = everything, 1 = the same-GPU expert-major rows only, 2 = the
+// remote-GPU rows (mode 3) only -- the split lets NVLink pushes and local HBM
+// copies run in different warps instead of alternating inside each warp
+template <int SH = 0, int PART = 0>
 __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lane,
                                            const uint8_t* __restrict__ x,
                                            const int32_t* __restrict__ ids,
@@ -749,7 +752,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
         my_ep = -1;
       }
     }
-    epos_out[t * w.K + lane] = my_ep;
+    if (PART != 2) epos_out[t * w.K + lane] = my_ep;
   }
   const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
   unsigned long long hit = hitmask[t];
@@ -758,7 +761,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
   int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
   uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
   // direct expert-major rows: every pick (mode 0) or picks on this GPU (modes 2, 3)
-  if (mode != 1) {
+  if (mode != 1 && PART != 2) {
     for (int k = 0; k < w.K; ++k) {
       int e = __shfl_sync(0xffffffffu, my_e, k);
       int ep = __shfl_sync(0xffffffffu, my_ep, k);
@@ -772,7 +775,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
   }
   // mode 3: one row per (token, other GPU hit); meta carries, per pick on
   // that GPU, its local rank's expert-major row (l * N_cap + epos)
-  if (mode == 3) {
+  if (mode == 3 && PART != 1) {
     for (int q = 0; q < w.P; ++q) {
       if (q == w.p) continue;
       if (!((hit >> (q * w.L)) & gmask)) {
@@ -868,12 +871,25 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               int32_t* __restrict__ epos_out,
                                               const int32_t* __restrict__ rank_g,
                                               int32_t* __restrict__ gpos_g,
-                                              int* __restrict__ status) {
+                                              int* __restrict__ status, int split) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t T = (int64_t)w.L * w.T_r;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  if (split) {   // odd warps push the remote-GPU rows, even warps write the local ones
+    const int64_t nh = nw >> 1;
+    if (warp & 1) {
+      for (int64_t t = warp >> 1; t < T; t += nh)
+        pack_token<SH, 2>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs,
+                          eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
+    } else {
+      for (int64_t t = warp >> 1; t < T; t += nh)
+        pack_token<SH, 1>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs,
+                          eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
+    }
+    return;
+  }
   for (int64_t t = warp; t < T; t += nw)
     pack_token<SH>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs, eoff,
                    nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
@@ -2065,6 +2081,7 @@ struct hm_world {
   // by HBM writes either way)
   bool bulk_pack = false;
   int pack_store = 0;          // hm_world_set_option(w, 6, v): pack store hint (0 na, 1 cs, 2 wb)
+  bool split_pack = true;      // hm_world_set_option(w, 7, 0): one warp does a token's local and remote rows
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -2432,7 +2449,8 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
 #define HM_PACK(SH)                                                                          \
   k_pack<SH><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d, \
                                     w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode, \
-                                    w->gpos, w->epos, w->rank_g, w->gpos_g, w->status)
+                                    w->gpos, w->epos, w->rank_g, w->gpos_g, w->status, split)
+    const int split = (mode == 3 && h.P > 1 && w->split_pack) ? 1 : 0;
     if (w->pack_store == 1)
       HM_PACK(1);
     else if (w->pack_store == 2)
@@ -2764,7 +2782,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 6, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 7, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -2778,5 +2796,6 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   if (option == 4) w->max_blocks = value > 0 ? value : 0;
   if (option == 5) w->bulk_pack = value != 0;
   if (option == 6) w->pack_store = value >= 0 && value <= 2 ? value : 0;
+  if (option == 7) w->split_pack = value != 0;
   return 0;
 }

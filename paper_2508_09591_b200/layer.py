@@ -265,6 +265,11 @@ class EPWorld:
         """One-GPU pack via cp.async.bulk copies or register copies (default)."""
         _lib.call("hm_world_set_option", self._h, 5, int(bool(enabled)))
 
+    def set_split_pack(self, enabled: bool) -> None:
+        """N > 1 per-GPU dedup pack: separate warps for NVLink pushes and
+        local copies (default) or one warp per token for both."""
+        _lib.call("hm_world_set_option", self._h, 7, int(bool(enabled)))
+
     def set_max_blocks(self, n: int) -> None:
         """Cap the exchange kernels' grid at n CTAs (0: 8 per SM)."""
         _lib.call("hm_world_set_option", self._h, 4, int(n))
