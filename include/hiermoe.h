@@ -144,8 +144,8 @@ int hm_world_barrier(hm_world* w, void* stream);
  *   6: pack store hint: 0 = st.global.L1::no_allocate (default), 1 = .cs,
  *      2 = default caching (measured 0.219 / 0.219 / 0.234 ms, Qwen3 N = 1)
  *   7: 1 = per-GPU dedup pack at N > 1 with separate warps for the NVLink
- *      pushes and the local expert-major copies (default), 0 = one warp per
- *      token does both */
+ *      pushes and the local expert-major copies, 0 = one warp per token does
+ *      both (default; the split measured neutral) */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);
 /* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
  * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */

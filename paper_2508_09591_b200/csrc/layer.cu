@@ -2081,7 +2081,9 @@ struct hm_world {
   // by HBM writes either way)
   bool bulk_pack = false;
   int pack_store = 0;          // hm_world_set_option(w, 6, v): pack store hint (0 na, 1 cs, 2 wb)
-  bool split_pack = true;      // hm_world_set_option(w, 7, 0): one warp does a token's local and remote rows
+  // hm_world_set_option(w, 7, 1): separate warps for NVLink pushes and local
+  // copies in the N > 1 pack (measured neutral: 150 vs 152 us at N = 4)
+  bool split_pack = false;
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;

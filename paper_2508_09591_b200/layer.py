@@ -267,7 +267,7 @@ class EPWorld:
 
     def set_split_pack(self, enabled: bool) -> None:
         """N > 1 per-GPU dedup pack: separate warps for NVLink pushes and
-        local copies (default) or one warp per token for both."""
+        local copies, or one warp per token for both (default)."""
         _lib.call("hm_world_set_option", self._h, 7, int(bool(enabled)))
 
     def set_max_blocks(self, n: int) -> None:
