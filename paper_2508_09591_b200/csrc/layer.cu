@@ -712,6 +712,15 @@ constexpr int kUnroll = 8;  // 16-B vectors per lane in flight (4 KB per warp)
 
 // pack: warp per token.  dedup: one copy per hit destination + per-row meta;
 // raw: one copy per selection into expert-major rows.
+// Bijective spread of [0, n) (multiplication by a prime coprime with n): the
+// destination-side reducers walk their received rows in this order so that
+// at any moment the warps push to every source GPU instead of one source's
+// contiguous range at a time (spreads the NVLink traffic over the peers).
+__device__ __forceinline__ int64_t spread_index(int64_t i, int64_t n) {
+  const int64_t p = (n % 7919) ? 7919 : ((n % 104729) ? 104729 : 1);
+  return (i * p) % n;
+}
+
 // one token's dispatch (warp): expert-major positions of its picks, then the
 // row to every place it goes (direct expert-major rows for picks on this GPU
 // in modes 0/2/3, one row per hit remote GPU in mode 3, one row per hit
@@ -890,9 +899,13 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
     }
     return;
   }
-  for (int64_t t = warp; t < T; t += nw)
-    pack_token<SH>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs, eoff,
-                   nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
+  // across GPUs, tokens are walked in a spread order (like the reducers) so the
+  // concurrent warps' NVLink stores land all over the peers' receive buffers
+  const bool spread = mode == 3 && w.P > 1;
+  for (int64_t i = warp; i < T; i += nw)
+    pack_token<SH>(w, spread ? spread_index(i, T) : i, lane, x, ids, wts, chunk_off, rank_d,
+                   rank_e, hitmask, offs, eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g,
+                   status);
 }
 
 // expand (dedup, destination side): warp per received row -> its local
@@ -1076,14 +1089,6 @@ __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, con
     weighted_row_sum_any<T, CG>(srcs, ws, n, nvec, lane, dst);
 }
 
-// Bijective spread of [0, n) (multiplication by a prime coprime with n): the
-// destination-side reducers walk their received rows in this order so that
-// at any moment the warps push to every source GPU instead of one source's
-// contiguous range at a time (spreads the NVLink traffic over the peers).
-__device__ __forceinline__ int64_t spread_index(int64_t i, int64_t n) {
-  const int64_t p = (n % 7919) ? 7919 : ((n % 104729) ? 104729 : 1);
-  return (i * p) % n;
-}
 
 // expert-side source rows of a received row: lane k resolves meta k
 __device__ __forceinline__ int meta_sources_warp(const RowMeta* meta, int K, const uint8_t* ybase,
