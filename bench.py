@@ -223,16 +223,17 @@ def dsv3_layer_forward(G, E, K, M, inter, T_r, world, rank, x, flush, tokens_tot
     if world > 1:
         dist.barrier()
     acc = np.zeros(2)
-    for _ in range(n_l):
-        flush.zero_()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record()
-        layer(x, out=lout)
-        ev[1].record()
-        layer.backward(gout)
-        ev[2].record()
-        ev[2].synchronize()
-        acc += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])]
+    with ClockSampler(torch.cuda.current_device()) as lclk:
+        for _ in range(n_l):
+            flush.zero_()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+            layer(x, out=lout)
+            ev[1].record()
+            layer.backward(gout)
+            ev[2].record()
+            ev[2].synchronize()
+            acc += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])]
     t = torch.tensor(acc / n_l, dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -247,6 +248,7 @@ def dsv3_layer_forward(G, E, K, M, inter, T_r, world, rank, x, flush, tokens_tot
            "ffn_flops_per_gpu_incl_shared": int(fl),
            "fwd_tflops": fl / (fwd_ms * 1e-3) / 1e12,
            "fwd_bwd_tflops": 3 * fl / ((fwd_ms + bwd_ms) * 1e-3) / 1e12,
+           "clocks": lclk.summary(),
            "note": "router logits GEMM and gate bwd in torch (cuBLAS TF32)"}
     layer.close()
     return out
@@ -631,23 +633,24 @@ def main():
             dist.barrier()
         n_l = max(5, args.steps // 10)
         acc = np.zeros(4)
-        for _ in range(n_l):
-            flush.zero_()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-            ev[0].record()
-            slot_l, w_l, ex_l = layer.route(x)
-            layer._saved = (x, slot_l, w_l, ex_l)
-            layer.world.dispatch(x, slot_l, w_l, dedup=layer.dedup)
-            ev[1].record()
-            layer.experts_forward()
-            ev[2].record()
-            layer.world.combine(slot_l, w_l, dedup=layer.dedup, out=lout)
-            ev[3].record()
-            layer.backward(gout)
-            ev[4].record()
-            ev[4].synchronize()
-            acc += [ev[0].elapsed_time(ev[3]), ev[1].elapsed_time(ev[2]),
-                    ev[3].elapsed_time(ev[4]), ev[0].elapsed_time(ev[4])]
+        with ClockSampler(local) as lclk:
+            for _ in range(n_l):
+                flush.zero_()
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                ev[0].record()
+                slot_l, w_l, ex_l = layer.route(x)
+                layer._saved = (x, slot_l, w_l, ex_l)
+                layer.world.dispatch(x, slot_l, w_l, dedup=layer.dedup)
+                ev[1].record()
+                layer.experts_forward()
+                ev[2].record()
+                layer.world.combine(slot_l, w_l, dedup=layer.dedup, out=lout)
+                ev[3].record()
+                layer.backward(gout)
+                ev[4].record()
+                ev[4].synchronize()
+                acc += [ev[0].elapsed_time(ev[3]), ev[1].elapsed_time(ev[2]),
+                        ev[3].elapsed_time(ev[4]), ev[0].elapsed_time(ev[4])]
         t = torch.tensor(acc / n_l, dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -665,7 +668,7 @@ def main():
                      "ffn_roofline": {"bound": "tensor", "achieved": ffn_tflops, "peak": peak_tf,
                                       "unit": "TFLOP/s", "frac": ffn_tflops / peak_tf,
                                       "kernel": "k_grouped_gemm (tcgen05, 2 GEMMs, fwd)"},
-                     "inter": inter, "transport": layer.dedup,
+                     "inter": inter, "transport": layer.dedup, "clocks": lclk.summary(),
                      "note": "router logits GEMM and top-K softmax bwd in torch (cuBLAS); "
                              "dispatch/combine/experts fwd+bwd are our kernels"}
         layer.close()
