@@ -43,8 +43,11 @@ CONFIGS = {
              "DeepSeek-V3-shaped MoE layer: 256 routed experts, top-8, hidden 7168, bf16, EP=8"),
     "configA": (8, 16, 2, 256, 512,
                 "reference CPU config: 16 experts, top-2, hidden 256, 4096 tokens, 8-rank EP world"),
+    # one EP rank per GPU on a 4-GPU box: exercises the N = 8 layout (L = 1)
+    "qwen3_ep4": (4, 128, 8, 2048, 4096,
+                  "Qwen3-shaped MoE layer with EP=4 (one rank per GPU at N=4; the N=8 layout)"),
 }
-INTER = {"qwen3": 768, "dsv3": 2048, "configA": 512}
+INTER = {"qwen3": 768, "dsv3": 2048, "configA": 512, "qwen3_ep4": 768}
 NVLINK_GBS = 770.0   # B200_PROFILING.md: measured peer copy, per direction per GPU
 SEGMENTS = ["plan", "notify", "pack", "barrier1", "expand", "reduce", "barrier2", "gather"]
 
