@@ -114,6 +114,7 @@ class HierMoELayer:
             gb = torch.Generator(device="cuda").manual_seed(seed + 17)
             self.score_bias = torch.randn(experts, device="cuda", generator=gb) * 0.01
         self.shared_inter = shared_inter
+        self.shared_overlap = True    # shared expert on a side stream beside the exchange
         if shared_inter:
             gsh = torch.Generator(device="cuda").manual_seed(seed * 7919 + 1)
             w1 = torch.randn(1, shared_inter, hidden, device="cuda", generator=gsh) * hidden ** -0.5
@@ -237,10 +238,11 @@ class HierMoELayer:
         shared = None
         cur = torch.cuda.current_stream()
         if self.shared_inter:   # tensor-bound shared expert beside the link-bound dispatch
-            self._side.wait_stream(cur)
-            with torch.cuda.stream(self._side):
+            side = self._side if self.shared_overlap else cur
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
                 shared = self.shared_forward(x)
-                self._shared_done.record(self._side)
+                self._shared_done.record(side)
         if out is None:
             out = torch.empty_like(x)
         # micro-batch m on stream m, pipelined: dispatch m follows dispatch m-1

@@ -26,7 +26,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--gemm-ctas", type=int, nargs="+", default=[0])
     ap.add_argument("--exch-blocks", type=int, nargs="+", default=[0])
-    ap.add_argument("--gemm-pair", type=int, nargs="+", default=[0])
+    ap.add_argument("--gemm-pair", type=int, nargs="+", default=[1])
+    ap.add_argument("--shared-overlap", type=int, nargs="+", default=[1])
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -45,14 +46,16 @@ def main():
     x = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
     g = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
     from paper_2508_09591_b200.ffn import set_gemm_ctas, set_gemm_pair
-    for mb, ctas, xb, gp in [(m, c, b, p) for m in args.mbs for c in args.gemm_ctas
-                             for b in args.exch_blocks for p in args.gemm_pair]:
+    for mb, ctas, xb, gp, so in [(m, c, b, p, o) for m in args.mbs for c in args.gemm_ctas
+                                 for b in args.exch_blocks for p in args.gemm_pair
+                                 for o in args.shared_overlap]:
         set_gemm_ctas(ctas)
         set_gemm_pair(bool(gp))
         layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, grad=True,
                              n_cap_rows=2 * T_r * K, micro_batches=mb, **kw)
         for wd in layer.worlds:
             wd.set_max_blocks(xb)
+        layer.shared_overlap = bool(so)
         for _ in range(3):
             layer(x)
             layer.backward(g)
@@ -87,6 +90,7 @@ def main():
         if rank == 0:
             print(json.dumps({"config": args.config, "n_gpus": world, "micro_batches": mb,
                               "gemm_ctas": ctas, "exch_blocks": xb, "gemm_pair": gp,
+                              "shared_overlap": so,
                               "fwd_ms": round(t[0].item(), 4), "bwd_ms": round(t[1].item(), 4),
                               "fwd_bwd_ms": round(t[0].item() + t[1].item(), 4)}), flush=True)
         layer.close()
