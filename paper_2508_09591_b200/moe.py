@@ -13,7 +13,6 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import _lib
 from .ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs,
                   expert_ffn_save_ptrs, pack_w13)
 from .layer import EPWorld, route_group_limited, route_topk

@@ -12,7 +12,6 @@ tensors for every level, cost, argmin -- and transfers the result once.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -22,7 +21,7 @@ from . import _lib
 from ._lib import ptr, stream_ptr
 from .routing import DeviceMask, MaskLike, Placement, device_mask, propagate_device
 from .topology import LevelParams, Topology
-from .traffic import _device_counts, _Model, model_cuts
+from .traffic import _device_counts, _Model
 
 
 def smooth_max(x, gamma: float) -> float:
