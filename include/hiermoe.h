@@ -238,7 +238,8 @@ int hm_expert_ffn_backward_saved_acc(const void* x, int64_t a_rows, const int32_
  * 1 = transposed copies + K-major GEMMs (kept as the comparison path);
  * 1 = cap on the persistent GEMM grid in CTAs (0 = one per SM);
  * 2 = 1: CTA-pair (tcgen05 cta_group::2, 256 x 256 tile) kernels for the
- *     forward and data-gradient GEMMs (default), 0: single-CTA 128 x 256. */
+ *     forward and data-gradient GEMMs (default), 0: single-CTA 128 x 256;
+ * 3 = 1: the weight-gradient (MN-major) GEMMs on CTA pairs too. */
 int hm_ffn_set_option(int32_t option, int32_t value);
 
 /* ---------------- expert migration (K11) ------------------------------------

@@ -44,6 +44,7 @@ int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid 
 // default on: 8-17 % faster per GEMM in ncu, layer fwd 3.19 -> 3.07 ms (Qwen3)
 // and 25.2 -> 23.5 ms (DSv3) at N = 1
 int g_gemm_pair = 1;
+int g_wgrad_pair = 0;  // hm_ffn_set_option(3, 1): weight-gradient GEMMs on CTA pairs
 
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
@@ -694,6 +695,179 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// Weight-gradient GEMM (mode 3: out_g = A_g^T B_g over group g's token rows,
+// MN-major operands) on CTA pairs: 256 x 256 output tiles, each CTA stages
+// 128 features of A and 128 of B per 64-token k-block (4 boxes, 32 KB, 6
+// stages).  Each CTA's TMA completes on its own barrier; its MMA warp zeroes
+// the tail block's lines past the group in its own boxes, then arrives on
+// the leader's `ready` barrier (2 arrivals per stage), after which the
+// leader's MMA thread issues the pair MMA over both CTAs' shared memory.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_wgrad_pair(const __grid_constant__ CUtensorMap map_a,
+                 const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages2 * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
+  uint64_t* ready = full + kStages2;
+  uint64_t* empty = ready + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ TileMap tm;
+  constexpr uint32_t kIdescPairMN = kIdesc2 | (1u << 15) | (1u << 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    int acc = 0, row = 0;
+    tm.ntile_n = args.N / BN;
+    for (int g = 0; g < args.groups; ++g) {
+      const int n = args.n_rows[g];
+      tm.start[g] = acc;
+      tm.row0[g] = row;
+      tm.rows[g] = n;
+      acc += args.m_out / BM2 * tm.ntile_n;
+      row += n;
+    }
+    tm.start[args.groups] = acc;
+    tm.total = acc;
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(ready + s, 2);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < tm.total; t += ncl) {
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        const int a0 = mt * BM2 + (int)rank * 128, b0 = nt * BN + (int)rank * 128;
+        const int kblocks = (tm.rows[g] + BK - 1) / BK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_expect_tx(full + stage, kStageBytes2);
+          const int k0 = tm.row0[g] + kb * BK;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            tma_load_2d(sa + stage * kHalfBytes + j * 8192, &map_a, full + stage, a0 + 64 * j, k0);
+            tma_load_2d(sb + stage * kHalfBytes + j * 8192, &map_b, full + stage, b0 + 64 * j, k0);
+          }
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = cid; t < tm.total; t += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      if (leader && lane == 0) {
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+      }
+      const uint32_t d = tmem_base + acc * BN;
+      const int kblocks = (tm.rows[g] + BK - 1) / BK;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full + stage, phase);
+        const int valid = tm.rows[g] - kb * BK;
+        const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
+        const int zend = ksteps * UK;
+        if (valid < zend) {   // this CTA's 4 boxes: lines [valid, zend)
+          const int nlines = zend - valid;
+          for (int i = lane; i < 4 * nlines * 8; i += 32) {
+            const int box = i / (nlines * 8), rem = i % (nlines * 8);
+            const int line = valid + rem / 8, chunk = rem % 8;
+            uint8_t* base = box < 2 ? sa + stage * kHalfBytes + box * 8192
+                                    : sb + stage * kHalfBytes + (box - 2) * 8192;
+            *reinterpret_cast<int4*>(base + line * 128 + chunk * 16) = make_int4(0, 0, 0, 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(ready + stage, 0);
+        if (leader && lane == 0) {
+          mbar_wait(ready + stage, phase);
+          tc_fence_after();
+          const uint32_t sa0 = smem_u32(sa + stage * kHalfBytes);
+          const uint32_t sb0 = smem_u32(sb + stage * kHalfBytes);
+          for (int k = 0; k < ksteps; ++k) {
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                "l"(smem_desc_mn(sa0 + k * UK * 128)), "l"(smem_desc_mn(sb0 + k * UK * 128)),
+                "r"(kIdescPairMN), "r"((kb | k) ? 1u : 0u));
+          }
+          umma_commit_pair(empty + stage);
+        }
+        __syncwarp();
+        if (++stage == kStages2) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (leader && lane == 0) umma_commit_pair(tfull + acc);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    int it = 0;
+    for (int t = cid; t < tm.total; t += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int r_in = mt * BM2 + (int)rank * 128 + q * 32 + lane;
+      store_tile<3>(args, tm, g, nt, r_in, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // expert FFN backward helpers
 // group layout for the weight-gradient GEMMs: token rows of group g are
@@ -900,6 +1074,14 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
+  if (g_wgrad_pair && m_out % BM2 == 0) {
+    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
+    HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem2));
+    k_wgrad_pair<<<sms & ~1, kThreads, smem2, s>>>(ma, mb, args);
+    HM_LAUNCHED();
+    return 0;
+  }
   HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   k_grouped_gemm<3><<<sms, kThreads, smem, s>>>(ma, mb, args);
@@ -981,10 +1163,11 @@ int g_wgrad_transposed = 0;   // hm_ffn_set_option(0, 1): transposes + K-major w
 // concurrent exchange kernels keep SMs of their own; 2 = CTA-pair
 // (cta_group::2, 256 x 256 tiles) kernels for the forward / data-gradient GEMMs
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option >= 0 && option <= 2, "hm_ffn_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 3, "hm_ffn_set_option: unknown option %d", option);
   if (option == 0) g_wgrad_transposed = value != 0;
   if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
   if (option == 2) g_gemm_pair = value != 0;
+  if (option == 3) g_wgrad_pair = value != 0;
   return 0;
 }
 

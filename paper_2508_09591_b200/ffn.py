@@ -72,6 +72,11 @@ def set_gemm_pair(enabled: bool) -> None:
     _lib.call("hm_ffn_set_option", 2, int(bool(enabled)))
 
 
+def set_wgrad_pair(enabled: bool) -> None:
+    """Weight-gradient GEMMs on CTA pairs (256 x 256 output tiles)."""
+    _lib.call("hm_ffn_set_option", 3, int(bool(enabled)))
+
+
 def set_gemm_ctas(n: int) -> None:
     """Cap the persistent grouped-GEMM grid at n CTAs (0: one per SM)."""
     _lib.call("hm_ffn_set_option", 1, int(n))

@@ -65,3 +65,47 @@ def test_pair_swiglu_ffn_equals_single(hm, pair):
         res.append((h[:rows].clone(), y[:rows].clone(), g13[:rows].clone()))
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("shape", [(4, 2048, 768, [1000, 63, 0, 2049]), (3, 512, 256, [130, 0, 301])])
+def test_wgrad_pair_equals_single(hm, shape):
+    """Weight gradients from the CTA-pair MN-major GEMM equal the single-CTA
+    ones bit for bit (rows past the last group hold NaN: the tail zeroing
+    must keep them out)."""
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
+                                           expert_ffn_save_ptrs, set_wgrad_pair)
+    G, M, I, n_rows = shape
+    torch.manual_seed(7)
+    rows = sum(n_rows)
+    cap = rows + 100
+    x = torch.full((cap, M), float("nan"), device="cuda", dtype=torch.bfloat16)
+    x[:rows] = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    gy = torch.full((cap, M), float("nan"), device="cuda", dtype=torch.bfloat16)
+    gy[:rows] = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    w13t, w2t = w13.transpose(1, 2).contiguous(), w2.transpose(1, 2).contiguous()
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
+    g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
+    expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y.data_ptr(),
+                         g13.data_ptr())
+    res = []
+    try:
+        for on in (False, True):
+            set_wgrad_pair(on)
+            sc = FFNBackwardScratch(cap, G, M, I)
+            gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+            dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
+            dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
+            expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t,
+                                     gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2,
+                                     g13.data_ptr())
+            torch.cuda.synchronize()
+            res.append((dw13.clone(), dw2.clone()))
+    finally:
+        set_wgrad_pair(False)
+    assert not torch.isnan(res[1][0]).any() and not torch.isnan(res[1][1]).any()
+    assert torch.equal(res[0][0], res[1][0])
+    assert torch.equal(res[0][1], res[1][1])
