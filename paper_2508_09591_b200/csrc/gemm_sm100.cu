@@ -44,7 +44,10 @@ int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid 
 // default on: 8-17 % faster per GEMM in ncu, layer fwd 3.19 -> 3.07 ms (Qwen3)
 // and 25.2 -> 23.5 ms (DSv3) at N = 1
 int g_gemm_pair = 1;
-int g_wgrad_pair = 0;  // hm_ffn_set_option(3, 1): weight-gradient GEMMs on CTA pairs
+// hm_ffn_set_option(3, 1): weight-gradient GEMMs on CTA pairs -- bit-identical
+// but measured 2x slower (DSv3 dW13 4.22 vs 2.32 ms in ncu: the per-stage
+// ready hand-off between the two CTAs serialises the pipeline), so off
+int g_wgrad_pair = 0;
 
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
