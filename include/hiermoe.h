@@ -145,7 +145,9 @@ int hm_world_barrier(hm_world* w, void* stream);
  *      2 = default caching (measured 0.219 / 0.219 / 0.234 ms, Qwen3 N = 1)
  *   7: 1 = per-GPU dedup pack at N > 1 with separate warps for the NVLink
  *      pushes and the local expert-major copies, 0 = one warp per token does
- *      both (default; the split measured neutral) */
+ *      both (default; the split measured neutral)
+ *   8: 1 = lean one-GPU pack kernel (lane-held destinations, row load issued
+ *      before the position bookkeeping; default), 0 = the general pack */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);
 /* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
  * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */

@@ -748,6 +748,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
   const int s_loc = (int)(t / w.T_r);
   const int64_t t_in = t - (int64_t)s_loc * w.T_r;
   const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
+  const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
   // expert-major positions of my picks (lane k < K computes pick k)
   int my_e = -1, my_ep = -1;
   float my_w = 0.f;
@@ -763,7 +764,6 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
     }
     if (PART != 2) epos_out[t * w.K + lane] = my_ep;
   }
-  const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
   unsigned long long hit = hitmask[t];
   // destinations (dedup) or picks (raw) this row goes to
   int ndst = 0;
@@ -906,6 +906,58 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
     pack_token<SH>(w, spread ? spread_index(i, T) : i, lane, x, ids, wts, chunk_off, rank_d,
                    rank_e, hitmask, offs, eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g,
                    status);
+}
+
+// One-GPU pack (every destination local: modes 0, 2, 3 at P = 1): warp per
+// token, the row's first 4 KB loaded before the position bookkeeping, lane k
+// holds pick k's destination pointer (no per-token destination arrays), the
+// stores broadcast the pointers by shuffle.  Lean registers -> more resident
+// warps than the general pack_token.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_pack_local(const WorldDev* __restrict__ wp,
+                                                    const uint8_t* __restrict__ x,
+                                                    const int32_t* __restrict__ ids,
+                                                    const int32_t* __restrict__ chunk_off,
+                                                    const int32_t* __restrict__ rank_e,
+                                                    const int32_t* __restrict__ eoff, int nchunks,
+                                                    int32_t* __restrict__ epos_out,
+                                                    int* __restrict__ status) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int C = w.G + w.E + w.P;
+  const int64_t T = (int64_t)w.L * w.T_r;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = warp; t < T; t += nw) {
+    const int4* src = reinterpret_cast<const int4*>(x + t * w.row_bytes);
+    int4 buf[VPL];
+#pragma unroll
+    for (int u = 0; u < VPL; ++u) buf[u] = ld_nc_v4(src + u * 32 + lane);
+    const int s_loc = (int)(t / w.T_r);
+    const int64_t t_in = t - (int64_t)s_loc * w.T_r;
+    uint8_t* dst = nullptr;
+    if (lane < w.K) {
+      const int e = ids[t * w.K + lane];
+      int ep = -1;
+      if (e >= 0) {
+        const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
+        ep = eoff[s_loc * w.E + e] + coff[w.G + e] + rank_e[t * w.K + lane];
+        if (ep >= w.N_cap) {
+          atomicExch(status, 2);
+          ep = -1;
+        }
+      }
+      epos_out[t * w.K + lane] = ep;
+      if (ep >= 0) dst = w.xmaj[e / w.E_loc] + (int64_t)ep * w.row_bytes;
+    }
+    for (int k = 0; k < w.K; ++k) {
+      int4* d = reinterpret_cast<int4*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), k));
+      if (!d) continue;
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) st_na_v4(d + u * 32 + lane, buf[u]);
+    }
+  }
 }
 
 // expand (dedup, destination side): warp per received row -> its local
@@ -2089,6 +2141,7 @@ struct hm_world {
   // hm_world_set_option(w, 7, 1): separate warps for NVLink pushes and local
   // copies in the N > 1 pack (measured neutral: 150 vs 152 us at N = 4)
   bool split_pack = false;
+  bool lean_pack = true;       // hm_world_set_option(w, 8, 0): general pack on one GPU too
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -2439,7 +2492,24 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
   const size_t bulk_smem = (size_t)kBulkWarps * 2 * h.row_bytes;
-  if (w->bulk_pack && h.P == 1 && mode != 1 && !h.U1 && h.row_bytes % 16 == 0 &&
+  const int64_t nv = h.row_bytes / 16;
+  const bool local_only = h.P == 1 && mode != 1 && !h.U1;
+  if (local_only && w->lean_pack && !w->bulk_pack &&
+      (nv == 32 || nv == 64 || nv == 128 || nv == 256)) {
+    SegScope sc(w, kSegPack, s);
+#define HM_PL(V)                                                                             \
+  k_pack_local<V><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, w->chunk_cnt, w->rank_e, \
+                                         w->eoff, w->nchunks, w->epos, w->status)
+    if (nv == 32)
+      HM_PL(1);
+    else if (nv == 64)
+      HM_PL(2);
+    else if (nv == 128)
+      HM_PL(4);
+    else
+      HM_PL(8);
+#undef HM_PL
+  } else if (w->bulk_pack && h.P == 1 && mode != 1 && !h.U1 && h.row_bytes % 16 == 0 &&
       bulk_smem <= 200 * 1024) {
     HM_CUDA(cudaFuncSetAttribute(k_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bulk_smem));
@@ -2789,7 +2859,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 7, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 8, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -2804,5 +2874,6 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   if (option == 5) w->bulk_pack = value != 0;
   if (option == 6) w->pack_store = value >= 0 && value <= 2 ? value : 0;
   if (option == 7) w->split_pack = value != 0;
+  if (option == 8) w->lean_pack = value != 0;
   return 0;
 }

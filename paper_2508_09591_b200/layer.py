@@ -270,6 +270,10 @@ class EPWorld:
         local copies, or one warp per token for both (default)."""
         _lib.call("hm_world_set_option", self._h, 7, int(bool(enabled)))
 
+    def set_lean_pack(self, enabled: bool) -> None:
+        """One-GPU pack: the lean kernel (default) or the general pack."""
+        _lib.call("hm_world_set_option", self._h, 8, int(bool(enabled)))
+
     def set_max_blocks(self, n: int) -> None:
         """Cap the exchange kernels' grid at n CTAs (0: 8 per SM)."""
         _lib.call("hm_world_set_option", self._h, 4, int(n))

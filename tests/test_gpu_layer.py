@@ -116,14 +116,17 @@ def test_dispatch_combine_parity(hm, name, dedup):
             rx = world.read("recv_x", d, dtype, r * M).view(r, M).cpu()
             assert torch.equal(rx.view(xb.dtype), xb[plan.recv_rows(d)])
     # the bulk-copy pack (one GPU, direct modes) writes the same expert-major rows
-    if dedup != "all":
+    if dedup != "all":   # bulk-copy and general pack kernels agree with the lean one
         before = [world.read("xmaj", d, dtype, int(rn[d, 1]) * M).clone() for d in range(G)]
-        world.set_bulk_pack(True)
-        world.dispatch(xd, slot, w, dedup=dedup)
+        for bulk, lean in ((True, True), (False, False)):
+            world.set_bulk_pack(bulk)
+            world.set_lean_pack(lean)
+            world.dispatch(xd, slot, w, dedup=dedup)
+            torch.cuda.synchronize()
+            for d in range(G):
+                assert torch.equal(world.read("xmaj", d, dtype, int(rn[d, 1]) * M), before[d])
         world.set_bulk_pack(False)
-        torch.cuda.synchronize()
-        for d in range(G):
-            assert torch.equal(world.read("xmaj", d, dtype, int(rn[d, 1]) * M), before[d])
+        world.set_lean_pack(True)
     # combine with a stand-in expert y = x * scale[slot]; both gather variants
     _apply_experts(world, plan, E, dtype)
     world.set_tma_gather(False)
