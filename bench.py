@@ -478,7 +478,8 @@ def main():
     if (roof["bound"] == "hbm" and world == 1 and args.config == "qwen3" and args.tokens is None
             and tr_path.exists()):
         tr = json.loads(tr_path.read_text())["dram_bytes_per_launch"]
-        roof["traffic"] = tr.get("k_" + dom)
+        names = {"pack": ("k_pack_local", "k_pack")}.get(dom, ("k_" + dom,))
+        roof["traffic"] = next((tr[n] for n in names if n in tr), None)
         roof["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full, dram read+write)"
     per_kernel = {k: {"ms": round(seg_ms[k], 4), "bytes": alg[k],
                       "GBps": round(alg[k] / max(seg_ms[k], 1e-9) / 1e6, 1)} for k in alg}
