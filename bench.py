@@ -415,6 +415,9 @@ def main():
     ep.set_lean_pack(False)
     seg_general = seg_times(ep, MODE)
     ep.set_lean_pack(True)
+    _lib.call("hm_world_set_option", ep._h, 9, 1)
+    seg_su8 = seg_times(ep, MODE)
+    _lib.call("hm_world_set_option", ep._h, 9, 0)
     seg = seg_times(ep, MODE)
     seg_raw = seg_times(raw_ep, "none")
     seg_all = seg_times(all_ep, "all")
@@ -712,6 +715,7 @@ def main():
             "pack_bulk_variant_ms": round(float(seg_bulkpack[SEGMENTS.index("pack")]), 4),
             "pack_split_variant_ms": round(float(seg_split[SEGMENTS.index("pack")]), 4),
             "pack_general_variant_ms": round(float(seg_general[SEGMENTS.index("pack")]), 4),
+            "gather_su8_variant_ms": round(float(seg_su8[SEGMENTS.index("gather")]), 4),
             "transport": MODE,
             "nodedup": {"ms_per_step": ms_raw, "value": tokens_total / (ms_raw * 1e-3),
                         "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_raw.tolist())},

@@ -1053,7 +1053,7 @@ constexpr int kU = 4;
 constexpr int kCh = 2, kSu = 4;
 
 // compile-time row width: VPL 16-B vectors per lane (row = 32 * VPL vectors)
-template <typename T, int VPL, bool CG = false>
+template <typename T, int VPL, bool CG = false, int SU = kSu>
 __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* srcs, const float* ws,
                                                        int n, int lane, int4* dst) {
   constexpr int CH = VPL < kCh ? VPL : kCh;
@@ -1067,10 +1067,10 @@ __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* src
       for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
     const int off = c * 32 + lane;
 #pragma unroll 1
-    for (int j0 = 0; j0 < n; j0 += kSu) {
-      int4 buf[kSu][CH];
+    for (int j0 = 0; j0 < n; j0 += SU) {
+      int4 buf[SU][CH];
 #pragma unroll
-      for (int s = 0; s < kSu; ++s) {
+      for (int s = 0; s < SU; ++s) {
         if (j0 + s < n) {
           const int4* src = reinterpret_cast<const int4*>(srcs[j0 + s]) + off;
 #pragma unroll
@@ -1078,7 +1078,7 @@ __device__ __forceinline__ void weighted_row_sum_fixed(const uint8_t* const* src
         }
       }
 #pragma unroll
-      for (int s = 0; s < kSu; ++s) {
+      for (int s = 0; s < SU; ++s) {
         if (j0 + s < n) {
           const float wj = ws[j0 + s];
 #pragma unroll
@@ -1132,11 +1132,11 @@ __device__ __forceinline__ void weighted_row_sum_any(const uint8_t* const* srcs,
   }
 }
 
-template <typename T, int VPL, bool CG = false>
+template <typename T, int VPL, bool CG = false, int SU = kSu>
 __device__ __forceinline__ void weighted_row_sum(const uint8_t* const* srcs, const float* ws,
                                                  int n, int64_t nvec, int lane, int4* dst) {
   if constexpr (VPL > 0)
-    weighted_row_sum_fixed<T, VPL, CG>(srcs, ws, n, lane, dst);
+    weighted_row_sum_fixed<T, VPL, CG, SU>(srcs, ws, n, lane, dst);
   else
     weighted_row_sum_any<T, CG>(srcs, ws, n, nvec, lane, dst);
 }
@@ -1358,8 +1358,8 @@ __device__ __forceinline__ int gather_sources_warp(const WorldDev& w, int64_t t,
 
 constexpr int kMaxSrc = kMaxRanks > kMaxK ? kMaxRanks : kMaxK;
 
-template <typename T, int VPL>
-__global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ wp,
+template <typename T, int VPL, int SU = kSu>
+__global__ void __launch_bounds__(256, (SU > 4 ? 2 : 3)) k_gather(const WorldDev* __restrict__ wp,
                                                 const int32_t* __restrict__ ids,
                                                 const float* __restrict__ wts,
                                                 const unsigned long long* __restrict__ hitmask,
@@ -1390,7 +1390,8 @@ __global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ 
       ++n;
     }
     __syncwarp();
-    weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out + t * w.row_bytes));
+    weighted_row_sum<T, VPL, false, SU>(srcs, ws, n, nvec, lane,
+                                        reinterpret_cast<int4*>(out + t * w.row_bytes));
   }
 }
 
@@ -2142,6 +2143,7 @@ struct hm_world {
   // copies in the N > 1 pack (measured neutral: 150 vs 152 us at N = 4)
   bool split_pack = false;
   bool lean_pack = true;       // hm_world_set_option(w, 8, 0): general pack on one GPU too
+  bool gather_su8 = false;     // hm_world_set_option(w, 9, 1): 8-source load batches in the gather
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long epoch = 0;
@@ -2665,9 +2667,14 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
     return 0;
   }
   with_row_type(h, [&](auto t, auto v) {
-    k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
-        w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
-        (uint8_t*)out, addend);
+    if (w->gather_su8)   // 8 sources' loads in flight per lane (2 CTAs / SM)
+      k_gather<typename decltype(t)::type, decltype(v)::value, 8><<<blocks, 256, 0, s>>>(
+          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
+          (uint8_t*)out, addend);
+    else
+      k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
+          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
+          (uint8_t*)out, addend);
   });
   HM_LAUNCHED();
   return 0;
@@ -2859,7 +2866,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 8, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 9, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -2875,5 +2882,6 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   if (option == 6) w->pack_store = value >= 0 && value <= 2 ? value : 0;
   if (option == 7) w->split_pack = value != 0;
   if (option == 8) w->lean_pack = value != 0;
+  if (option == 9) w->gather_su8 = value != 0;
   return 0;
 }
