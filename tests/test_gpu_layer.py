@@ -159,3 +159,47 @@ def test_dedup_moves_fewer_rows(hm):
     ratio = rows[:, 1].sum() / rows[:, 0].sum()
     assert 1.3 < ratio < 1.7        # uniform E=128, K=8, G=8: 8 / 5.34 = 1.498
     world.close()
+
+
+@pytest.mark.parametrize("dedup", ["gpu", "remote", "all", "none"])
+def test_ragged_picks_padding(hm, dedup):
+    """Tokens with dropped picks (slot id -1, e.g. capacity-dropped) and one
+    token with no picks at all: the padding moves no rows and contributes
+    nothing to the combine."""
+    from paper_2508_09591_b200.layer import route_topk
+    G, E, K, M, T_r, dtype = 8, 64, 4, 512, 96, torch.bfloat16
+    logits, x = _inputs(G, E, K, M, T_r, dtype, seed=31)
+    slot, w, _ = route_topk(logits.cuda(), K)
+    g = torch.Generator().manual_seed(5)
+    drop = torch.rand(G * T_r, K, generator=g) < 0.25
+    drop[17] = True                                  # a token with no picks left
+    slot = slot.clone()
+    slot[drop.cuda()] = -1
+    world = _world(hm, G, E, K, M, T_r, dtype)
+    world.dispatch(x.cuda(), slot, w, dedup=dedup)
+    torch.cuda.synchronize()
+    world.check_status()
+    ids = slot.cpu().numpy()
+    valid = ids >= 0
+    e_loc = E // G
+    rn = world.rows_received()
+    sc = _scale(E)
+    for d in range(G):
+        n_want = int(((ids // e_loc == d) & valid).sum())
+        assert int(rn[d, 1]) == n_want
+        xm = world.read("xmaj", d, dtype, n_want * M).view(n_want, M)
+        # stand-in expert on the rows actually received: y = x * scale[slot]
+        tt, kk = np.nonzero((ids // e_loc == d) & valid)
+        epos = world.read("epos", 0, torch.int32).cpu().numpy().reshape(-1, K)
+        row_slot = np.zeros(n_want, dtype=np.int64)
+        row_slot[epos[tt, kk]] = ids[tt, kk]
+        world.set_expert_outputs(d, (xm.float() * sc[row_slot].float().cuda()[:, None]).to(dtype))
+    out = world.combine(slot, w, dedup=dedup)
+    torch.cuda.synchronize()
+    world.check_status()
+    wts = w.cpu().numpy().astype(np.float64) * valid
+    ref = (wts * sc.numpy()[np.where(valid, ids, 0)]).sum(axis=1)[:, None] * x.double().numpy()
+    np.testing.assert_allclose(out.double().cpu().numpy(), ref, rtol=2e-2,
+                               atol=2e-2 * np.abs(ref).max())
+    assert torch.count_nonzero(out[17]) == 0
+    world.close()
