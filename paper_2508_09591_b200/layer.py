@@ -188,8 +188,10 @@ class EPWorld:
     def dispatch(self, x: torch.Tensor, slot_ids: torch.Tensor, weights: torch.Tensor | None,
                  dedup=True) -> None:
         """Plan + exchange; afterwards each local rank's expert-major rows
-        (``xmaj``) hold its experts' inputs.  ``dedup``: True (= "remote"),
-        "all", or False (= "none"), see MODES."""
+        (``xmaj``) hold its experts' inputs.  ``dedup``: True (= "gpu": one
+        row per (token, other GPU hit), re-expanded at the destination),
+        "remote" (per remote rank), "all" (per rank, incl. this GPU's), or
+        False (= "none"), see MODES."""
         self._check_rows(x, slot_ids)
         mode = transport_mode(dedup)
         s = stream_ptr()
