@@ -74,10 +74,15 @@ def main():
                             dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(rows, op=dist.ReduceOp.MAX)
+        p0, p1, p2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        p0.record()
         plan = hm.select_swap(hm.mask_from_ids(slot, E), topo, params, 10.0, None, group=grp)
+        p1.record()
         layer.apply_swap(plan.pair)
+        p2.record()
+        p2.synchronize()
         log.append((step, rows[0].item(), rows[1].item(), plan.pair is not None,
-                    plan.predicted_saving))
+                    plan.predicted_saving, p0.elapsed_time(p1), p1.elapsed_time(p2)))
     layer.world.check_status()
     layer.store.check_status()
     if rank == 0:
@@ -89,6 +94,9 @@ def main():
             "gpu_dedup_rows_last10": float(np.mean([r[1] for r in last])),
             "step_ms_first10": float(np.mean([r[2] for r in first])),
             "step_ms_last10": float(np.mean([r[2] for r in last])),
+            "planner_ms_median": float(np.median([r[5] for r in log[5:]])),
+            "migration_ms_median_when_swapped": float(np.median([r[6] for r in log[5:] if r[3]]))
+            if any(r[3] for r in log[5:]) else None,
             "trace": [[r[0], r[1], round(r[2], 4), r[3]] for r in log[::10]]}))
     layer.close()
     if world > 1:
