@@ -55,7 +55,7 @@ class _Partials:
     """Device swap statistics of one group cut (``reduce`` sums them over a
     token-sharded mask before the tensor is built)."""
 
-    def __init__(self, dev: DeviceMask, groups: int, reduce=None):
+    def __init__(self, dev: DeviceMask, groups: int, reduce=None, defer: bool = False):
         e = dev.experts
         if groups < 1 or e % groups:
             raise ValueError(f"group count {groups} does not divide {e} experts")
@@ -73,10 +73,20 @@ class _Partials:
         if reduce is not None:
             for t in (self.base, self.sel, self.hitsel, self.lone, self.lonesel):
                 reduce(t)
-        self.z = torch.empty((e, e, groups), **kw)
+        self.experts = e
+        if not defer:
+            self.finish()
+
+    def stats(self):
+        """The additive statistics (all-reduced over a token-sharded mask)."""
+        return (self.base, self.sel, self.hitsel, self.lone, self.lonesel)
+
+    def finish(self):
+        e, groups = self.experts, self.groups
+        self.z = torch.empty((e, e, groups), dtype=torch.int64, device="cuda")
         _lib.call("hm_swap_tensor", ptr(self.base), ptr(self.sel), ptr(self.hitsel),
                   ptr(self.lone), ptr(self.lonesel), e, groups, ptr(self.z), stream_ptr())
-        self.experts = e
+        return self
 
     def adjust_ops(self) -> torch.Tensor:
         """The reference's op counter (swap.py:117) as a device scalar."""
@@ -232,14 +242,31 @@ def select_swap(mask: MaskLike, topology: Topology, params: LevelParams, gamma: 
     process group (NCCL) and every rank then computes the identical decision
     -- the same result as the reference on the concatenated global mask.
     """
-    reduce = None
+    sharded = False
     if group is not None:
         import torch.distributed as dist
-        if dist.get_world_size(group) > 1:
-            reduce = lambda t: dist.all_reduce(t, group=group)  # noqa: E731
-    model = _Model(mask, topology, params, placement, True, reduce)
+        sharded = dist.get_world_size(group) > 1
+    model = _Model(mask, topology, params, placement, True, defer=sharded)
     dev = model.dev
-    inter, intra = _build(dev, topology, topology.num_levels, reduce)
+    if sharded:
+        # every additive statistic in one flat buffer: one NCCL all-reduce
+        # instead of two per count vector and five per cut
+        u = topology.level_group_counts
+        parts = [_Partials(dev, u[level], defer=True) for level in range(1, topology.num_levels)]
+        parts.append(_Partials(dev, topology.num_gpus, defer=True))
+        bufs = [model.dedup_dev, model.raw_dev] + [t for p in parts for t in p.stats()]
+        flat = torch.cat([b.reshape(-1) for b in bufs])
+        dist.all_reduce(flat, group=group)
+        off = 0
+        for b in bufs:
+            b.view(-1).copy_(flat[off:off + b.numel()])
+            off += b.numel()
+        model.finish()
+        for p in parts:
+            p.finish()
+        inter, intra = parts[:-1], parts[-1]
+    else:
+        inter, intra = _build(dev, topology, topology.num_levels, None)
     q, qx = _launch_cost([p.z for p in inter], intra.z, topology, params, topology.num_levels,
                          model.dstar_dev, gamma, True, True)
     out_i = torch.empty(4, dtype=torch.int64, device="cuda")

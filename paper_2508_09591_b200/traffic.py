@@ -154,7 +154,10 @@ class _Model:
     """Device evaluation of counts + time model for one mask/placement."""
 
     def __init__(self, mask: MaskLike, topology: Topology, params: LevelParams,
-                 placement: Placement | None, dedup: bool = True, reduce=None):
+                 placement: Placement | None, dedup: bool = True, reduce=None,
+                 defer: bool = False):
+        """``defer``: stop after the counts (the caller all-reduces them, e.g.
+        batched with the swap statistics, then calls ``finish``)."""
         dev = device_mask(mask, placement)
         if dev.experts != topology.experts:
             # the reference indexes experts through the topology; keep its failure mode
@@ -166,6 +169,13 @@ class _Model:
             reduce(dd)
             reduce(raw)
         self.dedup_dev, self.raw_dev = dd, raw
+        self._args = (topology, params, dedup)
+        if not defer:
+            self.finish()
+
+    def finish(self):
+        topology, params, dedup = self._args
+        dd, raw = self.dedup_dev, self.raw_dev
         depth = topology.num_levels
         a_i, b_i, a_a, b_a = _param_arrays(topology, params)
         offs = np.cumsum([0] + self.cuts[:-1]).astype(np.int32)
@@ -181,6 +191,7 @@ class _Model:
                   aa.ctypes.data, ba.ctypes.data, ptr(offs_dev), ptr(self.times_dev),
                   ptr(self.dstar_dev), ptr(self.max_dev), stream_ptr())
         self.topology = topology
+        return self
 
     def fetch(self):
         """One device->host transfer of everything the API returns."""
