@@ -560,7 +560,8 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  int32_t* __restrict__ eoff,
                                                  int32_t* __restrict__ n_e, int mode,
                                                  unsigned long long epoch, int* __restrict__ status,
-                                                 int J, int32_t* __restrict__ pipe, int pipe_len) {
+                                                 int J, int32_t* __restrict__ pipe, int pipe_len,
+                                                 int stage_cnt) {
   const WorldDev& w = *wp;
   const int C = w.G + w.E + w.P;
   for (int i = threadIdx.x; i < pipe_len; i += blockDim.x) pipe[i] = 0;
@@ -596,8 +597,17 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
     }
   }
   cta_barrier(w, epoch, status);
-  const int32_t* cnt = w.counts[w.p * w.L];  // complete [G][G+E] matrix
-  __shared__ int32_t s_n[1024];
+  // complete [G][C] count matrix, staged in shared memory when it fits (the
+  // offset loops below read it many times), after the per-slot totals s_n
+  extern __shared__ int32_t notify_smem[];
+  int32_t* s_n = notify_smem;
+  const int32_t* cnt = w.counts[w.p * w.L];
+  if (stage_cnt) {
+    int32_t* s_cnt = notify_smem + w.E;
+    for (int i = threadIdx.x; i < w.G * C; i += blockDim.x) s_cnt[i] = cnt[i];
+    __syncthreads();
+    cnt = s_cnt;
+  }
   for (int e = threadIdx.x; e < w.E; e += blockDim.x) {
     int s = 0;
     for (int src = 0; src < w.G; ++src) s += cnt[(int64_t)src * C + w.G + e];
@@ -2470,8 +2480,14 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   }
   w->last_J = J;
   {SegScope sc(w, kSegNotify, s);
-  k_notify<<<1, 1024, 0, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e, mode,
-                              ++w->epoch, w->status, J, w->pipe, w->pipe_len);
+  const size_t cnt_bytes = (size_t)h.G * (h.G + h.E + h.P) * 4;
+  const int stage_cnt = (h.E * 4 + cnt_bytes) <= 160 * 1024 ? 1 : 0;
+  const size_t nsmem = (size_t)h.E * 4 + (stage_cnt ? cnt_bytes : 0);
+  if (nsmem > 48 * 1024)
+    HM_CUDA(cudaFuncSetAttribute(k_notify, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)nsmem));
+  k_notify<<<1, 1024, nsmem, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e, mode,
+                                  ++w->epoch, w->status, J, w->pipe, w->pipe_len, stage_cnt);
   }
   HM_LAUNCHED();
   if (J) {
