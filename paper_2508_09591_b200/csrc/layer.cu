@@ -807,17 +807,25 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
         if (lane == 0) atomicExch(status, 2);
         continue;
       }
+      const int dr = my_e >= 0 ? my_e / w.E_loc : -1;
+      const bool on_q = dr >= 0 && dr / w.L == q && my_ep >= 0;
       if (lane < w.K) {
         RowMeta m;
-        const int dr = my_e >= 0 ? my_e / w.E_loc : -1;
-        m.epos = (dr >= 0 && dr / w.L == q && my_ep >= 0)
-                     ? (int32_t)((dr - q * w.L) * w.N_cap + my_ep) : -1;
+        m.epos = on_q ? (int32_t)((dr - q * w.L) * w.N_cap + my_ep) : -1;
         m.w = my_w;
         w.meta_g[q][g * w.K + lane] = m;
       }
-      dst_base[ndst] = w.recv_g[q];
-      dst_row[ndst] = g;
-      ++ndst;
+      // the row lands directly in the expert-major slot of its first pick on
+      // GPU q; the destination's expansion copies it to the remaining picks
+      const unsigned on = __ballot_sync(0xffffffffu, on_q && lane < w.K);
+      if (on) {
+        const int k0 = __ffs(on) - 1;
+        const int d0 = __shfl_sync(0xffffffffu, dr, k0);
+        const int e0 = __shfl_sync(0xffffffffu, my_ep, k0);
+        dst_base[ndst] = w.xmaj[d0];
+        dst_row[ndst] = e0;
+        ++ndst;
+      }
     }
   }
   // dedup rows: every hit destination (mode 1) or destinations on other GPUs (mode 2)
@@ -1626,15 +1634,20 @@ __global__ void __launch_bounds__(256) k_expand_g(const WorldDev* __restrict__ w
   for (int64_t r = warp; r < total; r += nw) {
     int ep = -1;
     if (lane < w.K) ep = meta[r * w.K + lane].epos;
-    const int4* src = reinterpret_cast<const int4*>(w.recv_g[w.p] + r * w.row_bytes);
+    // the sender stored the row in its first pick's slot: copy it to the others
+    const unsigned on = __ballot_sync(0xffffffffu, ep >= 0);
+    if (__popc(on) < 2) continue;
+    const int k0 = __ffs(on) - 1;
+    const int e0 = __shfl_sync(0xffffffffu, ep, k0);
+    const int4* src = reinterpret_cast<const int4*>(xbase + (int64_t)e0 * w.row_bytes);
     for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
       int4 buf[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) buf[u] = ld_nc_v4(src + v);
+        if (v < nvec) buf[u] = ld_v4(src + v);
       }
-      for (int k = 0; k < w.K; ++k) {
+      for (int k = k0 + 1; k < w.K; ++k) {
         int e = __shfl_sync(0xffffffffu, ep, k);
         if (e < 0) continue;
         int4* dst = reinterpret_cast<int4*>(xbase + (int64_t)e * w.row_bytes);
@@ -1797,7 +1810,11 @@ __global__ void __launch_bounds__(256) k_dispatch_g(const WorldDev* __restrict__
       for (int64_t r = r0 + gw; r < r1; r += nw) {
         int ep = -1;
         if (lane < w.K) ep = __ldcg(&meta[r * w.K + lane].epos);
-        const int4* src = reinterpret_cast<const int4*>(w.recv_g[w.p] + r * w.row_bytes);
+        const unsigned on = __ballot_sync(0xffffffffu, ep >= 0);
+        if (__popc(on) < 2) continue;
+        const int k0 = __ffs(on) - 1;
+        const int e0 = __shfl_sync(0xffffffffu, ep, k0);
+        const int4* src = reinterpret_cast<const int4*>(xbase + (int64_t)e0 * w.row_bytes);
         for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
           int4 buf[kUnroll];
 #pragma unroll
@@ -1805,7 +1822,7 @@ __global__ void __launch_bounds__(256) k_dispatch_g(const WorldDev* __restrict__
             int64_t v = v0 + u * 32 + lane;
             if (v < nvec) buf[u] = ld_cg_v4(src + v);
           }
-          for (int kk = 0; kk < w.K; ++kk) {
+          for (int kk = k0 + 1; kk < w.K; ++kk) {
             int e = __shfl_sync(0xffffffffu, ep, kk);
             if (e < 0) continue;
             int4* dst = reinterpret_cast<int4*>(xbase + (int64_t)e * w.row_bytes);
