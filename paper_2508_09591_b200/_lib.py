@@ -63,6 +63,7 @@ _SIGS = {
     "hm_world_timings": (c_int32, [c_void_p, c_void_p, c_int32]),
     "hm_route_topk": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_int32, c_void_p,
                                 c_void_p, c_void_p, c_void_p]),
+    "hm_route_set_option": (c_int32, [c_int32]),
     "hm_route_group": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p,
                                  ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),

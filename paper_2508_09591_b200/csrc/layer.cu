@@ -221,6 +221,120 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
   }
 }
 
+// K1 router, four lanes per token (E % 16 == 0, E <= 256): a warp takes 8
+// tokens; lane j of a token's quad loads float4 columns j, j+4, ... (all in
+// flight at once), keeps its sorted top-K (strict > in ascending expert
+// order: ties keep the lower index), then the quad merges its four lists
+// by two butterfly steps with the same (value desc, index asc) order.  4x
+// the warps of the lane-per-token kernel for the same tokens.
+template <int K, int F4>   // F4 = float4 columns per lane = E / 16
+__global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ logits, int64_t T,
+                                                    int E, const int32_t* __restrict__ e2s,
+                                                    int renorm, int32_t* __restrict__ slot_ids,
+                                                    float* __restrict__ weights,
+                                                    int32_t* __restrict__ expert_ids) {
+  const int lane = threadIdx.x & 31, j = lane & 3;
+  int64_t warp = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t base = warp * 8; base < T; base += nw * 8) {
+    const int64_t t = base + (lane >> 2);
+    const bool live = t < T;
+    float4 v[F4];
+    const float4* row = reinterpret_cast<const float4*>(logits + (live ? t : 0) * E);
+#pragma unroll
+    for (int i = 0; i < F4; ++i)
+      v[i] = live ? __ldg(row + j + 4 * i)
+                  : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    float tv[K];
+    int ti[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      tv[k] = -INFINITY;
+      ti[k] = 0x7fffffff;
+    }
+    auto insert = [&](float x, int e) {
+      if (!(x > tv[K - 1])) return;
+#pragma unroll
+      for (int k = K - 1; k > 0; --k) {
+        if (x > tv[k]) {
+          const bool up = x > tv[k - 1];
+          tv[k] = up ? tv[k - 1] : x;
+          ti[k] = up ? ti[k - 1] : e;
+        }
+      }
+      if (x > tv[0]) {
+        tv[0] = x;
+        ti[0] = e;
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < F4; ++i) {
+      const int e = 4 * (j + 4 * i);
+      insert(v[i].x, e);
+      insert(v[i].y, e + 1);
+      insert(v[i].z, e + 2);
+      insert(v[i].w, e + 3);
+    }
+    // butterfly merge inside the quad
+#pragma unroll
+    for (int m = 1; m <= 2; m <<= 1) {
+      float ov[K];
+      int oi[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ov[k] = __shfl_xor_sync(0xffffffffu, tv[k], m);
+        oi[k] = __shfl_xor_sync(0xffffffffu, ti[k], m);
+      }
+      float nv[K];
+      int ni[K];
+      int a = 0, b = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        float av = -INFINITY, bv = -INFINITY;
+        int ai = 0x7fffffff, bi = 0x7fffffff;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          if (q == a) { av = tv[q]; ai = ti[q]; }
+          if (q == b) { bv = ov[q]; bi = oi[q]; }
+        }
+        const bool takea = av > bv || (av == bv && ai < bi);
+        nv[k] = takea ? av : bv;
+        ni[k] = takea ? ai : bi;
+        a += takea;
+        b += !takea;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        tv[k] = nv[k];
+        ti[k] = ni[k];
+      }
+    }
+    const float vmax = tv[0];
+    float denom = 0.f;
+    if (renorm) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) denom += expf(tv[k] - vmax);
+    } else {
+      float part = 0.f;
+#pragma unroll
+      for (int i = 0; i < F4; ++i)
+        part += expf(v[i].x - vmax) + expf(v[i].y - vmax) + expf(v[i].z - vmax) +
+                expf(v[i].w - vmax);
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      denom = part;
+    }
+    if (live && j == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        weights[t * K + k] = expf(tv[k] - vmax) / denom;
+        slot_ids[t * K + k] = e2s ? e2s[ti[k]] : ti[k];
+        if (expert_ids) expert_ids[t * K + k] = ti[k];
+      }
+    }
+  }
+}
+
 // DeepSeek-V3 gate (group-limited, sigmoid + bias correction):
 // scores = sigmoid(logit) (fp64, rounded to fp32), choice = scores + bias;
 // group score = sum of the two largest choices of each contiguous group of
@@ -2389,6 +2503,14 @@ HM_API int hm_world_open_peers(hm_world* w, const void* handles) {
   return 0;
 }
 
+// router kernel choice (hm_route_set_option): quad (4 lanes per token) or lane-per-token
+static int w_route_quad = 1;
+
+HM_API int hm_route_set_option(int32_t quad) {
+  w_route_quad = quad != 0;
+  return 0;
+}
+
 HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
                          const int32_t* expert_to_slot, int32_t renormalize, int32_t* slot_ids,
                          float* weights, int32_t* expert_ids, void* stream) {
@@ -2396,6 +2518,27 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
   HM_CHECK_ARG(K >= 1 && K <= kMaxK && K <= E, "hm_route_topk: K must be 1..%d and <= E", kMaxK);
   if (T == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  const bool quad_ok = w_route_quad && (E == 128 || E == 256 || E == 64 || E == 32) &&
+                       ((uintptr_t)logits & 15) == 0 && K <= 8;
+  if (quad_ok) {
+    const int blocks = grid_for(T, 64, kSMs * 8);
+#define HM_RQ(KK, FF) k_route_quad<KK, FF><<<blocks, 256, 0, s>>>(logits, T, E, expert_to_slot, \
+                                                               renormalize, slot_ids, weights, expert_ids)
+#define HM_RQ_K(KK)                    \
+  case KK:                             \
+    if (E == 32) HM_RQ(KK, 2);         \
+    else if (E == 64) HM_RQ(KK, 4);    \
+    else if (E == 128) HM_RQ(KK, 8);   \
+    else HM_RQ(KK, 16);                \
+    break;
+    switch (K) {
+      HM_RQ_K(1) HM_RQ_K(2) HM_RQ_K(3) HM_RQ_K(4) HM_RQ_K(5) HM_RQ_K(6) HM_RQ_K(7) HM_RQ_K(8)
+    }
+#undef HM_RQ_K
+#undef HM_RQ
+    HM_LAUNCHED();
+    return 0;
+  }
   if (K <= 8) {
     int blocks = grid_for(T, 256, kSMs * 8);
 #define HM_ROUTE_K(KK)                                                                      \

@@ -203,3 +203,26 @@ def test_ragged_picks_padding(hm, dedup):
                                atol=2e-2 * np.abs(ref).max())
     assert torch.count_nonzero(out[17]) == 0
     world.close()
+
+
+@pytest.mark.parametrize("E,K", [(128, 8), (256, 8), (64, 4), (32, 2), (128, 1)])
+@pytest.mark.parametrize("renorm", [True, False])
+def test_route_quad_equals_lane(hm, E, K, renorm):
+    """Four-lanes-per-token router == lane-per-token router, bit for bit
+    (ties included)."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200.layer import route_topk
+    g = torch.Generator().manual_seed(E + K)
+    logits = torch.randn(3001, E, generator=g)
+    logits[::5, 7] = logits[::5, 9]
+    logits[::11, 3:12] = 0.25           # wide ties
+    lg = logits.cuda()
+    try:
+        res = []
+        for quad in (0, 1):
+            _lib.call("hm_route_set_option", quad)
+            res.append(route_topk(lg, K, renormalize=renorm))
+    finally:
+        _lib.call("hm_route_set_option", 1)
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
