@@ -2518,7 +2518,9 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
   HM_CHECK_ARG(K >= 1 && K <= kMaxK && K <= E, "hm_route_topk: K must be 1..%d and <= E", kMaxK);
   if (T == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  const bool quad_ok = w_route_quad && (E == 128 || E == 256 || E == 64 || E == 32) &&
+  // (renormalised weights only: the full-softmax denominator is summed in the
+  // lane kernel's column order, which the quad's split sum would not reproduce)
+  const bool quad_ok = w_route_quad && renormalize && (E == 128 || E == 256 || E == 64 || E == 32) &&
                        ((uintptr_t)logits & 15) == 0 && K <= 8;
   if (quad_ok) {
     const int blocks = grid_for(T, 64, kSMs * 8);

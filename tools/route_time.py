@@ -1,0 +1,13 @@
+import torch, json
+from paper_2508_09591_b200 import _lib
+from paper_2508_09591_b200.layer import route_topk
+lg = torch.randn(32768, 128, device="cuda")
+for quad in (0, 1, 0, 1):
+    _lib.call("hm_route_set_option", quad)
+    for _ in range(5): route_topk(lg, 8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50): route_topk(lg, 8)
+    e1.record(); e1.synchronize()
+    print(json.dumps({"quad": quad, "us": e0.elapsed_time(e1) / 50 * 1e3}))
