@@ -1,4 +1,11 @@
-import torch, json
+"""Router kernel timing: lane-per-token vs four-lanes-per-token (Qwen3 shape)."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2508_09591_b200 import _lib
 from paper_2508_09591_b200.layer import route_topk
 lg = torch.randn(32768, 128, device="cuda")
