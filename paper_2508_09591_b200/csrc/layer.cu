@@ -88,6 +88,9 @@ struct WorldDev {
   int32_t* cpre[kMaxRanks];
   unsigned long long* dflag[kMaxRanks];
   unsigned long long* rflag[kMaxRanks];
+  // barrier epoch counter (this GPU, device memory): advanced by the device
+  // barriers themselves, so a step is replayable from a CUDA graph
+  unsigned long long* epoch_ctr;
 };
 
 __device__ __forceinline__ int dest_of(const WorldDev& w, int s, int e) {
@@ -119,30 +122,36 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// Called by one full CTA after its peer stores.  Thread 0 publishes `epoch`
-// to every GPU and waits (bounded, 20 s) until every GPU published it.
-__device__ void cta_barrier(const WorldDev& w, unsigned long long epoch, int* status) {
+// Called by one full CTA after its peer stores.  Thread 0 advances this GPU's
+// epoch counter, publishes the new epoch to every GPU and waits (bounded,
+// 20 s) until every GPU published it.  Every GPU issues the same sequence of
+// barriers, so the counters agree; keeping the counter on the device (not a
+// host-side argument) lets the whole step be captured in a CUDA graph.
+__device__ void cta_barrier(const WorldDev& w, int* status) {
   __syncthreads();
-  if (threadIdx.x == 0 && w.P > 1) {
-    __threadfence_system();
-    for (int q = 0; q < w.P; ++q) st_release_sys(w.flags[q * w.L] + w.p, epoch);
-    unsigned long long* mine = w.flags[w.p * w.L];
-    uint64_t t0 = globaltimer();
-    for (int q = 0; q < w.P; ++q) {
-      while (ld_acquire_sys(mine + q) < epoch) {
-        if (globaltimer() - t0 > 20000000000ull) {
-          atomicExch(status, 3);  // barrier timeout
-          break;
+  if (threadIdx.x == 0) {
+    const unsigned long long epoch = ++(*w.epoch_ctr);
+    if (w.P > 1) {
+      __threadfence_system();
+      for (int q = 0; q < w.P; ++q) st_release_sys(w.flags[q * w.L] + w.p, epoch);
+      unsigned long long* mine = w.flags[w.p * w.L];
+      uint64_t t0 = globaltimer();
+      for (int q = 0; q < w.P; ++q) {
+        while (ld_acquire_sys(mine + q) < epoch) {
+          if (globaltimer() - t0 > 20000000000ull) {
+            atomicExch(status, 3);  // barrier timeout
+            break;
+          }
+          __nanosleep(64);
         }
-        __nanosleep(64);
       }
     }
   }
   __syncthreads();
 }
 
-__global__ void k_barrier(const WorldDev* __restrict__ wp, unsigned long long epoch, int* status) {
-  cta_barrier(*wp, epoch, status);
+__global__ void k_barrier(const WorldDev* __restrict__ wp, int* status) {
+  cta_barrier(*wp, status);
 }
 
 // ---------------------------------------------------------------------------
@@ -673,7 +682,7 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  Offsets* __restrict__ offs,
                                                  int32_t* __restrict__ eoff,
                                                  int32_t* __restrict__ n_e, int mode,
-                                                 unsigned long long epoch, int* __restrict__ status,
+                                                 int* __restrict__ status,
                                                  int J, int32_t* __restrict__ pipe, int pipe_len,
                                                  int stage_cnt) {
   const WorldDev& w = *wp;
@@ -710,7 +719,7 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
       }
     }
   }
-  cta_barrier(w, epoch, status);
+  cta_barrier(w, status);
   // complete [G][C] count matrix, staged in shared memory when it fits (the
   // offset loops below read it many times), after the per-slot totals s_n
   extern __shared__ int32_t notify_smem[];
@@ -1874,8 +1883,9 @@ __global__ void __launch_bounds__(256) k_dispatch_g(const WorldDev* __restrict__
                                                     const int32_t* __restrict__ rank_g,
                                                     int32_t* __restrict__ gpos_g,
                                                     int* __restrict__ status, int* __restrict__ pipe,
-                                                    int n_push, unsigned long long seq) {
+                                                    int n_push) {
   const WorldDev& w = *wp;
+  const unsigned long long seq = *w.epoch_ctr;   // the notify barrier's epoch of this step
   __shared__ int s_role;
   if (threadIdx.x == 0) s_role = atomicAdd(pipe + 0, 1);
   __syncthreads();
@@ -1963,9 +1973,9 @@ __global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict
                                                       uint8_t* __restrict__ out, int nchunks, int J,
                                                       int* __restrict__ status,
                                                       int* __restrict__ pipe, int n_red,
-                                                      unsigned long long seq,
                                                       const uint8_t* __restrict__ addend) {
   const WorldDev& w = *wp;
+  const unsigned long long seq = *w.epoch_ctr;   // unchanged since this step's notify
   __shared__ int s_role;
   __shared__ const uint8_t* s_src[8][kMaxSrc];
   __shared__ float s_w[8][kMaxSrc];
@@ -2264,7 +2274,6 @@ struct hm_world {
   // step sequence number carried by the stage flags, CTA split
   int32_t* pipe = nullptr;
   int pipe_len = 0;
-  unsigned long long seq = 0;  // flag value of the current pipelined step
   // hm_world_set_option(w, 1, 1) -> staged dispatch/combine kernels.  Off by
   // default: measured slower on B200 (N = 2: 0.52-1.5 ms vs 0.40 ms for the
   // barrier-separated kernels, tools/pipe_tune.py) -- every stage boundary
@@ -2287,7 +2296,7 @@ struct hm_world {
   bool gather_su8 = false;     // hm_world_set_option(w, 9, 1): 8-source load batches in the gather
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
-  unsigned long long epoch = 0;
+  unsigned long long* epoch_ctr = nullptr;   // device barrier epoch counter
   bool peers_ready = false;
   int last_mode = 0;
   bool tma_gather = false;  // hm_world_set_option(w, 0, 1) selects the TMA bulk-copy gather
@@ -2442,6 +2451,9 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   HM_TRY(cudaMemset(w->pipe, 0, (size_t)w->pipe_len * 4));
   HM_TRY(cudaMalloc(&w->status, 16));
   HM_TRY(cudaMemset(w->status, 0, 16));
+  HM_TRY(cudaMalloc(&w->epoch_ctr, 8));
+  HM_TRY(cudaMemset(w->epoch_ctr, 0, 8));
+  h.epoch_ctr = w->epoch_ctr;
   HM_TRY(cudaMalloc(&w->d, sizeof(WorldDev)));
   fill_tables(w, h.p, w->sym);
   if (h.P == 1) {
@@ -2471,6 +2483,7 @@ HM_API int hm_world_destroy(hm_world* w) {
   cudaFree(w->eoff);
   cudaFree(w->n_e);
   cudaFree(w->status);
+  cudaFree(w->epoch_ctr);
   cudaFree(w->pipe);
   cudaFree(w->d);
   delete w;
@@ -2650,7 +2663,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     HM_CUDA(cudaFuncSetAttribute(k_notify, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   k_notify<<<1, 1024, nsmem, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e, mode,
-                                  ++w->epoch, w->status, J, w->pipe, w->pipe_len, stage_cnt);
+                                  w->status, J, w->pipe, w->pipe_len, stage_cnt);
   }
   HM_LAUNCHED();
   if (J) {
@@ -2660,13 +2673,10 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     int n_push = blocks * w->push_pct / 100;
     if (n_push < 1) n_push = 1;
     if (n_push > blocks - 1) n_push = blocks - 1;
-    // the notify barrier's epoch: equal on every GPU for the same step (all
-    // GPUs issue the same sequence of barrier-carrying calls), monotonic
-    w->seq = w->epoch;
     SegScope sc(w, kSegPack, s);
     k_dispatch_g<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_e,
                                         w->hitmask, w->offs, w->eoff, w->nchunks, J, w->epos,
-                                        w->rank_g, w->gpos_g, w->status, w->pipe, n_push, w->seq);
+                                        w->rank_g, w->gpos_g, w->status, w->pipe, n_push);
     HM_LAUNCHED();
     return 0;
   }
@@ -2720,7 +2730,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   HM_LAUNCHED();
   if (h.P > 1) {
     SegScope sc(w, kSegBarrier1, s);
-    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    k_barrier<<<1, 32, 0, s>>>(w->d, w->status);
     HM_LAUNCHED();
   }
   return 0;
@@ -2796,7 +2806,7 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
       SegScope sc(w, kSegGather, s);
       kern<<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->epos, w->offs, w->gpos_g,
                                   (uint8_t*)out, w->nchunks, w->last_J, w->status, w->pipe, n_red,
-                                  w->seq, addend);
+                                  addend);
       rc = hm::launch_status();
     });
     return rc;
@@ -2820,7 +2830,7 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
   if (mode != 1) HM_CHECK_ARG(wts && ids, "hm_combine: raw/hybrid combine needs ids and weights");
   if (h.P > 1) {
     SegScope sc(w, kSegBarrier2, s);
-    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    k_barrier<<<1, 32, 0, s>>>(w->d, w->status);
     HM_LAUNCHED();
   }
   const int64_t T = (int64_t)h.L * h.T_r;
@@ -2876,7 +2886,7 @@ HM_API int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int
 HM_API int hm_world_barrier(hm_world* w, void* stream) {
   HM_CHECK_ARG(w, "hm_world_barrier: null world");
   if (w->h.P > 1) {
-    k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(w->d, ++w->epoch, w->status);
+    k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(w->d, w->status);
     HM_LAUNCHED();
   }
   return 0;
@@ -2994,7 +3004,7 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
                                               w->gpos, w->epos, mode, dw);
   HM_LAUNCHED();
   if (h.P > 1) {
-    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    k_barrier<<<1, 32, 0, s>>>(w->d, w->status);
     HM_LAUNCHED();
   }
   if (mode != 0 && !(h.P == 1 && mode == 2)) {
@@ -3024,7 +3034,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
     HM_LAUNCHED();
   }
   if (h.P > 1) {
-    k_barrier<<<1, 32, 0, s>>>(w->d, ++w->epoch, w->status);
+    k_barrier<<<1, 32, 0, s>>>(w->d, w->status);
     HM_LAUNCHED();
   }
   const int64_t T = (int64_t)h.L * h.T_r;
