@@ -99,6 +99,27 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
             for l in range(L):
                 xm = ep.read("xmaj", l, dtype, int(rows[l, 1]) * M)
                 assert torch.equal(xm, xm0[l]), ("xmaj", pipelined, pct, l)
+        # the step replayed from a CUDA graph (device-side barrier epochs):
+        # every rank captures and replays the same sequence
+        xin = x[lo:hi].cuda()
+        gout = torch.empty_like(out)
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            ep.dispatch(xin, slot, w, dedup=dedup)
+            ep.combine(slot, w, dedup=dedup, out=gout)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            ep.dispatch(xin, slot, w, dedup=dedup)
+            ep.combine(slot, w, dedup=dedup, out=gout)
+        for _ in range(3):
+            gout.zero_()
+            graph.replay()
+        torch.cuda.synchronize()
+        ep.check_status()
+        assert torch.equal(gout, out), "graph replay"
     ep.close()
 
 
