@@ -379,6 +379,41 @@ def main():
     with ClockSampler(local) as clocks:
         ms = timed(ep, MODE, args.steps, args.warmup)
     main_launches = launches[MODE]
+    # the same step replayed from a CUDA graph (device-side barrier epochs make
+    # the exchange capturable): launch overhead and inter-kernel gaps removed
+    graph_ms = None
+    try:
+        gst = torch.cuda.Stream()
+        gst.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(gst):
+            step(ep, MODE, out)
+        torch.cuda.current_stream().wait_stream(gst)
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg):
+            step(ep, MODE, out)
+        for _ in range(3):
+            cg.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tot_g, n_g = 0.0, max(5, args.steps // 2)
+        for _ in range(n_g):
+            flush.zero_()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            cg.replay()
+            g1.record()
+            g1.synchronize()
+            tot_g += g0.elapsed_time(g1)
+        tg = torch.tensor([tot_g / n_g], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        graph_ms = float(tg.item())
+        ep.check_status()
+        del cg
+    except Exception as exc:   # noqa: BLE001 -- report, keep the eager numbers
+        graph_ms = f"unavailable: {exc}"
     ms_pipelined = None
     if world > 1 and args.pipelined_variant:   # staged kernels with NVLink flags (slower)
         ep.set_pipelined(True)
@@ -722,6 +757,7 @@ def main():
                         "speedup_dedup_vs_nodedup": ms_raw / ms,
                         "link_time_ratio": link_raw / max(link_dedup, 1e-9) if link_dedup else None},
             "pipelined_variant_ms_per_step": ms_pipelined,
+            "cuda_graph_ms_per_step": graph_ms,
             "hd2_2x4": hd2,
             "dedup_all_ranks": {"ms_per_step": ms_all,
                                 "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_all.tolist())}},
