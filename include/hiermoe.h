@@ -161,8 +161,9 @@ int hm_memcpy(void* dst, const void* src, int64_t bytes, void* stream);
 int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
                   const int32_t* expert_to_slot, int32_t renormalize, int32_t* slot_ids,
                   float* weights, int32_t* expert_ids, void* stream);
-/* Router kernel choice: 1 = four lanes per token (E in {32, 64, 128, 256},
- * renormalised weights), 0 = lane per token (default).  Identical results. */
+/* Router kernel choice: 1 = four lanes per token where it applies (default;
+ * E in {32, 64, 128, 256}, renormalised weights), 0 = lane per token always.
+ * Identical results. */
 int hm_route_set_option(int32_t quad);
 /* DeepSeek-V3 group-limited gate (the reference specifies only
  * softmax top-K): sigmoid scores + bias choice, the topk_group

@@ -57,6 +57,7 @@ struct RowMeta {
 // device-resident view of the world (pointers valid on this GPU)
 struct WorldDev {
   int G, L, P, p, E, K, M, E_loc, elem;
+  int e_shift;   // log2(E_loc) when E_loc is a power of two, else -1
   // relay (phase-1 of a two-level dispatch): U1 > 0 groups of F = G/U1 ranks;
   // pick e of source s goes to rank (e / (E/U1)) * F + s % F (the rank with
   // the source's local index inside the pick's group), carrying slot ids
@@ -93,8 +94,11 @@ struct WorldDev {
   unsigned long long* epoch_ctr;
 };
 
+__device__ __forceinline__ int rank_of_slot(const WorldDev& w, int e) {
+  return w.e_shift >= 0 ? e >> w.e_shift : e / w.E_loc;
+}
 __device__ __forceinline__ int dest_of(const WorldDev& w, int s, int e) {
-  return w.U1 ? (e / (w.E / w.U1)) * w.F + s % w.F : e / w.E_loc;
+  return w.U1 ? (e / (w.E / w.U1)) * w.F + s % w.F : rank_of_slot(w, e);
 }
 
 // per-step offsets computed by k_notify (local, not symmetric)
@@ -129,9 +133,9 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // host-side argument) lets the whole step be captured in a CUDA graph.
 __device__ void cta_barrier(const WorldDev& w, int* status) {
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && w.P > 1) {   // one GPU: nothing to wait for
     const unsigned long long epoch = ++(*w.epoch_ctr);
-    if (w.P > 1) {
+    {
       __threadfence_system();
       for (int q = 0; q < w.P; ++q) st_release_sys(w.flags[q * w.L] + w.p, epoch);
       unsigned long long* mine = w.flags[w.p * w.L];
@@ -580,6 +584,7 @@ __global__ void __launch_bounds__(256, 3) k_route_lane(const float* __restrict__
 // plan: grid (chunks, L).  Stable ranks: destination ranks by warp ballot,
 // slot ranks by comparing with earlier lanes' picks via shuffles, then a
 // prefix over the chunk's warps.
+template <int KT>   // KT = K (1..8) or kMaxK (any K, guarded by w.K)
 __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp,
                                                  const int32_t* __restrict__ ids, int nchunks,
                                                  int32_t* __restrict__ chunk_cnt,
@@ -600,12 +605,12 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
   const int64_t t_in = (int64_t)chunk * kChunk + warp * 32 + lane;  // token within source
   const bool valid = t_in < w.T_r;
   const int64_t t = (int64_t)s_loc * w.T_r + t_in;                   // local token index
-  int S[kMaxK];
+  int S[KT];
   unsigned long long hit = 0;
 #pragma unroll
-  for (int k = 0; k < kMaxK; ++k) {
+  for (int k = 0; k < KT; ++k) {
     S[k] = -1;
-    if (k < w.K && valid) {
+    if ((KT != kMaxK || k < w.K) && valid) {
       int e = ids[t * w.K + k];
       if (e < -1 || e >= w.E) {   // -1 = padding (no pick)
         atomicExch(status, 4);
@@ -632,13 +637,13 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
   // rank of my pick = earlier lanes in that slot's mask (stable, O(K))
   unsigned* s_lanes = reinterpret_cast<unsigned*>(s_cnt + kPlanWarps * C) + warp * w.E;
 #pragma unroll
-  for (int k = 0; k < kMaxK; ++k)
-    if (k < w.K && S[k] >= 0) atomicOr(s_lanes + S[k], 1u << lane);
+  for (int k = 0; k < KT; ++k)
+    if ((KT != kMaxK || k < w.K) && S[k] >= 0) atomicOr(s_lanes + S[k], 1u << lane);
   __syncwarp();
-  int re[kMaxK];
+  int re[KT];
 #pragma unroll
-  for (int k = 0; k < kMaxK; ++k)
-    re[k] = (k < w.K && S[k] >= 0) ? __popc(s_lanes[S[k]] & lt) : 0;
+  for (int k = 0; k < KT; ++k)
+    re[k] = ((KT != kMaxK || k < w.K) && S[k] >= 0) ? __popc(s_lanes[S[k]] & lt) : 0;
   for (int e = lane; e < w.E; e += 32) s_cnt[warp * C + w.G + e] = __popc(s_lanes[e]);
   __syncthreads();
   // exclusive prefix over warps per counter; chunk totals out
@@ -665,8 +670,8 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
   }
   if (valid) {
 #pragma unroll
-    for (int k = 0; k < kMaxK; ++k)
-      if (k < w.K) rank_e[t * w.K + k] = S[k] >= 0 ? re[k] + s_cnt[warp * C + w.G + S[k]] : -1;
+    for (int k = 0; k < KT; ++k)
+      if (KT != kMaxK || k < w.K) rank_e[t * w.K + k] = S[k] >= 0 ? re[k] + s_cnt[warp * C + w.G + S[k]] : -1;
     hitmask[t] = hit;
   }
 }
@@ -677,6 +682,11 @@ __global__ void __launch_bounds__(kChunk) k_plan(const WorldDev* __restrict__ wp
 //   eoff[s_loc][e] = ebase[e] + sum_{s' < s} c[s', e]  (expert-major base of
 //   source s's rows for slot e at dest(e)), where ebase[e] = sum of N_e' over
 //   earlier local slots of the same destination.
+// Latency-bound (one CTA, a few KB of counts): world scalars live in
+// registers, the chunk prefix keeps 16 loads in flight per column, and the
+// derived offsets are one flat index space over the whole CTA (every output
+// is a short sum over the staged count matrix), so no thread walks several
+// output families one after another.
 __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp, int nchunks,
                                                  int32_t* __restrict__ chunk_cnt,
                                                  Offsets* __restrict__ offs,
@@ -686,113 +696,120 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  int J, int32_t* __restrict__ pipe, int pipe_len,
                                                  int stage_cnt) {
   const WorldDev& w = *wp;
-  const int C = w.G + w.E + w.P;
+  const int G = w.G, E = w.E, L = w.L, P = w.P, gp = w.p, E_loc = w.E_loc;
+  const int C = G + E + P, CG = G + E;
   for (int i = threadIdx.x; i < pipe_len; i += blockDim.x) pipe[i] = 0;
-  // mode 2 (dedup across GPUs only): sources on the destination's own GPU
-  // write expert-major rows directly and occupy no receive rows
-  auto ships = [&](int src, int dst) {
-    return mode == 1 || (mode == 2 && src / w.L != dst / w.L);
-  };
-  for (int i = threadIdx.x; i < w.L * C; i += blockDim.x) {
-    int s_loc = i / C, c = i % C;
+  for (int i = threadIdx.x; i < L * C; i += blockDim.x) {
+    const int s_loc = i / C, c = i - s_loc * C;
     int32_t* col = chunk_cnt + (int64_t)s_loc * nchunks * C + c;
     int run = 0;
-    for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {   // 8 loads in flight, then the stores
-      int v[8];
+    for (int ch0 = 0; ch0 < nchunks; ch0 += 16) {   // 16 loads in flight, then the stores
+      int v[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = ch0 + j < nchunks ? col[(int64_t)(ch0 + j) * C] : 0;
+      for (int j = 0; j < 16; ++j) v[j] = ch0 + j < nchunks ? col[(int64_t)(ch0 + j) * C] : 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 16; ++j) {
         if (ch0 + j < nchunks) col[(int64_t)(ch0 + j) * C] = run;
         run += v[j];
       }
     }
-    int sg = w.p * w.L + s_loc;
-    for (int q = 0; q < w.P; ++q) w.counts[q * w.L][(int64_t)sg * C + c] = run;
+    const int sg = gp * L + s_loc;
+    for (int q = 0; q < P; ++q) w.counts[q * L][(int64_t)sg * C + c] = run;
     // pipelined mode 3: this source's row prefix for GPU q at every stage
     // boundary, stored on q (receive rows of stage j = [cpre[j], cpre[j+1]))
-    if (J > 0 && c >= w.G + w.E && c - (w.G + w.E) != w.p) {
-      const int q = c - (w.G + w.E);
+    if (J > 0 && c >= CG && c - CG != gp) {
+      const int q = c - CG;
       for (int j = 0; j <= J; ++j) {
         const int b = j * nchunks / J;
-        w.cpre[q * w.L][sg * (kMaxJ + 1) + j] = b < nchunks ? col[(int64_t)b * C] : run;
+        w.cpre[q * L][sg * (kMaxJ + 1) + j] = b < nchunks ? col[(int64_t)b * C] : run;
       }
     }
   }
   cta_barrier(w, status);
-  // complete [G][C] count matrix, staged in shared memory when it fits (the
-  // offset loops below read it many times), after the per-slot totals s_n
+  // shared memory: s_n[E] per-slot totals, s_eb[E] expert-major bases,
+  // s_gpu[G] GPU of each rank, then the [G][C] count matrix when it fits
   extern __shared__ int32_t notify_smem[];
   int32_t* s_n = notify_smem;
-  const int32_t* cnt = w.counts[w.p * w.L];
+  int32_t* s_eb = s_n + E;
+  int32_t* s_gpu = s_eb + E;
+  const int32_t* cnt = w.counts[gp * L];
+  for (int r = threadIdx.x; r < G; r += blockDim.x) s_gpu[r] = r / L;
   if (stage_cnt) {
-    int32_t* s_cnt = notify_smem + w.E;
-    for (int i = threadIdx.x; i < w.G * C; i += blockDim.x) s_cnt[i] = cnt[i];
+    int32_t* s_cnt = s_gpu + G;
+    for (int i = threadIdx.x; i < G * C; i += blockDim.x) s_cnt[i] = cnt[i];
     __syncthreads();
     cnt = s_cnt;
   }
-  for (int e = threadIdx.x; e < w.E; e += blockDim.x) {
-    int s = 0;
-    for (int src = 0; src < w.G; ++src) s += cnt[(int64_t)src * C + w.G + e];
-    s_n[e] = s;
-    n_e[e] = s;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int sum = 0;
+    for (int src = 0; src < G; ++src) sum += cnt[(int64_t)src * C + G + e];
+    s_n[e] = sum;
+    n_e[e] = sum;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < w.L * w.E; i += blockDim.x) {
-    int s_loc = i / w.E, e = i % w.E;
-    int sg = w.p * w.L + s_loc;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int base = 0;
-    for (int e2 = (e / w.E_loc) * w.E_loc; e2 < e; ++e2) base += s_n[e2];
-    for (int src = 0; src < sg; ++src) base += cnt[(int64_t)src * C + w.G + e];
-    eoff[i] = base;
+    for (int e2 = (e / E_loc) * E_loc; e2 < e; ++e2) base += s_n[e2];
+    s_eb[e] = base;
   }
-  for (int i = threadIdx.x; i < w.L * w.G; i += blockDim.x) {
-    int s_loc = i / w.G, d = i % w.G;
-    (void)0;
-    int sg = w.p * w.L + s_loc;
-    int o = 0;
-    for (int src = 0; src < sg; ++src)
-      if (ships(src, d)) o += cnt[(int64_t)src * C + d];
-    offs->off[s_loc][d] = o;
-  }
-  for (int i = threadIdx.x; i < w.L * (w.G + 1); i += blockDim.x) {
-    const int d_loc = i / (w.G + 1), src = i % (w.G + 1);
-    const int dg = w.p * w.L + d_loc;
-    int o = 0;
-    for (int s2 = 0; s2 < src; ++s2)
-      if (ships(s2, dg)) o += cnt[(int64_t)s2 * C + dg];
-    offs->offd[d_loc][src] = o;
-  }
-  // mode 3: GPU-level offsets (only sources on other GPUs ship)
-  const int CG = w.G + w.E;
-  for (int i = threadIdx.x; i < w.L * w.P; i += blockDim.x) {
-    const int s_loc = i / w.P, q = i % w.P;
-    const int sg = w.p * w.L + s_loc;
-    int o = 0;
-    for (int src = 0; src < sg; ++src)
-      if (src / w.L != q) o += cnt[(int64_t)src * C + CG + q];
-    offs->off_g[s_loc][q] = o;
-  }
-  for (int src = threadIdx.x; src <= w.G; src += blockDim.x) {
-    int o = 0;
-    for (int s2 = 0; s2 < src; ++s2)
-      if (s2 / w.L != w.p) o += cnt[(int64_t)s2 * C + CG + w.p];
-    offs->offd_g[src] = o;
-    if (src == w.G) {
-      offs->R_g = o;
-      if (mode == 3 && o > w.Rg_cap) atomicExch(status, 2);
+  __syncthreads();
+  // mode 2 (dedup across GPUs only): sources on the destination's own GPU
+  // write expert-major rows directly and occupy no receive rows
+  auto ships = [&](int src, int dst) {
+    return mode == 1 || (mode == 2 && s_gpu[src] != s_gpu[dst]);
+  };
+  // flat index space: [eoff L*E][off L*G][offd L*(G+1)][off_g L*P][offd_g G+1][R/Nd L]
+  const int n0 = L * E, n1 = n0 + L * G, n2 = n1 + L * (G + 1), n3 = n2 + L * P,
+            n4 = n3 + G + 1, n5 = n4 + L;
+  for (int i = threadIdx.x; i < n5; i += blockDim.x) {
+    if (i < n0) {
+      const int s_loc = i / E, e = i - s_loc * E;
+      const int sg = gp * L + s_loc;
+      int base = s_eb[e];
+      for (int src = 0; src < sg; ++src) base += cnt[(int64_t)src * C + G + e];
+      eoff[i] = base;
+    } else if (i < n1) {
+      const int k = i - n0, s_loc = k / G, d = k - s_loc * G;
+      const int sg = gp * L + s_loc;
+      int o = 0;
+      for (int src = 0; src < sg; ++src)
+        if (ships(src, d)) o += cnt[(int64_t)src * C + d];
+      offs->off[s_loc][d] = o;
+    } else if (i < n2) {
+      const int k = i - n1, d_loc = k / (G + 1), src = k - d_loc * (G + 1);
+      const int dg = gp * L + d_loc;
+      int o = 0;
+      for (int s2 = 0; s2 < src; ++s2)
+        if (ships(s2, dg)) o += cnt[(int64_t)s2 * C + dg];
+      offs->offd[d_loc][src] = o;
+    } else if (i < n3) {   // mode 3: GPU-level offsets (only sources on other GPUs ship)
+      const int k = i - n2, s_loc = k / P, q = k - s_loc * P;
+      const int sg = gp * L + s_loc;
+      int o = 0;
+      for (int src = 0; src < sg; ++src)
+        if (s_gpu[src] != q) o += cnt[(int64_t)src * C + CG + q];
+      offs->off_g[s_loc][q] = o;
+    } else if (i < n4) {
+      const int src = i - n3;
+      int o = 0;
+      for (int s2 = 0; s2 < src; ++s2)
+        if (s_gpu[s2] != gp) o += cnt[(int64_t)s2 * C + CG + gp];
+      offs->offd_g[src] = o;
+      if (src == G) {
+        offs->R_g = o;
+        if (mode == 3 && o > w.Rg_cap) atomicExch(status, 2);
+      }
+    } else {
+      const int d_loc = i - n4, dg = gp * L + d_loc;
+      int r = 0;
+      for (int src = 0; src < G; ++src)
+        if (ships(src, dg)) r += cnt[(int64_t)src * C + dg];
+      offs->R[d_loc] = r;
+      int n = 0;
+      for (int e = dg * E_loc; e < (dg + 1) * E_loc; ++e) n += s_n[e];
+      offs->Nd[d_loc] = n;
+      if (r > w.R_cap || (!w.U1 && n > w.N_cap)) atomicExch(status, 2);  // capacity overflow
     }
-  }
-  for (int d_loc = threadIdx.x; d_loc < w.L; d_loc += blockDim.x) {
-    int dg = w.p * w.L + d_loc;
-    int r = 0;
-    for (int src = 0; src < w.G; ++src)
-      if (ships(src, dg)) r += cnt[(int64_t)src * C + dg];
-    offs->R[d_loc] = r;
-    int n = 0;
-    for (int e = dg * w.E_loc; e < (dg + 1) * w.E_loc; ++e) n += s_n[e];
-    offs->Nd[d_loc] = n;
-    if (r > w.R_cap || (!w.U1 && n > w.N_cap)) atomicExch(status, 2);  // capacity overflow
   }
 }
 
@@ -908,7 +925,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
       int e = __shfl_sync(0xffffffffu, my_e, k);
       int ep = __shfl_sync(0xffffffffu, my_ep, k);
       if (e < 0 || ep < 0) continue;
-      const int d = e / w.E_loc;
+      const int d = rank_of_slot(w, e);
       if (mode >= 2 && d / w.L != w.p) continue;
       dst_base[ndst] = w.xmaj[d];
       dst_row[ndst] = ep;
@@ -930,7 +947,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
         if (lane == 0) atomicExch(status, 2);
         continue;
       }
-      const int dr = my_e >= 0 ? my_e / w.E_loc : -1;
+      const int dr = my_e >= 0 ? rank_of_slot(w, my_e) : -1;
       const bool on_q = dr >= 0 && dr / w.L == q && my_ep >= 0;
       if (lane < w.K) {
         RowMeta m;
@@ -1089,7 +1106,7 @@ __global__ void __launch_bounds__(256) k_pack_local(const WorldDev* __restrict__
         }
       }
       epos_out[t * w.K + lane] = ep;
-      if (ep >= 0) dst = w.xmaj[e / w.E_loc] + (int64_t)ep * w.row_bytes;
+      if (ep >= 0) dst = w.xmaj[rank_of_slot(w, e)] + (int64_t)ep * w.row_bytes;
     }
     for (int k = 0; k < w.K; ++k) {
       int4* d = reinterpret_cast<int4*>(
@@ -1362,7 +1379,7 @@ __device__ __forceinline__ int gather_sources(const WorldDev& w, int64_t t, cons
       int e = ids[t * w.K + k];
       int ep = epos[t * w.K + k];
       if (e < 0 || ep < 0) continue;
-      const int d = e / w.E_loc;
+      const int d = rank_of_slot(w, e);
       if (mode >= 2 && d / w.L != w.p) continue;
       srcs[n] = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
       ws[n] = grad ? 1.f : wts[t * w.K + k];
@@ -1427,7 +1444,7 @@ __device__ __forceinline__ int gather_sources_warp(const WorldDev& w, int64_t t,
       const int e = ids[t * w.K + lane];
       const int ep = epos[t * w.K + lane];
       if (e >= 0 && ep >= 0) {
-        const int d = e / w.E_loc;
+        const int d = rank_of_slot(w, e);
         if (!(mode >= 2 && d / w.L != w.p)) {
           v = true;
           ptr = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
@@ -1633,7 +1650,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32) k_pack_bulk(
     }
     if (lane == 0) mbar_wait(&bars[wid][b], phase[b]);
     // destinations: every lane resolves its own pick's address, lane 0 issues
-    uint8_t* dst = my_ep >= 0 ? w.xmaj[my_e / w.E_loc] + (int64_t)my_ep * w.row_bytes : nullptr;
+    uint8_t* dst = my_ep >= 0 ? w.xmaj[rank_of_slot(w, my_e)] + (int64_t)my_ep * w.row_bytes : nullptr;
     for (int k = 0; k < w.K; ++k) {
       uint8_t* dk = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)dst, k);
       if (lane == 0 && dk)
@@ -2108,7 +2125,7 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
       for (int k = 0; k < w.K; ++k) {
         int e = ids[t * w.K + k], ep = epos[t * w.K + k];
         if (e < 0 || ep < 0) continue;
-        const int d = e / w.E_loc;
+        const int d = rank_of_slot(w, e);
         if (mode == 2 && d / w.L != w.p) continue;
         drow[nd] = w.gy[d] + (int64_t)ep * w.row_bytes;
         yrow[nd] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
@@ -2232,7 +2249,7 @@ __global__ void k_gate_grad(const WorldDev* __restrict__ wp, const int32_t* __re
     const int k = (int)(i % w.K);
     const int e = ids[i];
     if (e < 0 || mode == 0) continue;
-    const int d = e / w.E_loc;
+    const int d = rank_of_slot(w, e);
     if (mode == 2 && d / w.L == w.p) continue;   // direct pick: k_pack_grad wrote it
     const int gp = gpos[t * w.G + d];
     if (gp >= 0) dw[i] = w.gw[d][(int64_t)gp * w.K + k];
@@ -2389,6 +2406,9 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   h.K = top_k;
   h.M = hidden;
   h.E_loc = experts / ranks;
+  h.e_shift = -1;
+  for (int b = 0; b < 31; ++b)
+    if ((1 << b) == h.E_loc) h.e_shift = b;
   h.elem = elem_bytes;
   h.T_r = tokens_per_rank;
   h.row_bytes = (int64_t)hidden * elem_bytes;
@@ -2517,8 +2537,10 @@ HM_API int hm_world_open_peers(hm_world* w, const void* handles) {
 }
 
 // router kernel choice (hm_route_set_option): quad (4 lanes per token) or
-// lane-per-token (default; the quad measured the same, 21.8 vs 21.9 us)
-static int w_route_quad = 0;
+// lane-per-token.  The quad is the default where it applies (renormalised
+// weights, E in {32, 64, 128, 256}): 14.7 vs 16.3 us device time for the
+// Qwen3 step's 32768 x 128 logits (warm, tools/ctrl_time.py); identical bits.
+static int w_route_quad = 1;
 
 HM_API int hm_route_set_option(int32_t quad) {
   w_route_quad = quad != 0;
@@ -2639,11 +2661,24 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   const WorldDev& h = w->h;
   dim3 grid(w->nchunks, h.L);
   size_t smem = (size_t)kPlanWarps * (h.G + 2 * h.E + h.P) * 4;
-  if (smem > 48 * 1024)
-    HM_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {SegScope sc(w, kSegPlan, s);
-  k_plan<<<grid, kChunk, smem, s>>>(w->d, ids, w->nchunks, w->chunk_cnt, w->rank_d, w->rank_e,
-                                    w->hitmask, w->rank_g, w->status);
+#define HM_PLAN(KK)                                                                          \
+  do {                                                                                       \
+    if (smem > 48 * 1024)                                                                    \
+      HM_CUDA(cudaFuncSetAttribute(k_plan<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                   (int)smem));                                              \
+    k_plan<KK><<<grid, kChunk, smem, s>>>(w->d, ids, w->nchunks, w->chunk_cnt, w->rank_d,    \
+                                          w->rank_e, w->hitmask, w->rank_g, w->status);      \
+  } while (0)
+  switch (h.K) {
+    case 1: HM_PLAN(1); break;
+    case 2: HM_PLAN(2); break;
+    case 4: HM_PLAN(4); break;
+    case 6: HM_PLAN(6); break;
+    case 8: HM_PLAN(8); break;
+    default: HM_PLAN(kMaxK); break;
+  }
+#undef HM_PLAN
   }
   HM_LAUNCHED();
   // pipelined per-GPU dedup: J stages per source (L * J ~ kStages per GPU)
@@ -2657,8 +2692,8 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   w->last_J = J;
   {SegScope sc(w, kSegNotify, s);
   const size_t cnt_bytes = (size_t)h.G * (h.G + h.E + h.P) * 4;
-  const int stage_cnt = (h.E * 4 + cnt_bytes) <= 160 * 1024 ? 1 : 0;
-  const size_t nsmem = (size_t)h.E * 4 + (stage_cnt ? cnt_bytes : 0);
+  const int stage_cnt = ((2 * h.E + h.G) * 4 + cnt_bytes) <= 160 * 1024 ? 1 : 0;
+  const size_t nsmem = (size_t)(2 * h.E + h.G) * 4 + (stage_cnt ? cnt_bytes : 0);
   if (nsmem > 48 * 1024)
     HM_CUDA(cudaFuncSetAttribute(k_notify, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));

@@ -223,6 +223,6 @@ def test_route_quad_equals_lane(hm, E, K, renorm):
             _lib.call("hm_route_set_option", quad)
             res.append(route_topk(lg, K, renormalize=renorm))
     finally:
-        _lib.call("hm_route_set_option", 0)
+        _lib.call("hm_route_set_option", 1)     # the default
     for a, b in zip(*res):
         assert torch.equal(a, b)
