@@ -127,10 +127,16 @@ def test_dispatch_combine_parity(hm, name, dedup):
                 assert torch.equal(world.read("xmaj", d, dtype, int(rn[d, 1]) * M), before[d])
         world.set_bulk_pack(False)
         world.set_lean_pack(True)
-    # combine with a stand-in expert y = x * scale[slot]; both gather variants
+    # combine with a stand-in expert y = x * scale[slot]; every gather variant
     _apply_experts(world, plan, E, dtype)
     world.set_tma_gather(False)
     out_reg = world.combine(slot, w, dedup=dedup).clone()
+    # addend (e.g. a shared expert's output) summed last in fp32
+    add = (x * 0.5).to(dtype).cuda()
+    out_add = world.combine(slot, w, dedup=dedup, addend=add).clone()
+    rtol_a = 1e-5 if dtype == torch.float32 else 2e-2
+    torch.testing.assert_close(out_add.float(), out_reg.float() + add.float(), rtol=rtol_a,
+                               atol=rtol_a * float(out_reg.float().abs().max()))
     world.set_tma_gather(True)
     out = world.combine(slot, w, dedup=dedup)
     torch.cuda.synchronize()
