@@ -23,6 +23,7 @@
 
 #include "hm_common.cuh"
 
+#include <atomic>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <string.h>
@@ -871,6 +872,192 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// Per-group copies of the two MN-major operand maps with the token extent cut
+// at the group's end (tensormap.replace of global_dim[1]), so a group's tail
+// k-block arrives from TMA with the rows past the group zero-filled and no
+// CTA has to patch shared memory: the weight-gradient pair kernel below then
+// runs the forward pair kernel's pipeline unchanged.
+__global__ void k_group_maps(const __grid_constant__ CUtensorMap map_a,
+                             const __grid_constant__ CUtensorMap map_b,
+                             const int32_t* __restrict__ n_rows, int groups,
+                             CUtensorMap* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  int row = 0;
+  for (int g = 0; g < groups; ++g) {
+    row += n_rows[g];
+    out[g] = map_a;
+    out[groups + g] = map_b;
+    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 1, %1;" ::"l"(
+                     reinterpret_cast<uint64_t>(out + g)),
+                 "r"(row)
+                 : "memory");
+    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 1, %1;" ::"l"(
+                     reinterpret_cast<uint64_t>(out + groups + g)),
+                 "r"(row)
+                 : "memory");
+  }
+  asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+}
+
+// Weight-gradient GEMM on CTA pairs with per-group tensor maps (hm_ffn_set_option(3, 2)):
+// 256 x 256 output tiles, both CTAs' TMA loads complete on the leader's
+// barrier (64 KB per stage), one MMA thread, no per-stage hand-off.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_wgrad_pair_tm(const CUtensorMap* __restrict__ gmaps, GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages2 * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
+  uint64_t* empty = full + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ TileMap tm;
+  constexpr uint32_t kIdescPairMN = kIdesc2 | (1u << 15) | (1u << 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    int acc = 0, row = 0;
+    tm.ntile_n = args.N / BN;
+    for (int g = 0; g < args.groups; ++g) {
+      const int n = args.n_rows[g];
+      tm.start[g] = acc;
+      tm.row0[g] = row;
+      tm.rows[g] = n;
+      acc += args.m_out / BM2 * tm.ntile_n;
+      row += n;
+    }
+    tm.start[args.groups] = acc;
+    tm.total = acc;
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int g_last = -1;
+      for (int t = cid; t < tm.total; t += ncl) {
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        const CUtensorMap* ma = gmaps + g;
+        const CUtensorMap* mb = gmaps + args.groups + g;
+        if (g != g_last) {   // maps written by k_group_maps: acquire in the tensormap proxy
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                           reinterpret_cast<uint64_t>(ma))
+                       : "memory");
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                           reinterpret_cast<uint64_t>(mb))
+                       : "memory");
+          g_last = g;
+        }
+        const int a0 = mt * BM2 + (int)rank * 128, b0 = nt * BN + (int)rank * 128;
+        const int kblocks = (tm.rows[g] + BK - 1) / BK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (leader) mbar_expect_tx(full + stage, 2 * kStageBytes2);
+          const int k0 = tm.row0[g] + kb * BK;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            tma_load_2d_pair(sa + stage * kHalfBytes + j * 8192, ma, full + stage, a0 + 64 * j, k0);
+            tma_load_2d_pair(sb + stage * kHalfBytes + j * 8192, mb, full + stage, b0 + 64 * j, k0);
+          }
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < tm.total; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        const int kblocks = (tm.rows[g] + BK - 1) / BK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t sa0 = smem_u32(sa + stage * kHalfBytes);
+          const uint32_t sb0 = smem_u32(sb + stage * kHalfBytes);
+          // tail k-block: only the k-steps that hold rows of the group (the
+          // single-CTA kernel's order, so the same bits); the rest are zero fill
+          const int valid = tm.rows[g] - kb * BK;
+          const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
+          for (int k = 0; k < ksteps; ++k) {
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                "l"(smem_desc_mn(sa0 + k * UK * 128)), "l"(smem_desc_mn(sb0 + k * UK * 128)),
+                "r"(kIdescPairMN), "r"((kb | k) ? 1u : 0u));
+          }
+          umma_commit_pair(empty + stage);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(tfull + acc);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    int it = 0;
+    for (int t = cid; t < tm.total; t += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int r_in = mt * BM2 + (int)rank * 128 + q * 32 + lane;
+      store_tile<3>(args, tm, g, nt, r_in, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // expert FFN backward helpers
 // group layout for the weight-gradient GEMMs: token rows of group g are
@@ -1077,7 +1264,24 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
-  if (g_wgrad_pair && m_out % BM2 == 0) {
+  if (g_wgrad_pair == 2 && m_out % BM2 == 0) {
+    // per-group maps live in a ring of slots so that GEMMs in flight on
+    // several streams (micro-batches) never share one
+    constexpr int kRing = 16;
+    static CUtensorMap* ring = nullptr;   // [kRing][2][kMaxGroups] (device)
+    static std::atomic<unsigned> next{0};
+    if (!ring) HM_CUDA(cudaMalloc(&ring, (size_t)kRing * 2 * kMaxGroups * sizeof(CUtensorMap)));
+    CUtensorMap* gmaps = ring + (size_t)(next++ % kRing) * 2 * kMaxGroups;
+    k_group_maps<<<1, 32, 0, s>>>(ma, mb, n_rows, groups, gmaps);
+    HM_LAUNCHED();
+    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
+    HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair_tm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem2));
+    k_wgrad_pair_tm<<<sms & ~1, kThreads, smem2, s>>>(gmaps, args);
+    HM_LAUNCHED();
+    return 0;
+  }
+  if (g_wgrad_pair == 1 && m_out % BM2 == 0) {
     const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
     HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem2));
@@ -1170,7 +1374,7 @@ HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
   if (option == 0) g_wgrad_transposed = value != 0;
   if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
   if (option == 2) g_gemm_pair = value != 0;
-  if (option == 3) g_wgrad_pair = value != 0;
+  if (option == 3) g_wgrad_pair = value < 0 ? 0 : (value > 2 ? 2 : value);
   return 0;
 }
 

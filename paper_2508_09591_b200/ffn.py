@@ -72,9 +72,11 @@ def set_gemm_pair(enabled: bool) -> None:
     _lib.call("hm_ffn_set_option", 2, int(bool(enabled)))
 
 
-def set_wgrad_pair(enabled: bool) -> None:
-    """Weight-gradient GEMMs on CTA pairs (256 x 256 output tiles)."""
-    _lib.call("hm_ffn_set_option", 3, int(bool(enabled)))
+def set_wgrad_pair(mode: int | bool) -> None:
+    """Weight-gradient GEMMs: 0/False single-CTA, 1/True CTA pairs with a
+    per-stage hand-off of the zeroed tail, 2 CTA pairs with per-group tensor
+    maps (TMA zero-fills the tail)."""
+    _lib.call("hm_ffn_set_option", 3, int(mode))
 
 
 def set_gemm_ctas(n: int) -> None:

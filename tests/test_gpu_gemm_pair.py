@@ -69,9 +69,9 @@ def test_pair_swiglu_ffn_equals_single(hm, pair):
 
 @pytest.mark.parametrize("shape", [(4, 2048, 768, [1000, 63, 0, 2049]), (3, 512, 256, [130, 0, 301])])
 def test_wgrad_pair_equals_single(hm, shape):
-    """Weight gradients from the CTA-pair MN-major GEMM equal the single-CTA
-    ones bit for bit (rows past the last group hold NaN: the tail zeroing
-    must keep them out)."""
+    """Weight gradients from both CTA-pair MN-major GEMMs equal the single-CTA
+    ones bit for bit (rows past the last group hold NaN: the tail zeroing /
+    the per-group maps' zero fill must keep them out)."""
     from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
                                            expert_ffn_save_ptrs, set_wgrad_pair)
     G, M, I, n_rows = shape
@@ -93,7 +93,7 @@ def test_wgrad_pair_equals_single(hm, shape):
                          g13.data_ptr())
     res = []
     try:
-        for on in (False, True):
+        for on in (0, 1, 2):   # single CTA, pair with hand-off, pair with per-group maps
             set_wgrad_pair(on)
             sc = FFNBackwardScratch(cap, G, M, I)
             gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
@@ -106,6 +106,7 @@ def test_wgrad_pair_equals_single(hm, shape):
             res.append((dw13.clone(), dw2.clone()))
     finally:
         set_wgrad_pair(False)
-    assert not torch.isnan(res[1][0]).any() and not torch.isnan(res[1][1]).any()
-    assert torch.equal(res[0][0], res[1][0])
-    assert torch.equal(res[0][1], res[1][1])
+    for other in res[1:]:
+        assert not torch.isnan(other[0]).any() and not torch.isnan(other[1]).any()
+        assert torch.equal(res[0][0], other[0])
+        assert torch.equal(res[0][1], other[1])
