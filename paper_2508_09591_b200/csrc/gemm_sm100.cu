@@ -588,11 +588,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0, row = 0;
     tm.ntile_n = args.N / BN;
     for (int g = 0; g < args.groups; ++g) {
-      const int n = args.n_rows[g];
+      int n = args.n_rows[g];
+      if (kMode == 2) n = (n + BK - 1) / BK * BK;   // K padded to the k-block
       tm.start[g] = acc;
       tm.row0[g] = row;
       tm.rows[g] = n;
-      acc += (n + BM2 - 1) / BM2 * tm.ntile_n;
+      acc += (kMode == 2 ? args.m_out / BM2 : (n + BM2 - 1) / BM2) * tm.ntile_n;
       row += n;
     }
     tm.start[args.groups] = acc;
@@ -618,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int kblocks = args.K / BK;
+  const int kblocks_fixed = args.K / BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -629,13 +630,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int t = cid; t < tm.total; t += ncl) {
         int g, mt, nt;
         tile_coords(tm, args.groups, t, g, mt, nt);
-        const int arow = tm.row0[g] + mt * BM2 + (int)rank * 128;
-        const int brow = g * args.N + nt * BN + (int)rank * 128;
+        // mode 2 (weight gradient from transposed operands): A [m_out][K_all],
+        // B [N][K_all], group g's reduction range = its padded token columns
+        const int arow = (kMode == 2 ? 0 : tm.row0[g]) + mt * BM2 + (int)rank * 128;
+        const int brow = (kMode == 2 ? 0 : g * args.N) + nt * BN + (int)rank * 128;
+        const int k0 = kMode == 2 ? tm.row0[g] : 0;
+        const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           if (leader) mbar_expect_tx(full + stage, 2 * kStageBytes2);
-          tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, kb * BK, arow);
-          tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, kb * BK, brow);
+          tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
+          tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, k0 + kb * BK, brow);
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
@@ -654,6 +659,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
+        int kblocks = kblocks_fixed;
+        if (kMode == 2) {
+          int g, mt, nt;
+          tile_coords(tm, args.groups, t, g, mt, nt);
+          kblocks = tm.rows[g] / BK;
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
@@ -1340,6 +1351,17 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       k_grouped_gemm_pair<0><<<grid, kThreads, smem2, s>>>(ma, mb2, args);
     }
+    HM_LAUNCHED();
+    return 0;
+  }
+  if (wgrad_m_out && g_gemm_pair && wgrad_m_out % BM2 == 0) {
+    CUtensorMap mb2;
+    st = make_map(&mb2, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, 128);
+    if (st) return st;
+    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
+    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    k_grouped_gemm_pair<2><<<sms & ~1, kThreads, smem2, s>>>(ma, mb2, args);
     HM_LAUNCHED();
     return 0;
   }

@@ -136,7 +136,22 @@ def test_wgrad_paths_agree(hm):
                                  gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2)
         torch.cuda.synchronize()
         outs.append((dw13.float(), dw2.float()))
-    set_wgrad_transposed(False)
+    # the transposed path on single CTAs: the CTA-pair kernel gives the same bits
+    from paper_2508_09591_b200.ffn import set_gemm_pair
+    set_wgrad_transposed(True)
+    set_gemm_pair(False)
+    try:
+        sc = FFNBackwardScratch(cap, G, M, I)
+        gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+        dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
+        dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
+        expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t,
+                                 gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2)
+        torch.cuda.synchronize()
+        assert torch.equal(dw13.float(), outs[0][0]) and torch.equal(dw2.float(), outs[0][1])
+    finally:
+        set_gemm_pair(True)
+        set_wgrad_transposed(False)
     for a, b in zip(outs[0], outs[1]):
         torch.testing.assert_close(b, a, rtol=1e-2, atol=1e-2 * a.abs().max().item())
     assert torch.count_nonzero(outs[1][0][2]) == 0 and torch.count_nonzero(outs[1][1][2]) == 0
