@@ -714,8 +714,7 @@ def main():
                 flush.zero_()
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
                 ev[0].record()
-                slot_l, w_l, ex_l = layer.route(x)
-                layer._saved = (x, slot_l, w_l, ex_l)
+                slot_l, w_l, ex_l = layer.route_saved(x)
                 layer.world.dispatch(x, slot_l, w_l, dedup=layer.dedup)
                 ev[1].record()
                 layer.experts_forward()

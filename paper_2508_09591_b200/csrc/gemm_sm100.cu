@@ -49,6 +49,9 @@ int g_gemm_pair = 1;
 // but measured 2x slower (DSv3 dW13 4.22 vs 2.32 ms in ncu: the per-stage
 // ready hand-off between the two CTAs serialises the pipeline), so off
 int g_wgrad_pair = 0;
+// hm_ffn_set_option(4, 1): the SwiGLU backward with 4-byte accesses (the
+// 16-byte k_swiglu_bwd_v8 is the default; bit-identical)
+int g_swiglu_scalar = 0;
 
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
@@ -1182,6 +1185,50 @@ __global__ void k_swiglu_bwd(const __nv_bfloat16* __restrict__ g13, const __nv_b
   }
 }
 
+// The same SwiGLU backward with 16-byte accesses: eight columns of one
+// 128-column block per thread (inter % 128 == 0), identical per-element math.
+__global__ void __launch_bounds__(256) k_swiglu_bwd_v8(const __nv_bfloat16* __restrict__ g13,
+                                                       const __nv_bfloat16* __restrict__ dh,
+                                                       const int32_t* __restrict__ row0, int groups,
+                                                       int inter, __nv_bfloat16* __restrict__ dg13,
+                                                       __nv_bfloat16* __restrict__ h) {
+  const int rows = row0[groups];
+  const int per_row = inter / 8;
+  const int64_t n = (int64_t)rows * per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / per_row);
+    const int j = 8 * (int)(i - (int64_t)r * per_row);
+    const int b = j >> 7, c = j & 127;
+    const int64_t ga = (int64_t)r * 2 * inter + 256 * b + c, gu = ga + 128;
+    const int4 av = __ldg(reinterpret_cast<const int4*>(g13 + ga));
+    const int4 uv = __ldg(reinterpret_cast<const int4*>(g13 + gu));
+    const int4 dv = __ldg(reinterpret_cast<const int4*>(dh + (int64_t)r * inter + j));
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+    const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+    int4 hv, dav, duv;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&hv);
+    __nv_bfloat162* da2 = reinterpret_cast<__nv_bfloat162*>(&dav);
+    __nv_bfloat162* du2 = reinterpret_cast<__nv_bfloat162*>(&duv);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 a = __bfloat1622float2(a2[q]);
+      const float2 u = __bfloat1622float2(u2[q]);
+      const float2 d = __bfloat1622float2(d2[q]);
+      const float s0 = 1.f / (1.f + __expf(-a.x)), s1 = 1.f / (1.f + __expf(-a.y));
+      const float si0 = a.x * s0, si1 = a.y * s1;
+      h2[q] = __floats2bfloat162_rn(si0 * u.x, si1 * u.y);
+      du2[q] = __floats2bfloat162_rn(d.x * si0, d.y * si1);
+      da2[q] = __floats2bfloat162_rn(d.x * u.x * s0 * (1.f + a.x * (1.f - s0)),
+                                     d.y * u.y * s1 * (1.f + a.y * (1.f - s1)));
+    }
+    *reinterpret_cast<int4*>(h + (int64_t)r * inter + j) = hv;
+    *reinterpret_cast<int4*>(dg13 + gu) = duv;
+    *reinterpret_cast<int4*>(dg13 + ga) = dav;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host: tensor maps through the driver entry point (no -lcuda link needed)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1390,13 +1437,15 @@ int g_wgrad_transposed = 0;   // hm_ffn_set_option(0, 1): transposes + K-major w
 // token-major activations directly, default; 1: transposed copies + K-major);
 // 1 = cap on the persistent GEMM grid (CTAs; 0 = one per SM, default) so
 // concurrent exchange kernels keep SMs of their own; 2 = CTA-pair
-// (cta_group::2, 256 x 256 tiles) kernels for the forward / data-gradient GEMMs
+// (cta_group::2, 256 x 256 tiles) kernels for the forward / data-gradient GEMMs;
+// 3 = weight-gradient pair kernels (0 off, 1 / 2 variants); 4 = scalar SwiGLU backward
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option >= 0 && option <= 3, "hm_ffn_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 4, "hm_ffn_set_option: unknown option %d", option);
   if (option == 0) g_wgrad_transposed = value != 0;
   if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
   if (option == 2) g_gemm_pair = value != 0;
   if (option == 3) g_wgrad_pair = value < 0 ? 0 : (value > 2 ? 2 : value);
+  if (option == 4) g_swiglu_scalar = value != 0;
   return 0;
 }
 
@@ -1509,8 +1558,14 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
   int32_t* col0 = layout + groups + 1;
   k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, row0, col0);
   HM_LAUNCHED();
-  k_swiglu_bwd<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh, row0,
-                                         groups, I, (__nv_bfloat16*)dg13, (__nv_bfloat16*)h);
+  if (I % 128 == 0 && !g_swiglu_scalar)
+    k_swiglu_bwd_v8<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
+                                              row0, groups, I, (__nv_bfloat16*)dg13,
+                                              (__nv_bfloat16*)h);
+  else
+    k_swiglu_bwd<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
+                                           row0, groups, I, (__nv_bfloat16*)dg13,
+                                           (__nv_bfloat16*)h);
   HM_LAUNCHED();
   // data gradient
   if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s))) return st;

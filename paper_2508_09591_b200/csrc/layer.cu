@@ -2176,6 +2176,91 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
   }
 }
 
+// Combine backward when every pick is direct (mode 0, or per-GPU dedup on one
+// GPU): warp per token, lane k holds pick k's gy / y row pointers and weight
+// (broadcast by shuffle, so no per-thread pointer arrays in local memory), the
+// gradient row is staged kGradU 16-B vectors per lane at a time and each
+// pick's y vectors are all loaded before its first store.  Same per-lane
+// accumulation order as k_pack_grad, so gy and the gate grads are bit-identical.
+constexpr int kGradU = 8;
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_grad_direct(const WorldDev* __restrict__ wp,
+                                                          const uint8_t* __restrict__ g,
+                                                          const int32_t* __restrict__ ids,
+                                                          const float* __restrict__ wts,
+                                                          const int32_t* __restrict__ epos,
+                                                          float* __restrict__ dw) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  const int64_t ntok = (int64_t)w.L * w.T_r;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = warp; t < ntok; t += nw) {
+    const int4* yl = nullptr;
+    int4* dl = nullptr;
+    float wl = 0.f;
+    if (lane < w.K) {
+      const int e = ids[t * w.K + lane], ep = epos[t * w.K + lane];
+      if (e >= 0 && ep >= 0) {
+        const int d = rank_of_slot(w, e);
+        yl = reinterpret_cast<const int4*>(w.ymaj[d] + (int64_t)ep * w.row_bytes);
+        dl = reinterpret_cast<int4*>(w.gy[d] + (int64_t)ep * w.row_bytes);
+        wl = wts[t * w.K + lane];
+      }
+    }
+    float dot[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) dot[j] = 0.f;
+    const int4* src = reinterpret_cast<const int4*>(g + t * w.row_bytes);
+    for (int64_t base = 0; base < nvec; base += 32 * kGradU) {
+      int4 gv[kGradU];
+#pragma unroll
+      for (int u = 0; u < kGradU; ++u) {
+        const int64_t v = base + u * 32 + lane;
+        if (v < nvec) gv[u] = ld_nc_v4(src + v);
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) {
+        if (j >= w.K) break;
+        const int4* yr = reinterpret_cast<const int4*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(yl), j));
+        int4* dr = reinterpret_cast<int4*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dl), j));
+        const float wk = __shfl_sync(0xffffffffu, wl, j);
+        if (!yr) continue;
+        int4 yv[kGradU];
+#pragma unroll
+        for (int u = 0; u < kGradU; ++u) {
+          const int64_t v = base + u * 32 + lane;
+          if (v < nvec) yv[u] = ld_nc_v4(yr + v);
+        }
+#pragma unroll
+        for (int u = 0; u < kGradU; ++u) {
+          const int64_t v = base + u * 32 + lane;
+          if (v >= nvec) break;
+          float gf[Vec<T>::N], yf[Vec<T>::N], sf[Vec<T>::N];
+          Vec<T>::to_f32(gv[u], gf);
+          Vec<T>::to_f32(yv[u], yf);
+#pragma unroll
+          for (int q = 0; q < Vec<T>::N; ++q) {
+            dot[j] = fmaf(gf[q], yf[q], dot[j]);
+            sf[q] = wk * gf[q];
+          }
+          st_na_v4(dr + v, Vec<T>::from_f32(sf));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j >= w.K) break;
+      float x = dot[j];
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == j && yl) dw[t * w.K + j] = x;
+    }
+  }
+}
+
 // destination: received gradient row -> scaled rows for each local pick, and
 // the pick's gate gradient <g, y_k> into gw[row][k]
 template <typename T>
@@ -3035,7 +3120,16 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
   const WorldDev& h = w->h;
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
-  if (h.elem == 2)
+  if ((mode == 0 || (mode == 2 && h.P == 1)) && w->lean_pack) {
+    // every pick direct: one token per warp, up to 32 CTAs per SM
+    blocks = grid_for(T, 8, w->max_blocks > 0 ? w->max_blocks : kSMs * 32);
+    if (h.elem == 2)
+      k_pack_grad_direct<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts,
+                                                               w->epos, dw);
+    else
+      k_pack_grad_direct<float><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->epos,
+                                                       dw);
+  } else if (h.elem == 2)
     k_pack_grad<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->hitmask,
                                                       w->gpos, w->epos, mode, dw);
   else

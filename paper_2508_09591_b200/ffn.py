@@ -79,6 +79,12 @@ def set_wgrad_pair(mode: int | bool) -> None:
     _lib.call("hm_ffn_set_option", 3, int(mode))
 
 
+def set_swiglu_scalar(enabled: bool) -> None:
+    """SwiGLU backward with 4-byte accesses (True) or the 16-byte kernel
+    (False, default); bit-identical."""
+    _lib.call("hm_ffn_set_option", 4, int(bool(enabled)))
+
+
 def set_gemm_ctas(n: int) -> None:
     """Cap the persistent grouped-GEMM grid at n CTAs (0: one per SM)."""
     _lib.call("hm_ffn_set_option", 1, int(n))

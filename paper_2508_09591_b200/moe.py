@@ -184,13 +184,33 @@ class HierMoELayer:
         if self.grad:
             self.refresh_transposed_weights()
 
-    def route(self, x: torch.Tensor):
+    def route(self, x: torch.Tensor, xf: torch.Tensor | None = None,
+              logits: torch.Tensor | None = None):
+        """Router logits (fp32 GEMM on the fp32 copy ``xf`` of x) -> top-K picks.
+        ``logits``, if given, receives the logits (kept for the backward)."""
+        if xf is None:
+            xf = x.float()
         with _tf32():
-            logits = x.float() @ self.w_router.T
+            if logits is None:
+                logits = xf @ self.w_router.T
+            else:
+                torch.mm(xf, self.w_router.T, out=logits)
         if self.router == "dsv3":
             return route_group_limited(logits, self.top_k, self.n_group, self.topk_group,
                                        self.score_bias, self.route_scale, self.expert_to_slot)
         return route_topk(logits, self.top_k, self.expert_to_slot, self.renormalize)
+
+    def route_saved(self, x: torch.Tensor):
+        """The forward's routing step: route x and, for a training layer, keep
+        what the backward needs (x, its fp32 copy and the router logits are
+        reused by the router backward)."""
+        if not self.grad:
+            return self.route(x)
+        xf = x.float()
+        logits = torch.empty(x.shape[0], self.experts, device="cuda")
+        slot, w, ex = self.route(x, xf, logits)
+        self._saved = (x, xf, logits, slot, w, ex)
+        return slot, w, ex
 
     def shared_forward(self, x: torch.Tensor) -> torch.Tensor:
         """The shared expert on every local token (one-group tcgen05 FFN)."""
@@ -228,9 +248,7 @@ class HierMoELayer:
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         x = x.contiguous()
-        slot, w, ex = self.route(x)
-        if self.grad:
-            self._saved = (x, slot, w, ex)
+        slot, w, ex = self.route_saved(x)
         if self._trace is not None:
             self._trace.append((self.iteration, ex.clone()))
         self.iteration += 1
@@ -301,7 +319,7 @@ class HierMoELayer:
         """
         if not self.grad or self._saved is None:
             raise RuntimeError("HierMoELayer.backward needs grad=True and a forward first")
-        x, slot, w, ex = self._saved
+        x, xf, logits, slot, w, ex = self._saved
         g = grad_out.contiguous()
         if self.shared_inter:   # shared expert backward beside the routed one
             cur = torch.cuda.current_stream()
@@ -348,8 +366,6 @@ class HierMoELayer:
             cur.wait_stream(st)
         if self.router == "dsv3":
             # w_k = c s_k / S, s = sigmoid(logit); the bias only steers selection
-            with _tf32():
-                logits = x.float() @ self.w_router.T
             sk = torch.sigmoid(torch.gather(logits, 1, ex.long()))
             c = self.route_scale
             ds = (c / sk.sum(dim=1, keepdim=True)) * (dw - (dw * w).sum(dim=1, keepdim=True) / c)
@@ -360,17 +376,19 @@ class HierMoELayer:
             dlogits = torch.zeros(x.shape[0], self.experts, device="cuda")
             dlogits.scatter_(1, ex.long(), dsel)
         else:                    # softmax over all experts
-            logits = x.float() @ self.w_router.T
             p = torch.softmax(logits, dim=1)
             dp = torch.zeros_like(p).scatter_(1, ex.long(), dw)
             dlogits = p * (dp - (p * dp).sum(dim=1, keepdim=True))
         with _tf32():
-            self.dw_router += dlogits.T @ x.float()
-            dxf = torch.addmm(dx.float(), dlogits, self.w_router)
+            self.dw_router += dlogits.T @ xf
+            dxf = dlogits @ self.w_router
         if self.shared_inter:
+            dxf += dx
             torch.cuda.current_stream().wait_event(self._shared_done)
-            dxf += self._shared_dx.float()
-        return dxf.to(x.dtype)
+            dxf += self._shared_dx
+            return dxf.to(x.dtype)
+        # fp32 sum rounded once into the bf16 result (no fp32 copy of dx)
+        return torch.add(dxf, dx, out=torch.empty_like(dx))
 
     # --- routing traces and placements in the reference's file formats ---
     def record_trace(self, enabled: bool = True) -> None:

@@ -110,3 +110,45 @@ def test_wgrad_pair_equals_single(hm, shape):
         assert not torch.isnan(other[0]).any() and not torch.isnan(other[1]).any()
         assert torch.equal(res[0][0], other[0])
         assert torch.equal(res[0][1], other[1])
+
+
+@pytest.mark.parametrize("shape", [(4, 2048, 768, [1000, 63, 0, 2049]), (3, 512, 256, [130, 0, 301])])
+def test_swiglu_bwd_vector_equals_scalar(hm, shape):
+    """The 16-byte SwiGLU backward (default) and the 4-byte one give the same
+    data and weight gradients bit for bit."""
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
+                                           expert_ffn_save_ptrs, set_swiglu_scalar)
+    G, M, I, n_rows = shape
+    torch.manual_seed(11)
+    rows = sum(n_rows)
+    cap = rows + 100
+    x = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+    x[:rows] = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    gy = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+    gy[:rows] = torch.randn(rows, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    w13t, w2t = w13.transpose(1, 2).contiguous(), w2.transpose(1, 2).contiguous()
+    nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
+    h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
+    g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
+    expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y.data_ptr(),
+                         g13.data_ptr())
+    res = []
+    try:
+        for scalar in (True, False):
+            set_swiglu_scalar(scalar)
+            sc = FFNBackwardScratch(cap, G, M, I)
+            gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
+            dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
+            dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
+            expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t,
+                                     gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2,
+                                     g13.data_ptr())
+            torch.cuda.synchronize()
+            res.append((gx[:rows].clone(), dw13.clone(), dw2.clone()))
+    finally:
+        set_swiglu_scalar(False)
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
