@@ -190,6 +190,15 @@ int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup,
  * counterpart. */
 int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int32_t mode,
                    const void* addend, void* out, void* stream);
+/* bf16 -> fp32 widening of n elements (16-byte aligned buffers): the fp32
+ * operand of the router logits GEMM (the step before the
+ * path); no reference counterpart. */
+int hm_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream);
+/* out = bf16((a + b) + c), fp32 sums, c may be NULL (b, c, out bf16; 16-byte
+ * aligned): the layer's input gradient, router-GEMM term + routed dx (+ the
+ * shared expert's dx), rounded once; no reference counterpart. */
+int hm_sum_to_bf16(const float* a, const void* b, const void* c, void* out, int64_t n,
+                   void* stream);
 /* Backward (world created with flags & 1).  hm_dispatch_grad = combine
  * backward: output grads -> expert-output grads (dedup broadcast, replaying the
  * forward plan) + direct picks' gate grads; hm_combine_grad = dispatch

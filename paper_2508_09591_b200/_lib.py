@@ -76,6 +76,8 @@ _SIGS = {
     "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                    c_void_p]),
     "hm_combine_grad": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "hm_bf16_to_f32": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "hm_sum_to_bf16": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "hm_combine_add": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
                                  c_void_p]),

@@ -3000,6 +3000,81 @@ HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t
 
 // combine + an addend row per token (e.g. the shared expert's output), summed
 // in fp32 after the routed rows: out = sum_k w_k y_k + addend
+// bf16 -> fp32 widening with 16-byte loads and stores (the router GEMM's
+// fp32 operand; torch's casting copy runs at ~2.3 TB/s on B200)
+__global__ void __launch_bounds__(256) k_bf16_to_f32(const __nv_bfloat16* __restrict__ src,
+                                                     float* __restrict__ dst, int64_t n) {
+  const int64_t nv = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const int4 v = ld_nc_v4(reinterpret_cast<const int4*>(src) + i);
+    float f[8];
+    Vec<__nv_bfloat16>::to_f32(v, f);
+    float4* d = reinterpret_cast<float4*>(dst) + 2 * i;
+    d[0] = make_float4(f[0], f[1], f[2], f[3]);
+    d[1] = make_float4(f[4], f[5], f[6], f[7]);
+  }
+  for (int64_t i = nv * 8 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = __bfloat162float(src[i]);
+}
+
+HM_API int hm_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream) {
+  HM_CHECK_ARG(n >= 0 && (n == 0 || (src && dst)), "hm_bf16_to_f32: null argument");
+  HM_CHECK_ARG(((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0,
+               "hm_bf16_to_f32: buffers must be 16-byte aligned");
+  if (n == 0) return 0;
+  const int64_t want = (n / 8 + 255) / 256;
+  const int blocks = (int)(want < 1 ? 1 : (want > kSMs * 16 ? kSMs * 16 : want));
+  k_bf16_to_f32<<<blocks, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)src, dst, n);
+  HM_LAUNCHED();
+  return 0;
+}
+
+// out = bf16((a + b) + c) with fp32 sums (c optional): the router backward's
+// input gradient (router-GEMM term + routed-path dx + shared-expert dx)
+// rounded once, 16-byte accesses
+__global__ void __launch_bounds__(256) k_sum_to_bf16(const float* __restrict__ a,
+                                                     const __nv_bfloat16* __restrict__ b,
+                                                     const __nv_bfloat16* __restrict__ c,
+                                                     __nv_bfloat16* __restrict__ out, int64_t n) {
+  const int64_t nv = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const float4 a0 = __ldg(reinterpret_cast<const float4*>(a) + 2 * i);
+    const float4 a1 = __ldg(reinterpret_cast<const float4*>(a) + 2 * i + 1);
+    float f[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    float fb[8];
+    Vec<__nv_bfloat16>::to_f32(ld_nc_v4(reinterpret_cast<const int4*>(b) + i), fb);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) f[q] += fb[q];
+    if (c) {
+      Vec<__nv_bfloat16>::to_f32(ld_nc_v4(reinterpret_cast<const int4*>(c) + i), fb);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) f[q] += fb[q];
+    }
+    reinterpret_cast<int4*>(out)[i] = Vec<__nv_bfloat16>::from_f32(f);
+  }
+  for (int64_t i = nv * 8 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float v = a[i] + __bfloat162float(b[i]);
+    if (c) v += __bfloat162float(c[i]);
+    out[i] = __float2bfloat16(v);
+  }
+}
+
+HM_API int hm_sum_to_bf16(const float* a, const void* b, const void* c, void* out, int64_t n,
+                          void* stream) {
+  HM_CHECK_ARG(n >= 0 && (n == 0 || (a && b && out)), "hm_sum_to_bf16: null argument");
+  HM_CHECK_ARG((((uintptr_t)a | (uintptr_t)b | (uintptr_t)c | (uintptr_t)out) & 15) == 0,
+               "hm_sum_to_bf16: buffers must be 16-byte aligned");
+  if (n == 0) return 0;
+  const int64_t want = (n / 8 + 255) / 256;
+  const int blocks = (int)(want < 1 ? 1 : (want > kSMs * 16 ? kSMs * 16 : want));
+  k_sum_to_bf16<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      a, (const __nv_bfloat16*)b, (const __nv_bfloat16*)c, (__nv_bfloat16*)out, n);
+  HM_LAUNCHED();
+  return 0;
+}
+
 HM_API int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int32_t mode,
                           const void* addend, void* out, void* stream) {
   HM_CHECK_ARG(addend, "hm_combine_add: null addend");

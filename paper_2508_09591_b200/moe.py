@@ -15,6 +15,8 @@ import torch
 
 from .ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs,
                   expert_ffn_save_ptrs, pack_w13)
+from . import _lib
+from ._lib import ptr, stream_ptr
 from .layer import EPWorld, route_group_limited, route_topk
 from .migrate import ExpertStore
 from .routing import Placement, RoutingMask, load_placements, save_placements, save_trace
@@ -184,12 +186,23 @@ class HierMoELayer:
         if self.grad:
             self.refresh_transposed_weights()
 
+    @staticmethod
+    def widen(x: torch.Tensor) -> torch.Tensor:
+        """fp32 copy of the activations for the router GEMM (16-byte
+        vectorised kernel for bf16, ``hm_bf16_to_f32``)."""
+        if x.dtype != torch.bfloat16:
+            return x.float()
+        x = x.contiguous()
+        xf = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+        _lib.call("hm_bf16_to_f32", ptr(x), ptr(xf), x.numel(), stream_ptr())
+        return xf
+
     def route(self, x: torch.Tensor, xf: torch.Tensor | None = None,
               logits: torch.Tensor | None = None):
         """Router logits (fp32 GEMM on the fp32 copy ``xf`` of x) -> top-K picks.
         ``logits``, if given, receives the logits (kept for the backward)."""
         if xf is None:
-            xf = x.float()
+            xf = self.widen(x)
         with _tf32():
             if logits is None:
                 logits = xf @ self.w_router.T
@@ -206,7 +219,7 @@ class HierMoELayer:
         reused by the router backward)."""
         if not self.grad:
             return self.route(x)
-        xf = x.float()
+        xf = self.widen(x)
         logits = torch.empty(x.shape[0], self.experts, device="cuda")
         slot, w, ex = self.route(x, xf, logits)
         self._saved = (x, xf, logits, slot, w, ex)
@@ -382,13 +395,18 @@ class HierMoELayer:
         with _tf32():
             self.dw_router += dlogits.T @ xf
             dxf = dlogits @ self.w_router
+        shared_dx = None
         if self.shared_inter:
-            dxf += dx
             torch.cuda.current_stream().wait_event(self._shared_done)
-            dxf += self._shared_dx
-            return dxf.to(x.dtype)
-        # fp32 sum rounded once into the bf16 result (no fp32 copy of dx)
-        return torch.add(dxf, dx, out=torch.empty_like(dx))
+            shared_dx = self._shared_dx
+        if dx.dtype != torch.bfloat16:
+            out = dxf + dx
+            return out if shared_dx is None else out + shared_dx
+        # ((router term + dx) + shared dx) in fp32, rounded once to bf16
+        out = torch.empty_like(dx)
+        _lib.call("hm_sum_to_bf16", ptr(dxf), ptr(dx), ptr(shared_dx), ptr(out), dx.numel(),
+                  stream_ptr())
+        return out
 
     # --- routing traces and placements in the reference's file formats ---
     def record_trace(self, enabled: bool = True) -> None:

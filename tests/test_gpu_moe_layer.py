@@ -140,3 +140,32 @@ def test_layer_dsv3_router_shared_expert(hm, dedup):
     np.testing.assert_allclose(out.double().cpu().numpy(), ref, rtol=2e-2,
                                atol=2e-2 * np.abs(ref).max())
     layer.close()
+
+
+@pytest.mark.parametrize("shape", [(4096, 2048), (3, 7), (1, 8), (0, 16)])
+def test_widen_equals_float(shape):
+    """hm_bf16_to_f32 (the router GEMM's fp32 operand) equals torch's cast bit
+    for bit, including ragged tails and empty input."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    x = (torch.randn(shape, device="cuda") * 100).to(torch.bfloat16)
+    xf = HierMoELayer.widen(x)
+    torch.cuda.synchronize()
+    assert xf.dtype == torch.float32 and torch.equal(xf, x.float())
+
+
+@pytest.mark.parametrize("n", [4096 * 2048, 13, 8, 0])
+@pytest.mark.parametrize("third", [False, True])
+def test_sum_to_bf16(n, third):
+    """hm_sum_to_bf16 = bf16((a + b) + c) with fp32 sums, bit for bit."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200._lib import ptr, stream_ptr
+    a = torch.randn(n, device="cuda") * 3
+    b = torch.randn(n, device="cuda").to(torch.bfloat16)
+    c = torch.randn(n, device="cuda").to(torch.bfloat16) if third else None
+    out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    _lib.call("hm_sum_to_bf16", ptr(a), ptr(b), ptr(c), ptr(out), n, stream_ptr())
+    want = a + b.float()
+    if third:
+        want = want + c.float()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want.to(torch.bfloat16))
