@@ -3006,13 +3006,22 @@ __global__ void __launch_bounds__(256) k_bf16_to_f32(const __nv_bfloat16* __rest
                                                      float* __restrict__ dst, int64_t n) {
   const int64_t nv = n / 8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-    const int4 v = ld_nc_v4(reinterpret_cast<const int4*>(src) + i);
-    float f[8];
-    Vec<__nv_bfloat16>::to_f32(v, f);
-    float4* d = reinterpret_cast<float4*>(dst) + 2 * i;
-    d[0] = make_float4(f[0], f[1], f[2], f[3]);
-    d[1] = make_float4(f[4], f[5], f[6], f[7]);
+  // four independent 16-byte loads in flight per thread
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += 4 * stride) {
+    int4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * stride < nv) v[u] = ld_nc_v4(reinterpret_cast<const int4*>(src) + i0 + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nv) break;
+      float f[8];
+      Vec<__nv_bfloat16>::to_f32(v[u], f);
+      float4* d = reinterpret_cast<float4*>(dst) + 2 * i;
+      d[0] = make_float4(f[0], f[1], f[2], f[3]);
+      d[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
   }
   for (int64_t i = nv * 8 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     dst[i] = __bfloat162float(src[i]);
@@ -3039,20 +3048,35 @@ __global__ void __launch_bounds__(256) k_sum_to_bf16(const float* __restrict__ a
                                                      __nv_bfloat16* __restrict__ out, int64_t n) {
   const int64_t nv = n / 8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-    const float4 a0 = __ldg(reinterpret_cast<const float4*>(a) + 2 * i);
-    const float4 a1 = __ldg(reinterpret_cast<const float4*>(a) + 2 * i + 1);
-    float f[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    float fb[8];
-    Vec<__nv_bfloat16>::to_f32(ld_nc_v4(reinterpret_cast<const int4*>(b) + i), fb);
+  // two elements-of-8 per thread per iteration, all loads issued first
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += 2 * stride) {
+    float4 a0[2], a1[2];
+    int4 bv[2], cv[2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) f[q] += fb[q];
-    if (c) {
-      Vec<__nv_bfloat16>::to_f32(ld_nc_v4(reinterpret_cast<const int4*>(c) + i), fb);
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nv) break;
+      a0[u] = __ldg(reinterpret_cast<const float4*>(a) + 2 * i);
+      a1[u] = __ldg(reinterpret_cast<const float4*>(a) + 2 * i + 1);
+      bv[u] = ld_nc_v4(reinterpret_cast<const int4*>(b) + i);
+      if (c) cv[u] = ld_nc_v4(reinterpret_cast<const int4*>(c) + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nv) break;
+      float f[8] = {a0[u].x, a0[u].y, a0[u].z, a0[u].w, a1[u].x, a1[u].y, a1[u].z, a1[u].w};
+      float fb[8];
+      Vec<__nv_bfloat16>::to_f32(bv[u], fb);
 #pragma unroll
       for (int q = 0; q < 8; ++q) f[q] += fb[q];
+      if (c) {
+        Vec<__nv_bfloat16>::to_f32(cv[u], fb);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] += fb[q];
+      }
+      reinterpret_cast<int4*>(out)[i] = Vec<__nv_bfloat16>::from_f32(f);
     }
-    reinterpret_cast<int4*>(out)[i] = Vec<__nv_bfloat16>::from_f32(f);
   }
   for (int64_t i = nv * 8 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float v = a[i] + __bfloat162float(b[i]);
