@@ -447,6 +447,9 @@ def main():
 
     # per-kernel timing (CUDA events recorded by the library on the launch stream)
     def seg_times(w_, dedup):
+        # one untimed step first: a variant's kernels load lazily on their first launch
+        step(w_, dedup, out)
+        torch.cuda.synchronize()
         _lib.call("hm_world_set_timing", w_._h, 1)
         acc = np.zeros(len(SEGMENTS))
         n = 5
