@@ -280,12 +280,12 @@ def _bind_gpu_local_cpus(dev: int):
         cpus = [w * 64 + b for w, m in enumerate(mask) for b in range(64) if (m >> b) & 1]
         cpus = [c for c in cpus if c in os.sched_getaffinity(0)]
         if not cpus:
-            return None, None
+            return f"unbound: {len(os.sched_getaffinity(0))} cpus (no NVML affinity)", None
         old = os.sched_getaffinity(0)
         os.sched_setaffinity(0, cpus)
         return f"{len(cpus)} cpus {cpus[0]}-{cpus[-1]}", old
     except Exception:   # noqa: BLE001 -- affinity is an optimisation only
-        return None, None
+        return f"unbound: {len(os.sched_getaffinity(0))} cpus (no NVML affinity)", None
 
 
 def main():
