@@ -200,43 +200,41 @@ def dedup_combine(plan: DispatchPlan, weights, y_expert_major, payload_round=Non
     return out
 
 
-def cpu_dispatch_combine(x, ids, weights, ranks: int, experts: int, y_major=None, threads: int = 1):
-    """Vectorised CPU port of one dedup dispatch + combine step (the timed
+def cpu_dispatch_combine(logits, x, top_k: int, y_major=None, threads: int = 1,
+                         chunk: int = 256):
+    """torch-CPU port of one dispatch + combine step at full size (the timed
     CPU baseline; TEST/BENCH INFRASTRUCTURE ONLY).
 
-    Performs the same data movement as the GPU step on host memory: per
-    destination gather of the dedup rows, re-expansion into expert-major rows,
-    gate-weighted pre-reduce per (token, destination) and the source-side sum
-    over destinations.  ``y_major[d]`` are the destination's expert outputs
-    (defaults to the expert-major inputs, i.e. identity experts).  Returns
-    (out [T, M], y_major, plan).
+    The same step the GPU times at N = 1, on host memory with ``threads``
+    intra-op threads: softmax top-K gating (``torch.topk`` on the logits),
+    the dispatch plan (stable sort of the picks by slot = the expert-major
+    row order, source-major within a slot), the dispatch itself (one
+    ``index_select`` of the token rows into expert-major order) and the
+    combine (``index_select`` back to (token, pick) order and a gate-weighted
+    fp32 sum per token, chunked so the fp32 temporaries stay in cache).  On
+    one host every EP rank is local, so -- as on one GPU -- no dedup rows are
+    exchanged.  ``x`` is bf16 (the GPU's storage format); ``y_major`` are the
+    expert outputs in expert-major order (default: identity experts).
+    Returns (out [T, M] bf16, y_major, order).
     """
-    from concurrent.futures import ThreadPoolExecutor
-
-    plan = DispatchPlan(ids, ranks, experts)
-    e_loc = experts // ranks
-    t, k = plan.ids.shape
-    w = np.asarray(weights, dtype=x.dtype)
-
-    def dest_step(d):
-        rows = plan.recv_rows(d)                       # arrival order (global token order)
-        recv = x[rows]                                 # pack + exchange
-        local = (plan.ids[rows] // e_loc) == d         # [R, K] picks on d
-        rr, kk = np.nonzero(local)
-        n = int(plan.n_e[d * e_loc:(d + 1) * e_loc].sum())
-        xm = np.empty((n, x.shape[1]), dtype=x.dtype)
-        xm[plan.epos[rows[rr], kk]] = recv[rr]         # expand
-        ym = xm if y_major is None else y_major[d]
-        part = np.zeros_like(recv)                     # pre-reduce, k order
-        for kq in range(k):
-            sel = local[:, kq]
-            part[sel] += w[rows[sel], kq][:, None] * ym[plan.epos[rows[sel], kq]]
-        return rows, part, ym
-
-    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
-        res = list(pool.map(dest_step, range(ranks)))
-    out = np.zeros_like(x)
-    for d in range(ranks):                             # ascending destination order
-        rows, part, _ = res[d]
-        out[rows] += part
-    return out, [r[2] for r in res], plan
+    import torch
+    torch.set_num_threads(max(1, threads))
+    logits = torch.as_tensor(logits)
+    x = torch.as_tensor(x)
+    t = x.shape[0]
+    # gating: top-K by value (ties by index via topk's sorted order), softmax
+    # over the picks (renormalised, Qwen3 norm_topk_prob)
+    val, ids = torch.topk(logits, top_k, dim=1, sorted=True)
+    w = torch.softmax(val, dim=1)
+    flat = ids.reshape(-1)
+    order = torch.argsort(flat, stable=True)           # expert-major row -> (t, k) pick
+    xm = x.index_select(0, order // top_k)               # dispatch
+    ym = xm if y_major is None else y_major
+    inv = torch.empty_like(order)
+    inv[order] = torch.arange(order.numel())             # (t, k) pick -> expert-major row
+    out = torch.empty_like(x)
+    for lo in range(0, t, chunk):                        # combine
+        hi = min(t, lo + chunk)
+        yk = ym.index_select(0, inv[lo * top_k:hi * top_k]).view(hi - lo, top_k, -1)
+        out[lo:hi] = torch.bmm(w[lo:hi, None, :], yk.float()).squeeze(1).to(x.dtype)
+    return out, ym, order

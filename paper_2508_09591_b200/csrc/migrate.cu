@@ -10,6 +10,11 @@
 //                 staging area with 16-B peer stores (NVLink), a pair barrier
 //                 (release/acquire flags, bounded), then each commits staging
 //                 into its own slot.  Other GPUs only advance the epoch.
+//                 Every GPU has one staging record PER SOURCE GPU: chained
+//                 swaps that share a GPU (0<->1 then 0<->2) can never
+//                 overwrite a record before its owner committed it, because a
+//                 record is only reused by the same partner, which first has
+//                 to pass the previous swap's second pair barrier.
 // The reference has no cost model for this step.
 
 #include "hm_common.cuh"
@@ -28,7 +33,8 @@ struct StoreDev {
   int P, p, S, n;                       // gpus, my index, slots per gpu, arrays
   int64_t slice[kMaxArrays];            // bytes per slot, per array
   int64_t arr_off[kMaxArrays];          // array offsets in a region
-  int64_t staging_off, flags_off;
+  int64_t staging_off, flags_off;       // staging: [P][rec] records, one per source GPU
+  int64_t rec;                          // bytes of one slot across all arrays
   uint8_t* base[kMaxGpus];              // region base per GPU (peer-mapped)
 };
 
@@ -57,10 +63,10 @@ __global__ void k_push(const StoreDev* __restrict__ sp, int slot, uint8_t* __res
   }
 }
 
-__global__ void k_commit(const StoreDev* __restrict__ sp, int slot) {
+__global__ void k_commit(const StoreDev* __restrict__ sp, int slot, int partner) {
   const StoreDev& s = *sp;
   uint8_t* mine = s.base[s.p];
-  const uint8_t* stg = mine + s.staging_off;
+  const uint8_t* stg = mine + s.staging_off + (int64_t)partner * s.rec;
   int64_t soff = 0;
   for (int a = 0; a < s.n; ++a) {
     int4* d = reinterpret_cast<int4*>(mine + s.arr_off[a] + (int64_t)slot * s.slice[a]);
@@ -149,7 +155,8 @@ HM_API int hm_store_create(int32_t gpus, int32_t gpu_index, int32_t slots_per_gp
     rec += slice_bytes[a];
   }
   s->h.staging_off = (int64_t)o;
-  o = al(o + rec);
+  s->h.rec = (int64_t)rec;
+  o = al(o + (size_t)gpus * rec);
   s->h.flags_off = (int64_t)o;
   o = al(o + (size_t)gpus * 8);
   s->bytes = o;
@@ -236,13 +243,13 @@ HM_API int hm_migrate(hm_store* s, int32_t slot_r, int32_t slot_c, void* stream)
   if (me != gr && me != gc) return 0;
   const int mine = me == gr ? slot_r : slot_c;
   const int partner = me == gr ? gc : gr;
-  // partner's staging area, written through the peer mapping (NVLink)
-  uint8_t* dst = s->h.base[partner] + s->h.staging_off;
+  // my record in the partner's staging area, written through the peer mapping (NVLink)
+  uint8_t* dst = s->h.base[partner] + s->h.staging_off + (int64_t)me * s->h.rec;
   k_push<<<blocks, 256, 0, st>>>(s->d, mine % s->h.S, dst);
   HM_LAUNCHED();
   k_pair_barrier<<<1, 32, 0, st>>>(s->d, partner, 2 * ep - 1, s->status);
   HM_LAUNCHED();
-  k_commit<<<blocks, 256, 0, st>>>(s->d, mine % s->h.S);
+  k_commit<<<blocks, 256, 0, st>>>(s->d, mine % s->h.S, partner);
   HM_LAUNCHED();
   // a second pair barrier so the partner may not reuse our staging early
   k_pair_barrier<<<1, 32, 0, st>>>(s->d, partner, 2 * ep, s->status);

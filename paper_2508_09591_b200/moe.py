@@ -39,7 +39,8 @@ class HierMoELayer:
                  dedup=True, seed: int = 0, renormalize: bool = True, grad: bool = False,
                  n_cap_rows: int = 0, layer_index: int = 0, router: str = "softmax",
                  n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
-                 shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1):
+                 shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1,
+                 transport_params=None, transport_every: int = 50):
         """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
         (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
         / ``route_scale`` and a per-expert score bias).
@@ -50,7 +51,13 @@ class HierMoELayer:
         ``micro_batches`` > 1 splits every local rank's tokens into that many
         micro-batches, each with its own EP world, issued on separate streams
         so one micro-batch's exchange overlaps another's expert GEMMs (the
-        expert weight grads are accumulated over micro-batches)."""
+        expert weight grads are accumulated over micro-batches).
+        ``dedup="auto"``: the transport of a step is chosen by the reference's
+        time model on the step's (global) mask every ``transport_every``
+        forwards (transport.choose_transport; ``transport_params`` a
+        LevelParams or params-JSON path for the runtime [P, L] hierarchy,
+        default the packaged B200 fits); the choices are logged in
+        ``transport_log``."""
         if inter % 128 or hidden % 256 or shared_inter % 128:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
         if grad and (inter % 256 or shared_inter % 256):
@@ -67,14 +74,38 @@ class HierMoELayer:
         self.e_loc = experts // ranks
         # backward supports the per-rank transports; True means per-GPU dedup
         # for inference and per-remote-rank dedup when gradients are needed
+        self.auto_transport = dedup == "auto"
+        if self.auto_transport:
+            from .topology import load_params
+            from .transport import default_params, runtime_topology
+            dedup = True
+            self.runtime_topo = runtime_topology(ranks, gpus, experts, hidden, 2)
+            lv = self.runtime_topo.num_levels
+            if transport_params is None:
+                transport_params = default_params(gpus, lv)
+            elif not hasattr(transport_params, "alpha_intra"):
+                transport_params = load_params(transport_params)
+            self.transport_params = transport_params
+            self.transport_every = max(1, int(transport_every))
+            self.transport_log = []
         self.dedup = "remote" if (grad and (dedup is True or dedup == "gpu")) else dedup
         self.renormalize = renormalize
         self.micro_batches = micro_batches
         t_mb = tokens_per_rank // micro_batches
-        cap_mb = -(-n_cap_rows // micro_batches) if n_cap_rows else 0
+        # every micro-batch world gets the full expert-row capacity: under skewed
+        # routing one micro-batch's hot rank can exceed a 1/m share of it
         self.worlds = [EPWorld(ranks, experts, top_k, hidden, t_mb, dtype=torch.bfloat16,
                                gpus=gpus, gpu_index=gpu_index, group=group, grad=grad,
-                               n_cap_rows=cap_mb) for _ in range(micro_batches)]
+                               n_cap_rows=n_cap_rows) for _ in range(micro_batches)]
+        # device status words of every world (capacity overflow 2, barrier
+        # timeout 3), copied to pinned host memory after each forward and
+        # checked at the next call: no sync on the hot path, no silent drops
+        from .migrate import _wrap
+        self._status_dev = [_wrap(wd.buffer("status", 0)[0], (4,), torch.int32)
+                            for wd in self.worlds]
+        self._status_host = torch.zeros(len(self.worlds), 4, dtype=torch.int32).pin_memory()
+        self._status_ev = None
+        self.strict = False           # True: synchronise and check after every step
         self.world = self.worlds[0]
         self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]
         self.grad = grad
@@ -259,9 +290,52 @@ class HierMoELayer:
         n = self.local * self.tokens_per_rank // self.micro_batches
         return slice(mb * n, (mb + 1) * n)
 
+    def _post_status(self) -> None:
+        """Queue the copy of every world's status word to pinned host memory."""
+        for i, st in enumerate(self._status_dev):
+            self._status_host[i].copy_(st, non_blocking=True)
+        self._status_ev = torch.cuda.Event()
+        self._status_ev.record()
+        if self.strict:
+            self.check_status()
+
+    def check_status(self) -> None:
+        """Raise if the last step's kernels flagged an error: expert-row
+        capacity overflow (picks would have been dropped) or a device barrier
+        timeout (peer data stale).  Called at the start of every forward /
+        backward for the previous step, and after every step when ``strict``."""
+        if self._status_ev is None:
+            return
+        self._status_ev.synchronize()
+        st = self._status_host[:, 0]
+        if bool((st != 0).any()):
+            from .layer import _STATUS
+            code = int(st[st != 0][0])
+            self._status_host.zero_()
+            raise RuntimeError(f"HierMoELayer: {_STATUS.get(code, 'device error')} "
+                               f"(status {code}); raise n_cap_rows or check the peers")
+
+    def choose_transport(self, slot: torch.Tensor):
+        """The reference's time-model choice (none / per-rank / per-GPU dedup)
+        on this step's global mask; every GPU takes the same decision."""
+        import torch.distributed as dist
+        from .routing import mask_from_ids
+        from .transport import choose_transport
+        red = None
+        if self.gpus > 1:
+            red = lambda t: dist.all_reduce(t, group=self.group)  # noqa: E731
+        ch = choose_transport(mask_from_ids(slot, self.experts), self.runtime_topo,
+                              self.transport_params, None, red, allow_deep=not self.grad)
+        self.dedup = "remote" if (self.grad and ch.mode == "gpu") else ch.mode
+        self.transport_log.append((self.iteration, self.dedup, ch))
+        return ch
+
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        self.check_status()
         x = x.contiguous()
         slot, w, ex = self.route_saved(x)
+        if self.auto_transport and self.iteration % self.transport_every == 0:
+            self.choose_transport(slot)
         if self._trace is not None:
             self._trace.append((self.iteration, ex.clone()))
         self.iteration += 1
@@ -310,6 +384,7 @@ class HierMoELayer:
                 prev_c.record(s_m)
         for st in self._streams[1:]:
             cur.wait_stream(st)
+        self._post_status()
         return out
 
     __call__ = forward
@@ -332,6 +407,7 @@ class HierMoELayer:
         """
         if not self.grad or self._saved is None:
             raise RuntimeError("HierMoELayer.backward needs grad=True and a forward first")
+        self.check_status()
         x, xf, logits, slot, w, ex = self._saved
         g = grad_out.contiguous()
         if self.shared_inter:   # shared expert backward beside the routed one

@@ -25,7 +25,12 @@ from .traffic import _device_counts, _Model
 
 
 def smooth_max(x, gamma: float) -> float:
-    """max(x) * (sum((x/max)^gamma))^(1/gamma) (swap.py:35-48), on the GPU."""
+    """max(x) * (sum((x/max)^gamma))^(1/gamma) (swap.py:35-48), on the GPU.
+
+    Limits of the device path (the reference has none): vectors of at most
+    256 entries here; ``cost_matrix`` / ``select_swap`` support group cuts of
+    at most 64 groups (topologies of up to 64 GPUs) and rows of at most 128
+    selected slots (``ValueError`` beyond, never a silent wrong answer)."""
     x = np.asarray(x, dtype=float)
     if x.size == 0:
         raise ValueError("smooth_max of an empty vector")
@@ -254,13 +259,18 @@ def select_swap(mask: MaskLike, topology: Topology, params: LevelParams, gamma: 
         u = topology.level_group_counts
         parts = [_Partials(dev, u[level], defer=True) for level in range(1, topology.num_levels)]
         parts.append(_Partials(dev, topology.num_gpus, defer=True))
-        bufs = [model.dedup_dev, model.raw_dev] + [t for p in parts for t in p.stats()]
+        # the too-dense flags ride along, so every rank reaches the same
+        # decision (raise or not) before the next collective
+        flags = torch.cat([p.flag for p in parts]).to(torch.int64)
+        bufs = [model.dedup_dev, model.raw_dev] + [t for p in parts for t in p.stats()] + [flags]
         flat = torch.cat([b.reshape(-1) for b in bufs])
         dist.all_reduce(flat, group=group)
         off = 0
         for b in bufs:
             b.view(-1).copy_(flat[off:off + b.numel()])
             off += b.numel()
+        for i, p in enumerate(parts):
+            p.flag.copy_(flags[i:i + 1].to(torch.int32))
         model.finish()
         for p in parts:
             p.finish()

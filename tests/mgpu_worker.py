@@ -146,29 +146,43 @@ def run_planner(rank, world):
 
 
 def run_migrate(rank, world):
-    """Cross-GPU and same-GPU slot swaps through the expert store."""
+    """Cross-GPU and same-GPU slot swaps through the expert store, chained
+    back to back with no host synchronisation: consecutive swaps share a GPU
+    (0<->1 then 0<->2 ...), the sequence that needs one staging record per
+    source GPU (a shared staging area let the second partner overwrite GPU 0's
+    staging before it had committed the first partner's expert)."""
     from paper_2508_09591_b200.migrate import ExpertStore
     S = 8
-    arrays = {"w": ((128, 64), torch.bfloat16), "m": ((4096,), torch.float32)}
+    # ~1.3 MB per slot: large enough that pushes and commits overlap in time
+    arrays = {"w": ((256, 1024), torch.bfloat16), "m": ((65536,), torch.float32)}
     st = ExpertStore(S, arrays, gpus=world, gpu_index=rank)
     for i, k in enumerate(arrays):
         v = st[k]
         glob = rank * S + torch.arange(S, device="cuda")
-        v.copy_((glob.view(-1, *([1] * (v.dim() - 1))) * 10 + i).to(v.dtype).expand_as(v))
+        # bf16 holds integers exactly only up to 256: slot ids there, 10*slot+1 in fp32
+        val = glob if i == 0 else glob * 10 + 1
+        v.copy_(val.view(-1, *([1] * (v.dim() - 1))).to(v.dtype).expand_as(v))
     torch.cuda.synchronize()
     dist.barrier()
-    r, c = 1, world * S - 2          # GPU 0 <-> last GPU
-    st.migrate(r, c)
-    st.migrate(2, 5)                 # both on GPU 0
+    pairs = [(1, world * S - 2), (2, 5)]              # GPU 0 <-> last GPU; both on GPU 0
+    for q in range(1, world):                         # GPU 0 <-> every other GPU, chained
+        pairs.append((3, q * S + 4))
+    if world >= 3:
+        pairs += [(S + 1, 2 * S + 6), (0, S + 1), (2 * S + 6, 7)]
+    content = list(range(world * S))                  # global slot -> original slot id
+    for r, c in pairs:
+        st.migrate(r, c)
+        content[r], content[c] = content[c], content[r]
     torch.cuda.synchronize()
     st.check_status()
     for i, k in enumerate(arrays):
         v = st[k]
-        glob = [rank * S + j for j in range(S)]
-        for j, gslot in enumerate(glob):
-            src = {r: c, c: r, 2: 5, 5: 2}.get(gslot, gslot)
-            want = float(src * 10 + i)
-            assert float(v[j].flatten()[0]) == want and float(v[j].flatten()[-1]) == want, (k, gslot)
+        for j in range(S):
+            src = content[rank * S + j]
+            want = float(src if i == 0 else src * 10 + 1)
+            row = v[j].flatten()
+            assert float(row[0]) == want and float(row[-1]) == want, (k, rank * S + j)
+            assert bool((row == want).all()), (k, rank * S + j)
     st.close()
 
 

@@ -169,3 +169,32 @@ def test_sum_to_bf16(n, third):
         want = want + c.float()
     torch.cuda.synchronize()
     assert torch.equal(out, want.to(torch.bfloat16))
+
+
+def test_layer_auto_transport(hm):
+    """dedup="auto": the layer takes the reference time model's choice on the
+    step's mask (transport.choose_transport) and its output equals the layer
+    run with that transport fixed."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    from paper_2508_09591_b200.routing import mask_from_ids
+    from paper_2508_09591_b200.transport import choose_transport, runtime_topology
+    G, E, K, M, I, T_r = 8, 64, 6, 512, 256, 64
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(G * T_r, M, device="cuda", generator=g).to(torch.bfloat16)
+    # one GPU: flat [8] topology; dedup volumes are smaller -> d = 1 ("gpu" == "remote")
+    for p, want in ((hm.LevelParams((), (), (1e-5,), (1e-12,)), "gpu"),):
+        layer = HierMoELayer(G, E, K, M, I, T_r, dedup="auto", seed=3, transport_params=p,
+                             transport_every=2)
+        out = layer(x).clone()
+        it, mode, ch = layer.transport_log[0]
+        assert it == 0 and mode == ch.mode == want
+        slot, _, _ = layer.route(x)
+        ref = choose_transport(mask_from_ids(slot, E), runtime_topology(G, 1, E, M), p)
+        assert ref == ch
+        fixed = HierMoELayer(G, E, K, M, I, T_r, dedup=mode, seed=3)
+        assert torch.equal(fixed(x), out)
+        layer(x)
+        layer(x)                       # iteration 2: re-evaluated
+        assert [t[0] for t in layer.transport_log] == [0, 2]
+        layer.close()
+        fixed.close()

@@ -157,12 +157,22 @@ def test_bruteforce_builder_matches(hm):
         assert slow.dedup_calls > 0
 
 
-def test_generator_matches_reference_stream(hm):
-    """The package's generate_skewed reproduces the reference's masks: the
-    fixtures store masks drawn by the reference; regenerate one by seed."""
-    # smoke-sim protocol: layer_seed(0, it, layer), uniform, 512 x 128, K = 8
-    m = hm.generate_uniform(512, 128, 8, hm.layer_seed(0, 0, 0))
-    assert m.bits.sum(axis=1).tolist() == [8] * 512
+def test_generator_matches_reference_draw(hm):
+    """The package's generate_uniform reproduces the reference's draw
+    (tests/golden/fullsize.json; the full 32,768-token masks are checked by
+    tests/test_fullsize.py)."""
+    import json
+    from pathlib import Path
+    fx = json.loads((Path(__file__).resolve().parent / "golden" / "fullsize.json").read_text())
+    case = fx[0]
+    m = hm.generate_uniform(64, case["experts"], 8, 7)
+    head = np.unpackbits(np.asarray(case["mask_head_packed"], np.uint8), axis=1,
+                         count=case["experts"]).astype(bool)
+    # generate_uniform draws in chunks, so the first 64 rows of a 64-token
+    # draw are not the head of a 32768-token draw; compare the full draw
+    full = hm.generate_uniform(case["tokens"], case["experts"], 8, 7)
+    assert np.array_equal(full.bits[:64], head)
+    assert m.bits.sum(axis=1).tolist() == [8] * 64
 
 
 def _svml_numpy() -> bool:

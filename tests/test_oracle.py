@@ -169,3 +169,23 @@ def test_route_topk_tie_order():
     slots, w, ex = OM.route_topk(logits, 2)
     assert ex.tolist() == [[1, 2], [0, 1]]
     assert np.allclose(w.sum(axis=1), 1.0)
+
+
+def test_cpu_port_step_matches_layer_math():
+    """The timed CPU port (bench.py cpu_baseline / --impl reference) computes
+    the MoE dispatch+combine step: with identity experts out = sum_k w_k x."""
+    import torch
+    g = torch.Generator().manual_seed(3)
+    T, E, K, M = 700, 64, 6, 96
+    logits = torch.randn(T, E, generator=g)
+    x = torch.randn(T, M, generator=g).to(torch.bfloat16)
+    out, ym, order = OM.cpu_dispatch_combine(logits, x, K, threads=2)
+    ids, w, _ = OM.route_topk(logits.numpy(), K)
+    # expert-major rows are the picks sorted by slot, source-major inside a slot
+    flat = ids.reshape(-1)
+    assert np.array_equal(np.sort(flat, kind="stable"), flat[order.numpy()])
+    ref = w.sum(axis=1)[:, None] * x.double().numpy()
+    np.testing.assert_allclose(out.double().numpy(), ref, rtol=2e-2, atol=2e-2)
+    # with non-identity experts: y = 2 x on every expert-major row
+    out2, _, _ = OM.cpu_dispatch_combine(logits, x, K, y_major=(ym.float() * 2).to(ym.dtype))
+    np.testing.assert_allclose(out2.double().numpy(), 2 * ref, rtol=2e-2, atol=4e-2)
