@@ -421,8 +421,6 @@ def main():
     ap.add_argument("--no-layer", action="store_true", help="skip the full layer forward")
     ap.add_argument("--no-planner", action="store_true", help="skip the swap-planner timing")
     ap.add_argument("--no-hd2", action="store_true", help="skip config C's two-level timing")
-    ap.add_argument("--pipelined-variant", action="store_true",
-                    help="also time the staged (flag-pipelined) exchange at N > 1")
     args = ap.parse_args()
     world, rank, local = dist_env()
     G, E, K, M, T_r, desc = CONFIGS[args.config]
@@ -472,7 +470,20 @@ def main():
     ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, n_cap_rows=cap)
     raw_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, n_cap_rows=cap)
     all_ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, n_cap_rows=cap)
-    MODE = "gpu"   # one row per (token, remote GPU); same-GPU ranks go expert-major directly
+    # the step's transport: the reference time model's choice (traffic.py:188-221,
+    # transport.choose_transport) on this step's global mask with the B200 fits
+    # of the runtime [P, L] hierarchy (paper_2508_09591_b200/params)
+    from paper_2508_09591_b200.routing import mask_from_ids
+    from paper_2508_09591_b200.transport import choose_transport, default_params, runtime_topology
+    rtopo = runtime_topology(G, world, E, M, 2)
+    rparams = default_params(world, rtopo.num_levels)
+    slot0, _, _ = route_topk(logits, K)
+    red = (lambda t_: dist.all_reduce(t_)) if world > 1 else None
+    choice = choose_transport(mask_from_ids(slot0, E), rtopo, rparams, None, red)
+    MODE = choice.mode
+    # one GPU: fused dispatch (row indices; the expert GEMM gathers the rows)
+    FUSED = world == 1
+    ep.set_fused(FUSED)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # 256 MB > L2
 
     def prime(w_, dedup):
@@ -561,12 +572,12 @@ def main():
         del cg
     except Exception as exc:   # noqa: BLE001 -- report, keep the eager numbers
         graph_ms = f"unavailable: {exc}"
-    ms_pipelined = None
-    if world > 1 and args.pipelined_variant:   # staged kernels with NVLink flags (slower)
-        ep.set_pipelined(True)
-        ms_pipelined = timed(ep, MODE, max(3, args.steps // 2), args.warmup)
-        ep.set_pipelined(False)
-        timed(ep, MODE, 3, 1)
+    ms_copy = None
+    if FUSED:   # the same step with the copying dispatch (materialised expert-major rows)
+        ep.set_fused(False)
+        ms_copy = timed(ep, MODE, max(3, args.steps // 2), args.warmup)
+        seg_copy = None
+        ep.set_fused(True)
     ms_raw = timed(raw_ep, "none", max(3, args.steps // 2), args.warmup)
     nccl = None
     if world > 1:   # the non-dedup AlltoAll on NCCL (what the >= 1.5x target is quoted against)
@@ -597,21 +608,10 @@ def main():
         _lib.call("hm_world_set_timing", w_._h, 0)
         return acc / n
 
-    ep.set_tma_gather(True)
-    seg_tma = seg_times(ep, MODE)
-    ep.set_tma_gather(False)
-    ep.set_bulk_pack(True)
-    seg_bulkpack = seg_times(ep, MODE)
-    ep.set_bulk_pack(False)
-    ep.set_split_pack(True)
-    seg_split = seg_times(ep, MODE)
-    ep.set_split_pack(False)
-    ep.set_lean_pack(False)
-    seg_general = seg_times(ep, MODE)
-    ep.set_lean_pack(True)
-    _lib.call("hm_world_set_option", ep._h, 9, 1)
-    seg_su8 = seg_times(ep, MODE)
-    _lib.call("hm_world_set_option", ep._h, 9, 0)
+    if FUSED:
+        ep.set_fused(False)
+        seg_copy = seg_times(ep, MODE)
+        ep.set_fused(True)
     seg = seg_times(ep, MODE)
     seg_raw = seg_times(raw_ep, "none")
     seg_all = seg_times(all_ep, "all")
@@ -635,7 +635,8 @@ def main():
     src_gpu = np.arange(G) // L
     N_rem_in = int(cnt[src_gpu != rank][:, G:][:, slot_gpu == rank].sum())
     alg = {
-        "pack": T * rb + (rem_dedup + loc_direct) * rb + rem_dedup * K * 8,
+        # fused (one GPU): ids + rank_e read, epos + row index written per pick
+        "pack": T * K * 16 if FUSED else T * rb + (rem_dedup + loc_direct) * rb + rem_dedup * K * 8,
         "expand": R_in * rb + N_rem_in * rb + R_in * K * 8,
         "reduce": N_rem_in * rb + R_in * rb + R_in * K * 8,
         "gather": (rem_dedup + loc_direct) * rb + T * rb,
@@ -645,13 +646,7 @@ def main():
     # the raw transport pushes in pack and pulls expert outputs in gather
     seg_ms = dict(zip(SEGMENTS, seg.tolist()))
     raw_ms = dict(zip(SEGMENTS, seg_raw.tolist()))
-    # pipelined exchange (N > 1): the dispatch is one kernel (pack segment:
-    # push + expand), the combine one kernel (gather segment: reduce + gather)
-    pipelined = world > 1 and seg_ms["reduce"] == 0.0
-    if pipelined:
-        alg["pack"] += alg.pop("expand")
-        alg["gather"] += alg.pop("reduce")
-    ret_key = "gather" if pipelined else "reduce"
+    ret_key = "reduce"
     link = {"pack": rem_dedup * rb, ret_key: R_in * rb} if world > 1 else {}
     link_dedup = seg_ms["pack"] + seg_ms[ret_key] if world > 1 else 0.0
     link_raw = raw_ms["pack"] + raw_ms["gather"] if world > 1 else 0.0
@@ -918,18 +913,24 @@ def main():
             "combine_us": 1e3 * (seg_ms["reduce"] + seg_ms["barrier2"] + seg_ms["gather"]),
             "kernel_ms": {k: round(v, 4) for k, v in seg_ms.items()},
             "kernels": per_kernel,
-            "gather_tma_variant_ms": round(float(seg_tma[SEGMENTS.index("gather")]), 4),
-            "pack_bulk_variant_ms": round(float(seg_bulkpack[SEGMENTS.index("pack")]), 4),
-            "pack_split_variant_ms": round(float(seg_split[SEGMENTS.index("pack")]), 4),
-            "pack_general_variant_ms": round(float(seg_general[SEGMENTS.index("pack")]), 4),
-            "gather_su8_variant_ms": round(float(seg_su8[SEGMENTS.index("gather")]), 4),
+            "dispatch": "fused: row indices, GEMM1 gathers the rows (TMA gather4)" if FUSED
+                        else "copy: rows to the expert-major buffers",
+            "materialized_dispatch": None if not FUSED else {
+                "ms_per_step": ms_copy, "value": tokens_total / (ms_copy * 1e-3),
+                "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_copy.tolist())},
+                "note": "the same step with the expert-major rows copied (k_pack_local)"},
             "transport": MODE,
+            "transport_choice": {"mode": choice.mode, "d_star": choice.d_star,
+                                 "times_s": list(choice.times),
+                                 "time_without_dedup_s": choice.time_without_dedup,
+                                 "runtime_topology": list(rtopo.level_fanouts),
+                                 "rule": "reference pick_dimension over dedup times; no dedup "
+                                         "only if strictly faster (transport.py)"},
             "nodedup": {"ms_per_step": ms_raw, "value": tokens_total / (ms_raw * 1e-3),
                         "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_raw.tolist())},
                         "speedup_dedup_vs_nodedup": ms_raw / ms,
                         "link_time_ratio": link_raw / max(link_dedup, 1e-9) if link_dedup else None},
             "nccl_nodedup": nccl,
-            "pipelined_variant_ms_per_step": ms_pipelined,
             "cuda_graph_ms_per_step": graph_ms,
             "hd2_2x4": hd2,
             "dedup_all_ranks": {"ms_per_step": ms_all,

@@ -225,6 +225,25 @@ int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t 
 int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                        const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                        void* y, void* g13, void* stream);
+/* Fused dispatch (one GPU): the expert-major rows are not materialised;
+ * layout row r (capacity a_rows, groups of n_rows[g]) is source row idx[r]
+ * of x [x_rows][hidden], loaded by GEMM1's TMA gather4.  g13 optional (the
+ * pre-activations for the backward).  Replaces the copy half of the dispatch
+ * the reference models as one AlltoAll row per selection (traffic.py:164-170)
+ * with row indices (hm_world_set_option 10 makes hm_dispatch emit them). */
+int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* idx, int64_t a_rows,
+                         const int32_t* n_rows, int32_t groups, const void* w13, const void* w2,
+                         int32_t hidden, int32_t inter, void* h, void* y, void* g13,
+                         void* stream);
+/* Its backward (saved pre-activations, MN-major weight gradients; dW13's
+ * token operand gathered from x by idx).  accumulate != 0 adds the weight
+ * grads to dw13 / dw2. */
+int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const int32_t* idx,
+                                  int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                                  const void* w13t, const void* w2t, const void* gy,
+                                  int32_t hidden, int32_t inter, const void* g13, void* dh,
+                                  void* dg13, void* h, int32_t* layout, void* gx, void* dw13,
+                                  void* dw2, int32_t accumulate, void* stream);
 /* Expert FFN backward: recomputed pre-activations, dgrad GEMMs with
  * transposed weights (w13t [g][M][2I], w2t [g][I][M]), SwiGLU backward, and
  * weight-gradient GEMMs over each expert's own token range. */

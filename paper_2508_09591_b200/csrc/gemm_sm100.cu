@@ -53,6 +53,7 @@ int g_wgrad_pair = 0;
 // 16-byte k_swiglu_bwd_v8 is the default; bit-identical)
 int g_swiglu_scalar = 0;
 
+
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
   int groups;
@@ -65,10 +66,30 @@ struct GemmArgs {
   __nv_bfloat16* out2;    // SwiGLU mode: optional pre-activations [rows, N] (gate/up blocks)
   int accumulate;         // modes 2/3: out += result (fp32 add of the stored bf16)
   int* status;
+  // fused dispatch: gather the A rows (modes 0/1, pair kernel) or the B token
+  // rows (mode 3) by row index from a token-major source (16-byte cp.async by
+  // four producer warps, straight into the 128-byte-swizzled stage) instead
+  // of reading materialised expert-major copies: row r of the group layout
+  // is source row idx[r] of src (row pitch ld bytes)
+  const int32_t* a_idx;
+  const int32_t* b_idx;
+  const uint8_t* g_src;
+  int64_t g_ld;
 };
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+constexpr int kGatherThreads = 128;   // warps 8-11 of a gathering kernel
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// arrive on `bar` once this thread's cp.async copies so far have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -100,6 +121,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try(addr, phase)) {
     uint64_t t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 10000000000ull) __trap();
+  }
+}
+
+// wait with cluster-scope acquire: the stage's arrivals include a release
+// from the peer CTA (the gathered A of a CTA pair)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  uint64_t t0 = 0;
+  for (int it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(phase)
+        : "memory");
+    if (ok) return;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (it == 0) t0 = t1;
     if (t1 - t0 > 10000000000ull) __trap();
   }
 }
@@ -306,8 +348,10 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
 // group's tokens are its rows), both operands MN-major in shared memory (TMA
 // boxes of 64 tokens x 64 features, one 128 B line per token); the tail
 // k-block's lines past the group are zeroed before the MMA reads them.
-template <int kMode>
-__global__ void __launch_bounds__(kThreads, 1)
+// GB (mode 3 only): B's token rows are gathered by index (args.b_idx) by
+// warps 8-11 with cp.async into the swizzled stage instead of TMA boxes
+template <int kMode, bool GB = false>
+__global__ void __launch_bounds__(GB ? kThreads + kGatherThreads : kThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -338,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tm.start[args.groups] = acc;
     tm.total = acc;
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, GB ? 1 + kGatherThreads : 1);
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -360,9 +404,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kblocks_fixed = args.K / BK;
 
   if (warp == 0) {
+    // lane 0 drives the ring (with GB only A's boxes; warps 8-11 fill B)
+    constexpr bool gather_b = kMode == 3 && GB;
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
@@ -375,20 +422,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                             : kMode == 3 ? (tm.rows[g] + BK - 1) / BK
                                          : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
-          mbar_expect_tx(full + stage, kStageBytes);
-          if (kMode == 3) {   // 64-token x 64-feature boxes: 2 for A, 4 for B
+          {
+            mbar_wait(empty + stage, phase ^ 1);
+            mbar_expect_tx(full + stage, gather_b ? kABytes : kStageBytes);
+            if (kMode == 3) {   // 64-token x 64-feature boxes: 2 for A, 4 for B
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(sa + stage * kABytes + j * 8192, &map_a, full + stage, arow + 64 * j,
-                          k0 + kb * BK);
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_2d(sa + stage * kABytes + j * 8192, &map_a, full + stage, arow + 64 * j,
+                            k0 + kb * BK);
+              if (!gather_b) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + stage * kBBytes + j * 8192, &map_b, full + stage, brow + 64 * j,
-                          k0 + kb * BK);
-          } else {
-            tma_load_2d(sa + stage * kABytes, &map_a, full + stage, k0 + kb * BK, arow);
-            tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, k0 + kb * BK, brow);
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_load_2d(sb + stage * kBBytes + j * 8192, &map_b, full + stage,
+                              brow + 64 * j, k0 + kb * BK);
+              }
+            } else {
+              tma_load_2d(sa + stage * kABytes, &map_a, full + stage, k0 + kb * BK, arow);
+              tma_load_2d(sb + stage * kBBytes, &map_b, full + stage, k0 + kb * BK, brow);
+            }
           }
           if (++stage == kStages) {
             stage = 0;
@@ -485,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(tfull + acc);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
     const int q = warp - 4;  // TMEM lane quarter
     int it = 0;
     for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++it) {
@@ -501,6 +552,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
+    }
+  } else if (GB && warp >= 8) {
+    // B gather (mode 3): 64 token lines x 4 feature boxes x 8 16-byte chunks
+    // per stage; thread g owns chunk g % 8 of lines g / 8 + 16 i in every box
+    const int g_t = threadIdx.x - kThreads;
+    const int c = g_t & 7, l0 = g_t >> 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      const int kblocks = (tm.rows[g] + BK - 1) / BK;
+      const int end = tm.row0[g] + tm.rows[g];
+      const uint8_t* col = args.g_src + (int64_t)(nt * BN + 8 * c) * 2;
+      // the k-block's token indices are loaded one k-block ahead (their load
+      // latency would otherwise sit in every stage's critical path)
+      auto load_tok = [&](int kb, int* tk) {
+        const int r0 = tm.row0[g] + kb * BK + l0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tk[i] = args.b_idx[r0 + 16 * i < end ? r0 + 16 * i : tm.row0[g]];
+      };
+      int nxt[4];
+      load_tok(0, nxt);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        int tok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tok[i] = nxt[i];
+        if (kb + 1 < kblocks) load_tok(kb + 1, nxt);
+        mbar_wait(empty + stage, phase ^ 1);
+        const uint32_t base = smem_u32(sb + stage * kBBytes);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int l = l0 + 16 * i;
+          const uint8_t* src = col + (int64_t)tok[i] * args.g_ld;
+          const uint32_t dl = base + l * 128 + ((c ^ (l & 7)) << 4);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) cp_async16(dl + j * 8192, src + j * 128);
+        }
+        cp_async_arrive(full + stage);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
   }
   __syncthreads();
@@ -567,8 +662,12 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
                : "memory");
 }
 
-template <int kMode>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// GA (modes 0/1): the A rows are gathered by index (args.a_idx) by warps 8-11
+// of each CTA with cp.async into its swizzled stage; they arrive on a local
+// gfull barrier, and warp 2's lane 0 forwards each completed stage to the
+// leader's full barrier (which then counts the B TMA bytes + 2 forwarders)
+template <int kMode, bool GA = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGatherThreads : kThreads, 1)
     k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -580,7 +679,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages2;
   uint64_t* tfull = empty + kStages2;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* gfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + kStages2);
   __shared__ TileMap tm;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -602,8 +702,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tm.start[args.groups] = acc;
     tm.total = acc;
     for (int s = 0; s < kStages2; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, GA ? 3 : 1);
       mbar_init(empty + s, 1);
+      mbar_init(gfull + s, kGatherThreads);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
@@ -625,6 +726,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int kblocks_fixed = args.K / BK;
 
   if (warp == 0) {
+    // lane 0 drives the ring (with GA only B's TMA loads; warps 8-11 fill A)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -641,8 +743,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          if (leader) mbar_expect_tx(full + stage, 2 * kStageBytes2);
-          tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
+          if (leader) mbar_expect_tx(full + stage, GA ? 2 * kHalfBytes : 2 * kStageBytes2);
+          if (!GA)
+            tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
           tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, k0 + kb * BK, brow);
           if (++stage == kStages2) {
             stage = 0;
@@ -669,7 +772,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           kblocks = tm.rows[g] / BK;
         }
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(full + stage, phase);
+          if (GA)
+            mbar_wait_cluster(full + stage, phase);
+          else
+            mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
           const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
@@ -686,7 +792,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         umma_commit_pair(tfull + acc);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
     const int q = warp - 4;
     int it = 0;
     for (int t = cid; t < tm.total; t += ncl, ++it) {
@@ -702,6 +808,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
+    }
+  } else if (GA && warp == 2) {
+    if (lane == 0) {   // forwarder: this CTA's gathered stage -> the leader's full barrier
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < tm.total; t += ncl) {
+        for (int kb = 0; kb < kblocks_fixed; ++kb) {
+          mbar_wait(gfull + stage, phase);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (leader) {
+            mbar_arrive(full + stage);
+          } else {
+            // relaxed: the stage's bytes live in THIS CTA's shared memory (the
+            // cp.async completion observed above + the proxy fence make them
+            // visible to this SM's tensor core); no cluster-wide release
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(remote) : "r"(smem_u32(full + stage)), "r"(0));
+            asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+                         ::"r"(remote) : "memory");
+          }
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (GA && warp >= 8) {
+    // A gather: this CTA's 128 rows x 8 16-byte chunks per stage; thread g owns
+    // chunk g % 8 of rows g / 8 + 16 i (row pointers loaded once per tile)
+    const int g_t = threadIdx.x - kThreads;
+    const int c = g_t & 7, r0 = g_t >> 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cid; t < tm.total; t += ncl) {
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      const uint8_t* src[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = mt * BM2 + (int)rank * 128 + r0 + 16 * i;   // row within the group
+        const int row = tm.row0[g] + (r < tm.rows[g] ? r : 0);
+        src[i] = args.g_src + (int64_t)args.a_idx[row] * args.g_ld + c * 16;
+      }
+      for (int kb = 0; kb < kblocks_fixed; ++kb) {
+        mbar_wait(empty + stage, phase ^ 1);
+        const uint32_t base = smem_u32(sa + stage * kHalfBytes);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 16 * i;
+          cp_async16(base + r * 128 + ((c ^ (r & 7)) << 4), src[i] + kb * (BK * 2));
+        }
+        cp_async_arrive(gfull + stage);
+        if (++stage == kStages2) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
   }
   __syncthreads();
@@ -1293,16 +1458,20 @@ int make_map_mn(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) 
 
 // out[g] ([m_out][N], ld_out) = A_g^T B_g over group g's token rows of
 // A [a_rows][m_out] and B [a_rows][N] (kMode 3)
+// b_idx: B's token rows are gathered from b [b_src_rows][N] (fused dispatch)
 int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
                       const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
-                      cudaStream_t s, int accumulate = 0) {
+                      cudaStream_t s, int accumulate = 0, const int32_t* b_idx = nullptr,
+                      int64_t b_src_rows = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
   HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
+  HM_CHECK_ARG(!b_idx || (b_src_rows >= 1 && g_wgrad_pair == 0),
+               "wgrad gemm: gathered B needs source rows and the single-CTA kernel");
   CUtensorMap ma, mb;
   int st = make_map_mn(&ma, a, (uint64_t)a_rows, (uint64_t)m_out);
   if (st) return st;
-  st = make_map_mn(&mb, b, (uint64_t)a_rows, (uint64_t)N);
+  st = make_map_mn(&mb, b, (uint64_t)(b_idx ? b_src_rows : a_rows), (uint64_t)N);
   if (st) return st;
   GemmArgs args;
   args.m_out = m_out;
@@ -1316,6 +1485,10 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.out2 = nullptr;
   args.accumulate = accumulate;
   args.status = nullptr;
+  args.a_idx = nullptr;
+  args.b_idx = b_idx;
+  args.g_src = reinterpret_cast<const uint8_t*>(b);
+  args.g_ld = (int64_t)N * 2;
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
@@ -1347,6 +1520,13 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
     HM_LAUNCHED();
     return 0;
   }
+  if (b_idx) {
+    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_grouped_gemm<3, true><<<sms, kThreads + kGatherThreads, smem, s>>>(ma, mb, args);
+    HM_LAUNCHED();
+    return 0;
+  }
   HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   k_grouped_gemm<3><<<sms, kThreads, smem, s>>>(ma, mb, args);
@@ -1354,14 +1534,19 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   return 0;
 }
 
+// a_idx: the A rows are gathered from a [a_src_rows][K] by row index (fused
+// dispatch, CTA-pair forward kernels only); a_rows is then the layout's capacity
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
-                cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0, void* out2 = nullptr) {
+                cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0, void* out2 = nullptr,
+                const int32_t* a_idx = nullptr, int64_t a_src_rows = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
+  HM_CHECK_ARG(!a_idx || (a_src_rows >= 1 && !wgrad_m_out),
+               "grouped gemm: gathered A needs source rows (forward modes)");
   CUtensorMap ma, mb;
-  int st = make_map(&ma, a, (uint64_t)a_rows, (uint64_t)K, BM);
+  int st = make_map(&ma, a, (uint64_t)(a_idx ? a_src_rows : a_rows), (uint64_t)K, BM);
   if (st) return st;
   st = make_map(&mb, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, BN);
   if (st) return st;
@@ -1377,19 +1562,34 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.out2 = reinterpret_cast<__nv_bfloat16*>(out2);
   args.accumulate = 0;
   args.status = status;
+  args.a_idx = a_idx;
+  args.b_idx = nullptr;
+  args.g_src = reinterpret_cast<const uint8_t*>(a);
+  args.g_ld = (int64_t)K * 2;
   const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
-  if (!wgrad_m_out && g_gemm_pair) {   // 256 x 256 tiles on CTA pairs
+  if (!wgrad_m_out && (g_gemm_pair || a_idx)) {   // 256 x 256 tiles on CTA pairs
     CUtensorMap mb2;
     st = make_map(&mb2, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, 128);
     if (st) return st;
     const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
     const int grid = sms & ~1;
-    if (swiglu) {
+    if (a_idx) {   // fused dispatch: A rows gathered by warps 8-11
+      const int thr = kThreads + kGatherThreads;
+      if (swiglu) {
+        HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<1, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        k_grouped_gemm_pair<1, true><<<grid, thr, smem2, s>>>(ma, mb2, args);
+      } else {
+        HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<0, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        k_grouped_gemm_pair<0, true><<<grid, thr, smem2, s>>>(ma, mb2, args);
+      }
+    } else if (swiglu) {
       HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       k_grouped_gemm_pair<1><<<grid, kThreads, smem2, s>>>(ma, mb2, args);
@@ -1499,7 +1699,38 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                         const void* w13, const void* w13t, const void* w2t, const void* gy,
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
-                        void* gx, void* dw13, void* dw2, void* stream, int accumulate = 0);
+                        void* gx, void* dw13, void* dw2, void* stream, int accumulate = 0,
+                        const int32_t* x_idx = nullptr, int64_t x_rows = 0);
+
+// Fused dispatch: the expert-major rows are never materialised -- row r of
+// the expert-major layout (capacity a_rows, groups of n_rows[g]) is source
+// row idx[r] of x [x_rows][hidden] (the tokens themselves), loaded by GEMM1's
+// TMA gather4.  g13 (optional) keeps the pre-activations for the backward.
+HM_API int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* idx, int64_t a_rows,
+                                const int32_t* n_rows, int32_t groups, const void* w13,
+                                const void* w2, int32_t hidden, int32_t inter, void* h, void* y,
+                                void* g13, void* stream) {
+  HM_CHECK_ARG(x && idx, "hm_expert_ffn_gather: null argument");
+  int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
+                       (cudaStream_t)stream, 0, 0, g13, idx, x_rows);
+  if (st) return st;
+  return launch_gemm(h, a_rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
+                     (cudaStream_t)stream);
+}
+
+// ... its backward (saved pre-activations): dW13's token operand is gathered
+// from x by the same row indices; accumulate adds the weight grads
+HM_API int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const int32_t* idx,
+                                         int64_t a_rows, const int32_t* n_rows, int32_t groups,
+                                         const void* w13t, const void* w2t, const void* gy,
+                                         int32_t hidden, int32_t inter, const void* g13, void* dh,
+                                         void* dg13, void* h, int32_t* layout, void* gx,
+                                         void* dw13, void* dw2, int32_t accumulate, void* stream) {
+  HM_CHECK_ARG(x && idx, "hm_expert_ffn_backward_gather: null argument");
+  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
+                      const_cast<void*>(g13), 1, dh, dg13, h, nullptr, nullptr, 0, layout, gx,
+                      dw13, dw2, stream, accumulate, idx, x_rows);
+}
 
 HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
                                   int32_t groups, const void* w13, const void* w13t,
@@ -1542,8 +1773,12 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                         const void* w13, const void* w13t, const void* w2t, const void* gy,
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
-                        void* gx, void* dw13, void* dw2, void* stream, int accumulate) {
+                        void* gx, void* dw13, void* dw2, void* stream, int accumulate,
+                        const int32_t* x_idx, int64_t x_rows) {
   cudaStream_t s = (cudaStream_t)stream;
+  HM_CHECK_ARG(!x_idx || (g13_saved && !g_wgrad_transposed),
+               "ffn backward: gathered activations need the saved pre-activations and the "
+               "MN-major weight gradients");
   if (g_wgrad_transposed)
   HM_CHECK_ARG(kmax % BK == 0 && kmax >= a_rows + (int64_t)BK * groups,
                "hm_expert_ffn_backward: kmax must cover the padded rows");
@@ -1590,5 +1825,6 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
   }
   if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate)))
     return st;
-  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate);
+  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate,
+                           x_idx, x_rows);
 }

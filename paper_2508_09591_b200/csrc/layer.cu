@@ -1118,6 +1118,44 @@ __global__ void __launch_bounds__(256) k_pack_local(const WorldDev* __restrict__
   }
 }
 
+// Fused one-GPU dispatch (hm_world_set_option 10): the expert-major rows are
+// not materialised -- each pick's expert-major position gets the token's row
+// index (xidx[local rank][epos] = t), and the expert GEMM gathers its A rows
+// from x with TMA gather4 (hm_expert_ffn_gather).  Thread per (token, pick):
+// T*K*(4 + 4) bytes instead of T*M*v + T*K*M*v.
+__global__ void __launch_bounds__(256) k_index_local(const WorldDev* __restrict__ wp,
+                                                     const int32_t* __restrict__ ids,
+                                                     const int32_t* __restrict__ chunk_off,
+                                                     const int32_t* __restrict__ rank_e,
+                                                     const int32_t* __restrict__ eoff, int nchunks,
+                                                     int32_t* __restrict__ epos_out,
+                                                     int32_t* __restrict__ xidx,
+                                                     int* __restrict__ status) {
+  const WorldDev& w = *wp;
+  const int C = w.G + w.E + w.P;
+  const int64_t T = (int64_t)w.L * w.T_r;
+  const int64_t n = T * w.K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / w.K;
+    const int e = ids[i];
+    int ep = -1;
+    if (e >= 0) {
+      const int s_loc = (int)(t / w.T_r);
+      const int64_t t_in = t - (int64_t)s_loc * w.T_r;
+      const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
+      ep = eoff[s_loc * w.E + e] + coff[w.G + e] + rank_e[i];
+      if (ep >= w.N_cap) {
+        atomicExch(status, 2);
+        ep = -1;
+      } else {
+        xidx[(int64_t)(rank_of_slot(w, e) - w.p * w.L) * w.N_cap + ep] = (int32_t)t;
+      }
+    }
+    epos_out[i] = ep;
+  }
+}
+
 // expand (dedup, destination side): warp per received row -> its local
 // experts' expert-major rows.
 __global__ void __launch_bounds__(256) k_expand(const WorldDev* __restrict__ wp,
@@ -2396,6 +2434,10 @@ struct hm_world {
   bool split_pack = false;
   bool lean_pack = true;       // hm_world_set_option(w, 8, 0): general pack on one GPU too
   bool gather_su8 = false;     // hm_world_set_option(w, 9, 1): 8-source load batches in the gather
+  // hm_world_set_option(w, 10, 1): fused one-GPU dispatch -- row indices
+  // instead of expert-major row copies (the expert GEMM gathers)
+  bool fused = false;
+  int32_t* xidx = nullptr;     // [L][N_cap] source row of every expert-major row
   int fused_blocks = 0;        // co-resident grid of the pipelined kernels
   int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long* epoch_ctr = nullptr;   // device barrier epoch counter
@@ -2588,6 +2630,7 @@ HM_API int hm_world_destroy(hm_world* w) {
   cudaFree(w->eoff);
   cudaFree(w->n_e);
   cudaFree(w->status);
+  cudaFree(w->xidx);
   cudaFree(w->epoch_ctr);
   cudaFree(w->pipe);
   cudaFree(w->d);
@@ -2805,6 +2848,15 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   const size_t bulk_smem = (size_t)kBulkWarps * 2 * h.row_bytes;
   const int64_t nv = h.row_bytes / 16;
   const bool local_only = h.P == 1 && mode != 1 && !h.U1;
+  HM_CHECK_ARG(!(w->fused && mode == 1),
+               "hm_dispatch: the fused dispatch writes expert-major row indices (modes 0, 2, 3)");
+  if (local_only && w->fused) {
+    SegScope sc(w, kSegPack, s);
+    k_index_local<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(
+        w->d, ids, w->chunk_cnt, w->rank_e, w->eoff, w->nchunks, w->epos, w->xidx, w->status);
+    HM_LAUNCHED();
+    return 0;
+  }
   if (local_only && w->lean_pack && !w->bulk_pack &&
       (nv == 32 || nv == 64 || nv == 128 || nv == 256)) {
     // one token per warp up to 32 CTAs per SM: the block scheduler keeps
@@ -3145,6 +3197,8 @@ HM_API int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void**
     case 14: *ptr = h.recv_g[h.p]; *bytes = h.Rg_cap * h.row_bytes; break;
     case 15: *ptr = w->gpos_g; *bytes = T * h.P * 4; break;
     case 16: *ptr = reinterpret_cast<uint8_t*>(w->offs) + offsetof(Offsets, R_g); *bytes = 4; break;
+    case 17: *ptr = w->xidx ? w->xidx + (int64_t)local_rank * h.N_cap : nullptr;
+             *bytes = w->xidx ? h.N_cap * 4 : 0; break;
     default: hm::set_error("hm_world_buffer: unknown kind %d", kind); return hm::kInvalid;
   }
   return 0;
@@ -3287,7 +3341,7 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
 // kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 9, "hm_world_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option >= 0 && option <= 10, "hm_world_set_option: unknown option %d", option);
   if (option == 0) w->tma_gather = value != 0;
   if (option == 1) w->pipelined = value != 0;
   if (option == 2) {
@@ -3304,5 +3358,14 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   if (option == 7) w->split_pack = value != 0;
   if (option == 8) w->lean_pack = value != 0;
   if (option == 9) w->gather_su8 = value != 0;
+  if (option == 10) {
+    HM_CHECK_ARG(!value || (w->h.P == 1 && !w->h.U1),
+                 "hm_world_set_option: the fused dispatch needs a one-GPU, non-relay world");
+    if (value && !w->xidx) {
+      HM_CUDA(cudaMalloc(&w->xidx, (size_t)w->h.L * w->h.N_cap * 4));
+      HM_CUDA(cudaMemset(w->xidx, 0, (size_t)w->h.L * w->h.N_cap * 4));
+    }
+    w->fused = value != 0;
+  }
   return 0;
 }

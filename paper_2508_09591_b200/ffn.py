@@ -66,6 +66,28 @@ def expert_ffn_save_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
               inter, ptr(h), y_ptr, g13_ptr, stream_ptr())
 
 
+def expert_ffn_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_rows: int, n_rows_ptr: int,
+                           groups: int, w13: torch.Tensor, w2: torch.Tensor, hidden: int,
+                           inter: int, h: torch.Tensor, y_ptr: int, g13_ptr: int = 0) -> None:
+    """FFN with the fused dispatch: GEMM1 gathers its rows from the token-major
+    x [x_rows, hidden] by the expert-major row indices idx (TMA gather4)."""
+    _lib.call("hm_expert_ffn_gather", x_ptr, x_rows, idx_ptr, a_rows, n_rows_ptr, groups,
+              ptr(w13), ptr(w2), hidden, inter, ptr(h), y_ptr, g13_ptr or None, stream_ptr())
+
+
+def expert_ffn_backward_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_rows: int,
+                                    n_rows_ptr: int, groups: int, w13t: torch.Tensor,
+                                    w2t: torch.Tensor, gy_ptr: int, hidden: int, inter: int,
+                                    sc: "FFNBackwardScratch", gx_ptr: int, dw13: torch.Tensor,
+                                    dw2: torch.Tensor, g13_saved_ptr: int,
+                                    accumulate: bool = False) -> None:
+    """Backward of expert_ffn_gather_ptrs (saved pre-activations)."""
+    _lib.call("hm_expert_ffn_backward_gather", x_ptr, x_rows, idx_ptr, a_rows, n_rows_ptr, groups,
+              ptr(w13t), ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh),
+              ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
+              int(bool(accumulate)), stream_ptr())
+
+
 def set_gemm_pair(enabled: bool) -> None:
     """CTA-pair (cta_group::2, 256 x 256 tiles) kernels for the forward and
     data-gradient GEMMs."""

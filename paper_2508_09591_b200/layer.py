@@ -34,7 +34,7 @@ from ._lib import ptr, stream_ptr
 
 _KIND = {"recv_x": 0, "recv_meta": 1, "xmaj": 2, "ymaj": 3, "comb": 4, "counts": 5, "gpos": 6,
          "epos": 7, "hitmask": 8, "offsets": 9, "n_e": 10, "status": 11, "gy": 12, "gx": 13,
-         "recv_g": 14, "gpos_g": 15, "rows_g": 16}
+         "recv_g": 14, "gpos_g": 15, "rows_g": 16, "xidx": 17}
 
 _STATUS = {2: "row capacity overflow", 3: "peer barrier timeout", 4: "slot id out of range"}
 
@@ -159,6 +159,7 @@ class EPWorld:
         info = (ctypes.c_int64 * 8)()
         _lib.check(lib.hm_world_info(h, info), "hm_world_info")
         self.r_cap, self.n_cap, self.row_bytes, self.sym_bytes = info[4], info[5], info[6], info[7]
+        self.fused = False
         if gpus > 1:
             self._open_peers(group)
 
@@ -275,6 +276,13 @@ class EPWorld:
     def set_lean_pack(self, enabled: bool) -> None:
         """One-GPU pack: the lean kernel (default) or the general pack."""
         _lib.call("hm_world_set_option", self._h, 8, int(bool(enabled)))
+
+    def set_fused(self, enabled: bool) -> None:
+        """One GPU: dispatch emits expert-major row indices (buffer "xidx")
+        instead of copying rows; the expert GEMM gathers the rows from x
+        (ffn.expert_ffn_gather_ptrs).  "xmaj" is then not written."""
+        _lib.call("hm_world_set_option", self._h, 10, int(bool(enabled)))
+        self.fused = bool(enabled)
 
     def set_max_blocks(self, n: int) -> None:
         """Cap the exchange kernels' grid at n CTAs (0: 8 per SM)."""

@@ -13,8 +13,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs, expert_ffn_ptrs,
-                  expert_ffn_save_ptrs, pack_w13)
+from .ffn import (FFNBackwardScratch, expert_ffn_backward_gather_ptrs, expert_ffn_backward_ptrs,
+                  expert_ffn_gather_ptrs, expert_ffn_ptrs, expert_ffn_save_ptrs, pack_w13)
 from . import _lib
 from ._lib import ptr, stream_ptr
 from .layer import EPWorld, route_group_limited, route_topk
@@ -40,7 +40,7 @@ class HierMoELayer:
                  n_cap_rows: int = 0, layer_index: int = 0, router: str = "softmax",
                  n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
                  shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1,
-                 transport_params=None, transport_every: int = 50):
+                 transport_params=None, transport_every: int = 50, fused_dispatch=None):
         """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
         (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
         / ``route_scale`` and a per-expert score bias).
@@ -57,7 +57,11 @@ class HierMoELayer:
         forwards (transport.choose_transport; ``transport_params`` a
         LevelParams or params-JSON path for the runtime [P, L] hierarchy,
         default the packaged B200 fits); the choices are logged in
-        ``transport_log``."""
+        ``transport_log``.
+        ``fused_dispatch`` (default: on with one GPU): the dispatch emits
+        expert-major row indices instead of row copies and GEMM1 gathers its
+        rows from x with TMA gather4 (the backward's dW13 likewise); outputs
+        and gradients are bit-identical to the copying dispatch."""
         if inter % 128 or hidden % 256 or shared_inter % 128:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
         if grad and (inter % 256 or shared_inter % 256):
@@ -107,6 +111,15 @@ class HierMoELayer:
         self._status_ev = None
         self.strict = False           # True: synchronise and check after every step
         self.world = self.worlds[0]
+        per_rank_copies = self.dedup == "all"    # dedup rows to every rank: copies by design
+        self.fused = (gpus == 1 and not per_rank_copies) if fused_dispatch is None \
+            else bool(fused_dispatch)
+        if self.fused and (gpus != 1 or per_rank_copies):
+            raise ValueError("the fused dispatch needs every EP rank on this GPU (gpus == 1) "
+                             "and a direct transport (not dedup='all')")
+        for wd in self.worlds:
+            wd.set_fused(self.fused)
+        self._x_cur = None
         self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]
         self.grad = grad
         # router replicated on every GPU (seeded identically); experts: the
@@ -248,6 +261,7 @@ class HierMoELayer:
         """The forward's routing step: route x and, for a training layer, keep
         what the backward needs (x, its fp32 copy and the router logits are
         reused by the router backward)."""
+        self._x_cur = x
         if not self.grad:
             return self.route(x)
         xf = self.widen(x)
@@ -278,7 +292,13 @@ class HierMoELayer:
             rank = self.gpu_index * self.local + l
             x_ptr, _ = wd.buffer("xmaj", l)
             y_ptr, _ = wd.buffer("ymaj", l)
-            if self.grad:
+            if self.fused:   # GEMM1 gathers the rows from the tokens themselves
+                xs = self._x_cur[self._mb_rows(mb)]
+                expert_ffn_gather_ptrs(xs.data_ptr(), xs.shape[0], wd.buffer("xidx", l)[0],
+                                       wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
+                                       self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr,
+                                       self.g13s[mb][l].data_ptr() if self.grad else 0)
+            elif self.grad:
                 expert_ffn_save_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
                                      self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr,
                                      self.g13s[mb][l].data_ptr())
@@ -443,6 +463,14 @@ class HierMoELayer:
                     x_ptr, _ = wd.buffer("xmaj", l)
                     gy_ptr, _ = wd.buffer("gy", l)
                     gx_ptr, _ = wd.buffer("gx", l)
+                    if self.fused:
+                        xs = x[rows]
+                        expert_ffn_backward_gather_ptrs(
+                            xs.data_ptr(), xs.shape[0], wd.buffer("xidx", l)[0], wd.n_cap,
+                            p_ne + 4 * rank * self.e_loc, self.e_loc, self.w13t[l], self.w2t[l],
+                            gy_ptr, self.hidden, self.inter, self.bwd, gx_ptr, self.dw13[l],
+                            self.dw2[l], self.g13s[m][l].data_ptr(), accumulate=m > 0)
+                        continue
                     expert_ffn_backward_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc,
                                              self.e_loc, self.w13[l], self.w13t[l], self.w2t[l],
                                              gy_ptr, self.hidden, self.inter, self.bwd, gx_ptr,
