@@ -130,24 +130,9 @@ int hm_world_open_peers(hm_world* w, const void* handles);
 int hm_world_buffer(hm_world* w, int32_t kind, int32_t local_rank, void** ptr, int64_t* bytes);
 int hm_world_info(hm_world* w, int64_t* out8);
 int hm_world_barrier(hm_world* w, void* stream);
-/* Runtime options (no reference counterpart):
- *   0: 1 = TMA bulk-copy gather, 0 = register gather (default, faster on B200)
- *   1: 1 = pipelined per-GPU dedup exchange at N > 1: dispatch and combine
- *      each one kernel with per-stage flags instead of barriers (bit-identical
- *      results, measured slower); 0 = barrier-separated pack / expand /
- *      reduce / gather kernels (default)
- *   2: percent (1..99) of the pipelined kernels' CTAs that push (default 50)
- *   3: target pipeline stages per GPU (default 8; stages per source = n / L)
- *   4: grid cap (CTAs) of the exchange kernels (0 = 8 per SM, default)
- *   5: 1 = bulk-copy (TMA) pack when every destination is local (one GPU),
- *      0 = register pack (default; measured faster)
- *   6: pack store hint: 0 = st.global.L1::no_allocate (default), 1 = .cs,
- *      2 = default caching (measured 0.219 / 0.219 / 0.234 ms, Qwen3 N = 1)
- *   7: 1 = per-GPU dedup pack at N > 1 with separate warps for the NVLink
- *      pushes and the local expert-major copies, 0 = one warp per token does
- *      both (default; the split measured neutral)
- *   8: 1 = lean one-GPU pack kernel (lane-held destinations, row load issued
- *      before the position bookkeeping; default), 0 = the general pack */
+/* World options: 4 = grid cap of the exchange kernels (CTAs, 0 = 8 per SM);
+ * 10 = fused one-GPU dispatch (expert-major row indices, buffer kind 17,
+ * instead of row copies; the expert GEMM gathers the rows). */
 int hm_world_set_option(hm_world* w, int32_t option, int32_t value);
 /* per-kernel CUDA-event timing of a world's launches: segments plan, notify,
  * pack, barrier1, expand, reduce, barrier2, gather (ms of the last launch) */
@@ -227,10 +212,11 @@ int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_rows, int
                        void* y, void* g13, void* stream);
 /* Fused dispatch (one GPU): the expert-major rows are not materialised;
  * layout row r (capacity a_rows, groups of n_rows[g]) is source row idx[r]
- * of x [x_rows][hidden], loaded by GEMM1's TMA gather4.  g13 optional (the
- * pre-activations for the backward).  Replaces the copy half of the dispatch
- * the reference models as one AlltoAll row per selection (traffic.py:164-170)
- * with row indices (hm_world_set_option 10 makes hm_dispatch emit them). */
+ * of x [x_rows][hidden], loaded by GEMM1's A-gather warps (cp.async into the
+ * swizzled stage).  g13 optional (the pre-activations for the backward).
+ * Replaces the copy half of the dispatch the reference models as one
+ * AlltoAll row per selection (traffic.py:164-170) with row indices
+ * (hm_world_set_option 10 makes hm_dispatch emit them). */
 int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* idx, int64_t a_rows,
                          const int32_t* n_rows, int32_t groups, const void* w13, const void* w2,
                          int32_t hidden, int32_t inter, void* h, void* y, void* g13,
@@ -246,34 +232,24 @@ int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const int32_t* 
                                   void* dw2, int32_t accumulate, void* stream);
 /* Expert FFN backward: recomputed pre-activations, dgrad GEMMs with
  * transposed weights (w13t [g][M][2I], w2t [g][I][M]), SwiGLU backward, and
- * weight-gradient GEMMs over each expert's own token range. */
+ * weight-gradient GEMMs over each expert's own token rows (MN-major tcgen05
+ * operands read the token-major activations directly). */
 int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                            const void* w13, const void* w13t, const void* w2t, const void* gy,
                            int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
-                           void* h, void* ta, void* tb, int64_t kmax, int32_t* layout, void* gx,
-                           void* dw13, void* dw2, void* stream);
+                           void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
+                           void* stream);
 /* hm_expert_ffn_backward with g13 holding the forward's pre-activations
- * (hm_expert_ffn_save): skips the GEMM1 recompute. */
+ * (hm_expert_ffn_save): skips the GEMM1 recompute.  accumulate != 0 adds the
+ * weight grads to dw13 / dw2 (fp32 add of the stored bf16): one call per
+ * micro-batch of a layer. */
 int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
                                  int32_t groups, const void* w13t, const void* w2t,
                                  const void* gy, int32_t hidden, int32_t inter, const void* g13,
-                                 void* dh, void* dg13, void* h, void* ta, void* tb, int64_t kmax,
-                                 int32_t* layout, void* gx, void* dw13, void* dw2, void* stream);
-/* ... adding the weight grads to dw13 / dw2 (fp32 add of the stored bf16)
- * instead of overwriting them: one call per micro-batch of a layer. */
-int hm_expert_ffn_backward_saved_acc(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                     int32_t groups, const void* w13t, const void* w2t,
-                                     const void* gy, int32_t hidden, int32_t inter,
-                                     const void* g13, void* dh, void* dg13, void* h,
-                                     int32_t* layout, void* gx, void* dw13, void* dw2,
-                                     void* stream);
-/* FFN options (no reference counterpart): 0 = weight-gradient path, 0 (default)
- * = MN-major tcgen05 operands read the token-major activations directly,
- * 1 = transposed copies + K-major GEMMs (kept as the comparison path);
- * 1 = cap on the persistent GEMM grid in CTAs (0 = one per SM);
- * 2 = 1: CTA-pair (tcgen05 cta_group::2, 256 x 256 tile) kernels for the
- *     forward and data-gradient GEMMs (default), 0: single-CTA 128 x 256;
- * 3 = 1: the weight-gradient (MN-major) GEMMs on CTA pairs too. */
+                                 void* dh, void* dg13, void* h, int32_t* layout, void* gx,
+                                 void* dw13, void* dw2, int32_t accumulate, void* stream);
+/* FFN option (no reference counterpart): 1 = cap on the persistent GEMM grid
+ * in CTAs (0 = one per SM), so a concurrent exchange keeps SMs of its own. */
 int hm_ffn_set_option(int32_t option, int32_t value);
 
 /* ---------------- expert migration (K11) ------------------------------------

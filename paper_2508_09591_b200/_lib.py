@@ -68,10 +68,6 @@ _SIGS = {
                                  ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_ffn_set_option": (c_int32, [c_int32, c_int32]),
-    "hm_expert_ffn_backward_saved_acc": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p,
-                                                   c_void_p, c_void_p, c_int32, c_int32, c_void_p,
-                                                   c_void_p, c_void_p, c_void_p, c_void_p,
-                                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
     "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                    c_void_p]),
@@ -92,8 +88,8 @@ _SIGS = {
     "hm_migrate": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "hm_expert_ffn_backward": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
-                                         c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
-                                         c_void_p, c_void_p, c_void_p, c_void_p]),
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p]),
     "hm_expert_ffn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "hm_expert_ffn_save": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
@@ -109,8 +105,7 @@ _SIGS = {
     "hm_expert_ffn_backward_saved": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p,
                                                c_void_p, c_void_p, c_int32, c_int32, c_void_p,
                                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                               c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
-                                               c_void_p]),
+                                               c_void_p, c_void_p, c_int32, c_void_p]),
 }
 
 

@@ -41,19 +41,6 @@ constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr int kMaxGroups = 64;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
 int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid (0 = all SMs)
-// hm_ffn_set_option(2, v): CTA-pair (cta_group::2) kernels for modes 0 / 1 --
-// default on: 8-17 % faster per GEMM in ncu, layer fwd 3.19 -> 3.07 ms (Qwen3)
-// and 25.2 -> 23.5 ms (DSv3) at N = 1
-int g_gemm_pair = 1;
-// hm_ffn_set_option(3, 1): weight-gradient GEMMs on CTA pairs -- bit-identical
-// but measured 2x slower (DSv3 dW13 4.22 vs 2.32 ms in ncu: the per-stage
-// ready hand-off between the two CTAs serialises the pipeline), so off
-int g_wgrad_pair = 0;
-// hm_ffn_set_option(4, 1): the SwiGLU backward with 4-byte accesses (the
-// 16-byte k_swiglu_bwd_v8 is the default; bit-identical)
-int g_swiglu_scalar = 0;
-
-
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
   int groups;
@@ -878,365 +865,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
   }
 }
 
-// Weight-gradient GEMM (mode 3: out_g = A_g^T B_g over group g's token rows,
-// MN-major operands) on CTA pairs: 256 x 256 output tiles, each CTA stages
-// 128 features of A and 128 of B per 64-token k-block (4 boxes, 32 KB, 6
-// stages).  Each CTA's TMA completes on its own barrier; its MMA warp zeroes
-// the tail block's lines past the group in its own boxes, then arrives on
-// the leader's `ready` barrier (2 arrivals per stage), after which the
-// leader's MMA thread issues the pair MMA over both CTAs' shared memory.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_wgrad_pair(const __grid_constant__ CUtensorMap map_a,
-                 const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sa = smem;
-  uint8_t* sb = smem + kStages2 * kHalfBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
-  uint64_t* ready = full + kStages2;
-  uint64_t* empty = ready + kStages2;
-  uint64_t* tfull = empty + kStages2;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ TileMap tm;
-  constexpr uint32_t kIdescPairMN = kIdesc2 | (1u << 15) | (1u << 16);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  if (threadIdx.x == 0) {
-    int acc = 0, row = 0;
-    tm.ntile_n = args.N / BN;
-    for (int g = 0; g < args.groups; ++g) {
-      const int n = args.n_rows[g];
-      tm.start[g] = acc;
-      tm.row0[g] = row;
-      tm.rows[g] = n;
-      acc += args.m_out / BM2 * tm.ntile_n;
-      row += n;
-    }
-    tm.start[args.groups] = acc;
-    tm.total = acc;
-    for (int s = 0; s < kStages2; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(ready + s, 2);
-      mbar_init(empty + s, 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = cid; t < tm.total; t += ncl) {
-        int g, mt, nt;
-        tile_coords(tm, args.groups, t, g, mt, nt);
-        const int a0 = mt * BM2 + (int)rank * 128, b0 = nt * BN + (int)rank * 128;
-        const int kblocks = (tm.rows[g] + BK - 1) / BK;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
-          mbar_expect_tx(full + stage, kStageBytes2);
-          const int k0 = tm.row0[g] + kb * BK;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            tma_load_2d(sa + stage * kHalfBytes + j * 8192, &map_a, full + stage, a0 + 64 * j, k0);
-            tma_load_2d(sb + stage * kHalfBytes + j * 8192, &map_b, full + stage, b0 + 64 * j, k0);
-          }
-          if (++stage == kStages2) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int t = cid; t < tm.total; t += ncl, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      int g, mt, nt;
-      tile_coords(tm, args.groups, t, g, mt, nt);
-      if (leader && lane == 0) {
-        mbar_wait(tempty + acc, acc_phase ^ 1);
-        tc_fence_after();
-      }
-      const uint32_t d = tmem_base + acc * BN;
-      const int kblocks = (tm.rows[g] + BK - 1) / BK;
-      for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(full + stage, phase);
-        const int valid = tm.rows[g] - kb * BK;
-        const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
-        const int zend = ksteps * UK;
-        if (valid < zend) {   // this CTA's 4 boxes: lines [valid, zend)
-          const int nlines = zend - valid;
-          for (int i = lane; i < 4 * nlines * 8; i += 32) {
-            const int box = i / (nlines * 8), rem = i % (nlines * 8);
-            const int line = valid + rem / 8, chunk = rem % 8;
-            uint8_t* base = box < 2 ? sa + stage * kHalfBytes + box * 8192
-                                    : sb + stage * kHalfBytes + (box - 2) * 8192;
-            *reinterpret_cast<int4*>(base + line * 128 + chunk * 16) = make_int4(0, 0, 0, 0);
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(ready + stage, 0);
-        if (leader && lane == 0) {
-          mbar_wait(ready + stage, phase);
-          tc_fence_after();
-          const uint32_t sa0 = smem_u32(sa + stage * kHalfBytes);
-          const uint32_t sb0 = smem_u32(sb + stage * kHalfBytes);
-          for (int k = 0; k < ksteps; ++k) {
-            asm volatile(
-                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                "l"(smem_desc_mn(sa0 + k * UK * 128)), "l"(smem_desc_mn(sb0 + k * UK * 128)),
-                "r"(kIdescPairMN), "r"((kb | k) ? 1u : 0u));
-          }
-          umma_commit_pair(empty + stage);
-        }
-        __syncwarp();
-        if (++stage == kStages2) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (leader && lane == 0) umma_commit_pair(tfull + acc);
-      __syncwarp();
-    }
-  } else if (warp >= 4) {
-    const int q = warp - 4;
-    int it = 0;
-    for (int t = cid; t < tm.total; t += ncl, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      int g, mt, nt;
-      tile_coords(tm, args.groups, t, g, mt, nt);
-      mbar_wait(tfull + acc, acc_phase);
-      tc_fence_after();
-      const int r_in = mt * BM2 + (int)rank * 128 + q * 32 + lane;
-      store_tile<3>(args, tm, g, nt, r_in, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
-    }
-  }
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
-  }
-}
-
-// Per-group copies of the two MN-major operand maps with the token extent cut
-// at the group's end (tensormap.replace of global_dim[1]), so a group's tail
-// k-block arrives from TMA with the rows past the group zero-filled and no
-// CTA has to patch shared memory: the weight-gradient pair kernel below then
-// runs the forward pair kernel's pipeline unchanged.
-__global__ void k_group_maps(const __grid_constant__ CUtensorMap map_a,
-                             const __grid_constant__ CUtensorMap map_b,
-                             const int32_t* __restrict__ n_rows, int groups,
-                             CUtensorMap* __restrict__ out) {
-  if (threadIdx.x != 0) return;
-  int row = 0;
-  for (int g = 0; g < groups; ++g) {
-    row += n_rows[g];
-    out[g] = map_a;
-    out[groups + g] = map_b;
-    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 1, %1;" ::"l"(
-                     reinterpret_cast<uint64_t>(out + g)),
-                 "r"(row)
-                 : "memory");
-    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 1, %1;" ::"l"(
-                     reinterpret_cast<uint64_t>(out + groups + g)),
-                 "r"(row)
-                 : "memory");
-  }
-  asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
-}
-
-// Weight-gradient GEMM on CTA pairs with per-group tensor maps (hm_ffn_set_option(3, 2)):
-// 256 x 256 output tiles, both CTAs' TMA loads complete on the leader's
-// barrier (64 KB per stage), one MMA thread, no per-stage hand-off.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_wgrad_pair_tm(const CUtensorMap* __restrict__ gmaps, GemmArgs args) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sa = smem;
-  uint8_t* sb = smem + kStages2 * kHalfBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
-  uint64_t* empty = full + kStages2;
-  uint64_t* tfull = empty + kStages2;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ TileMap tm;
-  constexpr uint32_t kIdescPairMN = kIdesc2 | (1u << 15) | (1u << 16);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  if (threadIdx.x == 0) {
-    int acc = 0, row = 0;
-    tm.ntile_n = args.N / BN;
-    for (int g = 0; g < args.groups; ++g) {
-      const int n = args.n_rows[g];
-      tm.start[g] = acc;
-      tm.row0[g] = row;
-      tm.rows[g] = n;
-      acc += args.m_out / BM2 * tm.ntile_n;
-      row += n;
-    }
-    tm.start[args.groups] = acc;
-    tm.total = acc;
-    for (int s = 0; s < kStages2; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int g_last = -1;
-      for (int t = cid; t < tm.total; t += ncl) {
-        int g, mt, nt;
-        tile_coords(tm, args.groups, t, g, mt, nt);
-        const CUtensorMap* ma = gmaps + g;
-        const CUtensorMap* mb = gmaps + args.groups + g;
-        if (g != g_last) {   // maps written by k_group_maps: acquire in the tensormap proxy
-          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
-                           reinterpret_cast<uint64_t>(ma))
-                       : "memory");
-          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
-                           reinterpret_cast<uint64_t>(mb))
-                       : "memory");
-          g_last = g;
-        }
-        const int a0 = mt * BM2 + (int)rank * 128, b0 = nt * BN + (int)rank * 128;
-        const int kblocks = (tm.rows[g] + BK - 1) / BK;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
-          if (leader) mbar_expect_tx(full + stage, 2 * kStageBytes2);
-          const int k0 = tm.row0[g] + kb * BK;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            tma_load_2d_pair(sa + stage * kHalfBytes + j * 8192, ma, full + stage, a0 + 64 * j, k0);
-            tma_load_2d_pair(sb + stage * kHalfBytes + j * 8192, mb, full + stage, b0 + 64 * j, k0);
-          }
-          if (++stage == kStages2) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (leader && lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = cid; t < tm.total; t += ncl, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        int g, mt, nt;
-        tile_coords(tm, args.groups, t, g, mt, nt);
-        mbar_wait(tempty + acc, acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
-        const int kblocks = (tm.rows[g] + BK - 1) / BK;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(full + stage, phase);
-          tc_fence_after();
-          const uint32_t sa0 = smem_u32(sa + stage * kHalfBytes);
-          const uint32_t sb0 = smem_u32(sb + stage * kHalfBytes);
-          // tail k-block: only the k-steps that hold rows of the group (the
-          // single-CTA kernel's order, so the same bits); the rest are zero fill
-          const int valid = tm.rows[g] - kb * BK;
-          const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
-          for (int k = 0; k < ksteps; ++k) {
-            asm volatile(
-                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                "l"(smem_desc_mn(sa0 + k * UK * 128)), "l"(smem_desc_mn(sb0 + k * UK * 128)),
-                "r"(kIdescPairMN), "r"((kb | k) ? 1u : 0u));
-          }
-          umma_commit_pair(empty + stage);
-          if (++stage == kStages2) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        umma_commit_pair(tfull + acc);
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp - 4;
-    int it = 0;
-    for (int t = cid; t < tm.total; t += ncl, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      int g, mt, nt;
-      tile_coords(tm, args.groups, t, g, mt, nt);
-      mbar_wait(tfull + acc, acc_phase);
-      tc_fence_after();
-      const int r_in = mt * BM2 + (int)rank * 128 + q * 32 + lane;
-      store_tile<3>(args, tm, g, nt, r_in, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
-    }
-  }
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
-  }
-}
-
 // ---------------------------------------------------------------------------
 // expert FFN backward helpers
 // group layout for the weight-gradient GEMMs: token rows of group g are
@@ -1255,103 +883,8 @@ __global__ void k_group_layout(const int32_t* __restrict__ n_rows, int groups,
   col0[groups] = c;
 }
 
-// dst[c][col0_g + i] = src[row0_g + i][c] (bf16), zero padding columns.
-// 64x64 tiles through shared memory; each source row's destination column
-// is resolved once per tile.
-__global__ void k_transpose_groups(const __nv_bfloat16* __restrict__ src, int C,
-                                   const int32_t* __restrict__ n_rows, int groups,
-                                   const int32_t* __restrict__ row0, const int32_t* __restrict__ col0,
-                                   __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
-  __shared__ __nv_bfloat16 tile[64][66];
-  __shared__ int dcol[64];
-  const int total = row0[groups];
-  const int r_base = blockIdx.y * 64, c_base = blockIdx.x * 64;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  if (r_base < total) {
-    if (tid < 64) {
-      const int r = r_base + tid;
-      int g = 0;
-      if (r < total)
-        while (g + 1 < groups && row0[g + 1] <= r) ++g;
-      dcol[tid] = r < total ? col0[g] + (r - row0[g]) : -1;
-    }
-    // coalesced loads: each thread moves bf16 pairs
-    for (int i = threadIdx.y; i < 64; i += blockDim.y) {
-      const int r = r_base + i;
-      const int j = 2 * threadIdx.x;
-      const int c = c_base + j;
-      __nv_bfloat162 v = __floats2bfloat162_rn(0.f, 0.f);
-      if (r < total && c + 1 < C)
-        v = *reinterpret_cast<const __nv_bfloat162*>(src + (int64_t)r * C + c);
-      else if (r < total && c < C)
-        v.x = src[(int64_t)r * C + c];
-      tile[i][j] = v.x;
-      tile[i][j + 1] = v.y;
-    }
-    __syncthreads();
-    // each lane writes two consecutive source rows: one 4-B store when they
-    // land in adjacent destination columns (same group), else two 2-B stores
-    for (int j = threadIdx.y; j < 64; j += blockDim.y) {
-      const int c = c_base + j;
-      if (c >= C) continue;
-      const int i = 2 * threadIdx.x;
-      const int d0 = dcol[i], d1 = dcol[i + 1];
-      __nv_bfloat16* row = dst + (int64_t)c * ld_dst;
-      if (d0 >= 0 && d1 == d0 + 1 && (d0 & 1) == 0) {
-        __nv_bfloat162 v;
-        v.x = tile[i][j];
-        v.y = tile[i + 1][j];
-        *reinterpret_cast<__nv_bfloat162*>(row + d0) = v;
-      } else {
-        if (d0 >= 0) row[d0] = tile[i][j];
-        if (d1 >= 0) row[d1] = tile[i + 1][j];
-      }
-    }
-  }
-  // padding columns of every group (first row-tile blocks only)
-  if (blockIdx.y == 0) {
-    for (int g = 0; g < groups; ++g) {
-      const int pad0 = col0[g] + n_rows[g], pad1 = col0[g + 1];
-      if (pad0 >= pad1) continue;
-      for (int j = threadIdx.y; j < 64; j += blockDim.y) {
-        const int c = c_base + j;
-        if (c >= C) continue;
-        for (int k = pad0 + threadIdx.x; k < pad1; k += blockDim.x)
-          dst[(int64_t)c * ld_dst + k] = __float2bfloat16(0.f);
-      }
-    }
-  }
-}
-
 // SwiGLU backward on 128-column gate/up interleaved pre-activations:
-// h = silu(a) u;  da = dh u silu'(a);  du = dh silu(a).  Two columns per thread.
-__global__ void k_swiglu_bwd(const __nv_bfloat16* __restrict__ g13, const __nv_bfloat16* __restrict__ dh,
-                             const int32_t* __restrict__ row0, int groups, int inter,
-                             __nv_bfloat16* __restrict__ dg13, __nv_bfloat16* __restrict__ h) {
-  const int rows = row0[groups];
-  const int half = inter / 2;
-  const int64_t n = (int64_t)rows * half;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / half);
-    const int j = 2 * (int)(i - (int64_t)r * half);
-    const int b = j >> 7, c = j & 127;
-    const int64_t ga = (int64_t)r * 2 * inter + 256 * b + c, gu = ga + 128;
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g13 + ga));
-    const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g13 + gu));
-    const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dh + (int64_t)r * inter + j));
-    const float s0 = 1.f / (1.f + __expf(-a.x)), s1 = 1.f / (1.f + __expf(-a.y));
-    const float si0 = a.x * s0, si1 = a.y * s1;
-    *reinterpret_cast<__nv_bfloat162*>(h + (int64_t)r * inter + j) = __floats2bfloat162_rn(si0 * u.x, si1 * u.y);
-    *reinterpret_cast<__nv_bfloat162*>(dg13 + gu) = __floats2bfloat162_rn(d.x * si0, d.y * si1);
-    *reinterpret_cast<__nv_bfloat162*>(dg13 + ga) =
-        __floats2bfloat162_rn(d.x * u.x * s0 * (1.f + a.x * (1.f - s0)),
-                              d.y * u.y * s1 * (1.f + a.y * (1.f - s1)));
-  }
-}
-
-// The same SwiGLU backward with 16-byte accesses: eight columns of one
-// 128-column block per thread (inter % 128 == 0), identical per-element math.
+// h = silu(a) u;  da = dh u silu'(a);  du = dh silu(a).
 __global__ void __launch_bounds__(256) k_swiglu_bwd_v8(const __nv_bfloat16* __restrict__ g13,
                                                        const __nv_bfloat16* __restrict__ dh,
                                                        const int32_t* __restrict__ row0, int groups,
@@ -1457,8 +990,9 @@ int make_map_mn(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) 
 }
 
 // out[g] ([m_out][N], ld_out) = A_g^T B_g over group g's token rows of
-// A [a_rows][m_out] and B [a_rows][N] (kMode 3)
-// b_idx: B's token rows are gathered from b [b_src_rows][N] (fused dispatch)
+// A [a_rows][m_out] and B [a_rows][N] (kMode 3, MN-major operands straight
+// from the token-major activations).  b_idx: B's token rows are gathered
+// from b [b_src_rows][N] (fused dispatch)
 int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
                       const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
                       cudaStream_t s, int accumulate = 0, const int32_t* b_idx = nullptr,
@@ -1466,8 +1000,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
   HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
-  HM_CHECK_ARG(!b_idx || (b_src_rows >= 1 && g_wgrad_pair == 0),
-               "wgrad gemm: gathered B needs source rows and the single-CTA kernel");
+  HM_CHECK_ARG(!b_idx || b_src_rows >= 1, "wgrad gemm: gathered B needs its source rows");
   CUtensorMap ma, mb;
   int st = make_map_mn(&ma, a, (uint64_t)a_rows, (uint64_t)m_out);
   if (st) return st;
@@ -1495,63 +1028,37 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
-  if (g_wgrad_pair == 2 && m_out % BM2 == 0) {
-    // per-group maps live in a ring of slots so that GEMMs in flight on
-    // several streams (micro-batches) never share one
-    constexpr int kRing = 16;
-    static CUtensorMap* ring = nullptr;   // [kRing][2][kMaxGroups] (device)
-    static std::atomic<unsigned> next{0};
-    if (!ring) HM_CUDA(cudaMalloc(&ring, (size_t)kRing * 2 * kMaxGroups * sizeof(CUtensorMap)));
-    CUtensorMap* gmaps = ring + (size_t)(next++ % kRing) * 2 * kMaxGroups;
-    k_group_maps<<<1, 32, 0, s>>>(ma, mb, n_rows, groups, gmaps);
-    HM_LAUNCHED();
-    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
-    HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair_tm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem2));
-    k_wgrad_pair_tm<<<sms & ~1, kThreads, smem2, s>>>(gmaps, args);
-    HM_LAUNCHED();
-    return 0;
-  }
-  if (g_wgrad_pair == 1 && m_out % BM2 == 0) {
-    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
-    HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem2));
-    k_wgrad_pair<<<sms & ~1, kThreads, smem2, s>>>(ma, mb, args);
-    HM_LAUNCHED();
-    return 0;
-  }
   if (b_idx) {
     HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_grouped_gemm<3, true><<<sms, kThreads + kGatherThreads, smem, s>>>(ma, mb, args);
-    HM_LAUNCHED();
-    return 0;
+  } else {
+    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_grouped_gemm<3><<<sms, kThreads, smem, s>>>(ma, mb, args);
   }
-  HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-  k_grouped_gemm<3><<<sms, kThreads, smem, s>>>(ma, mb, args);
   HM_LAUNCHED();
   return 0;
 }
 
+// out[rows of group g] = A[rows of g] . B_g^T on CTA pairs (256 x 256 tiles).
 // a_idx: the A rows are gathered from a [a_src_rows][K] by row index (fused
-// dispatch, CTA-pair forward kernels only); a_rows is then the layout's capacity
+// dispatch); a_rows is then the layout's capacity
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
-                cudaStream_t s, int wgrad_m_out = 0, int64_t b_rows = 0, void* out2 = nullptr,
-                const int32_t* a_idx = nullptr, int64_t a_src_rows = 0) {
+                cudaStream_t s, void* out2 = nullptr, const int32_t* a_idx = nullptr,
+                int64_t a_src_rows = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
-  HM_CHECK_ARG(!a_idx || (a_src_rows >= 1 && !wgrad_m_out),
-               "grouped gemm: gathered A needs source rows (forward modes)");
+  HM_CHECK_ARG(!a_idx || a_src_rows >= 1, "grouped gemm: gathered A needs its source rows");
   CUtensorMap ma, mb;
-  int st = make_map(&ma, a, (uint64_t)(a_idx ? a_src_rows : a_rows), (uint64_t)K, BM);
+  int st = make_map(&ma, a, (uint64_t)(a_idx ? a_src_rows : a_rows), (uint64_t)K, 128);
   if (st) return st;
-  st = make_map(&mb, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, BN);
+  st = make_map(&mb, b, (uint64_t)groups * N, (uint64_t)K, 128);
   if (st) return st;
   GemmArgs args;
-  args.m_out = wgrad_m_out;
+  args.m_out = 0;
   args.n_rows = n_rows;
   args.groups = groups;
   args.N = N;
@@ -1566,86 +1073,34 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.b_idx = nullptr;
   args.g_src = reinterpret_cast<const uint8_t*>(a);
   args.g_ld = (int64_t)K * 2;
-  const size_t smem = kStages * kStageBytes + 1024 + 256;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
-  if (!wgrad_m_out && (g_gemm_pair || a_idx)) {   // 256 x 256 tiles on CTA pairs
-    CUtensorMap mb2;
-    st = make_map(&mb2, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, 128);
-    if (st) return st;
-    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
-    const int grid = sms & ~1;
-    if (a_idx) {   // fused dispatch: A rows gathered by warps 8-11
-      const int thr = kThreads + kGatherThreads;
-      if (swiglu) {
-        HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<1, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        k_grouped_gemm_pair<1, true><<<grid, thr, smem2, s>>>(ma, mb2, args);
-      } else {
-        HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<0, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        k_grouped_gemm_pair<0, true><<<grid, thr, smem2, s>>>(ma, mb2, args);
-      }
-    } else if (swiglu) {
-      HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      k_grouped_gemm_pair<1><<<grid, kThreads, smem2, s>>>(ma, mb2, args);
-    } else {
-      HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<0>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      k_grouped_gemm_pair<0><<<grid, kThreads, smem2, s>>>(ma, mb2, args);
-    }
-    HM_LAUNCHED();
-    return 0;
-  }
-  if (wgrad_m_out && g_gemm_pair && wgrad_m_out % BM2 == 0) {
-    CUtensorMap mb2;
-    st = make_map(&mb2, b, (uint64_t)(b_rows ? b_rows : (int64_t)groups * N), (uint64_t)K, 128);
-    if (st) return st;
-    const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
-    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm_pair<2>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    k_grouped_gemm_pair<2><<<sms & ~1, kThreads, smem2, s>>>(ma, mb2, args);
-    HM_LAUNCHED();
-    return 0;
-  }
-  if (wgrad_m_out) {
-    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_grouped_gemm<2><<<sms, kThreads, smem, s>>>(ma, mb, args);
-  } else if (swiglu) {
-    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_grouped_gemm<1><<<sms, kThreads, smem, s>>>(ma, mb, args);
-  } else {
-    HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_grouped_gemm<0><<<sms, kThreads, smem, s>>>(ma, mb, args);
-  }
-  HM_LAUNCHED();
-  return 0;
+  const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
+  const int grid = sms & ~1;
+  auto run = [&](auto kern, int threads) -> int {
+    HM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    kern<<<grid, threads, smem2, s>>>(ma, mb, args);
+    return launch_status();
+  };
+  const int thr_g = kThreads + kGatherThreads;   // + the A-gather warps
+  if (a_idx) return swiglu ? run(k_grouped_gemm_pair<1, true>, thr_g)
+                           : run(k_grouped_gemm_pair<0, true>, thr_g);
+  return swiglu ? run(k_grouped_gemm_pair<1>, kThreads) : run(k_grouped_gemm_pair<0>, kThreads);
 }
-
-int g_wgrad_transposed = 0;   // hm_ffn_set_option(0, 1): transposes + K-major wgrad
 
 }  // namespace
 
-// FFN options: 0 = weight-gradient path (0: MN-major tcgen05 operands read the
-// token-major activations directly, default; 1: transposed copies + K-major);
-// 1 = cap on the persistent GEMM grid (CTAs; 0 = one per SM, default) so
-// concurrent exchange kernels keep SMs of their own; 2 = CTA-pair
-// (cta_group::2, 256 x 256 tiles) kernels for the forward / data-gradient GEMMs;
-// 3 = weight-gradient pair kernels (0 off, 1 / 2 variants); 4 = scalar SwiGLU backward
+// FFN option (no reference counterpart): 1 = cap on the persistent GEMM grid
+// (CTAs; 0 = one per SM, default) so concurrent exchange kernels keep SMs of
+// their own.  Options 0 and 2-4 selected measured-slower variants (transposed
+// K-major weight gradients, single-CTA forward GEMMs, CTA-pair weight
+// gradients, 4-byte SwiGLU backward) that round 2 removed; they are rejected.
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option >= 0 && option <= 4, "hm_ffn_set_option: unknown option %d", option);
-  if (option == 0) g_wgrad_transposed = value != 0;
-  if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
-  if (option == 2) g_gemm_pair = value != 0;
-  if (option == 3) g_wgrad_pair = value < 0 ? 0 : (value > 2 ? 2 : value);
-  if (option == 4) g_swiglu_scalar = value != 0;
+  HM_CHECK_ARG(option == 1, "hm_ffn_set_option: unknown option %d", option);
+  g_gemm_ctas = value > 0 ? value : 0;
   return 0;
 }
 
@@ -1680,39 +1135,89 @@ HM_API int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_ro
                               int32_t inter, void* h, void* y, void* g13, void* stream) {
   HM_CHECK_ARG(g13, "hm_expert_ffn_save: null g13");
   int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
-                       (cudaStream_t)stream, 0, 0, g13);
+                       (cudaStream_t)stream, g13);
   if (st) return st;
   return launch_gemm(h, a_rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
                      (cudaStream_t)stream);
 }
 
-// Expert SwiGLU FFN backward (tcgen05 GEMMs + elementwise/transposes):
-//   G13 = X W13^T (recomputed pre-activations), dH = gY W2 (via W2^T),
-//   dG13 = swiglu'(G13, dH), H = swiglu(G13), gX = dG13 W13 (via W13^T),
-//   dW2 = gY^T H, dW13 = dG13^T X  (weight-gradient GEMMs over each expert's
-//   own token range, K padded to 64).
+// Expert SwiGLU FFN backward (tcgen05 GEMMs + SwiGLU backward):
+//   G13 = X W13^T (recomputed pre-activations unless saved), dH = gY W2 (via
+//   W2^T), dG13 = swiglu'(G13, dH), H = swiglu(G13), gX = dG13 W13 (via
+//   W13^T), dW2 = gY^T H, dW13 = dG13^T X (weight-gradient GEMMs over each
+//   expert's own token rows, MN-major operands; x_idx: X's rows gathered).
 // Buffers (rows = a_rows capacity): g13, dg13 [rows, 2I]; dh, h [rows, I];
-// ta [max(M, 2I), kmax], tb [max(M, I), kmax] with kmax >= rows + 64*groups;
 // layout: 2*(groups+1) int32 scratch.  Outputs: gx [rows, M],
-// dw13 [groups][2I][M], dw2 [groups][M][I].
+// dw13 [groups][2I][M], dw2 [groups][M][I] (accumulate: added to).
 static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                         const void* w13, const void* w13t, const void* w2t, const void* gy,
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
-                        void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
-                        void* gx, void* dw13, void* dw2, void* stream, int accumulate = 0,
-                        const int32_t* x_idx = nullptr, int64_t x_rows = 0);
+                        void* dg13, void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
+                        void* stream, int accumulate = 0, const int32_t* x_idx = nullptr,
+                        int64_t x_rows = 0) {
+  cudaStream_t s = (cudaStream_t)stream;
+  HM_CHECK_ARG(!x_idx || g13_saved,
+               "ffn backward: gathered activations need the saved pre-activations");
+  const int M = hidden, I = inter;
+  int st;
+  // gate/up pre-activations (recomputed unless the forward saved them), then dH
+  if (!g13_saved &&
+      (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I, nullptr, s)))
+    return st;
+  if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s))) return st;
+  int32_t* row0 = layout;
+  int32_t* col0 = layout + groups + 1;
+  k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, row0, col0);
+  HM_LAUNCHED();
+  HM_CHECK_ARG(I % 128 == 0, "ffn backward: inter must be a multiple of 128");
+  k_swiglu_bwd_v8<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
+                                            row0, groups, I, (__nv_bfloat16*)dg13,
+                                            (__nv_bfloat16*)h);
+  HM_LAUNCHED();
+  // data gradient
+  if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s))) return st;
+  // weight gradients straight from the token-major activations (MN-major
+  // tcgen05 operands), reduction over each expert's own rows
+  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate)))
+    return st;
+  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate,
+                           x_idx, x_rows);
+}
+
+HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                  int32_t groups, const void* w13, const void* w13t,
+                                  const void* w2t, const void* gy, int32_t hidden, int32_t inter,
+                                  void* g13, void* dh, void* dg13, void* h, int32_t* layout,
+                                  void* gx, void* dw13, void* dw2, void* stream) {
+  return ffn_backward(x, a_rows, n_rows, groups, w13, w13t, w2t, gy, hidden, inter, g13, 0, dh,
+                      dg13, h, layout, gx, dw13, dw2, stream);
+}
+
+// ... with g13 holding the forward's pre-activations (hm_expert_ffn_save): no
+// GEMM1 recompute; accumulate != 0 adds the weight grads to dw13 / dw2
+// (micro-batched layers: one call per micro-batch)
+HM_API int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
+                                        int32_t groups, const void* w13t, const void* w2t,
+                                        const void* gy, int32_t hidden, int32_t inter,
+                                        const void* g13, void* dh, void* dg13, void* h,
+                                        int32_t* layout, void* gx, void* dw13, void* dw2,
+                                        int32_t accumulate, void* stream) {
+  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
+                      const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
+                      accumulate);
+}
 
 // Fused dispatch: the expert-major rows are never materialised -- row r of
 // the expert-major layout (capacity a_rows, groups of n_rows[g]) is source
 // row idx[r] of x [x_rows][hidden] (the tokens themselves), loaded by GEMM1's
-// TMA gather4.  g13 (optional) keeps the pre-activations for the backward.
+// A-gather warps.  g13 (optional) keeps the pre-activations for the backward.
 HM_API int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* idx, int64_t a_rows,
                                 const int32_t* n_rows, int32_t groups, const void* w13,
                                 const void* w2, int32_t hidden, int32_t inter, void* h, void* y,
                                 void* g13, void* stream) {
   HM_CHECK_ARG(x && idx, "hm_expert_ffn_gather: null argument");
   int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
-                       (cudaStream_t)stream, 0, 0, g13, idx, x_rows);
+                       (cudaStream_t)stream, g13, idx, x_rows);
   if (st) return st;
   return launch_gemm(h, a_rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
                      (cudaStream_t)stream);
@@ -1728,103 +1233,6 @@ HM_API int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const in
                                          void* dw13, void* dw2, int32_t accumulate, void* stream) {
   HM_CHECK_ARG(x && idx, "hm_expert_ffn_backward_gather: null argument");
   return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
-                      const_cast<void*>(g13), 1, dh, dg13, h, nullptr, nullptr, 0, layout, gx,
-                      dw13, dw2, stream, accumulate, idx, x_rows);
-}
-
-HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                  int32_t groups, const void* w13, const void* w13t,
-                                  const void* w2t, const void* gy, int32_t hidden, int32_t inter,
-                                  void* g13, void* dh, void* dg13, void* h, void* ta, void* tb,
-                                  int64_t kmax, int32_t* layout, void* gx, void* dw13, void* dw2,
-                                  void* stream) {
-  return ffn_backward(x, a_rows, n_rows, groups, w13, w13t, w2t, gy, hidden, inter, g13, 0, dh,
-                      dg13, h, ta, tb, kmax, layout, gx, dw13, dw2, stream);
-}
-
-// ... with g13 already holding the forward's pre-activations
-// (hm_expert_ffn_save): no GEMM1 recompute
-HM_API int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                        int32_t groups, const void* w13t, const void* w2t,
-                                        const void* gy, int32_t hidden, int32_t inter,
-                                        const void* g13, void* dh, void* dg13, void* h, void* ta,
-                                        void* tb, int64_t kmax, int32_t* layout, void* gx,
-                                        void* dw13, void* dw2, void* stream) {
-  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
-                      const_cast<void*>(g13), 1, dh, dg13, h, ta, tb, kmax, layout, gx, dw13, dw2,
-                      stream);
-}
-
-// ... and the weight grads added to dw13 / dw2 instead of overwriting them
-// (micro-batched layers: one call per micro-batch)
-HM_API int hm_expert_ffn_backward_saved_acc(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                            int32_t groups, const void* w13t, const void* w2t,
-                                            const void* gy, int32_t hidden, int32_t inter,
-                                            const void* g13, void* dh, void* dg13, void* h,
-                                            int32_t* layout, void* gx, void* dw13, void* dw2,
-                                            void* stream) {
-  HM_CHECK_ARG(!g_wgrad_transposed, "accumulating weight grads need the MN-major path");
-  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
-                      const_cast<void*>(g13), 1, dh, dg13, h, nullptr, nullptr, 0, layout, gx,
-                      dw13, dw2, stream, 1);
-}
-
-static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
-                        const void* w13, const void* w13t, const void* w2t, const void* gy,
-                        int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
-                        void* dg13, void* h, void* ta, void* tb, int64_t kmax, int32_t* layout,
-                        void* gx, void* dw13, void* dw2, void* stream, int accumulate,
-                        const int32_t* x_idx, int64_t x_rows) {
-  cudaStream_t s = (cudaStream_t)stream;
-  HM_CHECK_ARG(!x_idx || (g13_saved && !g_wgrad_transposed),
-               "ffn backward: gathered activations need the saved pre-activations and the "
-               "MN-major weight gradients");
-  if (g_wgrad_transposed)
-  HM_CHECK_ARG(kmax % BK == 0 && kmax >= a_rows + (int64_t)BK * groups,
-               "hm_expert_ffn_backward: kmax must cover the padded rows");
-  const int M = hidden, I = inter;
-  int st;
-  // gate/up pre-activations (recomputed unless the forward saved them), then dH
-  if (!g13_saved &&
-      (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I, nullptr, s)))
-    return st;
-  if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s))) return st;
-  int32_t* row0 = layout;
-  int32_t* col0 = layout + groups + 1;
-  k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, row0, col0);
-  HM_LAUNCHED();
-  if (I % 128 == 0 && !g_swiglu_scalar)
-    k_swiglu_bwd_v8<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
-                                              row0, groups, I, (__nv_bfloat16*)dg13,
-                                              (__nv_bfloat16*)h);
-  else
-    k_swiglu_bwd<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
-                                           row0, groups, I, (__nv_bfloat16*)dg13,
-                                           (__nv_bfloat16*)h);
-  HM_LAUNCHED();
-  // data gradient
-  if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s))) return st;
-  // weight gradients straight from the token-major activations (MN-major
-  // tcgen05 operands), reduction over each expert's own rows
-  if (g_wgrad_transposed) {   // reference path: transposed copies + K-major GEMMs
-    auto transpose = [&](const void* src, int C, void* dst) -> int {
-      dim3 grid((C + 63) / 64, (unsigned)((a_rows + 63) / 64));
-      k_transpose_groups<<<grid, dim3(32, 8), 0, s>>>((const __nv_bfloat16*)src, C, n_rows,
-                                                      groups, row0, col0, (__nv_bfloat16*)dst,
-                                                      kmax);
-      return launch_status();
-    };
-    if ((st = transpose(gy, M, ta))) return st;
-    if ((st = transpose(h, I, tb))) return st;
-    if ((st = launch_gemm(ta, M, tb, groups, n_rows, I, (int)kmax, 0, dw2, I, nullptr, s, M, I)))
-      return st;
-    if ((st = transpose(dg13, 2 * I, ta))) return st;
-    if ((st = transpose(x, M, tb))) return st;
-    return launch_gemm(ta, 2 * I, tb, groups, n_rows, M, (int)kmax, 0, dw13, M, nullptr, s,
-                       2 * I, M);
-  }
-  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate)))
-    return st;
-  return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate,
-                           x_idx, x_rows);
+                      const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
+                      accumulate, idx, x_rows);
 }

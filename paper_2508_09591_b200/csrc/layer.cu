@@ -42,8 +42,6 @@ namespace {
 using namespace hm;
 
 constexpr int kMaxRanks = 64;
-constexpr int kMaxJ = 8;      // pipeline stages per source rank (mode 3, N > 1)
-constexpr int kStages = 8;    // target pipeline stages per GPU (L * J)
 constexpr int kMaxK = 16;
 constexpr int kChunk = 256;      // tokens per plan chunk (8 warps x 32)
 constexpr int kPlanWarps = kChunk / 32;
@@ -81,14 +79,6 @@ struct WorldDev {
   float* gw[kMaxRanks];       // backward: gate grads of dedup picks [R_cap][K], or null
   int32_t* counts[kMaxRanks];                 // count matrix [G][G+E] on d's GPU
   unsigned long long* flags[kMaxRanks];       // per GPU q: flags[q][0..P)
-  // pipelined mode-3 exchange (indexed by the first rank of a GPU, q * L):
-  // cpre[G src][kMaxJ + 1] = rows of src for this GPU before each stage
-  // boundary (written by src's GPU), dflag[G src][kMaxJ] = dispatch stage j
-  // of src delivered, rflag[P * L][kMaxJ] = returns of stage j for local
-  // source (dest GPU * L + s_loc) delivered
-  int32_t* cpre[kMaxRanks];
-  unsigned long long* dflag[kMaxRanks];
-  unsigned long long* rflag[kMaxRanks];
   // barrier epoch counter (this GPU, device memory): advanced by the device
   // barriers themselves, so a step is replayable from a CUDA graph
   unsigned long long* epoch_ctr;
@@ -692,13 +682,10 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
                                                  Offsets* __restrict__ offs,
                                                  int32_t* __restrict__ eoff,
                                                  int32_t* __restrict__ n_e, int mode,
-                                                 int* __restrict__ status,
-                                                 int J, int32_t* __restrict__ pipe, int pipe_len,
-                                                 int stage_cnt) {
+                                                 int* __restrict__ status, int stage_cnt) {
   const WorldDev& w = *wp;
   const int G = w.G, E = w.E, L = w.L, P = w.P, gp = w.p, E_loc = w.E_loc;
   const int C = G + E + P, CG = G + E;
-  for (int i = threadIdx.x; i < pipe_len; i += blockDim.x) pipe[i] = 0;
   for (int i = threadIdx.x; i < L * C; i += blockDim.x) {
     const int s_loc = i / C, c = i - s_loc * C;
     int32_t* col = chunk_cnt + (int64_t)s_loc * nchunks * C + c;
@@ -715,15 +702,6 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
     }
     const int sg = gp * L + s_loc;
     for (int q = 0; q < P; ++q) w.counts[q * L][(int64_t)sg * C + c] = run;
-    // pipelined mode 3: this source's row prefix for GPU q at every stage
-    // boundary, stored on q (receive rows of stage j = [cpre[j], cpre[j+1]))
-    if (J > 0 && c >= CG && c - CG != gp) {
-      const int q = c - CG;
-      for (int j = 0; j <= J; ++j) {
-        const int b = j * nchunks / J;
-        w.cpre[q * L][sg * (kMaxJ + 1) + j] = b < nchunks ? col[(int64_t)b * C] : run;
-      }
-    }
   }
   cta_barrier(w, status);
   // shared memory: s_n[E] per-slot totals, s_eb[E] expert-major bases,
@@ -837,22 +815,6 @@ __device__ __forceinline__ int4 ld_cg_v4(const int4* p) {
                : "l"(p));
   return r;
 }
-__device__ __forceinline__ void st_cs_v4(int4* p, int4 v) {
-  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w));
-}
-__device__ __forceinline__ void st_wb_v4(int4* p, int4 v) {
-  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w));
-}
-// pack store flavour (hm_world_set_option 6): 0 L1::no_allocate, 1 .cs, 2 default
-template <int SH>
-__device__ __forceinline__ void st_pack_v4(int4* p, int4 v);
-__device__ __forceinline__ void st_na_v4(int4* p, int4 v);
-template <>
-__device__ __forceinline__ void st_pack_v4<1>(int4* p, int4 v) { st_cs_v4(p, v); }
-template <>
-__device__ __forceinline__ void st_pack_v4<2>(int4* p, int4 v) { st_wb_v4(p, v); }
 __device__ __forceinline__ void st_na_v4(int4* p, int4 v) {
   asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w));
@@ -875,10 +837,6 @@ __device__ __forceinline__ int64_t spread_index(int64_t i, int64_t n) {
 // row to every place it goes (direct expert-major rows for picks on this GPU
 // in modes 0/2/3, one row per hit remote GPU in mode 3, one row per hit
 // destination rank in modes 1/2) with its per-row metadata
-// PART: 0 = everything, 1 = the same-GPU expert-major rows only, 2 = the
-// remote-GPU rows (mode 3) only -- the split lets NVLink pushes and local HBM
-// copies run in different warps instead of alternating inside each warp
-template <int SH = 0, int PART = 0>
 __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lane,
                                            const uint8_t* __restrict__ x,
                                            const int32_t* __restrict__ ids,
@@ -912,7 +870,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
         my_ep = -1;
       }
     }
-    if (PART != 2) epos_out[t * w.K + lane] = my_ep;
+    epos_out[t * w.K + lane] = my_ep;
   }
   unsigned long long hit = hitmask[t];
   // destinations (dedup) or picks (raw) this row goes to
@@ -920,7 +878,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
   int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
   uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
   // direct expert-major rows: every pick (mode 0) or picks on this GPU (modes 2, 3)
-  if (mode != 1 && PART != 2) {
+  if (mode != 1) {
     for (int k = 0; k < w.K; ++k) {
       int e = __shfl_sync(0xffffffffu, my_e, k);
       int ep = __shfl_sync(0xffffffffu, my_ep, k);
@@ -934,7 +892,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
   }
   // mode 3: one row per (token, other GPU hit); meta carries, per pick on
   // that GPU, its local rank's expert-major row (l * N_cap + epos)
-  if (mode == 3 && PART != 1) {
+  if (mode == 3) {
     for (int q = 0; q < w.P; ++q) {
       if (q == w.p) continue;
       if (!((hit >> (q * w.L)) & gmask)) {
@@ -1012,18 +970,12 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) {
-          if constexpr (SH == 0)
-            st_na_v4(dst + v, buf[u]);
-          else
-            st_pack_v4<SH>(dst + v, buf[u]);
-        }
+        if (v < nvec) st_na_v4(dst + v, buf[u]);
       }
     }
   }
 }
 
-template <int SH>
 __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               const uint8_t* __restrict__ x,
                                               const int32_t* __restrict__ ids,
@@ -1038,30 +990,17 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               int32_t* __restrict__ epos_out,
                                               const int32_t* __restrict__ rank_g,
                                               int32_t* __restrict__ gpos_g,
-                                              int* __restrict__ status, int split) {
+                                              int* __restrict__ status) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t T = (int64_t)w.L * w.T_r;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  if (split) {   // odd warps push the remote-GPU rows, even warps write the local ones
-    const int64_t nh = nw >> 1;
-    if (warp & 1) {
-      for (int64_t t = warp >> 1; t < T; t += nh)
-        pack_token<SH, 2>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs,
-                          eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
-    } else {
-      for (int64_t t = warp >> 1; t < T; t += nh)
-        pack_token<SH, 1>(w, t, lane, x, ids, wts, chunk_off, rank_d, rank_e, hitmask, offs,
-                          eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g, status);
-    }
-    return;
-  }
   // across GPUs, tokens are walked in a spread order (like the reducers) so the
   // concurrent warps' NVLink stores land all over the peers' receive buffers
   const bool spread = mode == 3 && w.P > 1;
   for (int64_t i = warp; i < T; i += nw)
-    pack_token<SH>(w, spread ? spread_index(i, T) : i, lane, x, ids, wts, chunk_off, rank_d,
+    pack_token(w, spread ? spread_index(i, T) : i, lane, x, ids, wts, chunk_off, rank_d,
                    rank_e, hitmask, offs, eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g,
                    status);
 }
@@ -1403,64 +1342,6 @@ __global__ void __launch_bounds__(256, 3) k_reduce(const WorldDev* __restrict__ 
 
 // gather (source side).  dedup: out[t] = sum over hit destinations d
 // (ascending) of comb[d][gpos[t,d]]; raw: out[t] = sum_k w_k * ymaj[dest][epos].
-// Source rows of token t in summation order (shared by both gather kernels).
-__device__ __forceinline__ int gather_sources(const WorldDev& w, int64_t t, const int32_t* ids,
-                                              const float* wts, const unsigned long long* hitmask,
-                                              const int32_t* gpos, const int32_t* epos, int mode,
-                                              int grad, int push, const Offsets* offs,
-                                              const int32_t* gpos_g, const uint8_t** srcs,
-                                              float* ws) {
-  int n = 0;
-  // weighted expert rows: every pick (mode 0) or picks on this GPU (modes 2, 3), k order
-  if (mode != 1) {
-    for (int k = 0; k < w.K; ++k) {
-      int e = ids[t * w.K + k];
-      int ep = epos[t * w.K + k];
-      if (e < 0 || ep < 0) continue;
-      const int d = rank_of_slot(w, e);
-      if (mode >= 2 && d / w.L != w.p) continue;
-      srcs[n] = (grad ? w.gx[d] : w.ymaj[d]) + (int64_t)ep * w.row_bytes;
-      ws[n] = grad ? 1.f : wts[t * w.K + k];
-      ++n;
-    }
-  }
-  // mode 3: pre-reduced rows of the other GPUs hit, pushed into our return buffer
-  if (mode == 3) {
-    const unsigned long long hit = hitmask[t];
-    const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
-    const int s_loc = (int)(t / w.T_r);
-    for (int q = 0; q < w.P; ++q) {
-      if (q == w.p || !((hit >> (q * w.L)) & gmask)) continue;
-      const int g = gpos_g[t * w.P + q];
-      if (g < 0) continue;
-      const int64_t pos = g - offs->off_g[s_loc][q];
-      srcs[n] = w.ret_g[w.p * w.L + s_loc] + ((int64_t)q * w.T_r + pos) * w.row_bytes;
-      ws[n] = 1.f;
-      ++n;
-    }
-  }
-  // pre-reduced partial rows of dedup destinations, ascending rank
-  if (mode == 1 || mode == 2) {
-    unsigned long long hit = hitmask[t];
-    for (int d = 0; d < w.G; ++d) {
-      if (!((hit >> d) & 1ull)) continue;
-      if (mode == 2 && d / w.L == w.p) continue;
-      int g = gpos[t * w.G + d];
-      if (g < 0 || g >= w.R_cap) continue;
-      if (push) {
-        const int s_loc = (int)(t / w.T_r);
-        const int64_t pos = g - offs->off[s_loc][d];
-        srcs[n] = w.ret[w.p * w.L + s_loc] + ((int64_t)d * w.T_r + pos) * w.row_bytes;
-      } else {
-        srcs[n] = w.comb[d] + (int64_t)g * w.row_bytes;
-      }
-      ws[n] = 1.f;
-      ++n;
-    }
-  }
-  return n;
-}
-
 // Warp-cooperative gather_sources: lane k resolves pick k, lane q GPU q, lane
 // d rank d, in one round of loads; ballots compact them into the warp's
 // shared-memory source table in the same (summation) order.  Returns n
@@ -1554,8 +1435,8 @@ __device__ __forceinline__ int gather_sources_warp(const WorldDev& w, int64_t t,
 
 constexpr int kMaxSrc = kMaxRanks > kMaxK ? kMaxRanks : kMaxK;
 
-template <typename T, int VPL, int SU = kSu>
-__global__ void __launch_bounds__(256, (SU > 4 ? 2 : 3)) k_gather(const WorldDev* __restrict__ wp,
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256, 3) k_gather(const WorldDev* __restrict__ wp,
                                                 const int32_t* __restrict__ ids,
                                                 const float* __restrict__ wts,
                                                 const unsigned long long* __restrict__ hitmask,
@@ -1586,213 +1467,8 @@ __global__ void __launch_bounds__(256, (SU > 4 ? 2 : 3)) k_gather(const WorldDev
       ++n;
     }
     __syncwarp();
-    weighted_row_sum<T, VPL, false, SU>(srcs, ws, n, nvec, lane,
-                                        reinterpret_cast<int4*>(out + t * w.row_bytes));
-  }
-}
-
-// TMA variant: one lane per warp issues cp.async.bulk loads of every source's
-// 1 KB chunk into a shared-memory stage (mbarrier transaction count), the
-// warp accumulates from shared memory while the next chunk's loads are in
-// flight (2 stages).  Bytes in flight no longer cost registers.  Used when
-// the sources are local (modes 2/3, or any mode on one GPU) and rows are a
-// multiple of 1 KB; tokens with more than kTmaSrc sources take the register
-// path.
-constexpr int kTmaWarps = 6, kTmaStages = 2, kTmaSrc = 16, kTmaChunk = 1024;
-constexpr size_t kTmaSmem = (size_t)kTmaWarps * kTmaStages * kTmaSrc * kTmaChunk;
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  const uint32_t a = smem_addr(bar);
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(phase)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
-                                          uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-// Bulk-copy pack for one GPU (every destination local: modes 0, 2, 3 at
-// P = 1): per token one cp.async.bulk load of the row into a per-warp
-// shared-memory slot, then one cp.async.bulk store per pick straight from
-// that slot into the expert-major rows -- the row never passes through
-// registers.  Two slots per warp; a slot is reloaded once the stores issued
-// from it two tokens earlier have finished reading it.
-constexpr int kBulkWarps = 8;
-
-__global__ void __launch_bounds__(kBulkWarps * 32) k_pack_bulk(
-    const WorldDev* __restrict__ wp, const uint8_t* __restrict__ x, const int32_t* __restrict__ ids,
-    const int32_t* __restrict__ chunk_off, const int32_t* __restrict__ rank_e,
-    const int32_t* __restrict__ eoff, int nchunks, int32_t* __restrict__ epos_out,
-    int* __restrict__ status) {
-  extern __shared__ __align__(128) uint8_t bulk_smem[];
-  __shared__ __align__(8) uint64_t bars[kBulkWarps][2];
-  const WorldDev& w = *wp;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t rb = (uint32_t)w.row_bytes;
-  uint8_t* slot0 = bulk_smem + (size_t)wid * 2 * rb;
-  if (lane == 0) {
-    mbar_init(&bars[wid][0], 1);
-    mbar_init(&bars[wid][1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  const int C = w.G + w.E + w.P;
-  const int64_t T = (int64_t)w.L * w.T_r;
-  const int64_t nw = (int64_t)gridDim.x * kBulkWarps;
-  uint32_t phase[2] = {0u, 0u};
-  int it = 0;
-  for (int64_t t = (int64_t)blockIdx.x * kBulkWarps + wid; t < T; t += nw, ++it) {
-    const int b = it & 1;
-    uint8_t* slot = slot0 + b * rb;
-    if (lane == 0) {
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      mbar_expect_tx(&bars[wid][b], rb);
-      bulk_load(slot, x + t * w.row_bytes, rb, &bars[wid][b]);
-    }
-    const int s_loc = (int)(t / w.T_r);
-    const int64_t t_in = t - (int64_t)s_loc * w.T_r;
-    const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
-    int my_e = -1, my_ep = -1;
-    if (lane < w.K) {
-      my_e = ids[t * w.K + lane];
-      if (my_e >= 0) {
-        my_ep = eoff[s_loc * w.E + my_e] + coff[w.G + my_e] + rank_e[t * w.K + lane];
-        if (my_ep >= w.N_cap) {
-          atomicExch(status, 2);
-          my_ep = -1;
-        }
-      }
-      epos_out[t * w.K + lane] = my_ep;
-    }
-    if (lane == 0) mbar_wait(&bars[wid][b], phase[b]);
-    // destinations: every lane resolves its own pick's address, lane 0 issues
-    uint8_t* dst = my_ep >= 0 ? w.xmaj[rank_of_slot(w, my_e)] + (int64_t)my_ep * w.row_bytes : nullptr;
-    for (int k = 0; k < w.K; ++k) {
-      uint8_t* dk = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)dst, k);
-      if (lane == 0 && dk)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dk),
-                     "r"(smem_addr(slot)), "r"(rb)
-                     : "memory");
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    phase[b] ^= 1u;
-    __syncwarp();
-  }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kTmaWarps * 32, 1)
-    k_gather_tma(const WorldDev* __restrict__ wp, const int32_t* __restrict__ ids,
-                 const float* __restrict__ wts, const unsigned long long* __restrict__ hitmask,
-                 const int32_t* __restrict__ gpos, const int32_t* __restrict__ epos, int mode,
-                 int grad, int push, const Offsets* __restrict__ offs,
-                 const int32_t* __restrict__ gpos_g, uint8_t* __restrict__ out) {
-  extern __shared__ __align__(128) uint8_t tma_smem[];
-  __shared__ uint64_t bars[kTmaWarps][kTmaStages];
-  const WorldDev& w = *wp;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint8_t* stage_base = tma_smem + (size_t)wid * kTmaStages * kTmaSrc * kTmaChunk;
-  if (lane == 0)
-    for (int st = 0; st < kTmaStages; ++st) mbar_init(&bars[wid][st], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-  const int chunks = (int)(w.row_bytes / kTmaChunk);
-  const int64_t ntok = (int64_t)w.L * w.T_r;
-  const int64_t gw = (int64_t)blockIdx.x * kTmaWarps + wid;
-  const int64_t nw = (int64_t)gridDim.x * kTmaWarps;
-  const uint8_t* srcs[2][kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-  float ws[2][kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
-  int nsrc[2] = {0, 0};
-  uint32_t phase[kTmaStages] = {0, 0};
-  // item i = (token slot i / chunks, chunk i % chunks) of this warp's tokens
-  auto token_of = [&](int64_t i) { return gw + (i / chunks) * nw; };
-  auto issue = [&](int64_t i, int st) {
-    const int64_t t = token_of(i);
-    const int slot = (int)((i / chunks) & 1);
-    const int c = (int)(i % chunks);
-    const int n = nsrc[slot];
-    if (lane == 0 && n <= kTmaSrc) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[wid][st], (uint32_t)(n * kTmaChunk));
-      for (int j = 0; j < n; ++j)
-        bulk_load(stage_base + ((size_t)st * kTmaSrc + j) * kTmaChunk,
-                  srcs[slot][j] + (size_t)c * kTmaChunk, kTmaChunk, &bars[wid][st]);
-    }
-    (void)t;
-  };
-  auto build = [&](int64_t t, int slot) {
-    nsrc[slot] = t < ntok ? gather_sources(w, t, ids, wts, hitmask, gpos, epos, mode, grad, push,
-                                           offs, gpos_g, srcs[slot], ws[slot])
-                          : 0;
-  };
-  const int64_t my_tokens = gw < ntok ? (ntok - gw + nw - 1) / nw : 0;
-  const int64_t items = my_tokens * chunks;
-  if (items == 0) return;
-  build(token_of(0), 0);
-  issue(0, 0);
-  for (int64_t i = 0; i < items; ++i) {
-    const int st = (int)(i & 1);
-    const int64_t t = token_of(i);
-    const int slot = (int)((i / chunks) & 1);
-    const int c = (int)(i % chunks);
-    // prefetch the next item (building the next token's source list first)
-    if (i + 1 < items) {
-      if ((i + 1) % chunks == 0) build(token_of(i + 1), (int)(((i + 1) / chunks) & 1));
-      issue(i + 1, st ^ 1);
-    }
-    const int n = nsrc[slot];
-    int4* dst = reinterpret_cast<int4*>(out + t * w.row_bytes + (size_t)c * kTmaChunk);
-    constexpr int VPC = kTmaChunk / 16 / 32;   // 16-B vectors per lane per chunk (2)
-    if (n <= kTmaSrc) {
-      mbar_wait(&bars[wid][st], phase[st]);
-      phase[st] ^= 1;
-      float acc[VPC][Vec<T>::N];
-#pragma unroll
-      for (int u = 0; u < VPC; ++u)
-#pragma unroll
-        for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = 0.f;
-      for (int j = 0; j < n; ++j) {
-        const int4* sm = reinterpret_cast<const int4*>(stage_base + ((size_t)st * kTmaSrc + j) * kTmaChunk);
-        const float wj = ws[slot][j];
-#pragma unroll
-        for (int u = 0; u < VPC; ++u) {
-          float f[Vec<T>::N];
-          Vec<T>::to_f32(sm[u * 32 + lane], f);
-#pragma unroll
-          for (int q = 0; q < Vec<T>::N; ++q) acc[u][q] = fmaf(wj, f[q], acc[u][q]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < VPC; ++u) st_na_v4(dst + u * 32 + lane, Vec<T>::from_f32(acc[u]));
-    } else if (c == 0) {
-      // too many sources for a stage: whole row on the register path
-      weighted_row_sum<T, 0>(srcs[slot], ws[slot], n, w.row_bytes / 16, lane,
-                          reinterpret_cast<int4*>(out + t * w.row_bytes));
-    }
-    __syncwarp();
+    weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane,
+                             reinterpret_cast<int4*>(out + t * w.row_bytes));
   }
 }
 
@@ -1867,240 +1543,6 @@ __global__ void __launch_bounds__(256, 3) k_reduce_g(const WorldDev* __restrict_
     uint8_t* out_row = w.ret_g[src] + ((int64_t)w.p * w.T_r + pos) * w.row_bytes;
     __syncwarp();
     weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Pipelined per-GPU dedup exchange (mode 3, N > 1).  Each local source's
-// tokens are cut into J stages at chunk boundaries (L * J ~ kStages per GPU).
-// Dispatch: one kernel whose CTAs take a role by ticket: pushers pack the
-// stages in order (all pusher warps on stage k before k + 1) and the warp
-// that completes a stage publishes dflag[src][j] on every peer; expanders
-// walk the same stage order over the peers' sources, wait for the stage's
-// flag and re-expand its received rows into expert-major rows while the
-// later stages are still crossing NVLink.  Combine mirrors it: reducers push
-// the pre-reduced rows of each (source, stage) back and publish rflag at the
-// source; gatherers wait for a stage's returns from every peer and sum.  No
-// device-wide barrier: the flags carry the step sequence number; waits are
-// bounded (20 s -> status 3).  Every CTA is co-resident (grid = occupancy x
-// SMs), pushers/reducers never wait, so progress needs no particular CTA
-// schedule on either GPU.
-
-__device__ __forceinline__ void stage_tokens(const WorldDev& w, int nchunks, int J, int j,
-                                             int64_t& t0, int64_t& t1) {
-  const int b0 = j * nchunks / J, b1 = (j + 1) * nchunks / J;
-  t0 = (int64_t)b0 * kChunk;
-  t1 = (int64_t)b1 * kChunk < w.T_r ? (int64_t)b1 * kChunk : w.T_r;
-  if (t0 > t1) t0 = t1;
-}
-
-// lane 0 polls the flag (bounded, backoff), then every lane takes its own
-// acquire of the published value (one load each, no spinning)
-__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long seq,
-                                          int* status, int lane) {
-  if (lane == 0) {
-    const uint64_t t0 = globaltimer();
-    while (ld_acquire_sys(f) < seq) {
-      if (globaltimer() - t0 > 20000000000ull) {
-        atomicExch(status, 3);
-        break;
-      }
-      __nanosleep(128);
-    }
-  }
-  __syncwarp();
-  (void)ld_acquire_sys(f);
-}
-
-// after this warp's n > 0 items of a stage of `total`: true in the warp that
-// completed it (fence -> counter: the completing warp's later release covers
-// every contributing warp's stores)
-__device__ __forceinline__ bool stage_done(int* counter, int n, int total, int lane) {
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) {
-    __threadfence_system();
-    last = (atomicAdd(counter, n) + n == total);
-  }
-  return __shfl_sync(0xffffffffu, last, 0) != 0;
-}
-
-__global__ void __launch_bounds__(256) k_dispatch_g(const WorldDev* __restrict__ wp,
-                                                    const uint8_t* __restrict__ x,
-                                                    const int32_t* __restrict__ ids,
-                                                    const float* __restrict__ wts,
-                                                    const int32_t* __restrict__ chunk_off,
-                                                    const int32_t* __restrict__ rank_e,
-                                                    const unsigned long long* __restrict__ hitmask,
-                                                    const Offsets* __restrict__ offs,
-                                                    const int32_t* __restrict__ eoff, int nchunks,
-                                                    int J, int32_t* __restrict__ epos_out,
-                                                    const int32_t* __restrict__ rank_g,
-                                                    int32_t* __restrict__ gpos_g,
-                                                    int* __restrict__ status, int* __restrict__ pipe,
-                                                    int n_push) {
-  const WorldDev& w = *wp;
-  const unsigned long long seq = *w.epoch_ctr;   // the notify barrier's epoch of this step
-  __shared__ int s_role;
-  if (threadIdx.x == 0) s_role = atomicAdd(pipe + 0, 1);
-  __syncthreads();
-  const int role = s_role;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nstage = w.L * J;
-  if (role < n_push) {
-    int* done = pipe + 2;
-    const int64_t gw = (int64_t)role * 8 + wid, nw = (int64_t)n_push * 8;
-    for (int k = 0; k < nstage; ++k) {
-      const int s_loc = k / J, j = k % J;
-      int64_t t0, t1;
-      stage_tokens(w, nchunks, J, j, t0, t1);
-      int n = 0;
-      for (int64_t ti = t0 + gw; ti < t1; ti += nw, ++n)
-        pack_token(w, (int64_t)s_loc * w.T_r + ti, lane, x, ids, wts, chunk_off, nullptr, rank_e,
-                   hitmask, offs, eoff, nchunks, 3, nullptr, epos_out, rank_g, gpos_g, status);
-      const int total = (int)(t1 - t0);
-      const bool publish = n ? stage_done(done + k, n, total, lane) : (total == 0 && gw == 0);
-      if (publish && lane == 0) {
-        __threadfence_system();
-        const int sg = w.p * w.L + s_loc;
-        for (int q = 0; q < w.P; ++q)
-          if (q != w.p) st_release_sys(w.dflag[q * w.L] + sg * kMaxJ + j, seq);
-      }
-    }
-    return;
-  }
-  // expanders: received rows of (peer source, stage) -> local expert-major rows
-  const int64_t gw = (int64_t)(role - n_push) * 8 + wid;
-  const int64_t nw = (int64_t)(gridDim.x - n_push) * 8;
-  const int64_t nvec = w.row_bytes / 16;
-  uint8_t* xbase = w.xmaj[w.p * w.L];
-  const RowMeta* meta = w.meta_g[w.p];
-  const int32_t* cpre = w.cpre[w.p * w.L];
-  for (int k = 0; k < nstage; ++k) {
-    const int kl = k / J, j = k % J;
-    for (int q = 0; q < w.P; ++q) {
-      if (q == w.p) continue;
-      const int s = q * w.L + kl;
-      const int64_t base = offs->offd_g[s];
-      const int64_t r0 = base + cpre[s * (kMaxJ + 1) + j];
-      const int64_t r1 = base + cpre[s * (kMaxJ + 1) + j + 1];
-      if (r0 + gw >= r1) continue;
-      wait_flag(w.dflag[w.p * w.L] + s * kMaxJ + j, seq, status, lane);
-      for (int64_t r = r0 + gw; r < r1; r += nw) {
-        int ep = -1;
-        if (lane < w.K) ep = __ldcg(&meta[r * w.K + lane].epos);
-        const unsigned on = __ballot_sync(0xffffffffu, ep >= 0);
-        if (__popc(on) < 2) continue;
-        const int k0 = __ffs(on) - 1;
-        const int e0 = __shfl_sync(0xffffffffu, ep, k0);
-        const int4* src = reinterpret_cast<const int4*>(xbase + (int64_t)e0 * w.row_bytes);
-        for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
-          int4 buf[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            int64_t v = v0 + u * 32 + lane;
-            if (v < nvec) buf[u] = ld_cg_v4(src + v);
-          }
-          for (int kk = k0 + 1; kk < w.K; ++kk) {
-            int e = __shfl_sync(0xffffffffu, ep, kk);
-            if (e < 0) continue;
-            int4* dst = reinterpret_cast<int4*>(xbase + (int64_t)e * w.row_bytes);
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-              int64_t v = v0 + u * 32 + lane;
-              if (v < nvec) st_na_v4(dst + v, buf[u]);
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
-template <typename T, int VPL>
-__global__ void __launch_bounds__(256, 3) k_combine_g(const WorldDev* __restrict__ wp,
-                                                      const int32_t* __restrict__ ids,
-                                                      const float* __restrict__ wts,
-                                                      const unsigned long long* __restrict__ hitmask,
-                                                      const int32_t* __restrict__ epos,
-                                                      const Offsets* __restrict__ offs,
-                                                      const int32_t* __restrict__ gpos_g,
-                                                      uint8_t* __restrict__ out, int nchunks, int J,
-                                                      int* __restrict__ status,
-                                                      int* __restrict__ pipe, int n_red,
-                                                      const uint8_t* __restrict__ addend) {
-  const WorldDev& w = *wp;
-  const unsigned long long seq = *w.epoch_ctr;   // unchanged since this step's notify
-  __shared__ int s_role;
-  __shared__ const uint8_t* s_src[8][kMaxSrc];
-  __shared__ float s_w[8][kMaxSrc];
-  if (threadIdx.x == 0) s_role = atomicAdd(pipe + 1, 1);
-  __syncthreads();
-  const int role = s_role;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint8_t** srcs = s_src[wid];
-  float* ws = s_w[wid];
-  const int64_t nvec = w.row_bytes / 16;
-  const int nstage = w.L * J;
-  if (role < n_red) {
-    // reducers: pre-reduce this GPU's picks of every received row, push to the source
-    int* done = pipe + 2 + kMaxRanks * kMaxJ;
-    const int64_t gw = (int64_t)role * 8 + wid, nw = (int64_t)n_red * 8;
-    const uint8_t* ybase = w.ymaj[w.p * w.L];
-    const RowMeta* meta = w.meta_g[w.p];
-    const int32_t* cpre = w.cpre[w.p * w.L];
-    for (int k = 0; k < nstage; ++k) {
-      const int kl = k / J, j = k % J;
-      for (int q = 0; q < w.P; ++q) {
-        if (q == w.p) continue;
-        const int s = q * w.L + kl;
-        const int64_t base = offs->offd_g[s];
-        const int64_t r0 = base + cpre[s * (kMaxJ + 1) + j];
-        const int64_t r1 = base + cpre[s * (kMaxJ + 1) + j + 1];
-        int cnt = 0;
-        for (int64_t r = r0 + gw; r < r1; r += nw, ++cnt) {
-          __syncwarp();
-          const int n = meta_sources_warp(meta + r * w.K, w.K, ybase, w.row_bytes, 0, lane,
-                                          srcs, ws);
-          uint8_t* out_row = w.ret_g[s] + ((int64_t)w.p * w.T_r + (r - base)) * w.row_bytes;
-          __syncwarp();
-          weighted_row_sum<T, VPL>(srcs, ws, n, nvec, lane, reinterpret_cast<int4*>(out_row));
-        }
-        const int total = (int)(r1 - r0);
-        const bool publish = cnt ? stage_done(done + s * kMaxJ + j, cnt, total, lane)
-                                 : (total == 0 && gw == 0);
-        if (publish && lane == 0) {
-          __threadfence_system();
-          st_release_sys(w.rflag[q * w.L] + (w.p * w.L + kl) * kMaxJ + j, seq);
-        }
-      }
-    }
-    return;
-  }
-  // gatherers: a stage's tokens once every peer returned it
-  const int64_t gw = (int64_t)(role - n_red) * 8 + wid;
-  const int64_t nw = (int64_t)(gridDim.x - n_red) * 8;
-  for (int k = 0; k < nstage; ++k) {
-    const int s_loc = k / J, j = k % J;
-    int64_t t0, t1;
-    stage_tokens(w, nchunks, J, j, t0, t1);
-    if (t0 + gw >= t1) continue;
-    for (int q = 0; q < w.P; ++q)
-      if (q != w.p) wait_flag(w.rflag[w.p * w.L] + (q * w.L + s_loc) * kMaxJ + j, seq, status, lane);
-    for (int64_t ti = t0 + gw; ti < t1; ti += nw) {
-      const int64_t t = (int64_t)s_loc * w.T_r + ti;
-      __syncwarp();
-      int n = gather_sources_warp(w, t, lane, ids, wts, hitmask, nullptr, epos, 3, 0, 1, offs,
-                                  gpos_g, srcs, ws);
-      if (addend) {
-        srcs[n] = addend + t * w.row_bytes;
-        ws[n] = 1.f;
-        ++n;
-      }
-      __syncwarp();
-      weighted_row_sum<T, VPL, true>(srcs, ws, n, nvec, lane,
-                                     reinterpret_cast<int4*>(out + t * w.row_bytes));
-    }
   }
 }
 
@@ -2393,7 +1835,7 @@ struct hm_world {
   size_t sym_bytes = 0;
   size_t off_recv_x = 0, off_meta = 0, off_xmaj = 0, off_ymaj = 0, off_comb = 0, off_counts = 0,
          off_flags = 0, off_gy = 0, off_gx = 0, off_gw = 0, off_ret = 0, off_recv_g = 0,
-         off_meta_g = 0, off_ret_g = 0, off_cpre = 0, off_dflag = 0, off_rflag = 0;
+         off_meta_g = 0, off_ret_g = 0;
   bool grad = false;
   std::vector<void*> opened;  // peer bases opened via IPC
   // local scratch
@@ -2410,41 +1852,14 @@ struct hm_world {
   int32_t* eoff = nullptr;
   int32_t* n_e = nullptr;
   int* status = nullptr;
-  // pipelined mode 3 (N > 1): role tickets + stage completion counters,
-  // step sequence number carried by the stage flags, CTA split
-  int32_t* pipe = nullptr;
-  int pipe_len = 0;
-  // hm_world_set_option(w, 1, 1) -> staged dispatch/combine kernels.  Off by
-  // default: measured slower on B200 (N = 2: 0.52-1.5 ms vs 0.40 ms for the
-  // barrier-separated kernels, tools/pipe_tune.py) -- every stage boundary
-  // costs ~15 us because each pusher's release has to wait for its NVLink
-  // stores to be acknowledged, and splitting the SMs between pushers and
-  // expanders starves the local HBM copies the pushers also do.
-  bool pipelined = false;
-  int push_pct = 50;           // hm_world_set_option(w, 2, pct): pusher / reducer share of CTAs
-  int stages = kStages;        // hm_world_set_option(w, 3, n): target pipeline stages per GPU
   int max_blocks = 0;          // hm_world_set_option(w, 4, n): grid cap of the exchange kernels
-  // hm_world_set_option(w, 5, 1): bulk-copy pack on one GPU (measured 224 vs
-  // 217 us for the register pack, Qwen3 N = 1: the write-heavy pack is bound
-  // by HBM writes either way)
-  bool bulk_pack = false;
-  int pack_store = 0;          // hm_world_set_option(w, 6, v): pack store hint (0 na, 1 cs, 2 wb)
-  // hm_world_set_option(w, 7, 1): separate warps for NVLink pushes and local
-  // copies in the N > 1 pack (measured neutral: 150 vs 152 us at N = 4)
-  bool split_pack = false;
-  bool lean_pack = true;       // hm_world_set_option(w, 8, 0): general pack on one GPU too
-  bool gather_su8 = false;     // hm_world_set_option(w, 9, 1): 8-source load batches in the gather
   // hm_world_set_option(w, 10, 1): fused one-GPU dispatch -- row indices
   // instead of expert-major row copies (the expert GEMM gathers)
   bool fused = false;
   int32_t* xidx = nullptr;     // [L][N_cap] source row of every expert-major row
-  int fused_blocks = 0;        // co-resident grid of the pipelined kernels
-  int last_J = 0;              // stages per source of the last dispatch (0: not pipelined)
   unsigned long long* epoch_ctr = nullptr;   // device barrier epoch counter
   bool peers_ready = false;
   int last_mode = 0;
-  bool tma_gather = false;  // hm_world_set_option(w, 0, 1) selects the TMA bulk-copy gather
-                           // (measured slower than the register gather: 0.386 vs 0.311 ms, N=1)
   // optional per-kernel CUDA-event timing (segments recorded on the launch stream)
   bool timing = false;
   cudaEvent_t ev[2 * 16];
@@ -2497,9 +1912,6 @@ static void fill_tables(hm_world* w, int q, uint8_t* base) {
                       : nullptr;
     h.counts[d] = reinterpret_cast<int32_t*>(base + w->off_counts);
     h.flags[d] = reinterpret_cast<unsigned long long*>(base + w->off_flags);
-    h.cpre[d] = reinterpret_cast<int32_t*>(base + w->off_cpre);
-    h.dflag[d] = reinterpret_cast<unsigned long long*>(base + w->off_dflag);
-    h.rflag[d] = reinterpret_cast<unsigned long long*>(base + w->off_rflag);
   }
   h.recv_g[q] = base + w->off_recv_g;
   h.meta_g[q] = reinterpret_cast<RowMeta*>(base + w->off_meta_g);
@@ -2572,9 +1984,6 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   }
   w->off_counts = o; o = align_up(o + (size_t)h.G * (h.G + h.E + h.P) * 4, 256);
   w->off_flags = o;  o = align_up(o + (size_t)h.P * 8, 256);
-  w->off_cpre = o;   o = align_up(o + (size_t)h.G * (kMaxJ + 1) * 4, 256);
-  w->off_dflag = o;  o = align_up(o + (size_t)h.G * kMaxJ * 8, 256);
-  w->off_rflag = o;  o = align_up(o + (size_t)h.G * kMaxJ * 8, 256);
   w->sym_bytes = o;
   int st;
 #define HM_TRY(call) do { st = hm::cuda_status(call); if (st) { delete w; return st; } } while (0)
@@ -2593,9 +2002,6 @@ HM_API int hm_world_create(int32_t ranks, int32_t gpus, int32_t gpu_index, int32
   HM_TRY(cudaMalloc(&w->offs, sizeof(Offsets)));
   HM_TRY(cudaMalloc(&w->eoff, (size_t)h.L * h.E * 4));
   HM_TRY(cudaMalloc(&w->n_e, (size_t)h.E * 4));
-  w->pipe_len = 2 + 2 * kMaxRanks * kMaxJ;
-  HM_TRY(cudaMalloc(&w->pipe, (size_t)w->pipe_len * 4));
-  HM_TRY(cudaMemset(w->pipe, 0, (size_t)w->pipe_len * 4));
   HM_TRY(cudaMalloc(&w->status, 16));
   HM_TRY(cudaMemset(w->status, 0, 16));
   HM_TRY(cudaMalloc(&w->epoch_ctr, 8));
@@ -2632,7 +2038,6 @@ HM_API int hm_world_destroy(hm_world* w) {
   cudaFree(w->status);
   cudaFree(w->xidx);
   cudaFree(w->epoch_ctr);
-  cudaFree(w->pipe);
   cudaFree(w->d);
   delete w;
   return 0;
@@ -2809,15 +2214,6 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
 #undef HM_PLAN
   }
   HM_LAUNCHED();
-  // pipelined per-GPU dedup: J stages per source (L * J ~ kStages per GPU)
-  int J = 0;
-  if (mode == 3 && h.P > 1 && !h.U1 && w->pipelined) {
-    J = w->stages / h.L;
-    if (J < 1) J = 1;
-    if (J > kMaxJ) J = kMaxJ;
-    if (J > w->nchunks) J = w->nchunks;
-  }
-  w->last_J = J;
   {SegScope sc(w, kSegNotify, s);
   const size_t cnt_bytes = (size_t)h.G * (h.G + h.E + h.P) * 4;
   const int stage_cnt = ((2 * h.E + h.G) * 4 + cnt_bytes) <= 160 * 1024 ? 1 : 0;
@@ -2826,26 +2222,11 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     HM_CUDA(cudaFuncSetAttribute(k_notify, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   k_notify<<<1, 1024, nsmem, s>>>(w->d, w->nchunks, w->chunk_cnt, w->offs, w->eoff, w->n_e, mode,
-                                  w->status, J, w->pipe, w->pipe_len, stage_cnt);
+                                  w->status, stage_cnt);
   }
   HM_LAUNCHED();
-  if (J) {
-    int occ = 0;
-    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dispatch_g, 256, 0));
-    const int blocks = kSMs * (occ > 0 ? occ : 1);
-    int n_push = blocks * w->push_pct / 100;
-    if (n_push < 1) n_push = 1;
-    if (n_push > blocks - 1) n_push = blocks - 1;
-    SegScope sc(w, kSegPack, s);
-    k_dispatch_g<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_e,
-                                        w->hitmask, w->offs, w->eoff, w->nchunks, J, w->epos,
-                                        w->rank_g, w->gpos_g, w->status, w->pipe, n_push);
-    HM_LAUNCHED();
-    return 0;
-  }
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
-  const size_t bulk_smem = (size_t)kBulkWarps * 2 * h.row_bytes;
   const int64_t nv = h.row_bytes / 16;
   const bool local_only = h.P == 1 && mode != 1 && !h.U1;
   HM_CHECK_ARG(!(w->fused && mode == 1),
@@ -2857,8 +2238,7 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     HM_LAUNCHED();
     return 0;
   }
-  if (local_only && w->lean_pack && !w->bulk_pack &&
-      (nv == 32 || nv == 64 || nv == 128 || nv == 256)) {
+  if (local_only && (nv == 32 || nv == 64 || nv == 128 || nv == 256)) {
     // one token per warp up to 32 CTAs per SM: the block scheduler keeps
     // every SM full of fresh warps (233 -> 220 us for the Qwen3 N = 1 step
     // vs the 8-per-SM grid-stride grid, tools/pack_grid.py)
@@ -2876,32 +2256,11 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     else
       HM_PL(8);
 #undef HM_PL
-  } else if (w->bulk_pack && h.P == 1 && mode != 1 && !h.U1 && h.row_bytes % 16 == 0 &&
-      bulk_smem <= 200 * 1024) {
-    HM_CUDA(cudaFuncSetAttribute(k_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)bulk_smem));
-    int occ = 0;
-    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pack_bulk, kBulkWarps * 32,
-                                                          bulk_smem));
-    const int bb = grid_for(T, kBulkWarps, kSMs * (occ > 0 ? occ : 1));
-    SegScope sc(w, kSegPack, s);
-    k_pack_bulk<<<bb, kBulkWarps * 32, bulk_smem, s>>>(w->d, (const uint8_t*)x, ids,
-                                                       w->chunk_cnt, w->rank_e, w->eoff,
-                                                       w->nchunks, w->epos, w->status);
   } else {
     SegScope sc(w, kSegPack, s);
-#define HM_PACK(SH)                                                                          \
-  k_pack<SH><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d, \
-                                    w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode, \
-                                    w->gpos, w->epos, w->rank_g, w->gpos_g, w->status, split)
-    const int split = (mode == 3 && h.P > 1 && w->split_pack) ? 1 : 0;
-    if (w->pack_store == 1)
-      HM_PACK(1);
-    else if (w->pack_store == 2)
-      HM_PACK(2);
-    else
-      HM_PACK(0);
-#undef HM_PACK
+    k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
+                                  w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
+                                  w->gpos, w->epos, w->rank_g, w->gpos_g, w->status);
   }
   HM_LAUNCHED();
   if (h.P > 1) {
@@ -2917,7 +2276,6 @@ HM_API int hm_expand(hm_world* w, void* stream) {
   if (w->h.P == 1 && w->last_mode == 2) return 0;  // every rank shares this GPU: nothing received
   if (w->h.U1) return 0;                             // relay rows are re-dispatched, not expanded
   if (w->last_mode == 3 && w->h.P == 1) return 0;    // one GPU: every row went direct
-  if (w->last_J) return 0;                           // pipelined: expanded inside the dispatch
   int blocks = exch_blocks(w);
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
   if (w->last_mode == 3)
@@ -2966,27 +2324,6 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
   const int push = w->h.U1 ? 0 : 1;
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
-  if (mode == 3 && w->last_J) {   // pipelined reduce + gather, one kernel
-    HM_CHECK_ARG(w->last_mode == 3, "hm_combine: mode 3 combine after a mode %d dispatch",
-                 w->last_mode);
-    HM_CHECK_ARG(wts && ids, "hm_combine: mode 3 needs ids and weights");
-    int rc = 0;
-    with_row_type(h, [&](auto t, auto v) {
-      auto kern = k_combine_g<typename decltype(t)::type, decltype(v)::value>;
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
-      const int blocks = kSMs * (occ > 0 ? occ : 1);
-      int n_red = blocks * w->push_pct / 100;
-      if (n_red < 1) n_red = 1;
-      if (n_red > blocks - 1) n_red = blocks - 1;
-      SegScope sc(w, kSegGather, s);
-      kern<<<blocks, 256, 0, s>>>(w->d, ids, wts, w->hitmask, w->epos, w->offs, w->gpos_g,
-                                  (uint8_t*)out, w->nchunks, w->last_J, w->status, w->pipe, n_red,
-                                  addend);
-      rc = hm::launch_status();
-    });
-    return rc;
-  }
   if (mode == 3 && h.P > 1) {
     SegScope sc(w, kSegReduce, s);
     with_row_type(h, [&](auto t, auto v) {
@@ -3012,34 +2349,10 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
   SegScope sc(w, kSegGather, s);
-  // local sources: modes 2/3 (pushed returns + same-GPU rows) or one GPU
-  const bool local_src = (mode >= 2 || h.P == 1) && !(mode == 1 && !push);
-  if (local_src && w->tma_gather && h.row_bytes % kTmaChunk == 0 && !addend) {
-    if (h.elem == 2) {
-      HM_CUDA(cudaFuncSetAttribute(k_gather_tma<__nv_bfloat16>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-      k_gather_tma<__nv_bfloat16><<<kSMs, kTmaWarps * 32, kTmaSmem, s>>>(
-          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
-          (uint8_t*)out);
-    } else {
-      HM_CUDA(cudaFuncSetAttribute(k_gather_tma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kTmaSmem));
-      k_gather_tma<float><<<kSMs, kTmaWarps * 32, kTmaSmem, s>>>(
-          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
-          (uint8_t*)out);
-    }
-    HM_LAUNCHED();
-    return 0;
-  }
   with_row_type(h, [&](auto t, auto v) {
-    if (w->gather_su8)   // 8 sources' loads in flight per lane (2 CTAs / SM)
-      k_gather<typename decltype(t)::type, decltype(v)::value, 8><<<blocks, 256, 0, s>>>(
-          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
-          (uint8_t*)out, addend);
-    else
-      k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
-          w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
-          (uint8_t*)out, addend);
+    k_gather<typename decltype(t)::type, decltype(v)::value><<<blocks, 256, 0, s>>>(
+        w->d, ids, wts, w->hitmask, w->gpos, w->epos, mode, 0, push, w->offs, w->gpos_g,
+        (uint8_t*)out, addend);
   });
   HM_LAUNCHED();
   return 0;
@@ -3273,7 +2586,7 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
   const WorldDev& h = w->h;
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
-  if ((mode == 0 || (mode == 2 && h.P == 1)) && w->lean_pack) {
+  if (mode == 0 || (mode == 2 && h.P == 1)) {
     // every pick direct: one token per warp, up to 32 CTAs per SM
     blocks = grid_for(T, 8, w->max_blocks > 0 ? w->max_blocks : kSMs * 32);
     if (h.elem == 2)
@@ -3336,28 +2649,16 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   return 0;
 }
 
-// runtime options: 0 = TMA bulk-copy gather (1) or the register gather (0, default);
-// 1 = pipelined mode-3 exchange at N > 1 (1, default) or barrier-separated
-// kernels (0); 2 = percent of the pipelined kernels' CTAs that push (1..99)
+// runtime options: 4 = grid cap of the exchange kernels (CTAs, 0 = 8 per SM;
+// leaves SMs to concurrent kernels); 10 = fused one-GPU dispatch (row indices
+// instead of expert-major copies, hm_expert_ffn_gather).  Options 0-3 and 5-9
+// selected measured-slower variants (TMA gather, staged pipelined exchange,
+// bulk / split / general one-GPU pack, store hints, 8-source gather batches)
+// that round 2 removed; they are rejected.
 HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(w, "hm_world_set_option: null world");
-  HM_CHECK_ARG(option >= 0 && option <= 10, "hm_world_set_option: unknown option %d", option);
-  if (option == 0) w->tma_gather = value != 0;
-  if (option == 1) w->pipelined = value != 0;
-  if (option == 2) {
-    HM_CHECK_ARG(value >= 1 && value <= 99, "hm_world_set_option: split must be 1..99 %%");
-    w->push_pct = value;
-  }
-  if (option == 3) {
-    HM_CHECK_ARG(value >= 1 && value <= kMaxRanks * kMaxJ, "hm_world_set_option: bad stage count");
-    w->stages = value;
-  }
+  HM_CHECK_ARG(option == 4 || option == 10, "hm_world_set_option: unknown option %d", option);
   if (option == 4) w->max_blocks = value > 0 ? value : 0;
-  if (option == 5) w->bulk_pack = value != 0;
-  if (option == 6) w->pack_store = value >= 0 && value <= 2 ? value : 0;
-  if (option == 7) w->split_pack = value != 0;
-  if (option == 8) w->lean_pack = value != 0;
-  if (option == 9) w->gather_su8 = value != 0;
   if (option == 10) {
     HM_CHECK_ARG(!value || (w->h.P == 1 && !w->h.U1),
                  "hm_world_set_option: the fused dispatch needs a one-GPU, non-relay world");

@@ -47,17 +47,6 @@ def expert_ffn_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int, w13: 
               inter, ptr(h), y_ptr, stream_ptr())
 
 
-_WGRAD_TRANSPOSED = False
-
-
-def set_wgrad_transposed(enabled: bool) -> None:
-    """Weight-gradient GEMMs via transposed copies (True) or straight from the
-    token-major activations with MN-major tcgen05 operands (False, default)."""
-    global _WGRAD_TRANSPOSED
-    _lib.call("hm_ffn_set_option", 0, int(bool(enabled)))
-    _WGRAD_TRANSPOSED = bool(enabled)
-
-
 def expert_ffn_save_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
                          w13: torch.Tensor, w2: torch.Tensor, hidden: int, inter: int,
                          h: torch.Tensor, y_ptr: int, g13_ptr: int) -> None:
@@ -88,51 +77,22 @@ def expert_ffn_backward_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_row
               int(bool(accumulate)), stream_ptr())
 
 
-def set_gemm_pair(enabled: bool) -> None:
-    """CTA-pair (cta_group::2, 256 x 256 tiles) kernels for the forward and
-    data-gradient GEMMs."""
-    _lib.call("hm_ffn_set_option", 2, int(bool(enabled)))
-
-
-def set_wgrad_pair(mode: int | bool) -> None:
-    """Weight-gradient GEMMs: 0/False single-CTA, 1/True CTA pairs with a
-    per-stage hand-off of the zeroed tail, 2 CTA pairs with per-group tensor
-    maps (TMA zero-fills the tail)."""
-    _lib.call("hm_ffn_set_option", 3, int(mode))
-
-
-def set_swiglu_scalar(enabled: bool) -> None:
-    """SwiGLU backward with 4-byte accesses (True) or the 16-byte kernel
-    (False, default); bit-identical."""
-    _lib.call("hm_ffn_set_option", 4, int(bool(enabled)))
-
-
 def set_gemm_ctas(n: int) -> None:
     """Cap the persistent grouped-GEMM grid at n CTAs (0: one per SM)."""
     _lib.call("hm_ffn_set_option", 1, int(n))
 
 
 class FFNBackwardScratch:
-    """Work buffers of one expert-FFN backward (capacity rows x widths).  The
-    transposed-activation buffers (ta, tb) are only allocated for the
-    transposed weight-gradient path."""
+    """Work buffers of one expert-FFN backward (capacity rows x widths)."""
 
     def __init__(self, rows: int, groups: int, hidden: int, inter: int):
         kw = dict(dtype=torch.bfloat16, device="cuda")
         self.rows, self.groups, self.hidden, self.inter = rows, groups, hidden, inter
-        self.kmax = (rows + BLOCK // 2 * groups + 63) // 64 * 64 + 64 * groups
         self.g13 = torch.empty(rows, 2 * inter, **kw)
         self.dg13 = torch.empty(rows, 2 * inter, **kw)
         self.dh = torch.empty(rows, inter, **kw)
         self.h = torch.empty(rows, inter, **kw)
-        self.ta = self.tb = torch.empty(1, **kw)
         self.layout = torch.empty(2 * (groups + 1), dtype=torch.int32, device="cuda")
-
-    def ensure_transposed(self) -> None:
-        if self.ta.numel() == 1:
-            kw = dict(dtype=torch.bfloat16, device="cuda")
-            self.ta = torch.empty(max(self.hidden, 2 * self.inter), self.kmax, **kw)
-            self.tb = torch.empty(max(self.hidden, self.inter), self.kmax, **kw)
 
 
 def expert_ffn_backward_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
@@ -143,24 +103,15 @@ def expert_ffn_backward_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: i
     """Grads of the SwiGLU experts: gx (rows), dW13 [g][2I][M], dW2 [g][M][I].
     ``g13_saved_ptr``: the forward's pre-activations (expert_ffn_save_ptrs);
     0 -> recomputed.  ``accumulate``: add the weight grads to dw13 / dw2
-    (needs the saved pre-activations and the MN-major path)."""
-    if accumulate:
-        if not g13_saved_ptr:
-            raise ValueError("accumulate needs the saved pre-activations")
-        _lib.call("hm_expert_ffn_backward_saved_acc", x_ptr, a_rows, n_rows_ptr, groups,
-                  ptr(w13t), ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh),
-                  ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
-                  stream_ptr())
-        return
-    if _WGRAD_TRANSPOSED:
-        sc.ensure_transposed()
+    (needs the saved pre-activations)."""
     if g13_saved_ptr:
         _lib.call("hm_expert_ffn_backward_saved", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13t),
                   ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh), ptr(sc.dg13),
-                  ptr(sc.h), ptr(sc.ta), ptr(sc.tb), sc.kmax, ptr(sc.layout), gx_ptr, ptr(dw13),
-                  ptr(dw2), stream_ptr())
+                  ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2), int(bool(accumulate)),
+                  stream_ptr())
         return
+    if accumulate:
+        raise ValueError("accumulate needs the saved pre-activations")
     _lib.call("hm_expert_ffn_backward", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w13t),
               ptr(w2t), gy_ptr, hidden, inter, ptr(sc.g13), ptr(sc.dh), ptr(sc.dg13), ptr(sc.h),
-              ptr(sc.ta), ptr(sc.tb), sc.kmax, ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
-              stream_ptr())
+              ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2), stream_ptr())

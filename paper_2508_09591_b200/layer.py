@@ -260,23 +260,6 @@ class EPWorld:
     def barrier(self) -> None:
         _lib.call("hm_world_barrier", self._h, stream_ptr())
 
-    def set_tma_gather(self, enabled: bool) -> None:
-        """Source-side sum via TMA bulk copies or register loads (default; faster on B200)."""
-        _lib.call("hm_world_set_option", self._h, 0, int(bool(enabled)))
-
-    def set_bulk_pack(self, enabled: bool) -> None:
-        """One-GPU pack via cp.async.bulk copies or register copies (default)."""
-        _lib.call("hm_world_set_option", self._h, 5, int(bool(enabled)))
-
-    def set_split_pack(self, enabled: bool) -> None:
-        """N > 1 per-GPU dedup pack: separate warps for NVLink pushes and
-        local copies, or one warp per token for both (default)."""
-        _lib.call("hm_world_set_option", self._h, 7, int(bool(enabled)))
-
-    def set_lean_pack(self, enabled: bool) -> None:
-        """One-GPU pack: the lean kernel (default) or the general pack."""
-        _lib.call("hm_world_set_option", self._h, 8, int(bool(enabled)))
-
     def set_fused(self, enabled: bool) -> None:
         """One GPU: dispatch emits expert-major row indices (buffer "xidx")
         instead of copying rows; the expert GEMM gathers the rows from x
@@ -287,17 +270,6 @@ class EPWorld:
     def set_max_blocks(self, n: int) -> None:
         """Cap the exchange kernels' grid at n CTAs (0: 8 per SM)."""
         _lib.call("hm_world_set_option", self._h, 4, int(n))
-
-    def set_pipelined(self, enabled: bool, push_percent: int | None = None,
-                      stages: int | None = None) -> None:
-        """Per-GPU dedup at N > 1: one pipelined kernel per direction with
-        per-stage flags, or the barrier-separated kernels (default; faster on
-        B200).  Must be set identically on every GPU of the world."""
-        _lib.call("hm_world_set_option", self._h, 1, int(bool(enabled)))
-        if push_percent is not None:
-            _lib.call("hm_world_set_option", self._h, 2, int(push_percent))
-        if stages is not None:
-            _lib.call("hm_world_set_option", self._h, 3, int(stages))
 
     def _check_rows(self, x, ids):
         t = self.local * self.tokens_per_rank

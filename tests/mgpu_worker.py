@@ -83,22 +83,6 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
     ep.check_status()
     assert torch.equal(out2, out)
     if dedup == "gpu":
-        # barrier-separated kernels (and other CTA splits of the pipelined
-        # ones) produce the identical expert-major rows and output
-        xm0 = [ep.read("xmaj", l, dtype, int(rows[l, 1]) * M).clone() for l in range(L)]
-        for pipelined, pct, split in ((True, 50, False), (True, 25, False), (True, 75, False),
-                                      (False, None, True), (False, None, False)):
-            ep.set_pipelined(pipelined, pct)
-            ep.set_split_pack(split)
-            for _ in range(2):
-                ep.dispatch(x[lo:hi].cuda(), slot, w, dedup=dedup)
-                out3 = ep.combine(slot, w, dedup=dedup)
-            torch.cuda.synchronize()
-            ep.check_status()
-            assert torch.equal(out3, out), ("pipelined", pipelined, pct, split)
-            for l in range(L):
-                xm = ep.read("xmaj", l, dtype, int(rows[l, 1]) * M)
-                assert torch.equal(xm, xm0[l]), ("xmaj", pipelined, pct, l)
         # the step replayed from a CUDA graph (device-side barrier epochs):
         # every rank captures and replays the same sequence
         xin = x[lo:hi].cuda()

@@ -42,17 +42,6 @@ def test_dispatch_combine_backward(hm, dedup, shape):
         ep.set_expert_outputs(d, (xm.float() * rs).to(dtype))
     ep.combine(slot, w, dedup=dedup)
     dw = ep.dispatch_grad(g.cuda(), slot, w, dedup=dedup)
-    if dedup != "all":   # direct picks: the lean kernel and the general one agree bit for bit
-        gy_lean = [ep.read("gy", d, dtype, int(row_scale[d].shape[0]) * M).clone()
-                   for d in range(G)]
-        ep.set_lean_pack(False)
-        dw_gen = ep.dispatch_grad(g.cuda(), slot, w, dedup=dedup)
-        ep.set_lean_pack(True)
-        torch.cuda.synchronize()
-        assert torch.equal(dw_gen, dw)
-        for d in range(G):
-            assert torch.equal(ep.read("gy", d, dtype, int(row_scale[d].shape[0]) * M),
-                               gy_lean[d])
     for d in range(G):
         n = row_scale[d].shape[0]
         gy = ep.read("gy", d, dtype, n * M).view(n, M)

@@ -60,10 +60,5 @@ def run(name, G, M, I, rows_per_group, steps=10):
 
 
 if __name__ == "__main__":
-    from paper_2508_09591_b200.ffn import set_gemm_pair, set_wgrad_pair
-    for pair, wpair in ((False, False), (True, False), (True, True)):
-        set_gemm_pair(pair)
-        set_wgrad_pair(wpair)
-        print(json.dumps({"gemm_pair": pair, "wgrad_pair": wpair}))
-        run("qwen3_rank", 16, 2048, 768, 2048)
-        run("dsv3_rank", 32, 7168, 2048, 1024)
+    run("qwen3_rank", 16, 2048, 768, 2048)
+    run("dsv3_rank", 32, 7168, 2048, 1024)

@@ -45,12 +45,11 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(5 + rank)
     x = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
     g = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
-    from paper_2508_09591_b200.ffn import set_gemm_ctas, set_gemm_pair
+    from paper_2508_09591_b200.ffn import set_gemm_ctas
     for mb, ctas, xb, gp, so in [(m, c, b, p, o) for m in args.mbs for c in args.gemm_ctas
                                  for b in args.exch_blocks for p in args.gemm_pair
                                  for o in args.shared_overlap]:
         set_gemm_ctas(ctas)
-        set_gemm_pair(bool(gp))
         layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, grad=True,
                              n_cap_rows=2 * T_r * K, micro_batches=mb, **kw)
         for wd in layer.worlds:
