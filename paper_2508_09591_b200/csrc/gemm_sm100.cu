@@ -241,89 +241,113 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
   nt = local % tm.ntile_n;
 }
 
+// Coalesced epilogue stores through a 4 KB per-warp shared-memory stage:
+// each lane writes its own row's U 16-byte units (swizzled: unit u of row r
+// at u ^ (r % U), conflict-free), then the warp stores R = 32 / U rows per
+// instruction with U lanes per row, so every global store instruction writes
+// whole 64 / 128-byte row segments instead of 32 rows x 16 bytes (the
+// row-per-lane TMEM layout made the epilogue the GEMM's bottleneck: with the
+// stores skipped, GEMM2 ran at 1450 instead of 1077 TFLOP/s).  Rows >= nvalid
+// (past the group) are not written.
+constexpr int kEpiStageBytes = 4096;   // per epilogue warp
+template <int U>
+__device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v,
+                                            __nv_bfloat16* dst0, int64_t ld, int nvalid) {
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    *reinterpret_cast<int4*>(sw + lane * (U * 16) + ((u ^ (lane % U)) << 4)) = v[u];
+  __syncwarp();
+  constexpr int R = 32 / U;
+  const int ur = lane % U, rr = lane / U;
+#pragma unroll
+  for (int p = 0; p < U; ++p) {
+    const int r = p * R + rr;
+    const int4 w = *reinterpret_cast<const int4*>(sw + r * (U * 16) + ((ur ^ (r % U)) << 4));
+    if (r < nvalid) *reinterpret_cast<int4*>(dst0 + (int64_t)r * ld + ur * 8) = w;
+  }
+  __syncwarp();
+}
+
 // Epilogue of one accumulator tile for the 32 rows of TMEM lane quarter q:
-// TMEM -> fp32 registers -> (SwiGLU / accumulate) -> bf16 row stores.  r_in =
-// this lane's row within group g (weight-gradient modes: output row).
+// TMEM -> fp32 registers -> (SwiGLU / accumulate) -> bf16 rows.  r0 = the
+// warp's first row within group g (weight-gradient modes: output row); sw =
+// the warp's shared-memory store stage.
 template <int kMode>
 __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& tm, int g, int nt,
-                                           int r_in, uint32_t tbase) {
-  const bool valid = kMode >= 2 ? true : r_in < tm.rows[g];
+                                           int r0, int lane, uint32_t tbase, uint8_t* sw,
+                                           int cb = 0, int ce = BN) {
+  const int r_in = r0 + lane;
+  int nvalid = kMode >= 2 ? 32 : tm.rows[g] - r0;
+  nvalid = nvalid < 0 ? 0 : (nvalid > 32 ? 32 : nvalid);
+  const bool valid = lane < nvalid;
   const bool zero = kMode >= 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
-  __nv_bfloat16* orow =
-      args.out + (kMode >= 2 ? (int64_t)g * args.m_out + r_in : (int64_t)(tm.row0[g] + r_in)) *
-                     args.ld_out;
-  if (kMode == 1) {
+  const int64_t row_base = kMode >= 2 ? (int64_t)g * args.m_out + r0 : (int64_t)(tm.row0[g] + r0);
+  __nv_bfloat16* orow = args.out + (row_base + lane) * args.ld_out;
+  if (kMode == 1) {   // [cb, ce) in h columns (0..BN/2)
 #pragma unroll 1
-    for (int c = 0; c < BN / 2; c += 32) {
+    for (int c = cb; c < ce; c += 32) {
       float gv[32], uv[32];
       tmem_ld32x2(tbase + c, tbase + BN / 2 + c, gv, uv);
-      if (valid) {
-        __align__(16) __nv_bfloat162 hv[16];
+      __align__(16) __nv_bfloat162 hv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float g0 = gv[2 * i], g1 = gv[2 * i + 1];
+        float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
+        float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
+        hv[i] = __floats2bfloat162_rn(h0, h1);
+      }
+      stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv),
+                     args.out + row_base * args.ld_out + nt * (BN / 2) + c, args.ld_out, nvalid);
+      if (args.out2) {   // keep the pre-activations for the backward
+        __nv_bfloat16* p0 = args.out2 + (int64_t)(tm.row0[g] + r0) * args.N + nt * BN + c;
+        __align__(16) __nv_bfloat162 gb[16], ub[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float g0 = gv[2 * i], g1 = gv[2 * i + 1];
-          float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
-          float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
-          hv[i] = __floats2bfloat162_rn(h0, h1);
+          gb[i] = __floats2bfloat162_rn(gv[2 * i], gv[2 * i + 1]);
+          ub[i] = __floats2bfloat162_rn(uv[2 * i], uv[2 * i + 1]);
         }
-        int4* dst = reinterpret_cast<int4*>(orow + nt * (BN / 2) + c);
-        const int4* src = reinterpret_cast<const int4*>(hv);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = src[i];
-        if (args.out2) {   // keep the pre-activations for the backward
-          __nv_bfloat16* prow = args.out2 + (int64_t)(tm.row0[g] + r_in) * args.N + nt * BN;
-          __align__(16) __nv_bfloat162 gb[16], ub[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            gb[i] = __floats2bfloat162_rn(gv[2 * i], gv[2 * i + 1]);
-            ub[i] = __floats2bfloat162_rn(uv[2 * i], uv[2 * i + 1]);
-          }
-          int4* pg = reinterpret_cast<int4*>(prow + c);
-          int4* pu = reinterpret_cast<int4*>(prow + BN / 2 + c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            pg[i] = reinterpret_cast<const int4*>(gb)[i];
-            pu[i] = reinterpret_cast<const int4*>(ub)[i];
-          }
-        }
+        stage_store<4>(sw, lane, reinterpret_cast<const int4*>(gb), p0, args.N, nvalid);
+        stage_store<4>(sw, lane, reinterpret_cast<const int4*>(ub), p0 + BN / 2, args.N, nvalid);
       }
     }
-  } else {
+  } else if (kMode >= 2 && args.accumulate) {   // weight grads summed over micro-batches
 #pragma unroll 1
-    for (int c2 = 0; c2 < BN; c2 += 64) {
-     float v2[2][32];
-     tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
-#pragma unroll
-     for (int half = 0; half < 2; ++half) {
-      const int c = c2 + 32 * half;
-      float* v = v2[half];
+    for (int c = 0; c < BN; c += 32) {
+      float v[32], unused[32];
+      tmem_ld32x2(tbase + c, tbase + c, v, unused);
       if (zero) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
       }
-      if (valid) {
-        __align__(16) __nv_bfloat162 hv[16];
-        int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
-        if (kMode >= 2 && args.accumulate) {   // weight grads summed over micro-batches
-          __align__(16) __nv_bfloat162 old[16];
+      int4* dst = reinterpret_cast<int4*>(orow + nt * BN + c);
+      __align__(16) __nv_bfloat162 old[16], hv[16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(old)[i] = dst[i];
+      for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(old)[i] = dst[i];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 o = __bfloat1622float2(old[i]);
-            v[2 * i] += o.x;
-            v[2 * i + 1] += o.y;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) hv[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-        const int4* src = reinterpret_cast<const int4*>(hv);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = src[i];
+      for (int i = 0; i < 16; ++i) {
+        const float2 o = __bfloat1622float2(old[i]);
+        hv[i] = __floats2bfloat162_rn(v[2 * i] + o.x, v[2 * i + 1] + o.y);
       }
-     }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dst[i] = reinterpret_cast<const int4*>(hv)[i];
+    }
+  } else {
+#pragma unroll 1
+    for (int c2 = cb; c2 < ce; c2 += 64) {
+      float v2[2][32];
+      tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
+      __align__(16) __nv_bfloat162 hv[32];
+#pragma unroll
+      for (int half = 0; half < 2; ++half)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          hv[16 * half + i] = zero ? __floats2bfloat162_rn(0.f, 0.f)
+                                   : __floats2bfloat162_rn(v2[half][2 * i], v2[half][2 * i + 1]);
+      stage_store<8>(sw, lane, reinterpret_cast<const int4*>(hv),
+                     args.out + row_base * args.ld_out + nt * BN + c2, args.ld_out, nvalid);
     }
   }
+  (void)valid;
 }
 
 // kMode 0: out = A_g B_g^T over row groups; 1: same + SwiGLU epilogue;
@@ -351,6 +375,7 @@ __global__ void __launch_bounds__(GB ? kThreads + kGatherThreads : kThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi = smem + kStages * kStageBytes + 256;   // epilogue store stages
   __shared__ TileMap tm;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -533,9 +558,9 @@ __global__ void __launch_bounds__(GB ? kThreads + kGatherThreads : kThreads, 1)
       tile_coords(tm, args.groups, t, g, mt, nt);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      const int r_in = mt * BM + q * 32 + lane;          // row within group
-      store_tile<kMode>(args, tm, g, nt, r_in,
-                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
+      store_tile<kMode>(args, tm, g, nt, mt * BM + q * 32, lane,
+                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN,
+                        epi + q * kEpiStageBytes);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
@@ -668,6 +693,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
   uint64_t* tempty = tfull + 2;
   uint64_t* gfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + kStages2);
+  uint8_t* epi = smem + kStages2 * kStageBytes2 + 256;   // epilogue store stages
   __shared__ TileMap tm;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -789,9 +815,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
       tile_coords(tm, args.groups, t, g, mt, nt);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      const int r_in = mt * BM2 + (int)rank * 128 + q * 32 + lane;
-      store_tile<kMode>(args, tm, g, nt, r_in,
-                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN);
+      store_tile<kMode>(args, tm, g, nt, mt * BM2 + (int)rank * 128 + q * 32, lane,
+                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN,
+                        epi + q * kEpiStageBytes);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
@@ -1022,7 +1048,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.b_idx = b_idx;
   args.g_src = reinterpret_cast<const uint8_t*>(b);
   args.g_ld = (int64_t)N * 2;
-  const size_t smem = kStages * kStageBytes + 1024 + 256;
+  const size_t smem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiStageBytes;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
@@ -1078,7 +1104,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
-  const size_t smem2 = kStages2 * kStageBytes2 + 1024 + 256;
+  const size_t smem2 = (size_t)kStages2 * kStageBytes2 + 1024 + 256 + 4 * kEpiStageBytes;
   const int grid = sms & ~1;
   auto run = [&](auto kern, int threads) -> int {
     HM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));

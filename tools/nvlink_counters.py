@@ -28,7 +28,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2508_09591_b200 import _lib  # noqa: E402
 from paper_2508_09591_b200.layer import EPWorld, route_topk  # noqa: E402
 
-TX, RX = 138, 139    # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX (KiB)
+# (tx, rx, unit bytes): NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/_RX (KiB) and
+# NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES (bytes); per link, or all links
+# (scope 0xFFFFFFFF) -- whichever the driver implements is reported
+FIELDS = {"throughput_data": (138, 139, 1024), "count_bytes": (202, 204, 1)}
+ALL = 0xFFFFFFFF
 
 
 class Links:
@@ -45,19 +49,30 @@ class Links:
             except pynvml.NVMLError:
                 pass
 
-    def read(self) -> tuple[int, int]:
-        """(tx KiB, rx KiB) summed over the active links."""
-        ids = [(fid, link) for link in self.links for fid in (TX, RX)]
-        vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
-        tx = rx = 0
-        for (fid, _), f in zip(ids, vals):
-            if f.nvmlReturn != 0:
-                continue
-            if fid == TX:
-                tx += int(f.value.ullVal)
-            else:
-                rx += int(f.value.ullVal)
-        return tx, rx
+    def read(self) -> dict:
+        """{counter: (tx bytes, rx bytes)} per counter family and scope."""
+        out = {}
+        for name, (tx_id, rx_id, unit) in FIELDS.items():
+            for scope_name, scopes in (("per_link", self.links), ("all_links", [ALL])):
+                ids = [(fid, sc) for sc in scopes for fid in (tx_id, rx_id)]
+                try:
+                    vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
+                except self.nv.NVMLError:
+                    continue
+                tx = rx = 0
+                ok = False
+                for (fid, _), f in zip(ids, vals):
+                    if f.nvmlReturn != 0:
+                        continue
+                    ok = True
+                    v = int(f.value.ullVal) * unit
+                    if fid == tx_id:
+                        tx += v
+                    else:
+                        rx += v
+                if ok:
+                    out[f"{name}.{scope_name}"] = (tx, rx)
+        return out
 
 
 def main():
@@ -88,6 +103,7 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         t0 = links.read()
+        dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
@@ -114,8 +130,9 @@ def main():
             tx_rows, rx_rows = sent + recv, recv + sent
         ms = e0.elapsed_time(e1) / args.steps
         res[mode] = {"ms_per_step": ms,
-                     "nvlink_tx_bytes_per_step": (t1[0] - t0[0]) * 1024 / args.steps,
-                     "nvlink_rx_bytes_per_step": (t1[1] - t0[1]) * 1024 / args.steps,
+                     "counters_bytes_per_step": {
+                         k: [(t1[k][0] - t0[k][0]) / args.steps, (t1[k][1] - t0[k][1]) / args.steps]
+                         for k in t1 if k in t0},
                      "algorithmic_tx_bytes_per_step": tx_rows * rb,
                      "algorithmic_rx_bytes_per_step": rx_rows * rb}
         ep.close()
