@@ -179,6 +179,23 @@ int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int32_t mo
  * operand of the router logits GEMM (the step before the
  * path); no reference counterpart. */
 int hm_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream);
+/* Router GEMMs on the tcgen05 kernels (gating PAPER.md:112):
+ * hm_gemm_f32: out[rows][ld] fp32 (first n_valid columns) = A[rows][K] . B^T,
+ * B [N][K] bf16, N % 256 == 0 (zero-padded expert rows), rows_dev = device
+ * {rows}: the router logits x . Wr^T and the router data gradient dlogits . Wr.
+ * hm_wgrad_f32: out[m_out][N] fp32 (+= if accumulate) = A^T . B over the
+ * token rows of A [rows][m_out], B [rows][N]: the router weight gradient. */
+int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, const void* b, int32_t N,
+                int32_t K, int32_t n_valid, float* out, int64_t ld_out, void* stream);
+int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
+                 int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
+                 void* stream);
+/* Gate backward: dense bf16 dlogits [T][ld] (zero past E) from the gate
+ * weights' gradient dw [T][K]; mode 0 softmax over the picks (renormalised),
+ * 1 softmax over all experts, 2 DeepSeek-V3 normalised sigmoid (route_scale). */
+int hm_gate_backward(const float* logits, const int32_t* expert_ids, const float* weights,
+                     const float* dw, int64_t T, int32_t E, int32_t K, int32_t mode,
+                     float route_scale, void* dlogits, int32_t ld, void* stream);
 /* out = bf16((a + b) + c), fp32 sums, c may be NULL (b, c, out bf16; 16-byte
  * aligned): the layer's input gradient, router-GEMM term + routed dx (+ the
  * shared expert's dx), rounded once; no reference counterpart. */

@@ -9,7 +9,7 @@ RuntimeError (> 0, CUDA error).
 from __future__ import annotations
 
 import ctypes
-from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_void_p
+from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_size_t, c_void_p
 from pathlib import Path
 
 import torch
@@ -73,6 +73,12 @@ _SIGS = {
                                    c_void_p]),
     "hm_combine_grad": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "hm_bf16_to_f32": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "hm_gate_backward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                   c_int32, c_int32, c_float, c_void_p, c_int32, c_void_p]),
+    "hm_gemm_f32": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_int32, c_int32,
+                              c_void_p, c_int64, c_void_p]),
+    "hm_wgrad_f32": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_int32,
+                               c_void_p, c_int64, c_int32, c_void_p]),
     "hm_sum_to_bf16": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "hm_combine_add": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,

@@ -62,6 +62,10 @@ struct GemmArgs {
   const int32_t* b_idx;
   const uint8_t* g_src;
   int64_t g_ld;
+  // fp32 output (modes 0 / 3; the router GEMMs): outf [rows, ld_out] floats,
+  // only the first n_valid columns stored (a zero-padded expert dimension)
+  float* outf;
+  int n_valid;
 };
 
 
@@ -252,7 +256,8 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
 constexpr int kEpiStageBytes = 4096;   // per epilogue warp
 template <int U>
 __device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v,
-                                            __nv_bfloat16* dst0, int64_t ld, int nvalid) {
+                                            __nv_bfloat16* dst0, int64_t ld, int nvalid,
+                                            int umax = U) {
 #pragma unroll
   for (int u = 0; u < U; ++u)
     *reinterpret_cast<int4*>(sw + lane * (U * 16) + ((u ^ (lane % U)) << 4)) = v[u];
@@ -263,7 +268,7 @@ __device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v
   for (int p = 0; p < U; ++p) {
     const int r = p * R + rr;
     const int4 w = *reinterpret_cast<const int4*>(sw + r * (U * 16) + ((ur ^ (r % U)) << 4));
-    if (r < nvalid) *reinterpret_cast<int4*>(dst0 + (int64_t)r * ld + ur * 8) = w;
+    if (r < nvalid && ur < umax) *reinterpret_cast<int4*>(dst0 + (int64_t)r * ld + ur * 8) = w;
   }
   __syncwarp();
 }
@@ -274,18 +279,53 @@ __device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v
 // the warp's shared-memory store stage.
 template <int kMode>
 __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& tm, int g, int nt,
-                                           int r0, int lane, uint32_t tbase, uint8_t* sw,
-                                           int cb = 0, int ce = BN) {
-  const int r_in = r0 + lane;
+                                           int r0, int lane, uint32_t tbase, uint8_t* sw) {
   int nvalid = kMode >= 2 ? 32 : tm.rows[g] - r0;
   nvalid = nvalid < 0 ? 0 : (nvalid > 32 ? 32 : nvalid);
   const bool valid = lane < nvalid;
   const bool zero = kMode >= 2 && tm.rows[g] == 0;    // empty K: nothing accumulated
   const int64_t row_base = kMode >= 2 ? (int64_t)g * args.m_out + r0 : (int64_t)(tm.row0[g] + r0);
-  __nv_bfloat16* orow = args.out + (row_base + lane) * args.ld_out;
-  if (kMode == 1) {   // [cb, ce) in h columns (0..BN/2)
+  if (kMode != 1 && args.outf) {   // fp32 rows, 32 columns (128 B) per staged store
 #pragma unroll 1
-    for (int c = cb; c < ce; c += 32) {
+    for (int c2 = 0; c2 < BN; c2 += 64) {
+      if (nt * BN + c2 >= args.n_valid) break;
+      float v2[2][32];
+      tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int col = nt * BN + c2 + 32 * half;
+        if (col >= args.n_valid) break;
+        float* v = v2[half];
+        if (zero) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (kMode >= 2 && args.accumulate && valid) {
+          const float4* old = reinterpret_cast<const float4*>(args.outf + (row_base + lane) *
+                                                              args.ld_out + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 o = old[i];
+            v[4 * i] += o.x;
+            v[4 * i + 1] += o.y;
+            v[4 * i + 2] += o.z;
+            v[4 * i + 3] += o.w;
+          }
+        }
+        // 32 floats = 8 16-byte units (stage_store moves them as raw bits);
+        // a partial last chunk stores only its first (n_valid - col) / 4 units
+        const int um = (args.n_valid - col) >= 32 ? 8 : (args.n_valid - col) / 4;
+        stage_store<8>(sw, lane, reinterpret_cast<const int4*>(v),
+                       reinterpret_cast<__nv_bfloat16*>(args.outf + row_base * args.ld_out + col),
+                       args.ld_out * 2, nvalid, um);
+      }
+    }
+    return;
+  }
+  __nv_bfloat16* orow = args.out + (row_base + lane) * args.ld_out;
+  if (kMode == 1) {
+#pragma unroll 1
+    for (int c = 0; c < BN / 2; c += 32) {
       float gv[32], uv[32];
       tmem_ld32x2(tbase + c, tbase + BN / 2 + c, gv, uv);
       __align__(16) __nv_bfloat162 hv[16];
@@ -333,7 +373,7 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
     }
   } else {
 #pragma unroll 1
-    for (int c2 = cb; c2 < ce; c2 += 64) {
+    for (int c2 = 0; c2 < BN; c2 += 64) {
       float v2[2][32];
       tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
       __align__(16) __nv_bfloat162 hv[32];
@@ -1022,7 +1062,7 @@ int make_map_mn(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) 
 int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
                       const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
                       cudaStream_t s, int accumulate = 0, const int32_t* b_idx = nullptr,
-                      int64_t b_src_rows = 0) {
+                      int64_t b_src_rows = 0, float* out_f32 = nullptr) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
   HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
@@ -1048,6 +1088,8 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.b_idx = b_idx;
   args.g_src = reinterpret_cast<const uint8_t*>(b);
   args.g_ld = (int64_t)N * 2;
+  args.outf = out_f32;
+  args.n_valid = N;
   const size_t smem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiStageBytes;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
@@ -1073,11 +1115,13 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
                 cudaStream_t s, void* out2 = nullptr, const int32_t* a_idx = nullptr,
-                int64_t a_src_rows = 0) {
+                int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
   HM_CHECK_ARG(!a_idx || a_src_rows >= 1, "grouped gemm: gathered A needs its source rows");
+  HM_CHECK_ARG(!out_f32 || (!swiglu && n_valid % 4 == 0 && ld_out % 4 == 0),
+               "grouped gemm: fp32 output needs mode 0 and 16-byte rows / widths");
   CUtensorMap ma, mb;
   int st = make_map(&ma, a, (uint64_t)(a_idx ? a_src_rows : a_rows), (uint64_t)K, 128);
   if (st) return st;
@@ -1099,6 +1143,8 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.b_idx = nullptr;
   args.g_src = reinterpret_cast<const uint8_t*>(a);
   args.g_ld = (int64_t)K * 2;
+  args.outf = out_f32;
+  args.n_valid = n_valid > 0 ? n_valid : N;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
@@ -1139,6 +1185,32 @@ HM_API int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t
                            int64_t ld_out, void* stream) {
   return launch_gemm(a, a_rows, b, groups, n_rows, N, K, swiglu, out, ld_out, nullptr,
                      (cudaStream_t)stream);
+}
+
+// Router GEMMs on the same tcgen05 kernels, fp32 results:
+//   hm_gemm_f32: out[rows, ld] (fp32, first n_valid columns) = A[rows, K] . B^T,
+//     B [N][K] bf16 K-major (N a multiple of 256: pad the expert dimension with
+//     zero rows); rows_dev = device int32 {rows}.  Router logits = x . Wr^T
+//     (bf16 operands, fp32 accumulation; no fp32 copy of x), and the router
+//     data gradient dX = dlogits . Wr (B = Wr^T [M][E]).
+//   hm_wgrad_f32: out[m_out][N] (fp32, += if accumulate) = A^T . B over rows
+//     A [rows, m_out], B [rows, N] token-major (MN-major tcgen05 operands):
+//     the router weight gradient dWr = dlogits^T . x.
+HM_API int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, const void* b,
+                       int32_t N, int32_t K, int32_t n_valid, float* out, int64_t ld_out,
+                       void* stream) {
+  HM_CHECK_ARG(a && b && out && rows_dev, "hm_gemm_f32: null argument");
+  HM_CHECK_ARG(n_valid > 0 && n_valid <= N, "hm_gemm_f32: 0 < n_valid <= N");
+  return launch_gemm(a, rows > 0 ? rows : 1, b, 1, rows_dev, N, K, 0, nullptr, ld_out, nullptr,
+                     (cudaStream_t)stream, nullptr, nullptr, 0, out, n_valid);
+}
+
+HM_API int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
+                        int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
+                        void* stream) {
+  HM_CHECK_ARG(a && b && out && rows_dev, "hm_wgrad_f32: null argument");
+  return launch_gemm_wgrad(a, b, rows > 0 ? rows : 1, 1, rows_dev, m_out, N, nullptr, ld_out,
+                           (cudaStream_t)stream, accumulate, nullptr, 0, out);
 }
 
 // Expert SwiGLU FFN on expert-major rows: H = silu(X W1^T) * (X W3^T),

@@ -2392,6 +2392,94 @@ __global__ void __launch_bounds__(256) k_bf16_to_f32(const __nv_bfloat16* __rest
     dst[i] = __bfloat162float(src[i]);
 }
 
+// Gate backward: gradient of the router logits from the gate
+// weights' gradient dw [T, K], written as a dense bf16 row (the router GEMMs'
+// operand).  mode 0: softmax over the K picks (renormalised; Qwen3):
+// dlogit[ex_k] = w_k (dw_k - sum_j w_j dw_j); mode 1: softmax over all E:
+// dlogit_e = p_e (dp_e - sum p . dp) with dp = dw scattered to the picks;
+// mode 2: DeepSeek-V3 normalised sigmoid (w_k = c s_k / S, s = sigmoid):
+// dlogit[ex_k] = (c / S) (dw_k - sum_j dw_j w_j / c) s_k (1 - s_k).  Warp per
+// token: the lanes zero the row (16-byte stores), then lane k writes pick k.
+__global__ void __launch_bounds__(256) k_gate_backward(const float* __restrict__ logits,
+                                                       const int32_t* __restrict__ ex,
+                                                       const float* __restrict__ w,
+                                                       const float* __restrict__ dw, int64_t T,
+                                                       int E, int K, int mode, float scale,
+                                                       __nv_bfloat16* __restrict__ dlogits, int ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nw) {
+    const float* lg = logits + t * E;
+    __nv_bfloat16* out = dlogits + t * ld;
+    int e = -1;
+    float wk = 0.f, dk = 0.f;
+    if (lane < K) {
+      e = ex[t * K + lane];
+      wk = w[t * K + lane];
+      dk = dw[t * K + lane];
+    }
+    if (mode == 1) {   // softmax over all experts: every entry is nonzero
+      float mx = -INFINITY;
+      for (int c = lane; c < E; c += 32) mx = fmaxf(mx, lg[c]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float den = 0.f;
+      for (int c = lane; c < E; c += 32) den += __expf(lg[c] - mx);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+      float pd = lane < K && e >= 0 ? __expf(lg[e] - mx) / den * dk : 0.f;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) pd += __shfl_xor_sync(0xffffffffu, pd, o);
+      for (int c0 = 0; c0 < ld; c0 += 32) {   // warp-uniform trip count (shuffles)
+        const int c = c0 + lane;
+        float dp = 0.f;
+        for (int k = 0; k < K; ++k) {
+          const int ek = __shfl_sync(0xffffffffu, e, k);
+          const float dwk = __shfl_sync(0xffffffffu, dk, k);
+          if (ek == c) dp += dwk;
+        }
+        if (c < E) out[c] = __float2bfloat16(__expf(lg[c] - mx) / den * (dp - pd));
+        else if (c < ld) out[c] = __float2bfloat16(0.f);
+      }
+      continue;
+    }
+    // sparse modes: zero the row, then the K picks
+    for (int c = lane * 8; c < ld; c += 256)
+      *reinterpret_cast<int4*>(out + c) = make_int4(0, 0, 0, 0);
+    __syncwarp();
+    float g = 0.f;
+    if (mode == 0) {
+      float sdot = lane < K ? wk * dk : 0.f;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+      g = wk * (dk - sdot);
+    } else {   // mode 2
+      const float sk = lane < K && e >= 0 ? 1.f / (1.f + __expf(-lg[e])) : 0.f;
+      float ssum = sk, sdw = lane < K ? dk * wk : 0.f;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        sdw += __shfl_xor_sync(0xffffffffu, sdw, o);
+      }
+      g = (scale / ssum) * (dk - sdw / scale) * sk * (1.f - sk);
+    }
+    if (lane < K && e >= 0) out[e] = __float2bfloat16(g);
+  }
+}
+
+HM_API int hm_gate_backward(const float* logits, const int32_t* expert_ids, const float* weights,
+                            const float* dw, int64_t T, int32_t E, int32_t K, int32_t mode,
+                            float route_scale, void* dlogits, int32_t ld, void* stream) {
+  HM_CHECK_ARG(logits && expert_ids && weights && dw && dlogits, "hm_gate_backward: null argument");
+  HM_CHECK_ARG(ld >= E && ld % 8 == 0 && K >= 1 && K <= 32 && mode >= 0 && mode <= 2,
+               "hm_gate_backward: ld >= E, ld %% 8 == 0, 1 <= K <= 32, mode 0..2");
+  if (T <= 0) return 0;
+  k_gate_backward<<<grid_for(T, 8, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      logits, expert_ids, weights, dw, T, E, K, mode, route_scale, (__nv_bfloat16*)dlogits, ld);
+  HM_LAUNCHED();
+  return 0;
+}
+
 HM_API int hm_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream) {
   HM_CHECK_ARG(n >= 0 && (n == 0 || (src && dst)), "hm_bf16_to_f32: null argument");
   HM_CHECK_ARG(((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0,

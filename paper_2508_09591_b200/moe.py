@@ -22,17 +22,6 @@ from .migrate import ExpertStore
 from .routing import Placement, RoutingMask, load_placements, save_placements, save_trace
 
 
-class _tf32:
-    """Router GEMMs on TF32 tensor cores (cuBLAS); restores the global flag."""
-
-    def __enter__(self):
-        self.old = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = True
-
-    def __exit__(self, *exc):
-        torch.backends.cuda.matmul.allow_tf32 = self.old
-
-
 class HierMoELayer:
     def __init__(self, ranks: int, experts: int, top_k: int, hidden: int, inter: int,
                  tokens_per_rank: int, gpus: int = 1, gpu_index: int = 0, group=None,
@@ -127,6 +116,7 @@ class HierMoELayer:
         # the same model
         g = torch.Generator(device="cuda").manual_seed(seed)
         self.w_router = torch.randn(experts, hidden, device="cuda", generator=g) * hidden ** -0.5
+        self.refresh_router()
         n_loc = self.local * self.e_loc
         n_par = 3 * hidden * inter
         # expert state in a symmetric store: bf16 weights (used by the FFN), fp32
@@ -205,13 +195,21 @@ class HierMoELayer:
             self.g13_saved = self.g13s[0]
             self.dw13 = torch.zeros_like(self.w13)
             self.dw2 = torch.zeros_like(self.w2)
-            self.dw_router = torch.zeros_like(self.w_router)
+            # fp32 router weight grad, padded to the wgrad GEMM's 128-row tiles
+            self._dwr_pad = torch.zeros(self._e128, hidden, device="cuda")
+            self.dw_router = self._dwr_pad[:experts]
 
-    def refresh_transposed_weights(self) -> None:
-        """Transposed bf16 weights for the data-gradient GEMMs (after any
-        weight update or migration)."""
-        self.w13t = self.w13.transpose(2, 3).contiguous()
-        self.w2t = self.w2.transpose(2, 3).contiguous()
+    def refresh_transposed_weights(self, slot: int | None = None) -> None:
+        """Transposed bf16 weights for the data-gradient GEMMs (after a
+        weight update: every local slot; after a migration: ``slot`` only,
+        the local slot index whose weights changed)."""
+        if slot is None or not hasattr(self, "w13t"):
+            self.w13t = self.w13.transpose(2, 3).contiguous()
+            self.w2t = self.w2.transpose(2, 3).contiguous()
+            return
+        l, e = divmod(int(slot), self.e_loc)
+        self.w13t[l, e].copy_(self.w13[l, e].T)
+        self.w2t[l, e].copy_(self.w2[l, e].T)
 
     def set_placement(self, placement: Placement) -> None:
         self.placement = placement
@@ -227,13 +225,17 @@ class HierMoELayer:
         r, c = int(pair[0]), int(pair[1])
         self.set_placement(self.placement.swapped(r, c))
         self.store.migrate(r, c)
-        if self.grad:
-            self.refresh_transposed_weights()
+        if self.grad:   # re-transpose only the local slots whose weights moved
+            first = self.gpu_index * self.local * self.e_loc
+            for slot in {r, c}:
+                i = slot - first
+                if 0 <= i < self.local * self.e_loc:
+                    self.refresh_transposed_weights(i)
 
     @staticmethod
     def widen(x: torch.Tensor) -> torch.Tensor:
-        """fp32 copy of the activations for the router GEMM (16-byte
-        vectorised kernel for bf16, ``hm_bf16_to_f32``)."""
+        """fp32 copy of bf16 activations (16-byte vectorised kernel,
+        ``hm_bf16_to_f32``)."""
         if x.dtype != torch.bfloat16:
             return x.float()
         x = x.contiguous()
@@ -241,17 +243,43 @@ class HierMoELayer:
         _lib.call("hm_bf16_to_f32", ptr(x), ptr(xf), x.numel(), stream_ptr())
         return xf
 
-    def route(self, x: torch.Tensor, xf: torch.Tensor | None = None,
-              logits: torch.Tensor | None = None):
-        """Router logits (fp32 GEMM on the fp32 copy ``xf`` of x) -> top-K picks.
-        ``logits``, if given, receives the logits (kept for the backward)."""
-        if xf is None:
-            xf = self.widen(x)
-        with _tf32():
-            if logits is None:
-                logits = xf @ self.w_router.T
-            else:
-                torch.mm(xf, self.w_router.T, out=logits)
+    def refresh_router(self) -> None:
+        """bf16 operands of the router GEMMs from the fp32 router weights
+        (after a weight update): Wr [E_256][M] (expert rows zero-padded to the
+        GEMM's 256-column tile) and Wr^T [M][E_128] (the data gradient's B,
+        reduction zero-padded to 128)."""
+        e, m = self.experts, self.hidden
+        self._e256 = -(-e // 256) * 256
+        self._e128 = -(-e // 128) * 128
+        wb = self.w_router.to(torch.bfloat16)
+        self._wr = torch.zeros(self._e256, m, dtype=torch.bfloat16, device="cuda")
+        self._wr[:e] = wb
+        self._wrt = torch.zeros(m, self._e128, dtype=torch.bfloat16, device="cuda")
+        self._wrt[:, :e] = wb.T
+        self._rows = {}
+
+    def _rows_dev(self, t: int) -> torch.Tensor:
+        r = self._rows.get(t)
+        if r is None:
+            r = self._rows[t] = torch.tensor([t], dtype=torch.int32, device="cuda")
+        return r
+
+    def router_logits(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """fp32 router logits x . Wr^T on the tcgen05 GEMM (bf16 operands,
+        fp32 accumulation, hm_gemm_f32) -- no fp32 copy of x."""
+        x = x.contiguous()
+        t = x.shape[0]
+        if out is None:
+            out = torch.empty(t, self.experts, device="cuda")
+        if t:
+            _lib.call("hm_gemm_f32", ptr(x), t, ptr(self._rows_dev(t)), ptr(self._wr),
+                      self._e256, self.hidden, self.experts, ptr(out), self.experts, stream_ptr())
+        return out
+
+    def route(self, x: torch.Tensor, logits: torch.Tensor | None = None):
+        """Router logits (tcgen05 GEMM) -> top-K picks; ``logits``, if given,
+        receives the logits (kept for the backward)."""
+        logits = self.router_logits(x, logits)
         if self.router == "dsv3":
             return route_group_limited(logits, self.top_k, self.n_group, self.topk_group,
                                        self.score_bias, self.route_scale, self.expert_to_slot)
@@ -259,15 +287,13 @@ class HierMoELayer:
 
     def route_saved(self, x: torch.Tensor):
         """The forward's routing step: route x and, for a training layer, keep
-        what the backward needs (x, its fp32 copy and the router logits are
-        reused by the router backward)."""
+        what the backward needs (x and the router logits)."""
         self._x_cur = x
         if not self.grad:
             return self.route(x)
-        xf = self.widen(x)
         logits = torch.empty(x.shape[0], self.experts, device="cuda")
-        slot, w, ex = self.route(x, xf, logits)
-        self._saved = (x, xf, logits, slot, w, ex)
+        slot, w, ex = self.route(x, logits)
+        self._saved = (x, logits, slot, w, ex)
         return slot, w, ex
 
     def shared_forward(self, x: torch.Tensor) -> torch.Tensor:
@@ -428,7 +454,7 @@ class HierMoELayer:
         if not self.grad or self._saved is None:
             raise RuntimeError("HierMoELayer.backward needs grad=True and a forward first")
         self.check_status()
-        x, xf, logits, slot, w, ex = self._saved
+        x, logits, slot, w, ex = self._saved
         g = grad_out.contiguous()
         if self.shared_inter:   # shared expert backward beside the routed one
             cur = torch.cuda.current_stream()
@@ -481,24 +507,21 @@ class HierMoELayer:
                 wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])
         for st in self._streams[1:]:
             cur.wait_stream(st)
-        if self.router == "dsv3":
-            # w_k = c s_k / S, s = sigmoid(logit); the bias only steers selection
-            sk = torch.sigmoid(torch.gather(logits, 1, ex.long()))
-            c = self.route_scale
-            ds = (c / sk.sum(dim=1, keepdim=True)) * (dw - (dw * w).sum(dim=1, keepdim=True) / c)
-            dlogits = torch.zeros(x.shape[0], self.experts, device="cuda")
-            dlogits.scatter_(1, ex.long(), ds * sk * (1.0 - sk))
-        elif self.renormalize:   # softmax over the K picks
-            dsel = w * (dw - (w * dw).sum(dim=1, keepdim=True))
-            dlogits = torch.zeros(x.shape[0], self.experts, device="cuda")
-            dlogits.scatter_(1, ex.long(), dsel)
-        else:                    # softmax over all experts
-            p = torch.softmax(logits, dim=1)
-            dp = torch.zeros_like(p).scatter_(1, ex.long(), dw)
-            dlogits = p * (dp - (p * dp).sum(dim=1, keepdim=True))
-        with _tf32():
-            self.dw_router += dlogits.T @ xf
-            dxf = dlogits @ self.w_router
+        # gate backward on the device (dense bf16 dlogits, zero past E), then
+        # the router GEMMs on the tcgen05 kernels: dX_r = dlogits . Wr (fp32)
+        # and dWr += dlogits^T . x (fp32, accumulated)
+        t = x.shape[0]
+        mode = 2 if self.router == "dsv3" else (0 if self.renormalize else 1)
+        dlogits = torch.empty(t, self._e128, dtype=torch.bfloat16, device="cuda")
+        _lib.call("hm_gate_backward", ptr(logits), ptr(ex), ptr(w), ptr(dw), t, self.experts,
+                  self.top_k, mode, float(self.route_scale), ptr(dlogits), self._e128,
+                  stream_ptr())
+        dxf = torch.empty(t, self.hidden, device="cuda")
+        rows = self._rows_dev(t)
+        _lib.call("hm_gemm_f32", ptr(dlogits), t, ptr(rows), ptr(self._wrt), self.hidden,
+                  self._e128, self.hidden, ptr(dxf), self.hidden, stream_ptr())
+        _lib.call("hm_wgrad_f32", ptr(dlogits), ptr(x), t, ptr(rows), self._e128, self.hidden,
+                  ptr(self._dwr_pad), self.hidden, 1, stream_ptr())
         shared_dx = None
         if self.shared_inter:
             torch.cuda.current_stream().wait_event(self._shared_done)

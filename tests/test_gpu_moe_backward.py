@@ -23,7 +23,7 @@ def test_layer_backward_matches_autograd(hm, dedup):
     slot, w, ex = layer._saved[-3:]
     # reference: same picks, fp32 autograd
     xr = x.float().requires_grad_(True)
-    wr = layer.w_router.clone().requires_grad_(True)
+    wr = layer.w_router.to(torch.bfloat16).float().requires_grad_(True)   # the GEMM's operand
     nb = I // 128
     w13 = layer.w13.reshape(E, nb, 2, 128, M).float()
     w1 = w13[:, :, 0].reshape(E, I, M).clone().requires_grad_(True)
@@ -70,7 +70,7 @@ def test_layer_backward_dsv3_shared_matches_autograd(hm):
     layer.world.check_status()
     slot, w, ex = layer._saved[-3:]
     xr = x.float().requires_grad_(True)
-    wr = layer.w_router.clone().requires_grad_(True)
+    wr = layer.w_router.to(torch.bfloat16).float().requires_grad_(True)   # the GEMM's operand
 
     def split13(w13, n, i):
         v = w13.reshape(n, i // 128, 2, 128, M).float()

@@ -25,7 +25,11 @@ def test_layer_forward_matches_oracle(hm, dedup, shape):
     out = layer(x)
     torch.cuda.synchronize()
     layer.world.check_status()
-    logits = (x.float() @ layer.w_router.T).cpu().numpy()
+    # the layer's router logits (tcgen05 GEMM, bf16 operands, fp32 accumulation)
+    logits = layer.router_logits(x)
+    ref_l = x.float() @ layer.w_router.to(torch.bfloat16).float().T
+    torch.testing.assert_close(logits, ref_l, rtol=1e-4, atol=1e-4)
+    logits = logits.cpu().numpy()
     slot, w, _ = OM.route_topk(logits, K, layer.expert_to_slot.cpu().numpy())
     # experts in slot space: local rank l holds slots [l*E_loc, (l+1)*E_loc)
     e_loc = E // G
@@ -106,9 +110,7 @@ def test_layer_dsv3_router_shared_expert(hm, dedup):
     torch.cuda.synchronize()
     layer.world.check_status()
     slot, w, ex = layer.route(x)
-    from paper_2508_09591_b200.moe import _tf32
-    with _tf32():
-        logits = (x.float() @ layer.w_router.T).cpu().numpy()
+    logits = layer.router_logits(x).cpu().numpy()
     rs, rw, rex = OM.route_group_limited(logits, K, 4, 2, layer.score_bias.cpu().numpy(), 2.5,
                                          layer.expert_to_slot.cpu().numpy())
     assert np.array_equal(ex.cpu().numpy(), rex)
