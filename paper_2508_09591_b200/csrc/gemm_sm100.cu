@@ -38,7 +38,7 @@ constexpr int kThreads = 256;
 constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB
 constexpr uint32_t kBBytes = BN * BK * 2;   // 32 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
-constexpr int kMaxGroups = 64;
+constexpr int kMaxGroups = 256;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
 int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid (0 = all SMs)
 struct GemmArgs {
@@ -66,6 +66,11 @@ struct GemmArgs {
   // only the first n_valid columns stored (a zero-padded expert dimension)
   float* outf;
   int n_valid;
+  // several EP ranks' expert groups in one launch: groups [s * seg_groups,
+  // (s + 1) * seg_groups) are segment s, whose rows start at s * seg_rows
+  // (the [L][N_cap] expert-major buffers); seg_groups = 0: one segment
+  int seg_groups;
+  int64_t seg_rows;
 };
 
 
@@ -236,10 +241,21 @@ struct TileMap {
   int rows[kMaxGroups];         // rows of each group (wgrad: padded K extent)
 };
 
+// first row of each group: prefix sums of the group sizes, restarting at
+// every segment's base row
+__device__ __forceinline__ int seg_row0(const GemmArgs& a, int g, int run) {
+  return (a.seg_groups > 0 && g % a.seg_groups == 0) ? (int)((g / a.seg_groups) * a.seg_rows)
+                                                       : run;
+}
+
 __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t, int& g, int& mt,
                                             int& nt) {
-  g = 0;
-  while (g + 1 < groups && tm.start[g + 1] <= t) ++g;
+  int lo = 0, hi = groups - 1;   // last group with start <= t (binary search)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tm.start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  g = lo;
   int local = t - tm.start[g];
   mt = local / tm.ntile_n;
   nt = local % tm.ntile_n;
@@ -425,6 +441,7 @@ __global__ void __launch_bounds__(GB ? kThreads + kGatherThreads : kThreads, 1)
     for (int g = 0; g < args.groups; ++g) {
       int n = args.n_rows[g];
       if (kMode == 2) n = (n + BK - 1) / BK * BK;   // K padded to the k-block
+      row = seg_row0(args, g, row);
       tm.start[g] = acc;
       tm.row0[g] = row;
       tm.rows[g] = n;
@@ -746,6 +763,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
     for (int g = 0; g < args.groups; ++g) {
       int n = args.n_rows[g];
       if (kMode == 2) n = (n + BK - 1) / BK * BK;   // K padded to the k-block
+      row = seg_row0(args, g, row);
       tm.start[g] = acc;
       tm.row0[g] = row;
       tm.rows[g] = n;
@@ -935,34 +953,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
 // expert FFN backward helpers
 // group layout for the weight-gradient GEMMs: token rows of group g are
 // [row0_g, row0_g + n_g); as K columns they start at col0_g, padded to 64
-__global__ void k_group_layout(const int32_t* __restrict__ n_rows, int groups,
-                               int32_t* __restrict__ row0, int32_t* __restrict__ col0) {
+// used rows per segment (segments of seg_groups groups; rows of segment s
+// start at s * seg_rows): pre[0..segs] = prefix sums, the SwiGLU backward's
+// flat row space
+__global__ void k_group_layout(const int32_t* __restrict__ n_rows, int groups, int seg_groups,
+                               int32_t* __restrict__ pre) {
   if (threadIdx.x || blockIdx.x) return;
-  int r = 0, c = 0;
+  const int per = seg_groups > 0 ? seg_groups : groups;
+  int run = 0;
   for (int g = 0; g < groups; ++g) {
-    row0[g] = r;
-    col0[g] = c;
-    r += n_rows[g];
-    c += (n_rows[g] + BK - 1) / BK * BK;
+    if (g % per == 0) pre[g / per] = run;
+    run += n_rows[g];
   }
-  row0[groups] = r;
-  col0[groups] = c;
+  pre[(groups + per - 1) / per] = run;
 }
 
 // SwiGLU backward on 128-column gate/up interleaved pre-activations:
 // h = silu(a) u;  da = dh u silu'(a);  du = dh silu(a).
 __global__ void __launch_bounds__(256) k_swiglu_bwd_v8(const __nv_bfloat16* __restrict__ g13,
                                                        const __nv_bfloat16* __restrict__ dh,
-                                                       const int32_t* __restrict__ row0, int groups,
-                                                       int inter, __nv_bfloat16* __restrict__ dg13,
+                                                       const int32_t* __restrict__ pre, int segs,
+                                                       int64_t seg_rows, int inter,
+                                                       __nv_bfloat16* __restrict__ dg13,
                                                        __nv_bfloat16* __restrict__ h) {
-  const int rows = row0[groups];
+  const int rows = pre[segs];
   const int per_row = inter / 8;
   const int64_t n = (int64_t)rows * per_row;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / per_row);
-    const int j = 8 * (int)(i - (int64_t)r * per_row);
+    const int f = (int)(i / per_row);          // flat used row -> (segment, row)
+    int sg = 0;
+    while (sg + 1 < segs && pre[sg + 1] <= f) ++sg;
+    const int64_t r = sg * seg_rows + (f - pre[sg]);
+    const int j = 8 * (int)(i - (int64_t)f * per_row);
     const int b = j >> 7, c = j & 127;
     const int64_t ga = (int64_t)r * 2 * inter + 256 * b + c, gu = ga + 128;
     const int4 av = __ldg(reinterpret_cast<const int4*>(g13 + ga));
@@ -1062,7 +1085,8 @@ int make_map_mn(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) 
 int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
                       const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
                       cudaStream_t s, int accumulate = 0, const int32_t* b_idx = nullptr,
-                      int64_t b_src_rows = 0, float* out_f32 = nullptr) {
+                      int64_t b_src_rows = 0, float* out_f32 = nullptr, int seg_groups = 0,
+                      int64_t seg_rows = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
   HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
@@ -1090,6 +1114,8 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.g_ld = (int64_t)N * 2;
   args.outf = out_f32;
   args.n_valid = N;
+  args.seg_groups = seg_groups;
+  args.seg_rows = seg_rows;
   const size_t smem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiStageBytes;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
@@ -1115,7 +1141,8 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
 int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const int32_t* n_rows,
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
                 cudaStream_t s, void* out2 = nullptr, const int32_t* a_idx = nullptr,
-                int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0) {
+                int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0,
+                int seg_groups = 0, int64_t seg_rows = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -1145,6 +1172,8 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.g_ld = (int64_t)K * 2;
   args.outf = out_f32;
   args.n_valid = n_valid > 0 ? n_valid : N;
+  args.seg_groups = seg_groups;
+  args.seg_rows = seg_rows;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
@@ -1252,34 +1281,38 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
                         void* stream, int accumulate = 0, const int32_t* x_idx = nullptr,
-                        int64_t x_rows = 0) {
+                        int64_t x_rows = 0, int seg_groups = 0, int64_t seg_rows = 0) {
   cudaStream_t s = (cudaStream_t)stream;
   HM_CHECK_ARG(!x_idx || g13_saved,
                "ffn backward: gathered activations need the saved pre-activations");
   const int M = hidden, I = inter;
   int st;
   // gate/up pre-activations (recomputed unless the forward saved them), then dH
-  if (!g13_saved &&
-      (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I, nullptr, s)))
+  const int sg = seg_groups, segs = sg > 0 ? (groups + sg - 1) / sg : 1;
+  if (!g13_saved && (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I,
+                                      nullptr, s, nullptr, nullptr, 0, nullptr, 0, sg, seg_rows)))
     return st;
-  if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s))) return st;
-  int32_t* row0 = layout;
-  int32_t* col0 = layout + groups + 1;
-  k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, row0, col0);
+  if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s, nullptr,
+                        nullptr, 0, nullptr, 0, sg, seg_rows)))
+    return st;
+  k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, sg, layout);
   HM_LAUNCHED();
   HM_CHECK_ARG(I % 128 == 0, "ffn backward: inter must be a multiple of 128");
   k_swiglu_bwd_v8<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
-                                            row0, groups, I, (__nv_bfloat16*)dg13,
-                                            (__nv_bfloat16*)h);
+                                            layout, segs, sg > 0 ? seg_rows : 0, I,
+                                            (__nv_bfloat16*)dg13, (__nv_bfloat16*)h);
   HM_LAUNCHED();
   // data gradient
-  if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s))) return st;
+  if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s,
+                        nullptr, nullptr, 0, nullptr, 0, sg, seg_rows)))
+    return st;
   // weight gradients straight from the token-major activations (MN-major
   // tcgen05 operands), reduction over each expert's own rows
-  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate)))
+  if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate, nullptr,
+                              0, nullptr, sg, seg_rows)))
     return st;
   return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate,
-                           x_idx, x_rows);
+                           x_idx, x_rows, nullptr, sg, seg_rows);
 }
 
 HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
@@ -1333,4 +1366,45 @@ HM_API int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const in
   return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
                       const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
                       accumulate, idx, x_rows);
+}
+
+// Several EP ranks' expert FFNs in ONE launch per GEMM (a GPU hosting L ranks):
+// segment s = rank s's groups [s * groups_per_seg, (s + 1) * groups_per_seg)
+// with its expert-major rows at [s * seg_rows, ...) of every row buffer
+// (x / idx / h / y / g13 / gy / gx / dh / dg13: [segs][seg_rows][...]),
+// weights [segs * groups_per_seg][...] contiguous.  One grid over all tiles
+// instead of L launches: no per-rank fill / drain and one wave tail.  idx
+// null: x holds the materialised expert-major rows; otherwise row r of the
+// layout is x row idx[r] (fused dispatch).
+HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx,
+                               int64_t seg_rows, int32_t segs, const int32_t* n_rows,
+                               int32_t groups_per_seg, const void* w13, const void* w2,
+                               int32_t hidden, int32_t inter, void* h, void* y, void* g13,
+                               void* stream) {
+  HM_CHECK_ARG(x && segs >= 1 && groups_per_seg >= 1 && seg_rows >= 1,
+               "hm_expert_ffn_multi: bad argument");
+  const int groups = segs * groups_per_seg;
+  const int64_t rows = (int64_t)segs * seg_rows;
+  int st = launch_gemm(x, rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
+                       (cudaStream_t)stream, g13, idx, idx ? x_rows : 0, nullptr, 0,
+                       groups_per_seg, seg_rows);
+  if (st) return st;
+  return launch_gemm(h, rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
+                     (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, groups_per_seg,
+                     seg_rows);
+}
+
+HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,
+                                        int64_t seg_rows, int32_t segs, const int32_t* n_rows,
+                                        int32_t groups_per_seg, const void* w13t, const void* w2t,
+                                        const void* gy, int32_t hidden, int32_t inter,
+                                        const void* g13, void* dh, void* dg13, void* h,
+                                        int32_t* layout, void* gx, void* dw13, void* dw2,
+                                        int32_t accumulate, void* stream) {
+  HM_CHECK_ARG(x && g13 && segs >= 1 && groups_per_seg >= 1 && seg_rows >= 1,
+               "hm_expert_ffn_backward_multi: bad argument");
+  return ffn_backward(x, (int64_t)segs * seg_rows, n_rows, segs * groups_per_seg, nullptr, w13t,
+                      w2t, gy, hidden, inter, const_cast<void*>(g13), 1, dh, dg13, h, layout, gx,
+                      dw13, dw2, stream, accumulate, idx, idx ? x_rows : 0, groups_per_seg,
+                      seg_rows);
 }

@@ -13,8 +13,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .ffn import (FFNBackwardScratch, expert_ffn_backward_gather_ptrs, expert_ffn_backward_ptrs,
-                  expert_ffn_gather_ptrs, expert_ffn_ptrs, expert_ffn_save_ptrs, pack_w13)
+from .ffn import (FFNBackwardScratch, expert_ffn_backward_multi_ptrs, expert_ffn_backward_ptrs,
+                  expert_ffn_multi_ptrs, expert_ffn_ptrs, expert_ffn_save_ptrs, pack_w13)
 from . import _lib
 from ._lib import ptr, stream_ptr
 from .layer import EPWorld, route_group_limited, route_topk
@@ -176,7 +176,8 @@ class HierMoELayer:
                                                device="cuda")
         self.w13 = self.store["w13"].view(self.local, self.e_loc, 2 * inter, hidden)
         self.w2 = self.store["w2"].view(self.local, self.e_loc, hidden, inter)
-        self.hs = [torch.empty(wd.n_cap, inter, dtype=torch.bfloat16, device="cuda")
+        # one launch per GEMM covers every local rank ([L][n_cap] row segments)
+        self.hs = [torch.empty(self.local * wd.n_cap, inter, dtype=torch.bfloat16, device="cuda")
                    for wd in self.worlds]
         self.h = self.hs[0]
         self.set_placement(Placement.identity(experts))
@@ -188,7 +189,8 @@ class HierMoELayer:
         self.timeline = None          # [(label, event)] of the forward phases when a list
         if grad:
             self.refresh_transposed_weights()
-            self.bwd = FFNBackwardScratch(self.world.n_cap, self.e_loc, hidden, inter)
+            self.bwd = FFNBackwardScratch(self.local * self.world.n_cap, self.local * self.e_loc,
+                                          hidden, inter)
             # the forward keeps GEMM1's pre-activations per local rank (no recompute)
             self.g13s = [torch.empty(self.local, wd.n_cap, 2 * inter, dtype=torch.bfloat16,
                                      device="cuda") for wd in self.worlds]
@@ -314,23 +316,16 @@ class HierMoELayer:
         (of micro-batch ``mb``'s world)."""
         wd, h = self.worlds[mb], self.hs[mb]
         p_ne, _ = wd.buffer("n_e", 0)
-        for l in range(self.local):
-            rank = self.gpu_index * self.local + l
-            x_ptr, _ = wd.buffer("xmaj", l)
-            y_ptr, _ = wd.buffer("ymaj", l)
-            if self.fused:   # GEMM1 gathers the rows from the tokens themselves
-                xs = self._x_cur[self._mb_rows(mb)]
-                expert_ffn_gather_ptrs(xs.data_ptr(), xs.shape[0], wd.buffer("xidx", l)[0],
-                                       wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
-                                       self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr,
-                                       self.g13s[mb][l].data_ptr() if self.grad else 0)
-            elif self.grad:
-                expert_ffn_save_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
-                                     self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr,
-                                     self.g13s[mb][l].data_ptr())
-            else:
-                expert_ffn_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc, self.e_loc,
-                                self.w13[l], self.w2[l], self.hidden, self.inter, h, y_ptr)
+        first = self.gpu_index * self.local * self.e_loc   # this GPU's first slot
+        if self.fused:   # GEMM1 gathers the rows from the tokens themselves
+            xs = self._x_cur[self._mb_rows(mb)]
+            x_ptr, x_rows, idx = xs.data_ptr(), xs.shape[0], wd.buffer("xidx", 0)[0]
+        else:
+            x_ptr, x_rows, idx = wd.buffer("xmaj", 0)[0], self.local * wd.n_cap, 0
+        expert_ffn_multi_ptrs(x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first,
+                              self.e_loc, self.w13, self.w2, self.hidden, self.inter, h,
+                              wd.buffer("ymaj", 0)[0],
+                              self.g13s[mb].data_ptr() if self.grad else 0)
 
     def _mb_rows(self, mb: int) -> slice:
         n = self.local * self.tokens_per_rank // self.micro_batches
@@ -484,24 +479,17 @@ class HierMoELayer:
                 if ffn_done is not None:   # weight grads accumulate in micro-batch order
                     torch.cuda.current_stream().wait_event(ffn_done)
                 p_ne, _ = wd.buffer("n_e", 0)
-                for l in range(self.local):
-                    rank = self.gpu_index * self.local + l
-                    x_ptr, _ = wd.buffer("xmaj", l)
-                    gy_ptr, _ = wd.buffer("gy", l)
-                    gx_ptr, _ = wd.buffer("gx", l)
-                    if self.fused:
-                        xs = x[rows]
-                        expert_ffn_backward_gather_ptrs(
-                            xs.data_ptr(), xs.shape[0], wd.buffer("xidx", l)[0], wd.n_cap,
-                            p_ne + 4 * rank * self.e_loc, self.e_loc, self.w13t[l], self.w2t[l],
-                            gy_ptr, self.hidden, self.inter, self.bwd, gx_ptr, self.dw13[l],
-                            self.dw2[l], self.g13s[m][l].data_ptr(), accumulate=m > 0)
-                        continue
-                    expert_ffn_backward_ptrs(x_ptr, wd.n_cap, p_ne + 4 * rank * self.e_loc,
-                                             self.e_loc, self.w13[l], self.w13t[l], self.w2t[l],
-                                             gy_ptr, self.hidden, self.inter, self.bwd, gx_ptr,
-                                             self.dw13[l], self.dw2[l],
-                                             self.g13s[m][l].data_ptr(), accumulate=m > 0)
+                first = self.gpu_index * self.local * self.e_loc
+                if self.fused:
+                    xs = x[rows]
+                    x_ptr, x_rows, idx = xs.data_ptr(), xs.shape[0], wd.buffer("xidx", 0)[0]
+                else:
+                    x_ptr, x_rows, idx = wd.buffer("xmaj", 0)[0], self.local * wd.n_cap, 0
+                expert_ffn_backward_multi_ptrs(
+                    x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first, self.e_loc,
+                    self.w13t, self.w2t, wd.buffer("gy", 0)[0], self.hidden, self.inter, self.bwd,
+                    wd.buffer("gx", 0)[0], self.dw13, self.dw2, self.g13s[m].data_ptr(),
+                    accumulate=m > 0)
                 ffn_done = torch.cuda.Event()
                 ffn_done.record()
                 wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])

@@ -143,3 +143,53 @@ def test_saved_preactivations_match_recompute(hm):
         res.append((gx[:rows].clone(), dw13.clone(), dw2.clone()))
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+def test_multi_segment_ffn_equals_per_rank(hm):
+    """One launch per GEMM over several EP ranks' expert groups (row segments
+    [s * seg_rows, ...)) gives bit-identical forward outputs, pre-activations,
+    input grads and weight grads to one launch per rank."""
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_multi_ptrs,
+                                           expert_ffn_backward_ptrs, expert_ffn_multi_ptrs,
+                                           expert_ffn_save_ptrs)
+    torch.manual_seed(12)
+    S, Gs, M, I, cap = 3, 4, 512, 256, 1500
+    n = torch.randint(0, 350, (S * Gs,), dtype=torch.int32)
+    n[5] = 0
+    nr = n.cuda()
+    x = torch.randn(S, cap, M, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(S, cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(S, Gs, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(S, Gs, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    w13t, w2t = w13.transpose(2, 3).contiguous(), w2.transpose(2, 3).contiguous()
+    outs = []
+    for multi in (False, True):
+        h = torch.zeros(S * cap, I, dtype=torch.bfloat16, device="cuda")
+        y = torch.zeros(S, cap, M, dtype=torch.bfloat16, device="cuda")
+        g13 = torch.zeros(S, cap, 2 * I, dtype=torch.bfloat16, device="cuda")
+        gx = torch.zeros(S, cap, M, dtype=torch.bfloat16, device="cuda")
+        dw13 = torch.zeros_like(w13)
+        dw2 = torch.zeros_like(w2)
+        if multi:
+            sc = FFNBackwardScratch(S * cap, S * Gs, M, I)
+            expert_ffn_multi_ptrs(x.data_ptr(), S * cap, 0, cap, S, nr.data_ptr(), Gs, w13, w2,
+                                  M, I, h, y.data_ptr(), g13.data_ptr())
+            expert_ffn_backward_multi_ptrs(x.data_ptr(), S * cap, 0, cap, S, nr.data_ptr(), Gs,
+                                           w13t, w2t, gy.data_ptr(), M, I, sc, gx.data_ptr(),
+                                           dw13, dw2, g13.data_ptr())
+        else:
+            for s in range(S):
+                sc = FFNBackwardScratch(cap, Gs, M, I)
+                hs = torch.zeros(cap, I, dtype=torch.bfloat16, device="cuda")
+                np_ = nr[s * Gs:].data_ptr()
+                expert_ffn_save_ptrs(x[s].data_ptr(), cap, np_, Gs, w13[s], w2[s], M, I, hs,
+                                     y[s].data_ptr(), g13[s].data_ptr())
+                expert_ffn_backward_ptrs(x[s].data_ptr(), cap, np_, Gs, w13[s], w13t[s], w2t[s],
+                                         gy[s].data_ptr(), M, I, sc, gx[s].data_ptr(), dw13[s],
+                                         dw2[s], g13[s].data_ptr())
+        torch.cuda.synchronize()
+        used = [int(n[s * Gs:(s + 1) * Gs].sum()) for s in range(S)]
+        outs.append([torch.cat([t[s, :used[s]] for s in range(S)]) for t in (y, g13, gx)]
+                    + [dw13.clone(), dw2.clone()])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
