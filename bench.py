@@ -481,8 +481,9 @@ def main():
     red = (lambda t_: dist.all_reduce(t_)) if world > 1 else None
     choice = choose_transport(mask_from_ids(slot0, E), rtopo, rparams, None, red)
     MODE = choice.mode
-    # one GPU: fused dispatch (row indices; the expert GEMM gathers the rows)
-    FUSED = world == 1
+    # fused dispatch (row indices; the expert GEMM gathers the rows from x and,
+    # at N > 1, from the receive buffers) wherever the chosen transport allows it
+    FUSED = world == 1 or MODE in ("gpu", "remote")
     ep.set_fused(FUSED)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # 256 MB > L2
 
@@ -635,9 +636,14 @@ def main():
     src_gpu = np.arange(G) // L
     N_rem_in = int(cnt[src_gpu != rank][:, G:][:, slot_gpu == rank].sum())
     alg = {
-        # fused (one GPU): ids + rank_e read, epos + row index written per pick
-        "pack": T * K * 16 if FUSED else T * rb + (rem_dedup + loc_direct) * rb + rem_dedup * K * 8,
-        "expand": R_in * rb + N_rem_in * rb + R_in * K * 8,
+        # fused: one GPU -- ids + rank_e read, epos + row index written per
+        # pick; N > 1 -- rows read and pushed to the other GPUs hit, local
+        # picks get row indices, no local row copies
+        "pack": (T * K * 16 if world == 1 else
+                 T * rb + rem_dedup * rb + rem_dedup * K * 8 + T * K * 12) if FUSED
+                else T * rb + (rem_dedup + loc_direct) * rb + rem_dedup * K * 8,
+        # fused: meta read + row index written per received pick
+        "expand": R_in * K * 12 if FUSED else R_in * rb + N_rem_in * rb + R_in * K * 8,
         "reduce": N_rem_in * rb + R_in * rb + R_in * K * 8,
         "gather": (rem_dedup + loc_direct) * rb + T * rb,
     }
@@ -847,6 +853,7 @@ def main():
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
                 ev[0].record()
                 slot_l, w_l, ex_l = layer.route_saved(x)
+                layer.world.set_fused(layer.fused_now())
                 layer.world.dispatch(x, slot_l, w_l, dedup=layer.dedup)
                 ev[1].record()
                 layer.experts_forward()
@@ -913,12 +920,14 @@ def main():
             "combine_us": 1e3 * (seg_ms["reduce"] + seg_ms["barrier2"] + seg_ms["gather"]),
             "kernel_ms": {k: round(v, 4) for k, v in seg_ms.items()},
             "kernels": per_kernel,
-            "dispatch": "fused: row indices, GEMM1 gathers the rows (TMA gather4)" if FUSED
+            "dispatch": "fused: row indices (local tokens / received rows), GEMM1 gathers the "
+                        "rows with cp.async producer warps" if FUSED
                         else "copy: rows to the expert-major buffers",
             "materialized_dispatch": None if not FUSED else {
                 "ms_per_step": ms_copy, "value": tokens_total / (ms_copy * 1e-3),
                 "kernel_ms": {k: round(v, 4) for k, v in zip(SEGMENTS, seg_copy.tolist())},
-                "note": "the same step with the expert-major rows copied (k_pack_local)"},
+                "note": "the same step with the expert-major rows materialised (copying pack "
+                        "and destination re-expansion)"},
             "transport": MODE,
             "transport_choice": {"mode": choice.mode, "d_star": choice.d_star,
                                  "times_s": list(choice.times),

@@ -268,13 +268,16 @@ int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n
 /* Several EP ranks' expert FFNs in one launch per GEMM (a GPU hosting L
  * ranks): segment s = groups [s * groups_per_seg, (s + 1) * groups_per_seg)
  * with its rows at [s * seg_rows, ...) of every row buffer ([segs][seg_rows]);
- * idx null -> x holds the expert-major rows, else layout row r = x row idx[r]. */
-int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx, int64_t seg_rows,
-                        int32_t segs, const int32_t* n_rows, int32_t groups_per_seg,
+ * idx null -> x holds the expert-major rows, else layout row r = x row idx[r]
+ * (idx >= 0) or x_recv row ~idx[r] (idx < 0: rows received over NVLink). */
+int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx, const void* x_recv,
+                        int64_t seg_rows, int32_t segs, const int32_t* n_rows,
+                        int32_t groups_per_seg,
                         const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                         void* y, void* g13, void* stream);
 int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,
-                                 int64_t seg_rows, int32_t segs, const int32_t* n_rows,
+                                 const void* x_recv, int64_t seg_rows, int32_t segs,
+                                 const int32_t* n_rows,
                                  int32_t groups_per_seg, const void* w13t, const void* w2t,
                                  const void* gy, int32_t hidden, int32_t inter, const void* g13,
                                  void* dh, void* dg13, void* h, int32_t* layout, void* gx,

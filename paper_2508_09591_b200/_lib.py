@@ -108,14 +108,14 @@ _SIGS = {
                                                 c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                                 c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                                                 c_void_p]),
-    "hm_expert_ffn_multi": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int32, c_void_p,
-                                      c_int32, c_void_p, c_void_p, c_int32, c_int32, c_void_p,
-                                      c_void_p, c_void_p, c_void_p]),
-    "hm_expert_ffn_backward_multi": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int32,
-                                               c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
-                                               c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+    "hm_expert_ffn_multi": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
+                                      c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32,
+                                      c_void_p, c_void_p, c_void_p, c_void_p]),
+    "hm_expert_ffn_backward_multi": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                               c_int32, c_void_p, c_int32, c_void_p, c_void_p,
+                                               c_void_p, c_int32, c_int32, c_void_p, c_void_p,
                                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                               c_int32, c_void_p]),
+                                               c_void_p, c_int32, c_void_p]),
     "hm_expert_ffn_backward_saved": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p,
                                                c_void_p, c_void_p, c_int32, c_int32, c_void_p,
                                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

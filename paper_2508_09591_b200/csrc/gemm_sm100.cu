@@ -62,6 +62,9 @@ struct GemmArgs {
   const int32_t* b_idx;
   const uint8_t* g_src;
   int64_t g_ld;
+  // fused dispatch across GPUs: a negative index ~r names row r of g_src2
+  // (the receive buffer of rows that arrived over NVLink); same row pitch
+  const uint8_t* g_src2;
   // fp32 output (modes 0 / 3; the router GEMMs): outf [rows, ld_out] floats,
   // only the first n_valid columns stored (a zero-padded expert dimension)
   float* outf;
@@ -654,7 +657,9 @@ __global__ void __launch_bounds__(GB ? kThreads + kGatherThreads : kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int l = l0 + 16 * i;
-          const uint8_t* src = col + (int64_t)tok[i] * args.g_ld;
+          const int v = tok[i];
+          const uint8_t* src = v >= 0 ? col + (int64_t)v * args.g_ld
+                                      : col + (args.g_src2 - args.g_src) + (int64_t)(~v) * args.g_ld;
           const uint32_t dl = base + l * 128 + ((c ^ (l & 7)) << 4);
 #pragma unroll
           for (int j = 0; j < BN / 64; ++j) cp_async16(dl + j * 8192, src + j * 128);
@@ -922,7 +927,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
       for (int i = 0; i < 8; ++i) {
         const int r = mt * BM2 + (int)rank * 128 + r0 + 16 * i;   // row within the group
         const int row = tm.row0[g] + (r < tm.rows[g] ? r : 0);
-        src[i] = args.g_src + (int64_t)args.a_idx[row] * args.g_ld + c * 16;
+        const int v = args.a_idx[row];
+        src[i] = (v >= 0 ? args.g_src + (int64_t)v * args.g_ld
+                         : args.g_src2 + (int64_t)(~v) * args.g_ld) + c * 16;
       }
       for (int kb = 0; kb < kblocks_fixed; ++kb) {
         mbar_wait(empty + stage, phase ^ 1);
@@ -1086,7 +1093,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
                       const int32_t* n_rows, int m_out, int N, void* out, int64_t ld_out,
                       cudaStream_t s, int accumulate = 0, const int32_t* b_idx = nullptr,
                       int64_t b_src_rows = 0, float* out_f32 = nullptr, int seg_groups = 0,
-                      int64_t seg_rows = 0) {
+                      int64_t seg_rows = 0, const void* b_src2 = nullptr) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "wgrad gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0, "wgrad gemm: m_out %% 128 == 0 and N %% 256 == 0");
   HM_CHECK_ARG(a_rows >= 1, "wgrad gemm: empty operands");
@@ -1112,6 +1119,7 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.b_idx = b_idx;
   args.g_src = reinterpret_cast<const uint8_t*>(b);
   args.g_ld = (int64_t)N * 2;
+  args.g_src2 = reinterpret_cast<const uint8_t*>(b_src2 ? b_src2 : b);
   args.outf = out_f32;
   args.n_valid = N;
   args.seg_groups = seg_groups;
@@ -1142,7 +1150,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
                 cudaStream_t s, void* out2 = nullptr, const int32_t* a_idx = nullptr,
                 int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0,
-                int seg_groups = 0, int64_t seg_rows = 0) {
+                int seg_groups = 0, int64_t seg_rows = 0, const void* a_src2 = nullptr) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -1170,6 +1178,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.b_idx = nullptr;
   args.g_src = reinterpret_cast<const uint8_t*>(a);
   args.g_ld = (int64_t)K * 2;
+  args.g_src2 = reinterpret_cast<const uint8_t*>(a_src2 ? a_src2 : a);
   args.outf = out_f32;
   args.n_valid = n_valid > 0 ? n_valid : N;
   args.seg_groups = seg_groups;
@@ -1281,7 +1290,8 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
                         void* stream, int accumulate = 0, const int32_t* x_idx = nullptr,
-                        int64_t x_rows = 0, int seg_groups = 0, int64_t seg_rows = 0) {
+                        int64_t x_rows = 0, int seg_groups = 0, int64_t seg_rows = 0,
+                        const void* x_recv = nullptr) {
   cudaStream_t s = (cudaStream_t)stream;
   HM_CHECK_ARG(!x_idx || g13_saved,
                "ffn backward: gathered activations need the saved pre-activations");
@@ -1312,7 +1322,7 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                               0, nullptr, sg, seg_rows)))
     return st;
   return launch_gemm_wgrad(dg13, x, a_rows, groups, n_rows, 2 * I, M, dw13, M, s, accumulate,
-                           x_idx, x_rows, nullptr, sg, seg_rows);
+                           x_idx, x_rows, nullptr, sg, seg_rows, x_recv);
 }
 
 HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
@@ -1375,9 +1385,11 @@ HM_API int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const in
 // weights [segs * groups_per_seg][...] contiguous.  One grid over all tiles
 // instead of L launches: no per-rank fill / drain and one wave tail.  idx
 // null: x holds the materialised expert-major rows; otherwise row r of the
-// layout is x row idx[r] (fused dispatch).
+// layout is x row idx[r] (fused dispatch), or -- idx < 0 -- row ~idx[r] of
+// x_recv (the rows received over NVLink; fused dispatch at N > 1).
 HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx,
-                               int64_t seg_rows, int32_t segs, const int32_t* n_rows,
+                               const void* x_recv, int64_t seg_rows, int32_t segs,
+                               const int32_t* n_rows,
                                int32_t groups_per_seg, const void* w13, const void* w2,
                                int32_t hidden, int32_t inter, void* h, void* y, void* g13,
                                void* stream) {
@@ -1387,7 +1399,7 @@ HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx
   const int64_t rows = (int64_t)segs * seg_rows;
   int st = launch_gemm(x, rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
                        (cudaStream_t)stream, g13, idx, idx ? x_rows : 0, nullptr, 0,
-                       groups_per_seg, seg_rows);
+                       groups_per_seg, seg_rows, x_recv);
   if (st) return st;
   return launch_gemm(h, rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
                      (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, groups_per_seg,
@@ -1395,7 +1407,8 @@ HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx
 }
 
 HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,
-                                        int64_t seg_rows, int32_t segs, const int32_t* n_rows,
+                                        const void* x_recv, int64_t seg_rows, int32_t segs,
+                                        const int32_t* n_rows,
                                         int32_t groups_per_seg, const void* w13t, const void* w2t,
                                         const void* gy, int32_t hidden, int32_t inter,
                                         const void* g13, void* dh, void* dg13, void* h,
@@ -1406,5 +1419,5 @@ HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int
   return ffn_backward(x, (int64_t)segs * seg_rows, n_rows, segs * groups_per_seg, nullptr, w13t,
                       w2t, gy, hidden, inter, const_cast<void*>(g13), 1, dh, dg13, h, layout, gx,
                       dw13, dw2, stream, accumulate, idx, idx ? x_rows : 0, groups_per_seg,
-                      seg_rows);
+                      seg_rows, x_recv);
 }

@@ -849,7 +849,8 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
                                            const int32_t* __restrict__ eoff, int nchunks, int mode,
                                            int32_t* __restrict__ gpos, int32_t* __restrict__ epos_out,
                                            const int32_t* __restrict__ rank_g,
-                                           int32_t* __restrict__ gpos_g, int* __restrict__ status) {
+                                           int32_t* __restrict__ gpos_g, int* __restrict__ status,
+                                           int32_t* __restrict__ xidx) {
   const int C = w.G + w.E + w.P;
   const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
   const int64_t nvec = w.row_bytes / 16;
@@ -877,8 +878,14 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
   int ndst = 0;
   int64_t dst_row[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
   uint8_t* dst_base[kMaxRanks > kMaxK ? kMaxRanks : kMaxK];
+  // fused dispatch (xidx): picks on this GPU get the token's row index
+  // instead of a row copy (the expert GEMM gathers from x)
+  if (xidx && lane < w.K && my_e >= 0 && my_ep >= 0) {
+    const int d = rank_of_slot(w, my_e);
+    if (d / w.L == w.p) xidx[(int64_t)(d - w.p * w.L) * w.N_cap + my_ep] = (int32_t)t;
+  }
   // direct expert-major rows: every pick (mode 0) or picks on this GPU (modes 2, 3)
-  if (mode != 1) {
+  if (mode != 1 && !xidx) {
     for (int k = 0; k < w.K; ++k) {
       int e = __shfl_sync(0xffffffffu, my_e, k);
       int ep = __shfl_sync(0xffffffffu, my_ep, k);
@@ -915,8 +922,13 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
       }
       // the row lands directly in the expert-major slot of its first pick on
       // GPU q; the destination's expansion copies it to the remaining picks
+      // (fused: into q's receive buffer, whose row index the picks then get)
       const unsigned on = __ballot_sync(0xffffffffu, on_q && lane < w.K);
-      if (on) {
+      if (on && xidx) {
+        dst_base[ndst] = w.recv_g[q];
+        dst_row[ndst] = g;
+        ++ndst;
+      } else if (on) {
         const int k0 = __ffs(on) - 1;
         const int d0 = __shfl_sync(0xffffffffu, dr, k0);
         const int e0 = __shfl_sync(0xffffffffu, my_ep, k0);
@@ -990,7 +1002,8 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               int32_t* __restrict__ epos_out,
                                               const int32_t* __restrict__ rank_g,
                                               int32_t* __restrict__ gpos_g,
-                                              int* __restrict__ status) {
+                                              int* __restrict__ status,
+                                              int32_t* __restrict__ xidx) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t T = (int64_t)w.L * w.T_r;
@@ -1002,7 +1015,7 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
   for (int64_t i = warp; i < T; i += nw)
     pack_token(w, spread ? spread_index(i, T) : i, lane, x, ids, wts, chunk_off, rank_d,
                    rank_e, hitmask, offs, eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g,
-                   status);
+                   status, xidx);
 }
 
 // One-GPU pack (every destination local: modes 0, 2, 3 at P = 1): warp per
@@ -1515,6 +1528,39 @@ __global__ void __launch_bounds__(256) k_expand_g(const WorldDev* __restrict__ w
   }
 }
 
+// Fused dispatch at N > 1: the received rows stay in the receive buffers and
+// every local pick they carry gets the row's index in the receive space
+// (encoded ~r, so xidx >= 0 = local token, < 0 = received row): mode 3 rows
+// of recv_g (meta epos = l * N_cap + row), mode 2 rows of recv_x [L][R_cap]
+// (meta epos = row of rank l).  Replaces the row copies of k_expand(_g).
+__global__ void __launch_bounds__(256) k_index_recv_g(const WorldDev* __restrict__ wp,
+                                                      const Offsets* __restrict__ offs,
+                                                      int32_t* __restrict__ xidx) {
+  const WorldDev& w = *wp;
+  const RowMeta* meta = w.meta_g[w.p];
+  const int64_t n = (int64_t)offs->R_g * w.K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ep = meta[i].epos;
+    if (ep >= 0) xidx[ep] = ~(int32_t)(i / w.K);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_index_recv(const WorldDev* __restrict__ wp,
+                                                    const Offsets* __restrict__ offs,
+                                                    int32_t* __restrict__ xidx) {
+  const WorldDev& w = *wp;
+  for (int l = 0; l < w.L; ++l) {
+    const RowMeta* meta = w.recv_meta[w.p * w.L + l];
+    const int64_t n = (int64_t)offs->R[l] * w.K;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int ep = meta[i].epos;
+      if (ep >= 0) xidx[(int64_t)l * w.N_cap + ep] = ~(int32_t)(l * w.R_cap + i / w.K);
+    }
+  }
+}
+
 // ... and pre-reduced (sum_k w_k y_k over this GPU's picks), pushed straight
 // into the source rank's return buffer slot [this GPU][position]
 template <typename T, int VPL>
@@ -1621,7 +1667,9 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
         if (mode == 2 && d / w.L == w.p) continue;
         int gp = gpos[t * w.G + d];
         if (gp < 0) continue;
-        rrow[nr++] = w.recv_x[d] + (int64_t)gp * w.row_bytes;
+        // gradient rows go to comb (free in push-combine worlds), not recv_x:
+        // the fused dispatch's backward still gathers x rows from recv_x
+        rrow[nr++] = w.comb[d] + (int64_t)gp * w.row_bytes;
       }
     }
     float dot[kMaxK];
@@ -1775,7 +1823,7 @@ __global__ void __launch_bounds__(256) k_expand_grad(const WorldDev* __restrict_
     float dot[kMaxK];
 #pragma unroll
     for (int j = 0; j < kMaxK; ++j) dot[j] = 0.f;
-    const int4* src = reinterpret_cast<const int4*>(w.recv_x[dg] + r * w.row_bytes);
+    const int4* src = reinterpret_cast<const int4*>(w.comb[dg] + r * w.row_bytes);
     for (int64_t v = lane; v < nvec; v += 32) {
       float gf[Vec<T>::N];
       Vec<T>::to_f32(ld_nc_v4(src + v), gf);
@@ -2229,8 +2277,9 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
   int blocks = grid_for(T, 8, exch_blocks(w));
   const int64_t nv = h.row_bytes / 16;
   const bool local_only = h.P == 1 && mode != 1 && !h.U1;
-  HM_CHECK_ARG(!(w->fused && mode == 1),
-               "hm_dispatch: the fused dispatch writes expert-major row indices (modes 0, 2, 3)");
+  HM_CHECK_ARG(!(w->fused && (mode == 1 || (mode == 0 && h.P > 1))),
+               "hm_dispatch: the fused dispatch writes expert-major row indices (modes 2, 3; "
+               "mode 0 on one GPU)");
   if (local_only && w->fused) {
     SegScope sc(w, kSegPack, s);
     k_index_local<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(
@@ -2260,7 +2309,8 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
     SegScope sc(w, kSegPack, s);
     k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
                                   w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
-                                  w->gpos, w->epos, w->rank_g, w->gpos_g, w->status);
+                                  w->gpos, w->epos, w->rank_g, w->gpos_g, w->status,
+                                  w->fused ? w->xidx : nullptr);
   }
   HM_LAUNCHED();
   if (h.P > 1) {
@@ -2278,6 +2328,14 @@ HM_API int hm_expand(hm_world* w, void* stream) {
   if (w->last_mode == 3 && w->h.P == 1) return 0;    // one GPU: every row went direct
   int blocks = exch_blocks(w);
   SegScope sc(w, kSegExpand, (cudaStream_t)stream);
+  if (w->fused) {   // row indices into the receive buffers instead of row copies
+    if (w->last_mode == 3)
+      k_index_recv_g<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs, w->xidx);
+    else
+      k_index_recv<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs, w->xidx);
+    HM_LAUNCHED();
+    return 0;
+  }
   if (w->last_mode == 3)
     k_expand_g<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
   else
@@ -2748,8 +2806,7 @@ HM_API int hm_world_set_option(hm_world* w, int32_t option, int32_t value) {
   HM_CHECK_ARG(option == 4 || option == 10, "hm_world_set_option: unknown option %d", option);
   if (option == 4) w->max_blocks = value > 0 ? value : 0;
   if (option == 10) {
-    HM_CHECK_ARG(!value || (w->h.P == 1 && !w->h.U1),
-                 "hm_world_set_option: the fused dispatch needs a one-GPU, non-relay world");
+    HM_CHECK_ARG(!value || !w->h.U1, "hm_world_set_option: no fused dispatch on a relay world");
     if (value && !w->xidx) {
       HM_CUDA(cudaMalloc(&w->xidx, (size_t)w->h.L * w->h.N_cap * 4));
       HM_CUDA(cudaMemset(w->xidx, 0, (size_t)w->h.L * w->h.N_cap * 4));

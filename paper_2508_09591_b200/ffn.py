@@ -80,11 +80,13 @@ def expert_ffn_backward_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_row
 def expert_ffn_multi_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, seg_rows: int, segs: int,
                           n_rows_ptr: int, groups_per_seg: int, w13: torch.Tensor,
                           w2: torch.Tensor, hidden: int, inter: int, h: torch.Tensor, y_ptr: int,
-                          g13_ptr: int = 0) -> None:
+                          g13_ptr: int = 0, recv_ptr: int = 0) -> None:
     """All of a GPU's EP ranks' expert FFNs in one launch per GEMM (segments
     of ``groups_per_seg`` groups, rows at s * seg_rows); idx_ptr 0: x holds
-    the expert-major rows, else the rows are gathered from x by index."""
-    _lib.call("hm_expert_ffn_multi", x_ptr, x_rows, idx_ptr or None, seg_rows, segs, n_rows_ptr,
+    the expert-major rows, else the rows are gathered from x by index
+    (negative index ~r: row r of the receive buffer at recv_ptr)."""
+    _lib.call("hm_expert_ffn_multi", x_ptr, x_rows, idx_ptr or None, recv_ptr or None, seg_rows,
+              segs, n_rows_ptr,
               groups_per_seg, ptr(w13), ptr(w2), hidden, inter, ptr(h), y_ptr, g13_ptr or None,
               stream_ptr())
 
@@ -94,9 +96,10 @@ def expert_ffn_backward_multi_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, seg_ro
                                    w13t: torch.Tensor, w2t: torch.Tensor, gy_ptr: int, hidden: int,
                                    inter: int, sc: "FFNBackwardScratch", gx_ptr: int,
                                    dw13: torch.Tensor, dw2: torch.Tensor, g13_ptr: int,
-                                   accumulate: bool = False) -> None:
+                                   accumulate: bool = False, recv_ptr: int = 0) -> None:
     """Backward of expert_ffn_multi_ptrs (saved pre-activations)."""
-    _lib.call("hm_expert_ffn_backward_multi", x_ptr, x_rows, idx_ptr or None, seg_rows, segs,
+    _lib.call("hm_expert_ffn_backward_multi", x_ptr, x_rows, idx_ptr or None, recv_ptr or None,
+              seg_rows, segs,
               n_rows_ptr, groups_per_seg, ptr(w13t), ptr(w2t), gy_ptr, hidden, inter, g13_ptr,
               ptr(sc.dh), ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
               int(bool(accumulate)), stream_ptr())

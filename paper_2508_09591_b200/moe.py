@@ -100,14 +100,12 @@ class HierMoELayer:
         self._status_ev = None
         self.strict = False           # True: synchronise and check after every step
         self.world = self.worlds[0]
-        per_rank_copies = self.dedup == "all"    # dedup rows to every rank: copies by design
-        self.fused = (gpus == 1 and not per_rank_copies) if fused_dispatch is None \
-            else bool(fused_dispatch)
-        if self.fused and (gpus != 1 or per_rank_copies):
-            raise ValueError("the fused dispatch needs every EP rank on this GPU (gpus == 1) "
-                             "and a direct transport (not dedup='all')")
-        for wd in self.worlds:
-            wd.set_fused(self.fused)
+        # fused dispatch: expert-major row indices instead of row copies (one
+        # GPU: into x; N > 1 with per-rank / per-GPU dedup: into x for local
+        # picks, into the receive buffers for rows that crossed NVLink)
+        self.fused = (self.dedup != "all") if fused_dispatch is None else bool(fused_dispatch)
+        if self.fused and self.dedup == "all":
+            raise ValueError("the fused dispatch needs a direct transport (not dedup='all')")
         self._x_cur = None
         self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]
         self.grad = grad
@@ -311,21 +309,31 @@ class HierMoELayer:
                             self.shared_inter, self._shared_h, self._shared_y.data_ptr())
         return self._shared_y
 
+    def fused_now(self) -> bool:
+        """Whether this step's transport supports the fused dispatch (not the
+        raw transport across GPUs, whose rows land expert-major on the peer)."""
+        return self.fused and (self.gpus == 1 or self.dedup in (True, "gpu", "remote"))
+
+    def _rows_source(self, wd, x_rows_t: torch.Tensor):
+        """(x_ptr, x_rows, idx_ptr, recv_ptr) of the experts' A rows."""
+        if not wd.fused:
+            return wd.buffer("xmaj", 0)[0], self.local * wd.n_cap, 0, 0
+        recv = 0
+        if self.gpus > 1:   # rows that crossed NVLink: per-GPU (mode 3) / per-rank receive rows
+            recv = wd.buffer("recv_g" if self.dedup in (True, "gpu") else "recv_x", 0)[0]
+        return x_rows_t.data_ptr(), x_rows_t.shape[0], wd.buffer("xidx", 0)[0], recv
+
     def experts_forward(self, mb: int = 0) -> None:
         """SwiGLU FFN of every local rank's experts on its expert-major rows
-        (of micro-batch ``mb``'s world)."""
+        (of micro-batch ``mb``'s world), all ranks in one launch per GEMM."""
         wd, h = self.worlds[mb], self.hs[mb]
         p_ne, _ = wd.buffer("n_e", 0)
         first = self.gpu_index * self.local * self.e_loc   # this GPU's first slot
-        if self.fused:   # GEMM1 gathers the rows from the tokens themselves
-            xs = self._x_cur[self._mb_rows(mb)]
-            x_ptr, x_rows, idx = xs.data_ptr(), xs.shape[0], wd.buffer("xidx", 0)[0]
-        else:
-            x_ptr, x_rows, idx = wd.buffer("xmaj", 0)[0], self.local * wd.n_cap, 0
+        x_ptr, x_rows, idx, recv = self._rows_source(wd, self._x_cur[self._mb_rows(mb)])
         expert_ffn_multi_ptrs(x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first,
                               self.e_loc, self.w13, self.w2, self.hidden, self.inter, h,
                               wd.buffer("ymaj", 0)[0],
-                              self.g13s[mb].data_ptr() if self.grad else 0)
+                              self.g13s[mb].data_ptr() if self.grad else 0, recv)
 
     def _mb_rows(self, mb: int) -> slice:
         n = self.local * self.tokens_per_rank // self.micro_batches
@@ -407,6 +415,7 @@ class HierMoELayer:
                 if prev_d is not None:
                     s_m.wait_event(prev_d)
                 self._mark(f"dispatch{m}")
+                wd.set_fused(self.fused_now())
                 wd.dispatch(x[rows], slot[rows], w[rows], dedup=self.dedup)
                 prev_d = torch.cuda.Event()
                 prev_d.record(s_m)
@@ -480,16 +489,12 @@ class HierMoELayer:
                     torch.cuda.current_stream().wait_event(ffn_done)
                 p_ne, _ = wd.buffer("n_e", 0)
                 first = self.gpu_index * self.local * self.e_loc
-                if self.fused:
-                    xs = x[rows]
-                    x_ptr, x_rows, idx = xs.data_ptr(), xs.shape[0], wd.buffer("xidx", 0)[0]
-                else:
-                    x_ptr, x_rows, idx = wd.buffer("xmaj", 0)[0], self.local * wd.n_cap, 0
+                x_ptr, x_rows, idx, recv = self._rows_source(wd, x[rows])
                 expert_ffn_backward_multi_ptrs(
                     x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first, self.e_loc,
                     self.w13t, self.w2t, wd.buffer("gy", 0)[0], self.hidden, self.inter, self.bwd,
                     wd.buffer("gx", 0)[0], self.dw13, self.dw2, self.g13s[m].data_ptr(),
-                    accumulate=m > 0)
+                    accumulate=m > 0, recv_ptr=recv)
                 ffn_done = torch.cuda.Event()
                 ffn_done.record()
                 wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])

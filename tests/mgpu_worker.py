@@ -170,6 +170,38 @@ def run_migrate(rank, world):
     st.close()
 
 
+def run_layer_fused(rank, world):
+    """Fused dispatch across GPUs: local picks gathered from x, rows that crossed
+    NVLink gathered from the receive buffers (per-GPU dedup, mode 3, forward;
+    per-rank dedup, mode 2, forward + backward) -- outputs and gradients
+    bit-identical to the copying dispatch."""
+    from paper_2508_09591_b200.moe import HierMoELayer
+    G, E, K, M, I, T_r = 8, 64, 6, 512, 256, 96
+    L = G // world
+    gen = torch.Generator(device="cuda").manual_seed(40 + rank)
+    x = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    gout = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
+    for dedup, grad in (("gpu", False), ("remote", True)):
+        res = []
+        for fused in (False, True):
+            layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, dedup=dedup,
+                                 seed=3, grad=grad, fused_dispatch=fused, optimizer_state=False)
+            out = layer(x).clone()
+            got = [out]
+            if grad:
+                got += [layer.backward(gout).clone(), layer.dw13.clone(), layer.dw2.clone(),
+                        layer.dw_router.clone()]
+            torch.cuda.synchronize()
+            layer.check_status()
+            for wd in layer.worlds:
+                wd.check_status()
+            res.append(got)
+            layer.close()
+            dist.barrier()
+        for a, b in zip(*res):
+            assert torch.equal(a, b), ("fused", dedup)
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -184,6 +216,8 @@ def main():
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
             dist.barrier()
     run_migrate(rank, world)
+    dist.barrier()
+    run_layer_fused(rank, world)
     dist.barrier()
     run_planner(rank, world)
     dist.barrier()
