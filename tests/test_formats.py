@@ -50,3 +50,28 @@ def test_trace_errors(tmp_path):
     bad.write_text("iter,layer,tok,experts\n")
     with pytest.raises(hm.TraceFormatError):
         hm.load_trace(bad, 16)
+
+
+def test_runtime_params_packaged_and_loaded():
+    """The B200 alpha/beta of the runtime [P, L] transports ship in the
+    reference's params schema (tools/calibrate.py --runtime) and load into
+    the transport choice; a flat hierarchy uses the 'std' entry only."""
+    import json
+    from paper_2508_09591_b200.topology import load_params
+    from paper_2508_09591_b200.transport import PARAMS_DIR, default_params, runtime_topology
+    files = sorted(PARAMS_DIR.glob("b200_runtime_n*.json"))
+    assert [f.name for f in files] == ["b200_runtime_n2.json", "b200_runtime_n4.json"]
+    for f in files:
+        raw = json.loads(f.read_text())
+        assert set(raw) == {"std", "inter.1", "intra.1"}
+        p = load_params(f, 2)
+        assert p.alpha_std == raw["std"]["alpha"] and p.inter(1)[1] == raw["inter.1"]["beta"]
+    assert runtime_topology(8, 2, 128, 2048).level_fanouts == (2, 4)
+    assert runtime_topology(8, 4, 128, 2048).level_fanouts == (4, 2)
+    assert runtime_topology(8, 1, 128, 2048).level_fanouts == (8,)
+    assert runtime_topology(8, 8, 128, 2048).level_fanouts == (8,)
+    p2 = default_params(2, 2)
+    assert p2 == load_params(PARAMS_DIR / "b200_runtime_n2.json")
+    flat = default_params(8, 1)          # N = 8: nearest fit (n4), std entry only
+    n4 = load_params(PARAMS_DIR / "b200_runtime_n4.json")
+    assert flat.num_levels == 1 and flat.alpha_std == n4.alpha_std and flat.beta_std == n4.beta_std

@@ -65,6 +65,8 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         slot, w, _ = route_topk(lg, K, layer.expert_to_slot)
         e0.record()
+        layer._x_cur = x
+        layer.world.set_fused(layer.fused_now())
         layer.world.dispatch(x, slot, w, dedup=True)
         layer.experts_forward()
         layer.world.combine(slot, w, dedup=True)
@@ -81,8 +83,12 @@ def main():
         layer.apply_swap(plan.pair)
         p2.record()
         p2.synchronize()
+        kind = None
+        if plan.pair is not None:   # same GPU (local slice swap) or across GPUs (NVLink push)
+            per_gpu = layer.local * layer.e_loc
+            kind = "same_gpu" if plan.pair[0] // per_gpu == plan.pair[1] // per_gpu else "cross_gpu"
         log.append((step, rows[0].item(), rows[1].item(), plan.pair is not None,
-                    plan.predicted_saving, p0.elapsed_time(p1), p1.elapsed_time(p2)))
+                    plan.predicted_saving, p0.elapsed_time(p1), p1.elapsed_time(p2), kind))
     layer.world.check_status()
     layer.store.check_status()
     if rank == 0:
@@ -97,6 +103,17 @@ def main():
             "planner_ms_median": float(np.median([r[5] for r in log[5:]])),
             "migration_ms_median_when_swapped": float(np.median([r[6] for r in log[5:] if r[3]]))
             if any(r[3] for r in log[5:]) else None,
+            # per kind: a cross-GPU swap moves one expert each way (bytes_per_slot
+            # per direction over NVLink); a same-GPU swap exchanges two slices in HBM
+            "bytes_per_slot": layer.store.bytes_per_slot(),
+            "migration_by_kind": {
+                kd: {"swaps": len(ts), "median_ms": float(np.median(ts)),
+                     "GBps_per_direction": layer.store.bytes_per_slot() / (np.median(ts) * 1e-3) / 1e9
+                     if kd == "cross_gpu" else None,
+                     "HBM_GBps": 4 * layer.store.bytes_per_slot() / (np.median(ts) * 1e-3) / 1e9
+                     if kd == "same_gpu" else None}
+                for kd in ("same_gpu", "cross_gpu")
+                for ts in [[r[6] for r in log[5:] if r[7] == kd]] if ts},
             "trace": [[r[0], r[1], round(r[2], 4), r[3]] for r in log[::10]]}))
     layer.close()
     if world > 1:

@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--tokens", type=int, nargs="+", default=[4096, 8192, 16384, 32768, 65536])
     ap.add_argument("--topk", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--max-tokens-per-gpu", type=int, default=131072)
+    ap.add_argument("--hd2", action="store_true", help="also time the two-level relay worlds")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -74,14 +75,19 @@ def main():
             cap = 3 * t_r * k
             res = {"n_gpus": world, "tokens_per_rank": t_r, "top_k": k, "experts": E, "hidden": M}
             out = torch.empty_like(x)
-            for mode in ("gpu", "remote", "none"):
+            for mode, fused in (("gpu", False), ("remote", False), ("none", False),
+                                ("gpu", True), ("remote", True)):
                 ep = EPWorld(G, E, k, M, t_r, gpus=world, gpu_index=rank, n_cap_rows=cap)
+                ep.set_fused(fused)
 
                 def step():
                     ep.dispatch(x, slot, w, dedup=mode)
                     ep.combine(slot, w, dedup=mode, out=out)
 
-                res[f"flat_{mode}_ms"] = timed(step, world=world)
+                res[f"flat_{mode}{'_fused' if fused else ''}_ms"] = timed(step, world=world)
+                if fused:
+                    ep.close()
+                    continue
                 if mode == "gpu":
                     res["gpu_rows"] = int(ep.gpu_counts().sum())
                 if mode == "remote":
@@ -90,7 +96,21 @@ def main():
                     res["raw_rows"] = int(cnt[:, G:].sum())
                 ep.check_status()
                 ep.close()
-            for fan in ((2, 4), (4, 2)):
+            # the reference time model's transport choice on this mask with the
+            # B200 runtime fits (transport.py), next to the measured best
+            from paper_2508_09591_b200.transport import (choose_transport, default_params,
+                                                         runtime_topology)
+            rt = runtime_topology(G, world, E, M, 2)
+            red = (lambda t_: dist.all_reduce(t_)) if world > 1 else None
+            ch = choose_transport(hm.mask_from_ids(slot, E), rt, default_params(world, rt.num_levels),
+                                  None, red)
+            res["auto_mode"] = ch.mode
+            res["auto_model_us"] = [round(v * 1e6, 1) for v in ch.times] + \
+                [round(ch.time_without_dedup * 1e6, 1)]
+            meas = {m_: res[f"flat_{m_}_ms"] for m_ in ("gpu", "remote", "none")}
+            res["measured_best_mode"] = min(meas, key=meas.get)
+            res["auto_over_best"] = round(meas[ch.mode] / min(meas.values()), 3)
+            for fan in (((2, 4), (4, 2)) if args.hd2 else ()):
                 tw = TwoLevelWorld(fan, E, k, M, t_r, gpus=world, gpu_index=rank,
                                    n_cap_rows=cap)
 
