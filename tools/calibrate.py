@@ -20,11 +20,11 @@ in the reference schema.  Launch with torchrun for N > 1.
 layer's transport choice evaluates (paper_2508_09591_b200/transport.py):
 
   std      flat dispatch: "none" (one row per selection) and "remote" (one row
-           per (token, remote rank)) -- pack + barrier + expand, volume
+           per (token, remote rank), fused) -- pack + barrier + index, volume
            G * max rank count * token bytes (raw resp. dedup counts)
-  inter.1  the GPU-level dedup push ("gpu": pack + barrier), volume
+  inter.1  the GPU-level dedup push ("gpu", fused: pack + barrier), volume
            P * max per-GPU count * token bytes
-  intra.1  its re-expansion inside the GPU ("gpu": expand), volume
+  intra.1  its index step inside the GPU ("gpu": expand segment), volume
            L * max per-rank count * token bytes
 
     torchrun --nproc-per-node N tools/calibrate.py --runtime \
@@ -93,6 +93,9 @@ def runtime_fit(args, world: int, rank: int) -> None:
             ms = {"none": [], "remote": [], "inter": [], "intra": []}
             for it in range(10):
                 for mode in ("none", "remote", "gpu"):
+                    # the dedup transports run fused, as in the layer (row
+                    # indices instead of local copies and re-expansion)
+                    ep.set_fused(mode != "none")
                     ep.dispatch(x, slot, w, dedup=mode)
                     torch.cuda.synchronize()
                     sg = seg_list(ep)
