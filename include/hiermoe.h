@@ -165,6 +165,12 @@ int hm_route_group(const float* logits, int64_t T, int32_t E, int32_t K, int32_t
 int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts, int32_t dedup,
                 void* stream);
 /* Destination-side re-expansion of dedup rows into expert-major rows. */
+/* hm_dispatch in two phases: the plan (per-chunk ranks, count exchange,
+ * offsets) and the push (row movement + device barrier); hm_dispatch = both. */
+int hm_dispatch_plan(hm_world* w, const int32_t* ids, const float* wts, int32_t mode,
+                     void* stream);
+int hm_dispatch_push(hm_world* w, const void* x, const int32_t* ids, const float* wts,
+                     int32_t mode, void* stream);
 int hm_expand(hm_world* w, void* stream);
 /* Gate-weighted combine (pre-reduce per destination + source sum for dedup). */
 int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,

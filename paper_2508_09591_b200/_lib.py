@@ -68,6 +68,8 @@ _SIGS = {
                                  ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hm_dispatch": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_ffn_set_option": (c_int32, [c_int32, c_int32]),
+    "hm_dispatch_plan": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
+    "hm_dispatch_push": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
     "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                    c_void_p]),

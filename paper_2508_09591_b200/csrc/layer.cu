@@ -1097,11 +1097,12 @@ __global__ void __launch_bounds__(256) k_index_local(const WorldDev* __restrict_
       const int64_t t_in = t - (int64_t)s_loc * w.T_r;
       const int32_t* coff = chunk_off + ((int64_t)s_loc * nchunks + t_in / kChunk) * C;
       ep = eoff[s_loc * w.E + e] + coff[w.G + e] + rank_e[i];
+      const int d = rank_of_slot(w, e);
       if (ep >= w.N_cap) {
         atomicExch(status, 2);
         ep = -1;
-      } else {
-        xidx[(int64_t)(rank_of_slot(w, e) - w.p * w.L) * w.N_cap + ep] = (int32_t)t;
+      } else if (d / w.L == w.p) {   // picks on this GPU (every pick with one GPU)
+        xidx[(int64_t)(d - w.p * w.L) * w.N_cap + ep] = (int32_t)t;
       }
     }
     epos_out[i] = ep;
@@ -2225,9 +2226,16 @@ HM_API int hm_route_group(const float* logits, int64_t T, int32_t E, int32_t K, 
 
 // dispatch: plan + notify (+barrier) + pack + barrier.  x: [L*T_r, M] payload
 // rows of this GPU's local source ranks; ids/wts: [L*T_r, K] slot ids + gates.
-HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
-                       int32_t mode, void* stream) {
-  HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
+// The dispatch in two phases (hm_dispatch = both): plan = per-chunk plan +
+// count exchange + offsets (k_plan, k_notify); push = the row movement (pack /
+// index kernels + device barrier).  The counts are final after the plan, so a
+// caller may read them (e.g. the transport choice) before moving any row.
+static int dispatch_push(hm_world* w, const void* x, const int32_t* ids, const float* wts,
+                         int32_t mode, cudaStream_t s);
+
+HM_API int hm_dispatch_plan(hm_world* w, const int32_t* ids, const float* wts, int32_t mode,
+                            void* stream) {
+  HM_CHECK_ARG(w && ids, "hm_dispatch: null argument");
   HM_CHECK_ARG(mode >= 0 && mode <= 3,
                "hm_dispatch: mode must be 0 (raw), 1 (dedup per rank), 2 (dedup per remote rank), "
                "3 (dedup per remote GPU)");
@@ -2273,6 +2281,27 @@ HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const flo
                                   w->status, stage_cnt);
   }
   HM_LAUNCHED();
+  return 0;
+}
+
+HM_API int hm_dispatch_push(hm_world* w, const void* x, const int32_t* ids, const float* wts,
+                            int32_t mode, void* stream) {
+  HM_CHECK_ARG(w && x && ids, "hm_dispatch_push: null argument");
+  HM_CHECK_ARG(mode == w->last_mode, "hm_dispatch_push: mode differs from the plan's");
+  return dispatch_push(w, x, ids, wts, mode, (cudaStream_t)stream);
+}
+
+HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
+                       int32_t mode, void* stream) {
+  HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
+  int st = hm_dispatch_plan(w, ids, wts, mode, stream);
+  if (st) return st;
+  return dispatch_push(w, x, ids, wts, mode, (cudaStream_t)stream);
+}
+
+static int dispatch_push(hm_world* w, const void* x, const int32_t* ids, const float* wts,
+                         int32_t mode, cudaStream_t s) {
+  const WorldDev& h = w->h;
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
   const int64_t nv = h.row_bytes / 16;

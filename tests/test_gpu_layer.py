@@ -237,3 +237,32 @@ def test_route_quad_equals_lane(hm, E, K, renorm):
         _lib.call("hm_route_set_option", 1)     # the default
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dedup", ["gpu", "all", "none"])
+def test_dispatch_plan_then_push_equals_dispatch(hm, dedup):
+    """hm_dispatch = hm_dispatch_plan + hm_dispatch_push: the counts are final
+    after the plan, and the two phases move the same rows."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200._lib import ptr, stream_ptr
+    from paper_2508_09591_b200.layer import route_topk, transport_mode
+    G, E, K, M, T_r, dtype = CONFIGS["qwen3_small"]
+    logits, x = _inputs(G, E, K, M, T_r, dtype, seed=77)
+    slot, w, _ = route_topk(logits.cuda(), K)
+    xd = x.cuda()
+    world = _world(hm, G, E, K, M, T_r, dtype)
+    world.dispatch(xd, slot, w, dedup=dedup)
+    ref_counts = world.counts()
+    ref = world.combine(slot, w, dedup=dedup).clone()
+    mode = transport_mode(dedup)
+    _lib.call("hm_dispatch_plan", world._h, ptr(slot), ptr(w), mode, stream_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(world.counts(), ref_counts)
+    _lib.call("hm_dispatch_push", world._h, ptr(xd), ptr(slot), ptr(w), mode, stream_ptr())
+    if mode:
+        _lib.call("hm_expand", world._h, stream_ptr())
+    out = world.combine(slot, w, dedup=dedup)
+    torch.cuda.synchronize()
+    world.check_status()
+    assert torch.equal(out, ref)
+    world.close()
