@@ -9,12 +9,16 @@ RuntimeError (> 0, CUDA error).
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_size_t, c_void_p
 from pathlib import Path
 
 import torch
 
 LIB_PATH = Path(__file__).resolve().parent / "libhiermoe.so"
+# developer A/B runs only: HM_LIB=<path> loads another build of the same library
+if os.environ.get("HM_LIB"):
+    LIB_PATH = Path(os.environ["HM_LIB"])
 
 _lib = None
 

@@ -273,20 +273,33 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
 // stores skipped, GEMM2 ran at 1450 instead of 1077 TFLOP/s).  Rows >= nvalid
 // (past the group) are not written.
 constexpr int kEpiStageBytes = 4096;   // per epilogue warp
+__device__ __forceinline__ void sts128(uint32_t a, int4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
 template <int U>
 __device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v,
                                             __nv_bfloat16* dst0, int64_t ld, int nvalid,
                                             int umax = U) {
+  const uint32_t base = smem_u32(sw);   // explicit shared-window accesses (STS / LDS)
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    *reinterpret_cast<int4*>(sw + lane * (U * 16) + ((u ^ (lane % U)) << 4)) = v[u];
+  for (int u = 0; u < U; ++u) sts128(base + lane * (U * 16) + ((u ^ (lane % U)) << 4), v[u]);
   __syncwarp();
   constexpr int R = 32 / U;
   const int ur = lane % U, rr = lane / U;
 #pragma unroll
   for (int p = 0; p < U; ++p) {
     const int r = p * R + rr;
-    const int4 w = *reinterpret_cast<const int4*>(sw + r * (U * 16) + ((ur ^ (r % U)) << 4));
+    const int4 w = lds128(base + r * (U * 16) + ((ur ^ (r % U)) << 4));
     if (r < nvalid && ur < umax) *reinterpret_cast<int4*>(dst0 + (int64_t)r * ld + ur * 8) = w;
   }
   __syncwarp();
