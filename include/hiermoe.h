@@ -221,6 +221,11 @@ int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float* dw, vo
  * The only dense contraction of the layer (E expert FFNs); no
  * reference implementation.  Groups are consecutive row blocks of A with
  * device-side sizes n_rows[g] (the dispatch's expert-major layout). */
+/* hm_grouped_gemm with B as stored, [groups][K][N] (read MN-major by the
+ * tensor cores): the data-gradient GEMMs on the expert weights themselves. */
+int hm_grouped_gemm_kn(const void* a, int64_t a_rows, const void* b, int32_t groups,
+                       const int32_t* n_rows, int32_t N, int32_t K, void* out, int64_t ld_out,
+                       void* stream);
 int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t groups,
                     const int32_t* n_rows, int32_t N, int32_t K, int32_t swiglu, void* out,
                     int64_t ld_out, void* stream);
@@ -249,25 +254,24 @@ int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* idx, int6
  * grads to dw13 / dw2. */
 int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const int32_t* idx,
                                   int64_t a_rows, const int32_t* n_rows, int32_t groups,
-                                  const void* w13t, const void* w2t, const void* gy,
+                                  const void* w13, const void* w2, const void* gy,
                                   int32_t hidden, int32_t inter, const void* g13, void* dh,
                                   void* dg13, void* h, int32_t* layout, void* gx, void* dw13,
                                   void* dw2, int32_t accumulate, void* stream);
-/* Expert FFN backward: recomputed pre-activations, dgrad GEMMs with
- * transposed weights (w13t [g][M][2I], w2t [g][I][M]), SwiGLU backward, and
- * weight-gradient GEMMs over each expert's own token rows (MN-major tcgen05
- * operands read the token-major activations directly). */
+/* Expert FFN backward: pre-activations recomputed (GEMM1), data-gradient
+ * GEMMs on the weights as stored (w13 [g][2I][M], w2 [g][M][I], read MN-major
+ * by the tensor cores -- no transposed copies), SwiGLU backward, and
+ * weight-gradient GEMMs over each expert's own token rows. */
 int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
-                           const void* w13, const void* w13t, const void* w2t, const void* gy,
-                           int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
-                           void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
-                           void* stream);
+                           const void* w13, const void* w2, const void* gy, int32_t hidden,
+                           int32_t inter, void* g13, void* dh, void* dg13, void* h,
+                           int32_t* layout, void* gx, void* dw13, void* dw2, void* stream);
 /* hm_expert_ffn_backward with g13 holding the forward's pre-activations
  * (hm_expert_ffn_save): skips the GEMM1 recompute.  accumulate != 0 adds the
  * weight grads to dw13 / dw2 (fp32 add of the stored bf16): one call per
  * micro-batch of a layer. */
 int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                 int32_t groups, const void* w13t, const void* w2t,
+                                 int32_t groups, const void* w13, const void* w2,
                                  const void* gy, int32_t hidden, int32_t inter, const void* g13,
                                  void* dh, void* dg13, void* h, int32_t* layout, void* gx,
                                  void* dw13, void* dw2, int32_t accumulate, void* stream);
@@ -284,7 +288,7 @@ int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx, const
 int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,
                                  const void* x_recv, int64_t seg_rows, int32_t segs,
                                  const int32_t* n_rows,
-                                 int32_t groups_per_seg, const void* w13t, const void* w2t,
+                                 int32_t groups_per_seg, const void* w13, const void* w2,
                                  const void* gy, int32_t hidden, int32_t inter, const void* g13,
                                  void* dh, void* dg13, void* h, int32_t* layout, void* gx,
                                  void* dw13, void* dw2, int32_t accumulate, void* stream);

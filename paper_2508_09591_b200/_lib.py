@@ -89,6 +89,8 @@ _SIGS = {
     "hm_combine": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "hm_combine_add": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
                                  c_void_p]),
+    "hm_grouped_gemm_kn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32,
+                                     c_int32, c_void_p, c_int64, c_void_p]),
     "hm_grouped_gemm": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int32,
                                   c_int32, c_int32, c_void_p, c_int64, c_void_p]),
     "hm_store_create": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int32, POINTER(c_void_p)]),
@@ -99,9 +101,9 @@ _SIGS = {
     "hm_store_status": (c_int32, [c_void_p, c_void_p]),
     "hm_migrate": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "hm_expert_ffn_backward": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
-                                         c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
+                                         c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                         c_void_p, c_void_p]),
+                                         c_void_p]),
     "hm_expert_ffn": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "hm_expert_ffn_save": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,

@@ -727,13 +727,16 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
       : "memory");
 }
+template <uint32_t IDESC = kIdesc2>
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                                uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
+// ... with B MN-major (bit 16: transpose B): the weights used as stored
+constexpr uint32_t kIdesc2BMN = kIdesc2 | (1u << 16);
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -753,7 +756,10 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
 // of each CTA with cp.async into its swizzled stage; they arrive on a local
 // gfull barrier, and warp 2's lane 0 forwards each completed stage to the
 // leader's full barrier (which then counts the B TMA bytes + 2 forwarders)
-template <int kMode, bool GA = false>
+// BMN: B read MN-major straight from [groups][K][N] weights (two 64 x 64 TMA
+// boxes per CTA and k-block, the tcgen05 transpose-B bit) -- the data-gradient
+// GEMMs then need no transposed weight copies
+template <int kMode, bool GA = false, bool BMN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGatherThreads : kThreads, 1)
     k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
@@ -835,7 +841,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
           if (leader) mbar_expect_tx(full + stage, GA ? 2 * kHalfBytes : 2 * kStageBytes2);
           if (!GA)
             tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
-          tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, k0 + kb * BK, brow);
+          if (BMN) {   // B [g][K][N]: rows g * K + k, 64-column chunks of this CTA's 128
+            const int bcol = nt * BN + (int)rank * 128;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_2d_pair(sb + stage * kHalfBytes + j * 8192, &map_b, full + stage,
+                               bcol + 64 * j, g * args.K + kb * BK);
+          } else {
+            tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, k0 + kb * BK, brow);
+          }
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
@@ -869,9 +883,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
           const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
           const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)
-            umma_bf16_pair(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
-                           (kb | k) ? 1u : 0u);
+          for (int k = 0; k < BK / UK; ++k) {
+            if (BMN)
+              umma_bf16_pair<kIdesc2BMN>(d, smem_desc(a0 + k * UK * 2),
+                                         smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+            else
+              umma_bf16_pair(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
+                             (kb | k) ? 1u : 0u);
+          }
           umma_commit_pair(empty + stage);
           if (++stage == kStages2) {
             stage = 0;
@@ -1163,7 +1182,8 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
                 int N, int K, int swiglu, void* out, int64_t ld_out, int* status,
                 cudaStream_t s, void* out2 = nullptr, const int32_t* a_idx = nullptr,
                 int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0,
-                int seg_groups = 0, int64_t seg_rows = 0, const void* a_src2 = nullptr) {
+                int seg_groups = 0, int64_t seg_rows = 0, const void* a_src2 = nullptr,
+                bool b_mn = false) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -1173,8 +1193,10 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   CUtensorMap ma, mb;
   int st = make_map(&ma, a, (uint64_t)(a_idx ? a_src_rows : a_rows), (uint64_t)K, 128);
   if (st) return st;
-  st = make_map(&mb, b, (uint64_t)groups * N, (uint64_t)K, 128);
+  st = b_mn ? make_map_mn(&mb, b, (uint64_t)groups * K, (uint64_t)N)
+            : make_map(&mb, b, (uint64_t)groups * N, (uint64_t)K, 128);
   if (st) return st;
+  HM_CHECK_ARG(!b_mn || (!a_idx && !swiglu), "grouped gemm: MN-major B only for mode 0");
   GemmArgs args;
   args.m_out = 0;
   args.n_rows = n_rows;
@@ -1209,6 +1231,7 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
     return launch_status();
   };
   const int thr_g = kThreads + kGatherThreads;   // + the A-gather warps
+  if (b_mn) return run(k_grouped_gemm_pair<0, false, true>, kThreads);
   if (a_idx) return swiglu ? run(k_grouped_gemm_pair<1, true>, thr_g)
                            : run(k_grouped_gemm_pair<0, true>, thr_g);
   return swiglu ? run(k_grouped_gemm_pair<1>, kThreads) : run(k_grouped_gemm_pair<0>, kThreads);
@@ -1236,6 +1259,15 @@ HM_API int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t
                            int64_t ld_out, void* stream) {
   return launch_gemm(a, a_rows, b, groups, n_rows, N, K, swiglu, out, ld_out, nullptr,
                      (cudaStream_t)stream);
+}
+
+// ... with B given as stored [groups][K][N] (N contiguous): out = A . B_g,
+// read MN-major by the tensor cores (no transposed copy of B)
+HM_API int hm_grouped_gemm_kn(const void* a, int64_t a_rows, const void* b, int32_t groups,
+                              const int32_t* n_rows, int32_t N, int32_t K, void* out,
+                              int64_t ld_out, void* stream) {
+  return launch_gemm(a, a_rows, b, groups, n_rows, N, K, 0, out, ld_out, nullptr,
+                     (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr, true);
 }
 
 // Router GEMMs on the same tcgen05 kernels, fp32 results:
@@ -1291,15 +1323,16 @@ HM_API int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_ro
 }
 
 // Expert SwiGLU FFN backward (tcgen05 GEMMs + SwiGLU backward):
-//   G13 = X W13^T (recomputed pre-activations unless saved), dH = gY W2 (via
-//   W2^T), dG13 = swiglu'(G13, dH), H = swiglu(G13), gX = dG13 W13 (via
-//   W13^T), dW2 = gY^T H, dW13 = dG13^T X (weight-gradient GEMMs over each
-//   expert's own token rows, MN-major operands; x_idx: X's rows gathered).
+//   G13 = X W13^T (recomputed pre-activations unless saved), dH = gY W2,
+//   dG13 = swiglu'(G13, dH), H = swiglu(G13), gX = dG13 W13 (both data-gradient
+//   GEMMs read the weights as stored, MN-major: no transposed copies),
+//   dW2 = gY^T H, dW13 = dG13^T X (weight-gradient GEMMs over each expert's own
+//   token rows, MN-major operands; x_idx: X's rows gathered).
 // Buffers (rows = a_rows capacity): g13, dg13 [rows, 2I]; dh, h [rows, I];
 // layout: 2*(groups+1) int32 scratch.  Outputs: gx [rows, M],
 // dw13 [groups][2I][M], dw2 [groups][M][I] (accumulate: added to).
 static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
-                        const void* w13, const void* w13t, const void* w2t, const void* gy,
+                        const void* w13, const void* w2, const void* gy,
                         int32_t hidden, int32_t inter, void* g13, int g13_saved, void* dh,
                         void* dg13, void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
                         void* stream, int accumulate = 0, const int32_t* x_idx = nullptr,
@@ -1315,8 +1348,9 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
   if (!g13_saved && (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I,
                                       nullptr, s, nullptr, nullptr, 0, nullptr, 0, sg, seg_rows)))
     return st;
-  if ((st = launch_gemm(gy, a_rows, w2t, groups, n_rows, I, M, 0, dh, I, nullptr, s, nullptr,
-                        nullptr, 0, nullptr, 0, sg, seg_rows)))
+  // dH = gY W2: W2 [g][M][I] as stored = B [K = M][N = I], read MN-major
+  if ((st = launch_gemm(gy, a_rows, w2, groups, n_rows, I, M, 0, dh, I, nullptr, s, nullptr,
+                        nullptr, 0, nullptr, 0, sg, seg_rows, nullptr, true)))
     return st;
   k_group_layout<<<1, 32, 0, s>>>(n_rows, groups, sg, layout);
   HM_LAUNCHED();
@@ -1325,9 +1359,9 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                                             layout, segs, sg > 0 ? seg_rows : 0, I,
                                             (__nv_bfloat16*)dg13, (__nv_bfloat16*)h);
   HM_LAUNCHED();
-  // data gradient
-  if ((st = launch_gemm(dg13, a_rows, w13t, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s,
-                        nullptr, nullptr, 0, nullptr, 0, sg, seg_rows)))
+  // data gradient gX = dG13 W13: W13 [g][2I][M] as stored = B [K = 2I][N = M]
+  if ((st = launch_gemm(dg13, a_rows, w13, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s,
+                        nullptr, nullptr, 0, nullptr, 0, sg, seg_rows, nullptr, true)))
     return st;
   // weight gradients straight from the token-major activations (MN-major
   // tcgen05 operands), reduction over each expert's own rows
@@ -1339,24 +1373,24 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
 }
 
 HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                  int32_t groups, const void* w13, const void* w13t,
-                                  const void* w2t, const void* gy, int32_t hidden, int32_t inter,
-                                  void* g13, void* dh, void* dg13, void* h, int32_t* layout,
-                                  void* gx, void* dw13, void* dw2, void* stream) {
-  return ffn_backward(x, a_rows, n_rows, groups, w13, w13t, w2t, gy, hidden, inter, g13, 0, dh,
-                      dg13, h, layout, gx, dw13, dw2, stream);
+                                  int32_t groups, const void* w13, const void* w2, const void* gy,
+                                  int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
+                                  void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
+                                  void* stream) {
+  return ffn_backward(x, a_rows, n_rows, groups, w13, w2, gy, hidden, inter, g13, 0, dh, dg13, h,
+                      layout, gx, dw13, dw2, stream);
 }
 
 // ... with g13 holding the forward's pre-activations (hm_expert_ffn_save): no
 // GEMM1 recompute; accumulate != 0 adds the weight grads to dw13 / dw2
 // (micro-batched layers: one call per micro-batch)
 HM_API int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int32_t* n_rows,
-                                        int32_t groups, const void* w13t, const void* w2t,
+                                        int32_t groups, const void* w13, const void* w2,
                                         const void* gy, int32_t hidden, int32_t inter,
                                         const void* g13, void* dh, void* dg13, void* h,
                                         int32_t* layout, void* gx, void* dw13, void* dw2,
                                         int32_t accumulate, void* stream) {
-  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
+  return ffn_backward(x, a_rows, n_rows, groups, w13, w2, gy, hidden, inter,
                       const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
                       accumulate);
 }
@@ -1381,12 +1415,12 @@ HM_API int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* id
 // from x by the same row indices; accumulate adds the weight grads
 HM_API int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const int32_t* idx,
                                          int64_t a_rows, const int32_t* n_rows, int32_t groups,
-                                         const void* w13t, const void* w2t, const void* gy,
+                                         const void* w13, const void* w2, const void* gy,
                                          int32_t hidden, int32_t inter, const void* g13, void* dh,
                                          void* dg13, void* h, int32_t* layout, void* gx,
                                          void* dw13, void* dw2, int32_t accumulate, void* stream) {
   HM_CHECK_ARG(x && idx, "hm_expert_ffn_backward_gather: null argument");
-  return ffn_backward(x, a_rows, n_rows, groups, nullptr, w13t, w2t, gy, hidden, inter,
+  return ffn_backward(x, a_rows, n_rows, groups, w13, w2, gy, hidden, inter,
                       const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
                       accumulate, idx, x_rows);
 }
@@ -1422,15 +1456,15 @@ HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx
 HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,
                                         const void* x_recv, int64_t seg_rows, int32_t segs,
                                         const int32_t* n_rows,
-                                        int32_t groups_per_seg, const void* w13t, const void* w2t,
+                                        int32_t groups_per_seg, const void* w13, const void* w2,
                                         const void* gy, int32_t hidden, int32_t inter,
                                         const void* g13, void* dh, void* dg13, void* h,
                                         int32_t* layout, void* gx, void* dw13, void* dw2,
                                         int32_t accumulate, void* stream) {
   HM_CHECK_ARG(x && g13 && segs >= 1 && groups_per_seg >= 1 && seg_rows >= 1,
                "hm_expert_ffn_backward_multi: bad argument");
-  return ffn_backward(x, (int64_t)segs * seg_rows, n_rows, segs * groups_per_seg, nullptr, w13t,
-                      w2t, gy, hidden, inter, const_cast<void*>(g13), 1, dh, dg13, h, layout, gx,
+  return ffn_backward(x, (int64_t)segs * seg_rows, n_rows, segs * groups_per_seg, w13, w2, gy,
+                      hidden, inter, const_cast<void*>(g13), 1, dh, dg13, h, layout, gx,
                       dw13, dw2, stream, accumulate, idx, idx ? x_rows : 0, groups_per_seg,
                       seg_rows, x_recv);
 }

@@ -65,14 +65,14 @@ def expert_ffn_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_rows: int, n
 
 
 def expert_ffn_backward_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_rows: int,
-                                    n_rows_ptr: int, groups: int, w13t: torch.Tensor,
-                                    w2t: torch.Tensor, gy_ptr: int, hidden: int, inter: int,
+                                    n_rows_ptr: int, groups: int, w13: torch.Tensor,
+                                    w2: torch.Tensor, gy_ptr: int, hidden: int, inter: int,
                                     sc: "FFNBackwardScratch", gx_ptr: int, dw13: torch.Tensor,
                                     dw2: torch.Tensor, g13_saved_ptr: int,
                                     accumulate: bool = False) -> None:
     """Backward of expert_ffn_gather_ptrs (saved pre-activations)."""
     _lib.call("hm_expert_ffn_backward_gather", x_ptr, x_rows, idx_ptr, a_rows, n_rows_ptr, groups,
-              ptr(w13t), ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh),
+              ptr(w13), ptr(w2), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh),
               ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
               int(bool(accumulate)), stream_ptr())
 
@@ -93,14 +93,14 @@ def expert_ffn_multi_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, seg_rows: int, 
 
 def expert_ffn_backward_multi_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, seg_rows: int,
                                    segs: int, n_rows_ptr: int, groups_per_seg: int,
-                                   w13t: torch.Tensor, w2t: torch.Tensor, gy_ptr: int, hidden: int,
+                                   w13: torch.Tensor, w2: torch.Tensor, gy_ptr: int, hidden: int,
                                    inter: int, sc: "FFNBackwardScratch", gx_ptr: int,
                                    dw13: torch.Tensor, dw2: torch.Tensor, g13_ptr: int,
                                    accumulate: bool = False, recv_ptr: int = 0) -> None:
     """Backward of expert_ffn_multi_ptrs (saved pre-activations)."""
     _lib.call("hm_expert_ffn_backward_multi", x_ptr, x_rows, idx_ptr or None, recv_ptr or None,
               seg_rows, segs,
-              n_rows_ptr, groups_per_seg, ptr(w13t), ptr(w2t), gy_ptr, hidden, inter, g13_ptr,
+              n_rows_ptr, groups_per_seg, ptr(w13), ptr(w2), gy_ptr, hidden, inter, g13_ptr,
               ptr(sc.dh), ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
               int(bool(accumulate)), stream_ptr())
 
@@ -124,22 +124,23 @@ class FFNBackwardScratch:
 
 
 def expert_ffn_backward_ptrs(x_ptr: int, a_rows: int, n_rows_ptr: int, groups: int,
-                             w13: torch.Tensor, w13t: torch.Tensor, w2t: torch.Tensor,
-                             gy_ptr: int, hidden: int, inter: int, sc: FFNBackwardScratch,
-                             gx_ptr: int, dw13: torch.Tensor, dw2: torch.Tensor,
-                             g13_saved_ptr: int = 0, accumulate: bool = False) -> None:
+                             w13: torch.Tensor, w2: torch.Tensor, gy_ptr: int, hidden: int,
+                             inter: int, sc: FFNBackwardScratch, gx_ptr: int, dw13: torch.Tensor,
+                             dw2: torch.Tensor, g13_saved_ptr: int = 0,
+                             accumulate: bool = False) -> None:
     """Grads of the SwiGLU experts: gx (rows), dW13 [g][2I][M], dW2 [g][M][I].
+    The data-gradient GEMMs read w13 / w2 as stored (MN-major).
     ``g13_saved_ptr``: the forward's pre-activations (expert_ffn_save_ptrs);
     0 -> recomputed.  ``accumulate``: add the weight grads to dw13 / dw2
     (needs the saved pre-activations)."""
     if g13_saved_ptr:
-        _lib.call("hm_expert_ffn_backward_saved", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13t),
-                  ptr(w2t), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh), ptr(sc.dg13),
+        _lib.call("hm_expert_ffn_backward_saved", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13),
+                  ptr(w2), gy_ptr, hidden, inter, g13_saved_ptr, ptr(sc.dh), ptr(sc.dg13),
                   ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2), int(bool(accumulate)),
                   stream_ptr())
         return
     if accumulate:
         raise ValueError("accumulate needs the saved pre-activations")
-    _lib.call("hm_expert_ffn_backward", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w13t),
-              ptr(w2t), gy_ptr, hidden, inter, ptr(sc.g13), ptr(sc.dh), ptr(sc.dg13), ptr(sc.h),
+    _lib.call("hm_expert_ffn_backward", x_ptr, a_rows, n_rows_ptr, groups, ptr(w13), ptr(w2),
+              gy_ptr, hidden, inter, ptr(sc.g13), ptr(sc.dh), ptr(sc.dg13), ptr(sc.h),
               ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2), stream_ptr())

@@ -162,8 +162,6 @@ class HierMoELayer:
             self._side = torch.cuda.Stream()
             self._shared_done = torch.cuda.Event()
             if grad:
-                self.w13t_shared = self.w13_shared.T.contiguous()[None]
-                self.w2t_shared = self.w2_shared.T.contiguous()[None]
                 self.bwd_shared = FFNBackwardScratch(t_loc, 1, hidden, shared_inter)
                 self.dw13_shared = torch.zeros(1, 2 * shared_inter, hidden, dtype=torch.bfloat16,
                                                device="cuda")
@@ -186,7 +184,6 @@ class HierMoELayer:
         self._trace = None            # [(iter, expert ids [T_local, K] on device)] when recording
         self.timeline = None          # [(label, event)] of the forward phases when a list
         if grad:
-            self.refresh_transposed_weights()
             self.bwd = FFNBackwardScratch(self.local * self.world.n_cap, self.local * self.e_loc,
                                           hidden, inter)
             # the forward keeps GEMM1's pre-activations per local rank (no recompute)
@@ -198,18 +195,6 @@ class HierMoELayer:
             # fp32 router weight grad, padded to the wgrad GEMM's 128-row tiles
             self._dwr_pad = torch.zeros(self._e128, hidden, device="cuda")
             self.dw_router = self._dwr_pad[:experts]
-
-    def refresh_transposed_weights(self, slot: int | None = None) -> None:
-        """Transposed bf16 weights for the data-gradient GEMMs (after a
-        weight update: every local slot; after a migration: ``slot`` only,
-        the local slot index whose weights changed)."""
-        if slot is None or not hasattr(self, "w13t"):
-            self.w13t = self.w13.transpose(2, 3).contiguous()
-            self.w2t = self.w2.transpose(2, 3).contiguous()
-            return
-        l, e = divmod(int(slot), self.e_loc)
-        self.w13t[l, e].copy_(self.w13[l, e].T)
-        self.w2t[l, e].copy_(self.w2[l, e].T)
 
     def set_placement(self, placement: Placement) -> None:
         self.placement = placement
@@ -224,13 +209,7 @@ class HierMoELayer:
             return
         r, c = int(pair[0]), int(pair[1])
         self.set_placement(self.placement.swapped(r, c))
-        self.store.migrate(r, c)
-        if self.grad:   # re-transpose only the local slots whose weights moved
-            first = self.gpu_index * self.local * self.e_loc
-            for slot in {r, c}:
-                i = slot - first
-                if 0 <= i < self.local * self.e_loc:
-                    self.refresh_transposed_weights(i)
+        self.store.migrate(r, c)   # the backward reads the moved weights as stored
 
     @staticmethod
     def widen(x: torch.Tensor) -> torch.Tensor:
@@ -465,8 +444,8 @@ class HierMoELayer:
             self._side.wait_stream(cur)
             with torch.cuda.stream(self._side):
                 expert_ffn_backward_ptrs(x.data_ptr(), x.shape[0], self._shared_rows.data_ptr(),
-                                         1, self.w13_shared[None], self.w13t_shared,
-                                         self.w2t_shared, g.data_ptr(), self.hidden,
+                                         1, self.w13_shared[None], self.w2_shared[None],
+                                         g.data_ptr(), self.hidden,
                                          self.shared_inter, self.bwd_shared,
                                          self._shared_dx.data_ptr(), self.dw13_shared,
                                          self.dw2_shared, self._shared_g13.data_ptr())
@@ -492,7 +471,7 @@ class HierMoELayer:
                 x_ptr, x_rows, idx, recv = self._rows_source(wd, x[rows])
                 expert_ffn_backward_multi_ptrs(
                     x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first, self.e_loc,
-                    self.w13t, self.w2t, wd.buffer("gy", 0)[0], self.hidden, self.inter, self.bwd,
+                    self.w13, self.w2, wd.buffer("gy", 0)[0], self.hidden, self.inter, self.bwd,
                     wd.buffer("gx", 0)[0], self.dw13, self.dw2, self.g13s[m].data_ptr(),
                     accumulate=m > 0, recv_ptr=recv)
                 ffn_done = torch.cuda.Event()

@@ -81,14 +81,12 @@ def test_swiglu_ffn_backward_matches_autograd(hm, G, M, I, n_rows):
     w3 = (torch.randn(G, I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
     w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
     w13 = pack_w13(w1, w3)
-    w13t = w13.transpose(1, 2).contiguous()
-    w2t = w2.transpose(1, 2).contiguous()
     nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
     sc = FFNBackwardScratch(cap, G, M, I)
     gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
     dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
     dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
-    expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t, gy.data_ptr(),
+    expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, gy.data_ptr(),
                              M, I, sc, gx.data_ptr(), dw13, dw2)
     torch.cuda.synchronize()
     r = 0
@@ -119,8 +117,6 @@ def test_saved_preactivations_match_recompute(hm):
     gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
     w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
     w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
-    w13t = w13.transpose(1, 2).contiguous()
-    w2t = w2.transpose(1, 2).contiguous()
     nr = torch.tensor(n_rows, dtype=torch.int32, device="cuda")
     h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
     y0 = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
@@ -137,7 +133,7 @@ def test_saved_preactivations_match_recompute(hm):
         gx = torch.zeros(cap, M, device="cuda", dtype=torch.bfloat16)
         dw13 = torch.empty(G, 2 * I, M, device="cuda", dtype=torch.bfloat16)
         dw2 = torch.empty(G, M, I, device="cuda", dtype=torch.bfloat16)
-        expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t,
+        expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2,
                                  gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2, saved)
         torch.cuda.synchronize()
         res.append((gx[:rows].clone(), dw13.clone(), dw2.clone()))
@@ -161,7 +157,6 @@ def test_multi_segment_ffn_equals_per_rank(hm):
     gy = torch.randn(S, cap, M, device="cuda").to(torch.bfloat16)
     w13 = (torch.randn(S, Gs, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
     w2 = (torch.randn(S, Gs, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
-    w13t, w2t = w13.transpose(2, 3).contiguous(), w2.transpose(2, 3).contiguous()
     outs = []
     for multi in (False, True):
         h = torch.zeros(S * cap, I, dtype=torch.bfloat16, device="cuda")
@@ -175,7 +170,7 @@ def test_multi_segment_ffn_equals_per_rank(hm):
             expert_ffn_multi_ptrs(x.data_ptr(), S * cap, 0, cap, S, nr.data_ptr(), Gs, w13, w2,
                                   M, I, h, y.data_ptr(), g13.data_ptr())
             expert_ffn_backward_multi_ptrs(x.data_ptr(), S * cap, 0, cap, S, nr.data_ptr(), Gs,
-                                           w13t, w2t, gy.data_ptr(), M, I, sc, gx.data_ptr(),
+                                           w13, w2, gy.data_ptr(), M, I, sc, gx.data_ptr(),
                                            dw13, dw2, g13.data_ptr())
         else:
             for s in range(S):
@@ -184,7 +179,7 @@ def test_multi_segment_ffn_equals_per_rank(hm):
                 np_ = nr[s * Gs:].data_ptr()
                 expert_ffn_save_ptrs(x[s].data_ptr(), cap, np_, Gs, w13[s], w2[s], M, I, hs,
                                      y[s].data_ptr(), g13[s].data_ptr())
-                expert_ffn_backward_ptrs(x[s].data_ptr(), cap, np_, Gs, w13[s], w13t[s], w2t[s],
+                expert_ffn_backward_ptrs(x[s].data_ptr(), cap, np_, Gs, w13[s], w2[s],
                                          gy[s].data_ptr(), M, I, sc, gx[s].data_ptr(), dw13[s],
                                          dw2[s], g13[s].data_ptr())
         torch.cuda.synchronize()

@@ -51,18 +51,3 @@ def test_layer_swap_moves_weights_with_placement(hm):
     # rounding) may change with the new slot -> rank map
     torch.testing.assert_close(y1.float(), y0.float(), rtol=2e-2, atol=2e-2)
     layer.close()
-
-
-def test_swap_refreshes_only_moved_transposes(hm):
-    """A training layer keeps transposed weights for its data-gradient GEMMs;
-    a swap re-transposes just the two moved slots, and afterwards every
-    slot's transpose matches its (migrated) weights."""
-    from paper_2508_09591_b200.moe import HierMoELayer
-    G, E, K, M, I, T_r = 8, 16, 2, 256, 256, 64
-    layer = HierMoELayer(G, E, K, M, I, T_r, seed=5, grad=True)
-    layer.apply_swap((1, 9))
-    layer.apply_swap((4, 5))
-    torch.cuda.synchronize()
-    assert torch.equal(layer.w13t, layer.w13.transpose(2, 3))
-    assert torch.equal(layer.w2t, layer.w2.transpose(2, 3))
-    layer.close()

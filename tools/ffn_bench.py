@@ -25,7 +25,6 @@ def run(name, G, M, I, rows_per_group, steps=10):
     gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
     w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
     w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
-    w13t, w2t = w13.transpose(1, 2).contiguous(), w2.transpose(1, 2).contiguous()
     h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
     y = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
     g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
@@ -38,7 +37,7 @@ def run(name, G, M, I, rows_per_group, steps=10):
                              g13.data_ptr())
 
     def bwd():
-        expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t,
+        expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2,
                                  gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2,
                                  g13.data_ptr())
 

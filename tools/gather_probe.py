@@ -69,7 +69,6 @@ def backward():
     nr = n.cuda()
     w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
     w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
-    w13t, w2t = w13.transpose(1, 2).contiguous(), w2.transpose(1, 2).contiguous()
     h = torch.empty(cap, I, device="cuda", dtype=torch.bfloat16)
     y = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
     g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
@@ -80,10 +79,10 @@ def backward():
     expert_ffn_save_ptrs(xm.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y.data_ptr(),
                          g13.data_ptr())
     runs = {"bwd_copy": lambda: expert_ffn_backward_ptrs(
-                xm.data_ptr(), cap, nr.data_ptr(), G, w13, w13t, w2t, gy.data_ptr(), M, I, sc,
+                xm.data_ptr(), cap, nr.data_ptr(), G, w13, w2, gy.data_ptr(), M, I, sc,
                 gx.data_ptr(), dw13, dw2, g13.data_ptr()),
             "bwd_gather": lambda: expert_ffn_backward_gather_ptrs(
-                x.data_ptr(), T, idx.data_ptr(), cap, nr.data_ptr(), G, w13t, w2t, gy.data_ptr(),
+                x.data_ptr(), T, idx.data_ptr(), cap, nr.data_ptr(), G, w13, w2, gy.data_ptr(),
                 M, I, sc, gx.data_ptr(), dw13, dw2, g13.data_ptr())}
     outs = {}
     for name, fn in runs.items():
