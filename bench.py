@@ -306,7 +306,8 @@ def dsv3_layer_forward(G, E, K, M, inter, T_r, world, rank, x, flush, tokens_tot
            "fwd_tflops": fl / (fwd_ms * 1e-3) / 1e12,
            "fwd_bwd_tflops": 3 * fl / ((fwd_ms + bwd_ms) * 1e-3) / 1e12,
            "clocks": lclk.summary(),
-           "note": "router logits GEMM and gate bwd in torch (cuBLAS TF32)"}
+           "note": "router GEMMs, gate backward, dispatch/combine and experts fwd+bwd are our "
+                   "kernels"}
     layer.close()
     return out
 
@@ -883,8 +884,8 @@ def main():
                                       "unit": "TFLOP/s", "frac": ffn_tflops / peak_tf,
                                       "kernel": "k_grouped_gemm (tcgen05, 2 GEMMs, fwd)"},
                      "inter": inter, "transport": layer.dedup, "clocks": lclk.summary(),
-                     "note": "router logits GEMM and top-K softmax bwd in torch (cuBLAS); "
-                             "dispatch/combine/experts fwd+bwd are our kernels"}
+                     "note": "router GEMMs, gate backward, dispatch/combine and experts fwd+bwd "
+                             "are our kernels"}
         layer.close()
 
     planner = None

@@ -744,12 +744,15 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "h"((uint16_t)0x3)
       : "memory");
 }
-// arrive on the barrier at the same offset in CTA `rank` of the cluster
+// arrive on the barrier at the same offset in CTA `rank` of the cluster.
+// Default (.release.cta) semantics: the only user is the epilogue's
+// TMEM-empty arrive, ordered after its tcgen05.ld by the before_thread_sync
+// fence; a .release.cluster arrive compiled to MEMBAR.ALL.GPU + ERRBAR, i.e.
+// waited for the tile's global stores (2-3 % of GEMM time)
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 // GA (modes 0/1): the A rows are gathered by index (args.a_idx) by warps 8-11
@@ -1257,6 +1260,7 @@ HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
 HM_API int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t groups,
                            const int32_t* n_rows, int32_t N, int32_t K, int32_t swiglu, void* out,
                            int64_t ld_out, void* stream) {
+  HM_RANGE("hm_grouped_gemm");
   return launch_gemm(a, a_rows, b, groups, n_rows, N, K, swiglu, out, ld_out, nullptr,
                      (cudaStream_t)stream);
 }
@@ -1266,6 +1270,7 @@ HM_API int hm_grouped_gemm(const void* a, int64_t a_rows, const void* b, int32_t
 HM_API int hm_grouped_gemm_kn(const void* a, int64_t a_rows, const void* b, int32_t groups,
                               const int32_t* n_rows, int32_t N, int32_t K, void* out,
                               int64_t ld_out, void* stream) {
+  HM_RANGE("hm_grouped_gemm_kn");
   return launch_gemm(a, a_rows, b, groups, n_rows, N, K, 0, out, ld_out, nullptr,
                      (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr, true);
 }
@@ -1282,6 +1287,7 @@ HM_API int hm_grouped_gemm_kn(const void* a, int64_t a_rows, const void* b, int3
 HM_API int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, const void* b,
                        int32_t N, int32_t K, int32_t n_valid, float* out, int64_t ld_out,
                        void* stream) {
+  HM_RANGE("hm_gemm_f32");
   HM_CHECK_ARG(a && b && out && rows_dev, "hm_gemm_f32: null argument");
   HM_CHECK_ARG(n_valid > 0 && n_valid <= N, "hm_gemm_f32: 0 < n_valid <= N");
   return launch_gemm(a, rows > 0 ? rows : 1, b, 1, rows_dev, N, K, 0, nullptr, ld_out, nullptr,
@@ -1291,6 +1297,7 @@ HM_API int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, con
 HM_API int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
                         int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
                         void* stream) {
+  HM_RANGE("hm_wgrad_f32");
   HM_CHECK_ARG(a && b && out && rows_dev, "hm_wgrad_f32: null argument");
   return launch_gemm_wgrad(a, b, rows > 0 ? rows : 1, 1, rows_dev, m_out, N, nullptr, ld_out,
                            (cudaStream_t)stream, accumulate, nullptr, 0, out);
@@ -1302,6 +1309,7 @@ HM_API int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_
 HM_API int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, int32_t groups,
                          const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                          void* y, void* stream) {
+  HM_RANGE("hm_expert_ffn");
   int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
                        (cudaStream_t)stream);
   if (st) return st;
@@ -1314,6 +1322,7 @@ HM_API int hm_expert_ffn(const void* x, int64_t a_rows, const int32_t* n_rows, i
 HM_API int hm_expert_ffn_save(const void* x, int64_t a_rows, const int32_t* n_rows,
                               int32_t groups, const void* w13, const void* w2, int32_t hidden,
                               int32_t inter, void* h, void* y, void* g13, void* stream) {
+  HM_RANGE("hm_expert_ffn_save");
   HM_CHECK_ARG(g13, "hm_expert_ffn_save: null g13");
   int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
                        (cudaStream_t)stream, g13);
@@ -1377,6 +1386,7 @@ HM_API int hm_expert_ffn_backward(const void* x, int64_t a_rows, const int32_t* 
                                   int32_t hidden, int32_t inter, void* g13, void* dh, void* dg13,
                                   void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
                                   void* stream) {
+  HM_RANGE("hm_expert_ffn_backward");
   return ffn_backward(x, a_rows, n_rows, groups, w13, w2, gy, hidden, inter, g13, 0, dh, dg13, h,
                       layout, gx, dw13, dw2, stream);
 }
@@ -1390,6 +1400,7 @@ HM_API int hm_expert_ffn_backward_saved(const void* x, int64_t a_rows, const int
                                         const void* g13, void* dh, void* dg13, void* h,
                                         int32_t* layout, void* gx, void* dw13, void* dw2,
                                         int32_t accumulate, void* stream) {
+  HM_RANGE("hm_expert_ffn_backward_saved");
   return ffn_backward(x, a_rows, n_rows, groups, w13, w2, gy, hidden, inter,
                       const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
                       accumulate);
@@ -1403,6 +1414,7 @@ HM_API int hm_expert_ffn_gather(const void* x, int64_t x_rows, const int32_t* id
                                 const int32_t* n_rows, int32_t groups, const void* w13,
                                 const void* w2, int32_t hidden, int32_t inter, void* h, void* y,
                                 void* g13, void* stream) {
+  HM_RANGE("hm_expert_ffn_gather");
   HM_CHECK_ARG(x && idx, "hm_expert_ffn_gather: null argument");
   int st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * inter, hidden, 1, h, inter, nullptr,
                        (cudaStream_t)stream, g13, idx, x_rows);
@@ -1419,6 +1431,7 @@ HM_API int hm_expert_ffn_backward_gather(const void* x, int64_t x_rows, const in
                                          int32_t hidden, int32_t inter, const void* g13, void* dh,
                                          void* dg13, void* h, int32_t* layout, void* gx,
                                          void* dw13, void* dw2, int32_t accumulate, void* stream) {
+  HM_RANGE("hm_expert_ffn_backward_gather");
   HM_CHECK_ARG(x && idx, "hm_expert_ffn_backward_gather: null argument");
   return ffn_backward(x, a_rows, n_rows, groups, w13, w2, gy, hidden, inter,
                       const_cast<void*>(g13), 1, dh, dg13, h, layout, gx, dw13, dw2, stream,
@@ -1440,6 +1453,7 @@ HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx
                                int32_t groups_per_seg, const void* w13, const void* w2,
                                int32_t hidden, int32_t inter, void* h, void* y, void* g13,
                                void* stream) {
+  HM_RANGE("hm_expert_ffn_multi");
   HM_CHECK_ARG(x && segs >= 1 && groups_per_seg >= 1 && seg_rows >= 1,
                "hm_expert_ffn_multi: bad argument");
   const int groups = segs * groups_per_seg;
@@ -1461,6 +1475,7 @@ HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int
                                         const void* g13, void* dh, void* dg13, void* h,
                                         int32_t* layout, void* gx, void* dw13, void* dw2,
                                         int32_t accumulate, void* stream) {
+  HM_RANGE("hm_expert_ffn_backward_multi");
   HM_CHECK_ARG(x && g13 && segs >= 1 && groups_per_seg >= 1 && seg_rows >= 1,
                "hm_expert_ffn_backward_multi: bad argument");
   return ffn_backward(x, (int64_t)segs * seg_rows, n_rows, segs * groups_per_seg, w13, w2, gy,

@@ -10,6 +10,8 @@
 
 #include <atomic>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost a null check without a tool
+
 #define HM_API extern "C" __attribute__((visibility("default")))
 
 namespace hm {
@@ -47,7 +49,18 @@ inline int grid_for(int64_t work, int per_block, int max_blocks) {
 
 constexpr int kSMs = 148;
 
+// NVTX range over one C-ABI call (SURVEY §5 tracing): nsys / ncu --nvtx show
+// every dispatch / combine / FFN / planner call as a named range
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
+
 }  // namespace hm
+
+#define HM_RANGE(name) hm::Range _hm_nvtx_range(name)
 
 #define HM_CHECK_ARG(cond, ...)            \
   do {                                     \

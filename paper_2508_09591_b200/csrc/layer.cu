@@ -2132,6 +2132,7 @@ HM_API int hm_route_set_option(int32_t quad) {
 HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
                          const int32_t* expert_to_slot, int32_t renormalize, int32_t* slot_ids,
                          float* weights, int32_t* expert_ids, void* stream) {
+  HM_RANGE("hm_route_topk");
   HM_CHECK_ARG(E >= 1 && E <= 512, "hm_route_topk: E must be 1..512");
   HM_CHECK_ARG(K >= 1 && K <= kMaxK && K <= E, "hm_route_topk: K must be 1..%d and <= E", kMaxK);
   if (T == 0) return 0;
@@ -2199,6 +2200,7 @@ HM_API int hm_route_group(const float* logits, int64_t T, int32_t E, int32_t K, 
                           int32_t topk_group, const float* bias, float route_scale,
                           const int32_t* expert_to_slot, int32_t* slot_ids, float* weights,
                           int32_t* expert_ids, void* stream) {
+  HM_RANGE("hm_route_group");
   HM_CHECK_ARG(E >= 1 && E <= 512, "hm_route_group: E must be 1..512");
   HM_CHECK_ARG(n_group >= 1 && n_group <= 32 && E % n_group == 0,
                "hm_route_group: n_group must be 1..32 and divide E");
@@ -2235,6 +2237,7 @@ static int dispatch_push(hm_world* w, const void* x, const int32_t* ids, const f
 
 HM_API int hm_dispatch_plan(hm_world* w, const int32_t* ids, const float* wts, int32_t mode,
                             void* stream) {
+  HM_RANGE("hm_dispatch_plan");
   HM_CHECK_ARG(w && ids, "hm_dispatch: null argument");
   HM_CHECK_ARG(mode >= 0 && mode <= 3,
                "hm_dispatch: mode must be 0 (raw), 1 (dedup per rank), 2 (dedup per remote rank), "
@@ -2286,6 +2289,7 @@ HM_API int hm_dispatch_plan(hm_world* w, const int32_t* ids, const float* wts, i
 
 HM_API int hm_dispatch_push(hm_world* w, const void* x, const int32_t* ids, const float* wts,
                             int32_t mode, void* stream) {
+  HM_RANGE("hm_dispatch_push");
   HM_CHECK_ARG(w && x && ids, "hm_dispatch_push: null argument");
   HM_CHECK_ARG(mode == w->last_mode, "hm_dispatch_push: mode differs from the plan's");
   return dispatch_push(w, x, ids, wts, mode, (cudaStream_t)stream);
@@ -2293,6 +2297,7 @@ HM_API int hm_dispatch_push(hm_world* w, const void* x, const int32_t* ids, cons
 
 HM_API int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts,
                        int32_t mode, void* stream) {
+  HM_RANGE("hm_dispatch");
   HM_CHECK_ARG(w && x && ids, "hm_dispatch: null argument");
   int st = hm_dispatch_plan(w, ids, wts, mode, stream);
   if (st) return st;
@@ -2351,6 +2356,7 @@ static int dispatch_push(hm_world* w, const void* x, const int32_t* ids, const f
 }
 
 HM_API int hm_expand(hm_world* w, void* stream) {
+  HM_RANGE("hm_expand");
   HM_CHECK_ARG(w, "hm_expand: null world");
   if (w->h.P == 1 && w->last_mode == 2) return 0;  // every rank shares this GPU: nothing received
   if (w->h.U1) return 0;                             // relay rows are re-dispatched, not expanded
@@ -2447,6 +2453,7 @@ static int combine_impl(hm_world* w, const float* wts, const int32_t* ids, int32
 
 HM_API int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t mode, void* out,
                       void* stream) {
+  HM_RANGE("hm_combine");
   return combine_impl(w, wts, ids, mode, nullptr, out, stream);
 }
 
@@ -2557,6 +2564,7 @@ __global__ void __launch_bounds__(256) k_gate_backward(const float* __restrict__
 HM_API int hm_gate_backward(const float* logits, const int32_t* expert_ids, const float* weights,
                             const float* dw, int64_t T, int32_t E, int32_t K, int32_t mode,
                             float route_scale, void* dlogits, int32_t ld, void* stream) {
+  HM_RANGE("hm_gate_backward");
   HM_CHECK_ARG(logits && expert_ids && weights && dw && dlogits, "hm_gate_backward: null argument");
   HM_CHECK_ARG(ld >= E && ld % 8 == 0 && K >= 1 && K <= 32 && mode >= 0 && mode <= 2,
                "hm_gate_backward: ld >= E, ld %% 8 == 0, 1 <= K <= 32, mode 0..2");
@@ -2647,6 +2655,7 @@ HM_API int hm_combine_add(hm_world* w, const float* wts, const int32_t* ids, int
 
 // explicit barrier (e.g. after an expert FFN when the raw combine follows)
 HM_API int hm_world_barrier(hm_world* w, void* stream) {
+  HM_RANGE("hm_world_barrier");
   HM_CHECK_ARG(w, "hm_world_barrier: null world");
   if (w->h.P > 1) {
     k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(w->d, w->status);
@@ -2739,6 +2748,7 @@ HM_API int hm_world_timings(hm_world* w, float* ms, int32_t n) {
 // ids2/w2 are [L * R_cap, K] (R_cap = U1 * T_r), the same row layout as the
 // relay's receive buffer (which is the phase-2 payload).
 HM_API int hm_relay_ids(hm_world* w, int32_t* ids2, float* w2, void* stream) {
+  HM_RANGE("hm_relay_ids");
   HM_CHECK_ARG(w && ids2 && w2, "hm_relay_ids: null argument");
   HM_CHECK_ARG(w->h.U1 > 0, "hm_relay_ids: not a relay world");
   int64_t n = (int64_t)w->h.L * w->h.R_cap * w->h.K;
@@ -2752,6 +2762,7 @@ HM_API int hm_relay_ids(hm_world* w, int32_t* ids2, float* w2, void* stream) {
 // dw [L*T_r, K]; replays the last forward plan (no re-planning).
 HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, const float* wts,
                             int32_t mode, float* dw, void* stream) {
+  HM_RANGE("hm_dispatch_grad");
   HM_CHECK_ARG(w && g && ids && wts && dw, "hm_dispatch_grad: null argument");
   HM_CHECK_ARG(w->grad, "hm_dispatch_grad: world created without backward buffers");
   HM_CHECK_ARG(mode == w->last_mode, "hm_dispatch_grad: mode differs from the forward's");
@@ -2796,6 +2807,7 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
 // into dw.
 HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float* dw, void* dx,
                            void* stream) {
+  HM_RANGE("hm_combine_grad");
   HM_CHECK_ARG(w && ids && dw && dx, "hm_combine_grad: null argument");
   HM_CHECK_ARG(w->grad, "hm_combine_grad: world created without backward buffers");
   cudaStream_t s = (cudaStream_t)stream;

@@ -224,6 +224,7 @@ HM_API int hm_store_status(hm_store* s, int32_t* out4) {
 // Swap global slots r and c (slot s lives on GPU s / slots_per_gpu).  Every
 // GPU calls this with the same pair (SPMD); stream-ordered, no host sync.
 HM_API int hm_migrate(hm_store* s, int32_t slot_r, int32_t slot_c, void* stream) {
+  HM_RANGE("hm_migrate");
   HM_CHECK_ARG(s, "hm_migrate: null store");
   const int total = s->h.P * s->h.S;
   HM_CHECK_ARG(slot_r >= 0 && slot_c >= 0 && slot_r < total && slot_c < total,

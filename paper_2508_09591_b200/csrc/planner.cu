@@ -600,6 +600,7 @@ __global__ void k_np_pow(const double* __restrict__ x, const double* __restrict_
 
 HM_API int hm_mask_pack(const uint8_t* mask, int64_t T, int32_t E, const int32_t* slot_to_expert,
                         uint32_t* bits, int32_t* row_popcount, void* stream) {
+  HM_RANGE("hm_mask_pack");
   HM_CHECK_ARG(T >= 0 && E >= 1 && E <= 4096, "hm_mask_pack: bad shape T=%lld E=%d", (long long)T, E);
   if (T == 0) return 0;
   HM_CHECK_ARG(mask && bits, "hm_mask_pack: null pointer");
@@ -634,6 +635,7 @@ HM_API int hm_ids_to_bits(const int32_t* ids, int64_t T, int32_t K, int32_t E,
 HM_API int hm_level_counts(const uint32_t* bits, int64_t T, int32_t E, const int32_t* groups,
                            int32_t n_cuts, int64_t* dedup, int64_t* raw, uint8_t* hit,
                            int32_t hit_cut, void* stream) {
+  HM_RANGE("hm_level_counts");
   HM_CHECK_ARG(n_cuts >= 1 && n_cuts <= kMaxCuts, "hm_level_counts: 1..%d cuts", kMaxCuts);
   HM_CHECK_ARG(E >= 1 && E <= 4096, "hm_level_counts: E out of range");
   Cuts cuts;
@@ -692,6 +694,7 @@ HM_API int hm_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* gran
 
 HM_API int hm_propagate_count(const uint32_t* bits, int64_t T, int32_t E, int32_t groups,
                               int64_t* copies, void* stream) {
+  HM_RANGE("hm_propagate_count");
   HM_CHECK_ARG(groups >= 1 && E % groups == 0, "group count %d does not divide %d experts", groups, E);
   if (T == 0) return 0;
   int blocks = grid_for(T, 256, kSMs * 8);
@@ -703,6 +706,7 @@ HM_API int hm_propagate_count(const uint32_t* bits, int64_t T, int32_t E, int32_
 HM_API int hm_propagate_emit(const uint32_t* bits, int64_t T, int32_t E, int32_t groups,
                              const int64_t* first_copy, const int64_t* origin_in, uint32_t* out_bits,
                              int64_t* out_origin, int64_t* out_parent, void* stream) {
+  HM_RANGE("hm_propagate_emit");
   HM_CHECK_ARG(groups >= 1 && E % groups == 0, "group count %d does not divide %d experts", groups, E);
   if (T == 0) return 0;
   int blocks = grid_for(T, 256, kSMs * 8);
@@ -715,6 +719,7 @@ HM_API int hm_propagate_emit(const uint32_t* bits, int64_t T, int32_t E, int32_t
 HM_API int hm_swap_partials(const uint32_t* bits, int64_t T, int32_t E, int32_t groups, int64_t* base,
                             int64_t* sel, int64_t* hitsel, int64_t* lone, int64_t* lonesel,
                             int32_t* too_dense, void* stream) {
+  HM_RANGE("hm_swap_partials");
   HM_CHECK_ARG(groups >= 1 && E % groups == 0, "group count %d does not divide %d experts", groups, E);
   HM_CHECK_ARG(E <= 4096, "hm_swap_partials: E too large");
   cudaStream_t s = (cudaStream_t)stream;
@@ -746,6 +751,7 @@ HM_API int hm_swap_partials(const uint32_t* bits, int64_t T, int32_t E, int32_t 
 HM_API int hm_swap_tensor(const int64_t* base, const int64_t* sel, const int64_t* hitsel,
                           const int64_t* lone, const int64_t* lonesel, int32_t E, int32_t groups,
                           int64_t* z, void* stream) {
+  HM_RANGE("hm_swap_tensor");
   HM_CHECK_ARG(groups >= 1 && E % groups == 0, "group count %d does not divide %d experts", groups, E);
   int64_t n = (int64_t)E * E * groups;
   int blocks = grid_for(n, 256, kSMs * 16);
@@ -764,6 +770,7 @@ HM_API int hm_swap_cost(const int64_t* const* inter_z, const int32_t* inter_grou
                         int32_t depth, int32_t E, int64_t token_bytes, double gamma,
                         const int32_t* dim_dev, int32_t dim_host, double* q, double* q_exact,
                         void* stream) {
+  HM_RANGE("hm_swap_cost");
   HM_CHECK_ARG(depth >= 1 && depth <= kMaxPhases, "hm_swap_cost: depth out of range");
   HM_CHECK_ARG(gamma > 0.0, "gamma must be > 0, got %g", gamma);
   CostArgs a;
@@ -790,6 +797,7 @@ HM_API int hm_swap_cost(const int64_t* const* inter_z, const int32_t* inter_grou
 
 HM_API int hm_swap_select(const double* q, const double* q_exact, int32_t E, int64_t* out_i64,
                           double* out_f64, void* stream) {
+  HM_RANGE("hm_swap_select");
   HM_CHECK_ARG(E >= 1, "hm_swap_select: E < 1");
   k_argmin_select<<<1, 1024, 0, (cudaStream_t)stream>>>(q, q_exact, E, out_i64, out_f64);
   HM_LAUNCHED();
@@ -802,6 +810,7 @@ HM_API int hm_time_model(const int64_t* dedup_concat, const int32_t* fanout_grou
                          const double* b_inter, const double* a_intra, const double* b_intra,
                          int32_t* cut_offsets_dev, double* times, int32_t* d_star, int64_t* maxima,
                          void* stream) {
+  HM_RANGE("hm_time_model");
   HM_CHECK_ARG(depth >= 1 && depth <= kMaxPhases, "hm_time_model: depth out of range");
   TimeArgs a;
   memset(&a, 0, sizeof(a));

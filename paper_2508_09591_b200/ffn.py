@@ -59,7 +59,8 @@ def expert_ffn_gather_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, a_rows: int, n
                            groups: int, w13: torch.Tensor, w2: torch.Tensor, hidden: int,
                            inter: int, h: torch.Tensor, y_ptr: int, g13_ptr: int = 0) -> None:
     """FFN with the fused dispatch: GEMM1 gathers its rows from the token-major
-    x [x_rows, hidden] by the expert-major row indices idx (TMA gather4)."""
+    x [x_rows, hidden] by the expert-major row indices idx (cp.async producer
+    warps)."""
     _lib.call("hm_expert_ffn_gather", x_ptr, x_rows, idx_ptr, a_rows, n_rows_ptr, groups,
               ptr(w13), ptr(w2), hidden, inter, ptr(h), y_ptr, g13_ptr or None, stream_ptr())
 

@@ -49,7 +49,7 @@ class HierMoELayer:
         ``transport_log``.
         ``fused_dispatch`` (default: on with one GPU): the dispatch emits
         expert-major row indices instead of row copies and GEMM1 gathers its
-        rows from x with TMA gather4 (the backward's dW13 likewise); outputs
+        rows from x by index (the backward's dW13 likewise); outputs
         and gradients are bit-identical to the copying dispatch."""
         if inter % 128 or hidden % 256 or shared_inter % 128:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
