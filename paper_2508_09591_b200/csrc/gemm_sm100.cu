@@ -74,6 +74,12 @@ struct GemmArgs {
   // (the [L][N_cap] expert-major buffers); seg_groups = 0: one segment
   int seg_groups;
   int64_t seg_rows;
+  // explicit groups (pair kernel, modes 0 / 1): group g = rows
+  // [g_row0[g], g_row0[g] + n_rows[g]) of the row space, multiplied by weight
+  // g_wsel[g] -- e.g. only the rows of one source range of every expert (the
+  // overlapped exchange computes the rows already on this GPU first)
+  const int32_t* g_row0;
+  const int32_t* g_wsel;
 };
 
 
@@ -242,6 +248,7 @@ struct TileMap {
   int start[kMaxGroups + 1];    // first tile index of each group
   int row0[kMaxGroups];         // first row of each group in A (wgrad: first K column)
   int rows[kMaxGroups];         // rows of each group (wgrad: padded K extent)
+  int wsel[kMaxGroups];         // weight index of each group (pair kernel)
 };
 
 // first row of each group: prefix sums of the group sizes, restarting at
@@ -790,10 +797,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
     for (int g = 0; g < args.groups; ++g) {
       int n = args.n_rows[g];
       if (kMode == 2) n = (n + BK - 1) / BK * BK;   // K padded to the k-block
-      row = seg_row0(args, g, row);
+      row = args.g_row0 ? args.g_row0[g] : seg_row0(args, g, row);
       tm.start[g] = acc;
       tm.row0[g] = row;
       tm.rows[g] = n;
+      tm.wsel[g] = args.g_wsel ? args.g_wsel[g] : g;
       acc += (kMode == 2 ? args.m_out / BM2 : (n + BM2 - 1) / BM2) * tm.ntile_n;
       row += n;
     }
@@ -836,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
         // mode 2 (weight gradient from transposed operands): A [m_out][K_all],
         // B [N][K_all], group g's reduction range = its padded token columns
         const int arow = (kMode == 2 ? 0 : tm.row0[g]) + mt * BM2 + (int)rank * 128;
-        const int brow = (kMode == 2 ? 0 : g * args.N) + nt * BN + (int)rank * 128;
+        const int brow = (kMode == 2 ? 0 : tm.wsel[g] * args.N) + nt * BN + (int)rank * 128;
         const int k0 = kMode == 2 ? tm.row0[g] : 0;
         const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -849,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
 #pragma unroll
             for (int j = 0; j < 2; ++j)
               tma_load_2d_pair(sb + stage * kHalfBytes + j * 8192, &map_b, full + stage,
-                               bcol + 64 * j, g * args.K + kb * BK);
+                               bcol + 64 * j, tm.wsel[g] * args.K + kb * BK);
           } else {
             tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, k0 + kb * BK, brow);
           }
@@ -1159,6 +1167,8 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.n_valid = N;
   args.seg_groups = seg_groups;
   args.seg_rows = seg_rows;
+  args.g_row0 = nullptr;
+  args.g_wsel = nullptr;
   const size_t smem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiStageBytes;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
@@ -1186,7 +1196,8 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
                 cudaStream_t s, void* out2 = nullptr, const int32_t* a_idx = nullptr,
                 int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0,
                 int seg_groups = 0, int64_t seg_rows = 0, const void* a_src2 = nullptr,
-                bool b_mn = false) {
+                bool b_mn = false, const int32_t* g_row0 = nullptr,
+                const int32_t* g_wsel = nullptr, int nweights = 0, int ctas = 0) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -1196,8 +1207,10 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   CUtensorMap ma, mb;
   int st = make_map(&ma, a, (uint64_t)(a_idx ? a_src_rows : a_rows), (uint64_t)K, 128);
   if (st) return st;
-  st = b_mn ? make_map_mn(&mb, b, (uint64_t)groups * K, (uint64_t)N)
-            : make_map(&mb, b, (uint64_t)groups * N, (uint64_t)K, 128);
+  HM_CHECK_ARG(!g_row0 == !g_wsel && (!g_row0 || nweights >= 1),
+               "grouped gemm: explicit groups need row starts, weight indices and the weight count");
+  const uint64_t nw = g_wsel ? (uint64_t)nweights : (uint64_t)groups;
+  st = b_mn ? make_map_mn(&mb, b, nw * K, (uint64_t)N) : make_map(&mb, b, nw * N, (uint64_t)K, 128);
   if (st) return st;
   HM_CHECK_ARG(!b_mn || (!a_idx && !swiglu), "grouped gemm: MN-major B only for mode 0");
   GemmArgs args;
@@ -1221,11 +1234,15 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.n_valid = n_valid > 0 ? n_valid : N;
   args.seg_groups = seg_groups;
   args.seg_rows = seg_rows;
+  args.g_row0 = g_row0;
+  args.g_wsel = g_wsel;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
+  if (ctas > 0 && ctas < sms) sms = ctas;
+  HM_CHECK_ARG(sms >= 2, "grouped gemm: at least one CTA pair");
   const size_t smem2 = (size_t)kStages2 * kStageBytes2 + 1024 + 256 + 4 * kEpiStageBytes;
   const int grid = sms & ~1;
   auto run = [&](auto kern, int threads) -> int {
@@ -1465,6 +1482,30 @@ HM_API int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx
   return launch_gemm(h, rows, w2, groups, n_rows, hidden, inter, 0, y, hidden, nullptr,
                      (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, groups_per_seg,
                      seg_rows);
+}
+
+// ... over explicit row groups: group g = rows [g_row0[g], g_row0[g] + g_rows[g])
+// of the [rows] row space (x / idx / h / y / g13 as in hm_expert_ffn_multi),
+// multiplied by expert weight g_wsel[g] of w13 / w2 ([nweights][...]); ctas > 0
+// caps the grid (an exchange kernel running beside it keeps its SMs).  The
+// overlapped forward runs the rows already on this GPU while the rest cross
+// NVLink, then the received rows; per-row results equal the one-launch FFN's.
+HM_API int hm_expert_ffn_groups(const void* x, int64_t x_rows, const int32_t* idx,
+                                const void* x_recv, int64_t rows, int32_t groups,
+                                const int32_t* g_row0, const int32_t* g_rows,
+                                const int32_t* g_wsel, int32_t nweights, const void* w13,
+                                const void* w2, int32_t hidden, int32_t inter, void* h, void* y,
+                                void* g13, int32_t ctas, void* stream) {
+  HM_RANGE("hm_expert_ffn_groups");
+  HM_CHECK_ARG(x && g_row0 && g_rows && g_wsel && rows >= 1 && nweights >= 1,
+               "hm_expert_ffn_groups: bad argument");
+  int st = launch_gemm(x, rows, w13, groups, g_rows, 2 * inter, hidden, 1, h, inter, nullptr,
+                       (cudaStream_t)stream, g13, idx, idx ? x_rows : 0, nullptr, 0, 0, 0, x_recv,
+                       false, g_row0, g_wsel, nweights, ctas);
+  if (st) return st;
+  return launch_gemm(h, rows, w2, groups, g_rows, hidden, inter, 0, y, hidden, nullptr,
+                     (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr, false,
+                     g_row0, g_wsel, nweights, ctas);
 }
 
 HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,

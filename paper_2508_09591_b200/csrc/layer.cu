@@ -1633,6 +1633,7 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
                                                    const unsigned long long* __restrict__ hitmask,
                                                    const int32_t* __restrict__ gpos,
                                                    const int32_t* __restrict__ epos, int mode,
+                                                   const int32_t* __restrict__ gpos_g,
                                                    float* __restrict__ dw) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
@@ -1640,7 +1641,9 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
   const int64_t ntok = (int64_t)w.L * w.T_r;
   int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = warp; t < ntok; t += nw) {
+  const bool spread = mode == 3 && w.P > 1;   // NVLink stores all over the peers' buffers
+  for (int64_t i = warp; i < ntok; i += nw) {
+    const int64_t t = spread ? spread_index(i, ntok) : i;
     // direct picks (scaled rows + dot products) and dedup destinations (raw rows)
     int nd = 0, nr = 0;
     uint8_t* drow[kMaxK];
@@ -1653,7 +1656,7 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
         int e = ids[t * w.K + k], ep = epos[t * w.K + k];
         if (e < 0 || ep < 0) continue;
         const int d = rank_of_slot(w, e);
-        if (mode == 2 && d / w.L != w.p) continue;
+        if (mode >= 2 && d / w.L != w.p) continue;
         drow[nd] = w.gy[d] + (int64_t)ep * w.row_bytes;
         yrow[nd] = w.ymaj[d] + (int64_t)ep * w.row_bytes;
         dwk[nd] = wts[t * w.K + k];
@@ -1661,7 +1664,13 @@ __global__ void __launch_bounds__(256) k_pack_grad(const WorldDev* __restrict__ 
         ++nd;
       }
     }
-    if (mode != 0) {
+    if (mode == 3) {   // one row per other GPU hit, into its GPU-level row space of comb
+      for (int q = 0; q < w.P; ++q) {
+        if (q == w.p) continue;
+        const int gp = gpos_g[t * w.P + q];
+        if (gp >= 0 && gp < w.Rg_cap) rrow[nr++] = w.comb[q * w.L] + (int64_t)gp * w.row_bytes;
+      }
+    } else if (mode != 0) {
       unsigned long long hit = hitmask[t];
       for (int d = 0; d < w.G; ++d) {
         if (!((hit >> d) & 1ull)) continue;
@@ -1852,9 +1861,70 @@ __global__ void __launch_bounds__(256) k_expand_grad(const WorldDev* __restrict_
   }
 }
 
+// ... per-GPU dedup (mode 3): received gradient row r (the GPU-level row space
+// of comb, same positions as the forward's recv_g rows) -> scaled rows for
+// each of its picks on this GPU (meta_g epos = l * N_cap + row, flat over the
+// local ranks) and their gate gradients into the flat gw rows
+template <typename T>
+__global__ void __launch_bounds__(256) k_expand_grad_g(const WorldDev* __restrict__ wp,
+                                                       const Offsets* __restrict__ offs) {
+  const WorldDev& w = *wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = w.row_bytes / 16;
+  int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = offs->R_g;
+  const RowMeta* meta = w.meta_g[w.p];
+  const uint8_t* ybase = w.ymaj[w.p * w.L];
+  uint8_t* gbase = w.gy[w.p * w.L];
+  float* gw = w.gw[w.p * w.L];
+  for (int64_t r = warp; r < total; r += nw) {
+    int nd = 0;
+    int eps[kMaxK], ks[kMaxK];
+    float wk[kMaxK];
+    for (int k = 0; k < w.K; ++k) {
+      RowMeta m = meta[r * w.K + k];
+      if (m.epos < 0) continue;
+      eps[nd] = m.epos;
+      wk[nd] = m.w;
+      ks[nd] = k;
+      ++nd;
+    }
+    float dot[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) dot[j] = 0.f;
+    const int4* src = reinterpret_cast<const int4*>(w.comb[w.p * w.L] + r * w.row_bytes);
+    for (int64_t v = lane; v < nvec; v += 32) {
+      float gf[Vec<T>::N];
+      Vec<T>::to_f32(ld_nc_v4(src + v), gf);
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) {
+        if (j >= nd) break;
+        float yf[Vec<T>::N], sf[Vec<T>::N];
+        Vec<T>::to_f32(ld_nc_v4(reinterpret_cast<const int4*>(ybase + (int64_t)eps[j] * w.row_bytes) + v), yf);
+#pragma unroll
+        for (int q = 0; q < Vec<T>::N; ++q) {
+          dot[j] = fmaf(gf[q], yf[q], dot[j]);
+          sf[q] = wk[j] * gf[q];
+        }
+        st_na_v4(reinterpret_cast<int4*>(gbase + (int64_t)eps[j] * w.row_bytes) + v,
+                 Vec<T>::from_f32(sf));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j >= nd) break;
+      float x = dot[j];
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) gw[r * w.K + ks[j]] = x;
+    }
+  }
+}
+
 // source: gate grads of dedup picks from the destination's gw rows (peer loads)
 __global__ void k_gate_grad(const WorldDev* __restrict__ wp, const int32_t* __restrict__ ids,
-                            const int32_t* __restrict__ gpos, int mode, float* __restrict__ dw) {
+                            const int32_t* __restrict__ gpos, int mode,
+                            const int32_t* __restrict__ gpos_g, float* __restrict__ dw) {
   const WorldDev& w = *wp;
   const int64_t n = (int64_t)w.L * w.T_r * w.K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1864,7 +1934,13 @@ __global__ void k_gate_grad(const WorldDev* __restrict__ wp, const int32_t* __re
     const int e = ids[i];
     if (e < 0 || mode == 0) continue;
     const int d = rank_of_slot(w, e);
-    if (mode == 2 && d / w.L == w.p) continue;   // direct pick: k_pack_grad wrote it
+    if (mode >= 2 && d / w.L == w.p) continue;   // direct pick: k_pack_grad wrote it
+    if (mode == 3) {   // the pick's GPU q wrote it at its GPU-level row of this token
+      const int q = d / w.L;
+      const int gp = gpos_g[t * w.P + q];
+      if (gp >= 0) dw[i] = w.gw[q * w.L][(int64_t)gp * w.K + k];
+      continue;
+    }
     const int gp = gpos[t * w.G + d];
     if (gp >= 0) dw[i] = w.gw[d][(int64_t)gp * w.K + k];
   }
@@ -2766,13 +2842,13 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
   HM_CHECK_ARG(w && g && ids && wts && dw, "hm_dispatch_grad: null argument");
   HM_CHECK_ARG(w->grad, "hm_dispatch_grad: world created without backward buffers");
   HM_CHECK_ARG(mode == w->last_mode, "hm_dispatch_grad: mode differs from the forward's");
-  HM_CHECK_ARG(mode <= 2, "hm_dispatch_grad: backward supports modes 0..2");
+  HM_CHECK_ARG(mode <= 3, "hm_dispatch_grad: mode must be 0..3");
   HM_CHECK_ARG(!w->h.U1, "hm_dispatch_grad: relay worlds have no backward");
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
   const int64_t T = (int64_t)h.L * h.T_r;
   int blocks = grid_for(T, 8, exch_blocks(w));
-  if (mode == 0 || (mode == 2 && h.P == 1)) {
+  if (mode == 0 || (mode >= 2 && h.P == 1)) {
     // every pick direct: one token per warp, up to 32 CTAs per SM
     blocks = grid_for(T, 8, w->max_blocks > 0 ? w->max_blocks : kSMs * 32);
     if (h.elem == 2)
@@ -2783,16 +2859,22 @@ HM_API int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, cons
                                                        dw);
   } else if (h.elem == 2)
     k_pack_grad<__nv_bfloat16><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->hitmask,
-                                                      w->gpos, w->epos, mode, dw);
+                                                      w->gpos, w->epos, mode, w->gpos_g, dw);
   else
     k_pack_grad<float><<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)g, ids, wts, w->hitmask,
-                                              w->gpos, w->epos, mode, dw);
+                                              w->gpos, w->epos, mode, w->gpos_g, dw);
   HM_LAUNCHED();
   if (h.P > 1) {
     k_barrier<<<1, 32, 0, s>>>(w->d, w->status);
     HM_LAUNCHED();
   }
-  if (mode != 0 && !(h.P == 1 && mode == 2)) {
+  if (mode == 3 && h.P > 1) {
+    if (h.elem == 2)
+      k_expand_grad_g<__nv_bfloat16><<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs);
+    else
+      k_expand_grad_g<float><<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs);
+    HM_LAUNCHED();
+  } else if (mode != 0 && mode != 3 && !(h.P == 1 && mode == 2)) {
     if (h.elem == 2)
       k_expand_grad<__nv_bfloat16><<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs);
     else
@@ -2810,9 +2892,16 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
   HM_RANGE("hm_combine_grad");
   HM_CHECK_ARG(w && ids && dw && dx, "hm_combine_grad: null argument");
   HM_CHECK_ARG(w->grad, "hm_combine_grad: world created without backward buffers");
+  HM_CHECK_ARG(mode == w->last_mode, "hm_combine_grad: mode differs from the forward's");
   cudaStream_t s = (cudaStream_t)stream;
   const WorldDev& h = w->h;
-  if (mode != 0 && !(h.P == 1 && mode == 2)) {
+  if (mode == 3 && h.P > 1) {   // unweighted sums of this GPU's picks per received row
+    with_row_type(h, [&](auto t, auto v) {
+      k_reduce_g<typename decltype(t)::type, decltype(v)::value>
+          <<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs, 1);
+    });
+    HM_LAUNCHED();
+  } else if (mode != 0 && mode != 3 && !(h.P == 1 && mode == 2)) {
     with_row_type(h, [&](auto t, auto v) {
       k_reduce<typename decltype(t)::type, decltype(v)::value>
           <<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs, 1, 1);
@@ -2831,7 +2920,8 @@ HM_API int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float*
         (uint8_t*)dx, nullptr);
   });
   HM_LAUNCHED();
-  k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode, dw);
+  k_gate_grad<<<grid_for(T * h.K, 256, kSMs * 8), 256, 0, s>>>(w->d, ids, w->gpos, mode,
+                                                                 w->gpos_g, dw);
   HM_LAUNCHED();
   return 0;
 }

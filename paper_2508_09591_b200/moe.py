@@ -65,8 +65,7 @@ class HierMoELayer:
         self.gpus, self.gpu_index = gpus, gpu_index
         self.local = ranks // gpus
         self.e_loc = experts // ranks
-        # backward supports the per-rank transports; True means per-GPU dedup
-        # for inference and per-remote-rank dedup when gradients are needed
+        # True / "gpu": per-GPU dedup (forward and backward)
         self.auto_transport = dedup == "auto"
         if self.auto_transport:
             from .topology import load_params
@@ -81,7 +80,7 @@ class HierMoELayer:
             self.transport_params = transport_params
             self.transport_every = max(1, int(transport_every))
             self.transport_log = []
-        self.dedup = "remote" if (grad and (dedup is True or dedup == "gpu")) else dedup
+        self.dedup = "gpu" if dedup is True else dedup
         self.renormalize = renormalize
         self.micro_batches = micro_batches
         t_mb = tokens_per_rank // micro_batches
@@ -354,7 +353,7 @@ class HierMoELayer:
             red = lambda t: dist.all_reduce(t, group=self.group)  # noqa: E731
         ch = choose_transport(mask_from_ids(slot, self.experts), self.runtime_topo,
                               self.transport_params, None, red, allow_deep=not self.grad)
-        self.dedup = "remote" if (self.grad and ch.mode == "gpu") else ch.mode
+        self.dedup = ch.mode
         self.transport_log.append((self.iteration, self.dedup, ch))
         return ch
 

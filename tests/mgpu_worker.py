@@ -107,6 +107,56 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
     ep.close()
 
 
+def run_backward(rank, world, dedup):
+    """Dispatch / combine backward across GPUs (K8) vs the analytic gradients
+    of stand-in experts y = s_e x: dw_k = <g_t, y_k>, dx_t = sum_k w_k s_k g_t
+    (every transport, incl. per-GPU dedup: gradient rows cross NVLink once per
+    (token, GPU), gate grads and pre-reduced input grads come back)."""
+    G, E, K, M, T_r, dtype = 8, 128, 8, 512, 64, torch.bfloat16
+    L = G // world
+    gen = torch.Generator().manual_seed(31)
+    logits = torch.randn(G * T_r, E, generator=gen)
+    x = torch.randn(G * T_r, M, generator=gen).to(dtype)
+    g = torch.randn(G * T_r, M, generator=gen).to(dtype)
+    lo, hi = rank * L * T_r, (rank + 1) * L * T_r
+    slot, w, _ = route_topk(logits[lo:hi].cuda(), K)
+    ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank, grad=True)
+    ep.dispatch(x[lo:hi].cuda(), slot, w, dedup=dedup)
+    torch.cuda.synchronize()
+    rows = ep.rows_received()
+    e_loc = E // G
+    n_e = ep.counts()[:, G:].sum(axis=0)
+    scales = []
+    for l in range(L):
+        d = rank * L + l
+        n = int(rows[l, 1])
+        xm = ep.read("xmaj", l, dtype, n * M).view(n, M)
+        row_slot = np.repeat(np.arange(d * e_loc, (d + 1) * e_loc), n_e[d * e_loc:(d + 1) * e_loc])
+        sc = torch.as_tensor(1.0 + row_slot / E, dtype=torch.float32).cuda()[:, None]
+        scales.append(sc)
+        ep.set_expert_outputs(l, (xm.float() * sc).to(dtype))
+    ep.combine(slot, w, dedup=dedup)
+    dw = ep.dispatch_grad(g[lo:hi].cuda(), slot, w, dedup=dedup)
+    for l in range(L):
+        n = scales[l].shape[0]
+        gy = ep.read("gy", l, dtype, n * M).view(n, M)
+        ep.write("gx", (gy.float() * scales[l]).to(dtype).contiguous(), l)
+    dx = ep.combine_grad(slot, dw, dedup=dedup)
+    torch.cuda.synchronize()
+    ep.check_status()
+    ids = slot.cpu().numpy()
+    s = (1.0 + np.arange(E) / E)[ids]
+    wn = w.cpu().numpy().astype(np.float64)
+    xd, gd = x[lo:hi].double().numpy(), g[lo:hi].double().numpy()
+    ydot = (gd * xd).sum(axis=1)[:, None] * s
+    ref_dx = (wn * s).sum(axis=1)[:, None] * gd
+    np.testing.assert_allclose(dw.double().cpu().numpy(), ydot, rtol=3e-2,
+                               atol=3e-2 * np.abs(ydot).max(), err_msg=f"dw {dedup}")
+    np.testing.assert_allclose(dx.double().cpu().numpy(), ref_dx, rtol=3e-2,
+                               atol=3e-2 * np.abs(ref_dx).max(), err_msg=f"dx {dedup}")
+    ep.close()
+
+
 def run_planner(rank, world):
     """Token-sharded swap planning: all-reduced statistics give every rank the
     reference's decision on the concatenated global mask."""
@@ -172,7 +222,7 @@ def run_migrate(rank, world):
 
 def run_layer_fused(rank, world):
     """Fused dispatch across GPUs: local picks gathered from x, rows that crossed
-    NVLink gathered from the receive buffers (per-GPU dedup, mode 3, forward;
+    NVLink gathered from the receive buffers (per-GPU dedup, mode 3, and
     per-rank dedup, mode 2, forward + backward) -- outputs and gradients
     bit-identical to the copying dispatch."""
     from paper_2508_09591_b200.moe import HierMoELayer
@@ -181,7 +231,7 @@ def run_layer_fused(rank, world):
     gen = torch.Generator(device="cuda").manual_seed(40 + rank)
     x = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
     gout = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
-    for dedup, grad in (("gpu", False), ("remote", True)):
+    for dedup, grad in (("gpu", False), ("remote", True), ("gpu", True)):
         res = []
         for fused in (False, True):
             layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, dedup=dedup,
@@ -215,6 +265,9 @@ def main():
         for dedup in ("all", "remote", "gpu", "none"):
             run_case(rank, world, G, E, K, M, T_r, dt, dedup, seed=100 + i)
             dist.barrier()
+    for dedup in ("all", "remote", "gpu", "none"):
+        run_backward(rank, world, dedup)
+        dist.barrier()
     run_migrate(rank, world)
     dist.barrier()
     run_layer_fused(rank, world)

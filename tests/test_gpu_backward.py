@@ -15,7 +15,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("dedup", ["all", "remote", "none"])
+@pytest.mark.parametrize("dedup", ["all", "remote", "gpu", "none"])
 @pytest.mark.parametrize("shape", [(8, 16, 2, 256, 128, torch.float32),
                                    (8, 128, 8, 512, 64, torch.bfloat16)])
 def test_dispatch_combine_backward(hm, dedup, shape):

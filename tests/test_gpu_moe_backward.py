@@ -8,7 +8,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("dedup", ["all", "remote", "none"])
+@pytest.mark.parametrize("dedup", ["all", "remote", "gpu", "none"])
 def test_layer_backward_matches_autograd(hm, dedup):
     from paper_2508_09591_b200.moe import HierMoELayer
     G, E, K, M, I, T_r = 8, 16, 2, 256, 256, 32
