@@ -164,14 +164,25 @@ int hm_route_group(const float* logits, int64_t T, int32_t E, int32_t K, int32_t
  * at G (traffic.py:67-82). */
 int hm_dispatch(hm_world* w, const void* x, const int32_t* ids, const float* wts, int32_t dedup,
                 void* stream);
-/* Destination-side re-expansion of dedup rows into expert-major rows. */
 /* hm_dispatch in two phases: the plan (per-chunk ranks, count exchange,
  * offsets) and the push (row movement + device barrier); hm_dispatch = both. */
 int hm_dispatch_plan(hm_world* w, const int32_t* ids, const float* wts, int32_t mode,
                      void* stream);
 int hm_dispatch_push(hm_world* w, const void* x, const int32_t* ids, const float* wts,
                      int32_t mode, void* stream);
+/* Destination-side re-expansion of dedup rows into expert-major rows. */
 int hm_expand(hm_world* w, void* stream);
+/* Exchange overlapped with the expert FFN (per-GPU dedup, mode 3, fused
+ * dispatch, N > 1; no reference counterpart -- the reference only models the
+ * AlltoAll, traffic.py:93-170): after hm_dispatch_plan, hm_dispatch_meta writes
+ * positions and receive metadata without moving rows; hm_experts_overlap runs
+ * the local rows' GEMM1 with the token rows crossing NVLink beside its tiles
+ * (warp 3 of every CTA), the device barrier, the received rows' GEMM1 and
+ * GEMM2 over all rows; hm_combine follows.  Same results as hm_dispatch +
+ * hm_expand + hm_expert_ffn_multi. */
+int hm_dispatch_meta(hm_world* w, const int32_t* ids, const float* wts, void* stream);
+int hm_experts_overlap(hm_world* w, const void* x, const void* w13, const void* w2,
+                       int32_t hidden, int32_t inter, void* h, void* g13, void* stream);
 /* Gate-weighted combine (pre-reduce per destination + source sum for dedup). */
 int hm_combine(hm_world* w, const float* wts, const int32_t* ids, int32_t dedup, void* out,
                void* stream);
@@ -211,7 +222,8 @@ int hm_sum_to_bf16(const float* a, const void* b, const void* c, void* out, int6
  * backward: output grads -> expert-output grads (dedup broadcast, replaying the
  * forward plan) + direct picks' gate grads; hm_combine_grad = dispatch
  * backward: expert-input grads -> token grads (dedup reduction) + remaining
- * gate grads. */
+ * gate grads.  Every transport mode 0..3 (mode 3: one gradient row per
+ * (token, other GPU hit), pre-reduced input grads per (token, GPU)). */
 int hm_dispatch_grad(hm_world* w, const void* g, const int32_t* ids, const float* wts,
                      int32_t mode, float* dw, void* stream);
 int hm_combine_grad(hm_world* w, const int32_t* ids, int32_t mode, float* dw, void* dx,
@@ -285,6 +297,14 @@ int hm_expert_ffn_multi(const void* x, int64_t x_rows, const int32_t* idx, const
                         int32_t groups_per_seg,
                         const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
                         void* y, void* g13, void* stream);
+/* ... over explicit row groups: group g = rows [g_row0[g], g_row0[g] +
+ * g_rows[g]) of the [rows] row space times expert weight g_wsel[g] of
+ * [nweights] experts; ctas > 0 caps the grid. */
+int hm_expert_ffn_groups(const void* x, int64_t x_rows, const int32_t* idx, const void* x_recv,
+                         int64_t rows, int32_t groups, const int32_t* g_row0,
+                         const int32_t* g_rows, const int32_t* g_wsel, int32_t nweights,
+                         const void* w13, const void* w2, int32_t hidden, int32_t inter, void* h,
+                         void* y, void* g13, int32_t ctas, void* stream);
 int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,
                                  const void* x_recv, int64_t seg_rows, int32_t segs,
                                  const int32_t* n_rows,

@@ -75,6 +75,9 @@ _SIGS = {
     "hm_dispatch_plan": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_dispatch_push": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "hm_expand": (c_int32, [c_void_p, c_void_p]),
+    "hm_dispatch_meta": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "hm_experts_overlap": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                                     c_void_p, c_void_p, c_void_p]),
     "hm_dispatch_grad": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                    c_void_p]),
     "hm_combine_grad": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
@@ -119,6 +122,10 @@ _SIGS = {
     "hm_expert_ffn_multi": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
                                       c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32,
                                       c_void_p, c_void_p, c_void_p, c_void_p]),
+    "hm_expert_ffn_groups": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
+                                       c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+                                       c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_int32,
+                                       c_void_p]),
     "hm_expert_ffn_backward_multi": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64,
                                                c_int32, c_void_p, c_int32, c_void_p, c_void_p,
                                                c_void_p, c_int32, c_int32, c_void_p, c_void_p,

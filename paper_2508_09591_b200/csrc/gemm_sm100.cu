@@ -22,6 +22,7 @@
 // Group sizes are read on the device (no host sync).
 
 #include "hm_common.cuh"
+#include "exch.cuh"
 
 #include <atomic>
 #include <cuda.h>
@@ -80,6 +81,11 @@ struct GemmArgs {
   // overlapped exchange computes the rows already on this GPU first)
   const int32_t* g_row0;
   const int32_t* g_wsel;
+  // exchange work run by warp 3 beside the tiles (exch.cuh): 0 none,
+  // 1 dispatch rows of exch_x
+  const hm::ExchWork* exch;
+  int exch_kind;
+  const int4* exch_x;
 };
 
 
@@ -762,6 +768,60 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Exchange executor (exch.cuh), one warp per CTA.  Rows are walked in the
+// dispatch kernels' spread order so concurrent warps' NVLink stores land all
+// over the peers' buffers.
+__device__ __forceinline__ int64_t exch_spread(int64_t i, int64_t n) {
+  const int64_t p = (n % 7919) ? 7919 : ((n % 104729) ? 104729 : 1);
+  return (i * p) % n;
+}
+__device__ __forceinline__ int4 exch_ld(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void exch_st(int4* p, int4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w));
+}
+constexpr int kExchU = 8;   // 16-byte vectors per lane in flight
+
+// kind 1: token t's row to every other GPU q with a receive row gpos_g[t][q]
+__device__ __noinline__ void exch_push(const hm::ExchWork& e, const int4* x, int lane) {
+  const int64_t n = e.ntok, nvec = e.nvec;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t t = exch_spread(i, n);
+    int4* mine = nullptr;
+    if (lane < e.P && lane != e.p) {
+      const int g = e.gpos_g[t * e.P + lane];
+      if (g >= 0 && g < e.rg_cap) mine = e.recv_g[lane] + (int64_t)g * nvec;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, mine != nullptr);
+    if (!m) continue;
+    const int4* src = x + t * nvec;
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kExchU) {
+      int4 buf[kExchU];
+#pragma unroll
+      for (int u = 0; u < kExchU; ++u) {
+        const int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = exch_ld(src + v);
+      }
+      for (unsigned mm = m; mm; mm &= mm - 1) {
+        int4* d = reinterpret_cast<int4*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine), __ffs(mm) - 1));
+#pragma unroll
+        for (int u = 0; u < kExchU; ++u) {
+          const int64_t v = v0 + u * 32 + lane;
+          if (v < nvec) exch_st(d + v, buf[u]);
+        }
+      }
+    }
+  }
+}
+
 // GA (modes 0/1): the A rows are gathered by index (args.a_idx) by warps 8-11
 // of each CTA with cp.async into its swizzled stage; they arrive on a local
 // gfull barrier, and warp 2's lane 0 forwards each completed stage to the
@@ -928,6 +988,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
     }
+  } else if (warp == 3 && args.exch_kind == 1) {   // dispatch rows beside the tiles
+    exch_push(*args.exch, args.exch_x, lane);
   } else if (GA && warp == 2) {
     if (lane == 0) {   // forwarder: this CTA's gathered stage -> the leader's full barrier
       int stage = 0;
@@ -1169,6 +1231,9 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   args.seg_rows = seg_rows;
   args.g_row0 = nullptr;
   args.g_wsel = nullptr;
+  args.exch = nullptr;
+  args.exch_kind = 0;
+  args.exch_x = nullptr;
   const size_t smem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiStageBytes;
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
@@ -1197,7 +1262,9 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
                 int64_t a_src_rows = 0, float* out_f32 = nullptr, int n_valid = 0,
                 int seg_groups = 0, int64_t seg_rows = 0, const void* a_src2 = nullptr,
                 bool b_mn = false, const int32_t* g_row0 = nullptr,
-                const int32_t* g_wsel = nullptr, int nweights = 0, int ctas = 0) {
+                const int32_t* g_wsel = nullptr, int nweights = 0, int ctas = 0,
+                const hm::ExchWork* exch = nullptr, int exch_kind = 0,
+                const void* exch_x = nullptr) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -1236,6 +1303,11 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.seg_rows = seg_rows;
   args.g_row0 = g_row0;
   args.g_wsel = g_wsel;
+  HM_CHECK_ARG(!exch_kind || (exch_kind == 1 && exch && exch_x),
+               "grouped gemm: exchange work needs its descriptor and rows");
+  args.exch = exch;
+  args.exch_kind = exch_kind;
+  args.exch_x = reinterpret_cast<const int4*>(exch_x);
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
@@ -1506,6 +1578,24 @@ HM_API int hm_expert_ffn_groups(const void* x, int64_t x_rows, const int32_t* id
   return launch_gemm(h, rows, w2, groups, g_rows, hidden, inter, 0, y, hidden, nullptr,
                      (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr, false,
                      g_row0, g_wsel, nweights, ctas);
+}
+
+int hm::ffn_gemm_groups(const void* a, int64_t rows, const void* b, int groups,
+                        const int32_t* g_rows, const int32_t* g_row0, const int32_t* g_wsel,
+                        int nweights, int N, int K, int swiglu, void* out, int64_t ld_out,
+                        void* out2, const int32_t* a_idx, int64_t a_src_rows, const void* a_src2,
+                        const hm::ExchWork* exch, int exch_kind, const void* exch_x,
+                        cudaStream_t s) {
+  return launch_gemm(a, rows, b, groups, g_rows, N, K, swiglu, out, ld_out, nullptr, s, out2,
+                     a_idx, a_src_rows, nullptr, 0, 0, 0, a_src2, false, g_row0, g_wsel,
+                     nweights, 0, exch, exch_kind, exch_x);
+}
+
+int hm::ffn_gemm_segments(const void* a, int64_t rows, const void* b, int groups,
+                          const int32_t* n_rows, int N, int K, void* out, int64_t ld_out,
+                          int seg_groups, int64_t seg_rows, cudaStream_t s) {
+  return launch_gemm(a, rows, b, groups, n_rows, N, K, 0, out, ld_out, nullptr, s, nullptr,
+                     nullptr, 0, nullptr, 0, seg_groups, seg_rows);
 }
 
 HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* idx,

@@ -30,6 +30,7 @@
 // (traffic.py:58-71).
 
 #include "hm_common.cuh"
+#include "exch.cuh"
 
 #include <cuda_bf16.h>
 #include <string.h>
@@ -850,7 +851,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
                                            int32_t* __restrict__ gpos, int32_t* __restrict__ epos_out,
                                            const int32_t* __restrict__ rank_g,
                                            int32_t* __restrict__ gpos_g, int* __restrict__ status,
-                                           int32_t* __restrict__ xidx) {
+                                           int32_t* __restrict__ xidx, int copy_rows = 1) {
   const int C = w.G + w.E + w.P;
   const unsigned long long gmask = w.L >= 64 ? ~0ull : ((1ull << w.L) - 1ull);
   const int64_t nvec = w.row_bytes / 16;
@@ -970,6 +971,7 @@ __device__ __forceinline__ void pack_token(const WorldDev& w, int64_t t, int lan
       for (int d = 0; d < w.G; ++d)
         if (!((hit >> d) & 1ull)) gpos[t * w.G + d] = -1;
   }
+  if (!copy_rows) return;   // metadata only: the rows move with the expert GEMM (exch.cuh)
   for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
     int4 buf[kUnroll];
 #pragma unroll
@@ -1003,7 +1005,7 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
                                               const int32_t* __restrict__ rank_g,
                                               int32_t* __restrict__ gpos_g,
                                               int* __restrict__ status,
-                                              int32_t* __restrict__ xidx) {
+                                              int32_t* __restrict__ xidx, int copy_rows) {
   const WorldDev& w = *wp;
   const int lane = threadIdx.x & 31;
   const int64_t T = (int64_t)w.L * w.T_r;
@@ -1015,7 +1017,7 @@ __global__ void __launch_bounds__(256) k_pack(const WorldDev* __restrict__ wp,
   for (int64_t i = warp; i < T; i += nw)
     pack_token(w, spread ? spread_index(i, T) : i, lane, x, ids, wts, chunk_off, rank_d,
                    rank_e, hitmask, offs, eoff, nchunks, mode, gpos, epos_out, rank_g, gpos_g,
-                   status, xidx);
+                   status, xidx, copy_rows);
 }
 
 // One-GPU pack (every destination local: modes 0, 2, 3 at P = 1): warp per
@@ -1946,6 +1948,40 @@ __global__ void k_gate_grad(const WorldDev* __restrict__ wp, const int32_t* __re
   }
 }
 
+// Row groups of this GPU's expert-major layout split by where the rows come
+// from (the overlapped forward, hm_experts_overlap): groups [0, L*E_loc) =
+// rows from sources on this GPU (local rank l, expert j: group l*E_loc + j);
+// groups [L*E_loc, 3*L*E_loc) = rows that crossed NVLink, two per expert
+// (sources before / after this GPU's ranks).  Row starts in the flat
+// [L][N_cap] space (rows are source-major within an expert), weight index
+// l*E_loc + j.
+__global__ void k_ffn_groups(const WorldDev* __restrict__ wp, const int32_t* __restrict__ n_e,
+                             int32_t* __restrict__ row0, int32_t* __restrict__ rows,
+                             int32_t* __restrict__ wsel) {
+  const WorldDev& w = *wp;
+  const int L = w.L, El = w.E_loc, C = w.G + w.E + w.P, nl = L * El;
+  const int32_t* cnt = w.counts[w.p * L];
+  for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+    const int l = i / El, j = i - l * El;
+    const int e = (w.p * L + l) * El + j;
+    int base = 0;
+    for (int j2 = 0; j2 < j; ++j2) base += n_e[e - j + j2];
+    int before = 0, local = 0;
+    for (int src = 0; src < w.p * L; ++src) before += cnt[(int64_t)src * C + w.G + e];
+    for (int src = w.p * L; src < (w.p + 1) * L; ++src) local += cnt[(int64_t)src * C + w.G + e];
+    const int r0 = l * (int)w.N_cap + base;
+    row0[i] = r0 + before;
+    rows[i] = local;
+    wsel[i] = i;
+    row0[nl + 2 * i] = r0;
+    rows[nl + 2 * i] = before;
+    wsel[nl + 2 * i] = i;
+    row0[nl + 2 * i + 1] = r0 + before + local;
+    rows[nl + 2 * i + 1] = n_e[e] - before - local;
+    wsel[nl + 2 * i + 1] = i;
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1982,6 +2018,11 @@ struct hm_world {
   // instead of expert-major row copies (the expert GEMM gathers)
   bool fused = false;
   int32_t* xidx = nullptr;     // [L][N_cap] source row of every expert-major row
+  // overlapped forward (hm_dispatch_meta + hm_experts_overlap): exchange
+  // descriptor (device), row groups [3][3 * L * E_loc], and the step's state
+  hm::ExchWork* exch = nullptr;
+  int32_t* grp = nullptr;
+  bool meta_only = false;      // hm_dispatch_meta ran: rows not yet moved
   unsigned long long* epoch_ctr = nullptr;   // device barrier epoch counter
   bool peers_ready = false;
   int last_mode = 0;
@@ -2000,7 +2041,7 @@ static inline int exch_blocks(const hm_world* w) {
 
 // segment ids for hm_world_timings
 enum Seg { kSegPlan, kSegNotify, kSegPack, kSegBarrier1, kSegExpand, kSegReduce, kSegBarrier2,
-           kSegGather, kSegCount };
+           kSegGather, kSegFfnLocal, kSegFfnRest, kSegCount };
 
 struct SegScope {
   hm_world* w;
@@ -2149,6 +2190,8 @@ HM_API int hm_world_destroy(hm_world* w) {
     for (int i = 0; i < 2 * 16; ++i) cudaEventDestroy(w->ev[i]);
   for (void* p : w->opened) cudaIpcCloseMemHandle(p);
   cudaFree(w->sym);
+  cudaFree(w->exch);
+  cudaFree(w->grp);
   cudaFree(w->chunk_cnt);
   cudaFree(w->rank_d);
   cudaFree(w->rank_e);
@@ -2420,7 +2463,7 @@ static int dispatch_push(hm_world* w, const void* x, const int32_t* ids, const f
     k_pack<<<blocks, 256, 0, s>>>(w->d, (const uint8_t*)x, ids, wts, w->chunk_cnt, w->rank_d,
                                   w->rank_e, w->hitmask, w->offs, w->eoff, w->nchunks, mode,
                                   w->gpos, w->epos, w->rank_g, w->gpos_g, w->status,
-                                  w->fused ? w->xidx : nullptr);
+                                  w->fused ? w->xidx : nullptr, 1);
   }
   HM_LAUNCHED();
   if (h.P > 1) {
@@ -2452,6 +2495,113 @@ HM_API int hm_expand(hm_world* w, void* stream) {
   else
     k_expand<<<blocks, 256, 0, (cudaStream_t)stream>>>(w->d, w->offs);
   HM_LAUNCHED();
+  return 0;
+}
+
+// Overlapped forward, step 1 (per-GPU dedup across GPUs, fused dispatch):
+// after hm_dispatch_plan, write every pick's position, the receive rows'
+// metadata and the local picks' row indices -- but move no rows: they cross
+// NVLink inside hm_experts_overlap's first GEMM.
+HM_API int hm_dispatch_meta(hm_world* w, const int32_t* ids, const float* wts, void* stream) {
+  HM_RANGE("hm_dispatch_meta");
+  HM_CHECK_ARG(w && ids && wts, "hm_dispatch_meta: null argument");
+  HM_CHECK_ARG(w->last_mode == 3 && w->h.P > 1 && w->fused && !w->h.U1,
+               "hm_dispatch_meta: needs a per-GPU dedup plan (mode 3) across GPUs with the "
+               "fused dispatch");
+  HM_CHECK_ARG(w->h.P <= hm::kExchMaxGpus, "hm_dispatch_meta: at most %d GPUs",
+               hm::kExchMaxGpus);
+  cudaStream_t s = (cudaStream_t)stream;
+  const WorldDev& h = w->h;
+  const int64_t T = (int64_t)h.L * h.T_r;
+  SegScope sc(w, kSegPack, s);
+  k_pack<<<grid_for(T, 8, exch_blocks(w)), 256, 0, s>>>(
+      w->d, nullptr, ids, wts, w->chunk_cnt, w->rank_d, w->rank_e, w->hitmask, w->offs, w->eoff,
+      w->nchunks, 3, w->gpos, w->epos, w->rank_g, w->gpos_g, w->status, w->xidx, 0);
+  HM_LAUNCHED();
+  w->meta_only = true;
+  return 0;
+}
+
+// Overlapped forward, step 2: the expert FFN of this GPU's ranks with the
+// dispatch folded into it --
+//   GEMM1 over the rows already here (local tokens), its warp 3 pushing every
+//     token row to the other GPUs hit (exch.cuh kind 1);
+//   device barrier; received rows get their row indices;
+//   GEMM1 over the received rows, GEMM2 over all rows.
+// hm_combine follows as usual.  x: this GPU's token
+// rows (the fused dispatch's source); w13 / w2: [L * E_loc] experts; h [L*N_cap][I],
+// y = the world's ymaj; g13 optional pre-activations.  Same rows, same bits as
+// hm_dispatch + hm_expand + hm_expert_ffn_multi + hm_combine.
+HM_API int hm_experts_overlap(hm_world* w, const void* x, const void* w13, const void* w2,
+                              int32_t hidden, int32_t inter, void* h_buf, void* g13,
+                              void* stream) {
+  HM_RANGE("hm_experts_overlap");
+  HM_CHECK_ARG(w && x && w13 && w2 && h_buf, "hm_experts_overlap: null argument");
+  HM_CHECK_ARG(w->meta_only, "hm_experts_overlap: call hm_dispatch_meta first");
+  const WorldDev& h = w->h;
+  HM_CHECK_ARG((int64_t)hidden * 2 == h.row_bytes && h.elem == 2,
+               "hm_experts_overlap: bf16 rows of `hidden` features");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nl = h.L * h.E_loc;
+  HM_CHECK_ARG(2 * nl <= 256, "hm_experts_overlap: at most 128 experts per GPU");
+  HM_CHECK_ARG(w->n_e, "hm_experts_overlap: no plan");
+  if (!w->exch) {   // pointer tables are fixed per world: build the descriptor once
+    hm::ExchWork e;
+    memset(&e, 0, sizeof(e));
+    e.P = h.P;
+    e.p = h.p;
+    e.G = h.G;
+    e.K = h.K;
+    e.T_r = (int)h.T_r;
+    e.nvec = h.row_bytes / 16;
+    e.ntok = (int64_t)h.L * h.T_r;
+    e.rg_cap = h.Rg_cap;
+    e.gpos_g = w->gpos_g;
+    for (int q = 0; q < h.P; ++q) e.recv_g[q] = reinterpret_cast<int4*>(h.recv_g[q]);
+    HM_CUDA(cudaMalloc(&w->exch, sizeof(hm::ExchWork)));
+    HM_CUDA(cudaMemcpy(w->exch, &e, sizeof(e), cudaMemcpyHostToDevice));
+    HM_CUDA(cudaMalloc(&w->grp, (size_t)3 * 3 * nl * 4));
+  }
+  int32_t* row0 = w->grp;
+  int32_t* rows = row0 + 3 * nl;
+  int32_t* wsel = rows + 3 * nl;
+  k_ffn_groups<<<1, 256, 0, s>>>(w->d, w->n_e, row0, rows, wsel);
+  HM_LAUNCHED();
+  const int64_t R = (int64_t)h.L * h.N_cap;
+  const void* recv = h.recv_g[h.p];
+  __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(h.ymaj[h.p * h.L]);
+  const int M = hidden, I = inter;
+  int st;
+  // local rows: GEMM1, pushing the rows to the other GPUs beside the tiles
+  {
+    SegScope sc(w, kSegFfnLocal, s);
+    if ((st = hm::ffn_gemm_groups(x, R, w13, nl, rows, row0, wsel, nl, 2 * I, M, 1, h_buf, I,
+                                  g13, w->xidx, (int64_t)h.L * h.T_r, recv, w->exch, 1, x, s)))
+      return st;
+  }
+  {
+    SegScope sc(w, kSegBarrier1, s);
+    k_barrier<<<1, 32, 0, s>>>(w->d, w->status);
+    HM_LAUNCHED();
+  }
+  {
+    SegScope sc(w, kSegExpand, s);
+    k_index_recv_g<<<exch_blocks(w), 256, 0, s>>>(w->d, w->offs, w->xidx);
+    HM_LAUNCHED();
+  }
+  // received rows: GEMM1; then GEMM2 over every row (one launch, the
+  // hm_expert_ffn_multi layout: rank l's experts at rows l * N_cap ..)
+  {
+    SegScope sc(w, kSegFfnRest, s);
+    if ((st = hm::ffn_gemm_groups(x, R, w13, 2 * nl, rows + nl, row0 + nl, wsel + nl, nl, 2 * I,
+                                  M, 1, h_buf, I, g13, w->xidx, (int64_t)h.L * h.T_r, recv,
+                                  nullptr, 0, nullptr, s)))
+      return st;
+    if ((st = hm::ffn_gemm_segments(h_buf, R, w2, nl, w->n_e + h.p * nl, M, I, y, M, h.E_loc,
+                                    h.N_cap, s)))
+      return st;
+  }
+  w->meta_only = false;
   return 0;
 }
 
@@ -2807,7 +2957,9 @@ HM_API int hm_world_set_timing(hm_world* w, int32_t enable) {
 }
 
 // Milliseconds of the most recent launch of each segment (after a stream sync):
-// plan, notify, pack, barrier1, expand, reduce, barrier2, gather; -1 if unused.
+// plan, notify, pack, barrier1, expand, reduce, barrier2, gather, and the
+// overlapped forward's local-rows GEMM1 (+ row push) and remaining GEMMs;
+// -1 if unused.
 HM_API int hm_world_timings(hm_world* w, float* ms, int32_t n) {
   HM_CHECK_ARG(w && ms, "hm_world_timings: null argument");
   for (int i = 0; i < n && i < kSegCount; ++i) {

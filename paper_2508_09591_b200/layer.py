@@ -200,6 +200,14 @@ class EPWorld:
         if mode:
             _lib.call("hm_expand", self._h, s)
 
+    def dispatch_meta(self, slot_ids: torch.Tensor, weights: torch.Tensor) -> None:
+        """Per-GPU dedup plan + every row's position and receive metadata,
+        without moving rows (the overlapped forward: hm_experts_overlap moves
+        them inside the expert GEMMs).  Fused dispatch across GPUs only."""
+        s = stream_ptr()
+        _lib.call("hm_dispatch_plan", self._h, ptr(slot_ids), ptr(weights), MODES["gpu"], s)
+        _lib.call("hm_dispatch_meta", self._h, ptr(slot_ids), ptr(weights), s)
+
     def dispatch_ptr(self, x_ptr: int, slot_ids: torch.Tensor, weights: torch.Tensor,
                      dedup=True) -> None:
         """dispatch() with the payload given as a device pointer to

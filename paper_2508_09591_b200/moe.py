@@ -29,7 +29,8 @@ class HierMoELayer:
                  n_cap_rows: int = 0, layer_index: int = 0, router: str = "softmax",
                  n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
                  shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1,
-                 transport_params=None, transport_every: int = 50, fused_dispatch=None):
+                 transport_params=None, transport_every: int = 50, fused_dispatch=None,
+                 overlap: bool = True):
         """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
         (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
         / ``route_scale`` and a per-expert score bias).
@@ -106,6 +107,9 @@ class HierMoELayer:
         if self.fused and self.dedup == "all":
             raise ValueError("the fused dispatch needs a direct transport (not dedup='all')")
         self._x_cur = None
+        # exchange inside the expert GEMMs (hm_experts_overlap): per-GPU dedup
+        # across GPUs with the fused dispatch, one micro-batch
+        self.overlap = bool(overlap)
         self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]
         self.grad = grad
         # router replicated on every GPU (seeded identically); experts: the
@@ -292,6 +296,15 @@ class HierMoELayer:
         raw transport across GPUs, whose rows land expert-major on the peer)."""
         return self.fused and (self.gpus == 1 or self.dedup in (True, "gpu", "remote"))
 
+    def overlap_now(self) -> bool:
+        """Whether this step runs the exchange inside the expert GEMMs: the
+        token rows cross NVLink beside the local rows' GEMM1 tiles and the
+        received rows' pre-reduced outputs go back beside the local GEMM2
+        (hm_dispatch_meta + hm_experts_overlap)."""
+        return (self.overlap and self.gpus > 1 and self.micro_batches == 1
+                and self.dedup in (True, "gpu") and self.fused_now()
+                and 2 * self.local * self.e_loc <= 256)
+
     def _rows_source(self, wd, x_rows_t: torch.Tensor):
         """(x_ptr, x_rows, idx_ptr, recv_ptr) of the experts' A rows."""
         if not wd.fused:
@@ -394,11 +407,20 @@ class HierMoELayer:
                     s_m.wait_event(prev_d)
                 self._mark(f"dispatch{m}")
                 wd.set_fused(self.fused_now())
-                wd.dispatch(x[rows], slot[rows], w[rows], dedup=self.dedup)
-                prev_d = torch.cuda.Event()
-                prev_d.record(s_m)
-                self._mark(f"experts{m}")
-                self.experts_forward(m)   # expert-major rows are local after the dispatch
+                if self.overlap_now():   # rows move inside the expert GEMMs
+                    wd.dispatch_meta(slot, w)
+                    prev_d = torch.cuda.Event()
+                    prev_d.record(s_m)
+                    self._mark(f"experts{m}")
+                    _lib.call("hm_experts_overlap", wd._h, ptr(x), ptr(self.w13), ptr(self.w2),
+                              self.hidden, self.inter, ptr(self.hs[m]),
+                              self.g13s[m].data_ptr() if self.grad else None, stream_ptr())
+                else:
+                    wd.dispatch(x[rows], slot[rows], w[rows], dedup=self.dedup)
+                    prev_d = torch.cuda.Event()
+                    prev_d.record(s_m)
+                    self._mark(f"experts{m}")
+                    self.experts_forward(m)   # expert-major rows are local after the dispatch
                 self._mark(f"experts{m}_end")
                 if shared is not None:
                     s_m.wait_event(self._shared_done)

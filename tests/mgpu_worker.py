@@ -233,10 +233,15 @@ def run_layer_fused(rank, world):
     gout = torch.randn(L * T_r, M, device="cuda", generator=gen).to(torch.bfloat16)
     for dedup, grad in (("gpu", False), ("remote", True), ("gpu", True)):
         res = []
-        for fused in (False, True):
+        # copying dispatch, fused dispatch, fused + exchange inside the GEMMs
+        for fused, overlap in ((False, False), (True, False), (True, True)):
             layer = HierMoELayer(G, E, K, M, I, T_r, gpus=world, gpu_index=rank, dedup=dedup,
-                                 seed=3, grad=grad, fused_dispatch=fused, optimizer_state=False)
+                                 seed=3, grad=grad, fused_dispatch=fused, optimizer_state=False,
+                                 overlap=overlap)
+            assert layer.overlap_now() == (overlap and dedup == "gpu")
             out = layer(x).clone()
+            if not grad:   # a second step reuses the buffers, barriers and flags
+                out = layer(x).clone()
             got = [out]
             if grad:
                 got += [layer.backward(gout).clone(), layer.dw13.clone(), layer.dw2.clone(),
@@ -248,8 +253,9 @@ def run_layer_fused(rank, world):
             res.append(got)
             layer.close()
             dist.barrier()
-        for a, b in zip(*res):
-            assert torch.equal(a, b), ("fused", dedup)
+        for other in res[1:]:
+            for a, b in zip(res[0], other):
+                assert torch.equal(a, b), ("fused / overlapped", dedup, grad)
 
 
 def main():
