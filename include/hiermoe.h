@@ -311,7 +311,11 @@ int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* i
                                  int32_t groups_per_seg, const void* w13, const void* w2,
                                  const void* gy, int32_t hidden, int32_t inter, const void* g13,
                                  void* dh, void* dg13, void* h, int32_t* layout, void* gx,
-                                 void* dw13, void* dw2, int32_t accumulate, void* stream);
+                                 void* dw13, void* dw2, int32_t accumulate, int32_t parts,
+                                 void* stream);
+/* parts: 1 = data gradients (dH, SwiGLU backward, gX), 2 = weight gradients
+ * (dW2, dW13 from part 1's scratch), 3 = both -- a caller can run the
+ * dispatch backward of gX beside the weight-gradient GEMMs. */
 /* FFN option (no reference counterpart): 1 = cap on the persistent GEMM grid
  * in CTAs (0 = one per SM), so a concurrent exchange keeps SMs of its own. */
 int hm_ffn_set_option(int32_t option, int32_t value);

@@ -130,7 +130,7 @@ _SIGS = {
                                                c_int32, c_void_p, c_int32, c_void_p, c_void_p,
                                                c_void_p, c_int32, c_int32, c_void_p, c_void_p,
                                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                               c_void_p, c_int32, c_void_p]),
+                                               c_void_p, c_int32, c_int32, c_void_p]),
     "hm_expert_ffn_backward_saved": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p,
                                                c_void_p, c_void_p, c_int32, c_int32, c_void_p,
                                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -1435,14 +1435,16 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                         void* dg13, void* h, int32_t* layout, void* gx, void* dw13, void* dw2,
                         void* stream, int accumulate = 0, const int32_t* x_idx = nullptr,
                         int64_t x_rows = 0, int seg_groups = 0, int64_t seg_rows = 0,
-                        const void* x_recv = nullptr) {
+                        const void* x_recv = nullptr, int parts = 3) {
   cudaStream_t s = (cudaStream_t)stream;
   HM_CHECK_ARG(!x_idx || g13_saved,
                "ffn backward: gathered activations need the saved pre-activations");
+  HM_CHECK_ARG(parts >= 1 && parts <= 3, "ffn backward: parts must be 1, 2 or 3");
   const int M = hidden, I = inter;
   int st;
-  // gate/up pre-activations (recomputed unless the forward saved them), then dH
   const int sg = seg_groups, segs = sg > 0 ? (groups + sg - 1) / sg : 1;
+  if (parts & 1) {
+  // gate/up pre-activations (recomputed unless the forward saved them), then dH
   if (!g13_saved && (st = launch_gemm(x, a_rows, w13, groups, n_rows, 2 * I, M, 0, g13, 2 * I,
                                       nullptr, s, nullptr, nullptr, 0, nullptr, 0, sg, seg_rows)))
     return st;
@@ -1461,8 +1463,11 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
   if ((st = launch_gemm(dg13, a_rows, w13, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s,
                         nullptr, nullptr, 0, nullptr, 0, sg, seg_rows, nullptr, true)))
     return st;
+  }
+  if (!(parts & 2)) return 0;
   // weight gradients straight from the token-major activations (MN-major
-  // tcgen05 operands), reduction over each expert's own rows
+  // tcgen05 operands), reduction over each expert's own rows (dg13 and h from
+  // part 1, kept in the scratch buffers)
   if ((st = launch_gemm_wgrad(gy, h, a_rows, groups, n_rows, M, I, dw2, I, s, accumulate, nullptr,
                               0, nullptr, sg, seg_rows)))
     return st;
@@ -1605,12 +1610,12 @@ HM_API int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int
                                         const void* gy, int32_t hidden, int32_t inter,
                                         const void* g13, void* dh, void* dg13, void* h,
                                         int32_t* layout, void* gx, void* dw13, void* dw2,
-                                        int32_t accumulate, void* stream) {
+                                        int32_t accumulate, int32_t parts, void* stream) {
   HM_RANGE("hm_expert_ffn_backward_multi");
   HM_CHECK_ARG(x && g13 && segs >= 1 && groups_per_seg >= 1 && seg_rows >= 1,
                "hm_expert_ffn_backward_multi: bad argument");
   return ffn_backward(x, (int64_t)segs * seg_rows, n_rows, segs * groups_per_seg, w13, w2, gy,
                       hidden, inter, const_cast<void*>(g13), 1, dh, dg13, h, layout, gx,
                       dw13, dw2, stream, accumulate, idx, idx ? x_rows : 0, groups_per_seg,
-                      seg_rows, x_recv);
+                      seg_rows, x_recv, parts);
 }

@@ -30,7 +30,7 @@ class HierMoELayer:
                  n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
                  shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1,
                  transport_params=None, transport_every: int = 50, fused_dispatch=None,
-                 overlap: bool = True):
+                 overlap=None):
         """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
         (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
         / ``route_scale`` and a per-expert score bias).
@@ -107,9 +107,15 @@ class HierMoELayer:
         if self.fused and self.dedup == "all":
             raise ValueError("the fused dispatch needs a direct transport (not dedup='all')")
         self._x_cur = None
-        # exchange inside the expert GEMMs (hm_experts_overlap): per-GPU dedup
-        # across GPUs with the fused dispatch, one micro-batch
-        self.overlap = bool(overlap)
+        # dispatch inside the expert GEMMs (hm_experts_overlap): per-GPU dedup
+        # across GPUs with the fused dispatch, one micro-batch.  Default: on
+        # for inference layers only -- splitting GEMM1 at the local / received
+        # row boundary adds a partial tile per expert, which outweighs the
+        # hidden push once GEMM1 also stores the pre-activations
+        # (profiles/r02/overlap_*.jsonl)
+        self.overlap = (not grad) if overlap is None else bool(overlap)
+        self._cside = torch.cuda.Stream() if grad else None   # dispatch backward beside wgrads
+        self.bwd_overlap = True
         self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]
         self.grad = grad
         # router replicated on every GPU (seeded identically); experts: the
@@ -452,8 +458,9 @@ class HierMoELayer:
         combine bwd (dedup broadcast of dL/dout, replaying the forward plan)
         -> expert FFN bwd (tcgen05) -> dispatch bwd (dedup reduction) ->
         gate bwd (softmax top-K, or the DeepSeek-V3 normalised sigmoid) ->
-        router GEMM bwd (cuBLAS); the shared expert's FFN backward (tcgen05)
-        runs on a side stream beside the routed path.
+        router GEMMs (tcgen05); the shared expert's FFN backward runs on a
+        side stream beside the routed path, and the dispatch backward beside
+        the weight-gradient GEMMs.
         """
         if not self.grad or self._saved is None:
             raise RuntimeError("HierMoELayer.backward needs grad=True and a forward first")
@@ -490,11 +497,23 @@ class HierMoELayer:
                 p_ne, _ = wd.buffer("n_e", 0)
                 first = self.gpu_index * self.local * self.e_loc
                 x_ptr, x_rows, idx, recv = self._rows_source(wd, x[rows])
-                expert_ffn_backward_multi_ptrs(
-                    x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first, self.e_loc,
-                    self.w13, self.w2, wd.buffer("gy", 0)[0], self.hidden, self.inter, self.bwd,
-                    wd.buffer("gx", 0)[0], self.dw13, self.dw2, self.g13s[m].data_ptr(),
-                    accumulate=m > 0, recv_ptr=recv)
+                args = (x_ptr, x_rows, idx, wd.n_cap, self.local, p_ne + 4 * first, self.e_loc,
+                        self.w13, self.w2, wd.buffer("gy", 0)[0], self.hidden, self.inter,
+                        self.bwd, wd.buffer("gx", 0)[0], self.dw13, self.dw2,
+                        self.g13s[m].data_ptr())
+                if self.micro_batches == 1 and self.bwd_overlap:
+                    # data gradients, then the dispatch backward of gx (HBM /
+                    # NVLink) on a side stream beside the weight-gradient GEMMs
+                    # (tensor cores), which read only the FFN's own scratch
+                    s_m = torch.cuda.current_stream()
+                    expert_ffn_backward_multi_ptrs(*args, recv_ptr=recv, parts=1)
+                    self._cside.wait_stream(s_m)
+                    with torch.cuda.stream(self._cside):
+                        wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])
+                    expert_ffn_backward_multi_ptrs(*args, recv_ptr=recv, parts=2)
+                    s_m.wait_stream(self._cside)
+                    continue
+                expert_ffn_backward_multi_ptrs(*args, accumulate=m > 0, recv_ptr=recv)
                 ffn_done = torch.cuda.Event()
                 ffn_done.record()
                 wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])
