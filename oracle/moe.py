@@ -101,9 +101,14 @@ class DispatchPlan:
       c     [G, E]      selections rank s sends to slot e (no dedup)
       epos  [T, K]      expert-major row of (t, k) at rank dest(e_k)
       n_e   [E]         rows per slot (expert GEMM group sizes)
+
+    ``gpus``: the ranks' GPU count P.  A slot's rows are source-major starting
+    with the sources on the destination's own GPU (ranks rotated by the GPU's
+    first rank; the identity with one GPU), so the rows a GPU already holds
+    form one block in front of the ones that cross NVLink.
     """
 
-    def __init__(self, ids: np.ndarray, ranks: int, experts: int):
+    def __init__(self, ids: np.ndarray, ranks: int, experts: int, gpus: int = 1):
         ids = np.asarray(ids, dtype=np.int64)
         t, k = ids.shape
         if t % ranks:
@@ -134,8 +139,12 @@ class DispatchPlan:
             lo = (e // e_loc) * e_loc
             ebase[e] = self.n_e[lo:e].sum()
         epos = np.full((t, k), -1, dtype=np.int64)
+        per_gpu = ranks // gpus
         for e in range(experts):
             tt, kk = np.nonzero(ids == e)          # row-major => token order
+            q0 = (e // e_loc) // per_gpu * per_gpu
+            order = np.argsort((src[tt] - q0) % ranks, kind="stable")
+            tt, kk = tt[order], kk[order]
             epos[tt, kk] = ebase[e] + np.arange(tt.size)
         self.epos = epos
         self.ebase = ebase

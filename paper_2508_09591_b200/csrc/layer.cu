@@ -742,10 +742,17 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
             n4 = n3 + G + 1, n5 = n4 + L;
   for (int i = threadIdx.x; i < n5; i += blockDim.x) {
     if (i < n0) {
+      // expert e's rows at its destination GPU q are source-major starting
+      // with q's own ranks (rotation by q * L): the rows already on q form one
+      // block in front, so the overlapped forward computes them as whole
+      // tiles before the received ones arrive
       const int s_loc = i / E, e = i - s_loc * E;
       const int sg = gp * L + s_loc;
+      const int q0 = (e / E_loc) / L * L;
+      const int key = (sg - q0 + G) % G;
       int base = s_eb[e];
-      for (int src = 0; src < sg; ++src) base += cnt[(int64_t)src * C + G + e];
+      for (int src = 0; src < G; ++src)
+        if ((src - q0 + G) % G < key) base += cnt[(int64_t)src * C + G + e];
       eoff[i] = base;
     } else if (i < n1) {
       const int k = i - n0, s_loc = k / G, d = k - s_loc * G;
@@ -1949,12 +1956,12 @@ __global__ void k_gate_grad(const WorldDev* __restrict__ wp, const int32_t* __re
 }
 
 // Row groups of this GPU's expert-major layout split by where the rows come
-// from (the overlapped forward, hm_experts_overlap): groups [0, L*E_loc) =
-// rows from sources on this GPU (local rank l, expert j: group l*E_loc + j);
-// groups [L*E_loc, 3*L*E_loc) = rows that crossed NVLink, two per expert
-// (sources before / after this GPU's ranks).  Row starts in the flat
-// [L][N_cap] space (rows are source-major within an expert), weight index
-// l*E_loc + j.
+// from (the overlapped forward, hm_experts_overlap).  An expert's rows start
+// with the ones from this GPU's sources (k_notify's rotated order): group
+// l*E_loc + j = the whole 256-row tiles of those, group L*E_loc + l*E_loc + j =
+// the rest (the partial local tile + the rows that crossed NVLink), so the
+// split adds no partial tile.  Row starts in the flat [L][N_cap] space,
+// weight index l*E_loc + j.
 __global__ void k_ffn_groups(const WorldDev* __restrict__ wp, const int32_t* __restrict__ n_e,
                              int32_t* __restrict__ row0, int32_t* __restrict__ rows,
                              int32_t* __restrict__ wsel) {
@@ -1966,19 +1973,16 @@ __global__ void k_ffn_groups(const WorldDev* __restrict__ wp, const int32_t* __r
     const int e = (w.p * L + l) * El + j;
     int base = 0;
     for (int j2 = 0; j2 < j; ++j2) base += n_e[e - j + j2];
-    int before = 0, local = 0;
-    for (int src = 0; src < w.p * L; ++src) before += cnt[(int64_t)src * C + w.G + e];
+    int local = 0;
     for (int src = w.p * L; src < (w.p + 1) * L; ++src) local += cnt[(int64_t)src * C + w.G + e];
+    const int whole = local / 256 * 256;
     const int r0 = l * (int)w.N_cap + base;
-    row0[i] = r0 + before;
-    rows[i] = local;
+    row0[i] = r0;
+    rows[i] = whole;
     wsel[i] = i;
-    row0[nl + 2 * i] = r0;
-    rows[nl + 2 * i] = before;
-    wsel[nl + 2 * i] = i;
-    row0[nl + 2 * i + 1] = r0 + before + local;
-    rows[nl + 2 * i + 1] = n_e[e] - before - local;
-    wsel[nl + 2 * i + 1] = i;
+    row0[nl + i] = r0 + whole;
+    rows[nl + i] = n_e[e] - whole;
+    wsel[nl + i] = i;
   }
 }
 
@@ -2019,7 +2023,7 @@ struct hm_world {
   bool fused = false;
   int32_t* xidx = nullptr;     // [L][N_cap] source row of every expert-major row
   // overlapped forward (hm_dispatch_meta + hm_experts_overlap): exchange
-  // descriptor (device), row groups [3][3 * L * E_loc], and the step's state
+  // descriptor (device), row groups [3][2 * L * E_loc], and the step's state
   hm::ExchWork* exch = nullptr;
   int32_t* grp = nullptr;
   bool meta_only = false;      // hm_dispatch_meta ran: rows not yet moved
@@ -2524,10 +2528,10 @@ HM_API int hm_dispatch_meta(hm_world* w, const int32_t* ids, const float* wts, v
 
 // Overlapped forward, step 2: the expert FFN of this GPU's ranks with the
 // dispatch folded into it --
-//   GEMM1 over the rows already here (local tokens), its warp 3 pushing every
-//     token row to the other GPUs hit (exch.cuh kind 1);
+//   GEMM1 over the whole tiles of rows already here (local tokens), its warp 3
+//     pushing every token row to the other GPUs hit (exch.cuh);
 //   device barrier; received rows get their row indices;
-//   GEMM1 over the received rows, GEMM2 over all rows.
+//   GEMM1 over the remaining rows, GEMM2 over all rows.
 // hm_combine follows as usual.  x: this GPU's token
 // rows (the fused dispatch's source); w13 / w2: [L * E_loc] experts; h [L*N_cap][I],
 // y = the world's ymaj; g13 optional pre-activations.  Same rows, same bits as
@@ -2543,7 +2547,7 @@ HM_API int hm_experts_overlap(hm_world* w, const void* x, const void* w13, const
                "hm_experts_overlap: bf16 rows of `hidden` features");
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = h.L * h.E_loc;
-  HM_CHECK_ARG(2 * nl <= 256, "hm_experts_overlap: at most 128 experts per GPU");
+  HM_CHECK_ARG(nl <= 256, "hm_experts_overlap: at most 256 experts per GPU");
   HM_CHECK_ARG(w->n_e, "hm_experts_overlap: no plan");
   if (!w->exch) {   // pointer tables are fixed per world: build the descriptor once
     hm::ExchWork e;
@@ -2560,11 +2564,11 @@ HM_API int hm_experts_overlap(hm_world* w, const void* x, const void* w13, const
     for (int q = 0; q < h.P; ++q) e.recv_g[q] = reinterpret_cast<int4*>(h.recv_g[q]);
     HM_CUDA(cudaMalloc(&w->exch, sizeof(hm::ExchWork)));
     HM_CUDA(cudaMemcpy(w->exch, &e, sizeof(e), cudaMemcpyHostToDevice));
-    HM_CUDA(cudaMalloc(&w->grp, (size_t)3 * 3 * nl * 4));
+    HM_CUDA(cudaMalloc(&w->grp, (size_t)3 * 2 * nl * 4));
   }
   int32_t* row0 = w->grp;
-  int32_t* rows = row0 + 3 * nl;
-  int32_t* wsel = rows + 3 * nl;
+  int32_t* rows = row0 + 2 * nl;
+  int32_t* wsel = rows + 2 * nl;
   k_ffn_groups<<<1, 256, 0, s>>>(w->d, w->n_e, row0, rows, wsel);
   HM_LAUNCHED();
   const int64_t R = (int64_t)h.L * h.N_cap;
@@ -2593,9 +2597,9 @@ HM_API int hm_experts_overlap(hm_world* w, const void* x, const void* w13, const
   // hm_expert_ffn_multi layout: rank l's experts at rows l * N_cap ..)
   {
     SegScope sc(w, kSegFfnRest, s);
-    if ((st = hm::ffn_gemm_groups(x, R, w13, 2 * nl, rows + nl, row0 + nl, wsel + nl, nl, 2 * I,
-                                  M, 1, h_buf, I, g13, w->xidx, (int64_t)h.L * h.T_r, recv,
-                                  nullptr, 0, nullptr, s)))
+    if ((st = hm::ffn_gemm_groups(x, R, w13, nl, rows + nl, row0 + nl, wsel + nl, nl, 2 * I, M,
+                                  1, h_buf, I, g13, w->xidx, (int64_t)h.L * h.T_r, recv, nullptr,
+                                  0, nullptr, s)))
       return st;
     if ((st = hm::ffn_gemm_segments(h_buf, R, w2, nl, w->n_e + h.p * nl, M, I, y, M, h.E_loc,
                                     h.N_cap, s)))

@@ -30,7 +30,7 @@ class HierMoELayer:
                  n_group: int = 1, topk_group: int = 1, route_scale: float = 1.0,
                  shared_inter: int = 0, optimizer_state: bool = True, micro_batches: int = 1,
                  transport_params=None, transport_every: int = 50, fused_dispatch=None,
-                 overlap=None):
+                 overlap: bool = True):
         """``router``: "softmax" (softmax top-K; Qwen3) or "dsv3"
         (DeepSeek-V3 group-limited sigmoid gate: ``n_group`` / ``topk_group``
         / ``route_scale`` and a per-expert score bias).
@@ -108,12 +108,9 @@ class HierMoELayer:
             raise ValueError("the fused dispatch needs a direct transport (not dedup='all')")
         self._x_cur = None
         # dispatch inside the expert GEMMs (hm_experts_overlap): per-GPU dedup
-        # across GPUs with the fused dispatch, one micro-batch.  Default: on
-        # for inference layers only -- splitting GEMM1 at the local / received
-        # row boundary adds a partial tile per expert, which outweighs the
-        # hidden push once GEMM1 also stores the pre-activations
-        # (profiles/r02/overlap_*.jsonl)
-        self.overlap = (not grad) if overlap is None else bool(overlap)
+        # across GPUs with the fused dispatch, one micro-batch
+        # (profiles/r02/overlap_rotated.jsonl)
+        self.overlap = bool(overlap)
         self._cside = torch.cuda.Stream() if grad else None   # dispatch backward beside wgrads
         self.bwd_overlap = True
         self._streams = [None] + [torch.cuda.Stream() for _ in range(micro_batches - 1)]

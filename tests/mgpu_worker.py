@@ -28,7 +28,7 @@ def run_case(rank, world, G, E, K, M, T_r, dtype, dedup, seed):
     slot, w, _ = route_topk(logits[lo:hi].cuda(), K)
     ids_all, w_all, _ = OM.route_topk(logits.numpy(), K)
     assert np.array_equal(slot.cpu().numpy(), ids_all[lo:hi]), "router ids"
-    plan = OM.DispatchPlan(ids_all, G, E)
+    plan = OM.DispatchPlan(ids_all, G, E, gpus=world)
     ep = EPWorld(G, E, K, M, T_r, dtype=dtype, gpus=world, gpu_index=rank)
     ep.dispatch(x[lo:hi].cuda(), slot, w, dedup=dedup)
     torch.cuda.synchronize()
