@@ -279,7 +279,7 @@ __device__ __forceinline__ void tile_coords(const TileMap& tm, int groups, int t
 
 // Coalesced epilogue stores through a 4 KB per-warp shared-memory stage:
 // each lane writes its own row's U 16-byte units (swizzled: unit u of row r
-// at u ^ (r % U), conflict-free), then the warp stores R = 32 / U rows per
+// at u ^ key(r), conflict-free), then the warp stores R = 32 / U rows per
 // instruction with U lanes per row, so every global store instruction writes
 // whole 64 / 128-byte row segments instead of 32 rows x 16 bytes (the
 // row-per-lane TMEM layout made the epilogue the GEMM's bottleneck: with the
@@ -304,15 +304,20 @@ __device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v
                                             __nv_bfloat16* dst0, int64_t ld, int nvalid,
                                             int umax = U) {
   const uint32_t base = smem_u32(sw);   // explicit shared-window accesses (STS / LDS)
+  // swizzle key of row r: rows sharing a 128-byte bank line (8 / U of them)
+  // get the same key, consecutive lines different ones, so the 8 lanes of a
+  // 16-byte store phase hit 8 distinct 16-byte bank groups
+  constexpr int RPL = U >= 8 ? 1 : 8 / U;
 #pragma unroll
-  for (int u = 0; u < U; ++u) sts128(base + lane * (U * 16) + ((u ^ (lane % U)) << 4), v[u]);
+  for (int u = 0; u < U; ++u)
+    sts128(base + lane * (U * 16) + ((u ^ ((lane / RPL) % U)) << 4), v[u]);
   __syncwarp();
   constexpr int R = 32 / U;
   const int ur = lane % U, rr = lane / U;
 #pragma unroll
   for (int p = 0; p < U; ++p) {
     const int r = p * R + rr;
-    const int4 w = lds128(base + r * (U * 16) + ((ur ^ (r % U)) << 4));
+    const int4 w = lds128(base + r * (U * 16) + ((ur ^ ((r / RPL) % U)) << 4));
     if (r < nvalid && ur < umax) *reinterpret_cast<int4*>(dst0 + (int64_t)r * ld + ur * 8) = w;
   }
   __syncwarp();
