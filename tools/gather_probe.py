@@ -1,6 +1,6 @@
 """GEMM1 of one Qwen3 EP rank (16 experts x ~2048 rows, hidden 2048, I = 768,
 SwiGLU) with the rows copied expert-major vs gathered from the token-major x
-by index (TMA gather4).  python tools/gather_probe.py [--only copy|gather]"""
+by index (cp.async producer warps).  python tools/gather_probe.py [--only copy|gather]"""
 
 import json
 import sys

@@ -3,7 +3,7 @@
 # included), smoke, bench N = 1 / 2 / 4 (Qwen3) and N = 1 / 4 (DSv3), the
 # reference arm, and the FFN bench
 set -u
-OUT=gpurun_out/final
+OUT=${OUT:-gpurun_out/final}
 mkdir -p $OUT
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/gpu_tests.log 2>&1; echo "exit=$?" >> $OUT/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $OUT/smoke.log 2>&1; echo "exit=$?" >> $OUT/smoke.log
