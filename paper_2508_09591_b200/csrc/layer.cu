@@ -289,28 +289,59 @@ __global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ lo
         ov[k] = __shfl_xor_sync(0xffffffffu, tv[k], m);
         oi[k] = __shfl_xor_sync(0xffffffffu, ti[k], m);
       }
-      float nv[K];
-      int ni[K];
-      int a = 0, b = 0;
+      if constexpr ((K & (K - 1)) == 0) {
+        // bitonic top-K merge: the better of A[k] and B[K-1-k] is a bitonic
+        // sequence holding the top K of both lists; log2(K) half-cleaner
+        // stages sort it -- 20 compare-exchanges at K = 8 instead of the
+        // K^2 selects of the two-pointer merge, same (value desc, index asc)
+        // total order, so the same picks in the same order
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        float av = -INFINITY, bv = -INFINITY;
-        int ai = 0x7fffffff, bi = 0x7fffffff;
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-          if (q == a) { av = tv[q]; ai = ti[q]; }
-          if (q == b) { bv = ov[q]; bi = oi[q]; }
+        for (int k = 0; k < K; ++k) {
+          const float bv = ov[K - 1 - k];
+          const int bi = oi[K - 1 - k];
+          if (bv > tv[k] || (bv == tv[k] && bi < ti[k])) {
+            tv[k] = bv;
+            ti[k] = bi;
+          }
         }
-        const bool takea = av > bv || (av == bv && ai < bi);
-        nv[k] = takea ? av : bv;
-        ni[k] = takea ? ai : bi;
-        a += takea;
-        b += !takea;
-      }
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        tv[k] = nv[k];
-        ti[k] = ni[k];
+        for (int st = K / 2; st > 0; st >>= 1) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (k & st) continue;
+            const float xv = tv[k], yv = tv[k + st];
+            const int xi = ti[k], yi = ti[k + st];
+            const bool swap = yv > xv || (yv == xv && yi < xi);
+            tv[k] = swap ? yv : xv;
+            ti[k] = swap ? yi : xi;
+            tv[k + st] = swap ? xv : yv;
+            ti[k + st] = swap ? xi : yi;
+          }
+        }
+      } else {
+        float nv[K];
+        int ni[K];
+        int a = 0, b = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          float av = -INFINITY, bv = -INFINITY;
+          int ai = 0x7fffffff, bi = 0x7fffffff;
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            if (q == a) { av = tv[q]; ai = ti[q]; }
+            if (q == b) { bv = ov[q]; bi = oi[q]; }
+          }
+          const bool takea = av > bv || (av == bv && ai < bi);
+          nv[k] = takea ? av : bv;
+          ni[k] = takea ? ai : bi;
+          a += takea;
+          b += !takea;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          tv[k] = nv[k];
+          ti[k] = ni[k];
+        }
       }
     }
     const float vmax = tv[0];
