@@ -2269,6 +2269,27 @@ HM_API int hm_world_open_peers(hm_world* w, const void* handles) {
     fill_tables(w, q, reinterpret_cast<uint8_t*>(base));
   }
   HM_CUDA(cudaMemcpy(w->d, &w->h, sizeof(WorldDev), cudaMemcpyHostToDevice));
+  const WorldDev& h = w->h;
+  if (h.P > 1 && !h.U1 && h.P <= hm::kExchMaxGpus && !w->exch) {
+    // the overlapped forward's exchange descriptor (pointer tables are fixed
+    // per world) and row-group arrays, set up here so the step itself makes no
+    // allocation or synchronous copy (CUDA-graph capturable)
+    hm::ExchWork e;
+    memset(&e, 0, sizeof(e));
+    e.P = h.P;
+    e.p = h.p;
+    e.G = h.G;
+    e.K = h.K;
+    e.T_r = (int)h.T_r;
+    e.nvec = h.row_bytes / 16;
+    e.ntok = (int64_t)h.L * h.T_r;
+    e.rg_cap = h.Rg_cap;
+    e.gpos_g = w->gpos_g;
+    for (int q = 0; q < h.P; ++q) e.recv_g[q] = reinterpret_cast<int4*>(h.recv_g[q]);
+    HM_CUDA(cudaMalloc(&w->exch, sizeof(hm::ExchWork)));
+    HM_CUDA(cudaMemcpy(w->exch, &e, sizeof(e), cudaMemcpyHostToDevice));
+    HM_CUDA(cudaMalloc(&w->grp, (size_t)3 * 2 * h.L * h.E_loc * 4));
+  }
   w->peers_ready = true;
   return 0;
 }
@@ -2582,23 +2603,7 @@ HM_API int hm_experts_overlap(hm_world* w, const void* x, const void* w13, const
   const int nl = h.L * h.E_loc;
   HM_CHECK_ARG(nl <= 256, "hm_experts_overlap: at most 256 experts per GPU");
   HM_CHECK_ARG(w->n_e, "hm_experts_overlap: no plan");
-  if (!w->exch) {   // pointer tables are fixed per world: build the descriptor once
-    hm::ExchWork e;
-    memset(&e, 0, sizeof(e));
-    e.P = h.P;
-    e.p = h.p;
-    e.G = h.G;
-    e.K = h.K;
-    e.T_r = (int)h.T_r;
-    e.nvec = h.row_bytes / 16;
-    e.ntok = (int64_t)h.L * h.T_r;
-    e.rg_cap = h.Rg_cap;
-    e.gpos_g = w->gpos_g;
-    for (int q = 0; q < h.P; ++q) e.recv_g[q] = reinterpret_cast<int4*>(h.recv_g[q]);
-    HM_CUDA(cudaMalloc(&w->exch, sizeof(hm::ExchWork)));
-    HM_CUDA(cudaMemcpy(w->exch, &e, sizeof(e), cudaMemcpyHostToDevice));
-    HM_CUDA(cudaMalloc(&w->grp, (size_t)3 * 2 * nl * 4));
-  }
+  HM_CHECK_ARG(w->exch && w->grp, "hm_experts_overlap: world has no exchange descriptor");
   int32_t* row0 = w->grp;
   int32_t* rows = row0 + 2 * nl;
   int32_t* wsel = rows + 2 * nl;
