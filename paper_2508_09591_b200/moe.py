@@ -306,7 +306,7 @@ class HierMoELayer:
         (hm_dispatch_meta + hm_experts_overlap)."""
         return (self.overlap and self.gpus > 1 and self.micro_batches == 1
                 and self.dedup in (True, "gpu") and self.fused_now()
-                and 2 * self.local * self.e_loc <= 256)
+                and self.local * self.e_loc <= 256)
 
     def _rows_source(self, wd, x_rows_t: torch.Tensor):
         """(x_ptr, x_rows, idx_ptr, recv_ptr) of the experts' A rows."""

@@ -188,3 +188,52 @@ def test_multi_segment_ffn_equals_per_rank(hm):
                     + [dw13.clone(), dw2.clone()])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_ffn_explicit_groups_match_segments(hm):
+    """hm_expert_ffn_groups (explicit row start / count / weight index per
+    group, the overlapped forward's split) gives the rows the same bits as the
+    segment-layout launch, with every expert split at an arbitrary row into
+    two groups, and the groups listed out of order with empty ones."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200._lib import ptr, stream_ptr
+    from paper_2508_09591_b200.ffn import expert_ffn_multi_ptrs
+    torch.manual_seed(21)
+    S, Gs, M, I, cap = 2, 4, 512, 256, 1400
+    n = torch.randint(0, 330, (S * Gs,), dtype=torch.int32)
+    n[3] = 0
+    nr = n.cuda()
+    x = torch.randn(S * cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(S * Gs, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(S * Gs, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    outs = []
+    for explicit in (False, True):
+        h = torch.zeros(S * cap, I, dtype=torch.bfloat16, device="cuda")
+        y = torch.zeros(S * cap, M, dtype=torch.bfloat16, device="cuda")
+        g13 = torch.zeros(S * cap, 2 * I, dtype=torch.bfloat16, device="cuda")
+        if not explicit:
+            expert_ffn_multi_ptrs(x.data_ptr(), S * cap, 0, cap, S, nr.data_ptr(), Gs, w13, w2,
+                                  M, I, h, y.data_ptr(), g13.data_ptr())
+        else:
+            row0, rows, wsel = [], [], []
+            for s in range(S):
+                base = s * cap
+                for j in range(Gs):
+                    e = s * Gs + j
+                    ne = int(n[e])
+                    cut = ne // 3 if ne else 0
+                    row0 += [base + cut, base]          # second part first
+                    rows += [ne - cut, cut]
+                    wsel += [e, e]
+                    base += ne
+            g = len(rows)
+            t = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
+            r0, rc, ws = t(row0), t(rows), t(wsel)
+            _lib.call("hm_expert_ffn_groups", ptr(x), S * cap, None, None, S * cap, g, ptr(r0),
+                      ptr(rc), ptr(ws), S * Gs, ptr(w13), ptr(w2), M, I, ptr(h), ptr(y),
+                      ptr(g13), 0, stream_ptr())
+        torch.cuda.synchronize()
+        used = [(s * cap, s * cap + int(n[s * Gs:(s + 1) * Gs].sum())) for s in range(S)]
+        outs.append([torch.cat([v[a:b] for a, b in used]) for v in (h, y, g13)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
