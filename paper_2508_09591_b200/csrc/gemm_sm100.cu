@@ -42,6 +42,7 @@ constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr int kMaxGroups = 256;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
 int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid (0 = all SMs)
+int g_wgrad_pair = 1;  // hm_ffn_set_option(2, 0): single-CTA weight gradients (A/B reference)
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
   int groups;
@@ -1067,6 +1068,257 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
 }
 
 // ---------------------------------------------------------------------------
+// Weight gradients on CTA pairs (r2): out_g [m_out x N] = A_g^T B_g over group
+// g's token rows, A [tokens, m_out] and B [tokens, N] token-major -- both
+// MN-major tcgen05 operands (transpose bits), 256 x 256 output tiles, 64-token
+// k-blocks.  CTA rank r stages output rows [r*128, +128) of A's tile and
+// columns [r*128, +128) of B's (2 + 2 TMA boxes of 64 tokens x 64 features:
+// 32 KB, the forward's per-CTA operand bytes per 8.4 MFLOP instead of the
+// single-CTA kernel's 48 KB).  A group's last k-block reaches into the next
+// group's rows, so each CTA's loads land on its own gfull barrier; warp 2
+// zeroes those lines in its CTA's boxes, fences, and forwards the stage to the
+// leader's full barrier (relaxed cluster arrive, as in the gathered forward).
+// GB: B's token rows are gathered by index (warps 8-11, cp.async) -- dW13 under
+// the fused dispatch.
+constexpr uint32_t kIdesc2MN = kIdesc2 | (1u << 15) | (1u << 16);
+template <bool GB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGatherThreads : kThreads, 1)
+    k_wgrad_pair(const __grid_constant__ CUtensorMap map_a,
+                 const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages2 * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
+  uint64_t* empty = full + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* gfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + kStages2);
+  uint8_t* epi = smem + kStages2 * kStageBytes2 + 256;
+  __shared__ TileMap tm;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    int acc = 0, row = 0;
+    tm.ntile_n = args.N / BN;
+    for (int g = 0; g < args.groups; ++g) {
+      const int n = args.n_rows[g];
+      row = seg_row0(args, g, row);
+      tm.start[g] = acc;
+      tm.row0[g] = row;
+      tm.rows[g] = n;
+      tm.wsel[g] = g;
+      acc += args.m_out / BM2 * tm.ntile_n;
+      row += n;
+    }
+    tm.start[args.groups] = acc;
+    tm.total = acc;
+    for (int st = 0; st < kStages2; ++st) {
+      mbar_init(full + st, 2);                            // one forwarder per CTA
+      mbar_init(empty + st, 1);
+      mbar_init(gfull + st, 1 + (GB ? kGatherThreads : 0));
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // this CTA's boxes (A; B unless gathered) -> its own gfull
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < tm.total; t += ncl) {
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        const int arow = mt * BM2 + (int)rank * 128, bcol = nt * BN + (int)rank * 128;
+        const int kblocks = (tm.rows[g] + BK - 1) / BK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_expect_tx(gfull + stage, GB ? kHalfBytes : 2 * kHalfBytes);
+          const int tok = tm.row0[g] + kb * BK;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            tma_load_2d(sa + stage * kHalfBytes + j * 8192, &map_a, gfull + stage, arow + 64 * j,
+                        tok);
+          if (!GB) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_2d(sb + stage * kHalfBytes + j * 8192, &map_b, gfull + stage,
+                          bcol + 64 * j, tok);
+          }
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // forwarder: tail lines zeroed, then the stage -> the leader's full barrier
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cid; t < tm.total; t += ncl) {
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      const int kblocks = (tm.rows[g] + BK - 1) / BK;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(gfull + stage, phase);
+        const int valid = tm.rows[g] - kb * BK;
+        const int zend = valid >= BK ? BK : (valid + UK - 1) / UK * UK;
+        if (valid < zend) {
+          const int nlines = zend - valid;
+          for (int i = lane; i < 4 * nlines * 8; i += 32) {
+            const int box = i / (nlines * 8), rem = i % (nlines * 8);
+            const int line = valid + rem / 8, chunk = rem % 8;
+            uint8_t* base = box < 2 ? sa + stage * kHalfBytes + box * 8192
+                                    : sb + stage * kHalfBytes + (box - 2) * 8192;
+            *reinterpret_cast<int4*>(base + line * 128 + chunk * 16) = make_int4(0, 0, 0, 0);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) {
+            mbar_arrive(full + stage);
+          } else {
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(remote) : "r"(smem_u32(full + stage)), "r"(0));
+            asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+                         ::"r"(remote) : "memory");
+          }
+        }
+        __syncwarp();
+        if (++stage == kStages2) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < tm.total; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        int g, mt, nt;
+        tile_coords(tm, args.groups, t, g, mt, nt);
+        const int kblocks = (tm.rows[g] + BK - 1) / BK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_cluster(full + stage, phase);
+          tc_fence_after();
+          const int valid = tm.rows[g] - kb * BK;
+          const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
+          const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
+          const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
+          for (int k = 0; k < ksteps; ++k)
+            umma_bf16_pair<kIdesc2MN>(d, smem_desc_mn(a0 + k * UK * 128),
+                                      smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+          umma_commit_pair(empty + stage);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(tfull + acc);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    const int q = warp - 4;
+    int it = 0;
+    for (int t = cid; t < tm.total; t += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      store_tile<3>(args, tm, g, nt, mt * BM2 + (int)rank * 128 + q * 32, lane,
+                    tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, epi + q * kEpiStageBytes);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
+    }
+  } else if (GB && warp >= 8) {
+    // B gather: 64 token lines x 2 feature boxes (this CTA's 128 columns) x 8
+    // 16-byte chunks per stage; thread g owns chunk g % 8 of lines g / 8 + 16 i
+    const int g_t = threadIdx.x - kThreads;
+    const int c = g_t & 7, l0 = g_t >> 3;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cid; t < tm.total; t += ncl) {
+      int g, mt, nt;
+      tile_coords(tm, args.groups, t, g, mt, nt);
+      const int kblocks = (tm.rows[g] + BK - 1) / BK;
+      const int end = tm.row0[g] + tm.rows[g];
+      const uint8_t* col = args.g_src + (int64_t)(nt * BN + (int)rank * 128 + 8 * c) * 2;
+      auto load_tok = [&](int kb, int* tk) {
+        const int r0 = tm.row0[g] + kb * BK + l0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tk[i] = args.b_idx[r0 + 16 * i < end ? r0 + 16 * i : tm.row0[g]];
+      };
+      int nxt[4];
+      if (kblocks > 0) load_tok(0, nxt);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        int tok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tok[i] = nxt[i];
+        if (kb + 1 < kblocks) load_tok(kb + 1, nxt);
+        mbar_wait(empty + stage, phase ^ 1);
+        const uint32_t base = smem_u32(sb + stage * kHalfBytes);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int l = l0 + 16 * i;
+          const int v = tok[i];
+          const uint8_t* src = v >= 0 ? col + (int64_t)v * args.g_ld
+                                      : col + (args.g_src2 - args.g_src) + (int64_t)(~v) * args.g_ld;
+          const uint32_t dl = base + l * 128 + ((c ^ (l & 7)) << 4);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) cp_async16(dl + j * 8192, src + j * 128);
+        }
+        cp_async_arrive(gfull + stage);
+        if (++stage == kStages2) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // expert FFN backward helpers
 // group layout for the weight-gradient GEMMs: token rows of group g are
 // [row0_g, row0_g + n_g); as K columns they start at col0_g, padded to 64
@@ -1245,6 +1497,21 @@ int launch_gemm_wgrad(const void* a, const void* b, int64_t a_rows, int groups,
   int sms = kSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
+  if (g_wgrad_pair && m_out % BM2 == 0 && !out_f32 && sms >= 2) {
+    // CTA pairs, 256 x 256 tiles (the expert weight gradients)
+    const size_t smem2 = (size_t)kStages2 * kStageBytes2 + 1024 + 256 + 4 * kEpiStageBytes;
+    if (b_idx) {
+      HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem2));
+      k_wgrad_pair<true><<<sms & ~1, kThreads + kGatherThreads, smem2, s>>>(ma, mb, args);
+    } else {
+      HM_CUDA(cudaFuncSetAttribute(k_wgrad_pair<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      k_wgrad_pair<false><<<sms & ~1, kThreads, smem2, s>>>(ma, mb, args);
+    }
+    HM_LAUNCHED();
+    return 0;
+  }
   if (b_idx) {
     HM_CUDA(cudaFuncSetAttribute(k_grouped_gemm<3, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1336,14 +1603,17 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
 
 }  // namespace
 
-// FFN option (no reference counterpart): 1 = cap on the persistent GEMM grid
+// FFN options (no reference counterpart): 1 = cap on the persistent GEMM grid
 // (CTAs; 0 = one per SM, default) so concurrent exchange kernels keep SMs of
-// their own.  Options 0 and 2-4 selected measured-slower variants (transposed
-// K-major weight gradients, single-CTA forward GEMMs, CTA-pair weight
-// gradients, 4-byte SwiGLU backward) that round 2 removed; they are rejected.
+// their own; 2 = CTA-pair weight gradients (default 1; 0 = the single-CTA
+// kernel, kept as the bit-exactness reference of the pair kernel's tests).
+// Options 0, 3 and 4 selected measured-slower variants (transposed K-major
+// weight gradients, single-CTA forward GEMMs, 4-byte SwiGLU backward) that
+// round 2 removed; they are rejected.
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option == 1, "hm_ffn_set_option: unknown option %d", option);
-  g_gemm_ctas = value > 0 ? value : 0;
+  HM_CHECK_ARG(option == 1 || option == 2, "hm_ffn_set_option: unknown option %d", option);
+  if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
+  if (option == 2) g_wgrad_pair = value != 0;
   return 0;
 }
 

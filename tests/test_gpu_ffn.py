@@ -237,3 +237,53 @@ def test_ffn_explicit_groups_match_segments(hm):
         outs.append([torch.cat([v[a:b] for a, b in used]) for v in (h, y, g13)])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("gathered", [False, True])
+def test_wgrad_pair_matches_single_cta(hm, gathered):
+    """The CTA-pair weight-gradient kernel (256 x 256 tiles, both operands
+    MN-major, tail tokens zeroed by the forwarder warp) gives dW13 / dW2 bit
+    for bit equal to the single-CTA kernel -- ragged groups, an empty group,
+    sizes off the 16-token MMA step -- with and without the gathered x rows."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_gather_ptrs,
+                                           expert_ffn_backward_ptrs, expert_ffn_save_ptrs)
+    torch.manual_seed(33)
+    G, M, I = 5, 512, 256
+    n = torch.tensor([300, 0, 77, 513, 129], dtype=torch.int32)
+    rows = int(n.sum())
+    cap = rows + 64
+    nr = n.cuda()
+    x = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    h = torch.zeros(cap, I, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(cap, M, dtype=torch.bfloat16, device="cuda")
+    g13 = torch.zeros(cap, 2 * I, dtype=torch.bfloat16, device="cuda")
+    expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h, y.data_ptr(),
+                         g13.data_ptr())
+    perm = torch.randperm(cap, device="cuda").to(torch.int32)   # gathered: x_src[perm[r]] = x[r]
+    outs = []
+    for pair in (0, 1):
+        _lib.call("hm_ffn_set_option", 2, pair)
+        sc = FFNBackwardScratch(cap, G, M, I)
+        gx = torch.zeros(cap, M, dtype=torch.bfloat16, device="cuda")
+        dw13, dw2 = torch.zeros_like(w13), torch.zeros_like(w2)
+        if gathered:
+            # x_src row perm[r] holds layout row r's activations
+            x_src = torch.empty_like(x)
+            x_src[perm.long()] = x
+            expert_ffn_backward_gather_ptrs(x_src.data_ptr(), cap, perm.data_ptr(), cap,
+                                            nr.data_ptr(), G, w13, w2, gy.data_ptr(), M, I, sc,
+                                            gx.data_ptr(), dw13, dw2, g13.data_ptr())
+        else:
+            expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, gy.data_ptr(),
+                                     M, I, sc, gx.data_ptr(), dw13, dw2, g13.data_ptr())
+        torch.cuda.synchronize()
+        outs.append((dw13.clone(), dw2.clone(), gx.clone()))
+    _lib.call("hm_ffn_set_option", 2, 1)
+    assert torch.equal(outs[0][0], outs[1][0]), "dW13"
+    assert torch.equal(outs[0][1], outs[1][1]), "dW2"
+    assert torch.equal(outs[0][2], outs[1][2]), "gX"
+    assert torch.count_nonzero(outs[1][0][1]) == 0      # empty group: zero gradient
