@@ -1074,10 +1074,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
 // k-blocks.  CTA rank r stages output rows [r*128, +128) of A's tile and
 // columns [r*128, +128) of B's (2 + 2 TMA boxes of 64 tokens x 64 features:
 // 32 KB, the forward's per-CTA operand bytes per 8.4 MFLOP instead of the
-// single-CTA kernel's 48 KB).  A group's last k-block reaches into the next
-// group's rows, so each CTA's loads land on its own gfull barrier; warp 2
-// zeroes those lines in its CTA's boxes, fences, and forwards the stage to the
-// leader's full barrier (relaxed cluster arrive, as in the gathered forward).
+// single-CTA kernel's 48 KB).  Whole k-blocks load straight onto the
+// leader's full barrier (cta_group::2 TMA, as the forward); a group's last,
+// partial k-block reaches into the next group's rows, so its loads land on
+// each CTA's own gfull barrier and warp 2 zeroes those lines, fences and
+// forwards the stage to the leader (relaxed cluster arrive).  Either way the
+// leader's full barrier sees two arrivals per stage.
 // GB: B's token rows are gathered by index (warps 8-11, cp.async) -- dW13 under
 // the fused dispatch.
 constexpr uint32_t kIdesc2MN = kIdesc2 | (1u << 15) | (1u << 16);
@@ -1154,17 +1156,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGat
         const int kblocks = (tm.rows[g] + BK - 1) / BK;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_expect_tx(gfull + stage, GB ? kHalfBytes : 2 * kHalfBytes);
           const int tok = tm.row0[g] + kb * BK;
+          if (!GB && tm.rows[g] - kb * BK >= BK) {
+            // a whole k-block: both CTAs' boxes complete on the leader's full
+            // barrier (its expect_tx is one arrival, the peer's arrive the other)
+            if (leader) {
+              mbar_expect_tx(full + stage, 2 * kStageBytes2);
+            } else {
+              uint32_t remote;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                           : "=r"(remote) : "r"(smem_u32(full + stage)), "r"(0));
+              asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+                           ::"r"(remote) : "memory");
+            }
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
-            tma_load_2d(sa + stage * kHalfBytes + j * 8192, &map_a, gfull + stage, arow + 64 * j,
-                        tok);
-          if (!GB) {
+            for (int j = 0; j < 2; ++j) {
+              tma_load_2d_pair(sa + stage * kHalfBytes + j * 8192, &map_a, full + stage,
+                               arow + 64 * j, tok);
+              tma_load_2d_pair(sb + stage * kHalfBytes + j * 8192, &map_b, full + stage,
+                               bcol + 64 * j, tok);
+            }
+          } else {   // the tail block (or gathered B): own gfull, then the forwarder
+            mbar_expect_tx(gfull + stage, GB ? kHalfBytes : 2 * kHalfBytes);
 #pragma unroll
             for (int j = 0; j < 2; ++j)
-              tma_load_2d(sb + stage * kHalfBytes + j * 8192, &map_b, gfull + stage,
-                          bcol + 64 * j, tok);
+              tma_load_2d(sa + stage * kHalfBytes + j * 8192, &map_a, gfull + stage,
+                          arow + 64 * j, tok);
+            if (!GB) {
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tma_load_2d(sb + stage * kHalfBytes + j * 8192, &map_b, gfull + stage,
+                            bcol + 64 * j, tok);
+            }
           }
           if (++stage == kStages2) {
             stage = 0;
@@ -1174,16 +1197,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGat
       }
     }
   } else if (warp == 2) {
-    // forwarder: tail lines zeroed, then the stage -> the leader's full barrier
+    // forwarder: tail lines zeroed, then the stage -> the leader's full barrier.
+    // gfull[s] completes only when stage s carries a forwarded block, so its
+    // parity is tracked per stage (bit s of gph), not by ring laps
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t gph = 0;
     for (int t = cid; t < tm.total; t += ncl) {
       int g, mt, nt;
       tile_coords(tm, args.groups, t, g, mt, nt);
       const int kblocks = (tm.rows[g] + BK - 1) / BK;
       for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(gfull + stage, phase);
         const int valid = tm.rows[g] - kb * BK;
+        if (!GB && valid >= BK) {   // went straight to the leader's barrier
+          if (++stage == kStages2) stage = 0;
+          continue;
+        }
+        mbar_wait(gfull + stage, (gph >> stage) & 1u);
+        gph ^= 1u << stage;
         const int zend = valid >= BK ? BK : (valid + UK - 1) / UK * UK;
         if (valid < zend) {
           const int nlines = zend - valid;
@@ -1209,10 +1239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGat
           }
         }
         __syncwarp();
-        if (++stage == kStages2) {
-          stage = 0;
-          phase ^= 1;
-        }
+        if (++stage == kStages2) stage = 0;
       }
     }
   } else if (warp == 1) {
