@@ -1255,17 +1255,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGat
         const uint32_t d = tmem_base + acc * BN;
         int g, mt, nt;
         tile_coords(tm, args.groups, t, g, mt, nt);
-        const int kblocks = (tm.rows[g] + BK - 1) / BK;
+        const int rows = tm.rows[g];
+        const int whole = rows / BK, kblocks = (rows + BK - 1) / BK;
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait_cluster(full + stage, phase);
-          tc_fence_after();
-          const int valid = tm.rows[g] - kb * BK;
-          const int ksteps = valid >= BK ? BK / UK : (valid + UK - 1) / UK;
           const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
           const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
-          for (int k = 0; k < ksteps; ++k)
-            umma_bf16_pair<kIdesc2MN>(d, smem_desc_mn(a0 + k * UK * 128),
-                                      smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+          if (kb < whole) {   // TMA-only stage: the 4 k-steps unrolled
+            mbar_wait(full + stage, phase);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k)
+              umma_bf16_pair<kIdesc2MN>(d, smem_desc_mn(a0 + k * UK * 128),
+                                        smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+          } else {   // the forwarded tail block (zeroed lines: cluster acquire)
+            mbar_wait_cluster(full + stage, phase);
+            tc_fence_after();
+            const int ksteps = (rows - kb * BK + UK - 1) / UK;
+            for (int k = 0; k < ksteps; ++k)
+              umma_bf16_pair<kIdesc2MN>(d, smem_desc_mn(a0 + k * UK * 128),
+                                        smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+          }
           umma_commit_pair(empty + stage);
           if (++stage == kStages2) {
             stage = 0;
