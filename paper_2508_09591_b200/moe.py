@@ -48,10 +48,16 @@ class HierMoELayer:
         LevelParams or params-JSON path for the runtime [P, L] hierarchy,
         default the packaged B200 fits); the choices are logged in
         ``transport_log``.
-        ``fused_dispatch`` (default: on with one GPU): the dispatch emits
-        expert-major row indices instead of row copies and GEMM1 gathers its
-        rows from x by index (the backward's dW13 likewise); outputs
-        and gradients are bit-identical to the copying dispatch."""
+        ``fused_dispatch`` (default: on unless ``dedup="all"``): the dispatch
+        emits expert-major row indices instead of row copies and GEMM1 gathers
+        its rows from x (or, across GPUs, from the receive buffer) by index
+        (the backward's dW13 likewise); outputs and gradients are
+        bit-identical to the copying dispatch.
+        ``overlap`` (default on): with per-GPU dedup across GPUs the token
+        rows cross NVLink from an idle warp of the local rows' GEMM1
+        (hm_experts_overlap), and in the backward the dispatch backward runs
+        on a side stream beside the weight-gradient GEMMs (``bwd_overlap``);
+        bit-identical to the serial path."""
         if inter % 128 or hidden % 256 or shared_inter % 128:
             raise ValueError("hidden must be a multiple of 256 and inter / shared_inter of 128")
         if grad and (inter % 256 or shared_inter % 256):
