@@ -316,8 +316,11 @@ int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* i
 /* parts: 1 = data gradients (dH, SwiGLU backward, gX), 2 = weight gradients
  * (dW2, dW13 from part 1's scratch), 3 = both -- a caller can run the
  * dispatch backward of gX beside the weight-gradient GEMMs. */
-/* FFN option (no reference counterpart): 1 = cap on the persistent GEMM grid
- * in CTAs (0 = one per SM), so a concurrent exchange keeps SMs of its own. */
+/* FFN options (no reference counterpart): 1 = cap on the persistent GEMM grid
+ * in CTAs (0 = one per SM), so a concurrent exchange keeps SMs of its own;
+ * 2 = CTA-pair weight gradients (default 1; 0 = single-CTA kernel);
+ * 5 = 256 x 512 pair tiles: 0 never, 1 (default) for the long-K (>= 4096)
+ * data-gradient GEMMs on the weights as stored, 2 wherever N % 512 == 0. */
 int hm_ffn_set_option(int32_t option, int32_t value);
 
 /* ---------------- expert migration (K11) ------------------------------------

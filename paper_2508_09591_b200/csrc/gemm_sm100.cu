@@ -43,6 +43,10 @@ constexpr int kMaxGroups = 256;
 constexpr uint32_t kTmemCols = 2 * BN;      // double-buffered accumulator
 int g_gemm_ctas = 0;   // hm_ffn_set_option(1, n): cap the persistent GEMM grid (0 = all SMs)
 int g_wgrad_pair = 1;  // hm_ffn_set_option(2, 0): single-CTA weight gradients (A/B reference)
+// hm_ffn_set_option(5, v): 256 x 512 pair tiles -- 0 never, 1 (default) for
+// the long-K data-gradient GEMMs with B read as stored (K >= 4096: measured
+// 11-16 % faster there, slower elsewhere), 2 wherever N % 512 == 0
+int g_wide_tiles = 1;
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
   int groups;
@@ -324,11 +328,21 @@ __device__ __forceinline__ void stage_store(uint8_t* sw, int lane, const int4* v
   __syncwarp();
 }
 
+// silu(g) = g * rcp(1 + exp(-g)) on the MUFU (the IEEE division's fix-up
+// sequence made the SwiGLU epilogue instruction-bound); g << 0: rcp(inf) = 0
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Epilogue of one accumulator tile for the 32 rows of TMEM lane quarter q:
 // TMEM -> fp32 registers -> (SwiGLU / accumulate) -> bf16 rows.  r0 = the
 // warp's first row within group g (weight-gradient modes: output row); sw =
 // the warp's shared-memory store stage.
-template <int kMode>
+// kHalfStage: 2 KB store stages (the NA = 2 pair kernel's eight epilogue
+// warps): bf16 rows go out as 64-byte instead of 128-byte row segments
+template <int kMode, bool kHalfStage = false>
 __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& tm, int g, int nt,
                                            int r0, int lane, uint32_t tbase, uint8_t* sw) {
   int nvalid = kMode >= 2 ? 32 : tm.rows[g] - r0;
@@ -383,8 +397,8 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float g0 = gv[2 * i], g1 = gv[2 * i + 1];
-        float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
-        float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
+        float h0 = g0 * rcp_approx(1.f + __expf(-g0)) * uv[2 * i];
+        float h1 = g1 * rcp_approx(1.f + __expf(-g1)) * uv[2 * i + 1];
         hv[i] = __floats2bfloat162_rn(h0, h1);
       }
       stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv),
@@ -434,8 +448,14 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
         for (int i = 0; i < 16; ++i)
           hv[16 * half + i] = zero ? __floats2bfloat162_rn(0.f, 0.f)
                                    : __floats2bfloat162_rn(v2[half][2 * i], v2[half][2 * i + 1]);
-      stage_store<8>(sw, lane, reinterpret_cast<const int4*>(hv),
-                     args.out + row_base * args.ld_out + nt * BN + c2, args.ld_out, nvalid);
+      __nv_bfloat16* dst = args.out + row_base * args.ld_out + nt * BN + c2;
+      if (kHalfStage) {
+        stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv), dst, args.ld_out, nvalid);
+        stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv) + 4, dst + 32, args.ld_out,
+                       nvalid);
+      } else {
+        stage_store<8>(sw, lane, reinterpret_cast<const int4*>(hv), dst, args.ld_out, nvalid);
+      }
     }
   }
   (void)valid;
@@ -835,22 +855,45 @@ __device__ __noinline__ void exch_push(const hm::ExchWork& e, const int4* x, int
 // BMN: B read MN-major straight from [groups][K][N] weights (two 64 x 64 TMA
 // boxes per CTA and k-block, the tcgen05 transpose-B bit) -- the data-gradient
 // GEMMs then need no transposed weight copies
-template <int kMode, bool GA = false, bool BMN = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGatherThreads : kThreads, 1)
+// NA = 2 (r2, "wide" tiles): 256 x 512 output tiles, two N = 256 MMAs per
+// k-step sharing the A half (per-CTA operand bytes per flop -25 %: 48 KB per
+// 16.8 MFLOP instead of 32 KB per 8.4) -- the TMEM then holds one tile's two
+// accumulators (all 512 columns), so the epilogue releases them one at a
+// time (tempty[0] / tempty[1]) and the MMA warp runs the next tile's first
+// k-blocks on accumulator 0 (holding their stages) until accumulator 1 is
+// drained.  4 ring stages of 48 KB.  Same k order per output element as
+// NA = 1: bit-identical results.
+constexpr int kEpi2Threads = 128;   // NA = 2: a second epilogue warpgroup (accumulator 1)
+template <int NA>
+struct PairCfg {
+  static constexpr int kStages = NA == 1 ? kStages2 : 4;
+  static constexpr uint32_t kBBytes = NA * kHalfBytes;        // this CTA's B halves
+  static constexpr uint32_t kStage = kHalfBytes + kBBytes;    // A half + B halves
+  static constexpr int kEpiStage = kEpiStageBytes / NA;       // per epilogue warp
+  static constexpr size_t smem() {
+    return (size_t)kStages * kStage + 1024 + 256 + 4 * NA * kEpiStage;
+  }
+};
+template <int kMode, bool GA = false, bool BMN = false, int NA = 1>
+__global__ void __cluster_dims__(2, 1, 1)
+    __launch_bounds__(kThreads + (GA ? kGatherThreads : 0) + (NA == 2 ? kEpi2Threads : 0), 1)
     k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+  using C = PairCfg<NA>;
+  constexpr int ST = C::kStages;
+  constexpr int kEpi2Warp = (kThreads + (GA ? kGatherThreads : 0)) / 32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = smem + kStages2 * kHalfBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStageBytes2);
-  uint64_t* empty = full + kStages2;
-  uint64_t* tfull = empty + kStages2;
+  uint8_t* sb = smem + ST * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * C::kStage);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
   uint64_t* gfull = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + kStages2);
-  uint8_t* epi = smem + kStages2 * kStageBytes2 + 256;   // epilogue store stages
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + ST);
+  uint8_t* epi = smem + ST * C::kStage + 256;   // epilogue store stages
   __shared__ TileMap tm;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -859,7 +902,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   if (threadIdx.x == 0) {
     int acc = 0, row = 0;
-    tm.ntile_n = args.N / BN;
+    tm.ntile_n = args.N / (BN * NA);
     for (int g = 0; g < args.groups; ++g) {
       int n = args.n_rows[g];
       if (kMode == 2) n = (n + BK - 1) / BK * BK;   // K padded to the k-block
@@ -873,7 +916,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
     }
     tm.start[args.groups] = acc;
     tm.total = acc;
-    for (int s = 0; s < kStages2; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(full + s, GA ? 3 : 1);
       mbar_init(empty + s, 1);
       mbar_init(gfull + s, kGatherThreads);
@@ -910,24 +953,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
         // mode 2 (weight gradient from transposed operands): A [m_out][K_all],
         // B [N][K_all], group g's reduction range = its padded token columns
         const int arow = (kMode == 2 ? 0 : tm.row0[g]) + mt * BM2 + (int)rank * 128;
-        const int brow = (kMode == 2 ? 0 : tm.wsel[g] * args.N) + nt * BN + (int)rank * 128;
+        const int brow = (kMode == 2 ? 0 : tm.wsel[g] * args.N) + nt * BN * NA + (int)rank * 128;
         const int k0 = kMode == 2 ? tm.row0[g] : 0;
         const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          if (leader) mbar_expect_tx(full + stage, GA ? 2 * kHalfBytes : 2 * kStageBytes2);
+          if (leader) mbar_expect_tx(full + stage, GA ? 2 * C::kBBytes : 2 * C::kStage);
           if (!GA)
             tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
-          if (BMN) {   // B [g][K][N]: rows g * K + k, 64-column chunks of this CTA's 128
-            const int bcol = nt * BN + (int)rank * 128;
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-              tma_load_2d_pair(sb + stage * kHalfBytes + j * 8192, &map_b, full + stage,
-                               bcol + 64 * j, tm.wsel[g] * args.K + kb * BK);
-          } else {
-            tma_load_2d_pair(sb + stage * kHalfBytes, &map_b, full + stage, k0 + kb * BK, brow);
+          for (int a = 0; a < NA; ++a) {
+            uint8_t* sbs = sb + stage * C::kBBytes + a * kHalfBytes;
+            if (BMN) {   // B [g][K][N]: rows g * K + k, 64-column chunks of this CTA's 128
+              const int bcol = nt * BN * NA + a * BN + (int)rank * 128;
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tma_load_2d_pair(sbs + j * 8192, &map_b, full + stage, bcol + 64 * j,
+                                 tm.wsel[g] * args.K + kb * BK);
+            } else {
+              tma_load_2d_pair(sbs, &map_b, full + stage, k0 + kb * BK, brow + a * BN);
+            }
           }
-          if (++stage == kStages2) {
+          if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
@@ -939,60 +986,122 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = cid; t < tm.total; t += ncl, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(tempty + acc, acc_phase ^ 1);
+      // one k-block's MMAs into accumulator a (TMEM columns a * 256)
+      auto mma_kb = [&](uint32_t d, int st, int kb, int a) {
+        const uint32_t a0 = smem_u32(sa + st * kHalfBytes);
+        const uint32_t b0 = smem_u32(sb + st * C::kBBytes + a * kHalfBytes);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+          if (BMN)
+            umma_bf16_pair<kIdesc2BMN>(d, smem_desc(a0 + k * UK * 2),
+                                       smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+          else
+            umma_bf16_pair(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
+                           (kb | k) ? 1u : 0u);
+        }
+      };
+      auto wait_full = [&](int st, uint32_t ph) {
+        if (GA)
+          mbar_wait_cluster(full + st, ph);
+        else
+          mbar_wait(full + st, ph);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+      };
+      for (int t = cid; t < tm.total; t += ncl, ++it) {
         int kblocks = kblocks_fixed;
         if (kMode == 2) {
           int g, mt, nt;
           tile_coords(tm, args.groups, t, g, mt, nt);
           kblocks = tm.rows[g] / BK;
         }
-        for (int kb = 0; kb < kblocks; ++kb) {
-          if (GA)
-            mbar_wait_cluster(full + stage, phase);
-          else
-            mbar_wait(full + stage, phase);
+        if (NA == 1) {
+          const int acc = it & 1;
+          const uint32_t acc_phase = (it >> 1) & 1;
+          mbar_wait(tempty + acc, acc_phase ^ 1);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
-          const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
-#pragma unroll
-          for (int k = 0; k < BK / UK; ++k) {
-            if (BMN)
-              umma_bf16_pair<kIdesc2BMN>(d, smem_desc(a0 + k * UK * 2),
-                                         smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
-            else
-              umma_bf16_pair(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
-                             (kb | k) ? 1u : 0u);
+          const uint32_t d = tmem_base + acc * BN;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            wait_full(stage, phase);
+            mma_kb(d, stage, kb, 0);
+            umma_commit_pair(empty + stage);
+            if (++stage == ST) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          umma_commit_pair(empty + stage);
-          if (++stage == kStages2) {
-            stage = 0;
-            phase ^= 1;
+          umma_commit_pair(tfull + acc);
+        } else {
+          // single TMEM buffer: accumulator 0 as soon as the epilogue released
+          // it; accumulator 1's MMAs of the held stages once it is released too
+          const uint32_t tph = (it & 1) ^ 1;
+          mbar_wait(tempty + 0, tph);
+          tc_fence_after();
+          bool free1 = false;
+          int held = 0, hstage = stage, hkb = 0;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            wait_full(stage, phase);
+            mma_kb(tmem_base, stage, kb, 0);
+            if (!free1) {
+              if (held + 1 >= ST) {
+                mbar_wait(tempty + 1, tph);
+                free1 = true;
+              } else {
+                free1 = mbar_try(smem_u32(tempty + 1), tph) != 0;
+              }
+              if (free1) tc_fence_after();
+            }
+            if (free1) {
+              for (; held > 0; --held) {   // catch up on the held stages
+                mma_kb(tmem_base + BN, hstage, hkb, 1);
+                umma_commit_pair(empty + hstage);
+                if (++hstage == ST) hstage = 0;
+                ++hkb;
+              }
+              mma_kb(tmem_base + BN, stage, kb, 1);
+              umma_commit_pair(empty + stage);
+            } else {
+              if (held++ == 0) {
+                hstage = stage;
+                hkb = kb;
+              }
+            }
+            if (++stage == ST) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          if (!free1) {   // fewer k-blocks than the epilogue took to drain
+            mbar_wait(tempty + 1, tph);
+            tc_fence_after();
+            for (; held > 0; --held) {
+              mma_kb(tmem_base + BN, hstage, hkb, 1);
+              umma_commit_pair(empty + hstage);
+              if (++hstage == ST) hstage = 0;
+              ++hkb;
+            }
+          }
+          umma_commit_pair(tfull + 0);
         }
-        umma_commit_pair(tfull + acc);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    const int q = warp - 4;
+  } else if ((warp >= 4 && warp < 8) || (NA == 2 && warp >= kEpi2Warp)) {
+    // NA = 2: warps 4-7 drain accumulator 0, the second warpgroup accumulator 1
+    const int q = warp & 3;
+    const int a = (NA == 2 && warp >= kEpi2Warp) ? 1 : 0;
     int it = 0;
     for (int t = cid; t < tm.total; t += ncl, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = NA == 1 ? it & 1 : 0;
+      const uint32_t acc_phase = NA == 1 ? (it >> 1) & 1 : it & 1;
       int g, mt, nt;
       tile_coords(tm, args.groups, t, g, mt, nt);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      store_tile<kMode>(args, tm, g, nt, mt * BM2 + (int)rank * 128 + q * 32, lane,
-                        tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN,
-                        epi + q * kEpiStageBytes);
+      store_tile<kMode, NA == 2>(args, tm, g, nt * NA + a, mt * BM2 + (int)rank * 128 + q * 32,
+                                 lane, tmem_base + ((uint32_t)(q * 32) << 16) + (acc + a) * BN,
+                                 epi + (a * 4 + q) * C::kEpiStage);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty + acc, 0);
+      if (lane == 0) mbar_arrive_cluster(tempty + acc + a, 0);
     }
   } else if (warp == 3 && args.exch_kind == 1) {   // dispatch rows beside the tiles
     exch_push(*args.exch, args.exch_x, lane);
@@ -1016,14 +1125,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
             asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
                          ::"r"(remote) : "memory");
           }
-          if (++stage == kStages2) {
+          if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
     }
-  } else if (GA && warp >= 8) {
+  } else if (GA && warp >= 8 && warp < 12) {
     // A gather: this CTA's 128 rows x 8 16-byte chunks per stage; thread g owns
     // chunk g % 8 of rows g / 8 + 16 i (row pointers loaded once per tile)
     const int g_t = threadIdx.x - kThreads;
@@ -1051,7 +1160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GA ? kThreads + kGat
           cp_async16(base + r * 128 + ((c ^ (r & 7)) << 4), src[i] + kb * (BK * 2));
         }
         cp_async_arrive(gfull + stage);
-        if (++stage == kStages2) {
+        if (++stage == ST) {
           stage = 0;
           phase ^= 1;
         }
@@ -1623,18 +1732,33 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   if (g_gemm_ctas > 0 && g_gemm_ctas < sms) sms = g_gemm_ctas;
   if (ctas > 0 && ctas < sms) sms = ctas;
   HM_CHECK_ARG(sms >= 2, "grouped gemm: at least one CTA pair");
-  const size_t smem2 = (size_t)kStages2 * kStageBytes2 + 1024 + 256 + 4 * kEpiStageBytes;
   const int grid = sms & ~1;
-  auto run = [&](auto kern, int threads) -> int {
+  auto run = [&](auto kern, int threads, size_t smem2) -> int {
     HM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     kern<<<grid, threads, smem2, s>>>(ma, mb, args);
     return launch_status();
   };
   const int thr_g = kThreads + kGatherThreads;   // + the A-gather warps
-  if (b_mn) return run(k_grouped_gemm_pair<0, false, true>, kThreads);
-  if (a_idx) return swiglu ? run(k_grouped_gemm_pair<1, true>, thr_g)
-                           : run(k_grouped_gemm_pair<0, true>, thr_g);
-  return swiglu ? run(k_grouped_gemm_pair<1>, kThreads) : run(k_grouped_gemm_pair<0>, kThreads);
+  // 256 x 512 tiles (hm_ffn_set_option(5, .)): the data-gradient GEMMs over a
+  // long K (DeepSeek-V3's dH / gX: -11..-16 %); the forward GEMMs and short-K
+  // ones measured faster on double-buffered 256 x 256 tiles, whose epilogue
+  // hides entirely behind the next tile's k-loop
+  const bool wide = g_wide_tiles == 2 || (g_wide_tiles == 1 && b_mn && K >= 4096);
+  if (wide && N % (2 * BN) == 0 && !out_f32) {
+    const size_t sm = PairCfg<2>::smem();
+    const int e2 = kEpi2Threads;   // + the accumulator-1 epilogue warpgroup
+    if (b_mn) return run(k_grouped_gemm_pair<0, false, true, 2>, kThreads + e2, sm);
+    if (a_idx) return swiglu ? run(k_grouped_gemm_pair<1, true, false, 2>, thr_g + e2, sm)
+                             : run(k_grouped_gemm_pair<0, true, false, 2>, thr_g + e2, sm);
+    return swiglu ? run(k_grouped_gemm_pair<1, false, false, 2>, kThreads + e2, sm)
+                  : run(k_grouped_gemm_pair<0, false, false, 2>, kThreads + e2, sm);
+  }
+  const size_t sm = PairCfg<1>::smem();
+  if (b_mn) return run(k_grouped_gemm_pair<0, false, true>, kThreads, sm);
+  if (a_idx) return swiglu ? run(k_grouped_gemm_pair<1, true>, thr_g, sm)
+                           : run(k_grouped_gemm_pair<0, true>, thr_g, sm);
+  return swiglu ? run(k_grouped_gemm_pair<1>, kThreads, sm)
+                : run(k_grouped_gemm_pair<0>, kThreads, sm);
 }
 
 }  // namespace
@@ -1642,14 +1766,19 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
 // FFN options (no reference counterpart): 1 = cap on the persistent GEMM grid
 // (CTAs; 0 = one per SM, default) so concurrent exchange kernels keep SMs of
 // their own; 2 = CTA-pair weight gradients (default 1; 0 = the single-CTA
-// kernel, kept as the bit-exactness reference of the pair kernel's tests).
+// kernel, kept as the bit-exactness reference of the pair kernel's tests);
+// 5 = 256 x 512 pair tiles: 0 never (the wide kernel's bit-exactness
+// reference), 1 (default) for the long-K MN-major data gradients, 2 wherever
+// N % 512 == 0.
 // Options 0, 3 and 4 selected measured-slower variants (transposed K-major
 // weight gradients, single-CTA forward GEMMs, 4-byte SwiGLU backward) that
 // round 2 removed; they are rejected.
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option == 1 || option == 2, "hm_ffn_set_option: unknown option %d", option);
+  HM_CHECK_ARG(option == 1 || option == 2 || option == 5, "hm_ffn_set_option: unknown option %d",
+               option);
   if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
   if (option == 2) g_wgrad_pair = value != 0;
+  if (option == 5) g_wide_tiles = value < 0 ? 0 : (value > 2 ? 2 : value);
   return 0;
 }
 

@@ -287,3 +287,70 @@ def test_wgrad_pair_matches_single_cta(hm, gathered):
     assert torch.equal(outs[0][1], outs[1][1]), "dW2"
     assert torch.equal(outs[0][2], outs[1][2]), "gX"
     assert torch.count_nonzero(outs[1][0][1]) == 0      # empty group: zero gradient
+
+
+@pytest.mark.parametrize("shape", [(5, 512, 256, [300, 0, 77, 513, 129]),
+                                   (3, 512, 128, [1, 260, 511]),
+                                   (4, 1024, 512, [700, 33, 0, 1030])])
+def test_wide_tiles_match_256_tiles(hm, shape):
+    """256 x 512 pair tiles (two accumulators sharing the A half, the epilogue
+    releasing them one at a time, the next tile's first k-blocks run on
+    accumulator 0 while accumulator 1 drains) give the forward (plain,
+    SwiGLU with saved pre-activations, gathered A rows) and the backward bit
+    for bit equal to 256 x 256 tiles -- ragged and empty groups, a
+    single-k-block reduction (hidden 64), partial row tiles."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
+                                           expert_ffn_gather_ptrs, expert_ffn_save_ptrs)
+    G, M, I, sizes = shape
+    torch.manual_seed(44)
+    n = torch.tensor(sizes, dtype=torch.int32)
+    rows = int(n.sum())
+    cap = rows + 64
+    nr = n.cuda()
+    x = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    perm = torch.randperm(cap, device="cuda").to(torch.int32)
+    x_src = torch.empty_like(x)
+    x_src[perm.long()] = x
+    outs = []
+    try:
+        for wide in (0, 2):   # 256 x 256 only / 256 x 512 wherever N allows
+            _lib.call("hm_ffn_set_option", 5, wide)
+            h = torch.zeros(cap, I, dtype=torch.bfloat16, device="cuda")
+            y = torch.zeros(cap, M, dtype=torch.bfloat16, device="cuda")
+            g13 = torch.zeros(cap, 2 * I, dtype=torch.bfloat16, device="cuda")
+            expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h,
+                                 y.data_ptr(), g13.data_ptr())
+            hg = torch.zeros_like(h)
+            yg = torch.zeros_like(y)
+            expert_ffn_gather_ptrs(x_src.data_ptr(), cap, perm.data_ptr(), cap, nr.data_ptr(), G,
+                                   w13, w2, M, I, hg, yg.data_ptr())
+            gx = torch.zeros(cap, M, dtype=torch.bfloat16, device="cuda")
+            dw13, dw2 = torch.zeros_like(w13), torch.zeros_like(w2)
+            if I % 256 == 0:   # the backward's dH GEMM needs N = I in 256-column tiles
+                sc = FFNBackwardScratch(cap, G, M, I)
+                expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2,
+                                         gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13, dw2,
+                                         g13.data_ptr())
+            torch.cuda.synchronize()
+            outs.append([t[:rows].clone() for t in (h, y, g13, hg, yg, gx)] +
+                        [dw13.clone(), dw2.clone()])
+    finally:
+        _lib.call("hm_ffn_set_option", 5, 1)
+    names = ["h", "y", "g13", "h (gathered)", "y (gathered)", "gX", "dW13", "dW2"]
+    for name, a, b in zip(names, outs[0], outs[1]):
+        assert torch.equal(a, b), name
+    # and the wide forward is right, not just self-consistent
+    ref_rows = []
+    r0 = 0
+    for g in range(G):
+        xs = x[r0:r0 + sizes[g]].float()
+        a13 = xs @ w13[g].float().t()
+        blk = a13.view(-1, I // 128, 2, 128)
+        hh = torch.nn.functional.silu(blk[:, :, 0]) * blk[:, :, 1]
+        ref_rows.append(hh.reshape(-1, I))
+        r0 += sizes[g]
+    torch.testing.assert_close(outs[1][0].float(), torch.cat(ref_rows), rtol=2e-2, atol=2e-2)
