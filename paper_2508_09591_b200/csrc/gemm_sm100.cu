@@ -397,8 +397,13 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float g0 = gv[2 * i], g1 = gv[2 * i + 1];
+#ifdef HM_IEEE_SILU   // A/B reference build (tools/variant_build.sh)
+        float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
+        float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
+#else
         float h0 = g0 * rcp_approx(1.f + __expf(-g0)) * uv[2 * i];
         float h1 = g1 * rcp_approx(1.f + __expf(-g1)) * uv[2 * i + 1];
+#endif
         hv[i] = __floats2bfloat162_rn(h0, h1);
       }
       stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv),
@@ -1823,13 +1828,90 @@ HM_API int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, con
                      (cudaStream_t)stream, nullptr, nullptr, 0, out, n_valid);
 }
 
+// Split-K for the router weight gradient: its output is only m_out x N (8
+// tiles of 128 x 256 for 128 experts x hidden 2048), so one group would keep
+// 8 of 148 SMs busy over all T tokens.  The token range is cut into S chunks
+// (device-side sizes from the device row count), each chunk an mode-3 group
+// with its own fp32 partial [m_out][N], and the partials are summed (+ the
+// accumulated gradient) by k_sum_splits.
+namespace {
+__global__ void k_split_rows(const int32_t* __restrict__ total, int S, int chunk,
+                             int32_t* __restrict__ n_rows) {
+  const int s = threadIdx.x;
+  if (s < S) {
+    const int r = *total - s * chunk;
+    n_rows[s] = r < 0 ? 0 : (r > chunk ? chunk : r);
+  }
+}
+__global__ void __launch_bounds__(256) k_sum_splits(const float4* __restrict__ part, int S,
+                                                    int m_out, int N, float* __restrict__ out,
+                                                    int64_t ld_out, int accumulate) {
+  const int n4 = N / 4;
+  const int64_t total = (int64_t)m_out * n4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / n4, c = (i % n4) * 4;
+    float4* o = reinterpret_cast<float4*>(out + r * ld_out + c);
+    float4 acc = accumulate ? *o : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sp = 0; sp < S; ++sp) {
+      const float4 v = part[sp * total + i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    *o = acc;
+  }
+}
+struct SplitScratch {
+  float* part = nullptr;
+  size_t bytes = 0;
+  int32_t* n_rows = nullptr;
+};
+SplitScratch g_split[64];   // per device
+}  // namespace
+
 HM_API int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
                         int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
                         void* stream) {
   HM_RANGE("hm_wgrad_f32");
   HM_CHECK_ARG(a && b && out && rows_dev, "hm_wgrad_f32: null argument");
-  return launch_gemm_wgrad(a, b, rows > 0 ? rows : 1, 1, rows_dev, m_out, N, nullptr, ld_out,
-                           (cudaStream_t)stream, accumulate, nullptr, 0, out);
+  HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0 && ld_out % 4 == 0,
+               "hm_wgrad_f32: m_out %% 128 == 0, N %% 256 == 0, 16-byte output rows");
+  cudaStream_t s = (cudaStream_t)stream;
+  rows = rows > 0 ? rows : 1;
+  int dev = 0, sms = kSMs;
+  HM_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (m_out / BM) * (N / BN);
+  int S = sms / tiles;
+  S = S > 64 ? 64 : S;
+  if ((int64_t)S * 4 * BK > rows) S = (int)(rows / (4 * BK));   // >= 4 k-blocks per chunk
+  if (S < 2 || dev >= 64)
+    return launch_gemm_wgrad(a, b, rows, 1, rows_dev, m_out, N, nullptr, ld_out, s, accumulate,
+                             nullptr, 0, out);
+  const int chunk = (int)((rows + S - 1) / S + BK - 1) / BK * BK;
+  SplitScratch& sc = g_split[dev];
+  const size_t need = (size_t)S * m_out * N * 4;
+  if (sc.bytes < need) {
+    if (sc.part) cudaFree(sc.part);
+    sc.part = nullptr;
+    sc.bytes = 0;
+    HM_CUDA(cudaMalloc(&sc.part, need));
+    sc.bytes = need;
+  }
+  if (!sc.n_rows) HM_CUDA(cudaMalloc(&sc.n_rows, 64 * sizeof(int32_t)));
+  k_split_rows<<<1, 64, 0, s>>>(rows_dev, S, chunk, sc.n_rows);
+  HM_LAUNCHED();
+  int st = launch_gemm_wgrad(a, b, rows, S, sc.n_rows, m_out, N, nullptr, N, s, 0, nullptr, 0,
+                             sc.part);
+  if (st) return st;
+  const int64_t n4 = (int64_t)m_out * N / 4;
+  const int grid = (int)((n4 + 255) / 256 < 4 * sms ? (n4 + 255) / 256 : 4 * sms);
+  k_sum_splits<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(sc.part), S, m_out, N, out,
+                                    ld_out, accumulate);
+  HM_LAUNCHED();
+  return 0;
 }
 
 // Expert SwiGLU FFN on expert-major rows: H = silu(X W1^T) * (X W3^T),
@@ -1889,6 +1971,9 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
                                       nullptr, s, nullptr, nullptr, 0, nullptr, 0, sg, seg_rows)))
     return st;
   // dH = gY W2: W2 [g][M][I] as stored = B [K = M][N = I], read MN-major
+  // (the SwiGLU backward stays a separate HBM-rate kernel: folded into this
+  // GEMM's epilogue it made the epilogue the bottleneck, Qwen3 rank backward
+  // 0.543 -> 0.590 ms; profiles/r02/negative/swiglu_bwd_in_dh_epilogue_ab.jsonl)
   if ((st = launch_gemm(gy, a_rows, w2, groups, n_rows, I, M, 0, dh, I, nullptr, s, nullptr,
                         nullptr, 0, nullptr, 0, sg, seg_rows, nullptr, true)))
     return st;

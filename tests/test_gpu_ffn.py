@@ -354,3 +354,4 @@ def test_wide_tiles_match_256_tiles(hm, shape):
         ref_rows.append(hh.reshape(-1, I))
         r0 += sizes[g]
     torch.testing.assert_close(outs[1][0].float(), torch.cat(ref_rows), rtol=2e-2, atol=2e-2)
+

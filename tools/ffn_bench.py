@@ -60,8 +60,8 @@ def run(name, G, M, I, rows_per_group, steps=10):
 
 if __name__ == "__main__":
     import os
-    if "HM_WIDE" in os.environ:   # hm_ffn_set_option(5, .): 256 x 512 tiles on / off
-        from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200 import _lib
+    if "HM_WIDE" in os.environ:   # hm_ffn_set_option(5, .): 256 x 512 tiles
         _lib.call("hm_ffn_set_option", 5, int(os.environ["HM_WIDE"]))
     run("qwen3_rank", 16, 2048, 768, 2048)
     run("dsv3_rank", 32, 7168, 2048, 1024)
