@@ -15,4 +15,10 @@ CUDA_VISIBLE_DEVICES=0 timeout 1200 python bench.py --config dsv3 --steps 20 --w
 timeout 1200 $TR --nproc-per-node 4 --master-port 29793 bench.py --gpus 4 --config dsv3 --steps 20 --warmup 3 > $OUT/bench_dsv3_n4.json 2> $OUT/bench_dsv3_n4.err; echo "exit=$?" >> $OUT/bench_dsv3_n4.err
 CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --impl reference > $OUT/ref_n1.json 2> $OUT/ref_n1.err; echo "exit=$?" >> $OUT/ref_n1.err
 CUDA_VISIBLE_DEVICES=0 timeout 600 python tools/ffn_bench.py > $OUT/ffn.jsonl 2>&1
+# launch list of the N = 1 bench command (short run; its numbers are not bench values)
+CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $OUT/bench_n1_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
+  --no-e2e --no-planner --no-hd2 > $OUT/bench_n1_ncu.log 2>&1
+CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $OUT/layer_qwen3_launches.csv python tools/profile_layer.py --steps 3 > $OUT/layer_ncu.log 2>&1
 echo done
