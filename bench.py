@@ -49,6 +49,10 @@ CONFIGS = {
 }
 INTER = {"qwen3": 768, "dsv3": 2048, "configA": 512, "qwen3_ep4": 768}
 NVLINK_GBS = 770.0   # B200_PROFILING.md: measured peer copy, per direction per GPU
+# all-to-all pushes of 4 KB rows driven by SMs (16-B peer stores or TMA bulk
+# stores, every GPU to every other at once): the ceiling of an SM-driven
+# exchange on these boxes (tools/link_probe.cu, profiles/r01_link_probe.jsonl)
+SM_PUSH_GBS = 678.0
 SEGMENTS = ["plan", "notify", "pack", "barrier1", "expand", "reduce", "barrier2", "gather"]
 
 
@@ -975,7 +979,12 @@ def main():
                 "achieved": (link["pack"] + link[ret_key]) / (link_dedup * 1e-3) / 1e9,
                 "peak": NVLINK_GBS, "unit": "GB/s",
                 "frac": (link["pack"] + link[ret_key]) / (link_dedup * 1e-3) / 1e9 / NVLINK_GBS,
-                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"},
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction",
+                "sm_push_ceiling": SM_PUSH_GBS,
+                "frac_of_sm_push_ceiling":
+                    (link["pack"] + link[ret_key]) / (link_dedup * 1e-3) / 1e9 / SM_PUSH_GBS,
+                "sm_push_source": "tools/link_probe.cu all-to-all SM pushes (16-B stores / TMA "
+                                  "bulk), profiles/r01_link_probe.jsonl"},
             "cpu_baseline": None if cpu is None else
             {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": e2e,
