@@ -320,7 +320,9 @@ int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* i
  * in CTAs (0 = one per SM), so a concurrent exchange keeps SMs of its own;
  * 2 = CTA-pair weight gradients (default 1; 0 = single-CTA kernel);
  * 5 = 256 x 512 pair tiles: 0 never, 1 (default) for the long-K (>= 4096)
- * data-gradient GEMMs on the weights as stored, 2 wherever N % 512 == 0. */
+ * data-gradient GEMMs on the weights as stored, 2 wherever N % 512 == 0;
+ * 6 = TMA tensor stores for whole 32-row output blocks of the bf16 GEMMs
+ * (default 1; 0 = LSU stores only). */
 int hm_ffn_set_option(int32_t option, int32_t value);
 
 /* ---------------- expert migration (K11) ------------------------------------

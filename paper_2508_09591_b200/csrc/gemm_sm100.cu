@@ -47,6 +47,7 @@ int g_wgrad_pair = 1;  // hm_ffn_set_option(2, 0): single-CTA weight gradients (
 // the long-K data-gradient GEMMs with B read as stored (K >= 4096: measured
 // 11-16 % faster there, slower elsewhere), 2 wherever N % 512 == 0
 int g_wide_tiles = 1;
+int g_tma_store = 1;   // hm_ffn_set_option(6, 0): LSU epilogue stores only
 struct GemmArgs {
   const int32_t* n_rows;  // [groups] rows per group (device); wgrad: K extent per group
   int groups;
@@ -91,6 +92,9 @@ struct GemmArgs {
   const hm::ExchWork* exch;
   int exch_kind;
   const int4* exch_x;
+  // mode 0, bf16 rows of exactly N columns: whole 32-row blocks leave the
+  // epilogue through TMA tensor stores (map_c) instead of LSU stores
+  int tma_store = 0;
 };
 
 
@@ -340,11 +344,40 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // TMEM -> fp32 registers -> (SwiGLU / accumulate) -> bf16 rows.  r0 = the
 // warp's first row within group g (weight-gradient modes: output row); sw =
 // the warp's shared-memory store stage.
+// TMA tensor store of one warp's 32 rows x 64 columns (bf16): the stage is
+// written in the 128-byte swizzle (unit u of row r at u ^ (r % 8), the same
+// layout stage_store<8> uses, stage 1024-byte aligned) and lane 0 issues one
+// cp.async.bulk.tensor store -- the row data leave through the async proxy
+// instead of 8 LSU store instructions per lane.  The previous store must have
+// finished reading the stage first (wait_group.read).
+__device__ __forceinline__ void tma_store_wait_read(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+}
+__device__ __forceinline__ void tma_store_chunk(uint8_t* sw, int lane, const int4* v,
+                                                const CUtensorMap* map, int col, int row) {
+  const uint32_t base = smem_u32(sw);
+  tma_store_wait_read(lane);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) sts128(base + lane * 128 + ((u ^ (lane & 7)) << 4), v[u]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(col), "r"(row), "r"(base)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 // kHalfStage: 2 KB store stages (the NA = 2 pair kernel's eight epilogue
 // warps): bf16 rows go out as 64-byte instead of 128-byte row segments
 template <int kMode, bool kHalfStage = false>
 __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& tm, int g, int nt,
-                                           int r0, int lane, uint32_t tbase, uint8_t* sw) {
+                                           int r0, int lane, uint32_t tbase, uint8_t* sw,
+                                           const CUtensorMap* tmac = nullptr) {
   int nvalid = kMode >= 2 ? 32 : tm.rows[g] - r0;
   nvalid = nvalid < 0 ? 0 : (nvalid > 32 ? 32 : nvalid);
   const bool valid = lane < nvalid;
@@ -454,6 +487,12 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
           hv[16 * half + i] = zero ? __floats2bfloat162_rn(0.f, 0.f)
                                    : __floats2bfloat162_rn(v2[half][2 * i], v2[half][2 * i + 1]);
       __nv_bfloat16* dst = args.out + row_base * args.ld_out + nt * BN + c2;
+      if (tmac && nvalid == 32 && !zero) {   // whole 32-row block: TMA tensor store
+        tma_store_chunk(sw, lane, reinterpret_cast<const int4*>(hv), tmac, nt * BN + c2,
+                        (int)row_base);
+        continue;
+      }
+      if (tmac) tma_store_wait_read(lane);    // the stage may still be read by a TMA store
       if (kHalfStage) {
         stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv), dst, args.ld_out, nvalid);
         stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv) + 4, dst + 32, args.ld_out,
@@ -876,14 +915,15 @@ struct PairCfg {
   static constexpr uint32_t kStage = kHalfBytes + kBBytes;    // A half + B halves
   static constexpr int kEpiStage = kEpiStageBytes / NA;       // per epilogue warp
   static constexpr size_t smem() {
-    return (size_t)kStages * kStage + 1024 + 256 + 4 * NA * kEpiStage;
+    return (size_t)kStages * kStage + 1024 + 1024 + 4 * NA * kEpiStage;
   }
 };
 template <int kMode, bool GA = false, bool BMN = false, int NA = 1>
 __global__ void __cluster_dims__(2, 1, 1)
     __launch_bounds__(kThreads + (GA ? kGatherThreads : 0) + (NA == 2 ? kEpi2Threads : 0), 1)
     k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c, GemmArgs args) {
   using C = PairCfg<NA>;
   constexpr int ST = C::kStages;
   constexpr int kEpi2Warp = (kThreads + (GA ? kGatherThreads : 0)) / 32;
@@ -898,7 +938,7 @@ __global__ void __cluster_dims__(2, 1, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* gfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gfull + ST);
-  uint8_t* epi = smem + ST * C::kStage + 256;   // epilogue store stages
+  uint8_t* epi = smem + ST * C::kStage + 1024;   // epilogue store stages (1024-B aligned)
   __shared__ TileMap tm;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1103,11 +1143,15 @@ __global__ void __cluster_dims__(2, 1, 1)
       tc_fence_after();
       store_tile<kMode, NA == 2>(args, tm, g, nt * NA + a, mt * BM2 + (int)rank * 128 + q * 32,
                                  lane, tmem_base + ((uint32_t)(q * 32) << 16) + (acc + a) * BN,
-                                 epi + (a * 4 + q) * C::kEpiStage);
+                                 epi + (a * 4 + q) * C::kEpiStage,
+                                 (kMode == 0 && NA == 1 && args.tma_store) ? &map_c : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty + acc + a, 0);
     }
+    // the TMA stores must be complete (and done reading the stages) before exit
+    if (kMode == 0 && NA == 1 && args.tma_store && lane == 0)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp == 3 && args.exch_kind == 1) {   // dispatch rows beside the tiles
     exch_push(*args.exch, args.exch_x, lane);
   } else if (GA && warp == 2) {
@@ -1738,9 +1782,14 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   if (ctas > 0 && ctas < sms) sms = ctas;
   HM_CHECK_ARG(sms >= 2, "grouped gemm: at least one CTA pair");
   const int grid = sms & ~1;
+  // TMA tensor stores of the output (mode 0, bf16 rows of exactly N columns)
+  CUtensorMap mc = ma;
+  if (g_tma_store && !swiglu && !out_f32 && out && ld_out == N && N % 64 == 0) {
+    if (make_map(&mc, out, (uint64_t)a_rows, (uint64_t)N, 32) == 0) args.tma_store = 1;
+  }
   auto run = [&](auto kern, int threads, size_t smem2) -> int {
     HM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    kern<<<grid, threads, smem2, s>>>(ma, mb, args);
+    kern<<<grid, threads, smem2, s>>>(ma, mb, mc, args);
     return launch_status();
   };
   const int thr_g = kThreads + kGatherThreads;   // + the A-gather warps
@@ -1779,8 +1828,9 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
 // weight gradients, single-CTA forward GEMMs, 4-byte SwiGLU backward) that
 // round 2 removed; they are rejected.
 HM_API int hm_ffn_set_option(int32_t option, int32_t value) {
-  HM_CHECK_ARG(option == 1 || option == 2 || option == 5, "hm_ffn_set_option: unknown option %d",
-               option);
+  HM_CHECK_ARG(option == 1 || option == 2 || option == 5 || option == 6,
+               "hm_ffn_set_option: unknown option %d", option);
+  if (option == 6) g_tma_store = value != 0;
   if (option == 1) g_gemm_ctas = value > 0 ? value : 0;
   if (option == 2) g_wgrad_pair = value != 0;
   if (option == 5) g_wide_tiles = value < 0 ? 0 : (value > 2 ? 2 : value);

@@ -355,3 +355,46 @@ def test_wide_tiles_match_256_tiles(hm, shape):
         r0 += sizes[g]
     torch.testing.assert_close(outs[1][0].float(), torch.cat(ref_rows), rtol=2e-2, atol=2e-2)
 
+
+
+@pytest.mark.parametrize("shape", [(5, 512, 256, [300, 0, 77, 513, 129]),
+                                   (3, 1024, 512, [31, 700, 96])])
+def test_tma_store_epilogue_matches_lsu_stores(hm, shape):
+    """GEMM2 / dH / gX epilogues with whole 32-row blocks leaving through TMA
+    tensor stores (partial blocks at group ends through LSU stores) write the
+    same rows bit for bit as the all-LSU epilogue -- and nothing past a group."""
+    from paper_2508_09591_b200 import _lib
+    from paper_2508_09591_b200.ffn import (FFNBackwardScratch, expert_ffn_backward_ptrs,
+                                           expert_ffn_save_ptrs)
+    G, M, I, sizes = shape
+    torch.manual_seed(66)
+    n = torch.tensor(sizes, dtype=torch.int32)
+    rows = int(n.sum())
+    cap = rows + 64
+    nr = n.cuda()
+    x = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    outs = []
+    try:
+        for tma in (0, 1):
+            _lib.call("hm_ffn_set_option", 6, tma)
+            h = torch.zeros(cap, I, dtype=torch.bfloat16, device="cuda")
+            y = torch.full((cap, M), 7.0, dtype=torch.bfloat16, device="cuda")
+            g13 = torch.zeros(cap, 2 * I, dtype=torch.bfloat16, device="cuda")
+            expert_ffn_save_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, M, I, h,
+                                 y.data_ptr(), g13.data_ptr())
+            sc = FFNBackwardScratch(cap, G, M, I)
+            gx = torch.full((cap, M), 7.0, dtype=torch.bfloat16, device="cuda")
+            dw13, dw2 = torch.zeros_like(w13), torch.zeros_like(w2)
+            expert_ffn_backward_ptrs(x.data_ptr(), cap, nr.data_ptr(), G, w13, w2, gy.data_ptr(),
+                                     M, I, sc, gx.data_ptr(), dw13, dw2, g13.data_ptr())
+            torch.cuda.synchronize()
+            outs.append((y.clone(), gx.clone(), dw13.clone(), dw2.clone(), sc.dh[:rows].clone()))
+    finally:
+        _lib.call("hm_ffn_set_option", 6, 1)
+    for name, a, b in zip(["y", "gX", "dW13", "dW2", "dH"], outs[0], outs[1]):
+        assert torch.equal(a, b), name
+    # rows past the last group are never written
+    assert torch.all(outs[1][0][rows:] == 7.0) and torch.all(outs[1][1][rows:] == 7.0)

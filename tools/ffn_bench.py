@@ -63,5 +63,7 @@ if __name__ == "__main__":
     from paper_2508_09591_b200 import _lib
     if "HM_WIDE" in os.environ:   # hm_ffn_set_option(5, .): 256 x 512 tiles
         _lib.call("hm_ffn_set_option", 5, int(os.environ["HM_WIDE"]))
+    if "HM_TMA_STORE" in os.environ:   # hm_ffn_set_option(6, .): TMA epilogue stores
+        _lib.call("hm_ffn_set_option", 6, int(os.environ["HM_TMA_STORE"]))
     run("qwen3_rank", 16, 2048, 768, 2048)
     run("dsv3_rank", 32, 7168, 2048, 1024)

@@ -16,7 +16,9 @@ ONCE = "--once" in sys.argv     # one launch of each, Qwen3 only (for ncu)
 GRIDS = [int(a.split("=")[1]) for a in sys.argv if a.startswith("--grid=")] or [0]
 # --wide=0,2: hm_ffn_set_option(5, w) per run (256 x 256 vs 256 x 512 tiles), interleaved
 WIDE = [int(w) for a in sys.argv if a.startswith("--wide=") for w in a.split("=")[1].split(",")] or [1]
-REPS = 2 if len(WIDE) > 1 else 1
+# --tma=0,1: hm_ffn_set_option(6, t) (LSU vs TMA epilogue stores), interleaved
+TMA = [int(w) for a in sys.argv if a.startswith("--tma=") for w in a.split("=")[1].split(",")] or [1]
+REPS = 2 if len(WIDE) > 1 or len(TMA) > 1 else 1
 
 
 def t(fn, n=20):
@@ -51,9 +53,11 @@ for name, G, M, I, per in (("qwen3", 16, 2048, 768, 2048), ("dsv3", 32, 7168, 20
     y = torch.empty(cap, M, device="cuda", dtype=torch.bfloat16)
     g13 = torch.empty(cap, 2 * I, device="cuda", dtype=torch.bfloat16)
     st = _lib.stream_ptr()
-    for grid, wide in [(g, w) for _ in range(REPS) for g in GRIDS for w in WIDE]:
+    for grid, wide, tma in [(g, w, t) for _ in range(REPS) for g in GRIDS for w in WIDE
+                            for t in TMA]:
         _lib.call("hm_ffn_set_option", 1, grid)
         _lib.call("hm_ffn_set_option", 5, wide)
+        _lib.call("hm_ffn_set_option", 6, tma)
         g1 = t(lambda: _lib.call("hm_grouped_gemm", x.data_ptr(), cap, w13.data_ptr(), G,
                                  nr.data_ptr(), 2 * I, M, 1, h.data_ptr(), I, st))
         g2 = t(lambda: _lib.call("hm_grouped_gemm", h.data_ptr(), cap, w2.data_ptr(), G,
@@ -63,7 +67,7 @@ for name, G, M, I, per in (("qwen3", 16, 2048, 768, 2048), ("dsv3", 32, 7168, 20
         gx = t(lambda: _lib.call("hm_grouped_gemm_kn", g13.data_ptr(), cap, w13.data_ptr(), G,
                                  nr.data_ptr(), M, 2 * I, y.data_ptr(), M, st))
         f1, f2 = 2 * rows * 2 * I * M, 2 * rows * M * I
-        print(json.dumps({"shape": name, "rows": rows, "grid": grid, "wide": wide,
+        print(json.dumps({"shape": name, "rows": rows, "grid": grid, "wide": wide, "tma": tma,
                           "gemm1_ms": round(g1, 4), "gemm1_tf": round(f1 / g1 / 1e9, 1),
                           "gemm2_ms": round(g2, 4), "gemm2_tf": round(f2 / g2 / 1e9, 1),
                           "fwd_save_ms": round(fs, 4),
