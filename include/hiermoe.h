@@ -207,6 +207,14 @@ int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, const void
 int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
                  int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
                  void* stream);
+/* ... the same with the token reduction split into chunks (sized on the device
+ * from rows_dev) over the SMs, fp32 partials in the caller's scratch
+ * (hm_wgrad_f32_scratch_bytes(rows, m_out, N) bytes; 0 = no split needed)
+ * summed into out: a 128 x 2048 router gradient is only 8 output tiles. */
+int64_t hm_wgrad_f32_scratch_bytes(int64_t rows, int32_t m_out, int32_t N);
+int hm_wgrad_f32_split(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
+                       int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
+                       void* scratch, int64_t scratch_bytes, void* stream);
 /* Gate backward: dense bf16 dlogits [T][ld] (zero past E) from the gate
  * weights' gradient dw [T][K]; mode 0 softmax over the picks (renormalised),
  * 1 softmax over all experts, 2 DeepSeek-V3 normalised sigmoid (route_scale). */

@@ -1881,9 +1881,9 @@ HM_API int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, con
 // Split-K for the router weight gradient: its output is only m_out x N (8
 // tiles of 128 x 256 for 128 experts x hidden 2048), so one group would keep
 // 8 of 148 SMs busy over all T tokens.  The token range is cut into S chunks
-// (device-side sizes from the device row count), each chunk an mode-3 group
-// with its own fp32 partial [m_out][N], and the partials are summed (+ the
-// accumulated gradient) by k_sum_splits.
+// (device-side sizes from the device row count), each chunk a mode-3 group
+// with its own fp32 partial [m_out][N] in the caller's scratch, and the
+// partials are summed (+ the accumulated gradient) by k_sum_splits.
 namespace {
 __global__ void k_split_rows(const int32_t* __restrict__ total, int S, int chunk,
                              int32_t* __restrict__ n_rows) {
@@ -1913,52 +1913,63 @@ __global__ void __launch_bounds__(256) k_sum_splits(const float4* __restrict__ p
     *o = acc;
   }
 }
-struct SplitScratch {
-  float* part = nullptr;
-  size_t bytes = 0;
-  int32_t* n_rows = nullptr;
-};
-SplitScratch g_split[64];   // per device
+// chunks of the split: ~one per 8-tile output per SM, >= 4 k-blocks each
+int wgrad_splits(int64_t rows, int m_out, int N) {
+  int dev = 0, sms = kSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (m_out / BM) * (N / BN);
+  int S = tiles > 0 ? sms / tiles : 1;
+  S = S > 64 ? 64 : S;
+  if ((int64_t)S * 4 * BK > rows) S = (int)(rows / (4 * BK));
+  return S < 1 ? 1 : S;
+}
 }  // namespace
+
+HM_API int64_t hm_wgrad_f32_scratch_bytes(int64_t rows, int32_t m_out, int32_t N) {
+  const int S = wgrad_splits(rows > 0 ? rows : 1, m_out, N);
+  return S < 2 ? 0 : 256 + (int64_t)S * m_out * N * 4;
+}
 
 HM_API int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
                         int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
                         void* stream) {
   HM_RANGE("hm_wgrad_f32");
   HM_CHECK_ARG(a && b && out && rows_dev, "hm_wgrad_f32: null argument");
+  return launch_gemm_wgrad(a, b, rows > 0 ? rows : 1, 1, rows_dev, m_out, N, nullptr, ld_out,
+                           (cudaStream_t)stream, accumulate, nullptr, 0, out);
+}
+
+HM_API int hm_wgrad_f32_split(const void* a, const void* b, int64_t rows,
+                              const int32_t* rows_dev, int32_t m_out, int32_t N, float* out,
+                              int64_t ld_out, int32_t accumulate, void* scratch,
+                              int64_t scratch_bytes, void* stream) {
+  HM_RANGE("hm_wgrad_f32_split");
+  HM_CHECK_ARG(a && b && out && rows_dev, "hm_wgrad_f32_split: null argument");
   HM_CHECK_ARG(m_out % BM == 0 && N % BN == 0 && ld_out % 4 == 0,
-               "hm_wgrad_f32: m_out %% 128 == 0, N %% 256 == 0, 16-byte output rows");
+               "hm_wgrad_f32_split: m_out %% 128 == 0, N %% 256 == 0, 16-byte output rows");
   cudaStream_t s = (cudaStream_t)stream;
   rows = rows > 0 ? rows : 1;
+  const int S = wgrad_splits(rows, m_out, N);
+  const int64_t need = S < 2 ? 0 : 256 + (int64_t)S * m_out * N * 4;
+  if (S < 2)
+    return launch_gemm_wgrad(a, b, rows, 1, rows_dev, m_out, N, nullptr, ld_out, s, accumulate,
+                             nullptr, 0, out);
+  HM_CHECK_ARG(scratch && scratch_bytes >= need,
+               "hm_wgrad_f32_split: scratch of hm_wgrad_f32_scratch_bytes() bytes required");
+  int32_t* n_rows = reinterpret_cast<int32_t*>(scratch);   // 64 counts in the first 256 B
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(scratch) + 256);
+  const int chunk = (int)((rows + S - 1) / S + BK - 1) / BK * BK;
+  k_split_rows<<<1, 64, 0, s>>>(rows_dev, S, chunk, n_rows);
+  HM_LAUNCHED();
+  int st = launch_gemm_wgrad(a, b, rows, S, n_rows, m_out, N, nullptr, N, s, 0, nullptr, 0, part);
+  if (st) return st;
   int dev = 0, sms = kSMs;
   HM_CUDA(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = (m_out / BM) * (N / BN);
-  int S = sms / tiles;
-  S = S > 64 ? 64 : S;
-  if ((int64_t)S * 4 * BK > rows) S = (int)(rows / (4 * BK));   // >= 4 k-blocks per chunk
-  if (S < 2 || dev >= 64)
-    return launch_gemm_wgrad(a, b, rows, 1, rows_dev, m_out, N, nullptr, ld_out, s, accumulate,
-                             nullptr, 0, out);
-  const int chunk = (int)((rows + S - 1) / S + BK - 1) / BK * BK;
-  SplitScratch& sc = g_split[dev];
-  const size_t need = (size_t)S * m_out * N * 4;
-  if (sc.bytes < need) {
-    if (sc.part) cudaFree(sc.part);
-    sc.part = nullptr;
-    sc.bytes = 0;
-    HM_CUDA(cudaMalloc(&sc.part, need));
-    sc.bytes = need;
-  }
-  if (!sc.n_rows) HM_CUDA(cudaMalloc(&sc.n_rows, 64 * sizeof(int32_t)));
-  k_split_rows<<<1, 64, 0, s>>>(rows_dev, S, chunk, sc.n_rows);
-  HM_LAUNCHED();
-  int st = launch_gemm_wgrad(a, b, rows, S, sc.n_rows, m_out, N, nullptr, N, s, 0, nullptr, 0,
-                             sc.part);
-  if (st) return st;
   const int64_t n4 = (int64_t)m_out * N / 4;
   const int grid = (int)((n4 + 255) / 256 < 4 * sms ? (n4 + 255) / 256 : 4 * sms);
-  k_sum_splits<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(sc.part), S, m_out, N, out,
+  k_sum_splits<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(part), S, m_out, N, out,
                                     ld_out, accumulate);
   HM_LAUNCHED();
   return 0;

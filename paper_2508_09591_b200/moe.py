@@ -206,6 +206,7 @@ class HierMoELayer:
             self.dw2 = torch.zeros_like(self.w2)
             # fp32 router weight grad, padded to the wgrad GEMM's 128-row tiles
             self._dwr_pad = torch.zeros(self._e128, hidden, device="cuda")
+            self._wgrad_scratch = None   # split-K partials of the router weight gradient
             self.dw_router = self._dwr_pad[:experts]
 
     def set_placement(self, placement: Placement) -> None:
@@ -535,8 +536,14 @@ class HierMoELayer:
         rows = self._rows_dev(t)
         _lib.call("hm_gemm_f32", ptr(dlogits), t, ptr(rows), ptr(self._wrt), self.hidden,
                   self._e128, self.hidden, ptr(dxf), self.hidden, stream_ptr())
-        _lib.call("hm_wgrad_f32", ptr(dlogits), ptr(x), t, ptr(rows), self._e128, self.hidden,
-                  ptr(self._dwr_pad), self.hidden, 1, stream_ptr())
+        # split over the token range (an E x M gradient is only a few output
+        # tiles); the fp32 partials live in a layer-owned scratch
+        need = int(_lib.load().hm_wgrad_f32_scratch_bytes(t, self._e128, self.hidden))
+        if need and (self._wgrad_scratch is None or self._wgrad_scratch.numel() < need):
+            self._wgrad_scratch = torch.empty(need, dtype=torch.uint8, device="cuda")
+        _lib.call("hm_wgrad_f32_split", ptr(dlogits), ptr(x), t, ptr(rows), self._e128,
+                  self.hidden, ptr(self._dwr_pad), self.hidden, 1,
+                  ptr(self._wgrad_scratch) if need else None, need, stream_ptr())
         shared_dx = None
         if self.shared_inter:
             torch.cuda.current_stream().wait_event(self._shared_done)

@@ -94,7 +94,7 @@ def test_router_backward_gemms(hm, E, M, T):
 
 @pytest.mark.parametrize("valid", [4096, 3000, 200, 0])
 def test_router_wgrad_split_k_device_count(hm, valid):
-    """hm_wgrad_f32 splits the token reduction into chunks sized on the device
+    """hm_wgrad_f32_split splits the token reduction into chunks sized on the device
     from the live row count: rows past the count (capacity 4096) never enter
     the gradient, empty chunks add zero, the accumulated value is kept."""
     from paper_2508_09591_b200._lib import ptr, stream_ptr
@@ -104,7 +104,15 @@ def test_router_wgrad_split_k_device_count(hm, valid):
     dl = torch.randn(T, e128, device="cuda", generator=g).to(torch.bfloat16)
     rows = torch.tensor([valid], dtype=torch.int32, device="cuda")
     dwp = torch.full((e128, M), 0.5, device="cuda")
-    _call("hm_wgrad_f32", ptr(dl), ptr(x), T, ptr(rows), e128, M, ptr(dwp), M, 1, stream_ptr())
+    from paper_2508_09591_b200 import _lib
+    need = int(_lib.load().hm_wgrad_f32_scratch_bytes(T, e128, M))
+    assert need > 0
+    with pytest.raises(ValueError):   # the split needs its scratch
+        _call("hm_wgrad_f32_split", ptr(dl), ptr(x), T, ptr(rows), e128, M, ptr(dwp), M, 1,
+              None, 0, stream_ptr())
+    scratch = torch.empty(need, dtype=torch.uint8, device="cuda")
+    _call("hm_wgrad_f32_split", ptr(dl), ptr(x), T, ptr(rows), e128, M, ptr(dwp), M, 1,
+          ptr(scratch), need, stream_ptr())
     torch.cuda.synchronize()
     ref = 0.5 + dl[:valid].float().T @ x[:valid].float()
     torch.testing.assert_close(dwp, ref, rtol=1e-4, atol=1e-3)
