@@ -478,6 +478,9 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
 #pragma unroll 1
     for (int c2 = 0; c2 < BN; c2 += 64) {
       float v2[2][32];
+#ifdef HM_EPI_LD_TWICE   // A/B probe (tools/variant_build.sh): double the TMEM reads
+      tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
+#endif
       tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
       __align__(16) __nv_bfloat162 hv[32];
 #pragma unroll
@@ -1032,17 +1035,19 @@ __global__ void __cluster_dims__(2, 1, 1)
       uint32_t phase = 0;
       int it = 0;
       // one k-block's MMAs into accumulator a (TMEM columns a * 256)
+      // descriptors built once per k-block; the k-steps advance the 14-bit
+      // start-address field (16-byte units, no carry below 256 KB): +2 per
+      // 32-byte K step (K-major), +128 per 16 K lines (MN-major B)
       auto mma_kb = [&](uint32_t d, int st, int kb, int a) {
-        const uint32_t a0 = smem_u32(sa + st * kHalfBytes);
+        const uint64_t da = smem_desc(smem_u32(sa + st * kHalfBytes));
         const uint32_t b0 = smem_u32(sb + st * C::kBBytes + a * kHalfBytes);
+        const uint64_t db = BMN ? smem_desc_mn(b0) : smem_desc(b0);
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k) {
           if (BMN)
-            umma_bf16_pair<kIdesc2BMN>(d, smem_desc(a0 + k * UK * 2),
-                                       smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+            umma_bf16_pair<kIdesc2BMN>(d, da + 2 * k, db + 128 * k, (kb | k) ? 1u : 0u);
           else
-            umma_bf16_pair(d, smem_desc(a0 + k * UK * 2), smem_desc(b0 + k * UK * 2),
-                           (kb | k) ? 1u : 0u);
+            umma_bf16_pair(d, da + 2 * k, db + 2 * k, (kb | k) ? 1u : 0u);
         }
       };
       auto wait_full = [&](int st, uint32_t ph) {
