@@ -323,7 +323,8 @@ int hm_expert_ffn_backward_multi(const void* x, int64_t x_rows, const int32_t* i
                                  void* stream);
 /* parts: 1 = data gradients (dH, SwiGLU backward, gX), 2 = weight gradients
  * (dW2, dW13 from part 1's scratch), 3 = both -- a caller can run the
- * dispatch backward of gX beside the weight-gradient GEMMs. */
+ * dispatch backward of gX beside the weight-gradient GEMMs; + 4: h holds the
+ * forward's H (not rewritten by the SwiGLU backward; dW2 uses it). */
 /* FFN options (no reference counterpart): 1 = cap on the persistent GEMM grid
  * in CTAs (0 = one per SM), so a concurrent exchange keeps SMs of its own;
  * 2 = CTA-pair weight gradients (default 1; 0 = single-CTA kernel);

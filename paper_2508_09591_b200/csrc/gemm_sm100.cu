@@ -1578,7 +1578,7 @@ __global__ void __launch_bounds__(256) k_swiglu_bwd_v8(const __nv_bfloat16* __re
       da2[q] = __floats2bfloat162_rn(d.x * u.x * s0 * (1.f + a.x * (1.f - s0)),
                                      d.y * u.y * s1 * (1.f + a.y * (1.f - s1)));
     }
-    *reinterpret_cast<int4*>(h + (int64_t)r * inter + j) = hv;
+    if (h) *reinterpret_cast<int4*>(h + (int64_t)r * inter + j) = hv;   // null: H kept
     *reinterpret_cast<int4*>(dg13 + gu) = duv;
     *reinterpret_cast<int4*>(dg13 + ga) = dav;
   }
@@ -2027,7 +2027,12 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
   cudaStream_t s = (cudaStream_t)stream;
   HM_CHECK_ARG(!x_idx || g13_saved,
                "ffn backward: gathered activations need the saved pre-activations");
-  HM_CHECK_ARG(parts >= 1 && parts <= 3, "ffn backward: parts must be 1, 2 or 3");
+  // parts bit 4: h already holds the forward's H (GEMM1's epilogue output),
+  // so the SwiGLU backward does not rewrite it and dW2 uses the very H that
+  // produced the forward's Y
+  const bool h_fwd = (parts & 4) != 0;
+  parts &= 3;
+  HM_CHECK_ARG(parts >= 1 && parts <= 3, "ffn backward: parts must be 1, 2 or 3 (+4)");
   const int M = hidden, I = inter;
   int st;
   const int sg = seg_groups, segs = sg > 0 ? (groups + sg - 1) / sg : 1;
@@ -2048,7 +2053,7 @@ static int ffn_backward(const void* x, int64_t a_rows, const int32_t* n_rows, in
   HM_CHECK_ARG(I % 128 == 0, "ffn backward: inter must be a multiple of 128");
   k_swiglu_bwd_v8<<<kSMs * 8, 256, 0, s>>>((const __nv_bfloat16*)g13, (const __nv_bfloat16*)dh,
                                             layout, segs, sg > 0 ? seg_rows : 0, I,
-                                            (__nv_bfloat16*)dg13, (__nv_bfloat16*)h);
+                                            (__nv_bfloat16*)dg13, h_fwd ? nullptr : (__nv_bfloat16*)h);
   HM_LAUNCHED();
   // data gradient gX = dG13 W13: W13 [g][2I][M] as stored = B [K = 2I][N = M]
   if ((st = launch_gemm(dg13, a_rows, w13, groups, n_rows, M, 2 * I, 0, gx, M, nullptr, s,

@@ -98,14 +98,17 @@ def expert_ffn_backward_multi_ptrs(x_ptr: int, x_rows: int, idx_ptr: int, seg_ro
                                    inter: int, sc: "FFNBackwardScratch", gx_ptr: int,
                                    dw13: torch.Tensor, dw2: torch.Tensor, g13_ptr: int,
                                    accumulate: bool = False, recv_ptr: int = 0,
-                                   parts: int = 3) -> None:
+                                   parts: int = 3, h_fwd: torch.Tensor | None = None) -> None:
     """Backward of expert_ffn_multi_ptrs (saved pre-activations).  parts: 1 =
-    data gradients (gx), 2 = weight gradients (from part 1's scratch), 3 = both."""
+    data gradients (gx), 2 = weight gradients (from part 1's scratch), 3 = both.
+    h_fwd: the forward's H (same row layout) -- dW2 uses it and the SwiGLU
+    backward does not recompute it into the scratch."""
+    h = sc.h if h_fwd is None else h_fwd
     _lib.call("hm_expert_ffn_backward_multi", x_ptr, x_rows, idx_ptr or None, recv_ptr or None,
               seg_rows, segs,
               n_rows_ptr, groups_per_seg, ptr(w13), ptr(w2), gy_ptr, hidden, inter, g13_ptr,
-              ptr(sc.dh), ptr(sc.dg13), ptr(sc.h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
-              int(bool(accumulate)), int(parts), stream_ptr())
+              ptr(sc.dh), ptr(sc.dg13), ptr(h), ptr(sc.layout), gx_ptr, ptr(dw13), ptr(dw2),
+              int(bool(accumulate)), int(parts) | (4 if h_fwd is not None else 0), stream_ptr())
 
 
 def set_gemm_ctas(n: int) -> None:

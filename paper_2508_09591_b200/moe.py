@@ -510,14 +510,17 @@ class HierMoELayer:
                     # NVLink) on a side stream beside the weight-gradient GEMMs
                     # (tensor cores), which read only the FFN's own scratch
                     s_m = torch.cuda.current_stream()
-                    expert_ffn_backward_multi_ptrs(*args, recv_ptr=recv, parts=1)
+                    expert_ffn_backward_multi_ptrs(*args, recv_ptr=recv, parts=1,
+                                                   h_fwd=self.hs[m])
                     self._cside.wait_stream(s_m)
                     with torch.cuda.stream(self._cside):
                         wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])
-                    expert_ffn_backward_multi_ptrs(*args, recv_ptr=recv, parts=2)
+                    expert_ffn_backward_multi_ptrs(*args, recv_ptr=recv, parts=2,
+                                                   h_fwd=self.hs[m])
                     s_m.wait_stream(self._cside)
                     continue
-                expert_ffn_backward_multi_ptrs(*args, accumulate=m > 0, recv_ptr=recv)
+                expert_ffn_backward_multi_ptrs(*args, accumulate=m > 0, recv_ptr=recv,
+                                               h_fwd=self.hs[m])
                 ffn_done = torch.cuda.Event()
                 ffn_done.record()
                 wd.combine_grad(slot[rows], dw[rows], dedup=self.dedup, out=dx[rows])

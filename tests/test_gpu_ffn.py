@@ -398,3 +398,44 @@ def test_tma_store_epilogue_matches_lsu_stores(hm, shape):
         assert torch.equal(a, b), name
     # rows past the last group are never written
     assert torch.all(outs[1][0][rows:] == 7.0) and torch.all(outs[1][1][rows:] == 7.0)
+
+
+def test_backward_with_forward_h_matches_recompute(hm):
+    """Backward part bit 4 (h = the forward's H, not rewritten; dW2 from it)
+    gives gX / dW13 / dW2 / dG13 bit for bit equal to the recomputing
+    backward when handed the same H, and leaves that H untouched."""
+    from paper_2508_09591_b200.ffn import FFNBackwardScratch, expert_ffn_backward_multi_ptrs
+    from paper_2508_09591_b200.ffn import expert_ffn_multi_ptrs
+    torch.manual_seed(77)
+    G, M, I = 4, 512, 256
+    n = torch.tensor([300, 0, 77, 257], dtype=torch.int32)
+    cap = 704
+    nr = n.cuda()
+    x = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(cap, M, device="cuda").to(torch.bfloat16)
+    w13 = (torch.randn(G, 2 * I, M, device="cuda") * M ** -0.5).to(torch.bfloat16)
+    w2 = (torch.randn(G, M, I, device="cuda") * I ** -0.5).to(torch.bfloat16)
+    idx = torch.arange(cap, dtype=torch.int32, device="cuda")
+    h = torch.zeros(cap, I, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(cap, M, dtype=torch.bfloat16, device="cuda")
+    g13 = torch.zeros(cap, 2 * I, dtype=torch.bfloat16, device="cuda")
+    expert_ffn_multi_ptrs(x.data_ptr(), cap, idx.data_ptr(), cap, 1, nr.data_ptr(), G, w13, w2,
+                          M, I, h, y.data_ptr(), g13.data_ptr())
+    outs = []
+    h_given = None
+    for use_fwd in (False, True):
+        sc = FFNBackwardScratch(cap, G, M, I)
+        gx = torch.zeros(cap, M, dtype=torch.bfloat16, device="cuda")
+        dw13, dw2 = torch.zeros_like(w13), torch.zeros_like(w2)
+        expert_ffn_backward_multi_ptrs(x.data_ptr(), cap, idx.data_ptr(), cap, 1, nr.data_ptr(),
+                                       G, w13, w2, gy.data_ptr(), M, I, sc, gx.data_ptr(), dw13,
+                                       dw2, g13.data_ptr(),
+                                       h_fwd=h_given if use_fwd else None)
+        torch.cuda.synchronize()
+        outs.append((gx.clone(), dw13.clone(), dw2.clone(), sc.dg13[:int(n.sum())].clone()))
+        if not use_fwd:
+            h_given = sc.h.clone()          # the recomputed H, handed in as "the forward's"
+            h_keep = h_given.clone()
+    for name, a, b in zip(["gX", "dW13", "dW2", "dG13"], outs[0], outs[1]):
+        assert torch.equal(a, b), name
+    assert torch.equal(h_given, h_keep), "the forward's H is not rewritten"
