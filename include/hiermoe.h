@@ -207,6 +207,12 @@ int hm_gemm_f32(const void* a, int64_t rows, const int32_t* rows_dev, const void
 int hm_wgrad_f32(const void* a, const void* b, int64_t rows, const int32_t* rows_dev,
                  int32_t m_out, int32_t N, float* out, int64_t ld_out, int32_t accumulate,
                  void* stream);
+/* out[rows][ld] bf16 = bf16((A . B^T + add1) + add2) (fp32 sums, add2 may be
+ * NULL): the router input gradient fused with the routed / shared-expert
+ * input gradients -- hm_gemm_f32 + hm_sum_to_bf16 in one launch. */
+int hm_gemm_add_bf16(const void* a, int64_t rows, const int32_t* rows_dev, const void* b,
+                     int32_t N, int32_t K, const void* add1, const void* add2, void* out,
+                     int64_t ld_out, void* stream);
 /* ... the same with the token reduction split into chunks (sized on the device
  * from rows_dev) over the SMs, fp32 partials in the caller's scratch
  * (hm_wgrad_f32_scratch_bytes(rows, m_out, N) bytes; 0 = no split needed)

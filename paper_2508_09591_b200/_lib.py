@@ -89,6 +89,8 @@ _SIGS = {
     "hm_wgrad_f32": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_int32,
                                c_void_p, c_int64, c_int32, c_void_p]),
     "hm_wgrad_f32_scratch_bytes": (c_int64, [c_int64, c_int32, c_int32]),
+    "hm_gemm_add_bf16": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_int32,
+                                   c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "hm_wgrad_f32_split": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_int32,
                                      c_void_p, c_int64, c_int32, c_void_p, c_int64, c_void_p]),
     "hm_sum_to_bf16": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),

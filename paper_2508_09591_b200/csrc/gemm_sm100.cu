@@ -95,6 +95,11 @@ struct GemmArgs {
   // mode 0, bf16 rows of exactly N columns: whole 32-row blocks leave the
   // epilogue through TMA tensor stores (map_c) instead of LSU stores
   int tma_store = 0;
+  // mode 0, bf16 out: out = bf16((acc + add1) + add2) with fp32 sums, addend
+  // rows [rows][ld_out] bf16 (add2 optional) -- the router's input gradient
+  // summed with the routed and shared-expert ones, rounded once
+  const __nv_bfloat16* add1 = nullptr;
+  const __nv_bfloat16* add2 = nullptr;
 };
 
 
@@ -478,10 +483,27 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
 #pragma unroll 1
     for (int c2 = 0; c2 < BN; c2 += 64) {
       float v2[2][32];
-#ifdef HM_EPI_LD_TWICE   // A/B probe (tools/variant_build.sh): double the TMEM reads
       tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
-#endif
-      tmem_ld32x2(tbase + c2, tbase + c2 + 32, v2[0], v2[1]);
+      if (kMode == 0 && args.add1 && valid) {   // + bf16 addends, this lane's row
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const __nv_bfloat16* ad = t ? args.add2 : args.add1;
+          if (!ad) break;
+          const int4* ap =
+              reinterpret_cast<const int4*>(ad + (row_base + lane) * args.ld_out + nt * BN + c2);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int4 w = __ldg(ap + q);
+            const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(w2[e]);
+              v2[q >> 2][(q & 3) * 8 + 2 * e] += f.x;
+              v2[q >> 2][(q & 3) * 8 + 2 * e + 1] += f.y;
+            }
+          }
+        }
+      }
       __align__(16) __nv_bfloat162 hv[32];
 #pragma unroll
       for (int half = 0; half < 2; ++half)
@@ -1735,7 +1757,8 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
                 bool b_mn = false, const int32_t* g_row0 = nullptr,
                 const int32_t* g_wsel = nullptr, int nweights = 0, int ctas = 0,
                 const hm::ExchWork* exch = nullptr, int exch_kind = 0,
-                const void* exch_x = nullptr) {
+                const void* exch_x = nullptr, const void* add1 = nullptr,
+                const void* add2 = nullptr) {
   HM_CHECK_ARG(groups >= 1 && groups <= kMaxGroups, "grouped gemm: 1..%d groups", kMaxGroups);
   HM_CHECK_ARG(N % BN == 0 && K % BK == 0, "grouped gemm: N %% 256 == 0 and K %% 64 == 0 required");
   HM_CHECK_ARG(a_rows >= 1, "grouped gemm: empty A");
@@ -1779,6 +1802,10 @@ int launch_gemm(const void* a, int64_t a_rows, const void* b, int groups, const 
   args.exch = exch;
   args.exch_kind = exch_kind;
   args.exch_x = reinterpret_cast<const int4*>(exch_x);
+  HM_CHECK_ARG(!add1 || (!swiglu && !out_f32 && out), "grouped gemm: addends need bf16 mode 0");
+  HM_CHECK_ARG(!add2 || add1, "grouped gemm: the second addend needs the first");
+  args.add1 = reinterpret_cast<const __nv_bfloat16*>(add1);
+  args.add2 = reinterpret_cast<const __nv_bfloat16*>(add2);
   int dev = 0;
   HM_CUDA(cudaGetDevice(&dev));
   int sms = kSMs;
@@ -1930,6 +1957,19 @@ int wgrad_splits(int64_t rows, int m_out, int N) {
   return S < 1 ? 1 : S;
 }
 }  // namespace
+
+// out[rows][ld] bf16 = bf16((A . B^T + add1) + add2), fp32 sums, add2 optional:
+// the router's input gradient dlogits . Wr fused with the routed / shared-expert
+// input gradients (replaces hm_gemm_f32 + hm_sum_to_bf16, bit-identical)
+HM_API int hm_gemm_add_bf16(const void* a, int64_t rows, const int32_t* rows_dev, const void* b,
+                            int32_t N, int32_t K, const void* add1, const void* add2, void* out,
+                            int64_t ld_out, void* stream) {
+  HM_RANGE("hm_gemm_add_bf16");
+  HM_CHECK_ARG(a && b && out && rows_dev && add1, "hm_gemm_add_bf16: null argument");
+  return launch_gemm(a, rows > 0 ? rows : 1, b, 1, rows_dev, N, K, 0, out, ld_out, nullptr,
+                     (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr, false,
+                     nullptr, nullptr, 0, 0, nullptr, 0, nullptr, add1, add2);
+}
 
 HM_API int64_t hm_wgrad_f32_scratch_bytes(int64_t rows, int32_t m_out, int32_t N) {
   const int S = wgrad_splits(rows > 0 ? rows : 1, m_out, N);

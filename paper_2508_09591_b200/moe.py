@@ -535,10 +535,7 @@ class HierMoELayer:
         _lib.call("hm_gate_backward", ptr(logits), ptr(ex), ptr(w), ptr(dw), t, self.experts,
                   self.top_k, mode, float(self.route_scale), ptr(dlogits), self._e128,
                   stream_ptr())
-        dxf = torch.empty(t, self.hidden, device="cuda")
         rows = self._rows_dev(t)
-        _lib.call("hm_gemm_f32", ptr(dlogits), t, ptr(rows), ptr(self._wrt), self.hidden,
-                  self._e128, self.hidden, ptr(dxf), self.hidden, stream_ptr())
         # split over the token range (an E x M gradient is only a few output
         # tiles); the fp32 partials live in a layer-owned scratch
         need = int(_lib.load().hm_wgrad_f32_scratch_bytes(t, self._e128, self.hidden))
@@ -552,12 +549,16 @@ class HierMoELayer:
             torch.cuda.current_stream().wait_event(self._shared_done)
             shared_dx = self._shared_dx
         if dx.dtype != torch.bfloat16:
+            dxf = torch.empty(t, self.hidden, device="cuda")
+            _lib.call("hm_gemm_f32", ptr(dlogits), t, ptr(rows), ptr(self._wrt), self.hidden,
+                      self._e128, self.hidden, ptr(dxf), self.hidden, stream_ptr())
             out = dxf + dx
             return out if shared_dx is None else out + shared_dx
-        # ((router term + dx) + shared dx) in fp32, rounded once to bf16
+        # ((router term dlogits . Wr + dx) + shared dx) in fp32, rounded once
+        # to bf16 in the router GEMM's epilogue
         out = torch.empty_like(dx)
-        _lib.call("hm_sum_to_bf16", ptr(dxf), ptr(dx), ptr(shared_dx), ptr(out), dx.numel(),
-                  stream_ptr())
+        _lib.call("hm_gemm_add_bf16", ptr(dlogits), t, ptr(rows), ptr(self._wrt), self.hidden,
+                  self._e128, ptr(dx), ptr(shared_dx), ptr(out), self.hidden, stream_ptr())
         return out
 
     # --- routing traces and placements in the reference's file formats ---

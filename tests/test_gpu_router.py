@@ -116,3 +116,27 @@ def test_router_wgrad_split_k_device_count(hm, valid):
     torch.cuda.synchronize()
     ref = 0.5 + dl[:valid].float().T @ x[:valid].float()
     torch.testing.assert_close(dwp, ref, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("T,shared", [(4096, True), (1000, False), (777, True)])
+def test_router_dx_fused_sum_matches_separate(hm, T, shared):
+    """hm_gemm_add_bf16 (router input gradient with the routed / shared dx
+    added in the GEMM epilogue, one rounding) equals hm_gemm_f32 followed by
+    hm_sum_to_bf16 bit for bit -- whole and partial 32-row blocks."""
+    from paper_2508_09591_b200._lib import ptr, stream_ptr
+    g = torch.Generator(device="cuda").manual_seed(T)
+    E, M = 128, 2048
+    dl = torch.randn(T, E, device="cuda", generator=g).to(torch.bfloat16)
+    wt = (torch.randn(M, E, device="cuda", generator=g) * E ** -0.5).to(torch.bfloat16)
+    dx = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16)
+    sdx = torch.randn(T, M, device="cuda", generator=g).to(torch.bfloat16) if shared else None
+    rows = torch.tensor([T], dtype=torch.int32, device="cuda")
+    dxf = torch.empty(T, M, device="cuda")
+    _call("hm_gemm_f32", ptr(dl), T, ptr(rows), ptr(wt), M, E, M, ptr(dxf), M, stream_ptr())
+    ref = torch.empty(T, M, dtype=torch.bfloat16, device="cuda")
+    _call("hm_sum_to_bf16", ptr(dxf), ptr(dx), ptr(sdx), ptr(ref), dx.numel(), stream_ptr())
+    out = torch.empty(T, M, dtype=torch.bfloat16, device="cuda")
+    _call("hm_gemm_add_bf16", ptr(dl), T, ptr(rows), ptr(wt), M, E, ptr(dx), ptr(sdx), ptr(out),
+          M, stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
