@@ -435,13 +435,8 @@ __device__ __forceinline__ void store_tile(const GemmArgs& args, const TileMap& 
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float g0 = gv[2 * i], g1 = gv[2 * i + 1];
-#ifdef HM_IEEE_SILU   // A/B reference build (tools/variant_build.sh)
-        float h0 = g0 / (1.f + __expf(-g0)) * uv[2 * i];
-        float h1 = g1 / (1.f + __expf(-g1)) * uv[2 * i + 1];
-#else
         float h0 = g0 * rcp_approx(1.f + __expf(-g0)) * uv[2 * i];
         float h1 = g1 * rcp_approx(1.f + __expf(-g1)) * uv[2 * i + 1];
-#endif
         hv[i] = __floats2bfloat162_rn(h0, h1);
       }
       stage_store<4>(sw, lane, reinterpret_cast<const int4*>(hv),
