@@ -45,19 +45,43 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_handle_exchange_and_partition():
+@pytest.mark.parametrize("world", [2, 8])
+def test_gloo_handle_exchange_and_partition(world):
+    """world 2: the [2, 4] layout; world 8: one EP rank per GPU (the N = 8
+    layout the driver's scaling run uses, which no gpurun box here offers)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=120) for _ in procs)
+    res = sorted(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert [r[1] for r in res] == [True, True]
-    assert [r[2] for r in res] == [True, True]
-    assert res[0][3] == [0, 1, 2, 3] and res[1][3] == [4, 5, 6, 7]
+    assert [r[1] for r in res] == [True] * world
+    assert [r[2] for r in res] == [True] * world
+    per = 8 // world
+    assert [r[3] for r in res] == [list(range(k * per, (k + 1) * per)) for k in range(world)]
+
+
+@pytest.mark.gpu
+def test_transport_choice_one_rank_per_gpu(hm):
+    """N = 8 (one EP rank per GPU): the runtime hierarchy is flat [8], the
+    nearest calibrated B200 fit supplies its 'std' entry, and the choice is
+    per-GPU dedup (= per-rank at L = 1) or no dedup -- never a deep level."""
+    from paper_2508_09591_b200.routing import RoutingMask
+    from paper_2508_09591_b200.transport import (choose_transport, default_params,
+                                                 runtime_topology)
+    topo = runtime_topology(8, 8, 128, 2048)
+    assert topo.fanouts == (8,) or list(topo.fanouts) == [8]
+    params = default_params(8, topo.num_levels)
+    rng = np.random.default_rng(3)
+    logits = rng.standard_normal((8 * 256, 128)).astype(np.float32)
+    ids, _, _ = OM.route_topk(logits, 8)
+    bits = np.zeros((ids.shape[0], 128), dtype=bool)
+    np.put_along_axis(bits, ids, True, axis=1)
+    choice = choose_transport(RoutingMask(bits, 8), topo, params)
+    assert choice.d_star == 1 and choice.mode in ("gpu", "none")
 
 
 def test_rank_placement_rejects_uneven():
