@@ -73,7 +73,7 @@ def test_transport_choice_one_rank_per_gpu(hm):
     from paper_2508_09591_b200.transport import (choose_transport, default_params,
                                                  runtime_topology)
     topo = runtime_topology(8, 8, 128, 2048)
-    assert topo.fanouts == (8,) or list(topo.fanouts) == [8]
+    assert list(topo.level_fanouts) == [8]
     params = default_params(8, topo.num_levels)
     rng = np.random.default_rng(3)
     logits = rng.standard_normal((8 * 256, 128)).astype(np.float32)
