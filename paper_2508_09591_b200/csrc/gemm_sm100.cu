@@ -830,23 +830,28 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
       : "memory");
 }
+// tcgen05.mma / commit on a CTA pair, issued by one elected lane of a warp
+// that runs the loop in lockstep:
+// the operands are warp-uniform, so they stay on the uniform datapath (no
+// per-MMA waterfall loop moving a single lane's registers to uniform ones)
 template <uint32_t IDESC = kIdesc2>
-__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                               uint32_t accumulate) {
+__device__ __forceinline__ void umma_bf16_pair_elect(uint32_t tmem_d, uint64_t adesc,
+                                                     uint64_t bdesc, uint32_t accumulate) {
   asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
-// ... with B MN-major (bit 16: transpose B): the weights used as stored
-constexpr uint32_t kIdesc2BMN = kIdesc2 | (1u << 16);
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+__device__ __forceinline__ void umma_commit_pair_elect(uint64_t* bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
       "h"((uint16_t)0x3)
       : "memory");
 }
+// ... with B MN-major (bit 16: transpose B): the weights used as stored
+constexpr uint32_t kIdesc2BMN = kIdesc2 | (1u << 16);
 // arrive on the barrier at the same offset in CTA `rank` of the cluster.
 // Default (.release.cta) semantics: the only user is the epilogue's
 // TMEM-empty arrive, ordered after its tcgen05.ld by the before_thread_sync
@@ -1047,7 +1052,7 @@ __global__ void __cluster_dims__(2, 1, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {   // the whole warp runs the loop; one elected lane issues
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -1062,9 +1067,9 @@ __global__ void __cluster_dims__(2, 1, 1)
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k) {
           if (BMN)
-            umma_bf16_pair<kIdesc2BMN>(d, da + 2 * k, db + 128 * k, (kb | k) ? 1u : 0u);
+            umma_bf16_pair_elect<kIdesc2BMN>(d, da + 2 * k, db + 128 * k, (kb | k) ? 1u : 0u);
           else
-            umma_bf16_pair(d, da + 2 * k, db + 2 * k, (kb | k) ? 1u : 0u);
+            umma_bf16_pair_elect(d, da + 2 * k, db + 2 * k, (kb | k) ? 1u : 0u);
         }
       };
       auto wait_full = [&](int st, uint32_t ph) {
@@ -1090,13 +1095,13 @@ __global__ void __cluster_dims__(2, 1, 1)
           for (int kb = 0; kb < kblocks; ++kb) {
             wait_full(stage, phase);
             mma_kb(d, stage, kb, 0);
-            umma_commit_pair(empty + stage);
+            umma_commit_pair_elect(empty + stage);
             if (++stage == ST) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit_pair(tfull + acc);
+          umma_commit_pair_elect(tfull + acc);
         } else {
           // single TMEM buffer: accumulator 0 as soon as the epilogue released
           // it; accumulator 1's MMAs of the held stages once it is released too
@@ -1113,19 +1118,19 @@ __global__ void __cluster_dims__(2, 1, 1)
                 mbar_wait(tempty + 1, tph);
                 free1 = true;
               } else {
-                free1 = mbar_try(smem_u32(tempty + 1), tph) != 0;
+                free1 = __shfl_sync(0xffffffffu, mbar_try(smem_u32(tempty + 1), tph), 0) != 0;
               }
               if (free1) tc_fence_after();
             }
             if (free1) {
               for (; held > 0; --held) {   // catch up on the held stages
                 mma_kb(tmem_base + BN, hstage, hkb, 1);
-                umma_commit_pair(empty + hstage);
+                umma_commit_pair_elect(empty + hstage);
                 if (++hstage == ST) hstage = 0;
                 ++hkb;
               }
               mma_kb(tmem_base + BN, stage, kb, 1);
-              umma_commit_pair(empty + stage);
+              umma_commit_pair_elect(empty + stage);
             } else {
               if (held++ == 0) {
                 hstage = stage;
@@ -1142,12 +1147,12 @@ __global__ void __cluster_dims__(2, 1, 1)
             tc_fence_after();
             for (; held > 0; --held) {
               mma_kb(tmem_base + BN, hstage, hkb, 1);
-              umma_commit_pair(empty + hstage);
+              umma_commit_pair_elect(empty + hstage);
               if (++hstage == ST) hstage = 0;
               ++hkb;
             }
           }
-          umma_commit_pair(tfull + 0);
+          umma_commit_pair_elect(tfull + 0);
         }
       }
     }
@@ -1423,7 +1428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGat
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {   // the whole warp runs the loop; one elected lane issues
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -1438,30 +1443,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GB ? kThreads + kGat
         const int rows = tm.rows[g];
         const int whole = rows / BK, kblocks = (rows + BK - 1) / BK;
         for (int kb = 0; kb < kblocks; ++kb) {
-          const uint32_t a0 = smem_u32(sa + stage * kHalfBytes);
-          const uint32_t b0 = smem_u32(sb + stage * kHalfBytes);
+          // descriptors once per k-block, +128 (16 K lines) per k-step
+          const uint64_t da = smem_desc_mn(smem_u32(sa + stage * kHalfBytes));
+          const uint64_t db = smem_desc_mn(smem_u32(sb + stage * kHalfBytes));
           if (kb < whole) {   // TMA-only stage: the 4 k-steps unrolled
             mbar_wait(full + stage, phase);
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < BK / UK; ++k)
-              umma_bf16_pair<kIdesc2MN>(d, smem_desc_mn(a0 + k * UK * 128),
-                                        smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+              umma_bf16_pair_elect<kIdesc2MN>(d, da + 128 * k, db + 128 * k,
+                                              (kb | k) ? 1u : 0u);
           } else {   // the forwarded tail block (zeroed lines: cluster acquire)
             mbar_wait_cluster(full + stage, phase);
             tc_fence_after();
             const int ksteps = (rows - kb * BK + UK - 1) / UK;
             for (int k = 0; k < ksteps; ++k)
-              umma_bf16_pair<kIdesc2MN>(d, smem_desc_mn(a0 + k * UK * 128),
-                                        smem_desc_mn(b0 + k * UK * 128), (kb | k) ? 1u : 0u);
+              umma_bf16_pair_elect<kIdesc2MN>(d, da + 128 * k, db + 128 * k,
+                                              (kb | k) ? 1u : 0u);
           }
-          umma_commit_pair(empty + stage);
+          umma_commit_pair_elect(empty + stage);
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(tfull + acc);
+        umma_commit_pair_elect(tfull + acc);
       }
     }
   } else if (warp >= 4 && warp < 8) {
