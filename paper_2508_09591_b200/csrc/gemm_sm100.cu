@@ -834,6 +834,23 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorM
 // that runs the loop in lockstep:
 // the operands are warp-uniform, so they stay on the uniform datapath (no
 // per-MMA waterfall loop moving a single lane's registers to uniform ones)
+// TMA pair load / expect-tx by one elected lane of a lockstep warp
+__device__ __forceinline__ void tma_load_2d_pair_elect(void* smem_dst, const CUtensorMap* map,
+                                                       uint64_t* bar, int x, int y) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n}\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_elect(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
 template <uint32_t IDESC = kIdesc2>
 __device__ __forceinline__ void umma_bf16_pair_elect(uint32_t tmem_d, uint64_t adesc,
                                                      uint64_t bdesc, uint32_t accumulate) {
@@ -1011,10 +1028,13 @@ __global__ void __cluster_dims__(2, 1, 1)
   const int kblocks_fixed = args.K / BK;
 
   if (warp == 0) {
-    // lane 0 drives the ring (with GA only B's TMA loads; warps 8-11 fill A)
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    // the warp drives the ring in lockstep, one elected lane issuing (with GA
+    // only B's TMA loads; warps 8-11 fill A)
+    {
+      if (lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      }
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < tm.total; t += ncl) {
@@ -1028,9 +1048,9 @@ __global__ void __cluster_dims__(2, 1, 1)
         const int kblocks = kMode == 2 ? tm.rows[g] / BK : kblocks_fixed;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          if (leader) mbar_expect_tx(full + stage, GA ? 2 * C::kBBytes : 2 * C::kStage);
+          if (leader) mbar_expect_tx_elect(full + stage, GA ? 2 * C::kBBytes : 2 * C::kStage);
           if (!GA)
-            tma_load_2d_pair(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
+            tma_load_2d_pair_elect(sa + stage * kHalfBytes, &map_a, full + stage, k0 + kb * BK, arow);
 #pragma unroll
           for (int a = 0; a < NA; ++a) {
             uint8_t* sbs = sb + stage * C::kBBytes + a * kHalfBytes;
@@ -1038,10 +1058,10 @@ __global__ void __cluster_dims__(2, 1, 1)
               const int bcol = nt * BN * NA + a * BN + (int)rank * 128;
 #pragma unroll
               for (int j = 0; j < 2; ++j)
-                tma_load_2d_pair(sbs + j * 8192, &map_b, full + stage, bcol + 64 * j,
+                tma_load_2d_pair_elect(sbs + j * 8192, &map_b, full + stage, bcol + 64 * j,
                                  tm.wsel[g] * args.K + kb * BK);
             } else {
-              tma_load_2d_pair(sbs, &map_b, full + stage, k0 + kb * BK, brow + a * BN);
+              tma_load_2d_pair_elect(sbs, &map_b, full + stage, k0 + kb * BK, brow + a * BN);
             }
           }
           if (++stage == ST) {
