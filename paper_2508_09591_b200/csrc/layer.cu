@@ -231,6 +231,13 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
 // order: ties keep the lower index), then the quad merges its four lists
 // by two butterfly steps with the same (value desc, index asc) order.  4x
 // the warps of the lane-per-token kernel for the same tokens.
+// Threshold pre-pass (the kernel is issue-bound on the insertions): each
+// lane's two largest float4-group maxima are logits of the token, so the
+// quad holds >= 8 >= K logits at or above theta = the smallest of the four
+// lanes' second-largest group maxima, and no logit below theta is among the
+// top K.  Only the lane's candidates (>= theta, typically 2-4 of 32) are
+// inserted, in ascending expert order, read back from the lane's shared-
+// memory row; the merged top K is the one the full insertion builds.
 template <int K, int F4, int LPT = 4>   // F4 = float4 columns per lane = E / (4 LPT)
 __global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ logits, int64_t T,
                                                     int E, const int32_t* __restrict__ e2s,
@@ -238,6 +245,12 @@ __global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ lo
                                                     float* __restrict__ weights,
                                                     int32_t* __restrict__ expert_ids) {
   constexpr int TPW = 32 / LPT;   // tokens per warp
+  // the pre-pass keeps the lane's logits in a shared-memory row (E <= 128:
+  // up to 32 per lane, one 32-bit candidate mask); wider rows insert all
+  constexpr bool kPre = 4 * F4 <= 32;
+  constexpr int kRow = kPre ? 4 * F4 + 4 : 4;   // row stride (floats): float4 stores conflict-free
+  __shared__ float4 s_rows[256 * kRow / 4];
+  float* row_s = reinterpret_cast<float*>(s_rows) + threadIdx.x * kRow;
   const int lane = threadIdx.x & 31, j = lane & (LPT - 1);
   int64_t warp = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * 8;
@@ -272,13 +285,40 @@ __global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ lo
         ti[0] = e;
       }
     };
+    if constexpr (!kPre) {
 #pragma unroll
-    for (int i = 0; i < F4; ++i) {
-      const int e = 4 * (j + LPT * i);
-      insert(v[i].x, e);
-      insert(v[i].y, e + 1);
-      insert(v[i].z, e + 2);
-      insert(v[i].w, e + 3);
+      for (int i = 0; i < F4; ++i) {
+        const int e = 4 * (j + LPT * i);
+        insert(v[i].x, e);
+        insert(v[i].y, e + 1);
+        insert(v[i].z, e + 2);
+        insert(v[i].w, e + 3);
+      }
+    } else {
+      float m1 = -INFINITY, m2 = -INFINITY;   // the lane's two largest group maxima
+#pragma unroll
+      for (int i = 0; i < F4; ++i) {
+        const float gm = fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w));
+        m2 = fmaxf(m2, fminf(m1, gm));
+        m1 = fmaxf(m1, gm);
+        reinterpret_cast<float4*>(row_s)[i] = v[i];
+      }
+      float theta = m2;
+#pragma unroll
+      for (int m = 1; m < LPT; m <<= 1) theta = fminf(theta, __shfl_xor_sync(0xffffffffu, theta, m));
+      unsigned cand = 0;
+#pragma unroll
+      for (int i = 0; i < F4; ++i) {
+        cand |= (v[i].x >= theta ? 1u : 0u) << (4 * i);
+        cand |= (v[i].y >= theta ? 1u : 0u) << (4 * i + 1);
+        cand |= (v[i].z >= theta ? 1u : 0u) << (4 * i + 2);
+        cand |= (v[i].w >= theta ? 1u : 0u) << (4 * i + 3);
+      }
+      while (cand) {   // ascending position = ascending expert index
+        const int pos = __ffs(cand) - 1;
+        cand &= cand - 1;
+        insert(row_s[pos], 4 * (j + LPT * (pos >> 2)) + (pos & 3));
+      }
     }
     // butterfly merge inside the token's lane group
 #pragma unroll

@@ -227,6 +227,13 @@ def test_route_quad_equals_lane(hm, E, K, renorm):
     logits = torch.randn(3001, E, generator=g)
     logits[::5, 7] = logits[::5, 9]
     logits[::11, 3:12] = 0.25           # wide ties
+    # the router's threshold pre-pass: the whole top K inside one lane of the
+    # quad (lane 0 loads float4 columns 0, 4, 8, ... i.e. experts 16 i + 0..3),
+    # rows with only 8 finite logits (two lanes all -inf), rows of one value
+    lane0 = [16 * i + c for i in range(E // 16) for c in range(4)][:8]
+    logits[1::17, lane0] = 10.0 + torch.arange(len(lane0), dtype=torch.float32)
+    logits[2::19, 8:] = float("-inf")
+    logits[3::23] = 0.5
     lg = logits.cuda()
     try:
         res = []
