@@ -238,8 +238,12 @@ __global__ void k_route(const float* __restrict__ logits, int64_t T, int E, int 
 // top K.  Only the lane's candidates (>= theta, typically 2-4 of 32) are
 // inserted, in ascending expert order, read back from the lane's shared-
 // memory row; the merged top K is the one the full insertion builds.
+// 4-warp CTAs: the grid of 32-token CTAs spreads the (issue-bound) work over
+// the SMs in finer steps than 64-token CTAs (at most 28 instead of 32 warp-
+// tasks per SM for the Qwen3 step's 4096).
+constexpr int kRouteWarps = 4;
 template <int K, int F4, int LPT = 4>   // F4 = float4 columns per lane = E / (4 LPT)
-__global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ logits, int64_t T,
+__global__ void __launch_bounds__(32 * kRouteWarps) k_route_quad(const float* __restrict__ logits, int64_t T,
                                                     int E, const int32_t* __restrict__ e2s,
                                                     int renorm, int32_t* __restrict__ slot_ids,
                                                     float* __restrict__ weights,
@@ -249,11 +253,11 @@ __global__ void __launch_bounds__(256) k_route_quad(const float* __restrict__ lo
   // up to 32 per lane, one 32-bit candidate mask); wider rows insert all
   constexpr bool kPre = 4 * F4 <= 32;
   constexpr int kRow = kPre ? 4 * F4 + 4 : 4;   // row stride (floats): float4 stores conflict-free
-  __shared__ float4 s_rows[256 * kRow / 4];
+  __shared__ float4 s_rows[32 * kRouteWarps * kRow / 4];
   float* row_s = reinterpret_cast<float*>(s_rows) + threadIdx.x * kRow;
   const int lane = threadIdx.x & 31, j = lane & (LPT - 1);
-  int64_t warp = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t nw = (int64_t)gridDim.x * 8;
+  int64_t warp = (int64_t)blockIdx.x * kRouteWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kRouteWarps;
   for (int64_t base = warp * TPW; base < T; base += nw * TPW) {
     const int64_t t = base + lane / LPT;
     const bool live = t < T;
@@ -821,10 +825,12 @@ __global__ void __launch_bounds__(1024) k_notify(const WorldDev* __restrict__ wp
       const int s_loc = i / E, e = i - s_loc * E;
       const int sg = gp * L + s_loc;
       const int q0 = (e / E_loc) / L * L;
-      const int key = (sg - q0 + G) % G;
+      const int key = sg - q0 < 0 ? sg - q0 + G : sg - q0;   // (sg - q0) mod G
       int base = s_eb[e];
-      for (int src = 0; src < G; ++src)
-        if ((src - q0 + G) % G < key) base += cnt[(int64_t)src * C + G + e];
+      for (int src = 0; src < G; ++src) {
+        const int r = src - q0 < 0 ? src - q0 + G : src - q0;
+        if (r < key) base += cnt[(int64_t)src * C + G + e];
+      }
       eoff[i] = base;
     } else if (i < n1) {
       const int k = i - n0, s_loc = k / G, d = k - s_loc * G;
@@ -2359,8 +2365,8 @@ HM_API int hm_route_topk(const float* logits, int64_t T, int32_t E, int32_t K,
                        ((uintptr_t)logits & 15) == 0 && K <= 8;
   if (quad_ok) {
     constexpr int kL = 4;   // lanes per token (8: 0.2385 vs 0.2343 ms for the N = 1 step)
-    const int blocks = grid_for(T, 8 * (32 / kL), kSMs * 8);
-#define HM_RQ(KK, FF) k_route_quad<KK, FF, kL><<<blocks, 256, 0, s>>>(logits, T, E, expert_to_slot, \
+    const int blocks = grid_for(T, kRouteWarps * (32 / kL), kSMs * 16);
+#define HM_RQ(KK, FF) k_route_quad<KK, FF, kL><<<blocks, 32 * kRouteWarps, 0, s>>>(logits, T, E, expert_to_slot, \
                                                                renormalize, slot_ids, weights, expert_ids)
 #define HM_RQ_K(KK)                    \
   case KK:                             \
