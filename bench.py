@@ -673,7 +673,9 @@ def main():
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                 "unit": "GB/s", "traffic": None, "algorithmic_bytes": alg[dom],
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "peak_kind": "copy (1:1 read/write); the combine gather reads K rows per row it "
+                             "writes, and read-dominated traffic can exceed the copy rate"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     # DRAM bytes per launch of the same kernel from the committed ncu --set
     # full capture of this command (profiles/ncu_traffic.json, qwen3 at N=1)
